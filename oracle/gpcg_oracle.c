@@ -1,0 +1,472 @@
+/*
+ * gpcg_oracle.c -- plain, slow, obviously-correct CPU reference of GPCG (fp64).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path (libgpcg.so, the
+ * Python binding paper_cs_0101018_b200/gpcg.py) may include, link, import or
+ * execute this file.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg call it.  It shares no code with the
+ * CUDA path: it has its own operator assembly, loops, reductions and control.
+ *
+ * Paper: Benson, McInnes, More, "GPCG: A case study in the performance and
+ * scalability of optimization algorithms" (reference PAPER.md).  Every routine
+ * cites the passage it follows as "P:a-b (section, equation)".  Readings of
+ * silent/ambiguous passages are numbered R1.. in DESIGN.md ("Readings").
+ *
+ * Problem (Eq. def-quadratic, sign per reading R1):
+ *     minimise q(x) = 1/2 x'Ax - b'x + c   subject to  l <= x <= u.
+ * Gradient g = Ax - b.  A is held as CSR with both triangles stored.
+ *
+ * Style: straight loops in index order, left-to-right sums, no blocking, no
+ * fusion, no reordering.  Build with -O2 -ffp-contract=off so that every
+ * a*b+c rounds twice, as written.
+ *
+ * Pins (tests/test_oracle_*.py): dense brute-force products, the eps=0
+ * Laplacian eigenpairs, 3^n active-set enumeration, Cholesky solves with
+ * infinite bounds, KKT certificates, SPEC.md hand values, the paper's free
+ * fractions.  Parity unpinned: iteration counts vs the paper's
+ * tables (different discretisation and preconditioner).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+/* status codes (same meaning as the product ABI, defined independently) */
+#define ORA_OK 0
+#define ORA_NOT_CONVERGED 1
+#define ORA_EINVAL (-1)
+#define ORA_ENOMEM (-2)
+#define ORA_ENOTSPD (-5)
+#define ORA_ESEARCH (-6)
+
+typedef struct {
+    double mu;            /* sufficient-decrease constant, "mu in (0,1/2)"; 0.1 (R6)      */
+    double eta1;          /* Eq. pgstop2, P:789 eta1 = 0.1                                        */
+    double eta2;          /* Eq. cgstop1, P:790 eta2 = 0.05                                       */
+    double eta2_shrink;   /* Eq. cgstop3 "reduce eta2" P:491: x0.1 (R12)                          */
+    double eta2_floor;    /* 1e-12 (R12)                                                          */
+    int64_t gp_cap;       /* GP iterates per phase, 100 (R13)                                     */
+    int64_t refine_cap;   /* cgstop3 repetitions per outer iterate, 30 (R12)                      */
+    int64_t max_halvings; /* projected-search trials, 50 (R13)                                    */
+    int64_t cg_cap;       /* 0 => m_k, the finite-termination bound P:444-447                     */
+    double time_budget_s; /* 0 => none; else stop (NOT_CONVERGED) once exceeded (bounded samples) */
+} ora_params;
+
+typedef struct {
+    int64_t outer_iters, gp_iters, cg_iters, cg_calls, refinements, full_spmvs;
+    int64_t n_free, n_active, n_active_nonbinding;
+    double pg_norm, q, g0_norm, tau, seconds;
+    int64_t status;
+} ora_stats;
+
+/* ------------------------------------------------------------------------ */
+/* operator                                                                  */
+/* ------------------------------------------------------------------------ */
+
+/* Number of stored entries of the 5-point stencil matrix on an nx x ny grid. */
+int64_t ora_stencil2d_nnz(int64_t nx, int64_t ny)
+{
+    return 5 * nx * ny - 2 * nx - 2 * ny;
+}
+
+/* Assemble the 5-point face-weight operator as CSR.
+ * Definition (BASELINE.json configs[0], reading R2): A = sum over faces f of
+ * w_f (e_a - e_b)(e_a - e_b)' for interior faces joining points a, b, plus
+ * w_f e_a e_a' for faces on the Dirichlet boundary, plus diag(shift).
+ * Face conventions as in include/gpcg.h: wx[j*wx_ld + k] joins (k-1, j)-(k, j),
+ * k = 0..nx; wy[f*wy_ld + i] joins (i, f-1)-(i, f), f = 0..ny; ld 0 = broadcast.
+ * Columns come out in increasing order: (i,j-1), (i-1,j), (i,j), (i+1,j), (i,j+1). */
+int ora_stencil2d_to_csr(int64_t nx, int64_t ny, const double *wx, int64_t wx_ld,
+                         const double *wy, int64_t wy_ld, const double *shift,
+                         int64_t *rp, int32_t *ci, double *val)
+{
+    if (nx <= 0 || ny <= 0) return ORA_EINVAL;
+    int64_t p = 0;
+    rp[0] = 0;
+    for (int64_t j = 0; j < ny; j++) {
+        for (int64_t i = 0; i < nx; i++) {
+            int64_t v = i + nx * j;
+            double w_west = wx[j * wx_ld + i];
+            double w_east = wx[j * wx_ld + i + 1];
+            double w_south = wy[j * wy_ld + i];
+            double w_north = wy[(j + 1) * wy_ld + i];
+            double d = w_west + w_east + w_south + w_north;
+            if (shift) d = d + shift[v];
+            if (j > 0)      { ci[p] = (int32_t)(v - nx); val[p] = -w_south; p++; }
+            if (i > 0)      { ci[p] = (int32_t)(v - 1);  val[p] = -w_west;  p++; }
+            ci[p] = (int32_t)v; val[p] = d; p++;
+            if (i < nx - 1) { ci[p] = (int32_t)(v + 1);  val[p] = -w_east;  p++; }
+            if (j < ny - 1) { ci[p] = (int32_t)(v + nx); val[p] = -w_north; p++; }
+            rp[v + 1] = p;
+        }
+    }
+    return ORA_OK;
+}
+
+/* y = A x  (row-wise left-to-right sums) -- "Mat-Vec Multiply", T3 P:999-1005 */
+void ora_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+              const double *x, double *y)
+{
+    for (int64_t i = 0; i < n; i++) {
+        double s = 0.0;
+        for (int64_t k = rp[i]; k < rp[i + 1]; k++) s += val[k] * x[ci[k]];
+        y[i] = s;
+    }
+}
+
+/* y = Z Z' A Z Z' x : the reduced Hessian A_k = Z_k' A Z_k (Eq. cg2)
+ * embedded in R^n.  free[i] != 0 marks a free variable; x is read only on the
+ * free set and y is zero off it. */
+void ora_spmv_masked(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                     const unsigned char *free_, const double *x, double *y)
+{
+    for (int64_t i = 0; i < n; i++) {
+        double s = 0.0;
+        if (free_[i]) {
+            for (int64_t k = rp[i]; k < rp[i + 1]; k++)
+                if (free_[ci[k]]) s += val[k] * x[ci[k]];
+        }
+        y[i] = s;
+    }
+}
+
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+/* ------------------------------------------------------------------------ */
+/* vectors                                                                   */
+/* ------------------------------------------------------------------------ */
+static double dot(int64_t n, const double *a, const double *b)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
+    return s;
+}
+
+/* median of {l, u, x}: P[x] = mid(l, u, x) */
+static double mid(double l, double u, double x)
+{
+    if (x < l) return l;
+    if (x > u) return u;
+    return x;
+}
+
+void ora_project(int64_t n, const double *l, const double *u, const double *x, double *px)
+{
+    for (int64_t i = 0; i < n; i++) px[i] = mid(l[i], u[i], x[i]);
+}
+
+/* Projected gradient, Eq. proj-gradient.  Fixed variables l=u
+ * are active at both bounds; the two cases give min(g,0) and max(g,0), whose
+ * only common value is 0 (reading R16). */
+static double pgrad_i(double x, double g, double l, double u)
+{
+    int at_l = (x == l), at_u = (x == u);
+    if (at_l && at_u) return 0.0;
+    if (at_l) return g < 0.0 ? g : 0.0;
+    if (at_u) return g > 0.0 ? g : 0.0;
+    return g;
+}
+
+void ora_proj_grad(int64_t n, const double *x, const double *g, const double *l,
+                   const double *u, double *pg)
+{
+    for (int64_t i = 0; i < n; i++) pg[i] = pgrad_i(x[i], g[i], l[i], u[i]);
+}
+
+static double pgnorm(int64_t n, const double *x, const double *g, const double *l, const double *u)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; i++) { double d = pgrad_i(x[i], g[i], l[i], u[i]); s += d * d; }
+    return sqrt(s);
+}
+
+/* A(x) = {i : x_i = l_i or x_i = u_i}; B(x) binding set. */
+static int is_active(double x, double l, double u) { return x == l || x == u; }
+static int is_binding(double x, double g, double l, double u)
+{
+    return (x == l && g >= 0.0) || (x == u && g <= 0.0);
+}
+
+void ora_sets(int64_t n, const double *x, const double *g, const double *l, const double *u,
+              unsigned char *active, unsigned char *binding, int64_t *n_active, int64_t *n_binding)
+{
+    int64_t na = 0, nb = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int a = is_active(x[i], l[i], u[i]);
+        int b = is_binding(x[i], g[i], l[i], u[i]);
+        if (active) active[i] = (unsigned char)a;
+        if (binding) binding[i] = (unsigned char)b;
+        na += a; nb += b;
+    }
+    if (n_active) *n_active = na;
+    if (n_binding) *n_binding = nb;
+}
+
+/* q(x) = 1/2 x'Ax - b'x + c, computed as 1/2 x'(Ax) - b'x + c in index order */
+double ora_objective(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                     const double *b, double c, const double *x)
+{
+    double *Ax = (double *)malloc((size_t)n * sizeof(double));
+    if (!Ax) return NAN;
+    ora_spmv(n, rp, ci, val, x, Ax);
+    double q = 0.5 * dot(n, x, Ax) - dot(n, b, x) + c;
+    free(Ax);
+    return q;
+}
+
+/* g = A x - b */
+static void gradient(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                     const double *b, const double *x, double *g)
+{
+    ora_spmv(n, rp, ci, val, x, g);
+    for (int64_t i = 0; i < n; i++) g[i] = g[i] - b[i];
+}
+
+/* ------------------------------------------------------------------------ */
+/* gradient projection pieces                                                */
+/* ------------------------------------------------------------------------ */
+
+/* alpha_0 = argmin_{alpha>0} q(y - alpha d), d = grad_Omega q(y): Eq. bqpls
+ * (P:362-374).  The map is the quadratic q(y) - alpha <g,d> + alpha^2/2 <d,Ad>
+ * and <g,d> = <d,d> because d_i is g_i or 0.  Returns 0 and sets *status to
+ * ENOTSPD when <d,Ad> <= 0 (reading R7).  work: 2n doubles. */
+double ora_cauchy_alpha(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                        const double *y, const double *g, const double *l, const double *u,
+                        double *work, int *status)
+{
+    double *d = work, *Ad = work + n;
+    ora_proj_grad(n, y, g, l, u, d);
+    ora_spmv(n, rp, ci, val, d, Ad);
+    double dd = dot(n, d, d), dAd = dot(n, d, Ad);
+    *status = ORA_OK;
+    if (!(dAd > 0.0)) { *status = ORA_ENOTSPD; return 0.0; }
+    return dd / dAd;
+}
+
+/* Projected search along dir from y (Eqs. next-y/gplsstop P:341-361 with
+ * dir = -g, alpha_base = alpha_0; Eq. cglsstop2 P:475-481 with dir = d_k,
+ * alpha_base = 1): the first alpha = alpha_base * 2^-h, h = 0,1,.., with
+ *     q(P[y + alpha dir]) <= q(y) + mu <g, P[y + alpha dir] - y>.
+ * q(ytrial) - q(y) is evaluated by the exact expansion <g,s> + 1/2 <s,As>,
+ * s = ytrial - y (reading R17).  Writes the accepted point (the mid() result
+ * itself) to ynew.  Returns h >= 0, or -1 if no trial is accepted.
+ * work: 2n doubles.  *delta = q(ynew) - q(y). */
+int64_t ora_projected_search(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                             const double *y, const double *g, const double *dir,
+                             const double *l, const double *u, double alpha_base, double mu,
+                             int64_t max_halvings, double *ynew, double *work,
+                             double *delta, double *alpha_out)
+{
+    double *s = work, *As = work + n;
+    for (int64_t h = 0; h < max_halvings; h++) {
+        double alpha = ldexp(alpha_base, (int)-h);
+        for (int64_t i = 0; i < n; i++) {
+            ynew[i] = mid(l[i], u[i], y[i] + alpha * dir[i]);
+            s[i] = ynew[i] - y[i];
+        }
+        ora_spmv(n, rp, ci, val, s, As);
+        double gs = dot(n, g, s);
+        double sAs = dot(n, s, As);
+        double dq = gs + 0.5 * sAs;
+        if (dq <= mu * gs) {
+            *delta = dq;
+            *alpha_out = alpha;
+            return h;
+        }
+    }
+    return -1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* conjugate gradients on the reduced system (Eqs. cg, cg2, cgstop1) */
+/* ------------------------------------------------------------------------ */
+
+/* Textbook CG (Hestenes-Stiefel) on A_k w = -r_k, w_0 = 0 (Alg. GPCG),
+ * vectors embedded in R^n and zero off the free set.  Stops at the first j with
+ *   (a) j >= 2 and q_k(w_{j-1}) - q_k(w_j) <= eta2 max_{l<j} (q_k(w_{l-1}) - q_k(w_l))
+ *       (Eq. cgstop1; from j >= 2, reading R10), where the decrease of
+ *       step j is 1/2 alpha_j rho_j'rho_j (reading R17);
+ *   (b) ||rho_j|| <= 1e-14 (1 + ||r_k||)   (machine-precision guard);
+ *   (c) j = cap.
+ * Returns w_j at that j (reading R11).  Returns the iteration count, or
+ * ORA_ENOTSPD (negative) on <p, A_k p> <= 0.  work: 3n doubles. decs (nullable,
+ * length >= cap) receives the per-step decreases. */
+int64_t ora_cg(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+               const unsigned char *free_, const double *r, double eta2, int64_t cap,
+               double *w, double *work, double *decs, double deadline)
+{
+    double *rho = work, *p = work + n, *a = work + 2 * n;
+    for (int64_t i = 0; i < n; i++) {
+        rho[i] = free_[i] ? -r[i] : 0.0;
+        p[i] = rho[i];
+        w[i] = 0.0;
+    }
+    double rr = dot(n, rho, rho);
+    double rnorm0 = sqrt(rr);
+    double maxdec = 0.0;
+    int64_t it = 0;
+    if (cap <= 0) return 0;
+    for (;;) {
+        it++;
+        ora_spmv_masked(n, rp, ci, val, free_, p, a);
+        double pAp = dot(n, p, a);
+        if (!(pAp > 0.0)) return ORA_ENOTSPD;
+        double alpha = rr / pAp;
+        for (int64_t i = 0; i < n; i++) w[i] = w[i] + alpha * p[i];
+        double dec = 0.5 * alpha * rr;
+        if (decs) decs[it - 1] = dec;
+        for (int64_t i = 0; i < n; i++) rho[i] = rho[i] - alpha * a[i];
+        double rr_new = dot(n, rho, rho);
+        int stop = (it >= 2 && dec <= eta2 * maxdec) ||
+                   (sqrt(rr_new) <= 1e-14 * (1.0 + rnorm0)) || (it >= cap) ||
+                   (deadline > 0.0 && now_s() > deadline);  /* bounded-sample timing only */
+        if (dec > maxdec) maxdec = dec;
+        if (stop) break;
+        double beta = rr_new / rr;
+        for (int64_t i = 0; i < n; i++) p[i] = rho[i] + beta * p[i];
+        rr = rr_new;
+    }
+    return it;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Algorithm GPCG                                                */
+/* ------------------------------------------------------------------------ */
+
+void ora_params_default(ora_params *p)
+{
+    p->mu = 0.1; p->eta1 = 0.1; p->eta2 = 0.05; p->eta2_shrink = 0.1; p->eta2_floor = 1e-12;
+    p->gp_cap = 100; p->refine_cap = 30; p->max_halvings = 50; p->cg_cap = 0;
+    p->time_budget_s = 0.0;
+}
+
+/* Solve min q(x) s.t. l <= x <= u.  tol > 0: absolute tau on ||grad_Omega q||_2
+ * (Eq. bqp_approximate_sol, Euclidean norm R4); tol < 0: tau =
+ * |tol| * ||A P[x0] - b||_2 (R5).  max_it: outer-iteration cap.  Returns the
+ * status; x holds the last feasible iterate. */
+int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                   const double *b, const double *l, const double *u, double c,
+                   const double *x0, double tol, int64_t max_it, const ora_params *prm,
+                   double *x, ora_stats *st)
+{
+    double t0 = now_s();
+    memset(st, 0, sizeof(*st));
+    for (int64_t i = 0; i < n; i++)
+        if (!(l[i] <= u[i])) { st->status = ORA_EINVAL; return ORA_EINVAL; }
+
+    double *g = (double *)malloc((size_t)n * sizeof(double));
+    double *y = (double *)malloc((size_t)n * sizeof(double));
+    double *w = (double *)malloc((size_t)n * sizeof(double));
+    double *work = (double *)malloc((size_t)3 * n * sizeof(double));
+    unsigned char *act = (unsigned char *)malloc((size_t)n);
+    unsigned char *fr = (unsigned char *)malloc((size_t)n);
+    if (!g || !y || !w || !work || !act || !fr) {
+        free(g); free(y); free(w); free(work); free(act); free(fr);
+        st->status = ORA_ENOMEM; return ORA_ENOMEM;
+    }
+    int status = ORA_NOT_CONVERGED;
+
+    /* Setup: x <- P[x0] (Alg. GPCG "Choose x0 in Omega" P:504) */
+    ora_project(n, l, u, x0, x);
+    gradient(n, rp, ci, val, b, x, g); st->full_spmvs++;
+    st->g0_norm = sqrt(dot(n, g, g));
+    double tau = tol > 0.0 ? tol : -tol * st->g0_norm;
+    st->tau = tau;
+    if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
+
+    for (int64_t k = 0; k < max_it; k++) {
+        st->outer_iters = k + 1;
+        /* ---- gradient projection phase : y_0 = x_k ---------- */
+        int64_t j = 0;
+        double maxdec = 0.0;
+        for (;;) {
+            /* g = A y_j - b holds here */
+            if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
+            int cs;
+            double alpha0 = ora_cauchy_alpha(n, rp, ci, val, x, g, l, u, work, &cs);
+            st->full_spmvs++;
+            if (cs != ORA_OK) { status = cs; goto done; }
+            /* direction -grad q (Eq. next-y); identical trial points to the
+             * -grad_Omega q reading for feasible y (reading R8) */
+            for (int64_t i = 0; i < n; i++) w[i] = -g[i];
+            double delta, alpha;
+            int64_t h = ora_projected_search(n, rp, ci, val, x, g, w, l, u, alpha0, prm->mu,
+                                             prm->max_halvings, y, work, &delta, &alpha);
+            if (h < 0) { status = ORA_ESEARCH; goto done; }
+            st->full_spmvs += h + 1;
+            /* A(y_{j-1}) vs A(y_j), compared as index sets (Eq. pgstop1, R9) */
+            int same = 1;
+            for (int64_t i = 0; i < n; i++) {
+                int a_old = is_active(x[i], l[i], u[i]);
+                int a_new = is_active(y[i], l[i], u[i]);
+                if (a_old != a_new) { same = 0; break; }
+            }
+            memcpy(x, y, (size_t)n * sizeof(double));
+            j++;
+            st->gp_iters++;
+            gradient(n, rp, ci, val, b, x, g); st->full_spmvs++;
+            double dec = -delta;                            /* q(y_{j-1}) - q(y_j) */
+            int stop = same ||                               /* Eq. pgstop1 */
+                       (j >= 2 && dec <= prm->eta1 * maxdec) ||  /* Eq. pgstop2 (R10) */
+                       (j >= prm->gp_cap);
+            if (dec > maxdec) maxdec = dec;
+            if (stop) break;
+        }
+        /* x_k = y_{j_k}; convergence test (R13) */
+        if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
+
+        /* ---- CG phase with eta2 refinement ------------------- */
+        double eta2 = prm->eta2;
+        for (int64_t rep = 0; rep < prm->refine_cap; rep++) {
+            int64_t m = 0;
+            for (int64_t i = 0; i < n; i++) { fr[i] = !is_active(x[i], l[i], u[i]); m += fr[i]; }
+            if (m == 0) break;              /* reading R26: next GP phase frees variables */
+            int64_t cap = prm->cg_cap > 0 ? prm->cg_cap : m;
+            int64_t its = ora_cg(n, rp, ci, val, fr, g, eta2, cap, w, work, NULL,
+                                 prm->time_budget_s > 0.0 ? t0 + prm->time_budget_s : 0.0);
+            st->cg_calls++;
+            if (its < 0) { status = (int)its; goto done; }
+            st->cg_iters += its;
+            /* d_k = Z_k w_{j_k} is w itself (zero off F) */
+            double delta, alpha;
+            int64_t h = ora_projected_search(n, rp, ci, val, x, g, w, l, u, 1.0, prm->mu,
+                                             prm->max_halvings, y, work, &delta, &alpha);
+            if (h < 0) { status = ORA_ESEARCH; goto done; }
+            st->full_spmvs += h + 1;
+            memcpy(x, y, (size_t)n * sizeof(double));
+            gradient(n, rp, ci, val, b, x, g); st->full_spmvs++;
+            if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
+            /* Eq. cgstop3: B(x_{k+1}) = A(x_{k+1}) -> reduce eta2, continue CG */
+            int64_t nonbinding = 0;
+            for (int64_t i = 0; i < n; i++)
+                if (is_active(x[i], l[i], u[i]) && !is_binding(x[i], g[i], l[i], u[i])) nonbinding++;
+            if (nonbinding != 0) break;
+            eta2 = eta2 * prm->eta2_shrink;
+            if (eta2 < prm->eta2_floor) eta2 = prm->eta2_floor;
+            st->refinements++;
+            if (prm->time_budget_s > 0.0 && now_s() - t0 > prm->time_budget_s) goto done;
+        }
+        if (prm->time_budget_s > 0.0 && now_s() - t0 > prm->time_budget_s) goto done;
+    }
+
+done:
+    {
+        int64_t na = 0, nb = 0;
+        ora_sets(n, x, g, l, u, NULL, NULL, &na, &nb);
+        st->n_active = na;
+        st->n_free = n - na;
+        st->n_active_nonbinding = na - nb;
+        st->pg_norm = pgnorm(n, x, g, l, u);
+        st->q = ora_objective(n, rp, ci, val, b, c, x);
+        st->status = status;
+        st->seconds = now_s() - t0;
+    }
+    free(g); free(y); free(w); free(work); free(act); free(fr);
+    return status;
+}

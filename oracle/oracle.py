@@ -1,0 +1,247 @@
+"""ctypes front of the plain-C GPCG oracle (oracle/gpcg_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference leg, never by the product path
+(paper_cs_0101018_b200/).  Marshalling only -- all arithmetic is in the C file,
+which cites the paper passage each routine follows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "gpcg_oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+
+OK, NOT_CONVERGED, EINVAL, ENOMEM, ENOTSPD, ESEARCH = 0, 1, -1, -2, -5, -6
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (gcc -O2 -ffp-contract=off; no OpenMP, single thread)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c99",
+                               "-D_POSIX_C_SOURCE=199309L", "-fPIC", "-shared",
+                               "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+class Params(C.Structure):
+    _fields_ = [("mu", C.c_double), ("eta1", C.c_double), ("eta2", C.c_double),
+                ("eta2_shrink", C.c_double), ("eta2_floor", C.c_double),
+                ("gp_cap", C.c_int64), ("refine_cap", C.c_int64),
+                ("max_halvings", C.c_int64), ("cg_cap", C.c_int64),
+                ("time_budget_s", C.c_double)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("outer_iters", C.c_int64), ("gp_iters", C.c_int64), ("cg_iters", C.c_int64),
+                ("cg_calls", C.c_int64), ("refinements", C.c_int64), ("full_spmvs", C.c_int64),
+                ("n_free", C.c_int64), ("n_active", C.c_int64), ("n_active_nonbinding", C.c_int64),
+                ("pg_norm", C.c_double), ("q", C.c_double), ("g0_norm", C.c_double),
+                ("tau", C.c_double), ("seconds", C.c_double), ("status", C.c_int64)]
+
+    def asdict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        P = C.c_void_p
+        i64 = C.c_int64
+        L.ora_stencil2d_nnz.restype = i64
+        L.ora_stencil2d_nnz.argtypes = [i64, i64]
+        L.ora_stencil2d_to_csr.restype = C.c_int
+        L.ora_stencil2d_to_csr.argtypes = [i64, i64, P, i64, P, i64, P, P, P, P]
+        L.ora_spmv.restype = None
+        L.ora_spmv.argtypes = [i64, P, P, P, P, P]
+        L.ora_spmv_masked.restype = None
+        L.ora_spmv_masked.argtypes = [i64, P, P, P, P, P, P]
+        L.ora_project.restype = None
+        L.ora_project.argtypes = [i64, P, P, P, P]
+        L.ora_proj_grad.restype = None
+        L.ora_proj_grad.argtypes = [i64, P, P, P, P, P]
+        L.ora_sets.restype = None
+        L.ora_sets.argtypes = [i64, P, P, P, P, P, P, P, P]
+        L.ora_objective.restype = C.c_double
+        L.ora_objective.argtypes = [i64, P, P, P, P, C.c_double, P]
+        L.ora_cauchy_alpha.restype = C.c_double
+        L.ora_cauchy_alpha.argtypes = [i64, P, P, P, P, P, P, P, P, P]
+        L.ora_projected_search.restype = i64
+        L.ora_projected_search.argtypes = [i64, P, P, P, P, P, P, P, P, C.c_double, C.c_double,
+                                           i64, P, P, P, P]
+        L.ora_cg.restype = i64
+        L.ora_cg.argtypes = [i64, P, P, P, P, P, C.c_double, i64, P, P, P, C.c_double]
+        L.ora_params_default.restype = None
+        L.ora_params_default.argtypes = [P]
+        L.ora_gpcg_solve.restype = C.c_int
+        L.ora_gpcg_solve.argtypes = [i64, P, P, P, P, P, P, C.c_double, P, C.c_double, i64,
+                                     P, P, P]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+@dataclass
+class CSR:
+    n: int
+    rp: np.ndarray
+    ci: np.ndarray
+    val: np.ndarray
+
+    def todense(self):
+        A = np.zeros((self.n, self.n))
+        for i in range(self.n):
+            for k in range(self.rp[i], self.rp[i + 1]):
+                A[i, self.ci[k]] += self.val[k]
+        return A
+
+
+def stencil2d_to_csr(nx, ny, wx, wx_ld, wy, wy_ld, shift=None) -> CSR:
+    L = lib()
+    n = nx * ny
+    nnz = L.ora_stencil2d_nnz(nx, ny)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    ci = np.zeros(nnz, dtype=np.int32)
+    va = np.zeros(nnz, dtype=np.float64)
+    wx = _f64(wx); wy = _f64(wy)
+    sh = _f64(shift) if shift is not None else None
+    rc = L.ora_stencil2d_to_csr(nx, ny, _p(wx), wx_ld, _p(wy), wy_ld, _p(sh), _p(rp), _p(ci), _p(va))
+    if rc != 0:
+        raise ValueError("ora_stencil2d_to_csr failed")
+    return CSR(n, rp, ci, va)
+
+
+def problem_csr(prob) -> CSR:
+    """The oracle's own CSR of a problems.Problem (assembled here for stencils)."""
+    if prob.kind == "stencil2d":
+        return stencil2d_to_csr(prob.nx, prob.ny, prob.wx, prob.wx_ld, prob.wy, prob.wy_ld, prob.shift)
+    return CSR(prob.n, np.ascontiguousarray(prob.row_ptr, dtype=np.int64),
+               np.ascontiguousarray(prob.col, dtype=np.int32), _f64(prob.val))
+
+
+def spmv(A: CSR, x):
+    x = _f64(x)
+    y = np.empty(A.n)
+    lib().ora_spmv(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(x), _p(y))
+    return y
+
+
+def spmv_masked(A: CSR, free, x):
+    x = _f64(x)
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    y = np.empty(A.n)
+    lib().ora_spmv_masked(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(x), _p(y))
+    return y
+
+
+def project(l, u, x):
+    l, u, x = _f64(l), _f64(u), _f64(x)
+    px = np.empty_like(x)
+    lib().ora_project(x.size, _p(l), _p(u), _p(x), _p(px))
+    return px
+
+
+def proj_grad(x, g, l, u):
+    x, g, l, u = _f64(x), _f64(g), _f64(l), _f64(u)
+    pg = np.empty_like(x)
+    lib().ora_proj_grad(x.size, _p(x), _p(g), _p(l), _p(u), _p(pg))
+    return pg
+
+
+def sets(x, g, l, u):
+    """(active mask, binding mask, |A|, |B|)"""
+    x, g, l, u = _f64(x), _f64(g), _f64(l), _f64(u)
+    n = x.size
+    act = np.zeros(n, np.uint8)
+    bnd = np.zeros(n, np.uint8)
+    na = C.c_int64(); nb = C.c_int64()
+    lib().ora_sets(n, _p(x), _p(g), _p(l), _p(u), _p(act), _p(bnd), C.byref(na), C.byref(nb))
+    return act.astype(bool), bnd.astype(bool), na.value, nb.value
+
+
+def objective(A: CSR, b, c, x):
+    b, x = _f64(b), _f64(x)
+    return lib().ora_objective(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(b), c, _p(x))
+
+
+def gradient(A: CSR, b, x):
+    return spmv(A, x) - _f64(b)
+
+
+def cauchy_alpha(A: CSR, y, g, l, u):
+    y, g, l, u = _f64(y), _f64(g), _f64(l), _f64(u)
+    work = np.empty(2 * A.n)
+    st = C.c_int()
+    a = lib().ora_cauchy_alpha(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(y), _p(g), _p(l), _p(u),
+                               _p(work), C.byref(st))
+    return a, st.value
+
+
+def projected_search(A: CSR, y, g, direction, l, u, alpha_base, mu=0.1, max_halvings=50):
+    """-> (h, ynew, delta, alpha); h = -1 when no trial is accepted."""
+    y, g, d, l, u = _f64(y), _f64(g), _f64(direction), _f64(l), _f64(u)
+    ynew = np.empty_like(y)
+    work = np.empty(2 * A.n)
+    delta = C.c_double(); alpha = C.c_double()
+    h = lib().ora_projected_search(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(y), _p(g), _p(d),
+                                   _p(l), _p(u), alpha_base, mu, max_halvings, _p(ynew),
+                                   _p(work), C.byref(delta), C.byref(alpha))
+    return h, ynew, delta.value, alpha.value
+
+
+def cg(A: CSR, free, r, eta2, cap=0):
+    """Textbook CG on A_F w = -r.  -> (iterations or error code, w, decreases)."""
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    r = _f64(r)
+    m = int(fr.sum())
+    cap = cap if cap > 0 else m
+    w = np.empty(A.n)
+    work = np.empty(3 * A.n)
+    decs = np.zeros(max(cap, 1))
+    it = lib().ora_cg(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), eta2, cap,
+                      _p(w), _p(work), _p(decs), 0.0)
+    return it, w, decs[:max(it, 0)]
+
+
+def default_params(**kw) -> Params:
+    p = Params()
+    lib().ora_params_default(C.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+def solve(A: CSR, b, l, u, c, x0, tol, max_it=500, params: Params = None):
+    """Algorithm GPCG (oracle).  -> (status, x, stats dict)."""
+    b, l, u, x0 = _f64(b), _f64(l), _f64(u), _f64(x0)
+    params = params or default_params()
+    x = np.empty(A.n)
+    st = Stats()
+    rc = lib().ora_gpcg_solve(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(b), _p(l), _p(u), c,
+                              _p(x0), tol, max_it, C.byref(params), _p(x), C.byref(st))
+    return rc, x, st.asdict()
+
+
+def solve_problem(prob, tol=None, max_it=500, params: Params = None):
+    A = problem_csr(prob)
+    return solve(A, prob.b, prob.l, prob.u, prob.c, prob.x0,
+                 prob.tol if tol is None else tol, max_it, params)
