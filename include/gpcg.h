@@ -1,0 +1,190 @@
+/*
+ * gpcg.h -- C ABI of the B200-native GPCG hot path (libgpcg.so).
+ *
+ * Method: GPCG, gradient projection + conjugate gradients for bound-
+ * constrained strictly convex QPs, as studied in Benson, McInnes, More,
+ * "GPCG: a case study in the performance and scalability of optimization
+ * algorithms" (reference PAPER.md; citations "P:a-b" are PAPER.md lines).
+ *
+ * Problem (Eqs. def_bqp / def_bounds / def-quadratic):
+ *
+ *     minimise  q(x) = 1/2 x'Ax - b'x + c   subject to  l <= x <= u
+ *
+ * A symmetric positive definite, l_i in [-inf, inf), u_i in (-inf, +inf],
+ * l_i <= u_i (l_i = u_i allowed: a fixed variable).  NOTE the sign: the paper
+ * writes +b'x; this ABI follows BASELINE.json and writes -b'x, so
+ * b_abi = -b_paper (reading R1).  Gradient g(x) = Ax - b.
+ *
+ * API shape follows the paper's Fig. 1: create the problem from
+ * (A, b, c) and bounds (l, u), solve, destroy.
+ *
+ * Pointers: every array argument may be HOST memory or DEVICE memory of the
+ * handle's device (detected with cudaPointerGetAttributes); host arrays are
+ * staged through library-owned device buffers.  fp64 throughout.
+ * Ownership: create copies every input into library-owned device memory; the
+ * caller keeps ownership of all arrays passed in or out.
+ * Streams: all device work is enqueued on the `cuda_stream` passed to create
+ * (a cudaStream_t; NULL = the legacy default stream).  solve, project and
+ * objective synchronise that stream before returning; hessvec with device
+ * pointers is asynchronous (argument errors return immediately, device faults
+ * surface at the next synchronising call).
+ * Errors: functions never abort or throw; they return a gpcg_status and
+ * gpcg_last_error() holds a thread-local message.  There is no CPU fallback:
+ * without a CUDA device create returns GPCG_ECUDA.
+ * Threading: one handle is used from one host thread at a time.
+ * Determinism: results are bitwise reproducible for a fixed (inputs, params,
+ * device, build): every reduction is a fixed-order two-stage tree, no float
+ * atomics.
+ */
+#ifndef GPCG_H
+#define GPCG_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GPCG_API __attribute__((visibility("default")))
+#else
+#define GPCG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gpcg_problem gpcg_problem; /* opaque; library-owned */
+
+/* return codes */
+enum {
+    GPCG_OK = 0,
+    GPCG_NOT_CONVERGED = 1, /* >0: result valid (feasible), max_it reached       */
+    GPCG_EINVAL = -1,       /* bad argument, l_i > u_i, NaN in inputs            */
+    GPCG_ENOMEM = -2,       /* device allocation failed                          */
+    GPCG_ECUDA = -3,        /* CUDA runtime error / no device                    */
+    GPCG_ENCCL = -4,        /* reserved for the multi-GPU path                   */
+    GPCG_ENOTSPD = -5,      /* <d,Ad> <= 0 or <p,A_k p> <= 0: A not SPD          */
+    GPCG_ESEARCH = -6,      /* projected search found no step in max_halvings    */
+    GPCG_ESTATE = -7        /* e.g. reduced hessvec before any project/solve     */
+};
+
+/* Algorithm constants (P:788-793 gives eta1 = 0.1, eta2 = 0.05; the others are
+ * DESIGN.md readings R6, R12, R13).  Obtain defaults from gpcg_params_default. */
+typedef struct {
+    double mu;           /* sufficient decrease, Eqs. gplsstop/cglsstop2, in (0,1/2): 0.1 */
+    double eta1;         /* Eq. pgstop2: 0.1                                               */
+    double eta2;         /* Eq. cgstop1: 0.05                                              */
+    double eta2_shrink;  /* Eq. cgstop3 refinement factor: 0.1                             */
+    double eta2_floor;   /* 1e-12                                                          */
+    int64_t gp_cap;      /* GP iterates per phase: 100                                     */
+    int64_t refine_cap;  /* cgstop3 repetitions per outer iterate: 30                      */
+    int64_t max_halvings;/* projected-search trials: 50                                    */
+    int64_t cg_cap;      /* CG iterations per call, 0 => m_k (finite termination P:444-447)*/
+    int32_t search_k;    /* step sizes evaluated per projected-search sweep: 8 (1..16)     */
+    int32_t cg_chunk;    /* CG iterations per graph launch between host polls: 32          */
+} gpcg_params;
+
+typedef struct {
+    int64_t outer_iters;  /* GPCG iterates (Table 1 "iters")                         */
+    int64_t gp_iters;     /* gradient-projection iterates (Table 1 n_GP, reading R22) */
+    int64_t cg_iters;     /* CG iterations = reduced Hessian-vector products          */
+    int64_t cg_calls;     /* CG solves (one per CG phase / refinement)               */
+    int64_t refinements;  /* Eq. cgstop3 eta2 reductions                             */
+    int64_t full_spmvs;   /* full-operator applications (gradients, searches)        */
+    int64_t n_free, n_active, n_active_nonbinding;
+    double pg_norm;       /* ||grad_Omega q(x)||_2 at return                         */
+    double q;             /* q(x) at return                                          */
+    double g0_norm;       /* ||A P[x0] - b||_2                                       */
+    double tau;           /* the absolute tolerance used                             */
+    double t_total_ms, t_cg_ms, t_gp_ms;  /* CUDA-event times (CG chunks, GP sweeps) */
+    int32_t status;
+    int32_t kernel_launches; /* library kernels launched during the call (low 31 bits) */
+} gpcg_stats;
+
+GPCG_API gpcg_params gpcg_params_default(void);
+
+/*
+ * gpcg_create_stencil2d -- A is the 5-point face-weight operator on an nx x ny
+ * grid (BASELINE.json configs[0-3]; the paper's journal-bearing discretisation
+ * P:742-779 under reading R2).  Grid point (i, j), 0-based, linear index
+ * v = i + nx*j (i fastest).
+ *   wx: x-face weights, nx+1 per grid row; wx[j*wx_ld + k] joins points
+ *       (k-1, j) and (k, j); k = 0 and k = nx are Dirichlet boundary faces.
+ *       wx_ld = 0: one row of nx+1 weights broadcast to every grid row;
+ *       otherwise wx_ld >= nx+1 and wx holds ny rows.
+ *   wy: y-face weights, ny+1 face rows of nx; wy[f*wy_ld + i] joins (i, f-1)
+ *       and (i, f).  wy_ld = 0: one row of nx broadcast; else wy_ld >= nx.
+ *   shift: nullable diagonal added to A (n entries).
+ *   (Ap)_v = (w_W + w_E + w_S + w_N + shift_v) p_v - w_W p_{v-1} - w_E p_{v+1}
+ *            - w_S p_{v-nx} - w_N p_{v+nx}   (missing neighbours are 0).
+ *   Weights must be finite and >= 0 with A SPD (e.g. all > 0); not checked
+ *   beyond finiteness -- non-SPD operators surface as GPCG_ENOTSPD in solve.
+ *   b, l, u: n entries each.  c: constant term.
+ * Returns GPCG_EINVAL on nx,ny <= 0, n >= 2^31, bad ld, l_i > u_i or NaN.
+ */
+GPCG_API int gpcg_create_stencil2d(gpcg_problem **out, void *cuda_stream, int64_t nx, int64_t ny,
+                          const double *wx, int64_t wx_ld, const double *wy, int64_t wy_ld,
+                          const double *shift, const double *b, const double *l,
+                          const double *u, double c);
+
+/*
+ * gpcg_create_csr -- A given in CSR with BOTH triangles stored:
+ * row_ptr[n+1] (int64, row_ptr[0] = 0), col[nnz] (int32, sorted within each
+ * row, 0 <= col < n), val[nnz] (fp64).  The paper's PETSc "standard
+ * compressed, sparse row" format.  Symmetry is the
+ * caller's contract (not checked).  Returns GPCG_EINVAL on n <= 0,
+ * n >= 2^31, a non-monotone row_ptr, l_i > u_i or NaN.
+ */
+GPCG_API int gpcg_create_csr(gpcg_problem **out, void *cuda_stream, int64_t n, const int64_t *row_ptr,
+                    const int32_t *col, const double *val, const double *b, const double *l,
+                    const double *u, double c);
+
+/* Replace the algorithm constants (validated: 0 < mu < 1/2, 0 < eta1, eta2 < 1, ...). */
+GPCG_API int gpcg_set_params(gpcg_problem *h, const gpcg_params *p);
+
+/*
+ * gpcg_solve -- Algorithm GPCG from x0 (projected first).
+ *   tol > 0: stop when ||grad_Omega q(x)||_2 <= tol (Eq. bqp_approximate_sol
+ *            P:296-299, Euclidean norm R4);
+ *   tol < 0: tau = |tol| * ||A P[x0] - b||_2 (BASELINE.json convention, R5).
+ *   max_it:  outer-iteration cap.
+ *   x_out:   n entries (host or device), receives the last feasible iterate
+ *            (also on GPCG_NOT_CONVERGED, GPCG_ESEARCH, GPCG_ENOTSPD).
+ *   stats:   nullable.
+ * Records the free set of x_out for gpcg_hessvec(reduced = 1).
+ */
+GPCG_API int gpcg_solve(gpcg_problem *h, const double *x0, double tol, int64_t max_it, double *x_out,
+               gpcg_stats *stats);
+
+/*
+ * gpcg_hessvec -- y = A v (reduced = 0), or the reduced Hessian product
+ * y = Z Z' A Z Z' v on the free set F recorded by the last gpcg_project or
+ * gpcg_solve (reduced = 1): A_k = Z_k' A Z_k, P:411-442 (Eq. cg2), applied
+ * in place with no extraction (the "alternative technique" of P:680-683).
+ * v is read only on F and y is 0 off F.  Returns GPCG_ESTATE if reduced = 1
+ * and no free set has been recorded.  v, y: n entries, must not alias.
+ */
+GPCG_API int gpcg_hessvec(gpcg_problem *h, const double *v, double *y, int reduced);
+
+/*
+ * gpcg_project -- px = P[x] = mid(l, u, x) and records its free
+ * set F = {i : l_i < px_i < u_i}.  Optional outputs (nullable):
+ * ||grad_Omega q(px)||_2^2 (Eq. proj-gradient), |A(px)| and
+ * |A(px) \ B(px)| (active but not binding).
+ */
+GPCG_API int gpcg_project(gpcg_problem *h, const double *x, double *px, double *pg_norm2,
+                 int64_t *n_active, int64_t *n_active_nonbinding);
+
+/* q(x) = 1/2 x'Ax - b'x + c for any x (no projection). */
+GPCG_API int gpcg_objective(gpcg_problem *h, const double *x, double *q);
+
+/* Problem size n. */
+GPCG_API int64_t gpcg_size(const gpcg_problem *h);
+
+GPCG_API void gpcg_destroy(gpcg_problem *h);
+
+/* Thread-local message of the last error ("" if none). */
+GPCG_API const char *gpcg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPCG_H */

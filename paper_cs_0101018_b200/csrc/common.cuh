@@ -1,0 +1,221 @@
+// common.cuh -- operator policies, bounds policies, device scalars and the
+// deterministic two-stage block reductions shared by every GPCG kernel.
+//
+// Layout: every vector is a dense fp64 array
+// of the n grid points / CSR rows, linear index v = i + nx*j for stencils.
+// The free mask is one byte per point (1 = free).  Vectors used by CG are
+// zero off the free set, which makes A_F p = [v in F] (A p)_v.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gpcg {
+
+constexpr int kThreads = 256;      // every kernel: 256 threads = 8 warps
+constexpr int kMaxSums = 34;       // reductions per kernel (search: 2*16 + 2)
+constexpr int kMaxK = 16;          // projected-search step sizes per sweep
+
+// ----------------------------------------------------------------------------
+// point / neighbour iteration
+// ----------------------------------------------------------------------------
+struct Pt {
+    int v, i, j;
+};
+
+// 5-point face-weight operator (gpcg.h, gpcg_create_stencil2d).  ld 0 means a
+// broadcast row.  Iteration covers 32x8 point tiles: threadIdx.x&31 runs along
+// i (coalesced), threadIdx.x>>5 along j.
+struct StencilOp {
+    int nx, ny, n;
+    const double* __restrict__ wx;
+    const double* __restrict__ wy;
+    const double* __restrict__ shift;
+    long long wx_ld, wy_ld;
+
+    __device__ __forceinline__ int num_units() const { return ((nx + 31) >> 5) * ((ny + 7) >> 3); }
+
+    template <class Body>
+    __device__ __forceinline__ void for_each_point(Body&& body) const {
+        const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+        const int ntx = (nx + 31) >> 5;
+        const int T = num_units();
+        for (int t = blockIdx.x; t < T; t += gridDim.x) {
+            const int bj = t / ntx, bi = t - bj * ntx;
+            const int i = (bi << 5) + tx, j = (bj << 3) + ty;
+            if (i < nx && j < ny) body(Pt{i + nx * j, i, j});
+        }
+    }
+
+    // cb(column, coefficient) for every stored entry of row p.v; diagonal first.
+    template <class CB>
+    __device__ __forceinline__ void for_each_nbr(const Pt& p, CB&& cb) const {
+        const double ww = __ldg(wx + (long long)p.j * wx_ld + p.i);
+        const double we = __ldg(wx + (long long)p.j * wx_ld + p.i + 1);
+        const double ws = __ldg(wy + (long long)p.j * wy_ld + p.i);
+        const double wn = __ldg(wy + (long long)(p.j + 1) * wy_ld + p.i);
+        double d = (ww + we) + (ws + wn);
+        if (shift) d += __ldg(shift + p.v);
+        cb(p.v, d);
+        if (p.i > 0) cb(p.v - 1, -ww);
+        if (p.i < nx - 1) cb(p.v + 1, -we);
+        if (p.j > 0) cb(p.v - nx, -ws);
+        if (p.j < ny - 1) cb(p.v + nx, -wn);
+    }
+};
+
+// General CSR (both triangles, int64 row_ptr, int32 col).  One thread per row.
+struct CsrOp {
+    int n;
+    const long long* __restrict__ rp;
+    const int* __restrict__ ci;
+    const double* __restrict__ val;
+
+    __device__ __forceinline__ int num_units() const { return (n + kThreads - 1) / kThreads; }
+
+    template <class Body>
+    __device__ __forceinline__ void for_each_point(Body&& body) const {
+        for (int v = blockIdx.x * kThreads + threadIdx.x; v < n; v += gridDim.x * kThreads)
+            body(Pt{v, 0, 0});
+    }
+
+    template <class CB>
+    __device__ __forceinline__ void for_each_nbr(const Pt& p, CB&& cb) const {
+        const long long e = __ldg(rp + p.v + 1);
+        for (long long k = __ldg(rp + p.v); k < e; ++k) cb(__ldg(ci + k), __ldg(val + k));
+    }
+};
+
+// ----------------------------------------------------------------------------
+// bounds: per-point arrays, or one scalar pair detected at create time
+// ----------------------------------------------------------------------------
+struct Bounds {
+    const double* __restrict__ l;
+    const double* __restrict__ u;
+    double lc, uc;
+};
+
+template <bool kScalar>
+__device__ __forceinline__ double lo(const Bounds& B, int v) {
+    if constexpr (kScalar) return B.lc; else return __ldg(B.l + v);
+}
+template <bool kScalar>
+__device__ __forceinline__ double hi(const Bounds& B, int v) {
+    if constexpr (kScalar) return B.uc; else return __ldg(B.u + v);
+}
+
+// P[x] = mid(l, u, x).  Written so that the result is exactly l or
+// u whenever x is outside, which keeps A(x) an exact-equality test (R15).
+__device__ __forceinline__ double mid(double l, double u, double x) {
+    return x < l ? l : (x > u ? u : x);
+}
+
+// Trial point of both projected searches: mid(l, u, y + alpha * (sgn * dir)).
+// GP: sgn = -1, dir = g (Eq. next-y); CG: sgn = +1, dir = d_k (Eq. cglsstop2).
+// Used verbatim by the search sweep and by the accept kernel so that the
+// accepted iterate is bit-identical to the evaluated trial.
+__device__ __forceinline__ double trial(double y, double dir, double sgn, double alpha,
+                                        double l, double u) {
+    return mid(l, u, fma(alpha, sgn * dir, y));
+}
+
+// Eq. proj-gradient; fixed variables give 0 (R16).
+__device__ __forceinline__ double pgrad(double x, double g, double l, double u) {
+    const bool al = (x == l), au = (x == u);
+    if (al && au) return 0.0;
+    if (al) return g < 0.0 ? g : 0.0;
+    if (au) return g > 0.0 ? g : 0.0;
+    return g;
+}
+
+// ----------------------------------------------------------------------------
+// device scalars (one block per handle; the host mirrors it in pinned memory)
+// ----------------------------------------------------------------------------
+enum CgReason : int { CG_RUNNING = 0, CG_PROGRESS = 1, CG_EXACT = 2, CG_CAP = 3, CG_NOTSPD = -5 };
+
+struct Scal {
+    // a1: project / accept / regrad
+    double pg2, g2, n_active, n_changed, n_nonbinding;
+    // a2: Cauchy step
+    double dd, dAd, alpha0;
+    int cauchy_ok, pad0;
+    // a3: projected search
+    double s_alpha, s_delta, s_gs;
+    int s_h, s_pad;
+    // a5: CG (Chronopoulos-Gear single-reduction form)
+    double cg_alpha, cg_beta, cg_gamma, cg_rnorm0, cg_maxdec, cg_eta2, cg_dec;
+    long long cg_it, cg_cap;
+    int cg_done, cg_reason;
+    // generic dot products (objective)
+    double r0, r1;
+};
+
+// ----------------------------------------------------------------------------
+// deterministic two-stage reduction
+// ----------------------------------------------------------------------------
+struct RedScratch {
+    double* partials;          // [kMaxSums][gridDim.x]
+    unsigned int* counter;     // zero between launches
+};
+
+template <int NS>
+__device__ __forceinline__ void warp_reduce(double (&v)[NS]) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[s] += __shfl_xor_sync(0xffffffffu, v[s], o);
+    }
+}
+
+// Block-reduce v[NS] (all threads contribute); result valid in thread 0.
+template <int NS>
+__device__ __forceinline__ void block_reduce(double (&v)[NS], double* smem /* NS*32 */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    warp_reduce<NS>(v);
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) smem[s * 32 + wid] = v[s];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) v[s] = (lane < kThreads / 32) ? smem[s * 32 + lane] : 0.0;
+        warp_reduce<NS>(v);
+    }
+    __syncthreads();
+}
+
+// Stage 1: per-block partials; stage 2: the last block to finish sums them in
+// a fixed order and calls fin(total) on thread 0.  Bitwise deterministic for
+// a fixed grid size (no float atomics; "Vec Red").
+template <int NS, class Fin>
+__device__ __forceinline__ void reduce_and_finish(double (&v)[NS], const RedScratch& R, Fin&& fin) {
+    __shared__ double smem[NS * 32];
+    __shared__ bool am_last;
+    block_reduce<NS>(v, smem);
+    const int G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) R.partials[s * G + blockIdx.x] = v[s];
+        __threadfence();
+        const unsigned t = atomicAdd(R.counter, 1u);
+        am_last = (t == (unsigned)G - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    double t[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        double acc = 0.0;
+        for (int b = threadIdx.x; b < G; b += kThreads) acc += __ldcg(R.partials + s * G + b);
+        t[s] = acc;
+    }
+    block_reduce<NS>(t, smem);
+    if (threadIdx.x == 0) {
+        *R.counter = 0u;
+        fin(t);
+    }
+}
+
+}  // namespace gpcg

@@ -43,5 +43,5 @@ if __name__ == "__main__":
     if which in ("c3", "all"):
         nx = int(sys.argv[2]) if len(sys.argv) > 2 else 200
         print(f"C3: c such that |A(x*)|/n = 0.50 at {nx}x{nx}")
-        c = bisect(lambda c: P.c3_family(nx, nx, c=c), 0.05, 5.0, 0.50, increasing=False)
+        c = bisect(lambda c: P.c3_family(nx, nx, c=c), 1e-3, 1.0, 0.50, increasing=False)
         print(f"C3_OBSTACLE_C = {c:.4g}  (check: {active_fraction(P.c3_family(nx, nx, c=float(f'{c:.4g}'))):.4f})")

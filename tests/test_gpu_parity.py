@@ -1,0 +1,276 @@
+"""CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Tolerances are those of BASELINE.json's north_star:
+  * single SpMV: ||y - y_ora||_inf <= 1e-13 ||(|A||p|)||_inf and
+                 ||y - y_ora||_2  <= 1e-13 ||y_ora||_2;
+  * projection, active/free sets, counts: bit-exact;
+  * solve: |q - q_ora| <= 1e-10 |q_ora|, ||x - x_ora||_inf <= 1e-7 (both solved to
+    a tolerance whose a-posteriori bound certifies it), identical active sets
+    away from degenerate ties (free copy within 1e-7 of the bound).
+"""
+import numpy as np
+import pytest
+
+from paper_cs_0101018_b200 import problems as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_cs_0101018_b200 import _build, gpcg
+    _build.build()
+    return gpcg
+
+
+def abs_op(A, p):
+    """|A| |p| rowwise (oracle CSR), the cancellation-free SpMV scale."""
+    rows = np.repeat(np.arange(A.n), np.diff(A.rp))
+    return np.bincount(rows, weights=np.abs(A.val) * np.abs(p[A.ci]), minlength=A.n)
+
+
+def spmv_close(y, yref, scale):
+    d = np.abs(np.asarray(y) - yref)
+    assert d.max() <= 1e-13 * max(scale.max(), 1e-300), (d.max(), scale.max())
+    assert np.linalg.norm(d) <= 1e-13 * max(np.linalg.norm(yref), 1e-300) + 1e-13 * scale.max()
+
+
+def ragged_stencil(nx, ny, seed, full=True, shift=True, bounds="two"):
+    if full:
+        wx = 0.5 + P.uniform(seed, 1, ny * (nx + 1)); wx_ld = nx + 1
+        wy = 0.5 + P.uniform(seed, 2, (ny + 1) * nx); wy_ld = nx
+    else:
+        wx = 0.5 + P.uniform(seed, 1, nx + 1); wx_ld = 0
+        wy = 0.5 + P.uniform(seed, 2, nx); wy_ld = 0
+    n = nx * ny
+    sh = 0.01 * P.uniform(seed, 3, n) if shift else None
+    b = P.gaussian(seed, 4, n)
+    if bounds == "two":
+        l = -0.3 * P.uniform(seed, 5, n)
+        u = 0.3 * P.uniform(seed, 6, n)
+    elif bounds == "inf":
+        l = np.full(n, -np.inf); u = np.full(n, np.inf)
+    else:
+        l = np.zeros(n); u = np.full(n, np.inf)
+    return P.Problem(name=f"ragged{nx}x{ny}", kind="stencil2d", n=n, b=b, l=l, u=u,
+                     x0=P.gaussian(seed, 7, n), tol=-1e-10, nx=nx, ny=ny, wx=wx, wx_ld=wx_ld,
+                     wy=wy, wy_ld=wy_ld, shift=sh)
+
+
+def dense_problem(n, seed, bounds="mixed"):
+    A, b, l, u = P.random_dense_qp(n, seed, bounds)
+    return P.csr_problem(A, b, l, u, x0=P.gaussian(seed, 9, n), tol=-1e-12, name=f"dense{n}")
+
+
+SPMV_CASES = {
+    "C0": lambda: P.c0(),
+    "C1": lambda: P.c1(),
+    "ragged37x23": lambda: ragged_stencil(37, 23, 5),
+    "ragged1x9": lambda: ragged_stencil(1, 9, 6, full=False),
+    "ragged33x1": lambda: ragged_stencil(33, 1, 7),
+    "c4_m12": lambda: P.c4_family(m=12),
+    "dense40": lambda: dense_problem(40, 3),
+}
+
+
+@pytest.mark.parametrize("case", list(SPMV_CASES))
+def test_spmv_full_and_reduced(G, oracle, case):
+    prob = SPMV_CASES[case]()
+    A = oracle.problem_csr(prob)
+    p = 2.0 * P.uniform(99, 1, prob.n) - 1.0
+    with G.Solver.from_problem(prob) as s:
+        y = s.hessvec(p)
+        spmv_close(y, oracle.spmv(A, p), abs_op(A, p))
+        # reduced: free set of P[x] for a point with ~half the bounds active
+        x = prob.x0 if np.isfinite(prob.l).any() or np.isfinite(prob.u).any() else p
+        px, pg2, na, nnb = s.project(x)
+        pref = oracle.project(prob.l, prob.u, x)
+        assert np.array_equal(px, pref)
+        free = ~oracle.sets(pref, np.zeros(prob.n), prob.l, prob.u)[0]
+        yr = s.hessvec(p, reduced=True)
+        yref = oracle.spmv_masked(A, free, p)
+        spmv_close(yr, yref, abs_op(A, p * free))
+        assert np.all(np.asarray(yr)[~free] == 0.0)
+
+
+@pytest.mark.parametrize("case", ["C0", "C1", "ragged37x23", "c4_m12", "dense40"])
+def test_project_counts_exact(G, oracle, case):
+    prob = SPMV_CASES[case]()
+    A = oracle.problem_csr(prob)
+    x = prob.x0 + 0.05 * P.gaussian(5, 5, prob.n)
+    with G.Solver.from_problem(prob) as s:
+        px, pg2, na, nnb = s.project(x)
+    pref = oracle.project(prob.l, prob.u, x)
+    assert np.array_equal(px, pref)
+    g = oracle.gradient(A, prob.b, pref)
+    act, bnd, na_ref, nb_ref = oracle.sets(pref, g, prob.l, prob.u)
+    assert na == na_ref
+    assert nnb == na_ref - nb_ref
+    pg_ref = np.sum(oracle.proj_grad(pref, g, prob.l, prob.u) ** 2)
+    assert abs(pg2 - pg_ref) <= 1e-12 * pg_ref
+
+
+def test_objective(G, oracle):
+    prob = P.c1()
+    A = oracle.problem_csr(prob)
+    x = P.gaussian(3, 3, prob.n) * 1e-3
+    with G.Solver.from_problem(prob) as s:
+        q = s.objective(x)
+    qref = oracle.objective(A, prob.b, prob.c, x)
+    assert abs(q - qref) <= 1e-12 * abs(qref)
+
+
+def _tie_mismatches(x, xr, l, u):
+    act = (x == l) | (x == u)
+    actr = (xr == l) | (xr == u)
+    mism = np.flatnonzero(act != actr)
+    nontie = []
+    for i in mism:
+        free_val = x[i] if not act[i] else xr[i]
+        bound = l[i] if (xr[i] == l[i] or x[i] == l[i]) else u[i]
+        if abs(free_val - bound) > 1e-7:
+            nontie.append(i)
+    return len(mism), nontie
+
+
+SOLVE_CASES = {
+    "C0": (lambda: P.c0(), -1e-12),
+    "C1": (lambda: P.c1(), -1e-11),
+    "jb80_eps0.9": (lambda: P.journal_bearing(80, 60, eps=0.9), -1e-11),
+    "c3_family_160": (lambda: P.c3_family(160, 160), -1e-11),
+    "c4_family_m16": (lambda: P.c4_family(m=16), -1e-11),
+    "ragged37x23": (lambda: ragged_stencil(37, 23, 5), -1e-12),
+    "ragged_inf": (lambda: ragged_stencil(19, 13, 8, bounds="inf"), -1e-12),
+    "dense8": (lambda: dense_problem(8, 21), -1e-12),
+}
+
+
+@pytest.mark.parametrize("case", list(SOLVE_CASES))
+def test_solve_parity(G, oracle, case):
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    assert rc_o == 0
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0, (rc, st)
+    assert np.all(x >= prob.l) and np.all(x <= prob.u)
+    assert st["pg_norm"] <= st["tau"]
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
+    nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+    assert not nontie, (nm, nontie[:10])
+    # oracle's own certificate of the GPU point: KKT via one CPU SpMV
+    A = oracle.problem_csr(prob)
+    g = oracle.gradient(A, prob.b, x)
+    pg = np.linalg.norm(oracle.proj_grad(x, g, prob.l, prob.u))
+    assert pg <= 1.01 * st["tau"] + 1e-15
+
+
+def test_solve_unconstrained_is_direct_solve(G):
+    prob = dense_problem(30, 77, bounds="inf")
+    A = np.zeros((30, 30))
+    rows = np.repeat(np.arange(30), np.diff(prob.row_ptr))
+    A[rows, prob.col] = prob.val
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(np.zeros(30), -1e-13)
+    assert rc == 0 and np.max(np.abs(x - np.linalg.solve(A, prob.b))) <= 1e-9
+
+
+def test_solve_enumeration_small(G):
+    from tests import _brute as B
+    for sd in range(20):
+        n = 2 + sd % 7
+        A, b, l, u = P.random_dense_qp(n, seed=3000 + sd, bounds="mixed")
+        prob = P.csr_problem(A, b, l, u, x0=P.gaussian(sd, 1, n))
+        with G.Solver.from_problem(prob) as s:
+            rc, x, st = s.solve(prob.x0, -1e-12)
+        assert rc == 0
+        assert np.max(np.abs(x - B.enum_solve(A, b, l, u))) <= 1e-6
+
+
+def test_device_pointers_and_determinism(G):
+    import torch
+    prob = P.c1()
+    with G.Solver.from_problem(prob, device="cuda") as s:
+        x0 = torch.from_numpy(prob.x0).cuda()
+        rc1, x1, st1 = s.solve(x0, -1e-8)
+        rc2, x2, st2 = s.solve(x0, -1e-8)
+    assert x1.is_cuda and rc1 == 0
+    assert torch.equal(x1, x2)                     # bitwise reproducible
+    assert st1["cg_iters"] == st2["cg_iters"]
+
+
+# ------------------------------------------------------------------ edge cases
+def test_edge_tiny_grids(G, oracle):
+    for nx, ny in [(1, 1), (1, 2), (3, 1)]:
+        prob = ragged_stencil(nx, ny, 40 + nx + ny)
+        rc_o, x_o, st_o = oracle.solve_problem(prob, tol=-1e-12)
+        with G.Solver.from_problem(prob) as s:
+            rc, x, st = s.solve(prob.x0, -1e-12)
+        assert rc == 0 and np.max(np.abs(x - x_o)) <= 1e-9
+
+
+def test_edge_all_fixed_and_converged_start(G):
+    prob = ragged_stencil(9, 7, 3)
+    prob.l = prob.u = np.full(prob.n, 0.125)
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(np.zeros(prob.n), 1e-10)
+    assert rc == 0 and np.all(x == 0.125) and st["outer_iters"] == 0 and st["n_free"] == 0
+    prob = P.journal_bearing(10, 10, eps=0.0)                # x* = 0 = x0
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(np.zeros(prob.n), 1e-12)
+    assert rc == 0 and np.all(x == 0.0) and st["outer_iters"] == 0
+
+
+def test_edge_errors(G):
+    prob = ragged_stencil(5, 4, 1)
+    with G.Solver.from_problem(prob) as s:
+        with pytest.raises(G.GpcgError) as e:
+            s.hessvec(np.ones(prob.n), reduced=True)
+        assert e.value.code == G.ESTATE
+    bad = ragged_stencil(5, 4, 1)
+    bad.l = bad.l.copy(); bad.l[3] = 1.0; bad.u = bad.u.copy(); bad.u[3] = 0.0
+    with pytest.raises(G.GpcgError) as e:
+        G.Solver.from_problem(bad)
+    assert e.value.code == G.EINVAL
+    nanb = ragged_stencil(5, 4, 1)
+    nanb.b = nanb.b.copy(); nanb.b[0] = np.nan
+    with pytest.raises(G.GpcgError):
+        G.Solver.from_problem(nanb)
+    indef = P.csr_problem(np.array([[1.0, 2.0], [2.0, 1.0]]), [1.0, -1.0], [-1e3, -1e3], [1e3, 1e3])
+    with G.Solver.from_problem(indef) as s:
+        rc, x, st = s.solve(np.zeros(2), 1e-8, allow_error=True)
+    assert rc == G.ENOTSPD
+
+
+def test_not_converged_returns_feasible(G):
+    prob = P.c1()
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(prob.x0, -1e-12, max_it=1)
+    assert rc == G.NOT_CONVERGED and st["outer_iters"] == 1
+    assert np.all(x >= prob.l) and np.all(x <= prob.u)
+
+
+# ------------------------------------------------------------------ full size (bench config)
+def test_c2_full_size_certificate(G, oracle):
+    """C2 (1600^2, the bench workload): GPU solve certified by the oracle's own
+    SpMV (KKT / ||grad_Omega q|| / B = A), sampled SpMV rows, free fraction."""
+    prob = P.c2()
+    A = oracle.problem_csr(prob)
+    with G.Solver.from_problem(prob) as s:
+        p = 2.0 * P.uniform(5, 1, prob.n) - 1.0
+        y = s.hessvec(p)
+        idx = (P.uniform(5, 2, 2000) * prob.n).astype(np.int64)
+        sub = oracle.spmv(A, p)
+        spmv_close(y[idx], sub[idx], abs_op(A, p)[idx])
+        rc, x, st = s.solve(prob.x0, prob.tol)
+    assert rc == 0
+    g = oracle.gradient(A, prob.b, x)
+    pg = np.linalg.norm(oracle.proj_grad(x, g, prob.l, prob.u))
+    assert pg <= 1.01 * st["tau"]
+    act, bnd, na, nb = oracle.sets(x, g, prob.l, prob.u)
+    assert na == st["n_active"] and na - nb == 0
+    assert 0.60 <= 1 - na / prob.n <= 0.76           # PAPER.md:876-878 (~68% free)
