@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""bench.py -- GPCG hot-path benchmark (BASELINE.json metric) on B200.
+
+A "step" is one full GPCG solve (Algorithm GPCG: every row of
+SURVEY.md 8(a) -- GP sweeps a1/a2/a3, CG a4/a5, reductions a6, control a7) of
+the configured workload from x0 to tol, inputs resident in HBM.
+
+  value   = reduced Hessian-vector products per second over the K timed solves
+            (one per CG iteration: the masked SpMV A_F rho inside k_cg_iter),
+            aggregated over ranks; solve seconds are reported beside it.
+  e2e     = the same metric through the C ABI with HOST (pinned) buffers:
+            create (H2D of operator, b, l, u) + solve (H2D x0, D2H x) + destroy.
+  roofline: dominant kernel k_cg_iter; algorithmic bytes per launch
+            (80 + coef) B per free point + 1 B mask per point, over
+            its CUDA-event-timed steady-state launch duration.
+  cpu_baseline / --impl reference: the plain-C oracle (oracle/) on the same
+            workload, bounded by a time budget, on the host cores (1 thread).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+N > 1 runs under torchrun (one process per GPU); see DESIGN.md "Multi-GPU".
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reduced Hessian-vector products/s and HBM GB/s (% of 8 TB/s); GPCG solve s"
+UNIT = "reduced HVP/s"
+
+WORKLOADS = {
+    "C0": "C0: journal bearing 50x50 (n=2,500), eps=0.1, l=0, u=inf, x0=0, tol 1e-8*||g(x0)|| [BASELINE.json configs[0]]",
+    "C1": "C1: 400x400 (n=160,000) noisy faces, Gaussian b, 40%-active two-sided obstacles [configs[1]]",
+    "C2": "C2: journal bearing 1600x1600 (n=2,560,000), eps=0.1, l=0, u=inf, x0=0, tol 1e-8*||g(x0)||, "
+          "stencil-specialised masked SpMV, 1 B200 [configs[2]]",
+    "C3": "C3: 8000x8000 (n=64,000,000) journal bearing with 50%-active two-sided obstacles [configs[3]]",
+    "C4": "C4: 256^3 (n=16,777,216) 7-point lognormal CSR, box [-0.01,0.01] [configs[4]]",
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cg_bytes_per_free_point(prob):
+    """Algorithmic bytes of one k_cg_iter launch per free point:
+    5 fp64 vectors read (rho, q, s, p, w) + 5 written = 80 B, plus operator data
+    a free row must read: 0 (broadcast face weights, O(nx) cached), 16 B (full
+    face arrays: one x- and one y-face weight per point), CSR 8 B row_ptr +
+    12 B per stored entry."""
+    if prob.kind == "stencil2d":
+        return 80.0 + (16.0 if (prob.wx_ld or prob.wy_ld) else 0.0)
+    z = prob.val.size / prob.n
+    return 80.0 + 8.0 + 12.0 * z
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.f.read().splitlines():
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def oracle_sample(prob, budget_s):
+    """Oracle GPCG on prob for at most budget_s seconds -> (cg_iters, seconds, stats)."""
+    from oracle import oracle as O
+    A = O.problem_csr(prob)
+    params = O.default_params(time_budget_s=float(budget_s))
+    rc, x, st = O.solve(A, prob.b, prob.l, prob.u, prob.c, prob.x0, prob.tol, 500, params)
+    return st["cg_iters"], st["seconds"], st
+
+
+def run_reference(args):
+    """--impl reference: the oracle (plain C, 1 thread) timed on the host, same workload/metric."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    from paper_cs_0101018_b200 import problems as P
+    prob = P.get(args.config)
+    total = args.steps + args.warmup
+    budget = max(5.0, min(20.0, 150.0 / max(total, 1)))
+    for _ in range(args.warmup):
+        oracle_sample(prob, budget)
+    iters, secs = 0, 0.0
+    last = None
+    for _ in range(args.steps):
+        it, s, st = oracle_sample(prob, budget)
+        iters += it
+        secs += s
+        last = st
+    value = iters / secs if secs > 0 else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "n": prob.n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"each step: the first {budget:.0f} s of the {args.config} GPCG solve "
+                                   f"(oracle stops at the time budget; last step: {last['outer_iters']} outer, "
+                                   f"{last['gp_iters']} GP, {last['cg_iters']} CG iterations)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_cs_0101018_b200 import problems as P
+    from paper_cs_0101018_b200 import gpcg
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    prob = P.get(args.config)
+    stream = torch.cuda.current_stream()
+    solver = gpcg.Solver.from_problem(prob, stream=stream, device=dev)
+    x0 = torch.from_numpy(prob.x0).to(dev)
+    x_out = torch.empty_like(x0)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+
+    for _ in range(args.warmup):
+        solver.solve(x0, prob.tol, x_out=x_out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    tot_ms = 0.0
+    agg = {"cg_iters": 0, "gp_iters": 0, "outer_iters": 0, "kernel_launches": 0, "cg_iters_timed": 0,
+           "cg_free_iters_timed": 0, "t_cg_timed_ms": 0.0, "t_cg_ms": 0.0}
+    last = None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        flush.zero_()                                   # L2 flushed between timed solves
+        torch.cuda.synchronize()
+        e0.record(stream)
+        rc, _, st = solver.solve(x0, prob.tol, x_out=x_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tot_ms += e0.elapsed_time(e1)
+        assert rc == 0, (rc, st)
+        for k in agg:
+            agg[k] += st[k]
+        last = st
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    hvps = float(agg["cg_iters"])
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        h = torch.tensor([hvps], dtype=torch.float64, device=dev)
+        dist.all_reduce(h, op=dist.ReduceOp.SUM)
+        tot_ms, hvps = float(t.item()), float(h.item())
+    value = hvps / (tot_ms / 1e3)
+
+    # roofline of the dominant kernel (k_cg_iter), steady-state CUDA-event timing
+    peak, peak_src = load_peaks()
+    bpp = cg_bytes_per_free_point(prob)
+    it_t = max(agg["cg_iters_timed"], 1)
+    bytes_per_launch = (bpp * agg["cg_free_iters_timed"] + 1.0 * prob.n * agg["cg_iters_timed"]) / it_t
+    launch_s = (agg["t_cg_timed_ms"] / 1e3) / it_t
+    achieved = bytes_per_launch / launch_s / 1e9 if agg["cg_iters_timed"] else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+
+    # e2e: through the C ABI with host (pinned) buffers, H2D/D2H inside the timed region
+    def pinned(a):
+        return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hp = P.Problem(**{**prob.__dict__})
+    for k in ("b", "l", "u", "x0", "wx", "wy", "shift", "row_ptr", "col", "val"):
+        setattr(hp, k, pinned(getattr(prob, k)))
+    xh = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    s_e2e = gpcg.Solver.from_problem(hp, stream=stream)          # warm-up of the e2e path
+    s_e2e.solve(hp.x0, prob.tol, x_out=xh)
+    s_e2e.close()
+    e2e_s, e2e_hvps = 0.0, 0
+    for _ in range(e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2 = gpcg.Solver.from_problem(hp, stream=stream)
+        rc, _, st2 = s2.solve(hp.x0, prob.tol, x_out=xh)
+        s2.close()
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t0
+        e2e_hvps += st2["cg_iters"]
+    e2e_val = e2e_hvps / e2e_s
+    if world > 1:
+        t = torch.tensor([e2e_s, e2e_hvps], dtype=torch.float64, device=dev)
+        tm = t.clone(); dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_val = float(t[1].item()) / float(tm[0].item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        it, secs, stc = oracle_sample(prob, args.cpu_budget)
+        cpu = {"value": it / secs if secs > 0 else 0.0, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {args.cpu_budget:.0f} s of the {args.config} GPCG solve on 1 host core "
+                         f"({stc['outer_iters']} outer, {stc['gp_iters']} GP, {stc['cg_iters']} CG iterations "
+                         f"done; oracle stops at the time budget)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, paper_cs_0101018_b200/problems.py)",
+            "config": {"workload": WORKLOADS[args.config], "n": prob.n,
+                       "l2": "flushed (256 MB write) between timed solves",
+                       "parallelism": "1 GPU per solve" if world == 1 else f"{world} independent replicas"},
+            "solve": {"s_per_solve": tot_ms / args.steps / 1e3, "outer_iters": last["outer_iters"],
+                      "gp_iters": last["gp_iters"], "cg_iters": last["cg_iters"],
+                      "n_free": last["n_free"], "q": last["q"], "pg_norm": last["pg_norm"],
+                      "tau": last["tau"], "t_cg_share": agg["t_cg_ms"] / tot_ms},
+            "roofline": {"bound": "hbm", "kernel": "k_cg_iter<StencilOp>" if prob.kind == "stencil2d"
+                         else "k_cg_iter<CsrOp>",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None,
+                         "frac_of_8TBs": (achieved / 8000.0) if achieved else None,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_launch": bytes_per_launch, "us_per_launch": launch_s * 1e6,
+                         "algorithmic_bytes": f"{bpp:.0f} B per free point + 1 B mask per point"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT,
+                    "h2d_bytes_per_step": int(prob.input_bytes()),
+                    "d2h_bytes_per_step": int(prob.n * 8),
+                    "what": "gpcg_create (H2D operator,b,l,u from pinned host) + gpcg_solve (H2D x0, "
+                            "D2H x) + gpcg_destroy, wall clock, %d steps" % e2e_steps},
+            "gpu_launches": agg["kernel_launches"],
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    from paper_cs_0101018_b200 import _build
+    _build.build()
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

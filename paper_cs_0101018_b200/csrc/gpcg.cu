@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -53,6 +54,11 @@ int set_err(int code, const char* fmt, ...) {
                            __FILE__, __LINE__);                                               \
     } while (0)
 
+bool trace_on() {
+    static const bool on = getenv("GPCG_TRACE") != nullptr;
+    return on;
+}
+
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -86,6 +92,7 @@ struct gpcg_problem {
     // work vectors
     double *Y[2] = {nullptr, nullptr}, *G[2] = {nullptr, nullptr};
     unsigned char* M[2] = {nullptr, nullptr};
+    unsigned char* Mcg = nullptr;  // free mask of the running CG call (fixed address for the graph)
     double *W = nullptr, *P = nullptr;
     double *Rho[2] = {nullptr, nullptr}, *Q[2] = {nullptr, nullptr}, *S2[2] = {nullptr, nullptr};
     double *stage_in = nullptr, *stage_out = nullptr;
@@ -100,8 +107,10 @@ struct gpcg_problem {
     // CG graph chunk
     cudaGraphExec_t cg_exec = nullptr;
     int cg_exec_chunk = 0;
-    int cg_exec_mask = -1;
     long long launches = 0;
+    cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
+    long long cg_iters_timed = 0, cg_free_iters_timed = 0;
+    double t_cg_timed_ms = 0.0;
 
     RedScratch red() const { return RedScratch{partials, counter}; }
 };
@@ -178,7 +187,7 @@ void free_all(gpcg_problem* h) {
     cudaSetDevice(h->dev);
     if (h->st) cudaStreamSynchronize(h->st);
     void* ptrs[] = {h->wx, h->wy, h->shift, h->rp, h->ci, h->val, h->b, h->l, h->u,
-                    h->Y[0], h->Y[1], h->G[0], h->G[1], h->M[0], h->M[1], h->W, h->P,
+                    h->Y[0], h->Y[1], h->G[0], h->G[1], h->M[0], h->M[1], h->Mcg, h->W, h->P,
                     h->Rho[0], h->Rho[1], h->Q[0], h->Q[1], h->S2[0], h->S2[1],
                     h->stage_in, h->stage_out, h->dS, h->partials, h->counter};
     for (void* p : ptrs)
@@ -188,6 +197,8 @@ void free_all(gpcg_problem* h) {
     if (h->ev_sync) cudaEventDestroy(h->ev_sync);
     if (h->ev_a) cudaEventDestroy(h->ev_a);
     if (h->ev_b) cudaEventDestroy(h->ev_b);
+    if (h->ev_c0) cudaEventDestroy(h->ev_c0);
+    if (h->ev_c1) cudaEventDestroy(h->ev_c1);
     if (h->st) cudaStreamDestroy(h->st);
     delete h;
 }
@@ -206,6 +217,8 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
     CK(cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev_a));
     CK(cudaEventCreate(&h->ev_b));
+    CK(cudaEventCreate(&h->ev_c0));
+    CK(cudaEventCreate(&h->ev_c1));
     CK(cudaEventRecord(h->ev_sync, h->user));
     CK(cudaStreamWaitEvent(h->st, h->ev_sync, 0));
     const size_t nb = (size_t)h->n * sizeof(double);
@@ -216,6 +229,7 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
         CK(cudaMalloc(&h->Y[k], nb));
         CK(cudaMalloc(&h->G[k], nb));
         CK(cudaMalloc(&h->M[k], (size_t)h->n));
+        if (k == 0) CK(cudaMalloc(&h->Mcg, (size_t)h->n));
         CK(cudaMalloc(&h->Rho[k], nb));
         CK(cudaMalloc(&h->Q[k], nb));
         CK(cudaMalloc(&h->S2[k], nb));
@@ -342,7 +356,7 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
         const int a = i & 1, bb = a ^ 1;
         with_op_only(h, [&](auto& op) {
             using Op = std::decay_t<decltype(op)>;
-            k_cg_iter<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->M[h->free_mask], h->Rho[a], h->Q[a], h->S2[a],
+            k_cg_iter<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->Mcg, h->Rho[a], h->Q[a], h->S2[a],
                                                            h->Rho[bb], h->Q[bb], h->S2[bb], h->P, h->W,
                                                            h->dS, h->red());
         });
@@ -357,17 +371,11 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
 }
 
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
-int run_cg(gpcg_problem* h, int cur, double eta2, long long cap, long long* iters) {
+int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     int rc;
-    h->free_mask = cur;
-    // the graph bakes in the mask pointer: rebuild if the mask buffer changed
-    if (h->cg_exec && h->cg_exec_mask != cur) {
-        cudaGraphExecDestroy(h->cg_exec);
-        h->cg_exec = nullptr;
-    }
     with_op_only(h, [&](auto& op) {
         using Op = std::decay_t<decltype(op)>;
-        k_cg_init<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->G[cur], h->M[cur], h->Rho[0], h->Q[0], h->S2[0],
+        k_cg_init<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->G[cur], h->M[cur], h->Mcg, h->Rho[0], h->Q[0], h->S2[0],
                                                        h->Rho[1], h->Q[1], h->S2[1], h->P, h->W, eta2, cap,
                                                        h->dS, h->red());
     });
@@ -375,12 +383,19 @@ int run_cg(gpcg_problem* h, int cur, double eta2, long long cap, long long* iter
     CKLAUNCH();
     const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
     if ((rc = build_cg_graph(h, chunk))) return rc;
-    h->cg_exec_mask = cur;
     for (;;) {
+        CK(cudaEventRecord(h->ev_c0, h->st));
         CK(cudaGraphLaunch(h->cg_exec, h->st));
+        CK(cudaEventRecord(h->ev_c1, h->st));
         h->launches += chunk;
         if ((rc = sync_scal(h))) return rc;
         if (h->hS->cg_done) break;
+        // every iteration of this chunk was real: steady-state timing sample
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_c0, h->ev_c1));
+        h->t_cg_timed_ms += ms;
+        h->cg_iters_timed += chunk;
+        h->cg_free_iters_timed += chunk * m;
     }
     *iters = h->hS->cg_it;
     if (h->hS->cg_reason == CG_NOTSPD)
@@ -607,6 +622,8 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     gpcg_stats st;
     memset(&st, 0, sizeof st);
     h->launches = 0;
+    h->cg_iters_timed = h->cg_free_iters_timed = 0;
+    h->t_cg_timed_ms = 0.0;
     int rc;
     if ((rc = enter(h))) return rc;
     const gpcg_params& prm = h->prm;
@@ -647,6 +664,10 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 ++j;
                 st.gp_iters++;
                 const double dec = -S.s_delta;                      // q(y_{j-1}) - q(y_j)
+                if (trace_on())
+                    fprintf(stderr, "[gpcg] k=%lld GP j=%lld h=%d alpha=%.3e dec=%.3e |A|=%.0f changed=%.0f pg=%.3e t=%.2fms\n",
+                            (long long)k, j, S.s_h, S.s_alpha, dec, S.n_active, S.n_changed, std::sqrt(S.pg2),
+                            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
                 const bool stop = (S.n_changed == 0.0) ||           // Eq. pgstop1 (index sets, R9)
                                   (j >= 2 && dec <= prm.eta1 * maxdec) ||   // Eq. pgstop2 (R10)
                                   (j >= prm.gp_cap);
@@ -667,7 +688,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 const long long cap = prm.cg_cap > 0 ? prm.cg_cap : m;
                 long long its = 0;
                 CK(cudaEventRecord(h->ev_a, h->st));
-                rc = run_cg(h, cur, eta2, cap, &its);
+                rc = run_cg(h, cur, m, eta2, cap, &its);
                 st.cg_calls++;
                 st.cg_iters += its;
                 if (rc) goto fail;
@@ -680,6 +701,12 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 if ((rc = search_and_accept(h, cur, h->W, 1.0, 0, &hacc))) goto fail;
                 st.full_spmvs += 2;
                 cur ^= 1;
+                if (trace_on())
+                    fprintf(stderr, "[gpcg] k=%lld CG rep=%lld m=%lld its=%lld reason=%d cg_ms=%.2f search_h=%d "
+                            "|A|=%.0f nonbinding=%.0f pg=%.3e t=%.2fms\n",
+                            (long long)k, (long long)rep, m, its, S.cg_reason, ms, hacc, S.n_active, S.n_nonbinding,
+                            std::sqrt(S.pg2),
+                            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
                 if (std::sqrt(S.pg2) <= tau) { status = GPCG_OK; break; }
                 if (S.n_nonbinding != 0.0) break;                   // Eq. cgstop3 fails
                 eta2 = std::max(eta2 * prm.eta2_shrink, prm.eta2_floor);
@@ -706,6 +733,9 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     st.t_gp_ms = t_gp;
     st.status = status;
     st.kernel_launches = (int32_t)(h->launches & 0x7fffffff);
+    st.cg_iters_timed = h->cg_iters_timed;
+    st.cg_free_iters_timed = h->cg_free_iters_timed;
+    st.t_cg_timed_ms = h->t_cg_timed_ms;
     st.t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     if (stats) *stats = st;
     if ((rc = leave(h))) return rc;

@@ -217,16 +217,18 @@ k_objective(Op A, const double* __restrict__ x, const double* __restrict__ b, Sc
 template <class Op>
 __global__ void __launch_bounds__(kThreads)
 k_cg_init(Op A, const double* __restrict__ g, const unsigned char* __restrict__ mask,
-          double* __restrict__ rho, double* __restrict__ q, double* __restrict__ s,
+          unsigned char* __restrict__ mask_cg, double* __restrict__ rho, double* __restrict__ q, double* __restrict__ s,
           double* __restrict__ rho2, double* __restrict__ q2, double* __restrict__ s2,
           double* __restrict__ p, double* __restrict__ w, double eta2, long long cap,
           Scal* S, RedScratch R) {
     double acc[2] = {0.0, 0.0};
     A.for_each_point([&](const Pt& pt) {
         const int v = pt.v;
+        const unsigned char mv = mask[v];
+        mask_cg[v] = mv;                       // the CG graph reads this fixed buffer
         p[v] = 0.0; w[v] = 0.0; s[v] = 0.0;
         rho2[v] = 0.0; q2[v] = 0.0; s2[v] = 0.0;
-        if (!mask[v]) { rho[v] = 0.0; q[v] = 0.0; return; }
+        if (!mv) { rho[v] = 0.0; q[v] = 0.0; return; }
         double qv = 0.0, rv = 0.0;
         A.for_each_nbr(pt, [&](int c, double a) {
             const double rc = mask[c] ? -__ldg(g + c) : 0.0;

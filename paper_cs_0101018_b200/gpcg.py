@@ -39,7 +39,9 @@ class Stats(C.Structure):
                 ("n_free", C.c_int64), ("n_active", C.c_int64), ("n_active_nonbinding", C.c_int64),
                 ("pg_norm", C.c_double), ("q", C.c_double), ("g0_norm", C.c_double), ("tau", C.c_double),
                 ("t_total_ms", C.c_double), ("t_cg_ms", C.c_double), ("t_gp_ms", C.c_double),
-                ("status", C.c_int32), ("kernel_launches", C.c_int32)]
+                ("status", C.c_int32), ("kernel_launches", C.c_int32),
+                ("cg_iters_timed", C.c_int64), ("cg_free_iters_timed", C.c_int64),
+                ("t_cg_timed_ms", C.c_double)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
