@@ -241,8 +241,7 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
     CK(cudaMalloc(&h->dS, sizeof(Scal)));
     CK(cudaMemsetAsync(h->dS, 0, sizeof(Scal), h->st));
     CK(cudaMallocHost(&h->hS, sizeof(Scal)));
-    h->grid = std::max(1, std::min(units(h), h->sms * 4));
-    const int gmax = std::max(h->grid, h->sms * 4);
+    const int gmax = h->sms * 4;          // h->grid is set once the operator is known
     CK(cudaMalloc(&h->partials, (size_t)kMaxSums * gmax * sizeof(double)));
     CK(cudaMalloc(&h->counter, sizeof(unsigned int)));
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
@@ -473,6 +472,7 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     h->is_csr = false;
     h->sop = StencilOp{(int)nx, (int)ny, h->n, h->wx, h->wy, h->shift, (long long)wx_ld, (long long)wy_ld};
     h->nnz = 5 * (long long)h->n - 2 * nx - 2 * ny;
+    h->grid = std::max(1, std::min(units(h), h->sms * 4));
     if ((rc = leave(h))) return fail(rc);
     *out = h;
     return GPCG_OK;
@@ -518,6 +518,7 @@ int gpcg_create_csr(gpcg_problem** out, void* cuda_stream, int64_t n, const int6
     if (t != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite CSR values", t));
     h->is_csr = true;
     h->cop = CsrOp{h->n, h->rp, h->ci, h->val};
+    h->grid = std::max(1, std::min(units(h), h->sms * 4));
     if ((rc = leave(h))) return fail(rc);
     *out = h;
     return GPCG_OK;
