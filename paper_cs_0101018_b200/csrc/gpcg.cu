@@ -21,6 +21,7 @@
 
 #include "gpcg.h"
 #include "kernels.cuh"
+#include "march.cuh"
 
 using namespace gpcg;
 
@@ -101,7 +102,9 @@ struct gpcg_problem {
     Scal* hS = nullptr;            // pinned mirror
     double* partials = nullptr;
     unsigned int* counter = nullptr;
-    int grid = 1;
+    int grid = 1;                  // generic kernels (CSR, hessvec, objective)
+    MarchGeom mg1{}, mg2{};        // column-march geometry for halo 1 / halo 2 stencil kernels
+    int grid_m1 = 1, grid_m2 = 1;
     gpcg_params prm{};
     int free_mask = -1;            // index into M of the recorded free set, -1 none
     // CG graph chunk
@@ -203,6 +206,23 @@ void free_all(gpcg_problem* h) {
     delete h;
 }
 
+constexpr int kMarchTY = 16;
+
+MarchGeom march_geom(int nx, int ny, int H) {
+    MarchGeom g;
+    g.nstrips = (nx + (32 - 2 * H) - 1) / (32 - 2 * H);
+    g.TY = kMarchTY;
+    g.nchunks = (ny + g.TY - 1) / g.TY;
+    return g;
+}
+int march_grid(const MarchGeom& g) {
+    const long long items = (long long)g.nstrips * g.nchunks;
+    return (int)std::max<long long>(1, (items + kThreads / 32 - 1) / (kThreads / 32));
+}
+long long march_grid_bound(const gpcg_problem* h) {
+    return std::max(march_grid(h->mg1), march_grid(h->mg2));
+}
+
 // common part of create: device, streams, vectors, bounds, validation
 int create_common(gpcg_problem* h, void* stream, const double* b, const double* l, const double* u) {
     int ndev = 0;
@@ -241,7 +261,10 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
     CK(cudaMalloc(&h->dS, sizeof(Scal)));
     CK(cudaMemsetAsync(h->dS, 0, sizeof(Scal), h->st));
     CK(cudaMallocHost(&h->hS, sizeof(Scal)));
-    const int gmax = h->sms * 4;          // h->grid is set once the operator is known
+    // partial sums of the largest grid any kernel of this handle uses (grid-stride
+    // generic kernels are capped at 16 blocks/SM; march grids are one warp per item)
+    long long gmax = (long long)h->sms * 16;
+    if (!h->is_csr) gmax = std::max<long long>(gmax, march_grid_bound(h));
     CK(cudaMalloc(&h->partials, (size_t)kMaxSums * gmax * sizeof(double)));
     CK(cudaMalloc(&h->counter, sizeof(unsigned int)));
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
@@ -269,6 +292,17 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
 // ---------------------------------------------------------------- launches
 int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double sgn,
                   const unsigned char* mask_prev, double* y_out, double* g_out, unsigned char* m_out) {
+    if (!h->is_csr) {   // stencil: accept + regrad + mask + counts + next Cauchy step in one sweep
+        if (h->sb)
+            k2_accept<true><<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
+                                                                mask_prev, y_out, g_out, m_out, h->dS, h->red());
+        else
+            k2_accept<false><<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
+                                                                 mask_prev, y_out, g_out, m_out, h->dS, h->red());
+        h->launches++;
+        CKLAUNCH();
+        return GPCG_OK;
+    }
     with_op(h, [&](auto& op, auto sbt) {
         using Op = std::decay_t<decltype(op)>;
         constexpr bool SB = decltype(sbt)::value;
@@ -281,6 +315,7 @@ int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double
 }
 
 int launch_cauchy(gpcg_problem* h, const double* y, const double* g) {
+    if (!h->is_csr) return GPCG_OK;     // computed by the preceding k2_accept sweep
     with_op(h, [&](auto& op, auto sbt) {
         using Op = std::decay_t<decltype(op)>;
         constexpr bool SB = decltype(sbt)::value;
@@ -300,6 +335,28 @@ int launch_search(gpcg_problem* h, const double* y, const double* g, const doubl
                   int use_alpha0, int h0) {
     const int K = search_k(h);
     const double mu = h->prm.mu;
+    if (!h->is_csr) {
+        const bool dg = (dir == g);
+        auto go = [&](auto sbt, auto kt, auto dgt) {
+            constexpr bool SB = decltype(sbt)::value;
+            constexpr int KK = decltype(kt)::value;
+            constexpr bool DG = decltype(dgt)::value;
+            k2_search<SB, KK, DG><<<h->grid_m1, kThreads, 0, h->st>>>(h->sop, h->mg1, h->bounds, y, g, dir, sgn,
+                                                                       use_alpha0, h0, mu, h->dS, h->red());
+        };
+        auto byk = [&](auto sbt, auto dgt) {
+            if (K == 4) go(sbt, std::integral_constant<int, 4>(), dgt);
+            else if (K == 8) go(sbt, std::integral_constant<int, 8>(), dgt);
+            else go(sbt, std::integral_constant<int, 16>(), dgt);
+        };
+        auto bydg = [&](auto sbt) {
+            if (dg) byk(sbt, std::true_type()); else byk(sbt, std::false_type());
+        };
+        if (h->sb) bydg(std::true_type()); else bydg(std::false_type());
+        h->launches++;
+        CKLAUNCH();
+        return GPCG_OK;
+    }
     with_op(h, [&](auto& op, auto sbt) {
         using Op = std::decay_t<decltype(op)>;
         constexpr bool SB = decltype(sbt)::value;
@@ -353,6 +410,11 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < chunk; ++i) {
         const int a = i & 1, bb = a ^ 1;
+        if (!h->is_csr) {   // stencil: rho, p ping-pong (p in Q[]), w in place
+            k2_cg_iter<<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a], h->Rho[bb],
+                                                           h->Q[bb], h->W, h->dS, h->red());
+            continue;
+        }
         with_op_only(h, [&](auto& op) {
             using Op = std::decay_t<decltype(op)>;
             k_cg_iter<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->Mcg, h->Rho[a], h->Q[a], h->S2[a],
@@ -372,7 +434,10 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     int rc;
-    with_op_only(h, [&](auto& op) {
+    if (!h->is_csr) {
+        k2_cg_init<<<h->grid_m1, kThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg, h->Rho[0],
+                                                       h->Q[0], h->W, eta2, cap, h->dS, h->red());
+    } else with_op_only(h, [&](auto& op) {
         using Op = std::decay_t<decltype(op)>;
         k_cg_init<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->G[cur], h->M[cur], h->Mcg, h->Rho[0], h->Q[0], h->S2[0],
                                                        h->Rho[1], h->Q[1], h->S2[1], h->P, h->W, eta2, cap,
@@ -421,7 +486,7 @@ gpcg_params gpcg_params_default(void) {
     p.refine_cap = 30;
     p.max_halvings = 50;
     p.cg_cap = 0;
-    p.search_k = 8;
+    p.search_k = 4;
     p.cg_chunk = 32;
     return p;
 }
@@ -446,6 +511,11 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
     gpcg_problem* h = new gpcg_problem();
     h->n = (int)(nx * ny);
+    h->is_csr = false;
+    h->mg1 = march_geom((int)nx, (int)ny, 1);
+    h->mg2 = march_geom((int)nx, (int)ny, 2);
+    h->grid_m1 = march_grid(h->mg1);
+    h->grid_m2 = march_grid(h->mg2);
     int rc = create_common(h, cuda_stream, b, l, u);
     if (rc) { free_all(h); return rc; }
     h->c = c;
@@ -472,7 +542,7 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     h->is_csr = false;
     h->sop = StencilOp{(int)nx, (int)ny, h->n, h->wx, h->wy, h->shift, (long long)wx_ld, (long long)wy_ld};
     h->nnz = 5 * (long long)h->n - 2 * nx - 2 * ny;
-    h->grid = std::max(1, std::min(units(h), h->sms * 4));
+    h->grid = std::max(1, std::min(units(h), h->sms * 16));
     if ((rc = leave(h))) return fail(rc);
     *out = h;
     return GPCG_OK;
@@ -489,6 +559,7 @@ int gpcg_create_csr(gpcg_problem** out, void* cuda_stream, int64_t n, const int6
     if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
     gpcg_problem* h = new gpcg_problem();
     h->n = (int)n;
+    h->is_csr = true;
     auto fail = [&](int r) { free_all(h); return r; };
     int rc = create_common(h, cuda_stream, b, l, u);
     if (rc) return fail(rc);
@@ -518,7 +589,7 @@ int gpcg_create_csr(gpcg_problem** out, void* cuda_stream, int64_t n, const int6
     if (t != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite CSR values", t));
     h->is_csr = true;
     h->cop = CsrOp{h->n, h->rp, h->ci, h->val};
-    h->grid = std::max(1, std::min(units(h), h->sms * 4));
+    h->grid = std::max(1, std::min(units(h), h->sms * 16));
     if ((rc = leave(h))) return fail(rc);
     *out = h;
     return GPCG_OK;
