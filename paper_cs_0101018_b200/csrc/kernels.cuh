@@ -112,7 +112,10 @@ __global__ void __launch_bounds__(kThreads)
 k_search(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
          const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu,
          Scal* S, RedScratch R) {
-    if (use_alpha0 && !S->cauchy_ok) return;
+    if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
+        if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
+        return;
+    }
     const double base = use_alpha0 ? S->alpha0 : 1.0;
     double al[K];
 #pragma unroll

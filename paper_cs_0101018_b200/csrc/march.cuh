@@ -192,7 +192,6 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
         S->dAd = t[5];
         S->cauchy_ok = (t[5] > 0.0) ? 1 : 0;
         S->alpha0 = (t[5] > 0.0) ? t[0] / t[5] : 0.0;
-        S->s_h = -1;
     });
 }
 
@@ -207,7 +206,10 @@ __global__ void __launch_bounds__(kThreads)
 k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
           const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu, Scal* S,
           RedScratch R) {
-    if (use_alpha0 && !S->cauchy_ok) return;
+    if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
+        if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
+        return;
+    }
     const double base = use_alpha0 ? S->alpha0 : 1.0;
     double al[K];
 #pragma unroll
@@ -417,10 +419,9 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
         };
         // windows: pn(j), pn(j+1); rn(j-1), rn(j); raw(j+1) (mask, rho); rows j..j+1 masks
         unsigned char m0 = 0, m1 = 0;
-        double rho1 = 0.0, pr1 = 0.0, rho0x = 0.0;
+        double rho1 = 0.0, pr1 = 0.0;
         double pn0 = 0.0, pn1 = 0.0;
         double rnm = 0.0, rn0 = 0.0;
-        (void)rho0x;
         int j = j0 - 2;
         {
             unsigned char mx;
