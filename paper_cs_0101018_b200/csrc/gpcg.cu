@@ -77,6 +77,7 @@ struct gpcg_problem {
     cudaStream_t st = nullptr;     // private work stream (capturable)
     cudaEvent_t ev_sync = nullptr, ev_a = nullptr, ev_b = nullptr;
     bool is_csr = false;
+    bool generic = false;          // GPCG_GENERIC=1: stencil problems use the flat generic kernels (A/B tests)
     StencilOp sop{};
     CsrOp cop{};
     int n = 0;
@@ -292,7 +293,7 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
 // ---------------------------------------------------------------- launches
 int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double sgn,
                   const unsigned char* mask_prev, double* y_out, double* g_out, unsigned char* m_out) {
-    if (!h->is_csr) {   // stencil: accept + regrad + mask + counts + next Cauchy step in one sweep
+    if (!h->is_csr && !h->generic) {   // stencil: accept + regrad + mask + counts + next Cauchy step in one sweep
         if (h->sb)
             k2_accept<true><<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
                                                                 mask_prev, y_out, g_out, m_out, h->dS, h->red());
@@ -315,7 +316,7 @@ int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double
 }
 
 int launch_cauchy(gpcg_problem* h, const double* y, const double* g) {
-    if (!h->is_csr) return GPCG_OK;     // computed by the preceding k2_accept sweep
+    if (!h->is_csr && !h->generic) return GPCG_OK;     // computed by the preceding k2_accept sweep
     with_op(h, [&](auto& op, auto sbt) {
         using Op = std::decay_t<decltype(op)>;
         constexpr bool SB = decltype(sbt)::value;
@@ -335,7 +336,7 @@ int launch_search(gpcg_problem* h, const double* y, const double* g, const doubl
                   int use_alpha0, int h0) {
     const int K = search_k(h);
     const double mu = h->prm.mu;
-    if (!h->is_csr) {
+    if (!h->is_csr && !h->generic) {
         const bool dg = (dir == g);
         auto go = [&](auto sbt, auto kt, auto dgt) {
             constexpr bool SB = decltype(sbt)::value;
@@ -410,7 +411,7 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < chunk; ++i) {
         const int a = i & 1, bb = a ^ 1;
-        if (!h->is_csr) {   // stencil: rho, p ping-pong (p in Q[]), w in place
+        if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
             k2_cg_iter<<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a], h->Rho[bb],
                                                            h->Q[bb], h->W, h->dS, h->red());
             continue;
@@ -434,7 +435,7 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     int rc;
-    if (!h->is_csr) {
+    if (!h->is_csr && !h->generic) {
         k2_cg_init<<<h->grid_m1, kThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg, h->Rho[0],
                                                        h->Q[0], h->W, eta2, cap, h->dS, h->red());
     } else with_op_only(h, [&](auto& op) {
@@ -512,6 +513,7 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     gpcg_problem* h = new gpcg_problem();
     h->n = (int)(nx * ny);
     h->is_csr = false;
+    h->generic = getenv("GPCG_GENERIC") != nullptr && getenv("GPCG_GENERIC")[0] == '1';
     h->mg1 = march_geom((int)nx, (int)ny, 1);
     h->mg2 = march_geom((int)nx, (int)ny, 2);
     h->grid_m1 = march_grid(h->mg1);
