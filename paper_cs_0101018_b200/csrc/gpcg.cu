@@ -389,7 +389,9 @@ int search_and_accept(gpcg_problem* h, int cur, const double* dir, double sgn, i
         if ((rc = launch_accept(h, h->Y[cur], dir, sgn, h->M[cur], h->Y[nxt], h->G[nxt], h->M[nxt])))
             return rc;
         if ((rc = sync_scal(h))) return rc;
-        if (use_alpha0 && !h->hS->cauchy_ok)
+        // the search is skipped (s_h = -1) when the Cauchy step of y has <d, A d> <= 0;
+        // after an accepted step cauchy_ok already describes the NEW point (fused sweep)
+        if (h->hS->s_h < 0 && use_alpha0 && !h->hS->cauchy_ok)
             return set_err(GPCG_ENOTSPD, "<d, A d> = %g <= 0 in the Cauchy step: A is not SPD", h->hS->dAd);
         if (h->hS->s_h >= 0) {
             if (h->hS->s_h >= h->prm.max_halvings) break;
