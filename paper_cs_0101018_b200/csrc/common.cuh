@@ -12,7 +12,8 @@
 
 namespace gpcg {
 
-constexpr int kThreads = 256;      // every kernel: 256 threads = 8 warps
+constexpr int kThreads = 256;      // generic kernels: 256 threads = 8 warps
+constexpr int kMarchThreads = 128; // column-march kernels: 4 warps (finer occupancy steps)
 constexpr int kMaxSums = 34;       // reductions per kernel (search: 2*16 + 2)
 constexpr int kMaxK = 16;          // projected-search step sizes per sweep
 
@@ -179,7 +180,7 @@ __device__ __forceinline__ void block_reduce(double (&v)[NS], double* smem /* NS
     __syncthreads();
     if (wid == 0) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) v[s] = (lane < kThreads / 32) ? smem[s * 32 + lane] : 0.0;
+        for (int s = 0; s < NS; ++s) v[s] = (lane < (int)(blockDim.x >> 5)) ? smem[s * 32 + lane] : 0.0;
         warp_reduce<NS>(v);
     }
     __syncthreads();
@@ -208,7 +209,7 @@ __device__ __forceinline__ void reduce_and_finish(double (&v)[NS], const RedScra
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
         double acc = 0.0;
-        for (int b = threadIdx.x; b < G; b += kThreads) acc += __ldcg(R.partials + s * G + b);
+        for (int b = threadIdx.x; b < G; b += blockDim.x) acc += __ldcg(R.partials + s * G + b);
         t[s] = acc;
     }
     block_reduce<NS>(t, smem);

@@ -216,9 +216,9 @@ MarchGeom march_geom(int nx, int ny, int H) {
     g.nchunks = (ny + g.TY - 1) / g.TY;
     return g;
 }
-int march_grid(const MarchGeom& g) {
+int march_grid(const MarchGeom& g) {     // one work item per warp
     const long long items = (long long)g.nstrips * g.nchunks;
-    return (int)std::max<long long>(1, (items + kThreads / 32 - 1) / (kThreads / 32));
+    return (int)std::max<long long>(1, (items + kMarchThreads / 32 - 1) / (kMarchThreads / 32));
 }
 long long march_grid_bound(const gpcg_problem* h) {
     return std::max(march_grid(h->mg1), march_grid(h->mg2));
@@ -295,10 +295,10 @@ int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double
                   const unsigned char* mask_prev, double* y_out, double* g_out, unsigned char* m_out) {
     if (!h->is_csr && !h->generic) {   // stencil: accept + regrad + mask + counts + next Cauchy step in one sweep
         if (h->sb)
-            k2_accept<true><<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
+            k2_accept<true><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
                                                                 mask_prev, y_out, g_out, m_out, h->dS, h->red());
         else
-            k2_accept<false><<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
+            k2_accept<false><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
                                                                  mask_prev, y_out, g_out, m_out, h->dS, h->red());
         h->launches++;
         CKLAUNCH();
@@ -342,7 +342,7 @@ int launch_search(gpcg_problem* h, const double* y, const double* g, const doubl
             constexpr bool SB = decltype(sbt)::value;
             constexpr int KK = decltype(kt)::value;
             constexpr bool DG = decltype(dgt)::value;
-            k2_search<SB, KK, DG><<<h->grid_m1, kThreads, 0, h->st>>>(h->sop, h->mg1, h->bounds, y, g, dir, sgn,
+            k2_search<SB, KK, DG><<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->bounds, y, g, dir, sgn,
                                                                        use_alpha0, h0, mu, h->dS, h->red());
         };
         auto byk = [&](auto sbt, auto dgt) {
@@ -414,7 +414,7 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     for (int i = 0; i < chunk; ++i) {
         const int a = i & 1, bb = a ^ 1;
         if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
-            k2_cg_iter<<<h->grid_m2, kThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a], h->Rho[bb],
+            k2_cg_iter<<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a], h->Rho[bb],
                                                            h->Q[bb], h->W, h->dS, h->red());
             continue;
         }
@@ -438,7 +438,7 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     int rc;
     if (!h->is_csr && !h->generic) {
-        k2_cg_init<<<h->grid_m1, kThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg, h->Rho[0],
+        k2_cg_init<<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg, h->Rho[0],
                                                        h->Q[0], h->W, eta2, cap, h->dS, h->red());
     } else with_op_only(h, [&](auto& op) {
         using Op = std::decay_t<decltype(op)>;

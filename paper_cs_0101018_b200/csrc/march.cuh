@@ -4,13 +4,18 @@
 // Execution model ("column march"): a warp owns a strip of 32 consecutive grid
 // columns and marches down a chunk of TY rows.  Values needed at the four
 // neighbours of a point come from registers: west/east by warp shuffle, south/
-// north from a sliding window of rows.  Every input is therefore read from
-// HBM once per sweep (plus a few warm-up rows per chunk), all loads are
-// coalesced 256-byte rows, and derived values (trial points, projected
-// gradients, CG vectors) are computed once per point instead of once per
-// neighbour.  A kernel that applies the operator L times in sequence
-// (e.g. the CG iteration forms p, then rho = rho - alpha A p, then A rho) keeps
-// H = L halo lanes per side: outputs are written by lanes [H, 32-H).
+// north from a sliding window of rows.  Every input is read from HBM once per
+// sweep (plus a few warm-up rows per chunk); all loads are coalesced 256-byte
+// row segments; derived values (trial points, projected gradients, CG
+// vectors) are computed once per point instead of once per neighbour.  A
+// kernel that applies the operator L times in sequence (e.g. the CG iteration
+// forms p, then rho - alpha A p, then A rho) keeps H = L halo lanes per side:
+// outputs are written by lanes [H, 32-H).
+//
+// Latency hiding: raw rows are software-pipelined through a register ring of
+// depth kPipe (loads for row r + kPipe are issued while row r is consumed);
+// where a load is predicated on the free mask, masks run a further kPipe rows
+// ahead so no load waits on another.
 //
 // Reductions go through reduce_and_finish (common.cuh): fixed-order, so every
 // result is bitwise reproducible for a fixed grid.
@@ -19,6 +24,9 @@
 #include "common.cuh"
 
 namespace gpcg {
+
+constexpr int kPipe = 4;            // rows in flight per warp
+constexpr int kMarchMinBlocks = 4;  // >= 16 resident warps per SM (<= 128 registers)
 
 struct MarchGeom {
     int nstrips;   // ceil(nx / (32 - 2H))
@@ -56,18 +64,17 @@ __device__ __forceinline__ double apply5(const Faces& f, double shift, double vc
     return r;
 }
 
-// Work item -> strip column of this lane and row range.
+// One work item per warp: strip column of this lane and output row range.
 template <int H>
-__device__ __forceinline__ void march_item(const StencilOp& A, const MarchGeom& G, int item, int& i, int& j0,
-                                           int& j1) {
+__device__ __forceinline__ bool march_item(const StencilOp& A, const MarchGeom& G, int& i, int& j0, int& j1) {
+    const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (item >= G.nstrips * G.nchunks) return false;
     const int s = item % G.nstrips, c = item / G.nstrips;
     i = s * (32 - 2 * H) - H + (threadIdx.x & 31);
     j0 = c * G.TY;
     j1 = min(j0 + G.TY, A.ny);
+    return true;
 }
-
-__device__ __forceinline__ int warp_global() { return (blockIdx.x * blockDim.x + threadIdx.x) >> 5; }
-__device__ __forceinline__ int warps_total() { return (gridDim.x * blockDim.x) >> 5; }
 
 // Faces cache: broadcast weights are loaded once per strip; full arrays per row.
 struct FaceRow {
@@ -87,18 +94,49 @@ __device__ __forceinline__ double shift_at(const StencilOp& A, int v, bool ok) {
     return (A.shift && ok) ? __ldg(A.shift + v) : 0.0;
 }
 
+struct NoPre {};
+
+// Software pipeline over rows r0 .. r0+nsteps-1 (nsteps rounded up to kPipe):
+// ring[k] holds raw(r) loaded kPipe steps earlier; pre(r) (e.g. the mask) runs
+// 2*kPipe rows ahead so that load(r, pre(r)) never waits on pre.
+template <class Pre, class Raw, class PreF, class LoadF, class StepF>
+__device__ __forceinline__ void pipeline(int r0, int nsteps, PreF&& pre, LoadF&& load, StepF&& step) {
+    Raw ring[kPipe];
+    Pre pring[kPipe];
+#pragma unroll
+    for (int k = 0; k < kPipe; ++k) {
+        ring[k] = load(r0 + k, pre(r0 + k));
+        pring[k] = pre(r0 + kPipe + k);
+    }
+    for (int s0 = 0; s0 < nsteps; s0 += kPipe) {
+#pragma unroll
+        for (int k = 0; k < kPipe; ++k) {
+            const int r = r0 + s0 + k;
+            const Raw cur = ring[k];
+            ring[k] = load(r + kPipe, pring[k]);
+            pring[k] = pre(r + 2 * kPipe);
+            step(r, cur);
+        }
+    }
+}
+
 // ============================================================================
 // a1 + a2 fused: accept / project, regrad, free mask, set counts, and the
 // Cauchy quadratic form of the NEW point (so the next GP step's alpha_0 is
 // ready without another sweep).  H = 2.
-//   level 1  yn(r) = mid(l, u, y(r) + alpha sgn dir(r))   (or mid(l,u,y) if !dir)
-//   level 2  gn(r) = (A yn)(r) - b(r),  d(r) = grad_Omega q(yn)(r)   (Eq. proj-gradient)
-//   level 3  Ad(j) = (A d)(j)
+//   level 1  yn(r)   = mid(l, u, y(r) + alpha sgn dir(r))   (or mid(l,u,y) if !dir)
+//   level 2  gn(r-1) = (A yn)(r-1) - b,  d(r-1) = grad_Omega q(yn)(r-1)  (Eq. proj-gradient)
+//   level 3  Ad(r-2) = (A d)(r-2);  emit row r-2
 // sums: ||d||^2 (= ||grad_Omega q||^2), ||gn||^2, |A|, #changed, |A\B|, <d, A d>
 // finaliser: alpha_0 = ||d||^2 / <d, A d> (Eq. bqpls) for the next GP step.
 // ============================================================================
+struct RawAcc {
+    double y, d, b, l, u;
+    unsigned char mp;
+};
+
 template <bool SB>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, const double* __restrict__ dir,
           double sgn, const double* __restrict__ b, const unsigned char* __restrict__ mask_prev,
           double* __restrict__ y_out, double* __restrict__ g_out, unsigned char* __restrict__ mask_out,
@@ -112,75 +150,71 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
     const int lane = threadIdx.x & 31;
     const bool out_lane = lane >= H && lane < 32 - H;
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    const int nitems = G.nstrips * G.nchunks;
-    for (int item = warp_global(); item < nitems; item += warps_total()) {
-        int i, j0, j1;
-        march_item<H>(A, G, item, i, j0, j1);
+    int i, j0, j1;
+    if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
         FaceRow FR;
         FR.init(A, i, col_ok);
-        // raw row loader: y_in, dir -> yn ; b, l, u kept for levels 2/emit
-        auto yn_at = [&](int r, double& l_r, double& u_r, double& b_r) -> double {
-            l_r = 0.0; u_r = 0.0; b_r = 0.0;
-            if (!col_ok || r < 0 || r >= A.ny) return 0.0;
-            const int v = i + A.nx * r;
-            l_r = lo<SB>(Bd, v);
-            u_r = hi<SB>(Bd, v);
-            b_r = __ldg(b + v);
-            const double yv = __ldg(y_in + v);
-            return dir ? trial(yv, __ldg(dir + v), sgn, alpha, l_r, u_r) : mid(l_r, u_r, yv);
-        };
-        // windows
-        double yn0 = 0.0, yn1 = 0.0;              // yn(j), yn(j+1)
-        double l1 = 0.0, u1 = 0.0, b1 = 0.0;      // bounds/b of row j+1
-        double l0 = 0.0, u0 = 0.0;                // bounds of row j
-        double gn0 = 0.0;                          // gn(j)
-        double dm = 0.0, d0 = 0.0;                 // d(j-1), d(j)
-        // start 2 rows early to fill the windows (outputs begin at j0)
-        int j = j0 - 2;
-        {
-            double lx, ux, bx;
-            yn0 = yn_at(j, lx, ux, bx);
-            (void)lx; (void)ux; (void)bx;
-            yn1 = yn_at(j + 1, l1, u1, b1);
-        }
-        for (; j < j1; ++j) {
-            double l2, u2, b2;
-            const double yn2 = yn_at(j + 2, l2, u2, b2);
-            // level 2 at row j+1
-            const Faces f1 = FR.at(A, i, j + 1, col_ok);
-            const bool ok1 = col_ok && (j + 1) >= 0 && (j + 1) < A.ny;
-            const double sh1 = shift_at(A, i + A.nx * (j + 1), ok1);
-            const double ay1 = apply5(f1, sh1, yn1, yn0, yn2);
-            const double gn1 = ok1 ? ay1 - b1 : 0.0;
-            const double d1 = ok1 ? pgrad(yn1, gn1, l1, u1) : 0.0;
-            // level 3 at row j
-            const Faces f0 = FR.at(A, i, j, col_ok);
-            const bool ok0 = col_ok && j >= 0 && j < A.ny;
-            const double sh0 = shift_at(A, i + A.nx * j, ok0);
-            const double ad0 = apply5(f0, sh0, d0, dm, d1);
-            if (out_lane && ok0 && j >= j0) {
-                const int v = i + A.nx * j;
-                y_out[v] = yn0;
-                g_out[v] = gn0;
-                const bool act = (yn0 == l0) || (yn0 == u0);
-                const unsigned char m = act ? 0 : 1;
-                mask_out[v] = m;
-                acc[0] = fma(d0, d0, acc[0]);
-                acc[1] = fma(gn0, gn0, acc[1]);
-                acc[2] += act ? 1.0 : 0.0;
-                if (mask_prev) acc[3] += (mask_prev[v] != m) ? 1.0 : 0.0;
-                const bool binding = (yn0 == l0 && gn0 >= 0.0) || (yn0 == u0 && gn0 <= 0.0);
-                acc[4] += (act && !binding) ? 1.0 : 0.0;
-                acc[5] = fma(d0, ad0, acc[5]);
-            }
-            // shift windows
-            yn0 = yn1; yn1 = yn2;
-            l0 = l1; u0 = u1;
-            l1 = l2; u1 = u2; b1 = b2;
-            gn0 = gn1;
-            dm = d0; d0 = d1;
-        }
+        // windows (row index relative to the step row r)
+        double yn_m2 = 0.0, yn_m1 = 0.0;               // yn(r-2), yn(r-1)
+        double b_m1 = 0.0, l_m1 = 0.0, u_m1 = 0.0;      // row r-1
+        double l_m2 = 0.0, u_m2 = 0.0;                  // row r-2
+        unsigned char mp_m1 = 0, mp_m2 = 0;
+        double gn_m2 = 0.0;                             // gn(r-2)
+        double d_m3 = 0.0, d_m2 = 0.0;                  // d(r-3), d(r-2)
+        const int rend = min(A.ny, j1 + H);             // last raw row needed + 1
+        pipeline<NoPre, RawAcc>(
+            j0 - 2, j1 - j0 + 4, [&](int) { return NoPre{}; },
+            [&](int r, NoPre) {
+                RawAcc x{0.0, 0.0, 0.0, 0.0, 0.0, 0};
+                if (col_ok && r >= 0 && r < rend) {          // loads only; used kPipe rows later
+                    const int v = i + A.nx * r;
+                    x.l = lo<SB>(Bd, v);
+                    x.u = hi<SB>(Bd, v);
+                    x.b = __ldg(b + v);
+                    x.y = __ldg(y_in + v);
+                    if (dir) x.d = __ldg(dir + v);
+                    if (mask_prev) x.mp = __ldg(mask_prev + v);
+                }
+                return x;
+            },
+            [&](int r, const RawAcc& x) {
+                const bool okr = col_ok && r >= 0 && r < rend;
+                const double yn0 = okr ? (dir ? trial(x.y, x.d, sgn, alpha, x.l, x.u) : mid(x.l, x.u, x.y)) : 0.0;
+                // level 2 at row r-1
+                const int r1 = r - 1;
+                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
+                const Faces f1 = FR.at(A, i, r1, col_ok);
+                const double ay = apply5(f1, shift_at(A, i + A.nx * r1, ok1), yn_m1, yn_m2, yn0);
+                const double gn1 = ok1 ? ay - b_m1 : 0.0;
+                const double d1 = ok1 ? pgrad(yn_m1, gn1, l_m1, u_m1) : 0.0;
+                // level 3 at row r-2
+                const int r2 = r - 2;
+                const bool ok2 = col_ok && r2 >= 0 && r2 < A.ny;
+                const Faces f2 = FR.at(A, i, r2, col_ok);
+                const double ad = apply5(f2, shift_at(A, i + A.nx * r2, ok2), d_m2, d_m3, d1);
+                if (out_lane && ok2 && r2 >= j0 && r2 < j1) {
+                    const int v = i + A.nx * r2;
+                    y_out[v] = yn_m2;
+                    g_out[v] = gn_m2;
+                    const bool act = (yn_m2 == l_m2) || (yn_m2 == u_m2);
+                    const unsigned char m = act ? 0 : 1;
+                    mask_out[v] = m;
+                    acc[0] = fma(d_m2, d_m2, acc[0]);
+                    acc[1] = fma(gn_m2, gn_m2, acc[1]);
+                    acc[2] += act ? 1.0 : 0.0;
+                    if (mask_prev) acc[3] += (mp_m2 != m) ? 1.0 : 0.0;
+                    const bool binding = (yn_m2 == l_m2 && gn_m2 >= 0.0) || (yn_m2 == u_m2 && gn_m2 <= 0.0);
+                    acc[4] += (act && !binding) ? 1.0 : 0.0;
+                    acc[5] = fma(d_m2, ad, acc[5]);
+                }
+                // shift windows by one row
+                yn_m2 = yn_m1; yn_m1 = yn0;
+                l_m2 = l_m1; u_m2 = u_m1; mp_m2 = mp_m1;
+                l_m1 = x.l; u_m1 = x.u; b_m1 = x.b; mp_m1 = x.mp;
+                gn_m2 = gn1;
+                d_m3 = d_m2; d_m2 = d1;
+            });
     }
     reduce_and_finish<6>(acc, R, [&](double* t) {
         S->pg2 = t[0];
@@ -198,11 +232,15 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
 // ============================================================================
 // a3: projected search, K step sizes per sweep.  H = 1.
 //   level 1  s_h(r) = mid(l, u, y + alpha_h sgn dir) - y
-//   level 2  sums <g, s_h>(j), <s_h, A s_h>(j)
+//   level 2  sums <g, s_h>(r-1), <s_h, A s_h>(r-1)
 // kDirIsG: the GP direction is -g, so dir and g are the same array (one load).
 // ============================================================================
+struct RawY {
+    double y, d, g, l, u;
+};
+
 template <bool SB, int K, bool kDirIsG>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kMarchThreads, (K <= 4 ? kMarchMinBlocks : 2))
 k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
           const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu, Scal* S,
           RedScratch R) {
@@ -220,49 +258,53 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
     double acc[2 * K];
 #pragma unroll
     for (int s = 0; s < 2 * K; ++s) acc[s] = 0.0;
-    const int nitems = G.nstrips * G.nchunks;
-    for (int item = warp_global(); item < nitems; item += warps_total()) {
-        int i, j0, j1;
-        march_item<H>(A, G, item, i, j0, j1);
+    int i, j0, j1;
+    if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
         FaceRow FR;
         FR.init(A, i, col_ok);
-        auto load_s = [&](int r, double (&s)[K], double& gr) {
-            gr = 0.0;
+        // raw values (y, dir, g, l, u) are pipelined; s_h is formed at consumption
+        double s_m2[K], s_m1[K];
+        double g_m1 = 0.0;
 #pragma unroll
-            for (int h = 0; h < K; ++h) s[h] = 0.0;
-            if (!col_ok || r < 0 || r >= A.ny) return;
-            const int v = i + A.nx * r;
-            const double yv = __ldg(y + v);
-            const double dv = __ldg(dir + v);
-            gr = kDirIsG ? dv : __ldg(g + v);
-            const double l = lo<SB>(Bd, v), u = hi<SB>(Bd, v);
-#pragma unroll
-            for (int h = 0; h < K; ++h) s[h] = trial(yv, dv, sgn, al[h], l, u) - yv;
-        };
-        double sm[K], s0[K], s1[K];
-        double g0, g1, gx;
-        load_s(j0 - 1, sm, gx);
-        load_s(j0, s0, g0);
-        int j = j0;
-        // loop invariant: sm = s(j-1), s0 = s(j), g0 = g(j)
-        for (; j < j1; ++j) {
-            load_s(j + 1, s1, g1);
-            const Faces f = FR.at(A, i, j, col_ok);
-            const bool ok = col_ok && j < A.ny;
-            const double sh = shift_at(A, i + A.nx * j, ok);
-#pragma unroll
-            for (int h = 0; h < K; ++h) {
-                const double as = apply5(f, sh, s0[h], sm[h], s1[h]);
-                if (out_lane && ok) {
-                    acc[2 * h] = fma(g0, s0[h], acc[2 * h]);
-                    acc[2 * h + 1] = fma(s0[h], as, acc[2 * h + 1]);
+        for (int h = 0; h < K; ++h) { s_m2[h] = 0.0; s_m1[h] = 0.0; }
+        const int rend = min(A.ny, j1 + H);
+        pipeline<NoPre, RawY>(
+            j0 - 1, j1 - j0 + 2, [&](int) { return NoPre{}; },
+            [&](int r, NoPre) {
+                RawY x{0.0, 0.0, 0.0, 0.0, 0.0};
+                if (col_ok && r >= 0 && r < rend) {
+                    const int v = i + A.nx * r;
+                    x.y = __ldg(y + v);
+                    x.d = __ldg(dir + v);
+                    x.g = kDirIsG ? x.d : __ldg(g + v);
+                    x.l = lo<SB>(Bd, v);
+                    x.u = hi<SB>(Bd, v);
                 }
-            }
+                return x;
+            },
+            [&](int r, const RawY& x) {
+                const bool okr = col_ok && r >= 0 && r < rend;
+                double s0[K];
 #pragma unroll
-            for (int h = 0; h < K; ++h) { sm[h] = s0[h]; s0[h] = s1[h]; }
-            g0 = g1;
-        }
+                for (int h = 0; h < K; ++h) s0[h] = okr ? trial(x.y, x.d, sgn, al[h], x.l, x.u) - x.y : 0.0;
+                const int r1 = r - 1;
+                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
+                const Faces f = FR.at(A, i, r1, col_ok);
+                const double sh = shift_at(A, i + A.nx * r1, ok1);
+                const bool emit = out_lane && ok1 && r1 >= j0 && r1 < j1;
+#pragma unroll
+                for (int h = 0; h < K; ++h) {
+                    const double as = apply5(f, sh, s_m1[h], s_m2[h], s0[h]);
+                    if (emit) {
+                        acc[2 * h] = fma(g_m1, s_m1[h], acc[2 * h]);
+                        acc[2 * h + 1] = fma(s_m1[h], as, acc[2 * h + 1]);
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < K; ++h) { s_m2[h] = s_m1[h]; s_m1[h] = s0[h]; }
+                g_m1 = x.g;
+            });
     }
     reduce_and_finish<2 * K>(acc, R, [&](double* t) {
         S->s_h = -1;
@@ -271,7 +313,7 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
             const double dq = gs + 0.5 * sAs;
             if (dq <= mu * gs) {
                 S->s_h = h0 + h;
-                S->s_alpha = al[h];
+                S->s_alpha = scalbn(base, -(h0 + h));
                 S->s_delta = dq;
                 S->s_gs = gs;
                 break;
@@ -281,10 +323,36 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
 }
 
 // ============================================================================
-// a5 init: rho_0 = -[v in F] g_v, p_{-1} = 0, w_0 = 0; gamma_0, delta_0 = rho_0'A_F rho_0.
-// Also copies the free mask into the fixed CG mask buffer.  H = 1.
+// a5 init: rho_0 = -[v in F] g_v, p_{-1} = 0, w_0 = 0; gamma_0 = rho_0'rho_0,
+// delta_0 = rho_0'A_F rho_0.  Also copies the free mask into the fixed CG mask
+// buffer used by the captured CG graph.  H = 1.
 // ============================================================================
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ void cg_init_finalize(double gamma, double delta, double eta2, long long cap, Scal* S) {
+    S->cg_it = 0;
+    S->cg_cap = cap;
+    S->cg_eta2 = eta2;
+    S->cg_maxdec = 0.0;
+    S->cg_dec = 0.0;
+    S->cg_gamma = gamma;
+    S->cg_rnorm0 = sqrt(gamma);
+    S->cg_beta = 0.0;
+    S->cg_done = 0;
+    S->cg_reason = CG_RUNNING;
+    if (gamma == 0.0 || cap <= 0) {            // r_k = 0: w = 0 is exact (R27)
+        S->cg_done = 1; S->cg_reason = CG_EXACT; S->cg_alpha = 0.0;
+    } else if (!(delta > 0.0)) {
+        S->cg_done = 1; S->cg_reason = CG_NOTSPD; S->cg_alpha = 0.0;
+    } else {
+        S->cg_alpha = gamma / delta;
+    }
+}
+
+struct RawInit {
+    double rho;
+    unsigned char m;
+};
+
+__global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigned char* __restrict__ mask,
            unsigned char* __restrict__ mask_cg, double* __restrict__ rho, double* __restrict__ p,
            double* __restrict__ w, double eta2, long long cap, Scal* S, RedScratch R) {
@@ -292,73 +360,58 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
     const int lane = threadIdx.x & 31;
     const bool out_lane = lane >= H && lane < 32 - H;
     double acc[2] = {0.0, 0.0};
-    const int nitems = G.nstrips * G.nchunks;
-    for (int item = warp_global(); item < nitems; item += warps_total()) {
-        int i, j0, j1;
-        march_item<H>(A, G, item, i, j0, j1);
+    int i, j0, j1;
+    if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
         FaceRow FR;
         FR.init(A, i, col_ok);
-        auto rho_at = [&](int r, unsigned char& m) -> double {
-            m = 0;
-            if (!col_ok || r < 0 || r >= A.ny) return 0.0;
-            const int v = i + A.nx * r;
-            m = mask[v];
-            return m ? -__ldg(g + v) : 0.0;
-        };
-        unsigned char m0, m1, mx;
-        double rm = rho_at(j0 - 1, mx);
-        double r0 = rho_at(j0, m0);
-        for (int j = j0; j < j1; ++j) {
-            const double r1 = rho_at(j + 1, m1);
-            const Faces f = FR.at(A, i, j, col_ok);
-            const bool ok = col_ok && j < A.ny;
-            const double q = apply5(f, shift_at(A, i + A.nx * j, ok), r0, rm, r1);
-            if (out_lane && ok) {
-                const int v = i + A.nx * j;
-                mask_cg[v] = m0;
-                rho[v] = r0;
-                p[v] = 0.0;
-                w[v] = 0.0;
-                if (m0) {
-                    acc[0] = fma(r0, r0, acc[0]);
-                    acc[1] = fma(r0, q, acc[1]);
+        double r_m2 = 0.0, r_m1 = 0.0;
+        unsigned char m_m1 = 0;
+        const int rend = min(A.ny, j1 + H);
+        pipeline<NoPre, RawInit>(
+            j0 - 1, j1 - j0 + 2, [&](int) { return NoPre{}; },
+            [&](int r, NoPre) {
+                RawInit x{0.0, 0};
+                if (col_ok && r >= 0 && r < rend) {
+                    const int v = i + A.nx * r;
+                    x.m = __ldg(mask + v);
+                    x.rho = -__ldg(g + v);
                 }
-            }
-            rm = r0; r0 = r1; m0 = m1;
-        }
+                return x;
+            },
+            [&](int r, const RawInit& x) {
+                const double r0 = x.m ? x.rho : 0.0;
+                const int r1 = r - 1;
+                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
+                const Faces f = FR.at(A, i, r1, col_ok);
+                const double q = apply5(f, shift_at(A, i + A.nx * r1, ok1), r_m1, r_m2, r0);
+                if (out_lane && ok1 && r1 >= j0 && r1 < j1) {
+                    const int v = i + A.nx * r1;
+                    mask_cg[v] = m_m1;
+                    rho[v] = r_m1;
+                    p[v] = 0.0;
+                    w[v] = 0.0;
+                    if (m_m1) {
+                        acc[0] = fma(r_m1, r_m1, acc[0]);
+                        acc[1] = fma(r_m1, q, acc[1]);
+                    }
+                }
+                r_m2 = r_m1; r_m1 = r0; m_m1 = x.m;
+            });
     }
-    reduce_and_finish<2>(acc, R, [&](double* t) {
-        S->cg_it = 0;
-        S->cg_cap = cap;
-        S->cg_eta2 = eta2;
-        S->cg_maxdec = 0.0;
-        S->cg_dec = 0.0;
-        S->cg_gamma = t[0];
-        S->cg_rnorm0 = sqrt(t[0]);
-        S->cg_beta = 0.0;
-        S->cg_done = 0;
-        S->cg_reason = CG_RUNNING;
-        if (t[0] == 0.0 || cap <= 0) {
-            S->cg_done = 1; S->cg_reason = CG_EXACT; S->cg_alpha = 0.0;
-        } else if (!(t[1] > 0.0)) {
-            S->cg_done = 1; S->cg_reason = CG_NOTSPD; S->cg_alpha = 0.0;
-        } else {
-            S->cg_alpha = t[0] / t[1];
-        }
-    });
+    reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
 }
 
 // ============================================================================
 // a5 iteration, stencil form that stores only rho, p, w (49 B per free point
 // instead of 81): the products s = A_F p and q = A_F rho are recomputed from
 // neighbours instead of being carried as vectors.  H = 2.
-//   level 1  pn(r)  = [r in F] (rho(r) + beta p(r))                 p_i
-//   level 2  rn(r)  = [r in F] (rho(r) - alpha (A pn)(r))           rho_{i+1}
-//   level 3  q(j)   = [j in F] (A rn)(j)                            A_F rho_{i+1}
-//   emit     w(j) += alpha pn(j); rho'(j) = rn(j); p'(j) = pn(j); gamma += rn^2; delta += rn q
-// Loads of rho, p, w are predicated on the mask (active regions cost 1 B/pt).
-// Finaliser identical to the generic k_cg_iter (same recurrences).
+//   level 1  pn(r)   = [r in F] (rho(r) + beta p(r))                       p_i
+//   level 2  rn(r-1) = [r-1 in F] (rho(r-1) - alpha (A pn)(r-1))          rho_{i+1}
+//   level 3  q(r-2)  = [r-2 in F] (A rn)(r-2)                              A_F rho_{i+1}
+//   emit r-2: w += alpha pn; rho' = rn; p' = pn; gamma += rn^2; delta += rn q
+// Loads of rho, p, w are predicated on the mask (active regions cost 1 B/pt),
+// with masks pipelined kPipe rows ahead of the data.
 // ============================================================================
 __device__ __forceinline__ void cg_finalize(double gamma, double delta, Scal* S) {
     const double gamma_old = S->cg_gamma, alpha_old = S->cg_alpha;
@@ -388,7 +441,12 @@ __device__ __forceinline__ void cg_finalize(double gamma, double delta, Scal* S)
     S->cg_alpha = gamma / pap;
 }
 
-__global__ void __launch_bounds__(kThreads)
+struct RawCg {
+    double rho, p, w;
+    unsigned char m;
+};
+
+__global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
            const double* __restrict__ rho, const double* __restrict__ p,
            double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w,
@@ -399,68 +457,59 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
     const int lane = threadIdx.x & 31;
     const bool out_lane = lane >= H && lane < 32 - H;
     double acc[2] = {0.0, 0.0};
-    const int nitems = G.nstrips * G.nchunks;
-    for (int item = warp_global(); item < nitems; item += warps_total()) {
-        int i, j0, j1;
-        march_item<H>(A, G, item, i, j0, j1);
+    int i, j0, j1;
+    if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
         FaceRow FR;
         FR.init(A, i, col_ok);
-        // raw row: mask, rho, p (w is read at emit only)
-        auto raw_at = [&](int r, unsigned char& m, double& rr, double& pp) {
-            m = 0; rr = 0.0; pp = 0.0;
-            if (!col_ok || r < 0 || r >= A.ny) return;
-            const int v = i + A.nx * r;
-            m = mask[v];
-            if (m) {
-                rr = rho[v];
-                pp = p[v];
-            }
-        };
-        // windows: pn(j), pn(j+1); rn(j-1), rn(j); raw(j+1) (mask, rho); rows j..j+1 masks
-        unsigned char m0 = 0, m1 = 0;
-        double rho1 = 0.0, pr1 = 0.0;
-        double pn0 = 0.0, pn1 = 0.0;
-        double rnm = 0.0, rn0 = 0.0;
-        int j = j0 - 2;
-        {
-            unsigned char mx;
-            double rx, px;
-            raw_at(j, mx, rx, px);
-            pn0 = mx ? fma(beta, px, rx) : 0.0;         // pn(j0-2)
-            raw_at(j + 1, m1, rho1, pr1);
-            pn1 = m1 ? fma(beta, pr1, rho1) : 0.0;      // pn(j0-1)
-            m0 = mx;
-        }
-        // loop invariant at top: pn0 = pn(j), pn1 = pn(j+1), (m1, rho1) raw of row j+1,
-        //                        rnm = rn(j-1), rn0 = rn(j), m0 = mask(j)
-        for (; j < j1; ++j) {
-            unsigned char m2;
-            double rho2, pr2;
-            raw_at(j + 2, m2, rho2, pr2);
-            const double pn2 = m2 ? fma(beta, pr2, rho2) : 0.0;
-            // level 2 at row j+1
-            const Faces f1 = FR.at(A, i, j + 1, col_ok);
-            const bool ok1 = col_ok && (j + 1) >= 0 && (j + 1) < A.ny;
-            const double ap1 = apply5(f1, shift_at(A, i + A.nx * (j + 1), ok1 && m1), pn1, pn0, pn2);
-            const double rn1 = m1 ? fma(-alpha, ap1, rho1) : 0.0;
-            // level 3 at row j
-            const Faces f0 = FR.at(A, i, j, col_ok);
-            const bool ok0 = col_ok && j >= 0 && j < A.ny;
-            const double q0 = apply5(f0, shift_at(A, i + A.nx * j, ok0 && m0), rn0, rnm, rn1);
-            if (out_lane && ok0 && j >= j0 && m0) {
-                const int v = i + A.nx * j;
-                w[v] = fma(alpha, pn0, w[v]);
-                rho_n[v] = rn0;
-                p_n[v] = pn0;
-                acc[0] = fma(rn0, rn0, acc[0]);
-                acc[1] = fma(rn0, q0, acc[1]);
-            }
-            pn0 = pn1; pn1 = pn2;
-            rnm = rn0; rn0 = rn1;
-            m0 = m1; m1 = m2;
-            rho1 = rho2;
-        }
+        double pn_m2 = 0.0, pn_m1 = 0.0;          // pn(r-2), pn(r-1)
+        double rho_m1 = 0.0;                       // rho(r-1)
+        double w_m1 = 0.0, w_m2 = 0.0;             // w(r-1), w(r-2)
+        unsigned char m_m1 = 0, m_m2 = 0;
+        double rn_m3 = 0.0, rn_m2 = 0.0;           // rn(r-3), rn(r-2)
+        const int rend = min(A.ny, j1 + H);
+        pipeline<unsigned char, RawCg>(
+            j0 - 2, j1 - j0 + 4,
+            [&](int r) -> unsigned char {
+                return (col_ok && r >= 0 && r < rend) ? __ldg(mask + i + A.nx * r) : (unsigned char)0;
+            },
+            [&](int r, unsigned char m) {
+                RawCg x{0.0, 0.0, 0.0, m};
+                if (m) {
+                    const int v = i + A.nx * r;
+                    x.rho = rho[v];
+                    x.p = p[v];
+                    if (out_lane) x.w = w[v];       // w is only needed where this warp writes
+                }
+                return x;
+            },
+            [&](int r, const RawCg& x) {
+                const double pn0 = x.m ? fma(beta, x.p, x.rho) : 0.0;
+                // level 2 at row r-1
+                const int r1 = r - 1;
+                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
+                const Faces f1 = FR.at(A, i, r1, col_ok);
+                const double ap = apply5(f1, shift_at(A, i + A.nx * r1, ok1 && m_m1), pn_m1, pn_m2, pn0);
+                const double rn1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
+                // level 3 at row r-2
+                const int r2 = r - 2;
+                const bool ok2 = col_ok && r2 >= 0 && r2 < A.ny;
+                const Faces f2 = FR.at(A, i, r2, col_ok);
+                const double q = apply5(f2, shift_at(A, i + A.nx * r2, ok2 && m_m2), rn_m2, rn_m3, rn1);
+                if (out_lane && ok2 && r2 >= j0 && r2 < j1 && m_m2) {
+                    const int v = i + A.nx * r2;
+                    w[v] = fma(alpha, pn_m2, w_m2);
+                    rho_n[v] = rn_m2;
+                    p_n[v] = pn_m2;
+                    acc[0] = fma(rn_m2, rn_m2, acc[0]);
+                    acc[1] = fma(rn_m2, q, acc[1]);
+                }
+                pn_m2 = pn_m1; pn_m1 = pn0;
+                rho_m1 = x.rho;
+                w_m2 = w_m1; w_m1 = x.w;
+                m_m2 = m_m1; m_m1 = x.m;
+                rn_m3 = rn_m2; rn_m2 = rn1;
+            });
     }
     reduce_and_finish<2>(acc, R, [&](double* t) { cg_finalize(t[0], t[1], S); });
 }
