@@ -78,7 +78,7 @@ typedef struct {
     int64_t refine_cap;  /* cgstop3 repetitions per outer iterate: 30                      */
     int64_t max_halvings;/* projected-search trials: 50                                    */
     int64_t cg_cap;      /* CG iterations per call, 0 => m_k (finite termination P:444-447)*/
-    int32_t search_k;    /* step sizes per projected-search sweep: 4 (1..16; rounded up to 4/8/16) */
+    int32_t search_k;    /* step sizes in the first search sweep: 2 (<=2 -> 2, else 8); retries use 8 */
     int32_t cg_chunk;    /* CG iterations per graph launch between host polls: 32          */
 } gpcg_params;
 

@@ -90,6 +90,7 @@ struct gpcg_problem {
     double *b = nullptr, *l = nullptr, *u = nullptr;
     double c = 0.0;
     bool sb = false;               // scalar bounds detected
+    bool bc = false;               // stencil with broadcast faces and no shift
     Bounds bounds{};
     // work vectors
     double *Y[2] = {nullptr, nullptr}, *G[2] = {nullptr, nullptr};
@@ -294,12 +295,14 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
 int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double sgn,
                   const unsigned char* mask_prev, double* y_out, double* g_out, unsigned char* m_out) {
     if (!h->is_csr && !h->generic) {   // stencil: accept + regrad + mask + counts + next Cauchy step in one sweep
-        if (h->sb)
-            k2_accept<true><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
-                                                                mask_prev, y_out, g_out, m_out, h->dS, h->red());
-        else
-            k2_accept<false><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn, h->b,
-                                                                 mask_prev, y_out, g_out, m_out, h->dS, h->red());
+        auto go = [&](auto sbt, auto bct) {
+            constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value;
+            k2_accept<SB, BC><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn,
+                                                                       h->b, mask_prev, y_out, g_out, m_out, h->dS,
+                                                                       h->red());
+        };
+        if (h->sb) { if (h->bc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+        else { if (h->bc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
         h->launches++;
         CKLAUNCH();
         return GPCG_OK;
@@ -327,33 +330,32 @@ int launch_cauchy(gpcg_problem* h, const double* y, const double* g) {
     return GPCG_OK;
 }
 
-int search_k(const gpcg_problem* h) {
-    const int k = h->prm.search_k;
-    return k <= 4 ? 4 : (k <= 8 ? 8 : 16);
-}
+// step sizes per projected-search sweep: the first sweep evaluates search_k
+// (2 or 8 instantiated), later sweeps 8
+int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
 
 int launch_search(gpcg_problem* h, const double* y, const double* g, const double* dir, double sgn,
-                  int use_alpha0, int h0) {
-    const int K = search_k(h);
+                  int use_alpha0, int h0, int K) {
     const double mu = h->prm.mu;
     if (!h->is_csr && !h->generic) {
         const bool dg = (dir == g);
-        auto go = [&](auto sbt, auto kt, auto dgt) {
-            constexpr bool SB = decltype(sbt)::value;
+        auto go = [&](auto sbt, auto bct, auto kt, auto dgt) {
+            constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value, DG = decltype(dgt)::value;
             constexpr int KK = decltype(kt)::value;
-            constexpr bool DG = decltype(dgt)::value;
-            k2_search<SB, KK, DG><<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->bounds, y, g, dir, sgn,
-                                                                       use_alpha0, h0, mu, h->dS, h->red());
+            k2_search<SB, BC, KK, DG><<<h->grid_m1, kMarchThreads, 0, h->st>>>(
+                h->sop, h->mg1, h->bounds, y, g, dir, sgn, use_alpha0, h0, mu, h->dS, h->red());
         };
-        auto byk = [&](auto sbt, auto dgt) {
-            if (K == 4) go(sbt, std::integral_constant<int, 4>(), dgt);
-            else if (K == 8) go(sbt, std::integral_constant<int, 8>(), dgt);
-            else go(sbt, std::integral_constant<int, 16>(), dgt);
+        auto byk = [&](auto sbt, auto bct, auto dgt) {
+            if (K == 2) go(sbt, bct, std::integral_constant<int, 2>(), dgt);
+            else go(sbt, bct, std::integral_constant<int, 8>(), dgt);
         };
-        auto bydg = [&](auto sbt) {
-            if (dg) byk(sbt, std::true_type()); else byk(sbt, std::false_type());
+        auto bydg = [&](auto sbt, auto bct) {
+            if (dg) byk(sbt, bct, std::true_type()); else byk(sbt, bct, std::false_type());
         };
-        if (h->sb) bydg(std::true_type()); else bydg(std::false_type());
+        auto bybc = [&](auto sbt) {
+            if (h->bc) bydg(sbt, std::true_type()); else bydg(sbt, std::false_type());
+        };
+        if (h->sb) bybc(std::true_type()); else bybc(std::false_type());
         h->launches++;
         CKLAUNCH();
         return GPCG_OK;
@@ -361,15 +363,12 @@ int launch_search(gpcg_problem* h, const double* y, const double* g, const doubl
     with_op(h, [&](auto& op, auto sbt) {
         using Op = std::decay_t<decltype(op)>;
         constexpr bool SB = decltype(sbt)::value;
-        if (K == 4)
-            k_search<Op, SB, 4><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, dir, sgn, use_alpha0,
-                                                                 h0, mu, h->dS, h->red());
-        else if (K == 8)
-            k_search<Op, SB, 8><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, dir, sgn, use_alpha0,
+        if (K == 2)
+            k_search<Op, SB, 2><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, dir, sgn, use_alpha0,
                                                                  h0, mu, h->dS, h->red());
         else
-            k_search<Op, SB, 16><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, dir, sgn, use_alpha0,
-                                                                  h0, mu, h->dS, h->red());
+            k_search<Op, SB, 8><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, dir, sgn, use_alpha0,
+                                                                 h0, mu, h->dS, h->red());
     });
     h->launches++;
     CKLAUNCH();
@@ -382,10 +381,9 @@ int launch_search(gpcg_problem* h, const double* y, const double* g, const doubl
 int search_and_accept(gpcg_problem* h, int cur, const double* dir, double sgn, int use_alpha0,
                       int* accepted_h) {
     const int nxt = cur ^ 1;
-    const int K = search_k(h);
     int rc;
-    for (int h0 = 0; h0 < h->prm.max_halvings; h0 += K) {
-        if ((rc = launch_search(h, h->Y[cur], h->G[cur], dir, sgn, use_alpha0, h0))) return rc;
+    for (int h0 = 0, K = first_k(h); h0 < h->prm.max_halvings; h0 += K, K = 8) {
+        if ((rc = launch_search(h, h->Y[cur], h->G[cur], dir, sgn, use_alpha0, h0, K))) return rc;
         if ((rc = launch_accept(h, h->Y[cur], dir, sgn, h->M[cur], h->Y[nxt], h->G[nxt], h->M[nxt])))
             return rc;
         if ((rc = sync_scal(h))) return rc;
@@ -414,8 +412,12 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     for (int i = 0; i < chunk; ++i) {
         const int a = i & 1, bb = a ^ 1;
         if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
-            k2_cg_iter<<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a], h->Rho[bb],
-                                                           h->Q[bb], h->W, h->dS, h->red());
+            if (h->bc)
+                k2_cg_iter<true><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a],
+                                                                          h->Rho[bb], h->Q[bb], h->W, h->dS, h->red());
+            else
+                k2_cg_iter<false><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a],
+                                                                           h->Rho[bb], h->Q[bb], h->W, h->dS, h->red());
             continue;
         }
         with_op_only(h, [&](auto& op) {
@@ -438,8 +440,14 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     int rc;
     if (!h->is_csr && !h->generic) {
-        k2_cg_init<<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg, h->Rho[0],
-                                                       h->Q[0], h->W, eta2, cap, h->dS, h->red());
+        if (h->bc)
+            k2_cg_init<true><<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg,
+                                                                      h->Rho[0], h->Q[0], h->W, eta2, cap, h->dS,
+                                                                      h->red());
+        else
+            k2_cg_init<false><<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg,
+                                                                       h->Rho[0], h->Q[0], h->W, eta2, cap, h->dS,
+                                                                       h->red());
     } else with_op_only(h, [&](auto& op) {
         using Op = std::decay_t<decltype(op)>;
         k_cg_init<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->G[cur], h->M[cur], h->Mcg, h->Rho[0], h->Q[0], h->S2[0],
@@ -489,7 +497,7 @@ gpcg_params gpcg_params_default(void) {
     p.refine_cap = 30;
     p.max_halvings = 50;
     p.cg_cap = 0;
-    p.search_k = 4;
+    p.search_k = 2;
     p.cg_chunk = 32;
     return p;
 }
@@ -545,6 +553,7 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     if (bad != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite stencil weights", bad));
     h->is_csr = false;
     h->sop = StencilOp{(int)nx, (int)ny, h->n, h->wx, h->wy, h->shift, (long long)wx_ld, (long long)wy_ld};
+    h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
     h->nnz = 5 * (long long)h->n - 2 * nx - 2 * ny;
     h->grid = std::max(1, std::min(units(h), h->sms * 16));
     if ((rc = leave(h))) return fail(rc);

@@ -34,35 +34,56 @@ struct MarchGeom {
     int TY;        // output rows per work item
 };
 
-// Per-lane face weights of column i at grid row j (zero outside the grid).
-struct Faces {
-    double w, e, s, n;
-};
-
-__device__ __forceinline__ Faces load_faces(const StencilOp& A, int i, int j, bool col_ok) {
-    Faces f{0.0, 0.0, 0.0, 0.0};
-    if (col_ok && j >= 0 && j < A.ny) {
-        const double* wxr = A.wx + (long long)j * A.wx_ld;
-        f.w = __ldg(wxr + i);
-        f.e = __ldg(wxr + i + 1);
-        f.s = __ldg(A.wy + (long long)j * A.wy_ld + i);
-        f.n = __ldg(A.wy + (long long)(j + 1) * A.wy_ld + i);
+// ---------------------------------------------------------------------------
+// Per-lane 5-point operator.  BC = broadcast face weights and no diagonal
+// shift (the journal-bearing configs C0/C2/C3): weights live in registers for
+// the whole strip and the two y-faces of a point are equal.  Otherwise faces
+// (and shift) are loaded per row, at a clamped in-grid address -- results at
+// out-of-grid rows/columns are always discarded or multiplied by a zero mask,
+// so they only need to be finite.
+// Out-of-grid raw inputs are loaded as 0; every derived value (trial step,
+// projected gradient, CG vector) is then exactly 0 there as the Dirichlet
+// boundary requires (mid(0,0,0) = 0, pgrad of a fixed variable = 0, masks 0).
+// ---------------------------------------------------------------------------
+template <bool BC>
+struct Op5 {
+    double fw, fe, fs, fn, dg;     // BC: strip-constant faces and diagonal
+    int ic;                        // clamped column
+    __device__ __forceinline__ void init(const StencilOp& A, int i) {
+        ic = min(max(i, 0), A.nx - 1);
+        if constexpr (BC) {
+            fw = __ldg(A.wx + ic);
+            fe = __ldg(A.wx + ic + 1);
+            fs = __ldg(A.wy + ic);
+            fn = fs;
+            dg = (fw + fe) + (fs + fn);
+        }
     }
-    return f;
-}
-
-// (A v) at this lane's point: vc centre, vs/vn rows below/above, west/east by shuffle.
-__device__ __forceinline__ double apply5(const Faces& f, double shift, double vc, double vs, double vn) {
-    const double vw = __shfl_up_sync(0xffffffffu, vc, 1);
-    const double ve = __shfl_down_sync(0xffffffffu, vc, 1);
-    const double d = (f.w + f.e) + (f.s + f.n) + shift;
-    double r = d * vc;
-    r = fma(-f.w, vw, r);
-    r = fma(-f.e, ve, r);
-    r = fma(-f.s, vs, r);
-    r = fma(-f.n, vn, r);
-    return r;
-}
+    // (A v) at row r of this lane: vc centre, vs / vn rows r-1 / r+1, west/east by shuffle
+    __device__ __forceinline__ double apply(const StencilOp& A, int r, double vc, double vs, double vn) const {
+        const double vw = __shfl_up_sync(0xffffffffu, vc, 1);
+        const double ve = __shfl_down_sync(0xffffffffu, vc, 1);
+        if constexpr (BC) {
+            double t = dg * vc;
+            t = fma(-fw, vw, t);
+            t = fma(-fe, ve, t);
+            return fma(-fs, vs + vn, t);
+        } else {
+            const int rc = min(max(r, 0), A.ny - 1);
+            const double* wxr = A.wx + (long long)rc * A.wx_ld + ic;
+            const double w = __ldg(wxr), e = __ldg(wxr + 1);
+            const double s = __ldg(A.wy + (long long)rc * A.wy_ld + ic);
+            const double n = __ldg(A.wy + (long long)(rc + 1) * A.wy_ld + ic);
+            double d = (w + e) + (s + n);
+            if (A.shift) d += __ldg(A.shift + ic + A.nx * rc);
+            double t = d * vc;
+            t = fma(-w, vw, t);
+            t = fma(-e, ve, t);
+            t = fma(-s, vs, t);
+            return fma(-n, vn, t);
+        }
+    }
+};
 
 // One work item per warp: strip column of this lane and output row range.
 template <int H>
@@ -74,24 +95,6 @@ __device__ __forceinline__ bool march_item(const StencilOp& A, const MarchGeom& 
     j0 = c * G.TY;
     j1 = min(j0 + G.TY, A.ny);
     return true;
-}
-
-// Faces cache: broadcast weights are loaded once per strip; full arrays per row.
-struct FaceRow {
-    bool bcast;
-    Faces fb;
-    __device__ __forceinline__ void init(const StencilOp& A, int i, bool col_ok) {
-        bcast = (A.wx_ld == 0 && A.wy_ld == 0);
-        if (bcast) fb = load_faces(A, i, 0, col_ok);
-    }
-    __device__ __forceinline__ Faces at(const StencilOp& A, int i, int j, bool col_ok) const {
-        if (bcast) return (col_ok && j >= 0 && j < A.ny) ? fb : Faces{0.0, 0.0, 0.0, 0.0};
-        return load_faces(A, i, j, col_ok);
-    }
-};
-
-__device__ __forceinline__ double shift_at(const StencilOp& A, int v, bool ok) {
-    return (A.shift && ok) ? __ldg(A.shift + v) : 0.0;
 }
 
 struct NoPre {};
@@ -135,7 +138,7 @@ struct RawAcc {
     unsigned char mp;
 };
 
-template <bool SB>
+template <bool SB, bool BC>
 __global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, const double* __restrict__ dir,
           double sgn, const double* __restrict__ b, const unsigned char* __restrict__ mask_prev,
@@ -153,47 +156,42 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
     int i, j0, j1;
     if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
-        FaceRow FR;
-        FR.init(A, i, col_ok);
-        // windows (row index relative to the step row r)
+        Op5<BC> op;
+        op.init(A, i);
+        const int rend = min(A.ny, j1 + H);            // raw rows [j0-H, rend) are needed
         double yn_m2 = 0.0, yn_m1 = 0.0;               // yn(r-2), yn(r-1)
         double b_m1 = 0.0, l_m1 = 0.0, u_m1 = 0.0;      // row r-1
         double l_m2 = 0.0, u_m2 = 0.0;                  // row r-2
         unsigned char mp_m1 = 0, mp_m2 = 0;
         double gn_m2 = 0.0;                             // gn(r-2)
         double d_m3 = 0.0, d_m2 = 0.0;                  // d(r-3), d(r-2)
-        const int rend = min(A.ny, j1 + H);             // last raw row needed + 1
         pipeline<NoPre, RawAcc>(
             j0 - 2, j1 - j0 + 4, [&](int) { return NoPre{}; },
-            [&](int r, NoPre) {
-                RawAcc x{0.0, 0.0, 0.0, 0.0, 0.0, 0};
-                if (col_ok && r >= 0 && r < rend) {          // loads only; used kPipe rows later
-                    const int v = i + A.nx * r;
-                    x.l = lo<SB>(Bd, v);
-                    x.u = hi<SB>(Bd, v);
-                    x.b = __ldg(b + v);
-                    x.y = __ldg(y_in + v);
-                    if (dir) x.d = __ldg(dir + v);
-                    if (mask_prev) x.mp = __ldg(mask_prev + v);
+            [&](int r, NoPre) {                          // loads only; consumed kPipe rows later
+                RawAcc x{0.0, 0.0, 0.0, SB ? Bd.lc : 0.0, SB ? Bd.uc : 0.0, 0};
+                if (r >= 0 && r < rend) {                // warp-uniform
+                    if (col_ok) {
+                        const int v = i + A.nx * r;
+                        if constexpr (!SB) { x.l = __ldg(Bd.l + v); x.u = __ldg(Bd.u + v); }
+                        x.b = __ldg(b + v);
+                        x.y = __ldg(y_in + v);
+                        if (dir) x.d = __ldg(dir + v);
+                        if (mask_prev) x.mp = __ldg(mask_prev + v);
+                    }
                 }
+                if (!(col_ok && r >= 0 && r < rend)) { x.l = 0.0; x.u = 0.0; }   // fixed at 0 outside
                 return x;
             },
             [&](int r, const RawAcc& x) {
-                const bool okr = col_ok && r >= 0 && r < rend;
-                const double yn0 = okr ? (dir ? trial(x.y, x.d, sgn, alpha, x.l, x.u) : mid(x.l, x.u, x.y)) : 0.0;
+                const double yn0 = dir ? trial(x.y, x.d, sgn, alpha, x.l, x.u) : mid(x.l, x.u, x.y);
                 // level 2 at row r-1
-                const int r1 = r - 1;
-                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
-                const Faces f1 = FR.at(A, i, r1, col_ok);
-                const double ay = apply5(f1, shift_at(A, i + A.nx * r1, ok1), yn_m1, yn_m2, yn0);
-                const double gn1 = ok1 ? ay - b_m1 : 0.0;
-                const double d1 = ok1 ? pgrad(yn_m1, gn1, l_m1, u_m1) : 0.0;
+                const double ay = op.apply(A, r - 1, yn_m1, yn_m2, yn0);
+                const double gn1 = ay - b_m1;
+                const double d1 = pgrad(yn_m1, gn1, l_m1, u_m1);      // 0 outside the grid
                 // level 3 at row r-2
+                const double ad = op.apply(A, r - 2, d_m2, d_m3, d1);
                 const int r2 = r - 2;
-                const bool ok2 = col_ok && r2 >= 0 && r2 < A.ny;
-                const Faces f2 = FR.at(A, i, r2, col_ok);
-                const double ad = apply5(f2, shift_at(A, i + A.nx * r2, ok2), d_m2, d_m3, d1);
-                if (out_lane && ok2 && r2 >= j0 && r2 < j1) {
+                if (out_lane && col_ok && r2 >= j0 && r2 < j1) {
                     const int v = i + A.nx * r2;
                     y_out[v] = yn_m2;
                     g_out[v] = gn_m2;
@@ -208,7 +206,6 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
                     acc[4] += (act && !binding) ? 1.0 : 0.0;
                     acc[5] = fma(d_m2, ad, acc[5]);
                 }
-                // shift windows by one row
                 yn_m2 = yn_m1; yn_m1 = yn0;
                 l_m2 = l_m1; u_m2 = u_m1; mp_m2 = mp_m1;
                 l_m1 = x.l; u_m1 = x.u; b_m1 = x.b; mp_m1 = x.mp;
@@ -239,7 +236,7 @@ struct RawY {
     double y, d, g, l, u;
 };
 
-template <bool SB, int K, bool kDirIsG>
+template <bool SB, bool BC, int K, bool kDirIsG>
 __global__ void __launch_bounds__(kMarchThreads, (K <= 4 ? kMarchMinBlocks : 2))
 k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
           const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu, Scal* S,
@@ -261,41 +258,39 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
     int i, j0, j1;
     if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
-        FaceRow FR;
-        FR.init(A, i, col_ok);
-        // raw values (y, dir, g, l, u) are pipelined; s_h is formed at consumption
+        Op5<BC> op;
+        op.init(A, i);
+        const int rend = min(A.ny, j1 + H);
         double s_m2[K], s_m1[K];
         double g_m1 = 0.0;
 #pragma unroll
         for (int h = 0; h < K; ++h) { s_m2[h] = 0.0; s_m1[h] = 0.0; }
-        const int rend = min(A.ny, j1 + H);
         pipeline<NoPre, RawY>(
             j0 - 1, j1 - j0 + 2, [&](int) { return NoPre{}; },
             [&](int r, NoPre) {
-                RawY x{0.0, 0.0, 0.0, 0.0, 0.0};
-                if (col_ok && r >= 0 && r < rend) {
-                    const int v = i + A.nx * r;
-                    x.y = __ldg(y + v);
-                    x.d = __ldg(dir + v);
-                    x.g = kDirIsG ? x.d : __ldg(g + v);
-                    x.l = lo<SB>(Bd, v);
-                    x.u = hi<SB>(Bd, v);
+                RawY x{0.0, 0.0, 0.0, SB ? Bd.lc : 0.0, SB ? Bd.uc : 0.0};
+                if (r >= 0 && r < rend) {
+                    if (col_ok) {
+                        const int v = i + A.nx * r;
+                        x.y = __ldg(y + v);
+                        x.d = __ldg(dir + v);
+                        if constexpr (!kDirIsG) x.g = __ldg(g + v);
+                        if constexpr (!SB) { x.l = __ldg(Bd.l + v); x.u = __ldg(Bd.u + v); }
+                    }
                 }
+                if constexpr (kDirIsG) x.g = x.d;
+                if (!(col_ok && r >= 0 && r < rend)) { x.l = 0.0; x.u = 0.0; }
                 return x;
             },
             [&](int r, const RawY& x) {
-                const bool okr = col_ok && r >= 0 && r < rend;
                 double s0[K];
 #pragma unroll
-                for (int h = 0; h < K; ++h) s0[h] = okr ? trial(x.y, x.d, sgn, al[h], x.l, x.u) - x.y : 0.0;
+                for (int h = 0; h < K; ++h) s0[h] = trial(x.y, x.d, sgn, al[h], x.l, x.u) - x.y;   // 0 outside
                 const int r1 = r - 1;
-                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
-                const Faces f = FR.at(A, i, r1, col_ok);
-                const double sh = shift_at(A, i + A.nx * r1, ok1);
-                const bool emit = out_lane && ok1 && r1 >= j0 && r1 < j1;
+                const bool emit = out_lane && col_ok && r1 >= j0 && r1 < j1;
 #pragma unroll
                 for (int h = 0; h < K; ++h) {
-                    const double as = apply5(f, sh, s_m1[h], s_m2[h], s0[h]);
+                    const double as = op.apply(A, r1, s_m1[h], s_m2[h], s0[h]);
                     if (emit) {
                         acc[2 * h] = fma(g_m1, s_m1[h], acc[2 * h]);
                         acc[2 * h + 1] = fma(s_m1[h], as, acc[2 * h + 1]);
@@ -352,6 +347,7 @@ struct RawInit {
     unsigned char m;
 };
 
+template <bool BC>
 __global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigned char* __restrict__ mask,
            unsigned char* __restrict__ mask_cg, double* __restrict__ rho, double* __restrict__ p,
@@ -363,38 +359,36 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
     int i, j0, j1;
     if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
-        FaceRow FR;
-        FR.init(A, i, col_ok);
+        Op5<BC> op;
+        op.init(A, i);
+        const int rend = min(A.ny, j1 + H);
         double r_m2 = 0.0, r_m1 = 0.0;
         unsigned char m_m1 = 0;
-        const int rend = min(A.ny, j1 + H);
         pipeline<NoPre, RawInit>(
             j0 - 1, j1 - j0 + 2, [&](int) { return NoPre{}; },
             [&](int r, NoPre) {
                 RawInit x{0.0, 0};
-                if (col_ok && r >= 0 && r < rend) {
-                    const int v = i + A.nx * r;
-                    x.m = __ldg(mask + v);
-                    x.rho = -__ldg(g + v);
+                if (r >= 0 && r < rend) {
+                    if (col_ok) {
+                        const int v = i + A.nx * r;
+                        x.m = __ldg(mask + v);
+                        x.rho = -__ldg(g + v);
+                    }
                 }
                 return x;
             },
             [&](int r, const RawInit& x) {
                 const double r0 = x.m ? x.rho : 0.0;
                 const int r1 = r - 1;
-                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
-                const Faces f = FR.at(A, i, r1, col_ok);
-                const double q = apply5(f, shift_at(A, i + A.nx * r1, ok1), r_m1, r_m2, r0);
-                if (out_lane && ok1 && r1 >= j0 && r1 < j1) {
+                const double q = op.apply(A, r1, r_m1, r_m2, r0);
+                if (out_lane && col_ok && r1 >= j0 && r1 < j1) {
                     const int v = i + A.nx * r1;
                     mask_cg[v] = m_m1;
                     rho[v] = r_m1;
                     p[v] = 0.0;
                     w[v] = 0.0;
-                    if (m_m1) {
-                        acc[0] = fma(r_m1, r_m1, acc[0]);
-                        acc[1] = fma(r_m1, q, acc[1]);
-                    }
+                    acc[0] = fma(r_m1, r_m1, acc[0]);          // r_m1 = 0 off F
+                    acc[1] = m_m1 ? fma(r_m1, q, acc[1]) : acc[1];
                 }
                 r_m2 = r_m1; r_m1 = r0; m_m1 = x.m;
             });
@@ -446,6 +440,7 @@ struct RawCg {
     unsigned char m;
 };
 
+template <bool BC>
 __global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
            const double* __restrict__ rho, const double* __restrict__ p,
@@ -460,18 +455,22 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
     int i, j0, j1;
     if (march_item<H>(A, G, i, j0, j1)) {
         const bool col_ok = (i >= 0 && i < A.nx);
-        FaceRow FR;
-        FR.init(A, i, col_ok);
+        Op5<BC> op;
+        op.init(A, i);
+        const int rend = min(A.ny, j1 + H);
         double pn_m2 = 0.0, pn_m1 = 0.0;          // pn(r-2), pn(r-1)
         double rho_m1 = 0.0;                       // rho(r-1)
         double w_m1 = 0.0, w_m2 = 0.0;             // w(r-1), w(r-2)
         unsigned char m_m1 = 0, m_m2 = 0;
         double rn_m3 = 0.0, rn_m2 = 0.0;           // rn(r-3), rn(r-2)
-        const int rend = min(A.ny, j1 + H);
         pipeline<unsigned char, RawCg>(
             j0 - 2, j1 - j0 + 4,
             [&](int r) -> unsigned char {
-                return (col_ok && r >= 0 && r < rend) ? __ldg(mask + i + A.nx * r) : (unsigned char)0;
+                unsigned char m = 0;
+                if (r >= 0 && r < rend) {
+                    if (col_ok) m = __ldg(mask + i + A.nx * r);
+                }
+                return m;
             },
             [&](int r, unsigned char m) {
                 RawCg x{0.0, 0.0, 0.0, m};
@@ -486,17 +485,12 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
             [&](int r, const RawCg& x) {
                 const double pn0 = x.m ? fma(beta, x.p, x.rho) : 0.0;
                 // level 2 at row r-1
-                const int r1 = r - 1;
-                const bool ok1 = col_ok && r1 >= 0 && r1 < A.ny;
-                const Faces f1 = FR.at(A, i, r1, col_ok);
-                const double ap = apply5(f1, shift_at(A, i + A.nx * r1, ok1 && m_m1), pn_m1, pn_m2, pn0);
+                const double ap = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
                 const double rn1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
                 // level 3 at row r-2
+                const double q = op.apply(A, r - 2, rn_m2, rn_m3, rn1);
                 const int r2 = r - 2;
-                const bool ok2 = col_ok && r2 >= 0 && r2 < A.ny;
-                const Faces f2 = FR.at(A, i, r2, col_ok);
-                const double q = apply5(f2, shift_at(A, i + A.nx * r2, ok2 && m_m2), rn_m2, rn_m3, rn1);
-                if (out_lane && ok2 && r2 >= j0 && r2 < j1 && m_m2) {
+                if (out_lane && m_m2 && r2 >= j0 && r2 < j1) {   // m_m2 = 0 outside the grid
                     const int v = i + A.nx * r2;
                     w[v] = fma(alpha, pn_m2, w_m2);
                     rho_n[v] = rn_m2;
