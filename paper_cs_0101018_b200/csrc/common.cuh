@@ -2,8 +2,10 @@
 // deterministic two-stage block reductions shared by every GPCG kernel.
 //
 // Layout: every vector is a dense fp64 array
-// of the n grid points / CSR rows, linear index v = i + nx*j for stencils.
-// The free mask is one byte per point (1 = free).  Vectors used by CG are
+// of the CSR rows, or, for stencils, of the grid rows at a pitch of nx rounded
+// up to 32 points (256-byte aligned rows; linear index v = i + pitch*j; the
+// padding is never read).  The free mask is one byte per point (1 = free),
+// same pitch.  Vectors used by CG are
 // zero off the free set, which makes A_F p = [v in F] (A p)_v.
 #pragma once
 
@@ -28,7 +30,7 @@ struct Pt {
 // broadcast row.  Iteration covers 32x8 point tiles: threadIdx.x&31 runs along
 // i (coalesced), threadIdx.x>>5 along j.
 struct StencilOp {
-    int nx, ny, n;
+    int nx, ny, pitch;                 // point (i, j) lives at i + pitch*j (pitch = nx rounded up to 32)
     const double* __restrict__ wx;
     const double* __restrict__ wy;
     const double* __restrict__ shift;
@@ -44,7 +46,7 @@ struct StencilOp {
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
             const int bj = t / ntx, bi = t - bj * ntx;
             const int i = (bi << 5) + tx, j = (bj << 3) + ty;
-            if (i < nx && j < ny) body(Pt{i + nx * j, i, j});
+            if (i < nx && j < ny) body(Pt{i + pitch * j, i, j});
         }
     }
 
@@ -60,8 +62,8 @@ struct StencilOp {
         cb(p.v, d);
         if (p.i > 0) cb(p.v - 1, -ww);
         if (p.i < nx - 1) cb(p.v + 1, -we);
-        if (p.j > 0) cb(p.v - nx, -ws);
-        if (p.j < ny - 1) cb(p.v + nx, -wn);
+        if (p.j > 0) cb(p.v - pitch, -ws);
+        if (p.j < ny - 1) cb(p.v + pitch, -wn);
     }
 };
 

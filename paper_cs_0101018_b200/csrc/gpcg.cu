@@ -80,7 +80,9 @@ struct gpcg_problem {
     bool generic = false;          // GPCG_GENERIC=1: stencil problems use the flat generic kernels (A/B tests)
     StencilOp sop{};
     CsrOp cop{};
-    int n = 0;
+    int n = 0;                     // unknowns (nx*ny or CSR rows)
+    int rows = 1, cols = 0, pitch = 0;   // vector layout: rows x cols at a pitch (stencil: nx rounded up to 32)
+    long long nalloc = 0;          // doubles per internal vector = rows * pitch
     long long nnz = 0;
     // library-owned inputs
     double *wx = nullptr, *wy = nullptr, *shift = nullptr;
@@ -171,9 +173,18 @@ int upload_bytes(gpcg_problem* h, void* dst, const void* src, size_t bytes) {
     CK(cudaMemcpyAsync(dst, src, bytes, k, h->st));
     return GPCG_OK;
 }
-int download(gpcg_problem* h, double* dst, const double* src, size_t count) {
+
+// user vector (contiguous n) <-> internal vector (rows x cols at pitch)
+int upload_vec(gpcg_problem* h, double* dst, const double* src) {
+    const cudaMemcpyKind k = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpy2DAsync(dst, (size_t)h->pitch * sizeof(double), src, (size_t)h->cols * sizeof(double),
+                         (size_t)h->cols * sizeof(double), h->rows, k, h->st));
+    return GPCG_OK;
+}
+int download_vec(gpcg_problem* h, double* dst, const double* src) {
     const cudaMemcpyKind k = is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), k, h->st));
+    CK(cudaMemcpy2DAsync(dst, (size_t)h->cols * sizeof(double), src, (size_t)h->pitch * sizeof(double),
+                         (size_t)h->cols * sizeof(double), h->rows, k, h->st));
     return GPCG_OK;
 }
 
@@ -243,15 +254,19 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
     CK(cudaEventCreate(&h->ev_c1));
     CK(cudaEventRecord(h->ev_sync, h->user));
     CK(cudaStreamWaitEvent(h->st, h->ev_sync, 0));
-    const size_t nb = (size_t)h->n * sizeof(double);
+    const size_t nb = (size_t)h->nalloc * sizeof(double);
     CK(cudaMalloc(&h->b, nb));
     CK(cudaMalloc(&h->l, nb));
     CK(cudaMalloc(&h->u, nb));
     for (int k = 0; k < 2; ++k) {
         CK(cudaMalloc(&h->Y[k], nb));
         CK(cudaMalloc(&h->G[k], nb));
-        CK(cudaMalloc(&h->M[k], (size_t)h->n));
-        if (k == 0) CK(cudaMalloc(&h->Mcg, (size_t)h->n));
+        CK(cudaMalloc(&h->M[k], (size_t)h->nalloc));
+        CK(cudaMemsetAsync(h->M[k], 0, (size_t)h->nalloc, h->st));
+        if (k == 0) {
+            CK(cudaMalloc(&h->Mcg, (size_t)h->nalloc));
+            CK(cudaMemsetAsync(h->Mcg, 0, (size_t)h->nalloc, h->st));
+        }
         CK(cudaMalloc(&h->Rho[k], nb));
         CK(cudaMalloc(&h->Q[k], nb));
         CK(cudaMalloc(&h->S2[k], nb));
@@ -271,12 +286,15 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
     CK(cudaMalloc(&h->counter, sizeof(unsigned int)));
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
     int rc;
-    if ((rc = upload(h, h->b, b, h->n))) return rc;
-    if ((rc = upload(h, h->l, l, h->n))) return rc;
-    if ((rc = upload(h, h->u, u, h->n))) return rc;
+    for (double* v : {h->b, h->l, h->u, h->Y[0], h->Y[1], h->G[0], h->G[1], h->W, h->P, h->Rho[0], h->Rho[1],
+                      h->Q[0], h->Q[1], h->S2[0], h->S2[1], h->stage_in, h->stage_out})
+        CK(cudaMemsetAsync(v, 0, nb, h->st));        // padding columns stay 0
+    if ((rc = upload_vec(h, h->b, b))) return rc;
+    if ((rc = upload_vec(h, h->l, l))) return rc;
+    if ((rc = upload_vec(h, h->u, u))) return rc;
     // validation: l <= u, no NaN / inf in b, l != +inf, u != -inf; constant bounds?
     const int g = std::max(1, std::min((h->n + kThreads - 1) / kThreads, h->sms * 4));
-    k_check_inputs<<<g, kThreads, 0, h->st>>>(h->n, h->b, h->l, h->u, h->dS, h->red());
+    k_check_inputs<<<g, kThreads, 0, h->st>>>(h->cols, h->rows, h->pitch, h->b, h->l, h->u, h->dS, h->red());
     CKLAUNCH();
     if ((rc = sync_scal(h))) return rc;
     if (h->hS->r0 != 0.0)
@@ -522,6 +540,11 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
     gpcg_problem* h = new gpcg_problem();
     h->n = (int)(nx * ny);
+    h->rows = (int)ny;
+    h->cols = (int)nx;
+    h->pitch = (int)((nx + 31) / 32 * 32);
+    h->nalloc = (long long)h->pitch * ny;
+    if (h->nalloc >= (1LL << 31)) { delete h; return set_err(GPCG_EINVAL, "pitched grid too large"); }
     h->is_csr = false;
     h->generic = getenv("GPCG_GENERIC") != nullptr && getenv("GPCG_GENERIC")[0] == '1';
     h->mg1 = march_geom((int)nx, (int)ny, 1);
@@ -544,15 +567,17 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     if ((rc = count_nonfinite(h, h->wy, (long long)wyn, &t))) return fail(rc);
     bad += t;
     if (shift) {
-        if (cudaMalloc(&h->shift, (size_t)h->n * sizeof(double)) != cudaSuccess)
+        if (cudaMalloc(&h->shift, (size_t)h->nalloc * sizeof(double)) != cudaSuccess)
             return fail(set_err(GPCG_ENOMEM, "shift"));
-        if ((rc = upload(h, h->shift, shift, h->n))) return fail(rc);
-        if ((rc = count_nonfinite(h, h->shift, h->n, &t))) return fail(rc);
+        if (cudaMemsetAsync(h->shift, 0, (size_t)h->nalloc * sizeof(double), h->st) != cudaSuccess)
+            return fail(set_err(GPCG_ECUDA, "memset shift"));
+        if ((rc = upload_vec(h, h->shift, shift))) return fail(rc);
+        if ((rc = count_nonfinite(h, h->shift, h->nalloc, &t))) return fail(rc);
         bad += t;
     }
     if (bad != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite stencil weights", bad));
     h->is_csr = false;
-    h->sop = StencilOp{(int)nx, (int)ny, h->n, h->wx, h->wy, h->shift, (long long)wx_ld, (long long)wy_ld};
+    h->sop = StencilOp{(int)nx, (int)ny, h->pitch, h->wx, h->wy, h->shift, (long long)wx_ld, (long long)wy_ld};
     h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
     h->nnz = 5 * (long long)h->n - 2 * nx - 2 * ny;
     h->grid = std::max(1, std::min(units(h), h->sms * 16));
@@ -572,6 +597,10 @@ int gpcg_create_csr(gpcg_problem** out, void* cuda_stream, int64_t n, const int6
     if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
     gpcg_problem* h = new gpcg_problem();
     h->n = (int)n;
+    h->rows = 1;
+    h->cols = (int)n;
+    h->pitch = (int)n;
+    h->nalloc = n;
     h->is_csr = true;
     auto fail = [&](int r) { free_all(h); return r; };
     int rc = create_common(h, cuda_stream, b, l, u);
@@ -636,9 +665,9 @@ int gpcg_project(gpcg_problem* h, const double* x, double* px, double* pg_norm2,
     if (!h || !x || !px) return set_err(GPCG_EINVAL, "NULL argument");
     int rc;
     if ((rc = enter(h))) return rc;
-    if ((rc = upload(h, h->stage_in, x, h->n))) return rc;
+    if ((rc = upload_vec(h, h->stage_in, x))) return rc;
     if ((rc = launch_accept(h, h->stage_in, nullptr, 0.0, nullptr, h->Y[0], h->G[0], h->M[0]))) return rc;
-    if ((rc = download(h, px, h->Y[0], h->n))) return rc;
+    if ((rc = download_vec(h, px, h->Y[0]))) return rc;
     if ((rc = sync_scal(h))) return rc;
     h->free_mask = 0;
     if (pg_norm2) *pg_norm2 = h->hS->pg2;
@@ -655,10 +684,12 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
         return set_err(GPCG_ESTATE, "reduced hessvec needs a free set: call gpcg_project or gpcg_solve first");
     int rc;
     if ((rc = enter(h))) return rc;
-    const bool vdev = is_device_ptr(v), ydev = is_device_ptr(y);
+    // direct device access only when the layout is contiguous (CSR, or nx a multiple of 32)
+    const bool contiguous = (h->pitch == h->cols);
+    const bool vdev = is_device_ptr(v) && contiguous, ydev = is_device_ptr(y) && contiguous;
     const double* vin = v;
     if (!vdev) {
-        if ((rc = upload(h, h->stage_in, v, h->n))) return rc;
+        if ((rc = upload_vec(h, h->stage_in, v))) return rc;
         vin = h->stage_in;
     }
     double* yout = ydev ? y : h->stage_out;
@@ -673,8 +704,8 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
     h->launches++;
     CKLAUNCH();
     if (!ydev) {
-        if ((rc = download(h, y, h->stage_out, h->n))) return rc;
-        CK(cudaStreamSynchronize(h->st));
+        if ((rc = download_vec(h, y, h->stage_out))) return rc;
+        if (!is_device_ptr(y)) CK(cudaStreamSynchronize(h->st));
     }
     return leave(h);
 }
@@ -684,7 +715,7 @@ int gpcg_objective(gpcg_problem* h, const double* x, double* q) {
     if (!h || !x || !q) return set_err(GPCG_EINVAL, "NULL argument");
     int rc;
     if ((rc = enter(h))) return rc;
-    if ((rc = upload(h, h->stage_in, x, h->n))) return rc;
+    if ((rc = upload_vec(h, h->stage_in, x))) return rc;
     with_op_only(h, [&](auto& op) {
         using Op = std::decay_t<decltype(op)>;
         k_objective<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->stage_in, h->b, h->dS, h->red());
@@ -719,7 +750,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     const Scal& S = *h->hS;
 
     // Setup: x <- P[x0], g <- A x - b
-    if ((rc = upload(h, h->stage_in, x0, h->n))) return rc;
+    if ((rc = upload_vec(h, h->stage_in, x0))) return rc;
     if ((rc = launch_accept(h, h->stage_in, nullptr, 0.0, nullptr, h->Y[0], h->G[0], h->M[0]))) return rc;
     if ((rc = sync_scal(h))) return rc;
     st.full_spmvs++;
@@ -800,7 +831,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
         }
     }
     // x_out, q, sets
-    if ((rc = download(h, x_out, h->Y[cur], h->n))) return rc;
+    if ((rc = download_vec(h, x_out, h->Y[cur]))) return rc;
     with_op_only(h, [&](auto& op) {
         using Op = std::decay_t<decltype(op)>;
         k_objective<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->Y[cur], h->b, h->dS, h->red());
@@ -831,7 +862,7 @@ fail:
     {
         const std::string msg = g_err;
         cudaGetLastError();
-        download(h, x_out, h->Y[cur], h->n);
+        download_vec(h, x_out, h->Y[cur]);
         cudaStreamSynchronize(h->st);
         h->free_mask = cur;
         st.status = rc;

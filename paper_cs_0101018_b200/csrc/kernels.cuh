@@ -333,11 +333,13 @@ k_cg_iter(Op A, const unsigned char* __restrict__ mask,
 // input validation at create: #(l > u or NaN), #(b NaN), l / u constant?
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
-k_check_inputs(int n, const double* __restrict__ b, const double* __restrict__ l,
+k_check_inputs(int cols, int rows, int pitch, const double* __restrict__ b, const double* __restrict__ l,
                const double* __restrict__ u, Scal* S, RedScratch R) {
     double acc[3] = {0.0, 0.0, 0.0};
     const double l0 = l[0], u0 = u[0];
-    for (int v = blockIdx.x * kThreads + threadIdx.x; v < n; v += gridDim.x * kThreads) {
+    const long long n = (long long)cols * rows;
+    for (long long k = blockIdx.x * (long long)kThreads + threadIdx.x; k < n; k += (long long)gridDim.x * kThreads) {
+        const long long v = (k % cols) + (k / cols) * (long long)pitch;
         const double lv = l[v], uv = u[v], bv = b[v];
         acc[0] += (!(lv <= uv) || isnan(bv) || isinf(bv) || lv == INFINITY || uv == -INFINITY) ? 1.0 : 0.0;
         acc[1] += (lv != l0) ? 1.0 : 0.0;

@@ -75,7 +75,7 @@ struct Op5 {
             const double s = __ldg(A.wy + (long long)rc * A.wy_ld + ic);
             const double n = __ldg(A.wy + (long long)(rc + 1) * A.wy_ld + ic);
             double d = (w + e) + (s + n);
-            if (A.shift) d += __ldg(A.shift + ic + A.nx * rc);
+            if (A.shift) d += __ldg(A.shift + ic + A.pitch * rc);
             double t = d * vc;
             t = fma(-w, vw, t);
             t = fma(-e, ve, t);
@@ -171,7 +171,7 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
                 RawAcc x{0.0, 0.0, 0.0, SB ? Bd.lc : 0.0, SB ? Bd.uc : 0.0, 0};
                 if (r >= 0 && r < rend) {                // warp-uniform
                     if (col_ok) {
-                        const int v = i + A.nx * r;
+                        const int v = i + A.pitch * r;
                         if constexpr (!SB) { x.l = __ldg(Bd.l + v); x.u = __ldg(Bd.u + v); }
                         x.b = __ldg(b + v);
                         x.y = __ldg(y_in + v);
@@ -192,7 +192,7 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
                 const double ad = op.apply(A, r - 2, d_m2, d_m3, d1);
                 const int r2 = r - 2;
                 if (out_lane && col_ok && r2 >= j0 && r2 < j1) {
-                    const int v = i + A.nx * r2;
+                    const int v = i + A.pitch * r2;
                     y_out[v] = yn_m2;
                     g_out[v] = gn_m2;
                     const bool act = (yn_m2 == l_m2) || (yn_m2 == u_m2);
@@ -271,7 +271,7 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
                 RawY x{0.0, 0.0, 0.0, SB ? Bd.lc : 0.0, SB ? Bd.uc : 0.0};
                 if (r >= 0 && r < rend) {
                     if (col_ok) {
-                        const int v = i + A.nx * r;
+                        const int v = i + A.pitch * r;
                         x.y = __ldg(y + v);
                         x.d = __ldg(dir + v);
                         if constexpr (!kDirIsG) x.g = __ldg(g + v);
@@ -370,7 +370,7 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
                 RawInit x{0.0, 0};
                 if (r >= 0 && r < rend) {
                     if (col_ok) {
-                        const int v = i + A.nx * r;
+                        const int v = i + A.pitch * r;
                         x.m = __ldg(mask + v);
                         x.rho = -__ldg(g + v);
                     }
@@ -382,7 +382,7 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
                 const int r1 = r - 1;
                 const double q = op.apply(A, r1, r_m1, r_m2, r0);
                 if (out_lane && col_ok && r1 >= j0 && r1 < j1) {
-                    const int v = i + A.nx * r1;
+                    const int v = i + A.pitch * r1;
                     mask_cg[v] = m_m1;
                     rho[v] = r_m1;
                     p[v] = 0.0;
@@ -468,14 +468,14 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
             [&](int r) -> unsigned char {
                 unsigned char m = 0;
                 if (r >= 0 && r < rend) {
-                    if (col_ok) m = __ldg(mask + i + A.nx * r);
+                    if (col_ok) m = __ldg(mask + i + A.pitch * r);
                 }
                 return m;
             },
             [&](int r, unsigned char m) {
                 RawCg x{0.0, 0.0, 0.0, m};
                 if (m) {
-                    const int v = i + A.nx * r;
+                    const int v = i + A.pitch * r;
                     x.rho = rho[v];
                     x.p = p[v];
                     if (out_lane) x.w = w[v];       // w is only needed where this warp writes
@@ -491,7 +491,7 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
                 const double q = op.apply(A, r - 2, rn_m2, rn_m3, rn1);
                 const int r2 = r - 2;
                 if (out_lane && m_m2 && r2 >= j0 && r2 < j1) {   // m_m2 = 0 outside the grid
-                    const int v = i + A.nx * r2;
+                    const int v = i + A.pitch * r2;
                     w[v] = fma(alpha, pn_m2, w_m2);
                     rho_n[v] = rn_m2;
                     p_n[v] = pn_m2;

@@ -38,9 +38,11 @@ def report(path):
             except ValueError:
                 return float("nan")
         tu = units[idx["gpu__time_duration.sum"]]
-        t_ns = g("gpu__time_duration.sum") * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(tu, 1)
+        t_ns = g("gpu__time_duration.sum") * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3,
+                                               "msecond": 1e6, "ms": 1e6}.get(tu, 1)
         bu = units[idx["dram__bytes_read.sum"]]
-        bscale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(bu, 1)
+        bscale = {"byte": 1, "B": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6,
+                  "Gbyte": 1e9, "GB": 1e9}.get(bu, 1)
         byt = (g("dram__bytes_read.sum") + g("dram__bytes_write.sum")) * bscale
         print(f"{short(r[ki])[:38]:38s} {t_ns/1e3:8.2f} {byt/1e6:9.2f} {byt/t_ns:8.1f} "
               f"{g('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):6.1f} "
@@ -57,7 +59,8 @@ def launches(path):
     for r in rows[h + 1:]:
         if len(r) <= mi:
             continue
-        v = float(r[mi].replace(",", "")) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(r[ui], 1)
+        v = float(r[mi].replace(",", "")) * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3,
+                                             "msecond": 1e6, "ms": 1e6}.get(r[ui], 1)
         d[short(r[ki]).split("(")[0]].append(v)
     tot = sum(sum(v) for v in d.values())
     print(f"{'kernel':45s} {'launches':>8s} {'mean us':>9s} {'share %':>8s}")
