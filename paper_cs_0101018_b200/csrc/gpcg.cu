@@ -22,6 +22,9 @@
 #include "gpcg.h"
 #include "kernels.cuh"
 #include "march.cuh"
+#include "tile.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace gpcg;
 
@@ -109,6 +112,11 @@ struct gpcg_problem {
     int grid = 1;                  // generic kernels (CSR, hessvec, objective)
     MarchGeom mg1{}, mg2{};        // column-march geometry for halo 1 / halo 2 stencil kernels
     int grid_m1 = 1, grid_m2 = 1;
+    // TMA tile path (broadcast-face stencils): tensor maps of every internal array
+    bool tile = false;
+    TileGeom tg{};
+    int grid_t_cg = 1, grid_t_acc = 1, grid_t_srch = 1;
+    CUtensorMap tmY[2], tmG[2], tmW, tmWc, tmB, tmL, tmU, tmRho[2], tmP[2], tmM[2], tmMcg, tmStage;
     gpcg_params prm{};
     int free_mask = -1;            // index into M of the recorded free set, -1 none
     // CG graph chunk
@@ -236,6 +244,90 @@ long long march_grid_bound(const gpcg_problem* h) {
     return std::max(march_grid(h->mg1), march_grid(h->mg2));
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D tensor map over an internal (pitched) stencil array; out-of-grid elements read as 0
+int make_map(gpcg_problem* h, CUtensorMap* m, const void* ptr, bool u8, int bw, int bh) {
+    auto enc = tma_encode_fn();
+    if (!enc) return set_err(GPCG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)h->cols, (cuuint64_t)h->rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)h->pitch * (u8 ? 1 : 8)};
+    const cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                     const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(GPCG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return GPCG_OK;
+}
+
+template <class K>
+int set_smem(K kernel, int bytes) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    return GPCG_OK;
+}
+
+// Build the TMA tile path for a broadcast-face stencil handle (C0/C2/C3 family).
+int setup_tile(gpcg_problem* h) {
+    int rc;
+    for (int k = 0; k < 2; ++k) {
+        if ((rc = make_map(h, &h->tmY[k], h->Y[k], false, TBW, TBH))) return rc;
+        if ((rc = make_map(h, &h->tmG[k], h->G[k], false, TBW, TBH))) return rc;
+        if ((rc = make_map(h, &h->tmRho[k], h->Rho[k], false, TBW, TBH))) return rc;
+        if ((rc = make_map(h, &h->tmP[k], h->Q[k], false, TBW, TBH))) return rc;
+        if ((rc = make_map(h, &h->tmM[k], h->M[k], true, TBW, TBH))) return rc;
+    }
+    if ((rc = make_map(h, &h->tmW, h->W, false, TBW, TBH))) return rc;
+    if ((rc = make_map(h, &h->tmWc, h->W, false, TOX, TOY))) return rc;
+    if ((rc = make_map(h, &h->tmB, h->b, false, TBW, TBH))) return rc;
+    if ((rc = make_map(h, &h->tmL, h->l, false, TBW, TBH))) return rc;
+    if ((rc = make_map(h, &h->tmU, h->u, false, TBW, TBH))) return rc;
+    if ((rc = make_map(h, &h->tmMcg, h->Mcg, true, TBW, TBH))) return rc;
+    if ((rc = make_map(h, &h->tmStage, h->stage_in, false, TBW, TBH))) return rc;
+    h->tg = TileGeom{h->cols, h->rows, h->pitch, (h->cols + TOX - 1) / TOX, (h->rows + TOY - 1) / TOY};
+    const int ntiles = h->tg.ntx * h->tg.nty;
+    if ((rc = set_smem(k3_cg_iter<2>, CgStage<2>::kSmem))) return rc;
+    if ((rc = set_smem(k3_accept<true>, AccStage<true>::kSmem))) return rc;
+    if ((rc = set_smem(k3_accept<false>, AccStage<false>::kSmem))) return rc;
+    if ((rc = set_smem(k3_search<true, true>, SrchStage<true, true>::kSmem))) return rc;
+    if ((rc = set_smem(k3_search<true, false>, SrchStage<true, false>::kSmem))) return rc;
+    if ((rc = set_smem(k3_search<false, true>, SrchStage<false, true>::kSmem))) return rc;
+    if ((rc = set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem))) return rc;
+    auto resident = [&](auto kernel, int smem) {
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kTileThreads, smem);
+        return std::max(1, nb) * h->sms;
+    };
+    h->grid_t_cg = std::min(ntiles, resident(k3_cg_iter<2>, CgStage<2>::kSmem));
+    h->grid_t_acc = std::min(ntiles, h->sb ? resident(k3_accept<true>, AccStage<true>::kSmem)
+                                            : resident(k3_accept<false>, AccStage<false>::kSmem));
+    h->grid_t_srch = std::min(ntiles, h->sb ? resident(k3_search<true, true>, SrchStage<true, true>::kSmem)
+                                             : resident(k3_search<false, true>, SrchStage<false, true>::kSmem));
+    h->tile = true;
+    return GPCG_OK;
+}
+
+const CUtensorMap* map_of(gpcg_problem* h, const void* p) {
+    for (int k = 0; k < 2; ++k) {
+        if (p == h->Y[k]) return &h->tmY[k];
+        if (p == h->G[k]) return &h->tmG[k];
+        if (p == h->M[k]) return &h->tmM[k];
+    }
+    if (p == h->W) return &h->tmW;
+    if (p == h->stage_in) return &h->tmStage;
+    return nullptr;
+}
+
 // common part of create: device, streams, vectors, bounds, validation
 int create_common(gpcg_problem* h, void* stream, const double* b, const double* l, const double* u) {
     int ndev = 0;
@@ -312,6 +404,23 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
 // ---------------------------------------------------------------- launches
 int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double sgn,
                   const unsigned char* mask_prev, double* y_out, double* g_out, unsigned char* m_out) {
+    if (h->tile) {   // TMA tile path
+        const CUtensorMap* my = map_of(h, y_in);
+        const CUtensorMap* md = dir ? map_of(h, dir) : my;
+        const CUtensorMap* mp = mask_prev ? map_of(h, mask_prev) : &h->tmM[0];
+        if (!my || !md || !mp) return set_err(GPCG_ECUDA, "internal: no tensor map for an accept operand");
+        if (h->sb)
+            k3_accept<true><<<h->grid_t_acc, kTileThreads, AccStage<true>::kSmem, h->st>>>(
+                h->sop, h->tg, h->bounds, *my, *md, h->tmB, h->tmL, h->tmU, *mp, dir ? 1 : 0, sgn,
+                mask_prev ? 1 : 0, y_out, g_out, m_out, h->dS, h->red());
+        else
+            k3_accept<false><<<h->grid_t_acc, kTileThreads, AccStage<false>::kSmem, h->st>>>(
+                h->sop, h->tg, h->bounds, *my, *md, h->tmB, h->tmL, h->tmU, *mp, dir ? 1 : 0, sgn,
+                mask_prev ? 1 : 0, y_out, g_out, m_out, h->dS, h->red());
+        h->launches++;
+        CKLAUNCH();
+        return GPCG_OK;
+    }
     if (!h->is_csr && !h->generic) {   // stencil: accept + regrad + mask + counts + next Cauchy step in one sweep
         auto go = [&](auto sbt, auto bct) {
             constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value;
@@ -355,6 +464,23 @@ int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
 int launch_search(gpcg_problem* h, const double* y, const double* g, const double* dir, double sgn,
                   int use_alpha0, int h0, int K) {
     const double mu = h->prm.mu;
+    if (h->tile && K == 2) {   // TMA tile path (first sweep); retries use the column march
+        const CUtensorMap* my = map_of(h, y);
+        const CUtensorMap* md = map_of(h, dir);
+        const CUtensorMap* mg = map_of(h, g);
+        if (!my || !md || !mg) return set_err(GPCG_ECUDA, "internal: no tensor map for a search operand");
+        const bool dg = (dir == g);
+        auto go = [&](auto sbt, auto dgt) {
+            constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
+            k3_search<SB, DG><<<h->grid_t_srch, kTileThreads, SrchStage<SB, DG>::kSmem, h->st>>>(
+                h->sop, h->tg, h->bounds, *my, *md, *mg, h->tmL, h->tmU, sgn, use_alpha0, h0, mu, h->dS, h->red());
+        };
+        if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+        else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        h->launches++;
+        CKLAUNCH();
+        return GPCG_OK;
+    }
     if (!h->is_csr && !h->generic) {
         const bool dg = (dir == g);
         auto go = [&](auto sbt, auto bct, auto kt, auto dgt) {
@@ -429,6 +555,12 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < chunk; ++i) {
         const int a = i & 1, bb = a ^ 1;
+        if (h->tile) {
+            k3_cg_iter<2><<<h->grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
+                h->sop, h->tg, h->tmRho[a], h->tmP[a], h->tmWc, h->tmMcg, h->Rho[bb], h->Q[bb], h->W, h->dS,
+                h->red());
+            continue;
+        }
         if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
             if (h->bc)
                 k2_cg_iter<true><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a],
@@ -579,6 +711,11 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     h->is_csr = false;
     h->sop = StencilOp{(int)nx, (int)ny, h->pitch, h->wx, h->wy, h->shift, (long long)wx_ld, (long long)wy_ld};
     h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
+    {
+        const char* e = getenv("GPCG_TILE");
+        const bool want_tile = h->bc && !h->generic && !(e && e[0] == '0');
+        if (want_tile && (rc = setup_tile(h))) return fail(rc);
+    }
     h->nnz = 5 * (long long)h->n - 2 * nx - 2 * ny;
     h->grid = std::max(1, std::min(units(h), h->sms * 16));
     if ((rc = leave(h))) return fail(rc);
