@@ -114,6 +114,7 @@ struct gpcg_problem {
     int grid_m1 = 1, grid_m2 = 1;
     // TMA tile path (broadcast-face stencils): tensor maps of every internal array
     bool tile = false;
+    int tile_mask = 7;             // GPCG_TILE bits: 1 accept, 2 search, 4 CG iteration (A/B and debugging)
     TileGeom tg{};
     int grid_t_cg = 1, grid_t_acc = 1, grid_t_srch = 1;
     CUtensorMap tmY[2], tmG[2], tmW, tmWc, tmB, tmL, tmU, tmRho[2], tmP[2], tmM[2], tmMcg, tmStage;
@@ -404,7 +405,7 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
 // ---------------------------------------------------------------- launches
 int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double sgn,
                   const unsigned char* mask_prev, double* y_out, double* g_out, unsigned char* m_out) {
-    if (h->tile) {   // TMA tile path
+    if (h->tile && (h->tile_mask & 1)) {   // TMA tile path
         const CUtensorMap* my = map_of(h, y_in);
         const CUtensorMap* md = dir ? map_of(h, dir) : my;
         const CUtensorMap* mp = mask_prev ? map_of(h, mask_prev) : &h->tmM[0];
@@ -464,7 +465,7 @@ int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
 int launch_search(gpcg_problem* h, const double* y, const double* g, const double* dir, double sgn,
                   int use_alpha0, int h0, int K) {
     const double mu = h->prm.mu;
-    if (h->tile && K == 2) {   // TMA tile path (first sweep); retries use the column march
+    if (h->tile && (h->tile_mask & 2) && K == 2) {   // TMA tile path (first sweep); retries use the column march
         const CUtensorMap* my = map_of(h, y);
         const CUtensorMap* md = map_of(h, dir);
         const CUtensorMap* mg = map_of(h, g);
@@ -555,7 +556,7 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < chunk; ++i) {
         const int a = i & 1, bb = a ^ 1;
-        if (h->tile) {
+        if (h->tile && (h->tile_mask & 4)) {
             k3_cg_iter<2><<<h->grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
                 h->sop, h->tg, h->tmRho[a], h->tmP[a], h->tmWc, h->tmMcg, h->Rho[bb], h->Q[bb], h->W, h->dS,
                 h->red());
@@ -713,7 +714,8 @@ int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int
     h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
     {
         const char* e = getenv("GPCG_TILE");
-        const bool want_tile = h->bc && !h->generic && !(e && e[0] == '0');
+        if (e && *e) h->tile_mask = atoi(e) & 7;
+        const bool want_tile = h->bc && !h->generic && h->tile_mask != 0;
         if (want_tile && (rc = setup_tile(h))) return fail(rc);
     }
     h->nnz = 5 * (long long)h->n - 2 * nx - 2 * ny;
