@@ -286,14 +286,14 @@ int setup_tile(gpcg_problem* h) {
         if ((rc = make_map(h, &h->tmG[k], h->G[k], false, TBW, TBH))) return rc;
         if ((rc = make_map(h, &h->tmRho[k], h->Rho[k], false, TBW, TBH))) return rc;
         if ((rc = make_map(h, &h->tmP[k], h->Q[k], false, TBW, TBH))) return rc;
-        if ((rc = make_map(h, &h->tmM[k], h->M[k], true, TBW, TBH))) return rc;
+        if ((rc = make_map(h, &h->tmM[k], h->M[k], true, MBW, TBH))) return rc;
     }
     if ((rc = make_map(h, &h->tmW, h->W, false, TBW, TBH))) return rc;
     if ((rc = make_map(h, &h->tmWc, h->W, false, TOX, TOY))) return rc;
     if ((rc = make_map(h, &h->tmB, h->b, false, TBW, TBH))) return rc;
     if ((rc = make_map(h, &h->tmL, h->l, false, TBW, TBH))) return rc;
     if ((rc = make_map(h, &h->tmU, h->u, false, TBW, TBH))) return rc;
-    if ((rc = make_map(h, &h->tmMcg, h->Mcg, true, TBW, TBH))) return rc;
+    if ((rc = make_map(h, &h->tmMcg, h->Mcg, true, MBW, TBH))) return rc;
     if ((rc = make_map(h, &h->tmStage, h->stage_in, false, TBW, TBH))) return rc;
     h->tg = TileGeom{h->cols, h->rows, h->pitch, (h->cols + TOX - 1) / TOX, (h->rows + TOY - 1) / TOY};
     const int ntiles = h->tg.ntx * h->tg.nty;

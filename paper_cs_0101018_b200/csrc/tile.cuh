@@ -30,7 +30,11 @@ constexpr int THALO = 2;
 constexpr int TOX = TBW - 2 * THALO;    // 60 output columns
 constexpr int TOY = TBH - 2 * THALO;    // 32 output rows
 constexpr int kBoxF64 = TBW * TBH * 8;  // 18432 bytes
-constexpr int kBoxU8 = TBW * TBH;       // 2304 bytes
+// u8 boxes (free masks): the TMA box start must be 16-byte aligned in the inner
+// dimension, so mask boxes start at floor16(x) and are 80 columns wide; the
+// tile's 64 columns then sit at offset moff = x - floor16(x) in [0, 16).
+constexpr int MBW = 80;
+constexpr int kBoxU8 = 2944;            // MBW * TBH = 2880, padded to a multiple of 128
 constexpr int kCtrF64 = TOX * TOY * 8;  // 15360 bytes (centre box, CG w)
 
 struct TileGeom {
@@ -39,6 +43,8 @@ struct TileGeom {
 };
 
 // ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ int floor16(int x) { return x & ~15; }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -111,7 +117,8 @@ __device__ __forceinline__ double apply_box(const ColFaces& F, const double* v, 
 template <int NSTAGE>
 struct CgStage {
     static constexpr int kRho = 0, kP = kBoxF64, kW = 2 * kBoxF64, kMask = 2 * kBoxF64 + kCtrF64;
-    static constexpr int kBytes = 2 * kBoxF64 + kCtrF64 + kBoxU8;   // 54528 (multiple of 128)
+    static constexpr int kBytes = 2 * kBoxF64 + kCtrF64 + kBoxU8;   // multiple of 128
+    static constexpr int kTx = 2 * kBoxF64 + kCtrF64 + MBW * TBH;   // bytes the TMA delivers
     static constexpr int kSmem = NSTAGE * kBytes + (int)sizeof(ColFaces) + 64;
 };
 
@@ -130,11 +137,11 @@ k3_cg_iter(StencilOp A, TileGeom T, const __grid_constant__ CUtensorMap m_rho, c
     auto issue = [&](int stage, int t) {
         unsigned char* st = smem + stage * L::kBytes;
         const int x0 = (t % T.ntx) * TOX, y0 = (t / T.ntx) * TOY;
-        mbar_expect_tx(&bar[stage], L::kBytes);
+        mbar_expect_tx(&bar[stage], L::kTx);
         tma_load_2d(st + L::kRho, &m_rho, x0 - THALO, y0 - THALO, &bar[stage]);
         tma_load_2d(st + L::kP, &m_p, x0 - THALO, y0 - THALO, &bar[stage]);
         tma_load_2d(st + L::kW, &m_w, x0, y0, &bar[stage]);
-        tma_load_2d(st + L::kMask, &m_mask, x0 - THALO, y0 - THALO, &bar[stage]);
+        tma_load_2d(st + L::kMask, &m_mask, floor16(x0 - THALO), y0 - THALO, &bar[stage]);
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) mbar_init(&bar[s], 1);
@@ -156,17 +163,20 @@ k3_cg_iter(StencilOp A, TileGeom T, const __grid_constant__ CUtensorMap m_rho, c
         const double* ws = reinterpret_cast<const double*>(st + L::kW);
         const unsigned char* m = st + L::kMask;
         const int x0 = (t % T.ntx) * TOX, y0 = (t / T.ntx) * TOY;
+        const int moff = (x0 - THALO) - floor16(x0 - THALO);
         load_colfaces(F, A, x0 - THALO);
         mbar_wait(&bar[stage], parity);
         // level 1: pn over the whole box
-        for (int q = threadIdx.x; q < TBW * TBH; q += kTileThreads)
-            p[q] = m[q] ? fma(beta, p[q], rho[q]) : 0.0;
+        for (int q = threadIdx.x; q < TBW * TBH; q += kTileThreads) {
+            const int r = q / TBW, c = q % TBW;
+            p[q] = m[r * MBW + c + moff] ? fma(beta, p[q], rho[q]) : 0.0;
+        }
         __syncthreads();
         // level 2: rn on rows 1..TBH-2, cols 1..TBW-2
         for (int q = threadIdx.x; q < (TBH - 2) * (TBW - 2); q += kTileThreads) {
             const int r = 1 + q / (TBW - 2), c = 1 + q % (TBW - 2);
             const int kk = r * TBW + c;
-            if (m[kk]) rho[kk] = fma(-alpha, apply_box(F, p, r, c), rho[kk]);
+            if (m[r * MBW + c + moff]) rho[kk] = fma(-alpha, apply_box(F, p, r, c), rho[kk]);
             else rho[kk] = 0.0;
         }
         __syncthreads();
@@ -174,7 +184,7 @@ k3_cg_iter(StencilOp A, TileGeom T, const __grid_constant__ CUtensorMap m_rho, c
         for (int q = threadIdx.x; q < TOX * TOY; q += kTileThreads) {
             const int r = THALO + q / TOX, c = THALO + q % TOX;
             const int kk = r * TBW + c;
-            if (m[kk]) {
+            if (m[r * MBW + c + moff]) {
                 const double rn = rho[kk];
                 const double qv = apply_box(F, rho, r, c);
                 acc[0] = fma(rn, rn, acc[0]);
@@ -237,7 +247,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
     ColFaces& F = *reinterpret_cast<ColFaces*>(smem + L::kGN + kBoxF64);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kGN + kBoxF64 + sizeof(ColFaces));
     const int ntiles = T.ntx * T.nty;
-    const uint32_t bytes = kBoxF64 * (2 + (has_dir ? 1 : 0) + (SB ? 0 : 2)) + (has_mp ? kBoxU8 : 0);
+    const uint32_t bytes = kBoxF64 * (2 + (has_dir ? 1 : 0) + (SB ? 0 : 2)) + (has_mp ? MBW * TBH : 0);
     auto issue = [&](int t) {
         const int x0 = (t % T.ntx) * TOX - THALO, y0 = (t / T.ntx) * TOY - THALO;
         mbar_expect_tx(&bar[0], bytes);
@@ -248,7 +258,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
             tma_load_2d(smem + L::kL, &m_l, x0, y0, &bar[0]);
             tma_load_2d(smem + L::kU, &m_u, x0, y0, &bar[0]);
         }
-        if (has_mp) tma_load_2d(smem + L::kMP, &m_mp, x0, y0, &bar[0]);
+        if (has_mp) tma_load_2d(smem + L::kMP, &m_mp, floor16(x0), y0, &bar[0]);
     };
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -260,6 +270,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
     int k = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
         const int x0 = (t % T.ntx) * TOX, y0 = (t / T.ntx) * TOY;
+        const int moff = (x0 - THALO) - floor16(x0 - THALO);
         load_colfaces(F, A, x0 - THALO);
         mbar_wait(&bar[0], k & 1);
         // level 1: yn over the box; out-of-grid points: y = dir = 0, bounds forced to 0 -> yn = 0
@@ -301,7 +312,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
                 acc[0] = fma(d, d, acc[0]);
                 acc[1] = fma(g, g, acc[1]);
                 acc[2] += act ? 1.0 : 0.0;
-                if (has_mp) acc[3] += (mp[kk] != mm) ? 1.0 : 0.0;
+                if (has_mp) acc[3] += (mp[r * MBW + c + moff] != mm) ? 1.0 : 0.0;
                 const bool binding = (yn == l && g >= 0.0) || (yn == u && g <= 0.0);
                 acc[4] += (act && !binding) ? 1.0 : 0.0;
                 acc[5] = fma(d, ad, acc[5]);
