@@ -19,5 +19,10 @@ for name in sys.argv[1:]:
     rc, x, st = s.solve(x0, prob.tol)
     torch.cuda.synchronize()
     t3 = time.time()
-    print(f"{name}: gen {t1-t0:.2f}s create {t2-t1:.2f}s solve {t3-t2:.3f}s rc={rc} {st}", flush=True)
+    cg_us = 1e3 * st["t_cg_timed_ms"] / max(st["cg_iters_timed"], 1)
+    gp_us = 1e3 * st["t_gp_ms"] / max(st["gp_iters"], 1)
+    print(f"{name}: solve {t3-t2:.3f}s rc={rc} outer={st['outer_iters']} gp={st['gp_iters']} cg={st['cg_iters']} "
+          f"| CG {cg_us:.1f} us/iter (steady) | GP {gp_us:.1f} us/step | t_cg {st['t_cg_ms']:.0f} ms "
+          f"t_gp {st['t_gp_ms']:.0f} ms | q={st['q']:.15g} free={st['n_free']} launches={st['kernel_launches']}",
+          flush=True)
     s.close()
