@@ -4,7 +4,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("GPCG_TRACE", "1")
+if not os.environ.get("GPCG_TRACE_OFF"):
+    os.environ.setdefault("GPCG_TRACE", "1")
 import torch  # noqa: E402
 from paper_cs_0101018_b200 import problems as P, gpcg  # noqa: E402
 
