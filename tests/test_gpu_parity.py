@@ -274,3 +274,40 @@ def test_c2_full_size_certificate(G, oracle):
     act, bnd, na, nb = oracle.sets(x, g, prob.l, prob.u)
     assert na == st["n_active"] and na - nb == 0
     assert 0.60 <= 1 - na / prob.n <= 0.76           # PAPER.md:876-878 (~68% free)
+
+
+# ------------------------------------------------------------------ oracle goldens (sizes the oracle
+# cannot solve inside a test run; written by scripts/golden_oracle.py, which calls only oracle/)
+GOLDEN = {
+    "C2": lambda: P.c2(),
+    "C3_1600": lambda: P.c3_family(1600, 1600),
+    "C4_128": lambda: P.c4_family(m=128),
+    "C4": lambda: P.c4(),
+}
+
+
+@pytest.mark.parametrize("name", list(GOLDEN))
+def test_solve_parity_vs_oracle_golden(G, name):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet (python scripts/golden_oracle.py {name})")
+    gold = json.load(open(path))
+    prob = GOLDEN[name]()
+    assert prob.n == gold["n"] and gold["rc"] == 0
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(prob.x0, gold["tol"])
+    assert rc == 0, (rc, st)
+    assert abs(st["q"] - gold["q"]) <= 1e-10 * abs(gold["q"]), (st["q"], gold["q"])
+    idx = np.asarray(gold["idx"])
+    xo = np.asarray(gold["x"])
+    assert np.max(np.abs(x[idx] - xo)) <= 1e-7, np.max(np.abs(x[idx] - xo))
+    # active sets: identical away from ties (the free copy within 1e-7 of the bound)
+    act = (x[idx] == prob.l[idx]) | (x[idx] == prob.u[idx])
+    acto = np.asarray(gold["active_sample"], dtype=bool)
+    for k in np.flatnonzero(act != acto):
+        i = idx[k]
+        free_val = x[i] if acto[k] else xo[k]
+        assert min(abs(free_val - prob.l[i]), abs(free_val - prob.u[i])) <= 1e-7, (i, x[i], xo[k])
+    assert abs(st["n_active"] - gold["n_active"]) <= gold["n_free_near_bound"] + 0.001 * prob.n
