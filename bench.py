@@ -16,8 +16,11 @@ the configured workload from x0 to tol, inputs resident in HBM.
   cpu_baseline / --impl reference: the plain-C oracle (oracle/) on the same
             workload, bounded by a time budget, on the host cores (1 thread).
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
-N > 1 runs under torchrun (one process per GPU); see DESIGN.md "Multi-GPU".
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference] [--slabs S]
+N > 1 runs under torchrun (one process per GPU): the SAME problem split into N row
+slabs (gpcg_create_*_dist: NCCL halo exchange + one allreduce per CG iteration),
+i.e. strong scaling; see DESIGN.md "Multi-GPU".  --slabs S (N = 1) splits the
+problem into S slabs on the one GPU (device-copy halos: the multi-rank code path).
 """
 import argparse
 import json
@@ -51,6 +54,25 @@ def load_peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cg_kernel_name(prob):
+    if prob.kind != "stencil2d":
+        return "k_cg_iter<CsrOp>"
+    bc = not prob.wx_ld and not prob.wy_ld and prob.shift is None
+    tile = int(os.environ.get("GPCG_TILE", "7") or 7) & 4
+    if os.environ.get("GPCG_GENERIC") == "1":
+        return "k_cg_iter<StencilOp>"
+    return "k3_cg_iter<2> (TMA tile)" if (bc and tile) else "k2_cg_iter (column march)"
+
+
+def cg_min_bytes_per_free_point(prob):
+    """Bytes the stencil CG kernel's 3-vector recurrence must move per free point (read
+    rho, p, w; write rho', p', w' = 48 B; + 16 B of full face arrays for C1-type
+    operators) -- its own floor, below the 80 B of SURVEY.md 8(d)."""
+    if prob.kind == "stencil2d":
+        return 48.0 + (16.0 if (prob.wx_ld or prob.wy_ld) else 0.0)
+    return cg_bytes_per_free_point(prob)
 
 
 def cg_bytes_per_free_point(prob):
@@ -170,13 +192,24 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [gpcg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
     dev = torch.device("cuda", local)
     prob = P.get(args.config)
     stream = torch.cuda.current_stream()
-    solver = gpcg.Solver.from_problem(prob, stream=stream, device=dev)
-    x0 = torch.from_numpy(prob.x0).to(dev)
+    if world > 1 or args.slabs > 1:
+        solver, rb, re, loc = gpcg.Solver.dist(prob, rank, world, nccl_id, local_slabs=args.slabs,
+                                               stream=stream, device=dev)
+        x0_host = loc["x0"]
+    else:
+        solver = gpcg.Solver.from_problem(prob, stream=stream, device=dev)
+        x0_host = prob.x0
+        loc = None
+    x0 = torch.from_numpy(np.ascontiguousarray(x0_host)).to(dev)
     x_out = torch.empty_like(x0)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
 
@@ -211,22 +244,24 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
 
-    hvps = float(agg["cg_iters"])
+    hvps = float(agg["cg_iters"])       # global reduced HVPs (every rank counts the same iterations)
     if world > 1:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        h = torch.tensor([hvps], dtype=torch.float64, device=dev)
-        dist.all_reduce(h, op=dist.ReduceOp.SUM)
-        tot_ms, hvps = float(t.item()), float(h.item())
+        tot_ms = float(t.item())
     value = hvps / (tot_ms / 1e3)
 
     # roofline of the dominant kernel (k_cg_iter), steady-state CUDA-event timing
     peak, peak_src = load_peaks()
     bpp = cg_bytes_per_free_point(prob)
     it_t = max(agg["cg_iters_timed"], 1)
-    bytes_per_launch = (bpp * agg["cg_free_iters_timed"] + 1.0 * prob.n * agg["cg_iters_timed"]) / it_t
+    # per launch of this rank's kernel: the global free count split evenly over ranks
+    bytes_per_launch = (bpp * agg["cg_free_iters_timed"] + 1.0 * prob.n * agg["cg_iters_timed"]) / it_t / world
+    min_bytes_per_launch = (cg_min_bytes_per_free_point(prob) * agg["cg_free_iters_timed"]
+                            + 1.0 * prob.n * agg["cg_iters_timed"]) / it_t / world
     launch_s = (agg["t_cg_timed_ms"] / 1e3) / it_t
     achieved = bytes_per_launch / launch_s / 1e9 if agg["cg_iters_timed"] else None
+    achieved_min = min_bytes_per_launch / launch_s / 1e9 if agg["cg_iters_timed"] else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tr_path):
@@ -235,31 +270,44 @@ def run_ours(args):
     # e2e: through the C ABI with host (pinned) buffers, H2D/D2H inside the timed region
     def pinned(a):
         return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-    hp = P.Problem(**{**prob.__dict__})
-    for k in ("b", "l", "u", "x0", "wx", "wy", "shift", "row_ptr", "col", "val"):
-        setattr(hp, k, pinned(getattr(prob, k)))
-    xh = torch.empty(prob.n, dtype=torch.float64).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
-    s_e2e = gpcg.Solver.from_problem(hp, stream=stream)          # warm-up of the e2e path
-    s_e2e.solve(hp.x0, prob.tol, x_out=xh)
+    if loc is None:
+        hp = P.Problem(**{**prob.__dict__})
+        for k in ("b", "l", "u", "x0", "wx", "wy", "shift", "row_ptr", "col", "val"):
+            setattr(hp, k, pinned(getattr(prob, k)))
+        xh = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+        make = lambda: gpcg.Solver.from_problem(hp, stream=stream)             # noqa: E731
+        h2d = int(prob.input_bytes())
+    else:
+        # the rank's slab: local_part slices, pinned; create_*_dist uploads them
+        hp = P.Problem(**{**prob.__dict__})
+        lp = {k: (pinned(v) if isinstance(v, np.ndarray) else v) for k, v in loc.items()}
+        xh = torch.empty(loc["n"], dtype=torch.float64).pin_memory()
+        make = lambda: gpcg.Solver.dist(prob, rank, world, nccl_id, local_slabs=args.slabs,   # noqa: E731
+                                        stream=stream, local=lp)[0]
+        h2d = int(sum(v.numel() * v.element_size() for v in lp.values() if hasattr(v, "numel")))
+    x0h = pinned(np.ascontiguousarray(x0_host))
+    s_e2e = make()                                               # warm-up of the e2e path
+    s_e2e.solve(x0h, prob.tol, x_out=xh)
     s_e2e.close()
     e2e_s, e2e_hvps = 0.0, 0
     for _ in range(e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        s2 = gpcg.Solver.from_problem(hp, stream=stream)
-        rc, _, st2 = s2.solve(hp.x0, prob.tol, x_out=xh)
+        s2 = make()
+        rc, _, st2 = s2.solve(x0h, prob.tol, x_out=xh)
         s2.close()
         torch.cuda.synchronize()
         e2e_s += time.perf_counter() - t0
         e2e_hvps += st2["cg_iters"]
-    e2e_val = e2e_hvps / e2e_s
     if world > 1:
-        t = torch.tensor([e2e_s, e2e_hvps], dtype=torch.float64, device=dev)
-        tm = t.clone(); dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        e2e_val = float(t[1].item()) / float(tm[0].item())
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = e2e_hvps / e2e_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -273,27 +321,32 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, paper_cs_0101018_b200/problems.py)",
             "config": {"workload": WORKLOADS[args.config], "n": prob.n,
                        "l2": "flushed (256 MB write) between timed solves",
-                       "parallelism": "1 GPU per solve" if world == 1 else f"{world} independent replicas"},
+                       "parallelism": ("1 GPU, 1 slab" if world == 1 and args.slabs == 1 else
+                                       f"{world} GPU(s) x {args.slabs} row slab(s) of one problem "
+                                       f"(halo exchange + one allreduce per CG iteration)")},
             "solve": {"s_per_solve": tot_ms / args.steps / 1e3, "outer_iters": last["outer_iters"],
                       "gp_iters": last["gp_iters"], "cg_iters": last["cg_iters"],
                       "n_free": last["n_free"], "q": last["q"], "pg_norm": last["pg_norm"],
                       "tau": last["tau"], "t_cg_share": agg["t_cg_ms"] / tot_ms},
-            "roofline": {"bound": "hbm", "kernel": "k_cg_iter<StencilOp>" if prob.kind == "stencil2d"
-                         else "k_cg_iter<CsrOp>",
+            "roofline": {"bound": "hbm", "kernel": cg_kernel_name(prob),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
                          "frac_of_8TBs": (achieved / 8000.0) if achieved else None,
                          "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_launch": bytes_per_launch, "us_per_launch": launch_s * 1e6,
-                         "algorithmic_bytes": f"{bpp:.0f} B per free point + 1 B mask per point"},
+                         "algorithmic_bytes": f"{bpp:.0f} B per free point + 1 B mask per point "
+                                              f"(SURVEY.md 8(d) fused CG iteration)",
+                         "achieved_at_kernel_floor": achieved_min,
+                         "kernel_floor_bytes": f"{cg_min_bytes_per_free_point(prob):.0f} B per free point + "
+                                               f"1 B mask per point (the 3-vector recurrence's own minimum)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT,
-                    "h2d_bytes_per_step": int(prob.input_bytes()),
-                    "d2h_bytes_per_step": int(prob.n * 8),
+                    "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": int(x0.numel() * 8),
                     "what": "gpcg_create (H2D operator,b,l,u from pinned host) + gpcg_solve (H2D x0, "
                             "D2H x) + gpcg_destroy, wall clock, %d steps" % e2e_steps},
             "gpu_launches": agg["kernel_launches"],
@@ -315,6 +368,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slabs", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -60,7 +60,7 @@ enum {
     GPCG_EINVAL = -1,       /* bad argument, l_i > u_i, NaN in inputs            */
     GPCG_ENOMEM = -2,       /* device allocation failed                          */
     GPCG_ECUDA = -3,        /* CUDA runtime error / no device                    */
-    GPCG_ENCCL = -4,        /* reserved for the multi-GPU path                   */
+    GPCG_ENCCL = -4,        /* NCCL failure / not loadable (multi-rank path)     */
     GPCG_ENOTSPD = -5,      /* <d,Ad> <= 0 or <p,A_k p> <= 0: A not SPD          */
     GPCG_ESEARCH = -6,      /* projected search found no step in max_halvings    */
     GPCG_ESTATE = -7        /* e.g. reduced hessvec before any project/solve     */
@@ -107,6 +107,47 @@ typedef struct {
 GPCG_API gpcg_params gpcg_params_default(void);
 
 /*
+ * Row-slab distribution (the paper's row-block distribution of
+ * A, b, l, u over processes, without its redistribution
+ * of A_k after every free-set change).  One process per GPU; rank r
+ * owns the contiguous global rows [row_begin, row_end): grid rows j for
+ * stencil2d (each nx unknowns), matrix rows for CSR.  Ranks must cover the
+ * rows in rank order (rank 0 first).  Every rank calls every function with its
+ * own slab (same sequence on all ranks); user arrays hold the rank's rows only.
+ * Each operator application reads ghost rows of the neighbouring ranks
+ * (stencil: 2 grid rows; CSR: the band of rows its columns reach -- columns of
+ * a rank may only refer to rows of itself and of ranks r-1, r+1), exchanged by
+ * NCCL send/recv after every sweep that writes a vector a neighbour reads, and
+ * every global sum is one ncclAllReduce (one per CG iteration, one per search
+ * and accept sweep).  NCCL is the process's own libnccl.so.2, bound at run time.
+ *   rank, nranks: this process's rank, number of ranks (1 = single process).
+ *   nccl_id:      128-byte ncclUniqueId from gpcg_nccl_unique_id on rank 0,
+ *                 identical on every rank (broadcast it, e.g. with
+ *                 torch.distributed); ignored when nranks == 1.
+ *   local_slabs:  >= 1; > 1 splits this rank's rows further into that many
+ *                 slabs on the same device, exchanging ghost rows by device
+ *                 copies and summing slab totals in slab order -- the same
+ *                 arithmetic as nranks * local_slabs ranks (used to test the
+ *                 slab path on one GPU).
+ * Errors: GPCG_EINVAL for a bad range or a slab of < 2 stencil rows (< 1 CSR
+ * row) or a CSR band beyond the neighbouring slab; GPCG_ENCCL if NCCL fails.
+ */
+typedef struct {
+    int32_t rank, nranks;
+    const void *nccl_id;
+    int64_t row_begin, row_end;
+    int32_t local_slabs;
+} gpcg_dist;
+
+/* Balanced contiguous split: part k of `parts` gets [begin, end) of [0, total)
+ * (host-only helper; the split gpcg_dist's local_slabs uses internally). */
+GPCG_API void gpcg_partition_rows(int64_t total, int32_t parts, int32_t part, int64_t *begin, int64_t *end);
+
+/* ncclGetUniqueId of the process's NCCL into out128 (128 bytes).  GPCG_ENCCL
+ * if libnccl.so.2 cannot be loaded. */
+GPCG_API int gpcg_nccl_unique_id(void *out128);
+
+/*
  * gpcg_create_stencil2d -- A is the 5-point face-weight operator on an nx x ny
  * grid (BASELINE.json configs[0-3]; the paper's journal-bearing discretisation
  * P:742-779 under reading R2).  Grid point (i, j), 0-based, linear index
@@ -131,6 +172,19 @@ GPCG_API int gpcg_create_stencil2d(gpcg_problem **out, void *cuda_stream, int64_
                           const double *u, double c);
 
 /*
+ * gpcg_create_stencil2d_dist -- as gpcg_create_stencil2d for the rank's slab
+ * (gpcg_dist above; NULL = the whole grid on one slab).  ny is the GLOBAL
+ * number of grid rows; b, l, u, shift hold the rank's rows (row_end-row_begin)
+ * * nx entries; wx (wx_ld != 0) the rank's grid rows; wy (wy_ld != 0) the
+ * face rows row_begin .. row_end inclusive (row_end-row_begin+1 rows, so the
+ * face row shared by two ranks is passed by both).  Broadcast faces (ld 0)
+ * are passed whole by every rank.
+ */
+GPCG_API int gpcg_create_stencil2d_dist(gpcg_problem **out, const gpcg_dist *dist, void *cuda_stream, int64_t nx,
+                               int64_t ny, const double *wx, int64_t wx_ld, const double *wy, int64_t wy_ld,
+                               const double *shift, const double *b, const double *l, const double *u, double c);
+
+/*
  * gpcg_create_csr -- A given in CSR with BOTH triangles stored:
  * row_ptr[n+1] (int64, row_ptr[0] = 0), col[nnz] (int32, sorted within each
  * row, 0 <= col < n), val[nnz] (fp64).  The paper's PETSc "standard
@@ -141,6 +195,15 @@ GPCG_API int gpcg_create_stencil2d(gpcg_problem **out, void *cuda_stream, int64_
 GPCG_API int gpcg_create_csr(gpcg_problem **out, void *cuda_stream, int64_t n, const int64_t *row_ptr,
                     const int32_t *col, const double *val, const double *b, const double *l,
                     const double *u, double c);
+
+/*
+ * gpcg_create_csr_dist -- as gpcg_create_csr for the rank's rows: n is the
+ * GLOBAL size; row_ptr has row_end-row_begin+1 entries (row_ptr[0] = 0), col
+ * holds GLOBAL column ids, val, b, l, u the rank's rows.
+ */
+GPCG_API int gpcg_create_csr_dist(gpcg_problem **out, const gpcg_dist *dist, void *cuda_stream, int64_t n,
+                         const int64_t *row_ptr, const int32_t *col, const double *val, const double *b,
+                         const double *l, const double *u, double c);
 
 /* Replace the algorithm constants (validated: 0 < mu < 1/2, 0 < eta1, eta2 < 1, ...). */
 GPCG_API int gpcg_set_params(gpcg_problem *h, const gpcg_params *p);
@@ -181,7 +244,7 @@ GPCG_API int gpcg_project(gpcg_problem *h, const double *x, double *px, double *
 /* q(x) = 1/2 x'Ax - b'x + c for any x (no projection). */
 GPCG_API int gpcg_objective(gpcg_problem *h, const double *x, double *q);
 
-/* Problem size n. */
+/* Entries owned by this handle (n; the rank's rows with gpcg_dist). */
 GPCG_API int64_t gpcg_size(const gpcg_problem *h);
 
 GPCG_API void gpcg_destroy(gpcg_problem *h);

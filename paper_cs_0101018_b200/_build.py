@@ -18,7 +18,7 @@ DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "--extended-lambda", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "-shared", "-I", INCLUDE, "-I", CSRC]
+         "-shared", "-I", INCLUDE, "-I", CSRC, "-ldl"]
 
 
 def stale() -> bool:

@@ -29,12 +29,21 @@ struct Pt {
 // 5-point face-weight operator (gpcg.h, gpcg_create_stencil2d).  ld 0 means a
 // broadcast row.  Iteration covers 32x8 point tiles: threadIdx.x&31 runs along
 // i (coalesced), threadIdx.x>>5 along j.
+//
+// Slabs: a handle may own only grid rows [0, ny) of a larger
+// grid (a row slab of one rank, or one of several slabs on one device).  Rows
+// [rlo, 0) and [ny, rhi) are then GHOST rows holding the neighbouring slab's
+// values (refreshed by the host's halo exchange); rows outside [rlo, rhi) are
+// the Dirichlet boundary (zero).  Single slab: rlo = 0, rhi = ny.  Face arrays
+// (ld != 0) carry the ghost rows too; outputs are only ever written for owned
+// rows.
 struct StencilOp {
     int nx, ny, pitch;                 // point (i, j) lives at i + pitch*j (pitch = nx rounded up to 32)
     const double* __restrict__ wx;
     const double* __restrict__ wy;
     const double* __restrict__ shift;
     long long wx_ld, wy_ld;
+    int rlo, rhi;                      // readable rows (owned + ghost); outside: Dirichlet zero
 
     __device__ __forceinline__ int num_units() const { return ((nx + 31) >> 5) * ((ny + 7) >> 3); }
 
@@ -62,12 +71,15 @@ struct StencilOp {
         cb(p.v, d);
         if (p.i > 0) cb(p.v - 1, -ww);
         if (p.i < nx - 1) cb(p.v + 1, -we);
-        if (p.j > 0) cb(p.v - pitch, -ws);
-        if (p.j < ny - 1) cb(p.v + pitch, -wn);
+        if (p.j - 1 >= rlo) cb(p.v - pitch, -ws);
+        if (p.j + 1 < rhi) cb(p.v + pitch, -wn);
     }
 };
 
 // General CSR (both triangles, int64 row_ptr, int32 col).  One thread per row.
+// Columns are LOCAL offsets from the slab's first owned row: a slab's vectors
+// hold [lo ghost band | n owned rows | hi ghost band] and col may be negative
+// (lower band) or >= n (upper band).
 struct CsrOp {
     int n;
     const long long* __restrict__ rp;
@@ -159,6 +171,9 @@ struct Scal {
 struct RedScratch {
     double* partials;          // [kMaxSums][gridDim.x]
     unsigned int* counter;     // zero between launches
+    double* out;               // non-null: DEFERRED mode (slabs / ranks) -- the last block writes the
+                               // totals here and the decision logic runs in k_finalize after the
+                               // cross-slab / cross-rank sum (fin.cuh); null: finalise in place
 };
 
 template <int NS>
@@ -217,7 +232,12 @@ __device__ __forceinline__ void reduce_and_finish(double (&v)[NS], const RedScra
     block_reduce<NS>(t, smem);
     if (threadIdx.x == 0) {
         *R.counter = 0u;
-        fin(t);
+        if (R.out) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s) R.out[s] = t[s];
+        } else {
+            fin(t);
+        }
     }
 }
 

@@ -1,28 +1,45 @@
 // gpcg.cu -- libgpcg.so: the C ABI of include/gpcg.h and the host state machine
-// of Algorithm GPCG driving the sm_100a kernels of kernels.cuh.
+// of Algorithm GPCG driving the sm_100a kernels.
 //
 // Control: the host runs the outer / GP logic from a few
-// device scalars read once per GP sub-step (one pinned 200-byte readback); the
-// CG inner solve runs as CUDA-graph chunks of `cg_chunk` single-reduction
-// iterations whose device-side finaliser sets a done flag (later launches are
-// no-ops), polled once per chunk.  The decisions below follow, step by step,
-// the same algorithm as oracle/gpcg_oracle.c (written independently; the two
-// share no code).
+// device scalars read once per GP sub-step (one pinned readback); the CG inner
+// solve runs as CUDA-graph chunks of `cg_chunk` single-reduction iterations
+// whose device-side finaliser sets a done flag (later launches are no-ops),
+// polled once per chunk.  The decisions follow, step by step, the same
+// algorithm as oracle/gpcg_oracle.c (written independently; no shared code).
+//
+// Slabs: a handle owns one or more contiguous row slabs of
+// the problem.  Each slab stores its vectors with ghost rows (stencil: 2 grid
+// rows per side, CSR: the band of neighbour rows its columns reach), refreshed
+// after every sweep that writes a vector some neighbour reads -- by a device
+// copy between slabs of this process, or by NCCL send/recv between ranks.
+// With more than one slab (or rank) every reducing kernel DEFERS its decision
+// (RedScratch::out): the per-slab totals are summed in slab order (k_combine),
+// allreduced across ranks (one ncclAllReduce of <= 2K+2 doubles: one per CG
+// iteration, one per GP sub-step) and k_finalize applies the decision to the
+// global totals.  One slab on one rank: no ghosts, no copies, no collectives.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: the functions are resolved at run time (the process's own NCCL)
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include "gpcg.h"
+#include "fin.cuh"
 #include "kernels.cuh"
 #include "march.cuh"
 #include "tile.cuh"
+#include "march_tma.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -58,8 +75,14 @@ int set_err(int code, const char* fmt, ...) {
                            __FILE__, __LINE__);                                               \
     } while (0)
 
+#define RC(call)                    \
+    do {                            \
+        int rc_ = (call);           \
+        if (rc_) return rc_;        \
+    } while (0)
+
 bool trace_on() {
-    static const bool on = getenv("GPCG_TRACE") != nullptr;
+    static const bool on = getenv("GPCG_TRACE") != nullptr && getenv("GPCG_TRACE")[0] == '1';
     return on;
 }
 
@@ -72,63 +95,140 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// ---------------------------------------------------------------- NCCL (run-time bound)
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi* nccl_api() {
+    static NcclApi api;
+    static bool tried = false, ok = false;
+    if (!tried) {
+        tried = true;
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // the process's NCCL (e.g. torch's)
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (lib) {
+#define NSYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(lib, "nccl" #f))
+            NSYM(GetUniqueId); NSYM(CommInitRank); NSYM(CommDestroy); NSYM(AllReduce); NSYM(Broadcast);
+            NSYM(Send); NSYM(Recv); NSYM(GroupStart); NSYM(GroupEnd); NSYM(GetErrorString);
+#undef NSYM
+            ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Broadcast &&
+                 api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
+        }
+    }
+    return ok ? &api : nullptr;
+}
+
+#define NK(call)                                                                                \
+    do {                                                                                        \
+        ncclResult_t r_ = (call);                                                               \
+        if (r_ != ncclSuccess)                                                                  \
+            return set_err(GPCG_ENCCL, "%s: %s (%s:%d)", #call, nccl_api()->GetErrorString(r_), \
+                           __FILE__, __LINE__);                                                 \
+    } while (0)
+
+// ---------------------------------------------------------------- vectors of a slab
+enum Vec : int { VY0, VY1, VG0, VG1, VW, VP, VRHO0, VRHO1, VQ0, VQ1, VS0, VS1, VIN, VOUT, VB, VL, VU, NVEC };
+enum Msk : int { MK0, MK1, MKCG, NMSK };
+constexpr int NO_VEC = -1;
+constexpr int NB_NONE = -1, NB_REMOTE = -2;
+
+inline Vec vy(int k) { return (Vec)(VY0 + k); }
+inline Vec vg(int k) { return (Vec)(VG0 + k); }
+inline Vec vrho(int k) { return (Vec)(VRHO0 + k); }
+inline Vec vq(int k) { return (Vec)(VQ0 + k); }
+inline Vec vs(int k) { return (Vec)(VS0 + k); }
+inline Msk mk(int k) { return (Msk)(MK0 + k); }
+
+struct Slab {
+    int row0 = 0, rows = 0;         // owned rows [row0, row0+rows) of the rank's part (grid rows / CSR rows)
+    int uoff = 0;                   // offset of row0 in the rank's user arrays (rows)
+    int glo = 0, ghi = 0;           // ghost rows below / above
+    int send_lo = 0, send_hi = 0;   // rows the lower / upper neighbour reads from this slab
+    int nb_lo = NB_NONE, nb_hi = NB_NONE;
+    long long nalloc = 0;           // elements per vector = (glo + rows + ghi) * pitch
+    double* vb[NVEC] = {};          // allocation bases
+    double* v[NVEC] = {};           // origins (owned row 0)
+    unsigned char* mb[NMSK] = {};
+    unsigned char* m[NMSK] = {};
+    double *wxb = nullptr, *wyb = nullptr, *shb = nullptr;   // face arrays / shift (bases)
+    long long* rp = nullptr;
+    int* ci = nullptr;
+    double* val = nullptr;
+    StencilOp sop{};
+    CsrOp cop{};
+    double* partials = nullptr;
+    unsigned int* counter = nullptr;
+    MarchGeom mg1{}, mg2{};
+    int grid_m1 = 1, grid_m2 = 1, grid = 1;
+    TileGeom tg{};
+    int grid_t_cg = 1, grid_t_acc = 1, grid_t_srch = 1;
+    CUtensorMap tm[NVEC];
+    CUtensorMap tmm[NMSK];
+    CUtensorMap tmWc;               // w, centre box (CG)
+    // TMA-fed column march (k4_cg_iter): band boxes of rho / p (x2), w, CG mask
+    CUtensorMap t4rho[2], t4p[2], t4w, t4m;
+    BandGeom bg{};
+    int grid4 = 1;
+};
+
 }  // namespace
 
 struct gpcg_problem {
     int dev = 0, sms = 148;
-    cudaStream_t user = nullptr;   // caller's stream
-    cudaStream_t st = nullptr;     // private work stream (capturable)
-    cudaEvent_t ev_sync = nullptr, ev_a = nullptr, ev_b = nullptr;
+    cudaStream_t user = nullptr;    // caller's stream
+    cudaStream_t st = nullptr;      // private work stream (capturable)
+    cudaEvent_t ev_sync = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c0 = nullptr, ev_c1 = nullptr;
     bool is_csr = false;
-    bool generic = false;          // GPCG_GENERIC=1: stencil problems use the flat generic kernels (A/B tests)
-    StencilOp sop{};
-    CsrOp cop{};
-    int n = 0;                     // unknowns (nx*ny or CSR rows)
-    int rows = 1, cols = 0, pitch = 0;   // vector layout: rows x cols at a pitch (stencil: nx rounded up to 32)
-    long long nalloc = 0;          // doubles per internal vector = rows * pitch
+    bool generic = false;           // GPCG_GENERIC=1: stencil problems use the flat generic kernels (A/B tests)
+    bool sb = false;                // scalar (constant) bounds
+    bool bc = false;                // stencil with broadcast faces and no shift
+    bool tile = false;              // TMA tile path built
+    int tile_mask = 15;             // GPCG_TILE bits: 1 accept, 2 search, 4 CG iteration (k3),
+                                    // 8 CG iteration as the TMA-fed column march (k4, preferred over 4)
+    int nx = 0, pitch = 1;          // stencil: grid width and row pitch (nx rounded up to 32); CSR: 1
+    long long wx_ld = 0, wy_ld = 0; // user face layout (0 = broadcast)
+    long long n_local = 0;          // entries owned by this rank (the user's arrays)
+    long long n_global = 0;
+    long long rank_row0 = 0;        // this rank's first global row
     long long nnz = 0;
-    // library-owned inputs
-    double *wx = nullptr, *wy = nullptr, *shift = nullptr;
-    long long* rp = nullptr;
-    int* ci = nullptr;
-    double* val = nullptr;
-    double *b = nullptr, *l = nullptr, *u = nullptr;
     double c = 0.0;
-    bool sb = false;               // scalar bounds detected
-    bool bc = false;               // stencil with broadcast faces and no shift
-    Bounds bounds{};
-    // work vectors
-    double *Y[2] = {nullptr, nullptr}, *G[2] = {nullptr, nullptr};
-    unsigned char* M[2] = {nullptr, nullptr};
-    unsigned char* Mcg = nullptr;  // free mask of the running CG call (fixed address for the graph)
-    double *W = nullptr, *P = nullptr;
-    double *Rho[2] = {nullptr, nullptr}, *Q[2] = {nullptr, nullptr}, *S2[2] = {nullptr, nullptr};
-    double *stage_in = nullptr, *stage_out = nullptr;
-    // scalars + reduction scratch
+    double lc = 0.0, uc = 0.0;      // the scalar bounds when sb
+    std::vector<Slab> slabs;
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+    bool deferred = false;          // several slabs or ranks: reductions go through k_finalize
+    double* red_all = nullptr;      // [nslabs][kMaxSums] per-slab totals
+    double* red_tot = nullptr;      // [kMaxSums] global totals
+    double* lu0 = nullptr;          // global (l_0, u_0)
     Scal* dS = nullptr;
-    Scal* hS = nullptr;            // pinned mirror
-    double* partials = nullptr;
-    unsigned int* counter = nullptr;
-    int grid = 1;                  // generic kernels (CSR, hessvec, objective)
-    MarchGeom mg1{}, mg2{};        // column-march geometry for halo 1 / halo 2 stencil kernels
-    int grid_m1 = 1, grid_m2 = 1;
-    // TMA tile path (broadcast-face stencils): tensor maps of every internal array
-    bool tile = false;
-    int tile_mask = 7;             // GPCG_TILE bits: 1 accept, 2 search, 4 CG iteration (A/B and debugging)
-    TileGeom tg{};
-    int grid_t_cg = 1, grid_t_acc = 1, grid_t_srch = 1;
-    CUtensorMap tmY[2], tmG[2], tmW, tmWc, tmB, tmL, tmU, tmRho[2], tmP[2], tmM[2], tmMcg, tmStage;
+    Scal* hS = nullptr;             // pinned mirror
     gpcg_params prm{};
-    int free_mask = -1;            // index into M of the recorded free set, -1 none
-    // CG graph chunk
+    int free_mask = -1;             // index of the recorded free set, -1 none
     cudaGraphExec_t cg_exec = nullptr;
     int cg_exec_chunk = 0;
     long long launches = 0;
-    cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
     long long cg_iters_timed = 0, cg_free_iters_timed = 0;
     double t_cg_timed_ms = 0.0;
 
-    RedScratch red() const { return RedScratch{partials, counter}; }
+    int nslabs() const { return (int)slabs.size(); }
+    RedScratch red(int s) const {
+        double* out = nullptr;
+        if (deferred) out = nslabs() > 1 ? red_all + (long long)s * kMaxSums : red_tot;
+        return RedScratch{slabs[s].partials, slabs[s].counter, out};
+    }
+    Bounds bounds(const Slab& s) const { return Bounds{s.v[VL], s.v[VU], lc, uc}; }
 };
 
 namespace {
@@ -152,58 +252,135 @@ int leave(gpcg_problem* h) {
     return GPCG_OK;
 }
 
-template <class F>
-void with_op(gpcg_problem* h, F&& f) {
-    if (h->is_csr) {
-        if (h->sb) f(h->cop, std::true_type()); else f(h->cop, std::false_type());
-    } else {
-        if (h->sb) f(h->sop, std::true_type()); else f(h->sop, std::false_type());
+// ---------------------------------------------------------------- reductions (a6)
+// After the reducing kernel of every slab: nothing (one slab, decided in place)
+// or combine -> allreduce -> finalize.
+int finish_reduce(gpcg_problem* h, const FinArgs& a, int ns) {
+    if (!h->deferred) return GPCG_OK;
+    if (h->nslabs() > 1) {
+        k_combine<<<1, 64, 0, h->st>>>(h->red_all, h->nslabs(), ns, h->red_tot);
+        h->launches++;
+        CKLAUNCH();
     }
-}
-
-template <class F>
-void with_op_only(gpcg_problem* h, F&& f) {
-    if (h->is_csr) f(h->cop); else f(h->sop);
-}
-
-int units(const gpcg_problem* h) {
-    if (h->is_csr) return (h->n + kThreads - 1) / kThreads;
-    return ((h->sop.nx + 31) / 32) * ((h->sop.ny + 7) / 8);
-}
-
-// copy n doubles from a host-or-device pointer into a device buffer
-int upload(gpcg_problem* h, double* dst, const double* src, size_t count) {
-    const cudaMemcpyKind k = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), k, h->st));
-    return GPCG_OK;
-}
-int upload_bytes(gpcg_problem* h, void* dst, const void* src, size_t bytes) {
-    const cudaMemcpyKind k = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CK(cudaMemcpyAsync(dst, src, bytes, k, h->st));
-    return GPCG_OK;
-}
-
-// user vector (contiguous n) <-> internal vector (rows x cols at pitch)
-int upload_vec(gpcg_problem* h, double* dst, const double* src) {
-    const cudaMemcpyKind k = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CK(cudaMemcpy2DAsync(dst, (size_t)h->pitch * sizeof(double), src, (size_t)h->cols * sizeof(double),
-                         (size_t)h->cols * sizeof(double), h->rows, k, h->st));
-    return GPCG_OK;
-}
-int download_vec(gpcg_problem* h, double* dst, const double* src) {
-    const cudaMemcpyKind k = is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    CK(cudaMemcpy2DAsync(dst, (size_t)h->cols * sizeof(double), src, (size_t)h->pitch * sizeof(double),
-                         (size_t)h->cols * sizeof(double), h->rows, k, h->st));
-    return GPCG_OK;
-}
-
-int count_nonfinite(gpcg_problem* h, const double* a, long long cnt, double* out) {
-    const int g = (int)std::min<long long>((cnt + kThreads - 1) / kThreads, (long long)h->sms * 4);
-    k_count_nonfinite<<<std::max(g, 1), kThreads, 0, h->st>>>(cnt, a, h->dS, h->red());
+    if (h->nranks > 1)
+        NK(nccl_api()->AllReduce(h->red_tot, h->red_tot, (size_t)ns, ncclDouble, ncclSum, h->comm, h->st));
+    k_finalize<<<1, 32, 0, h->st>>>(h->red_tot, h->dS, a);
+    h->launches++;
     CKLAUNCH();
-    int rc = sync_scal(h);
-    if (rc) return rc;
-    *out = h->hS->r0;
+    return GPCG_OK;
+}
+FinArgs fin(int kind) {
+    FinArgs a;
+    memset(&a, 0, sizeof a);
+    a.kind = kind;
+    return a;
+}
+
+// ---------------------------------------------------------------- halo exchange (8(e))
+// A row-structured per-slab array: row r of slab s starts at base(s) + r*row_elems
+// (r may be negative: ghost rows).  Ghost rows [-glo, 0) come from the lower
+// neighbour's rows [lo_end - glo, lo_end) (lo_end = its rows); ghost rows
+// [top, top + ghi) (top = rows + top_extra) come from the upper neighbour's rows
+// [hi_begin, hi_begin + ghi).  Vectors: top_extra = hi_begin = 0; y-face rows
+// (rows + 1 per slab): 1.
+struct RowArray {
+    char* (*base)(gpcg_problem*, Slab&, int);   // origin (row 0) of slab s for array id
+    int id;
+    size_t row_elems, esize;
+    ncclDataType_t ntype;
+    int top_extra, hi_begin;
+};
+
+char* vec_base(gpcg_problem*, Slab& s, int id) { return reinterpret_cast<char*>(s.v[id]); }
+char* msk_base(gpcg_problem*, Slab& s, int id) { return reinterpret_cast<char*>(s.m[id]); }
+
+int exchange_arrays(gpcg_problem* h, const RowArray* arr, int na) {
+    bool remote = false;
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        for (int k = 0; k < na; ++k) {
+            const RowArray& A = arr[k];
+            const size_t rb = A.row_elems * A.esize;
+            char* me = A.base(h, S, A.id);
+            if (S.nb_lo >= 0 && S.glo > 0) {
+                Slab& N = h->slabs[S.nb_lo];
+                const char* src = A.base(h, N, A.id) + (long long)(N.rows - S.glo) * (long long)rb;
+                CK(cudaMemcpyAsync(me - (long long)S.glo * rb, src, S.glo * rb, cudaMemcpyDeviceToDevice, h->st));
+            }
+            if (S.nb_hi >= 0 && S.ghi > 0) {
+                Slab& N = h->slabs[S.nb_hi];
+                const char* src = A.base(h, N, A.id) + (long long)A.hi_begin * (long long)rb;
+                CK(cudaMemcpyAsync(me + (long long)(S.rows + A.top_extra) * rb, src, S.ghi * rb,
+                                   cudaMemcpyDeviceToDevice, h->st));
+            }
+            if (S.nb_lo == NB_REMOTE || S.nb_hi == NB_REMOTE) remote = true;
+        }
+    }
+    if (!remote) return GPCG_OK;
+    const NcclApi* N = nccl_api();
+    NK(N->GroupStart());
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        for (int k = 0; k < na; ++k) {
+            const RowArray& A = arr[k];
+            const size_t rb = A.row_elems;      // elements
+            char* me = A.base(h, S, A.id);
+            const long long eb = (long long)A.esize;
+            if (S.nb_lo == NB_REMOTE) {
+                if (S.send_lo > 0)
+                    NK(N->Send(me + (long long)A.hi_begin * rb * eb, S.send_lo * rb, A.ntype, h->rank - 1, h->comm, h->st));
+                if (S.glo > 0)
+                    NK(N->Recv(me - (long long)S.glo * rb * eb, S.glo * rb, A.ntype, h->rank - 1, h->comm, h->st));
+            }
+            if (S.nb_hi == NB_REMOTE) {
+                if (S.send_hi > 0)
+                    NK(N->Send(me + (long long)(S.rows - S.send_hi) * rb * eb, S.send_hi * rb, A.ntype, h->rank + 1,
+                               h->comm, h->st));
+                if (S.ghi > 0)
+                    NK(N->Recv(me + (long long)(S.rows + A.top_extra) * rb * eb, S.ghi * rb, A.ntype, h->rank + 1,
+                               h->comm, h->st));
+            }
+        }
+    }
+    NK(N->GroupEnd());
+    return GPCG_OK;
+}
+
+bool has_ghosts(const gpcg_problem* h) { return h->nslabs() > 1 || h->nranks > 1; }
+
+int exchange(gpcg_problem* h, std::initializer_list<int> vecs, std::initializer_list<int> msks = {}) {
+    if (!has_ghosts(h)) return GPCG_OK;
+    RowArray arr[8];
+    int na = 0;
+    for (int id : vecs)
+        arr[na++] = RowArray{vec_base, id, (size_t)h->pitch, sizeof(double), ncclDouble, 0, 0};
+    for (int id : msks)
+        arr[na++] = RowArray{msk_base, id, (size_t)h->pitch, 1, ncclUint8, 0, 0};
+    return exchange_arrays(h, arr, na);
+}
+
+// ---------------------------------------------------------------- user vectors <-> slabs
+int copy_kind(const void* p, bool to_device) {
+    const bool dev = is_device_ptr(p);
+    return to_device ? (dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice)
+                     : (dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+}
+
+// the rank's contiguous user vector (n_local entries) -> vector id of every slab (owned rows)
+int upload_vec(gpcg_problem* h, int id, const double* src) {
+    const cudaMemcpyKind k = (cudaMemcpyKind)copy_kind(src, true);
+    const size_t cols = h->is_csr ? 1 : (size_t)h->nx;
+    for (Slab& S : h->slabs)
+        CK(cudaMemcpy2DAsync(S.v[id], (size_t)h->pitch * sizeof(double), src + (long long)S.uoff * cols,
+                             cols * sizeof(double), cols * sizeof(double), S.rows, k, h->st));
+    return GPCG_OK;
+}
+int download_vec(gpcg_problem* h, double* dst, int id) {
+    const cudaMemcpyKind k = (cudaMemcpyKind)copy_kind(dst, false);
+    const size_t cols = h->is_csr ? 1 : (size_t)h->nx;
+    for (Slab& S : h->slabs)
+        CK(cudaMemcpy2DAsync(dst + (long long)S.uoff * cols, cols * sizeof(double), S.v[id],
+                             (size_t)h->pitch * sizeof(double), cols * sizeof(double), S.rows, k, h->st));
     return GPCG_OK;
 }
 
@@ -211,23 +388,25 @@ void free_all(gpcg_problem* h) {
     if (!h) return;
     cudaSetDevice(h->dev);
     if (h->st) cudaStreamSynchronize(h->st);
-    void* ptrs[] = {h->wx, h->wy, h->shift, h->rp, h->ci, h->val, h->b, h->l, h->u,
-                    h->Y[0], h->Y[1], h->G[0], h->G[1], h->M[0], h->M[1], h->Mcg, h->W, h->P,
-                    h->Rho[0], h->Rho[1], h->Q[0], h->Q[1], h->S2[0], h->S2[1],
-                    h->stage_in, h->stage_out, h->dS, h->partials, h->counter};
-    for (void* p : ptrs)
+    for (Slab& S : h->slabs) {
+        for (double* p : S.vb) if (p) cudaFree(p);
+        for (unsigned char* p : S.mb) if (p) cudaFree(p);
+        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.rp, (void*)S.ci, (void*)S.val,
+                        (void*)S.partials, (void*)S.counter})
+            if (p) cudaFree(p);
+    }
+    for (void* p : {(void*)h->red_all, (void*)h->red_tot, (void*)h->lu0, (void*)h->dS})
         if (p) cudaFree(p);
     if (h->hS) cudaFreeHost(h->hS);
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
-    if (h->ev_sync) cudaEventDestroy(h->ev_sync);
-    if (h->ev_a) cudaEventDestroy(h->ev_a);
-    if (h->ev_b) cudaEventDestroy(h->ev_b);
-    if (h->ev_c0) cudaEventDestroy(h->ev_c0);
-    if (h->ev_c1) cudaEventDestroy(h->ev_c1);
+    if (h->comm && nccl_api()) nccl_api()->CommDestroy(h->comm);
+    for (cudaEvent_t e : {h->ev_sync, h->ev_a, h->ev_b, h->ev_c0, h->ev_c1})
+        if (e) cudaEventDestroy(e);
     if (h->st) cudaStreamDestroy(h->st);
     delete h;
 }
 
+// ---------------------------------------------------------------- geometry
 constexpr int kMarchTY = 16;
 
 MarchGeom march_geom(int nx, int ny, int H) {
@@ -240,9 +419,6 @@ MarchGeom march_geom(int nx, int ny, int H) {
 int march_grid(const MarchGeom& g) {     // one work item per warp
     const long long items = (long long)g.nstrips * g.nchunks;
     return (int)std::max<long long>(1, (items + kMarchThreads / 32 - 1) / (kMarchThreads / 32));
-}
-long long march_grid_bound(const gpcg_problem* h) {
-    return std::max(march_grid(h->mg1), march_grid(h->mg2));
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
@@ -257,16 +433,20 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
     return fn;
 }
 
-// 2-D tensor map over an internal (pitched) stencil array; out-of-grid elements read as 0
-int make_map(gpcg_problem* h, CUtensorMap* m, const void* ptr, bool u8, int bw, int bh) {
+// 2-D tensor map over a slab array: rows [-glo, rows+ghi) (owned + ghost); elements outside the
+// tensor read as 0 (the Dirichlet boundary)
+int make_map(gpcg_problem* h, const Slab& S, CUtensorMap* m, const void* origin, bool u8, int bw, int bh) {
+    if (bw * (u8 ? 1 : 8) % 16 != 0) return set_err(GPCG_EINVAL, "internal: TMA box row not a multiple of 16 B");
     auto enc = tma_encode_fn();
     if (!enc) return set_err(GPCG_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    const cuuint64_t dims[2] = {(cuuint64_t)h->cols, (cuuint64_t)h->rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)h->pitch * (u8 ? 1 : 8)};
+    const long long es = u8 ? 1 : 8;
+    const char* base = static_cast<const char*>(origin) - (long long)S.glo * h->pitch * es;
+    const cuuint64_t dims[2] = {(cuuint64_t)h->nx, (cuuint64_t)(S.glo + S.rows + S.ghi)};
+    const cuuint64_t strides[1] = {(cuuint64_t)h->pitch * es};
     const cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
-    const cuuint32_t es[2] = {1, 1};
+    const cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
-                     const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     const_cast<char*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(GPCG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return GPCG_OK;
@@ -278,59 +458,81 @@ int set_smem(K kernel, int bytes) {
     return GPCG_OK;
 }
 
-// Build the TMA tile path for a broadcast-face stencil handle (C0/C2/C3 family).
+// TMA tile path for a broadcast-face stencil (C0/C2/C3 family)
 int setup_tile(gpcg_problem* h) {
-    int rc;
-    for (int k = 0; k < 2; ++k) {
-        if ((rc = make_map(h, &h->tmY[k], h->Y[k], false, TBW, TBH))) return rc;
-        if ((rc = make_map(h, &h->tmG[k], h->G[k], false, TBW, TBH))) return rc;
-        if ((rc = make_map(h, &h->tmRho[k], h->Rho[k], false, TBW, TBH))) return rc;
-        if ((rc = make_map(h, &h->tmP[k], h->Q[k], false, TBW, TBH))) return rc;
-        if ((rc = make_map(h, &h->tmM[k], h->M[k], true, MBW, TBH))) return rc;
-    }
-    if ((rc = make_map(h, &h->tmW, h->W, false, TBW, TBH))) return rc;
-    if ((rc = make_map(h, &h->tmWc, h->W, false, TOX, TOY))) return rc;
-    if ((rc = make_map(h, &h->tmB, h->b, false, TBW, TBH))) return rc;
-    if ((rc = make_map(h, &h->tmL, h->l, false, TBW, TBH))) return rc;
-    if ((rc = make_map(h, &h->tmU, h->u, false, TBW, TBH))) return rc;
-    if ((rc = make_map(h, &h->tmMcg, h->Mcg, true, MBW, TBH))) return rc;
-    if ((rc = make_map(h, &h->tmStage, h->stage_in, false, TBW, TBH))) return rc;
-    h->tg = TileGeom{h->cols, h->rows, h->pitch, (h->cols + TOX - 1) / TOX, (h->rows + TOY - 1) / TOY};
-    const int ntiles = h->tg.ntx * h->tg.nty;
-    if ((rc = set_smem(k3_cg_iter<2>, CgStage<2>::kSmem))) return rc;
-    if ((rc = set_smem(k3_accept<true>, AccStage<true>::kSmem))) return rc;
-    if ((rc = set_smem(k3_accept<false>, AccStage<false>::kSmem))) return rc;
-    if ((rc = set_smem(k3_search<true, true>, SrchStage<true, true>::kSmem))) return rc;
-    if ((rc = set_smem(k3_search<true, false>, SrchStage<true, false>::kSmem))) return rc;
-    if ((rc = set_smem(k3_search<false, true>, SrchStage<false, true>::kSmem))) return rc;
-    if ((rc = set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem))) return rc;
+    RC(set_smem(k3_cg_iter<2>, CgStage<2>::kSmem));
+    RC(set_smem(k3_accept<true>, AccStage<true>::kSmem));
+    RC(set_smem(k3_accept<false>, AccStage<false>::kSmem));
+    RC(set_smem(k3_search<true, true>, SrchStage<true, true>::kSmem));
+    RC(set_smem(k3_search<true, false>, SrchStage<true, false>::kSmem));
+    RC(set_smem(k3_search<false, true>, SrchStage<false, true>::kSmem));
+    RC(set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem));
+    RC(set_smem(k4_cg_iter, m4::kSmem));
     auto resident = [&](auto kernel, int smem) {
         int nb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kTileThreads, smem);
         return std::max(1, nb) * h->sms;
     };
-    h->grid_t_cg = std::min(ntiles, resident(k3_cg_iter<2>, CgStage<2>::kSmem));
-    h->grid_t_acc = std::min(ntiles, h->sb ? resident(k3_accept<true>, AccStage<true>::kSmem)
-                                            : resident(k3_accept<false>, AccStage<false>::kSmem));
-    h->grid_t_srch = std::min(ntiles, h->sb ? resident(k3_search<true, true>, SrchStage<true, true>::kSmem)
-                                             : resident(k3_search<false, true>, SrchStage<false, true>::kSmem));
+    const int r_cg = resident(k3_cg_iter<2>, CgStage<2>::kSmem);
+    const int r_acc = h->sb ? resident(k3_accept<true>, AccStage<true>::kSmem)
+                            : resident(k3_accept<false>, AccStage<false>::kSmem);
+    const int r_srch = h->sb ? resident(k3_search<true, true>, SrchStage<true, true>::kSmem)
+                             : resident(k3_search<false, true>, SrchStage<false, true>::kSmem);
+    int nb4 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb4, k4_cg_iter, m4::kThreads, m4::kSmem);
+    const int r4 = std::max(1, nb4) * h->sms;
+    for (Slab& S : h->slabs) {
+        for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
+            RC(make_map(h, S, &S.tm[id], S.v[id], false, TBW, TBH));
+        for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.tmm[k], S.m[k], true, MBW, TBH));
+        RC(make_map(h, S, &S.tmWc, S.v[VW], false, TOX, TOY));
+        S.tg = TileGeom{h->nx, S.rows, h->pitch, (h->nx + TOX - 1) / TOX, (S.rows + TOY - 1) / TOY, -S.glo,
+                        S.rows + S.ghi};
+        const int ntiles = S.tg.ntx * S.tg.nty;
+        // k4: bands of 112 columns, each split into nsegs row segments: one item per resident CTA
+        for (int k = 0; k < 2; ++k) {
+            RC(make_map(h, S, &S.t4rho[k], S.v[vrho(k)], false, m4::kBW, m4::kBR));
+            RC(make_map(h, S, &S.t4p[k], S.v[vq(k)], false, m4::kBW, m4::kBR));
+        }
+        RC(make_map(h, S, &S.t4w, S.v[VW], false, m4::kOut, m4::kBR));
+        RC(make_map(h, S, &S.t4m, S.m[MKCG], true, m4::kMW, m4::kBR));
+        S.bg.nbands = (h->nx + m4::kOut - 1) / m4::kOut;
+        S.bg.nsegs = std::max(1, std::min(r4 / S.bg.nbands, (S.rows + 15) / 16));
+        S.bg.seg = (S.rows + S.bg.nsegs - 1) / S.bg.nsegs;
+        S.bg.nsegs = (S.rows + S.bg.seg - 1) / S.bg.seg;
+        S.bg.rlo = -S.glo;
+        S.grid4 = std::min(S.bg.nbands * S.bg.nsegs, r4);
+        S.grid_t_cg = std::min(ntiles, r_cg);
+        S.grid_t_acc = std::min(ntiles, r_acc);
+        S.grid_t_srch = std::min(ntiles, r_srch);
+    }
     h->tile = true;
     return GPCG_OK;
 }
 
-const CUtensorMap* map_of(gpcg_problem* h, const void* p) {
-    for (int k = 0; k < 2; ++k) {
-        if (p == h->Y[k]) return &h->tmY[k];
-        if (p == h->G[k]) return &h->tmG[k];
-        if (p == h->M[k]) return &h->tmM[k];
-    }
-    if (p == h->W) return &h->tmW;
-    if (p == h->stage_in) return &h->tmStage;
-    return nullptr;
+// ---------------------------------------------------------------- create (common part)
+// Slab layout of the rank's rows [0, rows_rank): nsl balanced contiguous slabs.
+void partition(long long total, int parts, int k, long long* b, long long* e) {
+    const long long q = total / parts, r = total % parts;
+    *b = k * q + std::min<long long>(k, r);
+    *e = *b + q + (k < r ? 1 : 0);
 }
 
-// common part of create: device, streams, vectors, bounds, validation
-int create_common(gpcg_problem* h, void* stream, const double* b, const double* l, const double* u) {
+int setup_comm(gpcg_problem* h, const gpcg_dist* d) {
+    h->rank = d ? d->rank : 0;
+    h->nranks = d ? d->nranks : 1;
+    if (h->nranks > 1) {
+        const NcclApi* N = nccl_api();
+        if (!N) return set_err(GPCG_ENCCL, "libnccl.so.2 not loadable: the multi-rank path needs NCCL");
+        if (!d->nccl_id) return set_err(GPCG_EINVAL, "nccl_id is NULL with nranks > 1");
+        ncclUniqueId id;
+        memcpy(&id, d->nccl_id, sizeof id);
+        NK(N->CommInitRank(&h->comm, h->nranks, id, h->rank));
+    }
+    return GPCG_OK;
+}
+
+int create_streams(gpcg_problem* h, void* stream) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -347,191 +549,256 @@ int create_common(gpcg_problem* h, void* stream, const double* b, const double* 
     CK(cudaEventCreate(&h->ev_c1));
     CK(cudaEventRecord(h->ev_sync, h->user));
     CK(cudaStreamWaitEvent(h->st, h->ev_sync, 0));
-    const size_t nb = (size_t)h->nalloc * sizeof(double);
-    CK(cudaMalloc(&h->b, nb));
-    CK(cudaMalloc(&h->l, nb));
-    CK(cudaMalloc(&h->u, nb));
-    for (int k = 0; k < 2; ++k) {
-        CK(cudaMalloc(&h->Y[k], nb));
-        CK(cudaMalloc(&h->G[k], nb));
-        CK(cudaMalloc(&h->M[k], (size_t)h->nalloc));
-        CK(cudaMemsetAsync(h->M[k], 0, (size_t)h->nalloc, h->st));
-        if (k == 0) {
-            CK(cudaMalloc(&h->Mcg, (size_t)h->nalloc));
-            CK(cudaMemsetAsync(h->Mcg, 0, (size_t)h->nalloc, h->st));
+    return GPCG_OK;
+}
+
+// slab vectors, masks, scratch; b, l, u uploaded; inputs validated (globally)
+int create_vectors(gpcg_problem* h, const double* b, const double* l, const double* u) {
+    for (Slab& S : h->slabs) {
+        S.nalloc = (long long)(S.glo + S.rows + S.ghi) * h->pitch;
+        const size_t nb = (size_t)S.nalloc * sizeof(double);
+        const long long off = (long long)S.glo * h->pitch;
+        for (int k = 0; k < NVEC; ++k) {
+            CK(cudaMalloc(&S.vb[k], nb));
+            CK(cudaMemsetAsync(S.vb[k], 0, nb, h->st));     // padding columns and boundary ghosts stay 0
+            S.v[k] = S.vb[k] + off;
         }
-        CK(cudaMalloc(&h->Rho[k], nb));
-        CK(cudaMalloc(&h->Q[k], nb));
-        CK(cudaMalloc(&h->S2[k], nb));
+        for (int k = 0; k < NMSK; ++k) {
+            CK(cudaMalloc(&S.mb[k], (size_t)S.nalloc));
+            CK(cudaMemsetAsync(S.mb[k], 0, (size_t)S.nalloc, h->st));
+            S.m[k] = S.mb[k] + off;
+        }
+        // partial sums of the largest grid any kernel of this slab uses (grid-stride generic kernels
+        // are capped at 16 blocks/SM; march grids are one warp per item)
+        long long gmax = (long long)h->sms * 16;
+        if (!h->is_csr) {
+            S.mg1 = march_geom(h->nx, S.rows, 1);
+            S.mg2 = march_geom(h->nx, S.rows, 2);
+            S.grid_m1 = march_grid(S.mg1);
+            S.grid_m2 = march_grid(S.mg2);
+            gmax = std::max<long long>(gmax, std::max(S.grid_m1, S.grid_m2));
+        }
+        CK(cudaMalloc(&S.partials, (size_t)kMaxSums * gmax * sizeof(double)));
+        CK(cudaMalloc(&S.counter, sizeof(unsigned int)));
+        CK(cudaMemsetAsync(S.counter, 0, sizeof(unsigned int), h->st));
     }
-    CK(cudaMalloc(&h->W, nb));
-    CK(cudaMalloc(&h->P, nb));
-    CK(cudaMalloc(&h->stage_in, nb));
-    CK(cudaMalloc(&h->stage_out, nb));
+    CK(cudaMalloc(&h->red_all, (size_t)kMaxSums * h->nslabs() * sizeof(double)));
+    CK(cudaMalloc(&h->red_tot, (size_t)kMaxSums * sizeof(double)));
+    CK(cudaMemsetAsync(h->red_tot, 0, (size_t)kMaxSums * sizeof(double), h->st));
+    CK(cudaMalloc(&h->lu0, 2 * sizeof(double)));
     CK(cudaMalloc(&h->dS, sizeof(Scal)));
     CK(cudaMemsetAsync(h->dS, 0, sizeof(Scal), h->st));
     CK(cudaMallocHost(&h->hS, sizeof(Scal)));
-    // partial sums of the largest grid any kernel of this handle uses (grid-stride
-    // generic kernels are capped at 16 blocks/SM; march grids are one warp per item)
-    long long gmax = (long long)h->sms * 16;
-    if (!h->is_csr) gmax = std::max<long long>(gmax, march_grid_bound(h));
-    CK(cudaMalloc(&h->partials, (size_t)kMaxSums * gmax * sizeof(double)));
-    CK(cudaMalloc(&h->counter, sizeof(unsigned int)));
-    CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
-    int rc;
-    for (double* v : {h->b, h->l, h->u, h->Y[0], h->Y[1], h->G[0], h->G[1], h->W, h->P, h->Rho[0], h->Rho[1],
-                      h->Q[0], h->Q[1], h->S2[0], h->S2[1], h->stage_in, h->stage_out})
-        CK(cudaMemsetAsync(v, 0, nb, h->st));        // padding columns stay 0
-    if ((rc = upload_vec(h, h->b, b))) return rc;
-    if ((rc = upload_vec(h, h->l, l))) return rc;
-    if ((rc = upload_vec(h, h->u, u))) return rc;
-    // validation: l <= u, no NaN / inf in b, l != +inf, u != -inf; constant bounds?
-    const int g = std::max(1, std::min((h->n + kThreads - 1) / kThreads, h->sms * 4));
-    k_check_inputs<<<g, kThreads, 0, h->st>>>(h->cols, h->rows, h->pitch, h->b, h->l, h->u, h->dS, h->red());
-    CKLAUNCH();
-    if ((rc = sync_scal(h))) return rc;
+    RC(upload_vec(h, VB, b));
+    RC(upload_vec(h, VL, l));
+    RC(upload_vec(h, VU, u));
+    RC(exchange(h, {VB, VL, VU}));
+    // validation: l <= u, no NaN / inf in b, l != +inf, u != -inf; constant bounds (vs the global
+    // first pair, broadcast from rank 0)?
+    CK(cudaMemcpyAsync(h->lu0, h->slabs[0].v[VL], sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->lu0 + 1, h->slabs[0].v[VU], sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    if (h->nranks > 1) NK(nccl_api()->Broadcast(h->lu0, h->lu0, 2, ncclDouble, 0, h->comm, h->st));
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const int cols = h->is_csr ? S.rows : h->nx, rows = h->is_csr ? 1 : S.rows;
+        const int g = std::max(1, (int)std::min<long long>(((long long)S.rows * (h->is_csr ? 1 : h->nx) + kThreads - 1) / kThreads,
+                                                           (long long)h->sms * 4));
+        k_check_inputs<<<g, kThreads, 0, h->st>>>(cols, rows, h->is_csr ? S.rows : h->pitch, S.v[VB], S.v[VL], S.v[VU],
+                                                  h->lu0, h->dS, h->red(s));
+        CKLAUNCH();
+    }
+    RC(finish_reduce(h, fin(FIN_R2), 2));
+    RC(sync_scal(h));
     if (h->hS->r0 != 0.0)
-        return set_err(GPCG_EINVAL, "%.0f entries violate l <= u (or NaN/inf in b, l = +inf, u = -inf)",
-                       h->hS->r0);
+        return set_err(GPCG_EINVAL, "%.0f entries violate l <= u (or NaN/inf in b, l = +inf, u = -inf)", h->hS->r0);
     h->sb = (h->hS->r1 == 0.0);
     double lu[2];
-    CK(cudaMemcpy(&lu[0], h->l, sizeof(double), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&lu[1], h->u, sizeof(double), cudaMemcpyDeviceToHost));
-    h->bounds = Bounds{h->l, h->u, lu[0], lu[1]};
+    CK(cudaMemcpy(lu, h->lu0, sizeof lu, cudaMemcpyDeviceToHost));
+    h->lc = lu[0];
+    h->uc = lu[1];
     h->prm = gpcg_params_default();
     return GPCG_OK;
 }
 
-// ---------------------------------------------------------------- launches
-int launch_accept(gpcg_problem* h, const double* y_in, const double* dir, double sgn,
-                  const unsigned char* mask_prev, double* y_out, double* g_out, unsigned char* m_out) {
-    if (h->tile && (h->tile_mask & 1)) {   // TMA tile path
-        const CUtensorMap* my = map_of(h, y_in);
-        const CUtensorMap* md = dir ? map_of(h, dir) : my;
-        const CUtensorMap* mp = mask_prev ? map_of(h, mask_prev) : &h->tmM[0];
-        if (!my || !md || !mp) return set_err(GPCG_ECUDA, "internal: no tensor map for an accept operand");
-        if (h->sb)
-            k3_accept<true><<<h->grid_t_acc, kTileThreads, AccStage<true>::kSmem, h->st>>>(
-                h->sop, h->tg, h->bounds, *my, *md, h->tmB, h->tmL, h->tmU, *mp, dir ? 1 : 0, sgn,
-                mask_prev ? 1 : 0, y_out, g_out, m_out, h->dS, h->red());
-        else
-            k3_accept<false><<<h->grid_t_acc, kTileThreads, AccStage<false>::kSmem, h->st>>>(
-                h->sop, h->tg, h->bounds, *my, *md, h->tmB, h->tmL, h->tmU, *mp, dir ? 1 : 0, sgn,
-                mask_prev ? 1 : 0, y_out, g_out, m_out, h->dS, h->red());
-        h->launches++;
+// count of non-finite values of a per-slab array (owned part), summed over slabs and ranks
+int count_nonfinite(gpcg_problem* h, const double* const* arrs, const long long* cnts, double* out) {
+    for (int s = 0; s < h->nslabs(); ++s) {
+        const int g = (int)std::max<long long>(1, std::min<long long>((cnts[s] + kThreads - 1) / kThreads,
+                                                                      (long long)h->sms * 4));
+        k_count_nonfinite<<<g, kThreads, 0, h->st>>>(cnts[s], arrs[s], h->dS, h->red(s));
         CKLAUNCH();
-        return GPCG_OK;
     }
-    if (!h->is_csr && !h->generic) {   // stencil: accept + regrad + mask + counts + next Cauchy step in one sweep
-        auto go = [&](auto sbt, auto bct) {
-            constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value;
-            k2_accept<SB, BC><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->bounds, y_in, dir, sgn,
-                                                                       h->b, mask_prev, y_out, g_out, m_out, h->dS,
-                                                                       h->red());
-        };
-        if (h->sb) { if (h->bc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
-        else { if (h->bc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
-        h->launches++;
-        CKLAUNCH();
-        return GPCG_OK;
-    }
-    with_op(h, [&](auto& op, auto sbt) {
-        using Op = std::decay_t<decltype(op)>;
-        constexpr bool SB = decltype(sbt)::value;
-        k_accept<Op, SB><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y_in, dir, sgn, h->b, mask_prev,
-                                                          y_out, g_out, m_out, h->dS, h->red());
-    });
-    h->launches++;
-    CKLAUNCH();
+    RC(finish_reduce(h, fin(FIN_R2), 2));
+    RC(sync_scal(h));
+    *out = h->hS->r0;
     return GPCG_OK;
 }
 
-int launch_cauchy(gpcg_problem* h, const double* y, const double* g) {
-    if (!h->is_csr && !h->generic) return GPCG_OK;     // computed by the preceding k2_accept sweep
-    with_op(h, [&](auto& op, auto sbt) {
-        using Op = std::decay_t<decltype(op)>;
-        constexpr bool SB = decltype(sbt)::value;
-        k_cauchy<Op, SB><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, h->dS, h->red());
-    });
-    h->launches++;
-    CKLAUNCH();
+// slab rows of the rank's rows; neighbours; ghost widths (stencil: 2)
+int layout_slabs(gpcg_problem* h, long long rows_rank, int nsl, int ghost) {
+    if (nsl < 1 || nsl > 64) return set_err(GPCG_EINVAL, "local_slabs = %d out of range [1, 64]", nsl);
+    h->slabs.resize(nsl);
+    for (int s = 0; s < nsl; ++s) {
+        Slab& S = h->slabs[s];
+        long long b, e;
+        partition(rows_rank, nsl, s, &b, &e);
+        S.uoff = (int)b;
+        S.row0 = (int)b;
+        S.rows = (int)(e - b);
+        S.nb_lo = s > 0 ? s - 1 : (h->rank > 0 ? NB_REMOTE : NB_NONE);
+        S.nb_hi = s < nsl - 1 ? s + 1 : (h->rank < h->nranks - 1 ? NB_REMOTE : NB_NONE);
+        S.glo = S.nb_lo != NB_NONE ? ghost : 0;
+        S.ghi = S.nb_hi != NB_NONE ? ghost : 0;
+        S.send_lo = S.glo;
+        S.send_hi = S.ghi;
+        const int need = (S.nb_lo != NB_NONE || S.nb_hi != NB_NONE) ? std::max(ghost, 1) : 1;
+        if (S.rows < need) return set_err(GPCG_EINVAL, "slab %d has %d rows (need >= %d)", s, S.rows, need);
+    }
+    h->deferred = has_ghosts(h);
     return GPCG_OK;
+}
+
+// ---------------------------------------------------------------- launches (every slab)
+int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev, int y_out, int g_out, int m_out) {
+    const bool use_tile = h->tile && (h->tile_mask & 1);
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const Bounds B = h->bounds(S);
+        const RedScratch R = h->red(s);
+        if (use_tile) {
+            const CUtensorMap& md = S.tm[dir >= 0 ? dir : y_in];
+            const CUtensorMap& mp = S.tmm[mask_prev >= 0 ? mask_prev : MK0];
+            if (h->sb)
+                k3_accept<true><<<S.grid_t_acc, kTileThreads, AccStage<true>::kSmem, h->st>>>(
+                    S.sop, S.tg, B, S.tm[y_in], md, S.tm[VB], S.tm[VL], S.tm[VU], mp, dir >= 0 ? 1 : 0, sgn,
+                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R);
+            else
+                k3_accept<false><<<S.grid_t_acc, kTileThreads, AccStage<false>::kSmem, h->st>>>(
+                    S.sop, S.tg, B, S.tm[y_in], md, S.tm[VB], S.tm[VL], S.tm[VU], mp, dir >= 0 ? 1 : 0, sgn,
+                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R);
+        } else if (!h->is_csr && !h->generic) {   // accept + regrad + mask + counts + next Cauchy step, one sweep
+            const double* dp = dir >= 0 ? S.v[dir] : nullptr;
+            const unsigned char* mp = mask_prev >= 0 ? S.m[mask_prev] : nullptr;
+            auto go = [&](auto sbt, auto bct) {
+                constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value;
+                k2_accept<SB, BC><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, B, S.v[y_in], dp, sgn, S.v[VB],
+                                                                          mp, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R);
+            };
+            if (h->sb) { if (h->bc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+            else { if (h->bc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else {
+            const double* dp = dir >= 0 ? S.v[dir] : nullptr;
+            const unsigned char* mp = mask_prev >= 0 ? S.m[mask_prev] : nullptr;
+            auto go = [&](auto& op, auto sbt) {
+                using Op = std::decay_t<decltype(op)>;
+                constexpr bool SB = decltype(sbt)::value;
+                k_accept<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y_in], dp, sgn, S.v[VB], mp, S.v[y_out],
+                                                                S.v[g_out], S.m[m_out], h->dS, R);
+            };
+            if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
+            else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+        }
+        h->launches++;
+        CKLAUNCH();
+    }
+    FinArgs a = fin((h->is_csr || h->generic) && !use_tile ? FIN_ACCEPT5 : FIN_ACCEPT);
+    a.has_dir = dir >= 0 ? 1 : 0;
+    RC(finish_reduce(h, a, a.kind == FIN_ACCEPT ? 6 : 5));
+    return exchange(h, {y_out, g_out}, {m_out});
+}
+
+bool fused_cauchy(const gpcg_problem* h) { return !h->is_csr && !h->generic; }
+
+int launch_cauchy(gpcg_problem* h, int y, int g) {
+    if (fused_cauchy(h)) return GPCG_OK;     // computed by the preceding accept sweep
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const Bounds B = h->bounds(S);
+        auto go = [&](auto& op, auto sbt) {
+            using Op = std::decay_t<decltype(op)>;
+            constexpr bool SB = decltype(sbt)::value;
+            k_cauchy<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], h->dS, h->red(s));
+        };
+        if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
+        else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+        h->launches++;
+        CKLAUNCH();
+    }
+    return finish_reduce(h, fin(FIN_CAUCHY), 2);
 }
 
 // step sizes per projected-search sweep: the first sweep evaluates search_k
 // (2 or 8 instantiated), later sweeps 8
 int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
 
-int launch_search(gpcg_problem* h, const double* y, const double* g, const double* dir, double sgn,
-                  int use_alpha0, int h0, int K) {
+int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_alpha0, int h0, int K) {
     const double mu = h->prm.mu;
-    if (h->tile && (h->tile_mask & 2) && K == 2) {   // TMA tile path (first sweep); retries use the column march
-        const CUtensorMap* my = map_of(h, y);
-        const CUtensorMap* md = map_of(h, dir);
-        const CUtensorMap* mg = map_of(h, g);
-        if (!my || !md || !mg) return set_err(GPCG_ECUDA, "internal: no tensor map for a search operand");
-        const bool dg = (dir == g);
-        auto go = [&](auto sbt, auto dgt) {
-            constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
-            k3_search<SB, DG><<<h->grid_t_srch, kTileThreads, SrchStage<SB, DG>::kSmem, h->st>>>(
-                h->sop, h->tg, h->bounds, *my, *md, *mg, h->tmL, h->tmU, sgn, use_alpha0, h0, mu, h->dS, h->red());
-        };
-        if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
-        else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+    const bool dg = (dir == g);
+    const bool use_tile = h->tile && (h->tile_mask & 2) && K == 2;   // retries use the column march
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const Bounds B = h->bounds(S);
+        const RedScratch R = h->red(s);
+        if (use_tile) {
+            auto go = [&](auto sbt, auto dgt) {
+                constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
+                k3_search<SB, DG><<<S.grid_t_srch, kTileThreads, SrchStage<SB, DG>::kSmem, h->st>>>(
+                    S.sop, S.tg, B, S.tm[y], S.tm[dir], S.tm[g], S.tm[VL], S.tm[VU], sgn, use_alpha0, h0, mu, h->dS, R);
+            };
+            if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+            else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else if (!h->is_csr && !h->generic) {
+            auto go = [&](auto sbt, auto bct, auto kt, auto dgt) {
+                constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value, DG = decltype(dgt)::value;
+                constexpr int KK = decltype(kt)::value;
+                k2_search<SB, BC, KK, DG><<<S.grid_m1, kMarchThreads, 0, h->st>>>(
+                    S.sop, S.mg1, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0, h0, mu, h->dS, R);
+            };
+            auto byk = [&](auto sbt, auto bct, auto dgt) {
+                if (K == 2) go(sbt, bct, std::integral_constant<int, 2>(), dgt);
+                else go(sbt, bct, std::integral_constant<int, 8>(), dgt);
+            };
+            auto bydg = [&](auto sbt, auto bct) {
+                if (dg) byk(sbt, bct, std::true_type()); else byk(sbt, bct, std::false_type());
+            };
+            auto bybc = [&](auto sbt) {
+                if (h->bc) bydg(sbt, std::true_type()); else bydg(sbt, std::false_type());
+            };
+            if (h->sb) bybc(std::true_type()); else bybc(std::false_type());
+        } else {
+            auto go = [&](auto& op, auto sbt) {
+                using Op = std::decay_t<decltype(op)>;
+                constexpr bool SB = decltype(sbt)::value;
+                if (K == 2)
+                    k_search<Op, SB, 2><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0,
+                                                                        h0, mu, h->dS, R);
+                else
+                    k_search<Op, SB, 8><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0,
+                                                                        h0, mu, h->dS, R);
+            };
+            if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
+            else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+        }
         h->launches++;
         CKLAUNCH();
-        return GPCG_OK;
     }
-    if (!h->is_csr && !h->generic) {
-        const bool dg = (dir == g);
-        auto go = [&](auto sbt, auto bct, auto kt, auto dgt) {
-            constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value, DG = decltype(dgt)::value;
-            constexpr int KK = decltype(kt)::value;
-            k2_search<SB, BC, KK, DG><<<h->grid_m1, kMarchThreads, 0, h->st>>>(
-                h->sop, h->mg1, h->bounds, y, g, dir, sgn, use_alpha0, h0, mu, h->dS, h->red());
-        };
-        auto byk = [&](auto sbt, auto bct, auto dgt) {
-            if (K == 2) go(sbt, bct, std::integral_constant<int, 2>(), dgt);
-            else go(sbt, bct, std::integral_constant<int, 8>(), dgt);
-        };
-        auto bydg = [&](auto sbt, auto bct) {
-            if (dg) byk(sbt, bct, std::true_type()); else byk(sbt, bct, std::false_type());
-        };
-        auto bybc = [&](auto sbt) {
-            if (h->bc) bydg(sbt, std::true_type()); else bydg(sbt, std::false_type());
-        };
-        if (h->sb) bybc(std::true_type()); else bybc(std::false_type());
-        h->launches++;
-        CKLAUNCH();
-        return GPCG_OK;
-    }
-    with_op(h, [&](auto& op, auto sbt) {
-        using Op = std::decay_t<decltype(op)>;
-        constexpr bool SB = decltype(sbt)::value;
-        if (K == 2)
-            k_search<Op, SB, 2><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, dir, sgn, use_alpha0,
-                                                                 h0, mu, h->dS, h->red());
-        else
-            k_search<Op, SB, 8><<<h->grid, kThreads, 0, h->st>>>(op, h->bounds, y, g, dir, sgn, use_alpha0,
-                                                                 h0, mu, h->dS, h->red());
-    });
-    h->launches++;
-    CKLAUNCH();
-    return GPCG_OK;
+    FinArgs a = fin(FIN_SEARCH);
+    a.K = K;
+    a.h0 = h0;
+    a.use_alpha0 = use_alpha0;
+    a.mu = mu;
+    return finish_reduce(h, a, 2 * K);
 }
 
 // one projected search + accept:  y' = P[y + alpha sgn dir], g' = A y' - b.
 // Host loops over batches of K step sizes until one is accepted.  Returns
 // GPCG_OK with *accepted_h >= 0, or GPCG_ESEARCH.
-int search_and_accept(gpcg_problem* h, int cur, const double* dir, double sgn, int use_alpha0,
-                      int* accepted_h) {
+int search_and_accept(gpcg_problem* h, int cur, int dir, double sgn, int use_alpha0, int* accepted_h) {
     const int nxt = cur ^ 1;
-    int rc;
     for (int h0 = 0, K = first_k(h); h0 < h->prm.max_halvings; h0 += K, K = 8) {
-        if ((rc = launch_search(h, h->Y[cur], h->G[cur], dir, sgn, use_alpha0, h0, K))) return rc;
-        if ((rc = launch_accept(h, h->Y[cur], dir, sgn, h->M[cur], h->Y[nxt], h->G[nxt], h->M[nxt])))
-            return rc;
-        if ((rc = sync_scal(h))) return rc;
+        RC(launch_search(h, vy(cur), vg(cur), dir, sgn, use_alpha0, h0, K));
+        RC(launch_accept(h, vy(cur), dir, sgn, mk(cur), vy(nxt), vg(nxt), mk(nxt)));
+        RC(sync_scal(h));
         // the search is skipped (s_h = -1) when the Cauchy step of y has <d, A d> <= 0;
         // after an accepted step cauchy_ok already describes the NEW point (fused sweep)
         if (h->hS->s_h < 0 && use_alpha0 && !h->hS->cauchy_ok)
@@ -546,6 +813,47 @@ int search_and_accept(gpcg_problem* h, int cur, const double* dir, double sgn, i
                    (long long)h->prm.max_halvings);
 }
 
+// one CG iteration on every slab (+ exchange + deferred finalize): captured into the graph
+int enqueue_cg_iter(gpcg_problem* h, int a) {
+    const int bb = a ^ 1;
+    const bool use_k4 = h->tile && (h->tile_mask & 8);
+    const bool use_tile = h->tile && (h->tile_mask & 4);
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const RedScratch R = h->red(s);
+        if (use_k4) {
+            k4_cg_iter<<<S.grid4, m4::kThreads, m4::kSmem, h->st>>>(S.sop, S.bg, S.t4rho[a], S.t4p[a], S.t4w, S.t4m,
+                                                                   S.v[vrho(bb)], S.v[vq(bb)], S.v[VW], h->dS, R);
+        } else if (use_tile) {
+            k3_cg_iter<2><<<S.grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
+                S.sop, S.tg, S.tm[vrho(a)], S.tm[vq(a)], S.tmWc, S.tmm[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
+                h->dS, R);
+        } else if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
+            if (h->bc)
+                k2_cg_iter<true><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, S.m[MKCG], S.v[vrho(a)],
+                                                                         S.v[vq(a)], S.v[vrho(bb)], S.v[vq(bb)],
+                                                                         S.v[VW], h->dS, R);
+            else
+                k2_cg_iter<false><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, S.m[MKCG], S.v[vrho(a)],
+                                                                          S.v[vq(a)], S.v[vrho(bb)], S.v[vq(bb)],
+                                                                          S.v[VW], h->dS, R);
+        } else {
+            auto go = [&](auto& op) {
+                using Op = std::decay_t<decltype(op)>;
+                k_cg_iter<Op><<<S.grid, kThreads, 0, h->st>>>(op, S.m[MKCG], S.v[vrho(a)], S.v[vq(a)], S.v[vs(a)],
+                                                              S.v[vrho(bb)], S.v[vq(bb)], S.v[vs(bb)], S.v[VP],
+                                                              S.v[VW], h->dS, R);
+            };
+            if (h->is_csr) go(S.cop); else go(S.sop);
+        }
+        h->launches++;
+        CKLAUNCH();
+    }
+    if (h->is_csr || h->generic) RC(exchange(h, {vrho(bb), vq(bb), vs(bb)}));
+    else RC(exchange(h, {vrho(bb), vq(bb)}));
+    return finish_reduce(h, fin(FIN_CG_ITER), 2);
+}
+
 int build_cg_graph(gpcg_problem* h, int chunk) {
     if (h->cg_exec && h->cg_exec_chunk == chunk) return GPCG_OK;
     if (h->cg_exec) {
@@ -554,31 +862,15 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     }
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < chunk; ++i) {
-        const int a = i & 1, bb = a ^ 1;
-        if (h->tile && (h->tile_mask & 4)) {
-            k3_cg_iter<2><<<h->grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
-                h->sop, h->tg, h->tmRho[a], h->tmP[a], h->tmWc, h->tmMcg, h->Rho[bb], h->Q[bb], h->W, h->dS,
-                h->red());
-            continue;
-        }
-        if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
-            if (h->bc)
-                k2_cg_iter<true><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a],
-                                                                          h->Rho[bb], h->Q[bb], h->W, h->dS, h->red());
-            else
-                k2_cg_iter<false><<<h->grid_m2, kMarchThreads, 0, h->st>>>(h->sop, h->mg2, h->Mcg, h->Rho[a], h->Q[a],
-                                                                           h->Rho[bb], h->Q[bb], h->W, h->dS, h->red());
-            continue;
-        }
-        with_op_only(h, [&](auto& op) {
-            using Op = std::decay_t<decltype(op)>;
-            k_cg_iter<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->Mcg, h->Rho[a], h->Q[a], h->S2[a],
-                                                           h->Rho[bb], h->Q[bb], h->S2[bb], h->P, h->W,
-                                                           h->dS, h->red());
-        });
-    }
+    const long long l0 = h->launches;
+    int rc = GPCG_OK;
+    for (int i = 0; i < chunk && !rc; ++i) rc = enqueue_cg_iter(h, i & 1);
+    h->launches = l0;
     cudaError_t e = cudaStreamEndCapture(h->st, &graph);
+    if (rc) {
+        if (e == cudaSuccess) cudaGraphDestroy(graph);
+        return rc;
+    }
     if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
     e = cudaGraphInstantiate(&h->cg_exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -587,34 +879,53 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     return GPCG_OK;
 }
 
+// kernels per CG iteration (for the launch count)
+int launches_per_cg_iter(const gpcg_problem* h) {
+    int n = h->nslabs();
+    if (h->deferred) n += 1 + (h->nslabs() > 1 ? 1 : 0);
+    return n;
+}
+
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
-    int rc;
-    if (!h->is_csr && !h->generic) {
-        if (h->bc)
-            k2_cg_init<true><<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg,
-                                                                      h->Rho[0], h->Q[0], h->W, eta2, cap, h->dS,
-                                                                      h->red());
-        else
-            k2_cg_init<false><<<h->grid_m1, kMarchThreads, 0, h->st>>>(h->sop, h->mg1, h->G[cur], h->M[cur], h->Mcg,
-                                                                       h->Rho[0], h->Q[0], h->W, eta2, cap, h->dS,
-                                                                       h->red());
-    } else with_op_only(h, [&](auto& op) {
-        using Op = std::decay_t<decltype(op)>;
-        k_cg_init<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->G[cur], h->M[cur], h->Mcg, h->Rho[0], h->Q[0], h->S2[0],
-                                                       h->Rho[1], h->Q[1], h->S2[1], h->P, h->W, eta2, cap,
-                                                       h->dS, h->red());
-    });
-    h->launches++;
-    CKLAUNCH();
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const RedScratch R = h->red(s);
+        if (!h->is_csr && !h->generic) {
+            if (h->bc)
+                k2_cg_init<true><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.v[vg(cur)], S.m[cur],
+                                                                         S.m[MKCG], S.v[VRHO0], S.v[VQ0], S.v[VW],
+                                                                         eta2, cap, h->dS, R);
+            else
+                k2_cg_init<false><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.v[vg(cur)], S.m[cur],
+                                                                          S.m[MKCG], S.v[VRHO0], S.v[VQ0], S.v[VW],
+                                                                          eta2, cap, h->dS, R);
+        } else {
+            auto go = [&](auto& op) {
+                using Op = std::decay_t<decltype(op)>;
+                k_cg_init<Op><<<S.grid, kThreads, 0, h->st>>>(op, S.v[vg(cur)], S.m[cur], S.m[MKCG], S.v[VRHO0],
+                                                              S.v[VQ0], S.v[VS0], S.v[VRHO1], S.v[VQ1], S.v[VS1],
+                                                              S.v[VP], S.v[VW], eta2, cap, h->dS, R);
+            };
+            if (h->is_csr) go(S.cop); else go(S.sop);
+        }
+        h->launches++;
+        CKLAUNCH();
+    }
+    FinArgs a = fin(FIN_CG_INIT);
+    a.eta2 = eta2;
+    a.cap = cap;
+    RC(finish_reduce(h, a, 2));
+    if (h->is_csr || h->generic) RC(exchange(h, {VRHO0, VQ0, VS0}, {MKCG}));
+    else RC(exchange(h, {VRHO0, VQ0}, {MKCG}));
     const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
-    if ((rc = build_cg_graph(h, chunk))) return rc;
+    RC(build_cg_graph(h, chunk));
     for (;;) {
         CK(cudaEventRecord(h->ev_c0, h->st));
         CK(cudaGraphLaunch(h->cg_exec, h->st));
         CK(cudaEventRecord(h->ev_c1, h->st));
-        h->launches += chunk;
-        if ((rc = sync_scal(h))) return rc;
+        h->launches += (long long)chunk * launches_per_cg_iter(h);
+        RC(sync_scal(h));
         if (h->hS->cg_done) break;
         // every iteration of this chunk was real: steady-state timing sample
         float ms = 0.f;
@@ -627,6 +938,299 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     if (h->hS->cg_reason == CG_NOTSPD)
         return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
                        (long long)h->hS->cg_it);
+    // the search along d = w reads w at the neighbours
+    return exchange(h, {VW});
+}
+
+int launch_objective(gpcg_problem* h, int x) {
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        if (h->is_csr)
+            k_objective<CsrOp><<<S.grid, kThreads, 0, h->st>>>(S.cop, S.v[x], S.v[VB], h->dS, h->red(s));
+        else
+            k_objective<StencilOp><<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[x], S.v[VB], h->dS, h->red(s));
+        h->launches++;
+        CKLAUNCH();
+    }
+    return finish_reduce(h, fin(FIN_R2), 2);
+}
+
+// ---------------------------------------------------------------- stencil slabs: operator
+int setup_stencil_slabs(gpcg_problem* h, const double* wx, const double* wy, const double* shift) {
+    const int nx = h->nx;
+    double bad = 0.0;
+    std::vector<const double*> arrs(h->nslabs());
+    std::vector<long long> cnts(h->nslabs());
+    const long long wx_int = h->wx_ld ? nx + 1 : 0, wy_int = h->wy_ld ? nx : 0;   // internal face layout
+    for (Slab& S : h->slabs) {
+        // wx: (glo + rows + ghi) rows of nx+1 (or one broadcast row); wy: face rows [-glo, rows + ghi]
+        const long long wxr = h->wx_ld ? (S.glo + S.rows + S.ghi) : 1;
+        const long long wyr = h->wy_ld ? (S.glo + S.rows + 1 + S.ghi) : 1;
+        CK(cudaMalloc(&S.wxb, (size_t)(wxr * (nx + 1)) * sizeof(double)));
+        CK(cudaMalloc(&S.wyb, (size_t)(wyr * nx) * sizeof(double)));
+        CK(cudaMemsetAsync(S.wxb, 0, (size_t)(wxr * (nx + 1)) * sizeof(double), h->st));
+        CK(cudaMemsetAsync(S.wyb, 0, (size_t)(wyr * nx) * sizeof(double), h->st));
+        double* wxo = S.wxb + (h->wx_ld ? (long long)S.glo * (nx + 1) : 0);
+        double* wyo = S.wyb + (h->wy_ld ? (long long)S.glo * nx : 0);
+        const cudaMemcpyKind kx = (cudaMemcpyKind)copy_kind(wx, true), ky = (cudaMemcpyKind)copy_kind(wy, true);
+        if (h->wx_ld)
+            CK(cudaMemcpy2DAsync(wxo, (size_t)(nx + 1) * sizeof(double), wx + (long long)S.uoff * h->wx_ld,
+                                 (size_t)h->wx_ld * sizeof(double), (size_t)(nx + 1) * sizeof(double), S.rows, kx, h->st));
+        else
+            CK(cudaMemcpyAsync(wxo, wx, (size_t)(nx + 1) * sizeof(double), kx, h->st));
+        if (h->wy_ld)
+            CK(cudaMemcpy2DAsync(wyo, (size_t)nx * sizeof(double), wy + (long long)S.uoff * h->wy_ld,
+                                 (size_t)h->wy_ld * sizeof(double), (size_t)nx * sizeof(double), S.rows + 1, ky, h->st));
+        else
+            CK(cudaMemcpyAsync(wyo, wy, (size_t)nx * sizeof(double), ky, h->st));
+        double* sho = nullptr;
+        if (shift) {
+            CK(cudaMalloc(&S.shb, (size_t)S.nalloc * sizeof(double)));
+            CK(cudaMemsetAsync(S.shb, 0, (size_t)S.nalloc * sizeof(double), h->st));
+            sho = S.shb + (long long)S.glo * h->pitch;
+            CK(cudaMemcpy2DAsync(sho, (size_t)h->pitch * sizeof(double), shift + (long long)S.uoff * nx,
+                                 (size_t)nx * sizeof(double), (size_t)nx * sizeof(double), S.rows,
+                                 (cudaMemcpyKind)copy_kind(shift, true), h->st));
+        }
+        S.sop = StencilOp{nx, S.rows, h->pitch, wxo, wyo, sho, wx_int, wy_int, -S.glo, S.rows + S.ghi};
+        S.grid = std::max(1, std::min(((nx + 31) / 32) * ((S.rows + 7) / 8), h->sms * 16));
+    }
+    // validation of the owned weights (all slabs, all ranks)
+    for (int pass = 0; pass < 3; ++pass) {
+        for (int s = 0; s < h->nslabs(); ++s) {
+            Slab& S = h->slabs[s];
+            if (pass == 0) { arrs[s] = S.sop.wx; cnts[s] = h->wx_ld ? (long long)S.rows * (nx + 1) : nx + 1; }
+            if (pass == 1) { arrs[s] = S.sop.wy; cnts[s] = h->wy_ld ? (long long)(S.rows + 1) * nx : nx; }
+            if (pass == 2) { arrs[s] = S.shb ? S.shb : S.v[VB]; cnts[s] = S.shb ? S.nalloc : 0; }
+        }
+        if (pass == 2 && !shift) break;
+        double t = 0.0;
+        RC(count_nonfinite(h, arrs.data(), cnts.data(), &t));
+        bad += t;
+    }
+    if (bad != 0.0) return set_err(GPCG_EINVAL, "%.0f non-finite stencil weights", bad);
+    // ghost rows of the face arrays and the shift
+    if (has_ghosts(h)) {
+        RowArray arr[3];
+        int na = 0;
+        auto wxbase = [](gpcg_problem* hh, Slab& S, int) {
+            return reinterpret_cast<char*>(const_cast<double*>(S.sop.wx));
+        };
+        auto wybase = [](gpcg_problem* hh, Slab& S, int) {
+            return reinterpret_cast<char*>(const_cast<double*>(S.sop.wy));
+        };
+        auto shbase = [](gpcg_problem* hh, Slab& S, int) {
+            return reinterpret_cast<char*>(const_cast<double*>(S.sop.shift));
+        };
+        if (h->wx_ld) arr[na++] = RowArray{wxbase, 0, (size_t)(nx + 1), sizeof(double), ncclDouble, 0, 0};
+        if (h->wy_ld) arr[na++] = RowArray{wybase, 0, (size_t)nx, sizeof(double), ncclDouble, 1, 1};
+        if (shift) arr[na++] = RowArray{shbase, 0, (size_t)h->pitch, sizeof(double), ncclDouble, 0, 0};
+        if (na) RC(exchange_arrays(h, arr, na));
+    }
+    return GPCG_OK;
+}
+
+int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t nx, int64_t ny,
+                   const double* wx, int64_t wx_ld, const double* wy, int64_t wy_ld, const double* shift,
+                   const double* b, const double* l, const double* u, double c) {
+    g_err.clear();
+    if (!out) return set_err(GPCG_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (nx <= 0 || ny <= 0 || nx * ny >= (1LL << 31))
+        return set_err(GPCG_EINVAL, "grid %lld x %lld out of range (need 0 < n < 2^31)", (long long)nx, (long long)ny);
+    if (!wx || !wy || !b || !l || !u) return set_err(GPCG_EINVAL, "NULL array argument");
+    if ((wx_ld != 0 && wx_ld < nx + 1) || (wy_ld != 0 && wy_ld < nx) || wx_ld < 0 || wy_ld < 0)
+        return set_err(GPCG_EINVAL, "bad leading dimension (wx_ld %lld, wy_ld %lld)", (long long)wx_ld, (long long)wy_ld);
+    if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
+    long long rb = 0, re = ny;
+    int nsl = 1;
+    if (dist) {
+        if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)
+            return set_err(GPCG_EINVAL, "bad rank %d / nranks %d", dist->rank, dist->nranks);
+        rb = dist->row_begin;
+        re = dist->row_end;
+        nsl = dist->local_slabs > 0 ? dist->local_slabs : 1;
+        if (rb < 0 || re > ny || re <= rb) return set_err(GPCG_EINVAL, "bad row range [%lld, %lld)", rb, re);
+        if ((dist->rank == 0) != (rb == 0) || (dist->rank == dist->nranks - 1) != (re == ny))
+            return set_err(GPCG_EINVAL, "row range [%lld, %lld) inconsistent with rank %d of %d", rb, re, dist->rank,
+                           dist->nranks);
+    }
+    const long long pitch = (nx + 31) / 32 * 32;
+    if (pitch * (re - rb + 4 * nsl) >= (1LL << 31)) return set_err(GPCG_EINVAL, "pitched grid too large");
+    gpcg_problem* h = new gpcg_problem();
+    auto fail = [&](int r) { free_all(h); return r; };
+    h->is_csr = false;
+    h->nx = (int)nx;
+    h->pitch = (int)pitch;
+    h->wx_ld = wx_ld;
+    h->wy_ld = wy_ld;
+    h->n_global = nx * ny;
+    h->n_local = nx * (re - rb);
+    h->rank_row0 = rb;
+    h->generic = getenv("GPCG_GENERIC") != nullptr && getenv("GPCG_GENERIC")[0] == '1';
+    int rc;
+    if ((rc = create_streams(h, stream))) return fail(rc);
+    if ((rc = setup_comm(h, dist))) return fail(rc);
+    if ((rc = layout_slabs(h, re - rb, nsl, 2))) return fail(rc);
+    if ((rc = create_vectors(h, b, l, u))) return fail(rc);
+    h->c = c;
+    if ((rc = setup_stencil_slabs(h, wx, wy, shift))) return fail(rc);
+    h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
+    {
+        const char* e = getenv("GPCG_TILE");
+        if (e && *e) h->tile_mask = atoi(e) & 15;
+        if (h->bc && !h->generic && h->tile_mask != 0 && (rc = setup_tile(h))) return fail(rc);
+    }
+    h->nnz = 5 * h->n_global - 2 * nx - 2 * ny;
+    if ((rc = leave(h))) return fail(rc);
+    *out = h;
+    return GPCG_OK;
+}
+
+// ---------------------------------------------------------------- CSR slabs
+int create_csr(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t n_global, const int64_t* row_ptr,
+               const int32_t* col, const double* val, const double* b, const double* l, const double* u, double c) {
+    g_err.clear();
+    if (!out) return set_err(GPCG_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (n_global <= 0 || n_global >= (1LL << 31)) return set_err(GPCG_EINVAL, "n = %lld out of range", (long long)n_global);
+    if (!row_ptr || !col || !val || !b || !l || !u) return set_err(GPCG_EINVAL, "NULL array argument");
+    if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
+    long long rb = 0, re = n_global;
+    int nsl = 1;
+    if (dist) {
+        if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)
+            return set_err(GPCG_EINVAL, "bad rank %d / nranks %d", dist->rank, dist->nranks);
+        rb = dist->row_begin;
+        re = dist->row_end;
+        nsl = dist->local_slabs > 0 ? dist->local_slabs : 1;
+        if (rb < 0 || re > n_global || re <= rb) return set_err(GPCG_EINVAL, "bad row range [%lld, %lld)", rb, re);
+        if ((dist->rank == 0) != (rb == 0) || (dist->rank == dist->nranks - 1) != (re == n_global))
+            return set_err(GPCG_EINVAL, "row range [%lld, %lld) inconsistent with rank %d of %d", rb, re, dist->rank,
+                           dist->nranks);
+    }
+    const long long nloc = re - rb;
+    // the row structure on the host (create time only): ghost bands of every slab
+    std::vector<long long> rp(nloc + 1);
+    const bool rp_dev = is_device_ptr(row_ptr);
+    if (rp_dev) {
+        if (cudaMemcpy(rp.data(), row_ptr, (nloc + 1) * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(GPCG_ECUDA, "reading row_ptr");
+        }
+    } else {
+        memcpy(rp.data(), row_ptr, (nloc + 1) * sizeof(long long));
+    }
+    if (rp[0] != 0 || rp[nloc] < nloc || rp[nloc] >= (1LL << 40))
+        return set_err(GPCG_EINVAL, "row_ptr[0] = %lld, row_ptr[n] = %lld invalid", rp[0], rp[nloc]);
+    for (long long i = 0; i < nloc; ++i)
+        if (rp[i + 1] < rp[i]) return set_err(GPCG_EINVAL, "row_ptr not monotone at row %lld", i);
+    const long long nnz = rp[nloc];
+    std::vector<int32_t> colh;
+    const int32_t* cols = col;
+    if (is_device_ptr(col)) {
+        colh.resize(nnz);
+        if (cudaMemcpy(colh.data(), col, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(GPCG_ECUDA, "reading col");
+        }
+        cols = colh.data();
+    }
+    gpcg_problem* h = new gpcg_problem();
+    auto fail = [&](int r) { free_all(h); return r; };
+    h->is_csr = true;
+    h->pitch = 1;
+    h->n_global = n_global;
+    h->n_local = nloc;
+    h->rank_row0 = rb;
+    h->nnz = nnz;
+    int rc;
+    if ((rc = create_streams(h, stream))) return fail(rc);
+    if ((rc = setup_comm(h, dist))) return fail(rc);
+    if ((rc = layout_slabs(h, nloc, nsl, 0))) return fail(rc);
+    // ghost bands: columns below / above the slab's rows (global ids)
+    for (Slab& S : h->slabs) {
+        const long long g0 = rb + S.row0, g1 = g0 + S.rows;
+        long long cmin = g0, cmax = g1 - 1;
+        for (long long k = rp[S.row0]; k < rp[S.row0 + S.rows]; ++k) {
+            if (cols[k] < 0 || cols[k] >= n_global) return fail(set_err(GPCG_EINVAL, "col[%lld] = %d out of range", k, cols[k]));
+            cmin = std::min<long long>(cmin, cols[k]);
+            cmax = std::max<long long>(cmax, cols[k]);
+        }
+        S.glo = (int)(g0 - cmin);
+        S.ghi = (int)(cmax - (g1 - 1));
+        if ((S.glo > 0 && S.nb_lo == NB_NONE) || (S.ghi > 0 && S.nb_hi == NB_NONE))
+            return fail(set_err(GPCG_EINVAL, "internal: ghost band without a neighbour"));
+    }
+    // what each neighbour reads from a slab (local neighbours directly; remote via NCCL)
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        S.send_lo = S.nb_lo >= 0 ? h->slabs[S.nb_lo].ghi : 0;
+        S.send_hi = S.nb_hi >= 0 ? h->slabs[S.nb_hi].glo : 0;
+        if (S.nb_lo >= 0 && S.glo > h->slabs[S.nb_lo].rows)
+            return fail(set_err(GPCG_EINVAL, "slab %d: lower band (%d rows) exceeds the neighbour slab", s, S.glo));
+        if (S.nb_hi >= 0 && S.ghi > h->slabs[S.nb_hi].rows)
+            return fail(set_err(GPCG_EINVAL, "slab %d: upper band (%d rows) exceeds the neighbour slab", s, S.ghi));
+    }
+    if (h->nranks > 1) {
+        // exchange band widths with the neighbouring ranks: my glo is what rank-1 sends me
+        long long* dbuf = nullptr;
+        if (cudaMalloc(&dbuf, 4 * sizeof(long long)) != cudaSuccess) return fail(set_err(GPCG_ENOMEM, "band buffer"));
+        long long hb[4] = {h->slabs.front().glo, h->slabs.back().ghi, 0, 0};
+        cudaMemcpy(dbuf, hb, 4 * sizeof(long long), cudaMemcpyHostToDevice);
+        const NcclApi* N = nccl_api();
+        auto nk = [&](ncclResult_t r) { return r == ncclSuccess; };
+        bool ok = nk(N->GroupStart());
+        if (h->rank > 0) ok = ok && nk(N->Send(dbuf, 1, ncclInt64, h->rank - 1, h->comm, h->st)) &&
+                          nk(N->Recv(dbuf + 2, 1, ncclInt64, h->rank - 1, h->comm, h->st));
+        if (h->rank < h->nranks - 1) ok = ok && nk(N->Send(dbuf + 1, 1, ncclInt64, h->rank + 1, h->comm, h->st)) &&
+                                       nk(N->Recv(dbuf + 3, 1, ncclInt64, h->rank + 1, h->comm, h->st));
+        ok = nk(N->GroupEnd()) && ok;
+        cudaStreamSynchronize(h->st);
+        cudaMemcpy(hb, dbuf, 4 * sizeof(long long), cudaMemcpyDeviceToHost);
+        cudaFree(dbuf);
+        if (!ok) return fail(set_err(GPCG_ENCCL, "band-width exchange failed"));
+        h->slabs.front().send_lo = h->rank > 0 ? (int)hb[2] : 0;            // rank-1's ghi
+        h->slabs.back().send_hi = h->rank < h->nranks - 1 ? (int)hb[3] : 0; // rank+1's glo
+        if (h->slabs.front().send_lo > h->slabs.front().rows || h->slabs.back().send_hi > h->slabs.back().rows)
+            return fail(set_err(GPCG_EINVAL, "a neighbouring rank's band exceeds this rank's rows"));
+    }
+    if ((rc = create_vectors(h, b, l, u))) return fail(rc);
+    h->c = c;
+    // per-slab CSR: rows rebased, columns as local offsets from the slab's first row
+    std::vector<long long> rps;
+    std::vector<int32_t> cis;
+    const cudaMemcpyKind kv = (cudaMemcpyKind)copy_kind(val, true);
+    for (Slab& S : h->slabs) {
+        const long long k0 = rp[S.row0], k1 = rp[S.row0 + S.rows], g0 = rb + S.row0;
+        rps.resize(S.rows + 1);
+        for (int i = 0; i <= S.rows; ++i) rps[i] = rp[S.row0 + i] - k0;
+        cis.resize(k1 - k0);
+        for (long long k = k0; k < k1; ++k) cis[k - k0] = (int32_t)(cols[k] - g0);
+        if (cudaMalloc(&S.rp, (S.rows + 1) * sizeof(long long)) != cudaSuccess ||
+            cudaMalloc(&S.ci, std::max<long long>(1, k1 - k0) * sizeof(int)) != cudaSuccess ||
+            cudaMalloc(&S.val, std::max<long long>(1, k1 - k0) * sizeof(double)) != cudaSuccess)
+            return fail(set_err(GPCG_ENOMEM, "CSR arrays (nnz = %lld)", k1 - k0));
+        if (cudaMemcpy(S.rp, rps.data(), (S.rows + 1) * sizeof(long long), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(S.ci, cis.data(), (k1 - k0) * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpyAsync(S.val, val + k0, (k1 - k0) * sizeof(double), kv, h->st) != cudaSuccess)
+            return fail(set_err(GPCG_ECUDA, "CSR upload"));
+        S.cop = CsrOp{S.rows, S.rp, S.ci, S.val};
+        S.grid = std::max(1, std::min((S.rows + kThreads - 1) / kThreads, h->sms * 16));
+    }
+    {
+        std::vector<const double*> arrs;
+        std::vector<long long> cnts;
+        for (Slab& S : h->slabs) {
+            arrs.push_back(S.val);
+            cnts.push_back(rp[S.row0 + S.rows] - rp[S.row0]);
+        }
+        double t = 0.0;
+        if ((rc = count_nonfinite(h, arrs.data(), cnts.data(), &t))) return fail(rc);
+        if (t != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite CSR values", t));
+    }
+    if ((rc = leave(h))) return fail(rc);
+    *out = h;
     return GPCG_OK;
 }
 
@@ -655,125 +1259,47 @@ gpcg_params gpcg_params_default(void) {
 
 const char* gpcg_last_error(void) { return g_err.c_str(); }
 
-int64_t gpcg_size(const gpcg_problem* h) { return h ? h->n : -1; }
+int64_t gpcg_size(const gpcg_problem* h) { return h ? h->n_local : -1; }
 
-int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int64_t ny, const double* wx,
-                          int64_t wx_ld, const double* wy, int64_t wy_ld, const double* shift,
-                          const double* b, const double* l, const double* u, double c) {
+void gpcg_partition_rows(int64_t total, int32_t parts, int32_t part, int64_t* begin, int64_t* end) {
+    long long b = 0, e = 0;
+    if (total >= 0 && parts > 0 && part >= 0 && part < parts) partition(total, parts, part, &b, &e);
+    if (begin) *begin = b;
+    if (end) *end = e;
+}
+
+int gpcg_nccl_unique_id(void* out128) {
     g_err.clear();
-    if (!out) return set_err(GPCG_EINVAL, "out is NULL");
-    *out = nullptr;
-    if (nx <= 0 || ny <= 0 || nx * ny >= (1LL << 31))
-        return set_err(GPCG_EINVAL, "grid %lld x %lld out of range (need 0 < n < 2^31)", (long long)nx,
-                       (long long)ny);
-    if (!wx || !wy || !b || !l || !u) return set_err(GPCG_EINVAL, "NULL array argument");
-    if ((wx_ld != 0 && wx_ld < nx + 1) || (wy_ld != 0 && wy_ld < nx) || wx_ld < 0 || wy_ld < 0)
-        return set_err(GPCG_EINVAL, "bad leading dimension (wx_ld %lld, wy_ld %lld)", (long long)wx_ld,
-                       (long long)wy_ld);
-    if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
-    gpcg_problem* h = new gpcg_problem();
-    h->n = (int)(nx * ny);
-    h->rows = (int)ny;
-    h->cols = (int)nx;
-    h->pitch = (int)((nx + 31) / 32 * 32);
-    h->nalloc = (long long)h->pitch * ny;
-    if (h->nalloc >= (1LL << 31)) { delete h; return set_err(GPCG_EINVAL, "pitched grid too large"); }
-    h->is_csr = false;
-    h->generic = getenv("GPCG_GENERIC") != nullptr && getenv("GPCG_GENERIC")[0] == '1';
-    h->mg1 = march_geom((int)nx, (int)ny, 1);
-    h->mg2 = march_geom((int)nx, (int)ny, 2);
-    h->grid_m1 = march_grid(h->mg1);
-    h->grid_m2 = march_grid(h->mg2);
-    int rc = create_common(h, cuda_stream, b, l, u);
-    if (rc) { free_all(h); return rc; }
-    h->c = c;
-    const size_t wxn = (size_t)(wx_ld ? wx_ld * (ny - 1) + nx + 1 : nx + 1);
-    const size_t wyn = (size_t)(wy_ld ? wy_ld * ny + nx : nx);
-    auto fail = [&](int r) { free_all(h); return r; };
-    if (cudaMalloc(&h->wx, wxn * sizeof(double)) != cudaSuccess) return fail(set_err(GPCG_ENOMEM, "wx"));
-    if (cudaMalloc(&h->wy, wyn * sizeof(double)) != cudaSuccess) return fail(set_err(GPCG_ENOMEM, "wy"));
-    if ((rc = upload(h, h->wx, wx, wxn))) return fail(rc);
-    if ((rc = upload(h, h->wy, wy, wyn))) return fail(rc);
-    double bad = 0.0, t = 0.0;
-    if ((rc = count_nonfinite(h, h->wx, (long long)wxn, &t))) return fail(rc);
-    bad += t;
-    if ((rc = count_nonfinite(h, h->wy, (long long)wyn, &t))) return fail(rc);
-    bad += t;
-    if (shift) {
-        if (cudaMalloc(&h->shift, (size_t)h->nalloc * sizeof(double)) != cudaSuccess)
-            return fail(set_err(GPCG_ENOMEM, "shift"));
-        if (cudaMemsetAsync(h->shift, 0, (size_t)h->nalloc * sizeof(double), h->st) != cudaSuccess)
-            return fail(set_err(GPCG_ECUDA, "memset shift"));
-        if ((rc = upload_vec(h, h->shift, shift))) return fail(rc);
-        if ((rc = count_nonfinite(h, h->shift, h->nalloc, &t))) return fail(rc);
-        bad += t;
-    }
-    if (bad != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite stencil weights", bad));
-    h->is_csr = false;
-    h->sop = StencilOp{(int)nx, (int)ny, h->pitch, h->wx, h->wy, h->shift, (long long)wx_ld, (long long)wy_ld};
-    h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
-    {
-        const char* e = getenv("GPCG_TILE");
-        if (e && *e) h->tile_mask = atoi(e) & 7;
-        const bool want_tile = h->bc && !h->generic && h->tile_mask != 0;
-        if (want_tile && (rc = setup_tile(h))) return fail(rc);
-    }
-    h->nnz = 5 * (long long)h->n - 2 * nx - 2 * ny;
-    h->grid = std::max(1, std::min(units(h), h->sms * 16));
-    if ((rc = leave(h))) return fail(rc);
-    *out = h;
+    if (!out128) return set_err(GPCG_EINVAL, "NULL argument");
+    const NcclApi* N = nccl_api();
+    if (!N) return set_err(GPCG_ENCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    NK(N->GetUniqueId(&id));
+    memcpy(out128, &id, sizeof id);
     return GPCG_OK;
 }
 
-int gpcg_create_csr(gpcg_problem** out, void* cuda_stream, int64_t n, const int64_t* row_ptr,
-                    const int32_t* col, const double* val, const double* b, const double* l, const double* u,
-                    double c) {
-    g_err.clear();
-    if (!out) return set_err(GPCG_EINVAL, "out is NULL");
-    *out = nullptr;
-    if (n <= 0 || n >= (1LL << 31)) return set_err(GPCG_EINVAL, "n = %lld out of range", (long long)n);
-    if (!row_ptr || !col || !val || !b || !l || !u) return set_err(GPCG_EINVAL, "NULL array argument");
-    if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
-    gpcg_problem* h = new gpcg_problem();
-    h->n = (int)n;
-    h->rows = 1;
-    h->cols = (int)n;
-    h->pitch = (int)n;
-    h->nalloc = n;
-    h->is_csr = true;
-    auto fail = [&](int r) { free_all(h); return r; };
-    int rc = create_common(h, cuda_stream, b, l, u);
-    if (rc) return fail(rc);
-    h->c = c;
-    // row_ptr: need nnz on the host for the copies
-    long long rp_end = 0, rp0 = 0;
-    if (is_device_ptr(row_ptr)) {
-        if (cudaMemcpy(&rp_end, row_ptr + n, sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess ||
-            cudaMemcpy(&rp0, row_ptr, sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
-            return fail(set_err(GPCG_ECUDA, "reading row_ptr"));
-    } else {
-        rp_end = row_ptr[n];
-        rp0 = row_ptr[0];
-    }
-    if (rp0 != 0 || rp_end < n || rp_end >= (1LL << 40))
-        return fail(set_err(GPCG_EINVAL, "row_ptr[0] = %lld, row_ptr[n] = %lld invalid", rp0, rp_end));
-    h->nnz = rp_end;
-    if (cudaMalloc(&h->rp, (size_t)(n + 1) * sizeof(long long)) != cudaSuccess ||
-        cudaMalloc(&h->ci, (size_t)rp_end * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&h->val, (size_t)rp_end * sizeof(double)) != cudaSuccess)
-        return fail(set_err(GPCG_ENOMEM, "CSR arrays (nnz = %lld)", rp_end));
-    if ((rc = upload_bytes(h, h->rp, row_ptr, (size_t)(n + 1) * sizeof(long long)))) return fail(rc);
-    if ((rc = upload_bytes(h, h->ci, col, (size_t)rp_end * sizeof(int)))) return fail(rc);
-    if ((rc = upload(h, h->val, val, (size_t)rp_end))) return fail(rc);
-    double t = 0.0;
-    if ((rc = count_nonfinite(h, h->val, rp_end, &t))) return fail(rc);
-    if (t != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite CSR values", t));
-    h->is_csr = true;
-    h->cop = CsrOp{h->n, h->rp, h->ci, h->val};
-    h->grid = std::max(1, std::min(units(h), h->sms * 16));
-    if ((rc = leave(h))) return fail(rc);
-    *out = h;
-    return GPCG_OK;
+int gpcg_create_stencil2d(gpcg_problem** out, void* cuda_stream, int64_t nx, int64_t ny, const double* wx,
+                          int64_t wx_ld, const double* wy, int64_t wy_ld, const double* shift, const double* b,
+                          const double* l, const double* u, double c) {
+    return create_stencil(out, nullptr, cuda_stream, nx, ny, wx, wx_ld, wy, wy_ld, shift, b, l, u, c);
+}
+
+int gpcg_create_stencil2d_dist(gpcg_problem** out, const gpcg_dist* dist, void* cuda_stream, int64_t nx, int64_t ny,
+                               const double* wx, int64_t wx_ld, const double* wy, int64_t wy_ld, const double* shift,
+                               const double* b, const double* l, const double* u, double c) {
+    return create_stencil(out, dist, cuda_stream, nx, ny, wx, wx_ld, wy, wy_ld, shift, b, l, u, c);
+}
+
+int gpcg_create_csr(gpcg_problem** out, void* cuda_stream, int64_t n, const int64_t* row_ptr, const int32_t* col,
+                    const double* val, const double* b, const double* l, const double* u, double c) {
+    return create_csr(out, nullptr, cuda_stream, n, row_ptr, col, val, b, l, u, c);
+}
+
+int gpcg_create_csr_dist(gpcg_problem** out, const gpcg_dist* dist, void* cuda_stream, int64_t n,
+                         const int64_t* row_ptr, const int32_t* col, const double* val, const double* b,
+                         const double* l, const double* u, double c) {
+    return create_csr(out, dist, cuda_stream, n, row_ptr, col, val, b, l, u, c);
 }
 
 int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
@@ -784,8 +1310,8 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
         return set_err(GPCG_EINVAL, "eta1, eta2 must lie in (0, 1)");
     if (!(p->eta2_shrink > 0.0 && p->eta2_shrink < 1.0) || !(p->eta2_floor > 0.0))
         return set_err(GPCG_EINVAL, "eta2_shrink in (0,1), eta2_floor > 0 required");
-    if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 ||
-        p->cg_cap < 0 || p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096)
+    if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 || p->cg_cap < 0 ||
+        p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096)
         return set_err(GPCG_EINVAL, "integer parameter out of range");
     const int old_chunk = h->prm.cg_chunk;
     h->prm = *p;
@@ -802,12 +1328,12 @@ int gpcg_project(gpcg_problem* h, const double* x, double* px, double* pg_norm2,
                  int64_t* n_active_nonbinding) {
     g_err.clear();
     if (!h || !x || !px) return set_err(GPCG_EINVAL, "NULL argument");
-    int rc;
-    if ((rc = enter(h))) return rc;
-    if ((rc = upload_vec(h, h->stage_in, x))) return rc;
-    if ((rc = launch_accept(h, h->stage_in, nullptr, 0.0, nullptr, h->Y[0], h->G[0], h->M[0]))) return rc;
-    if ((rc = download_vec(h, px, h->Y[0]))) return rc;
-    if ((rc = sync_scal(h))) return rc;
+    RC(enter(h));
+    RC(upload_vec(h, VIN, x));
+    RC(exchange(h, {VIN}));
+    RC(launch_accept(h, VIN, NO_VEC, 0.0, NO_VEC, VY0, VG0, MK0));
+    RC(download_vec(h, px, VY0));
+    RC(sync_scal(h));
     h->free_mask = 0;
     if (pg_norm2) *pg_norm2 = h->hS->pg2;
     if (n_active) *n_active = (int64_t)h->hS->n_active;
@@ -821,29 +1347,29 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
     if (v == y) return set_err(GPCG_EINVAL, "v and y must not alias");
     if (reduced && h->free_mask < 0)
         return set_err(GPCG_ESTATE, "reduced hessvec needs a free set: call gpcg_project or gpcg_solve first");
-    int rc;
-    if ((rc = enter(h))) return rc;
-    // direct device access only when the layout is contiguous (CSR, or nx a multiple of 32)
-    const bool contiguous = (h->pitch == h->cols);
-    const bool vdev = is_device_ptr(v) && contiguous, ydev = is_device_ptr(y) && contiguous;
-    const double* vin = v;
+    RC(enter(h));
+    // direct device access only for one slab with a contiguous layout (CSR, or nx a multiple of 32)
+    const bool direct = h->nslabs() == 1 && !has_ghosts(h) && (h->is_csr || h->pitch == h->nx);
+    const bool vdev = direct && is_device_ptr(v), ydev = direct && is_device_ptr(y);
     if (!vdev) {
-        if ((rc = upload_vec(h, h->stage_in, v))) return rc;
-        vin = h->stage_in;
+        RC(upload_vec(h, VIN, v));
+        RC(exchange(h, {VIN}));
     }
-    double* yout = ydev ? y : h->stage_out;
-    const unsigned char* mask = reduced ? h->M[h->free_mask] : nullptr;
-    with_op_only(h, [&](auto& op) {
-        using Op = std::decay_t<decltype(op)>;
-        if (reduced)
-            k_hessvec<Op, true><<<h->grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
-        else
-            k_hessvec<Op, false><<<h->grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
-    });
-    h->launches++;
-    CKLAUNCH();
+    for (Slab& S : h->slabs) {
+        const double* vin = vdev ? v : S.v[VIN];
+        double* yout = ydev ? y : S.v[VOUT];
+        const unsigned char* mask = reduced ? S.m[h->free_mask] : nullptr;
+        auto go = [&](auto& op) {
+            using Op = std::decay_t<decltype(op)>;
+            if (reduced) k_hessvec<Op, true><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
+            else k_hessvec<Op, false><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
+        };
+        if (h->is_csr) go(S.cop); else go(S.sop);
+        h->launches++;
+        CKLAUNCH();
+    }
     if (!ydev) {
-        if ((rc = download_vec(h, y, h->stage_out))) return rc;
+        RC(download_vec(h, y, VOUT));
         if (!is_device_ptr(y)) CK(cudaStreamSynchronize(h->st));
     }
     return leave(h);
@@ -852,23 +1378,17 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
 int gpcg_objective(gpcg_problem* h, const double* x, double* q) {
     g_err.clear();
     if (!h || !x || !q) return set_err(GPCG_EINVAL, "NULL argument");
-    int rc;
-    if ((rc = enter(h))) return rc;
-    if ((rc = upload_vec(h, h->stage_in, x))) return rc;
-    with_op_only(h, [&](auto& op) {
-        using Op = std::decay_t<decltype(op)>;
-        k_objective<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->stage_in, h->b, h->dS, h->red());
-    });
-    h->launches++;
-    CKLAUNCH();
-    if ((rc = sync_scal(h))) return rc;
+    RC(enter(h));
+    RC(upload_vec(h, VIN, x));
+    RC(exchange(h, {VIN}));
+    RC(launch_objective(h, VIN));
+    RC(sync_scal(h));
     *q = 0.5 * h->hS->r0 - h->hS->r1 + h->c;
     return leave(h);
 }
 
 // Algorithm GPCG, same steps as the oracle.
-int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, double* x_out,
-               gpcg_stats* stats) {
+int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, double* x_out, gpcg_stats* stats) {
     g_err.clear();
     if (!h || !x0 || !x_out) return set_err(GPCG_EINVAL, "NULL argument");
     if (!(tol != 0.0) || !std::isfinite(tol)) return set_err(GPCG_EINVAL, "tol must be finite and nonzero");
@@ -880,7 +1400,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     h->cg_iters_timed = h->cg_free_iters_timed = 0;
     h->t_cg_timed_ms = 0.0;
     int rc;
-    if ((rc = enter(h))) return rc;
+    RC(enter(h));
     const gpcg_params& prm = h->prm;
     float t_cg = 0.f, t_gp = 0.f, ms = 0.f;
     int status = GPCG_NOT_CONVERGED;
@@ -889,9 +1409,10 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     const Scal& S = *h->hS;
 
     // Setup: x <- P[x0], g <- A x - b
-    if ((rc = upload_vec(h, h->stage_in, x0))) return rc;
-    if ((rc = launch_accept(h, h->stage_in, nullptr, 0.0, nullptr, h->Y[0], h->G[0], h->M[0]))) return rc;
-    if ((rc = sync_scal(h))) return rc;
+    RC(upload_vec(h, VIN, x0));
+    RC(exchange(h, {VIN}));
+    RC(launch_accept(h, VIN, NO_VEC, 0.0, NO_VEC, VY0, VG0, MK0));
+    RC(sync_scal(h));
     st.full_spmvs++;
     st.g0_norm = std::sqrt(S.g2);
     tau = tol > 0.0 ? tol : -tol * st.g0_norm;
@@ -908,12 +1429,12 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
             bool conv = false;
             for (;;) {
                 if (std::sqrt(S.pg2) <= tau) { conv = true; break; }
-                if ((rc = launch_cauchy(h, h->Y[cur], h->G[cur]))) goto fail;
+                if ((rc = launch_cauchy(h, vy(cur), vg(cur)))) goto fail;
                 st.full_spmvs++;
                 int hacc = -1;
                 // direction -grad q (Eq. next-y); trial points equal those of the
                 // -grad_Omega q reading for feasible y (reading R8)
-                if ((rc = search_and_accept(h, cur, h->G[cur], -1.0, 1, &hacc))) goto fail;
+                if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc))) goto fail;
                 st.full_spmvs += 2;
                 cur ^= 1;
                 ++j;
@@ -938,7 +1459,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
             // ---- CG phase with eta2 refinement -------------------
             double eta2 = prm.eta2;
             for (int64_t rep = 0; rep < prm.refine_cap; ++rep) {
-                const long long m = (long long)h->n - (long long)S.n_active;
+                const long long m = h->n_global - (long long)S.n_active;
                 if (m == 0) break;                                  // reading R26
                 const long long cap = prm.cg_cap > 0 ? prm.cg_cap : m;
                 long long its = 0;
@@ -953,7 +1474,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 t_cg += ms;
                 // projected search along d_k = Z_k w (Eq. cglsstop2), alpha = 2^-h
                 int hacc = -1;
-                if ((rc = search_and_accept(h, cur, h->W, 1.0, 0, &hacc))) goto fail;
+                if ((rc = search_and_accept(h, cur, VW, 1.0, 0, &hacc))) goto fail;
                 st.full_spmvs += 2;
                 cur ^= 1;
                 if (trace_on())
@@ -970,20 +1491,19 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
         }
     }
     // x_out, q, sets
-    if ((rc = download_vec(h, x_out, h->Y[cur]))) return rc;
-    with_op_only(h, [&](auto& op) {
-        using Op = std::decay_t<decltype(op)>;
-        k_objective<Op><<<h->grid, kThreads, 0, h->st>>>(op, h->Y[cur], h->b, h->dS, h->red());
-    });
-    h->launches++;
-    CKLAUNCH();
-    if ((rc = sync_scal(h))) return rc;
-    h->free_mask = cur;
-    st.q = 0.5 * S.r0 - S.r1 + h->c;
-    st.pg_norm = std::sqrt(S.pg2);
-    st.n_active = (int64_t)S.n_active;
-    st.n_free = h->n - st.n_active;
-    st.n_active_nonbinding = (int64_t)S.n_nonbinding;
+    RC(download_vec(h, x_out, vy(cur)));
+    {
+        // the sets and ||grad_Omega q|| of x_out are those of the last accept sweep (already in S)
+        const double pg2 = S.pg2, na = S.n_active, nnb = S.n_nonbinding;
+        RC(launch_objective(h, vy(cur)));
+        RC(sync_scal(h));
+        h->free_mask = cur;
+        st.q = 0.5 * S.r0 - S.r1 + h->c;
+        st.pg_norm = std::sqrt(pg2);
+        st.n_active = (int64_t)na;
+        st.n_free = h->n_global - st.n_active;
+        st.n_active_nonbinding = (int64_t)nnb;
+    }
     st.t_cg_ms = t_cg;
     st.t_gp_ms = t_gp;
     st.status = status;
@@ -993,7 +1513,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     st.t_cg_timed_ms = h->t_cg_timed_ms;
     st.t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     if (stats) *stats = st;
-    if ((rc = leave(h))) return rc;
+    RC(leave(h));
     return status;
 
 fail:
@@ -1001,7 +1521,7 @@ fail:
     {
         const std::string msg = g_err;
         cudaGetLastError();
-        download_vec(h, x_out, h->Y[cur]);
+        download_vec(h, x_out, vy(cur));
         cudaStreamSynchronize(h->st);
         h->free_mask = cur;
         st.status = rc;

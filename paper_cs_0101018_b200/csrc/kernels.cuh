@@ -14,6 +14,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "fin.cuh"
 
 namespace gpcg {
 
@@ -61,13 +62,7 @@ k_accept(Op A, Bounds Bd, const double* __restrict__ y_in, const double* __restr
         const bool binding = (yv == l && g >= 0.0) || (yv == u && g <= 0.0);
         acc[4] += (act && !binding) ? 1.0 : 0.0;
     });
-    reduce_and_finish<5>(acc, R, [&](double* t) {
-        S->pg2 = t[0];
-        S->g2 = t[1];
-        S->n_active = t[2];
-        S->n_changed = t[3];
-        S->n_nonbinding = t[4];
-    });
+    reduce_and_finish<5>(acc, R, [&](double* t) { fin_accept(t, false, S); });
 }
 
 // ----------------------------------------------------------------------------
@@ -90,13 +85,7 @@ k_cauchy(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict
         acc[0] = fma(dv, dv, acc[0]);
         acc[1] = fma(dv, ad, acc[1]);
     });
-    reduce_and_finish<2>(acc, R, [&](double* t) {
-        S->dd = t[0];
-        S->dAd = t[1];
-        S->cauchy_ok = (t[1] > 0.0) ? 1 : 0;          // <d,Ad> <= 0 -> ENOTSPD (R7)
-        S->alpha0 = (t[1] > 0.0) ? t[0] / t[1] : 0.0;
-        S->s_h = -1;                                   // no step accepted yet
-    });
+    reduce_and_finish<2>(acc, R, [&](double* t) { fin_cauchy(t, S); });
 }
 
 // ----------------------------------------------------------------------------
@@ -145,20 +134,7 @@ k_search(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict
             acc[2 * h + 1] = fma(sv[h], as[h], acc[2 * h + 1]);
         }
     });
-    reduce_and_finish<2 * K>(acc, R, [&](double* t) {
-        S->s_h = -1;
-        for (int h = 0; h < K; ++h) {
-            const double gs = t[2 * h], sAs = t[2 * h + 1];
-            const double dq = gs + 0.5 * sAs;
-            if (dq <= mu * gs) {
-                S->s_h = h0 + h;
-                S->s_alpha = al[h];
-                S->s_delta = dq;
-                S->s_gs = gs;
-                break;
-            }
-        }
-    });
+    reduce_and_finish<2 * K>(acc, R, [&](double* t) { fin_search(t, K, h0, base, mu, S); });
 }
 
 // ----------------------------------------------------------------------------
@@ -243,25 +219,7 @@ k_cg_init(Op A, const double* __restrict__ g, const unsigned char* __restrict__ 
         acc[0] = fma(rv, rv, acc[0]);
         acc[1] = fma(rv, qv, acc[1]);
     });
-    reduce_and_finish<2>(acc, R, [&](double* t) {
-        S->cg_it = 0;
-        S->cg_cap = cap;
-        S->cg_eta2 = eta2;
-        S->cg_maxdec = 0.0;
-        S->cg_dec = 0.0;
-        S->cg_gamma = t[0];
-        S->cg_rnorm0 = sqrt(t[0]);
-        S->cg_beta = 0.0;
-        S->cg_done = 0;
-        S->cg_reason = CG_RUNNING;
-        if (t[0] == 0.0 || cap <= 0) {            // r_k = 0: w = 0 is exact (R27)
-            S->cg_done = 1; S->cg_reason = CG_EXACT; S->cg_alpha = 0.0;
-        } else if (!(t[1] > 0.0)) {
-            S->cg_done = 1; S->cg_reason = CG_NOTSPD; S->cg_alpha = 0.0;
-        } else {
-            S->cg_alpha = t[0] / t[1];
-        }
-    });
+    reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
 }
 
 template <class Op>
@@ -299,34 +257,7 @@ k_cg_iter(Op A, const unsigned char* __restrict__ mask,
         acc[0] = fma(rnv, rnv, acc[0]);
         acc[1] = fma(rnv, qn, acc[1]);
     });
-    reduce_and_finish<2>(acc, R, [&](double* t) {
-        const double gamma_old = S->cg_gamma, alpha_old = S->cg_alpha;
-        const double gamma = t[0], delta = t[1];
-        const double dec = 0.5 * alpha_old * gamma_old;
-        const long long j = S->cg_it + 1;
-        S->cg_it = j;
-        S->cg_dec = dec;
-        int reason = CG_RUNNING;
-        if (j >= 2 && dec <= S->cg_eta2 * S->cg_maxdec) reason = CG_PROGRESS;
-        else if (sqrt(gamma) <= 1e-14 * (1.0 + S->cg_rnorm0)) reason = CG_EXACT;
-        else if (j >= S->cg_cap) reason = CG_CAP;
-        if (dec > S->cg_maxdec) S->cg_maxdec = dec;
-        S->cg_gamma = gamma;
-        if (reason != CG_RUNNING) {
-            S->cg_reason = reason;
-            S->cg_done = 1;
-            return;
-        }
-        const double beta = gamma / gamma_old;
-        const double pap = delta - beta * gamma / alpha_old;
-        S->cg_beta = beta;
-        if (!(pap > 0.0)) {
-            S->cg_reason = CG_NOTSPD;
-            S->cg_done = 1;
-            return;
-        }
-        S->cg_alpha = gamma / pap;
-    });
+    reduce_and_finish<2>(acc, R, [&](double* t) { cg_finalize(t[0], t[1], S); });
 }
 
 // ----------------------------------------------------------------------------
@@ -334,25 +265,25 @@ k_cg_iter(Op A, const unsigned char* __restrict__ mask,
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
 k_check_inputs(int cols, int rows, int pitch, const double* __restrict__ b, const double* __restrict__ l,
-               const double* __restrict__ u, Scal* S, RedScratch R) {
-    double acc[3] = {0.0, 0.0, 0.0};
-    const double l0 = l[0], u0 = u[0];
+               const double* __restrict__ u, const double* __restrict__ lu0, Scal* S, RedScratch R) {
+    // sums: #bad entries, #entries differing from the global first (l, u) pair lu0
+    double acc[2] = {0.0, 0.0};
+    const double l0 = lu0[0], u0 = lu0[1];
     const long long n = (long long)cols * rows;
     for (long long k = blockIdx.x * (long long)kThreads + threadIdx.x; k < n; k += (long long)gridDim.x * kThreads) {
         const long long v = (k % cols) + (k / cols) * (long long)pitch;
         const double lv = l[v], uv = u[v], bv = b[v];
         acc[0] += (!(lv <= uv) || isnan(bv) || isinf(bv) || lv == INFINITY || uv == -INFINITY) ? 1.0 : 0.0;
-        acc[1] += (lv != l0) ? 1.0 : 0.0;
-        acc[2] += (uv != u0) ? 1.0 : 0.0;
+        acc[1] += (lv != l0 || uv != u0) ? 1.0 : 0.0;
     }
-    reduce_and_finish<3>(acc, R, [&](double* t) { S->r0 = t[0]; S->r1 = t[1] + t[2]; });
+    reduce_and_finish<2>(acc, R, [&](double* t) { S->r0 = t[0]; S->r1 = t[1]; });
 }
 
 __global__ void k_count_nonfinite(long long n, const double* __restrict__ a, Scal* S, RedScratch R) {
-    double acc[1] = {0.0};
+    double acc[2] = {0.0, 0.0};
     for (long long v = blockIdx.x * (long long)kThreads + threadIdx.x; v < n; v += (long long)gridDim.x * kThreads)
         acc[0] += isfinite(a[v]) ? 0.0 : 1.0;
-    reduce_and_finish<1>(acc, R, [&](double* t) { S->r0 = t[0]; });
+    reduce_and_finish<2>(acc, R, [&](double* t) { S->r0 = t[0]; S->r1 = t[1]; });
 }
 
 }  // namespace gpcg

@@ -22,6 +22,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "fin.cuh"
 
 namespace gpcg {
 
@@ -69,7 +70,7 @@ struct Op5 {
             t = fma(-fe, ve, t);
             return fma(-fs, vs + vn, t);
         } else {
-            const int rc = min(max(r, 0), A.ny - 1);
+            const int rc = min(max(r, A.rlo), A.rhi - 1);
             const double* wxr = A.wx + (long long)rc * A.wx_ld + ic;
             const double w = __ldg(wxr), e = __ldg(wxr + 1);
             const double s = __ldg(A.wy + (long long)rc * A.wy_ld + ic);
@@ -158,7 +159,7 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
         const bool col_ok = (i >= 0 && i < A.nx);
         Op5<BC> op;
         op.init(A, i);
-        const int rend = min(A.ny, j1 + H);            // raw rows [j0-H, rend) are needed
+        const int rend = min(A.rhi, j1 + H);            // raw rows [j0-H, rend) are needed
         double yn_m2 = 0.0, yn_m1 = 0.0;               // yn(r-2), yn(r-1)
         double b_m1 = 0.0, l_m1 = 0.0, u_m1 = 0.0;      // row r-1
         double l_m2 = 0.0, u_m2 = 0.0;                  // row r-2
@@ -169,7 +170,7 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
             j0 - 2, j1 - j0 + 4, [&](int) { return NoPre{}; },
             [&](int r, NoPre) {                          // loads only; consumed kPipe rows later
                 RawAcc x{0.0, 0.0, 0.0, SB ? Bd.lc : 0.0, SB ? Bd.uc : 0.0, 0};
-                if (r >= 0 && r < rend) {                // warp-uniform
+                if (r >= A.rlo && r < rend) {                // warp-uniform
                     if (col_ok) {
                         const int v = i + A.pitch * r;
                         if constexpr (!SB) { x.l = __ldg(Bd.l + v); x.u = __ldg(Bd.u + v); }
@@ -179,7 +180,7 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
                         if (mask_prev) x.mp = __ldg(mask_prev + v);
                     }
                 }
-                if (!(col_ok && r >= 0 && r < rend)) { x.l = 0.0; x.u = 0.0; }   // fixed at 0 outside
+                if (!(col_ok && r >= A.rlo && r < rend)) { x.l = 0.0; x.u = 0.0; }   // fixed at 0 outside
                 return x;
             },
             [&](int r, const RawAcc& x) {
@@ -213,17 +214,7 @@ k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, 
                 d_m3 = d_m2; d_m2 = d1;
             });
     }
-    reduce_and_finish<6>(acc, R, [&](double* t) {
-        S->pg2 = t[0];
-        S->g2 = t[1];
-        S->n_active = t[2];
-        S->n_changed = t[3];
-        S->n_nonbinding = t[4];
-        S->dd = t[0];
-        S->dAd = t[5];
-        S->cauchy_ok = (t[5] > 0.0) ? 1 : 0;
-        S->alpha0 = (t[5] > 0.0) ? t[0] / t[5] : 0.0;
-    });
+    reduce_and_finish<6>(acc, R, [&](double* t) { fin_accept(t, true, S); });
 }
 
 // ============================================================================
@@ -260,7 +251,7 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
         const bool col_ok = (i >= 0 && i < A.nx);
         Op5<BC> op;
         op.init(A, i);
-        const int rend = min(A.ny, j1 + H);
+        const int rend = min(A.rhi, j1 + H);
         double s_m2[K], s_m1[K];
         double g_m1 = 0.0;
 #pragma unroll
@@ -269,7 +260,7 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
             j0 - 1, j1 - j0 + 2, [&](int) { return NoPre{}; },
             [&](int r, NoPre) {
                 RawY x{0.0, 0.0, 0.0, SB ? Bd.lc : 0.0, SB ? Bd.uc : 0.0};
-                if (r >= 0 && r < rend) {
+                if (r >= A.rlo && r < rend) {
                     if (col_ok) {
                         const int v = i + A.pitch * r;
                         x.y = __ldg(y + v);
@@ -279,7 +270,7 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
                     }
                 }
                 if constexpr (kDirIsG) x.g = x.d;
-                if (!(col_ok && r >= 0 && r < rend)) { x.l = 0.0; x.u = 0.0; }
+                if (!(col_ok && r >= A.rlo && r < rend)) { x.l = 0.0; x.u = 0.0; }
                 return x;
             },
             [&](int r, const RawY& x) {
@@ -301,20 +292,7 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
                 g_m1 = x.g;
             });
     }
-    reduce_and_finish<2 * K>(acc, R, [&](double* t) {
-        S->s_h = -1;
-        for (int h = 0; h < K; ++h) {
-            const double gs = t[2 * h], sAs = t[2 * h + 1];
-            const double dq = gs + 0.5 * sAs;
-            if (dq <= mu * gs) {
-                S->s_h = h0 + h;
-                S->s_alpha = scalbn(base, -(h0 + h));
-                S->s_delta = dq;
-                S->s_gs = gs;
-                break;
-            }
-        }
-    });
+    reduce_and_finish<2 * K>(acc, R, [&](double* t) { fin_search(t, K, h0, base, mu, S); });
 }
 
 // ============================================================================
@@ -322,26 +300,6 @@ k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, con
 // delta_0 = rho_0'A_F rho_0.  Also copies the free mask into the fixed CG mask
 // buffer used by the captured CG graph.  H = 1.
 // ============================================================================
-__device__ __forceinline__ void cg_init_finalize(double gamma, double delta, double eta2, long long cap, Scal* S) {
-    S->cg_it = 0;
-    S->cg_cap = cap;
-    S->cg_eta2 = eta2;
-    S->cg_maxdec = 0.0;
-    S->cg_dec = 0.0;
-    S->cg_gamma = gamma;
-    S->cg_rnorm0 = sqrt(gamma);
-    S->cg_beta = 0.0;
-    S->cg_done = 0;
-    S->cg_reason = CG_RUNNING;
-    if (gamma == 0.0 || cap <= 0) {            // r_k = 0: w = 0 is exact (R27)
-        S->cg_done = 1; S->cg_reason = CG_EXACT; S->cg_alpha = 0.0;
-    } else if (!(delta > 0.0)) {
-        S->cg_done = 1; S->cg_reason = CG_NOTSPD; S->cg_alpha = 0.0;
-    } else {
-        S->cg_alpha = gamma / delta;
-    }
-}
-
 struct RawInit {
     double rho;
     unsigned char m;
@@ -361,14 +319,14 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
         const bool col_ok = (i >= 0 && i < A.nx);
         Op5<BC> op;
         op.init(A, i);
-        const int rend = min(A.ny, j1 + H);
+        const int rend = min(A.rhi, j1 + H);
         double r_m2 = 0.0, r_m1 = 0.0;
         unsigned char m_m1 = 0;
         pipeline<NoPre, RawInit>(
             j0 - 1, j1 - j0 + 2, [&](int) { return NoPre{}; },
             [&](int r, NoPre) {
                 RawInit x{0.0, 0};
-                if (r >= 0 && r < rend) {
+                if (r >= A.rlo && r < rend) {
                     if (col_ok) {
                         const int v = i + A.pitch * r;
                         x.m = __ldg(mask + v);
@@ -407,34 +365,6 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
 // Loads of rho, p, w are predicated on the mask (active regions cost 1 B/pt),
 // with masks pipelined kPipe rows ahead of the data.
 // ============================================================================
-__device__ __forceinline__ void cg_finalize(double gamma, double delta, Scal* S) {
-    const double gamma_old = S->cg_gamma, alpha_old = S->cg_alpha;
-    const double dec = 0.5 * alpha_old * gamma_old;
-    const long long j = S->cg_it + 1;
-    S->cg_it = j;
-    S->cg_dec = dec;
-    int reason = CG_RUNNING;
-    if (j >= 2 && dec <= S->cg_eta2 * S->cg_maxdec) reason = CG_PROGRESS;
-    else if (sqrt(gamma) <= 1e-14 * (1.0 + S->cg_rnorm0)) reason = CG_EXACT;
-    else if (j >= S->cg_cap) reason = CG_CAP;
-    if (dec > S->cg_maxdec) S->cg_maxdec = dec;
-    S->cg_gamma = gamma;
-    if (reason != CG_RUNNING) {
-        S->cg_reason = reason;
-        S->cg_done = 1;
-        return;
-    }
-    const double beta = gamma / gamma_old;
-    const double pap = delta - beta * gamma / alpha_old;
-    S->cg_beta = beta;
-    if (!(pap > 0.0)) {
-        S->cg_reason = CG_NOTSPD;
-        S->cg_done = 1;
-        return;
-    }
-    S->cg_alpha = gamma / pap;
-}
-
 struct RawCg {
     double rho, p, w;
     unsigned char m;
@@ -457,7 +387,7 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
         const bool col_ok = (i >= 0 && i < A.nx);
         Op5<BC> op;
         op.init(A, i);
-        const int rend = min(A.ny, j1 + H);
+        const int rend = min(A.rhi, j1 + H);
         double pn_m2 = 0.0, pn_m1 = 0.0;          // pn(r-2), pn(r-1)
         double rho_m1 = 0.0;                       // rho(r-1)
         double w_m1 = 0.0, w_m2 = 0.0;             // w(r-1), w(r-2)
@@ -467,7 +397,7 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
             j0 - 2, j1 - j0 + 4,
             [&](int r) -> unsigned char {
                 unsigned char m = 0;
-                if (r >= 0 && r < rend) {
+                if (r >= A.rlo && r < rend) {
                     if (col_ok) m = __ldg(mask + i + A.pitch * r);
                 }
                 return m;

@@ -39,7 +39,8 @@ constexpr int kCtrF64 = TOX * TOY * 8;  // 15360 bytes (centre box, CG w)
 
 struct TileGeom {
     int nx, ny, pitch;
-    int ntx, nty;       // tiles per row / column
+    int ntx, nty;       // tiles per row / column (over the owned rows)
+    int rlo, rhi;       // readable rows (owned + ghost, StencilOp); the tensor maps start at row rlo
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -138,10 +139,10 @@ k3_cg_iter(StencilOp A, TileGeom T, const __grid_constant__ CUtensorMap m_rho, c
         unsigned char* st = smem + stage * L::kBytes;
         const int x0 = (t % T.ntx) * TOX, y0 = (t / T.ntx) * TOY;
         mbar_expect_tx(&bar[stage], L::kTx);
-        tma_load_2d(st + L::kRho, &m_rho, x0 - THALO, y0 - THALO, &bar[stage]);
-        tma_load_2d(st + L::kP, &m_p, x0 - THALO, y0 - THALO, &bar[stage]);
-        tma_load_2d(st + L::kW, &m_w, x0, y0, &bar[stage]);
-        tma_load_2d(st + L::kMask, &m_mask, floor16(x0 - THALO), y0 - THALO, &bar[stage]);
+        tma_load_2d(st + L::kRho, &m_rho, x0 - THALO, y0 - THALO - T.rlo, &bar[stage]);
+        tma_load_2d(st + L::kP, &m_p, x0 - THALO, y0 - THALO - T.rlo, &bar[stage]);
+        tma_load_2d(st + L::kW, &m_w, x0, y0 - T.rlo, &bar[stage]);
+        tma_load_2d(st + L::kMask, &m_mask, floor16(x0 - THALO), y0 - THALO - T.rlo, &bar[stage]);
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) mbar_init(&bar[s], 1);
@@ -184,7 +185,7 @@ k3_cg_iter(StencilOp A, TileGeom T, const __grid_constant__ CUtensorMap m_rho, c
         for (int q = threadIdx.x; q < TOX * TOY; q += kTileThreads) {
             const int r = THALO + q / TOX, c = THALO + q % TOX;
             const int kk = r * TBW + c;
-            if (m[r * MBW + c + moff]) {
+            if (m[r * MBW + c + moff] && y0 + r - THALO < T.ny) {     // owned rows only (ghost rows: the exchange)
                 const double rn = rho[kk];
                 const double qv = apply_box(F, rho, r, c);
                 acc[0] = fma(rn, rn, acc[0]);
@@ -249,7 +250,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
     const int ntiles = T.ntx * T.nty;
     const uint32_t bytes = kBoxF64 * (2 + (has_dir ? 1 : 0) + (SB ? 0 : 2)) + (has_mp ? MBW * TBH : 0);
     auto issue = [&](int t) {
-        const int x0 = (t % T.ntx) * TOX - THALO, y0 = (t / T.ntx) * TOY - THALO;
+        const int x0 = (t % T.ntx) * TOX - THALO, y0 = (t / T.ntx) * TOY - THALO - T.rlo;
         mbar_expect_tx(&bar[0], bytes);
         tma_load_2d(y, &m_y, x0, y0, &bar[0]);
         if (has_dir) tma_load_2d(dir, &m_dir, x0, y0, &bar[0]);
@@ -277,7 +278,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
         for (int q = threadIdx.x; q < TBW * TBH; q += kTileThreads) {
             const int r = q / TBW, c = q % TBW;
             const int gi = x0 - THALO + c, gj = y0 - THALO + r;
-            const bool in = gi >= 0 && gi < T.nx && gj >= 0 && gj < T.ny;
+            const bool in = gi >= 0 && gi < T.nx && gj >= T.rlo && gj < T.rhi;
             const double l = in ? (SB ? Bd.lc : lb[q]) : 0.0, u = in ? (SB ? Bd.uc : ub[q]) : 0.0;
             y[q] = has_dir ? trial(y[q], dir[q], sgn, alpha, l, u) : mid(l, u, y[q]);
         }
@@ -287,7 +288,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
             const int r = 1 + q / (TBW - 2), c = 1 + q % (TBW - 2);
             const int kk = r * TBW + c;
             const int gi = x0 - THALO + c, gj = y0 - THALO + r;
-            const bool in = gi >= 0 && gi < T.nx && gj >= 0 && gj < T.ny;
+            const bool in = gi >= 0 && gi < T.nx && gj >= T.rlo && gj < T.rhi;
             const double g = apply_box(F, y, r, c) - bd[kk];
             gn[kk] = g;
             const double l = in ? (SB ? Bd.lc : lb[kk]) : 0.0, u = in ? (SB ? Bd.uc : ub[kk]) : 0.0;
@@ -324,17 +325,7 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
             issue(t + gridDim.x);
         }
     }
-    reduce_and_finish<6>(acc, R, [&](double* tt) {
-        S->pg2 = tt[0];
-        S->g2 = tt[1];
-        S->n_active = tt[2];
-        S->n_changed = tt[3];
-        S->n_nonbinding = tt[4];
-        S->dd = tt[0];
-        S->dAd = tt[5];
-        S->cauchy_ok = (tt[5] > 0.0) ? 1 : 0;
-        S->alpha0 = (tt[5] > 0.0) ? tt[0] / tt[5] : 0.0;
-    });
+    reduce_and_finish<6>(acc, R, [&](double* tt) { fin_accept(tt, true, S); });
 }
 
 // ============================================================================
@@ -380,7 +371,7 @@ k3_search(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kS + 2 * kBoxF64 + sizeof(ColFaces));
     const int ntiles = T.ntx * T.nty;
     auto issue = [&](int t) {
-        const int x0 = (t % T.ntx) * TOX - THALO, y0 = (t / T.ntx) * TOY - THALO;
+        const int x0 = (t % T.ntx) * TOX - THALO, y0 = (t / T.ntx) * TOY - THALO - T.rlo;
         mbar_expect_tx(&bar[0], L::kBytes);
         tma_load_2d(smem + L::kY, &m_y, x0, y0, &bar[0]);
         tma_load_2d(smem + L::kD, &m_dir, x0, y0, &bar[0]);
@@ -405,7 +396,7 @@ k3_search(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
         for (int q = threadIdx.x; q < TBW * TBH; q += kTileThreads) {
             const int r = q / TBW, c = q % TBW;
             const int gi = x0 - THALO + c, gj = y0 - THALO + r;
-            const bool in = gi >= 0 && gi < T.nx && gj >= 0 && gj < T.ny;
+            const bool in = gi >= 0 && gi < T.nx && gj >= T.rlo && gj < T.rhi;
             const double l = in ? (SB ? Bd.lc : lb[q]) : 0.0, u = in ? (SB ? Bd.uc : ub[q]) : 0.0;
             const double yv = y[q], dv = dir[q];
             s0[q] = trial(yv, dv, sgn, al0, l, u) - yv;
@@ -431,20 +422,7 @@ k3_search(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
             issue(t + gridDim.x);
         }
     }
-    reduce_and_finish<2 * K>(acc, R, [&](double* tt) {
-        S->s_h = -1;
-        for (int h = 0; h < K; ++h) {
-            const double gs = tt[2 * h], sAs = tt[2 * h + 1];
-            const double dq = gs + 0.5 * sAs;
-            if (dq <= mu * gs) {
-                S->s_h = h0 + h;
-                S->s_alpha = scalbn(base, -(h0 + h));
-                S->s_delta = dq;
-                S->s_gs = gs;
-                break;
-            }
-        }
-    });
+    reduce_and_finish<2 * K>(acc, R, [&](double* tt) { fin_search(tt, K, h0, base, mu, S); });
 }
 
 }  // namespace gpcg

@@ -21,9 +21,10 @@ STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "ENOMEM", -3: "EC
                 -5: "ENOTSPD", -6: "ESEARCH", -7: "ESTATE"}
 
 # every symbol include/gpcg.h declares (checked by tests/test_abi.py)
-SYMBOLS = ["gpcg_params_default", "gpcg_create_stencil2d", "gpcg_create_csr", "gpcg_set_params",
-           "gpcg_solve", "gpcg_hessvec", "gpcg_project", "gpcg_objective", "gpcg_size",
-           "gpcg_destroy", "gpcg_last_error"]
+SYMBOLS = ["gpcg_params_default", "gpcg_create_stencil2d", "gpcg_create_stencil2d_dist", "gpcg_create_csr",
+           "gpcg_create_csr_dist", "gpcg_set_params", "gpcg_solve", "gpcg_hessvec", "gpcg_project",
+           "gpcg_objective", "gpcg_size", "gpcg_destroy", "gpcg_last_error", "gpcg_partition_rows",
+           "gpcg_nccl_unique_id"]
 
 
 class Params(C.Structure):
@@ -45,6 +46,12 @@ class Stats(C.Structure):
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Dist(C.Structure):
+    """gpcg_dist: the rank's row slab (include/gpcg.h)."""
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("local_slabs", C.c_int32)]
 
 
 class GpcgError(RuntimeError):
@@ -72,6 +79,15 @@ def load():
     L.gpcg_create_stencil2d.argtypes = [C.POINTER(P), P, i64, i64, P, i64, P, i64, P, P, P, P, dbl]
     L.gpcg_create_csr.restype = i32
     L.gpcg_create_csr.argtypes = [C.POINTER(P), P, i64, P, P, P, P, P, P, dbl]
+    L.gpcg_create_stencil2d_dist.restype = i32
+    L.gpcg_create_stencil2d_dist.argtypes = [C.POINTER(P), C.POINTER(Dist), P, i64, i64, P, i64, P, i64, P, P, P,
+                                             P, dbl]
+    L.gpcg_create_csr_dist.restype = i32
+    L.gpcg_create_csr_dist.argtypes = [C.POINTER(P), C.POINTER(Dist), P, i64, P, P, P, P, P, P, dbl]
+    L.gpcg_partition_rows.restype = None
+    L.gpcg_partition_rows.argtypes = [i64, C.c_int32, C.c_int32, C.POINTER(i64), C.POINTER(i64)]
+    L.gpcg_nccl_unique_id.restype = i32
+    L.gpcg_nccl_unique_id.argtypes = [P]
     L.gpcg_set_params.restype = i32
     L.gpcg_set_params.argtypes = [P, C.POINTER(Params)]
     L.gpcg_solve.restype = i32
@@ -140,6 +156,57 @@ def default_params() -> Params:
     return load().gpcg_params_default()
 
 
+# ---------------------------------------------------------------- row slabs (gpcg_dist)
+def partition_rows(total, parts, part):
+    """[begin, end) of part `part` of a balanced contiguous split of [0, total) (the C helper)."""
+    b, e = C.c_int64(), C.c_int64()
+    load().gpcg_partition_rows(int(total), int(parts), int(part), C.byref(b), C.byref(e))
+    return b.value, e.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load().gpcg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def problem_rows(prob):
+    """Rows the slab split runs over: grid rows (stencil2d) or matrix rows (CSR)."""
+    return prob.ny if prob.kind == "stencil2d" else prob.n
+
+
+def local_part(prob, row_begin, row_end):
+    """The arrays a rank owning global rows [row_begin, row_end) passes to the *_dist
+    creators (include/gpcg.h): its rows of b, l, u, x0, shift; its grid rows of
+    full x-face arrays and face rows row_begin..row_end of full y-face arrays; for
+    CSR its rows of row_ptr (rebased) / col (global ids) / val.  Host-side slicing
+    only."""
+    out = {}
+    if prob.kind == "stencil2d":
+        nx = prob.nx
+        sl = slice(row_begin * nx, row_end * nx)
+        for k in ("b", "l", "u", "x0"):
+            out[k] = np.ascontiguousarray(np.asarray(getattr(prob, k))[sl])
+        out["shift"] = None if prob.shift is None else np.ascontiguousarray(np.asarray(prob.shift)[sl])
+        wx = np.asarray(prob.wx)
+        wy = np.asarray(prob.wy)
+        out["wx"] = wx if not prob.wx_ld else np.ascontiguousarray(
+            wx[row_begin * prob.wx_ld:(row_end - 1) * prob.wx_ld + nx + 1])
+        out["wy"] = wy if not prob.wy_ld else np.ascontiguousarray(
+            wy[row_begin * prob.wy_ld:row_end * prob.wy_ld + nx])
+        out["n"] = (row_end - row_begin) * nx
+    else:
+        rp = np.asarray(prob.row_ptr, dtype=np.int64)
+        k0, k1 = int(rp[row_begin]), int(rp[row_end])
+        out["row_ptr"] = rp[row_begin:row_end + 1] - k0
+        out["col"] = np.ascontiguousarray(np.asarray(prob.col, dtype=np.int32)[k0:k1])
+        out["val"] = np.ascontiguousarray(np.asarray(prob.val, dtype=np.float64)[k0:k1])
+        for k in ("b", "l", "u", "x0"):
+            out[k] = np.ascontiguousarray(np.asarray(getattr(prob, k))[row_begin:row_end])
+        out["n"] = row_end - row_begin
+    return out
+
+
 class Solver:
     """One GPCG problem instance on the current CUDA device (wraps gpcg_problem*)."""
 
@@ -178,8 +245,43 @@ class Solver:
         return cls(h, n)
 
     @classmethod
-    def from_problem(cls, prob, stream=None, device=None):
-        """Create from a problems.Problem; device='cuda' uploads inputs as CUDA tensors first."""
+    def dist(cls, prob, rank=0, nranks=1, nccl_id=None, local_slabs=1, stream=None, device=None, local=None):
+        """The rank's slab of a problems.Problem (rows split by partition_rows) through
+        gpcg_create_*_dist.  Returns (solver, row_begin, row_end, local arrays).
+        local: precomputed local_part arrays (e.g. pinned copies) to pass instead."""
+        rb, re = partition_rows(problem_rows(prob), nranks, rank)
+        loc = local_part(prob, rb, re) if local is None else local
+        conv = (lambda a: a) if device is None else _to_device(device)
+        idbuf = None
+        if nranks > 1:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        d = Dist(rank, nranks, C.cast(idbuf, C.c_void_p) if idbuf is not None else None, rb, re, local_slabs)
+        L = load()
+        h = C.c_void_p()
+        keep = []
+
+        def P(a, dt=np.float64):
+            p, k = _ptr(None if a is None else conv(a), dt)
+            keep.append(k)
+            return p
+        if prob.kind == "stencil2d":
+            rc = L.gpcg_create_stencil2d_dist(C.byref(h), C.byref(d), _stream_ptr(stream), prob.nx, prob.ny,
+                                              P(loc["wx"]), prob.wx_ld, P(loc["wy"]), prob.wy_ld, P(loc["shift"]),
+                                              P(loc["b"]), P(loc["l"]), P(loc["u"]), float(prob.c))
+        else:
+            rc = L.gpcg_create_csr_dist(C.byref(h), C.byref(d), _stream_ptr(stream), prob.n,
+                                        P(loc["row_ptr"], np.int64), P(loc["col"], np.int32), P(loc["val"]),
+                                        P(loc["b"]), P(loc["l"]), P(loc["u"]), float(prob.c))
+        _check(rc)
+        return cls(h, loc["n"]), rb, re, loc
+
+    @classmethod
+    def from_problem(cls, prob, stream=None, device=None, slabs=1):
+        """Create from a problems.Problem; device='cuda' uploads inputs as CUDA tensors first.
+        slabs > 1: the same problem split into that many row slabs on this device (gpcg_dist
+        local_slabs; the multi-rank code path with device-copy halos)."""
+        if slabs > 1:
+            return cls.dist(prob, local_slabs=slabs, stream=stream, device=device)[0]
         conv = (lambda a: a) if device is None else _to_device(device)
         if prob.kind == "stencil2d":
             return cls.stencil2d(prob.nx, prob.ny, conv(prob.wx), prob.wx_ld, conv(prob.wy), prob.wy_ld,

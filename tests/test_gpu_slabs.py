@@ -1,0 +1,94 @@
+"""The multi-rank code path (row slabs, ghost-row halo exchange,
+per-slab partial sums combined in a fixed order, k_finalize on the global
+totals) on ONE GPU: gpcg_dist.local_slabs splits the problem into slabs whose
+halos are device copies -- the same kernels, exchange schedule and deferred
+reductions a multi-GPU run issues, with NCCL replaced by copies (the profiling
+guide forbids emulating ranks that wait on one another on one GPU; nothing here
+waits).  Compared with the CPU oracle on the same seeded inputs and with the
+single-slab solve."""
+import numpy as np
+import pytest
+
+from paper_cs_0101018_b200 import problems as P
+from tests.test_gpu_parity import G, abs_op, dense_problem, ragged_stencil, spmv_close, _tie_mismatches  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "C0": (lambda: P.c0(), -1e-12),
+    "C1": (lambda: P.c1(), -1e-11),
+    "ragged37x23_full_shift": (lambda: ragged_stencil(37, 23, 5), -1e-12),
+    "ragged29x17_bcast": (lambda: ragged_stencil(29, 17, 6, full=False, shift=False), -1e-12),
+    "c3_family_160": (lambda: P.c3_family(160, 160), -1e-11),
+    "c4_family_m12": (lambda: P.c4_family(m=12), -1e-11),
+    "dense12": (lambda: dense_problem(12, 31), -1e-12),
+}
+
+
+@pytest.mark.parametrize("slabs", [2, 3, 5])
+@pytest.mark.parametrize("case", list(CASES))
+def test_slab_solve_parity(G, oracle, case, slabs):
+    make, tol = CASES[case]
+    prob = make()
+    rows = prob.ny if prob.kind == "stencil2d" else prob.n
+    if rows < 2 * slabs:
+        pytest.skip("too few rows for this many slabs")
+    if case == "dense12" and slabs > 2:
+        # a dense row reaches every row: beyond the neighbouring slab -> documented EINVAL
+        with pytest.raises(G.GpcgError) as e:
+            G.Solver.from_problem(prob, slabs=slabs)
+        assert e.value.code == G.EINVAL
+        return
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    with G.Solver.from_problem(prob, slabs=slabs) as s:
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0 and rc_o == 0, (rc, st)
+    assert np.all(x >= prob.l) and np.all(x <= prob.u)
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
+    nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+    assert not nontie
+    A = oracle.problem_csr(prob)
+    pg = np.linalg.norm(oracle.proj_grad(x, oracle.gradient(A, prob.b, x), prob.l, prob.u))
+    assert pg <= 1.01 * st["tau"] + 1e-15
+
+
+@pytest.mark.parametrize("case", ["C1", "ragged37x23_full_shift", "ragged29x17_bcast", "c4_family_m12"])
+def test_slab_spmv_project(G, oracle, case):
+    prob = CASES[case][0]()
+    A = oracle.problem_csr(prob)
+    p = 2.0 * P.uniform(98, 1, prob.n) - 1.0
+    with G.Solver.from_problem(prob, slabs=3) as s:
+        y = s.hessvec(p)
+        spmv_close(y, oracle.spmv(A, p), abs_op(A, p))
+        px, pg2, na, nnb = s.project(prob.x0)
+        pref = oracle.project(prob.l, prob.u, prob.x0)
+        assert np.array_equal(px, pref)
+        g = oracle.gradient(A, prob.b, pref)
+        act, bnd, na_ref, nb_ref = oracle.sets(pref, g, prob.l, prob.u)
+        assert na == na_ref and nnb == na_ref - nb_ref
+        free = ~act
+        yr = s.hessvec(p, reduced=True)
+        spmv_close(yr, oracle.spmv_masked(A, free, p), abs_op(A, p * free))
+        q = s.objective(prob.x0)
+        qref = oracle.objective(A, prob.b, prob.c, prob.x0)
+        assert abs(q - qref) <= 1e-12 * max(abs(qref), 1e-300)
+
+
+def test_slab_matches_single_slab_iterates(G):
+    """Same iterates up to reduction order: identical outer/GP counts on C0, q to 1e-12."""
+    prob = P.c0()
+    with G.Solver.from_problem(prob) as s1:
+        rc1, x1, st1 = s1.solve(prob.x0, -1e-10)
+    with G.Solver.from_problem(prob, slabs=4) as s4:
+        rc4, x4, st4 = s4.solve(prob.x0, -1e-10)
+    assert rc1 == rc4 == 0
+    assert abs(st1["q"] - st4["q"]) <= 1e-12 * abs(st1["q"])
+    assert np.max(np.abs(x1 - x4)) <= 1e-9
+
+
+def test_slab_errors(G):
+    prob = ragged_stencil(9, 3, 2)
+    with pytest.raises(G.GpcgError) as e:
+        G.Solver.from_problem(prob, slabs=2)          # a slab of < 2 stencil rows
+    assert e.value.code == G.EINVAL
