@@ -177,8 +177,11 @@ struct Slab {
     CUtensorMap tm[NVEC];
     CUtensorMap tmm[NMSK];
     CUtensorMap tmWc;               // w, centre box (CG)
-    // TMA-fed column march (k4_cg_iter): band boxes of rho / p (x2), w, CG mask
-    CUtensorMap t4rho[2], t4p[2], t4w, t4m;
+    // TMA-fed column march (k4_*): 116-column band boxes of the vectors, the 112-column
+    // w box of the CG iteration, 144-byte mask boxes
+    CUtensorMap t4[NVEC];
+    CUtensorMap t4wo;
+    CUtensorMap t4m[NMSK];
     BandGeom bg{};
     int grid4 = 1;
 };
@@ -195,8 +198,9 @@ struct gpcg_problem {
     bool sb = false;                // scalar (constant) bounds
     bool bc = false;                // stencil with broadcast faces and no shift
     bool tile = false;              // TMA tile path built
-    int tile_mask = 15;             // GPCG_TILE bits: 1 accept, 2 search, 4 CG iteration (k3),
-                                    // 8 CG iteration as the TMA-fed column march (k4, preferred over 4)
+    int tile_mask = 63;             // GPCG_TILE bits: TMA tile kernels (k3) 1 accept, 2 search, 4 CG
+                                    // iteration; TMA-fed column march (k4, preferred) 8 CG, 16 accept,
+                                    // 32 search.  0 = column march (k2) only.
     int nx = 0, pitch = 1;          // stencil: grid width and row pitch (nx rounded up to 32); CSR: 1
     long long wx_ld = 0, wy_ld = 0; // user face layout (0 = broadcast)
     long long n_local = 0;          // entries owned by this rank (the user's arrays)
@@ -467,7 +471,15 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k3_search<true, false>, SrchStage<true, false>::kSmem));
     RC(set_smem(k3_search<false, true>, SrchStage<false, true>::kSmem));
     RC(set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem));
-    RC(set_smem(k4_cg_iter, m4::kSmem));
+    RC(set_smem(k4_cg_iter, m4cg::kSmem));
+    RC(set_smem(k4_accept<true, true>, AccLayout4<true, true>::kSmem));
+    RC(set_smem(k4_accept<true, false>, AccLayout4<true, false>::kSmem));
+    RC(set_smem(k4_accept<false, true>, AccLayout4<false, true>::kSmem));
+    RC(set_smem(k4_accept<false, false>, AccLayout4<false, false>::kSmem));
+    RC(set_smem(k4_search<true, true>, SrchLayout4<true, true>::kSmem));
+    RC(set_smem(k4_search<true, false>, SrchLayout4<true, false>::kSmem));
+    RC(set_smem(k4_search<false, true>, SrchLayout4<false, true>::kSmem));
+    RC(set_smem(k4_search<false, false>, SrchLayout4<false, false>::kSmem));
     auto resident = [&](auto kernel, int smem) {
         int nb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kTileThreads, smem);
@@ -479,7 +491,7 @@ int setup_tile(gpcg_problem* h) {
     const int r_srch = h->sb ? resident(k3_search<true, true>, SrchStage<true, true>::kSmem)
                              : resident(k3_search<false, true>, SrchStage<false, true>::kSmem);
     int nb4 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb4, k4_cg_iter, m4::kThreads, m4::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb4, k4_cg_iter, m4::kThreads, m4cg::kSmem);
     const int r4 = std::max(1, nb4) * h->sms;
     for (Slab& S : h->slabs) {
         for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
@@ -490,12 +502,10 @@ int setup_tile(gpcg_problem* h) {
                         S.rows + S.ghi};
         const int ntiles = S.tg.ntx * S.tg.nty;
         // k4: bands of 112 columns, each split into nsegs row segments: one item per resident CTA
-        for (int k = 0; k < 2; ++k) {
-            RC(make_map(h, S, &S.t4rho[k], S.v[vrho(k)], false, m4::kBW, m4::kBR));
-            RC(make_map(h, S, &S.t4p[k], S.v[vq(k)], false, m4::kBW, m4::kBR));
-        }
-        RC(make_map(h, S, &S.t4w, S.v[VW], false, m4::kOut, m4::kBR));
-        RC(make_map(h, S, &S.t4m, S.m[MKCG], true, m4::kMW, m4::kBR));
+        for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
+            RC(make_map(h, S, &S.t4[id], S.v[id], false, m4::kBW, m4::kBR));
+        RC(make_map(h, S, &S.t4wo, S.v[VW], false, m4::kOut, m4::kBR));
+        for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t4m[k], S.m[k], true, m4::kMW, m4::kBR));
         S.bg.nbands = (h->nx + m4::kOut - 1) / m4::kOut;
         S.bg.nsegs = std::max(1, std::min(r4 / S.bg.nbands, (S.rows + 15) / 16));
         S.bg.seg = (S.rows + S.bg.nsegs - 1) / S.bg.nsegs;
@@ -660,12 +670,25 @@ int layout_slabs(gpcg_problem* h, long long rows_rank, int nsl, int ghost) {
 
 // ---------------------------------------------------------------- launches (every slab)
 int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev, int y_out, int g_out, int m_out) {
-    const bool use_tile = h->tile && (h->tile_mask & 1);
+    const bool use_k4 = h->tile && (h->tile_mask & 16);
+    const bool use_tile = h->tile && (h->tile_mask & (1 | 16));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
         const RedScratch R = h->red(s);
-        if (use_tile) {
+        if (use_k4) {
+            const CUtensorMap& md = S.t4[dir >= 0 ? dir : y_in];
+            const CUtensorMap& mp = S.t4m[mask_prev >= 0 ? mask_prev : MK0];
+            const int has_mp = mask_prev >= 0 ? 1 : 0;
+            auto go = [&](auto sbt, auto hdt) {
+                constexpr bool SB = decltype(sbt)::value, HD = decltype(hdt)::value;
+                k4_accept<SB, HD><<<S.grid4, m4::kThreads, AccLayout4<SB, HD>::kSmem, h->st>>>(
+                    S.sop, S.bg, B, S.t4[y_in], md, S.t4[VB], S.t4[VL], S.t4[VU], mp, has_mp, sgn, S.v[y_out],
+                    S.v[g_out], S.m[m_out], h->dS, R);
+            };
+            if (h->sb) { if (dir >= 0) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+            else { if (dir >= 0) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else if (use_tile) {
             const CUtensorMap& md = S.tm[dir >= 0 ? dir : y_in];
             const CUtensorMap& mp = S.tmm[mask_prev >= 0 ? mask_prev : MK0];
             if (h->sb)
@@ -734,12 +757,21 @@ int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
 int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_alpha0, int h0, int K) {
     const double mu = h->prm.mu;
     const bool dg = (dir == g);
-    const bool use_tile = h->tile && (h->tile_mask & 2) && K == 2;   // retries use the column march
+    const bool use_k4 = h->tile && (h->tile_mask & 32) && K == 2;  // retries use the column march
+    const bool use_tile = h->tile && (h->tile_mask & 2) && K == 2;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
         const RedScratch R = h->red(s);
-        if (use_tile) {
+        if (use_k4) {
+            auto go = [&](auto sbt, auto dgt) {
+                constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
+                k4_search<SB, DG><<<S.grid4, m4::kThreads, SrchLayout4<SB, DG>::kSmem, h->st>>>(
+                    S.sop, S.bg, B, S.t4[y], S.t4[dir], S.t4[g], S.t4[VL], S.t4[VU], sgn, use_alpha0, h0, mu, h->dS, R);
+            };
+            if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+            else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else if (use_tile) {
             auto go = [&](auto sbt, auto dgt) {
                 constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
                 k3_search<SB, DG><<<S.grid_t_srch, kTileThreads, SrchStage<SB, DG>::kSmem, h->st>>>(
@@ -822,8 +854,9 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
         if (use_k4) {
-            k4_cg_iter<<<S.grid4, m4::kThreads, m4::kSmem, h->st>>>(S.sop, S.bg, S.t4rho[a], S.t4p[a], S.t4w, S.t4m,
-                                                                   S.v[vrho(bb)], S.v[vq(bb)], S.v[VW], h->dS, R);
+            k4_cg_iter<<<S.grid4, m4::kThreads, m4cg::kSmem, h->st>>>(S.sop, S.bg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo,
+                                                                     S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
+                                                                     h->dS, R);
         } else if (use_tile) {
             k3_cg_iter<2><<<S.grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
                 S.sop, S.tg, S.tm[vrho(a)], S.tm[vq(a)], S.tmWc, S.tmm[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
@@ -1078,7 +1111,7 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
     h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
     {
         const char* e = getenv("GPCG_TILE");
-        if (e && *e) h->tile_mask = atoi(e) & 15;
+        if (e && *e) h->tile_mask = atoi(e) & 63;
         if (h->bc && !h->generic && h->tile_mask != 0 && (rc = setup_tile(h))) return fail(rc);
     }
     h->nnz = 5 * h->n_global - 2 * nx - 2 * ny;

@@ -1,22 +1,25 @@
 // march_tma.cuh -- TMA-fed column march (sm_100a) for the broadcast-face
-// 5-point operator (journal-bearing family C0 / C2 / C3): the CG iteration (a5)
-// of SURVEY.md 8(a).
+// 5-point operator (journal-bearing family C0 / C2 / C3): the CG iteration (a5),
+// the fused accept / regrad / Cauchy sweep (a1 + a2) and the projected search
+// (a3) of SURVEY.md 8(a).
 //
 // Work item = a BAND of 4 x 28 = 112 output columns (one warp per 28-column
-// strip, 2 halo lanes per side, as in march.cuh) times a SEGMENT of kSeg grid
-// rows.  The raw rows of the segment plus 2 rows of warm-up on each side stream
+// strip, 2 halo lanes per side, as in march.cuh) times a SEGMENT of grid rows.
+// The raw rows of the segment plus 2 rows of warm-up on each side stream
 // through shared memory in blocks of kBR rows: one thread issues
-// cp.async.bulk.tensor.2d loads (rho, p, w boxes of 116 / 112 columns and a u8
-// mask box) up to kNST blocks ahead, completion counted on one mbarrier per
-// stage.  The warps march down the block rows with the column-march recurrences
-// of k2_cg_iter (values at west / east neighbours by warp shuffle, north /
-// south from a register window), so each raw value is read from shared memory
-// once -- the smem traffic of the tile kernels' five-point reads is gone, and
-// no register ring is needed to hide HBM latency.  CTAs are persistent over
-// the items; the load pipeline runs across item boundaries.
+// cp.async.bulk.tensor.2d loads (f64 boxes 116 columns wide, u8 mask boxes) up
+// to NST blocks ahead, completion counted on one mbarrier per stage.  The
+// warps march down the block rows with the column-march recurrences of
+// march.cuh (values at west / east neighbours by warp shuffle, north / south
+// from a register window), so each raw value is read from shared memory once
+// and no register ring is needed to hide HBM latency.  Out-of-grid rows and
+// columns are zero-filled by the TMA unit (the Dirichlet boundary; ghost rows
+// of a slab are inside the tensor).  Each CTA takes one (band, segment) item
+// (grid = bands x segments sized to the resident CTAs); the loop is persistent
+// for grids wider than that, with the load pipeline running across items.
 //
-// Same arithmetic and reduction structure as k2_cg_iter / k3_cg_iter; checked
-// against the CPU oracle by the same tests.
+// Same arithmetic and reduction structure as the k2_* kernels; checked against
+// the CPU oracle by the same tests.
 #pragma once
 
 #include "common.cuh"
@@ -32,125 +35,340 @@ constexpr int kThreads = 32 * kWarps;
 constexpr int kOut = 28 * kWarps;         // 112 output columns per band
 constexpr int kBW = kOut + 4;             // 116 box columns (2 halo each side)
 constexpr int kBR = 8;                    // rows per pipeline block
-constexpr int kNST = 4;                   // pipeline stages
 constexpr int kMW = 144;                  // u8 mask box width (start floored to 16 B, 116 + 15 < 144)
-constexpr int kRowF = kBW * 8;            // 928 B per f64 box row
-constexpr int kRho = 0;
-constexpr int kP = kBR * kRowF;                       // 7424
-constexpr int kW = 2 * kBR * kRowF;                   // 14848
-constexpr int kM = kW + kBR * kOut * 8;               // 14848 + 7168 = 22016
-constexpr int kStage = kM + kBR * kMW;                // 22016 + 1152 = 23168 (multiple of 128)
-constexpr int kTx = 2 * kBR * kBW * 8 + kBR * kOut * 8 + kBR * kMW;
-constexpr int kSmem = kNST * kStage + 64;
-static_assert(kStage % 128 == 0, "stage alignment");
+constexpr int kF = kBR * kBW * 8;         // 7424 B: one f64 band box
+constexpr int kFo = kBR * kOut * 8;       // 7168 B: one f64 box of the output columns only
+constexpr int kU = kBR * kMW;             // 1152 B: one u8 mask box
+static_assert(kF % 128 == 0 && kFo % 128 == 0 && kU % 128 == 0, "TMA destinations stay 128-byte aligned");
 }  // namespace m4
 
 struct BandGeom {
-    int nbands, nsegs, seg;     // items = nbands * nsegs; rows [s*seg, min((s+1)*seg, ny))
+    int nbands, nsegs, seg;     // items = nbands * nsegs; item rows [s*seg, min((s+1)*seg, ny))
     int rlo;                    // first tensor row (StencilOp::rlo)
 };
 
-// CG iteration, same recurrences as k2_cg_iter:
+// The pipeline engine.  issue(stage_ptr, x0, yr, bar): TMA loads of the block whose
+// first raw row is yr (band output columns start at x0); begin(x0, y0, y1): a new
+// item; row(stage_ptr, kk, r): one raw row (kk-th of the block).
+template <int NST, int STAGE, class Issue, class Begin, class Row>
+__device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
+                                              Begin&& begin, Row&& row) {
+    using namespace m4;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+    const int nitems = G.nbands * G.nsegs;
+    const int nblk = (G.seg + 4 + kBR - 1) / kBR;          // raw rows y0-2 .. y1+2
+    auto issue = [&](int k) {
+        const int i = k / nblk, b = k - i * nblk;
+        const int t = blockIdx.x + i * (int)gridDim.x;
+        if (t >= nitems) return;
+        const int stage = k % NST;
+        const int x0 = (t % G.nbands) * kOut;
+        const int yr = (t / G.nbands) * G.seg - 2 + b * kBR;
+        issue_loads(smem + stage * STAGE, x0, yr, &bar[stage]);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        for (int k = 0; k < NST; ++k) issue(k);
+    }
+    __syncthreads();
+    int k = 0;
+    for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
+        const int x0 = (t % G.nbands) * kOut;
+        const int y0 = (t / G.nbands) * G.seg, y1 = min(y0 + G.seg, ny);
+        begin(x0, y0, y1);
+        for (int b = 0; b < nblk; ++b, ++k) {
+            const int stage = k % NST;
+            unsigned char* st = smem + stage * STAGE;
+            mbar_wait(&bar[stage], (k / NST) & 1);
+            const int yr = y0 - 2 + b * kBR;
+#pragma unroll
+            for (int kk = 0; kk < kBR; ++kk) row(st, kk, yr + kk);
+            __syncthreads();                              // every warp is done with this stage
+            if (threadIdx.x == 0) {
+                fence_proxy_async();
+                issue(k + NST);
+            }
+        }
+    }
+}
+
+// ============================================================================
+// a5: CG iteration, same recurrences as k2_cg_iter:
 //   level 1  pn(r)   = [r in F] (rho(r) + beta p(r))
 //   level 2  rn(r-1) = [r-1 in F] (rho(r-1) - alpha (A pn)(r-1))
 //   level 3  q(r-2)  = (A rn)(r-2);  emit r-2 (free points): w += alpha pn, rho' = rn, p' = pn,
 //            gamma += rn^2, delta += rn q
+// Stage: rho | p (band boxes, rows yr..) | w (output columns, rows yr-2..) | mask (rows yr..)
+// ============================================================================
+namespace m4cg {
+using namespace m4;
+constexpr int kRho = 0, kP = kF, kW = 2 * kF, kM = 2 * kF + kFo;
+constexpr int kStage = kM + kU;                       // 23168
+constexpr int kNST = 4;
+constexpr int kSmem = kNST * kStage + 64;
+}  // namespace m4cg
+
 __global__ void __launch_bounds__(m4::kThreads, 2)
 k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, const __grid_constant__ CUtensorMap m_p,
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
            double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R) {
-    using namespace m4;
+    using namespace m4cg;
     if (*(volatile int*)&S->cg_done) return;
     const double alpha = S->cg_alpha, beta = S->cg_beta;
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kNST * kStage);
-    const int nitems = G.nbands * G.nsegs;
-    const int nblk_item = (G.seg + 4 + kBR - 1) / kBR;    // blocks per item (raw rows y0-2 .. y1+2)
-
-    // flat block sequence of this CTA: (item t = blockIdx.x + i*gridDim.x, block b)
-    auto block_of = [&](int k, int& t, int& b) {
-        const int i = k / nblk_item;
-        t = blockIdx.x + i * (int)gridDim.x;
-        b = k - i * nblk_item;
-        return t < nitems;
-    };
-    auto issue = [&](int k) {
-        int t, b;
-        if (!block_of(k, t, b)) return;
-        const int stage = k % kNST;
-        unsigned char* st = smem + stage * kStage;
-        const int band = t % G.nbands, segi = t / G.nbands;
-        const int x0 = band * kOut;                       // first output column
-        const int yr = segi * G.seg - 2 + b * kBR;        // first raw row of the block
-        mbar_expect_tx(&bar[stage], kTx);
-        tma_load_2d(st + kRho, &m_rho, x0 - 2, yr - G.rlo, &bar[stage]);
-        tma_load_2d(st + kP, &m_p, x0 - 2, yr - G.rlo, &bar[stage]);
-        tma_load_2d(st + kW, &m_w, x0, yr - 2 - G.rlo, &bar[stage]);    // w of the emitted rows (r - 2)
-        tma_load_2d(st + kM, &m_mask, floor16(x0 - 2), yr - G.rlo, &bar[stage]);
-    };
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kNST; ++s) mbar_init(&bar[s], 1);
-        fence_mbar_init();
-        for (int k = 0; k < kNST; ++k) issue(k);
-    }
-    __syncthreads();
-
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int c = 28 * wid + lane;                        // box column of this lane
     const bool out_lane = lane >= 2 && lane < 30;
     double acc[2] = {0.0, 0.0};
-    int k = 0;
-    for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
-        const int band = t % G.nbands, segi = t / G.nbands;
-        const int x0 = band * kOut;
-        const int gx = x0 - 2 + c;                        // grid column of this lane
-        const int moff = (x0 - 2) - floor16(x0 - 2);
-        const int y0 = segi * G.seg, y1 = min(y0 + G.seg, A.ny);
-        const bool col_ok = gx >= 0 && gx < A.nx;
-        Op5<true> op;
-        op.init(A, gx);
-        double pn_m2 = 0.0, pn_m1 = 0.0, rho_m1 = 0.0, rn_m3 = 0.0, rn_m2 = 0.0;
-        unsigned char m_m1 = 0, m_m2 = 0;
-        for (int b = 0; b < nblk_item; ++b, ++k) {
-            const int stage = k % kNST;
-            const unsigned char* st = smem + stage * kStage;
+    int gx = 0, moff = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double pn_m2 = 0.0, pn_m1 = 0.0, rho_m1 = 0.0, rn_m3 = 0.0, rn_m2 = 0.0;
+    unsigned char m_m1 = 0, m_m2 = 0;
+    band_pipeline<kNST, kStage>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, kStage);
+            tma_load_2d(st + kRho, &m_rho, x0 - 2, yr - G.rlo, bar);
+            tma_load_2d(st + kP, &m_p, x0 - 2, yr - G.rlo, bar);
+            tma_load_2d(st + kW, &m_w, x0, yr - 2 - G.rlo, bar);      // w of the emitted rows (r - 2)
+            tma_load_2d(st + kM, &m_mask, floor16(x0 - 2), yr - G.rlo, bar);
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 2 + c;
+            moff = (x0 - 2) - floor16(x0 - 2);
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            pn_m2 = pn_m1 = rho_m1 = rn_m3 = rn_m2 = 0.0;
+            m_m1 = m_m2 = 0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
             const double* rhoS = reinterpret_cast<const double*>(st + kRho);
             const double* pS = reinterpret_cast<const double*>(st + kP);
             const double* wS = reinterpret_cast<const double*>(st + kW);
-            const unsigned char* mS = st + kM;
-            mbar_wait(&bar[stage], (k / kNST) & 1);
-            const int yr = y0 - 2 + b * kBR;
-#pragma unroll
-            for (int kk = 0; kk < kBR; ++kk) {
-                const int r = yr + kk;
-                const unsigned char m = mS[kk * kMW + c + moff];
-                const double rho = rhoS[kk * kBW + c];
-                const double pn0 = m ? fma(beta, pS[kk * kBW + c], rho) : 0.0;
-                const double ap = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
-                const double rn1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
-                const double q = op.apply(A, r - 2, rn_m2, rn_m3, rn1);
-                const int r2 = r - 2;
-                if (out_lane && m_m2 && col_ok && r2 >= y0 && r2 < y1) {
-                    const long long v = (long long)gx + (long long)A.pitch * r2;
-                    w_out[v] = fma(alpha, pn_m2, wS[kk * kOut + c - 2]);
-                    rho_n[v] = rn_m2;
-                    p_n[v] = pn_m2;
-                    acc[0] = fma(rn_m2, rn_m2, acc[0]);
-                    acc[1] = fma(rn_m2, q, acc[1]);
-                }
-                pn_m2 = pn_m1; pn_m1 = pn0;
-                rho_m1 = rho;
-                m_m2 = m_m1; m_m1 = m;
-                rn_m3 = rn_m2; rn_m2 = rn1;
+            const unsigned char m = st[kM + kk * kMW + c + moff];
+            const double rho = rhoS[kk * kBW + c];
+            const double pn0 = m ? fma(beta, pS[kk * kBW + c], rho) : 0.0;
+            const double ap = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
+            const double rn1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
+            const double q = op.apply(A, r - 2, rn_m2, rn_m3, rn1);
+            const int r2 = r - 2;
+            if (out_lane && m_m2 && col_ok && r2 >= y0 && r2 < y1) {
+                const long long v = (long long)gx + (long long)A.pitch * r2;
+                w_out[v] = fma(alpha, pn_m2, wS[kk * kOut + c - 2]);
+                rho_n[v] = rn_m2;
+                p_n[v] = pn_m2;
+                acc[0] = fma(rn_m2, rn_m2, acc[0]);
+                acc[1] = fma(rn_m2, q, acc[1]);
             }
-            __syncthreads();                              // every warp is done with this stage
-            if (threadIdx.x == 0) {
-                fence_proxy_async();
-                issue(k + kNST);
-            }
-        }
-    }
+            pn_m2 = pn_m1; pn_m1 = pn0;
+            rho_m1 = rho;
+            m_m2 = m_m1; m_m1 = m;
+            rn_m3 = rn_m2; rn_m2 = rn1;
+        });
     reduce_and_finish<2>(acc, R, [&](double* tt) { cg_finalize(tt[0], tt[1], S); });
+}
+
+// ============================================================================
+// a1 + a2 fused (as k2_accept): accept / project, regrad, free mask, set counts
+// and the Cauchy form of the new point.
+//   level 1  yn(r)   = mid(l, u, y(r) + alpha sgn dir(r))   (or mid(l, u, y) without dir)
+//   level 2  gn(r-1) = (A yn)(r-1) - b,  d(r-1) = grad_Omega q(yn)(r-1)
+//   level 3  Ad(r-2) = (A d)(r-2);  emit row r-2
+// Stage: y | dir | b | l | u (band boxes, rows yr..; dir, l/u optional) | mask_prev (rows yr-2..)
+// ============================================================================
+template <bool SB, bool HasDir>
+struct AccLayout4 {
+    static constexpr int kY = 0;
+    static constexpr int kD = m4::kF;
+    static constexpr int kB = kD + (HasDir ? m4::kF : 0);
+    static constexpr int kL = kB + m4::kF;
+    static constexpr int kU = kL + (SB ? 0 : m4::kF);
+    static constexpr int kMP = kU + (SB ? 0 : m4::kF);
+    static constexpr int kStage = kMP + m4::kU;
+    static constexpr int kNST = SB ? 4 : 3;
+    static constexpr int kSmem = kNST * kStage + 64;
+};
+
+template <bool SB, bool HasDir>
+__global__ void __launch_bounds__(m4::kThreads, 2)
+k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMap m_y,
+          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
+          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
+          const __grid_constant__ CUtensorMap m_mp, int has_mp, double sgn, double* __restrict__ y_out,
+          double* __restrict__ g_out, unsigned char* __restrict__ mask_out, Scal* S, RedScratch R) {
+    using namespace m4;
+    using L = AccLayout4<SB, HasDir>;
+    double alpha = 0.0;
+    if (HasDir) {
+        if (S->s_h < 0) return;                   // uniform: no accepted step in this batch
+        alpha = S->s_alpha;
+    }
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 28 * wid + lane;
+    const bool out_lane = lane >= 2 && lane < 30;
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int gx = 0, moff = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double yn_m2 = 0.0, yn_m1 = 0.0, b_m1 = 0.0, l_m1 = 0.0, u_m1 = 0.0, l_m2 = 0.0, u_m2 = 0.0;
+    double gn_m2 = 0.0, d_m3 = 0.0, d_m2 = 0.0;
+    const uint32_t tx = L::kStage - (has_mp ? 0 : kU);
+    band_pipeline<L::kNST, L::kStage>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, tx);
+            const int yt = yr - G.rlo;
+            tma_load_2d(st + L::kY, &m_y, x0 - 2, yt, bar);
+            if (HasDir) tma_load_2d(st + L::kD, &m_dir, x0 - 2, yt, bar);
+            tma_load_2d(st + L::kB, &m_b, x0 - 2, yt, bar);
+            if (!SB) {
+                tma_load_2d(st + L::kL, &m_l, x0 - 2, yt, bar);
+                tma_load_2d(st + L::kU, &m_u, x0 - 2, yt, bar);
+            }
+            if (has_mp) tma_load_2d(st + L::kMP, &m_mp, floor16(x0 - 2), yt - 2, bar);
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 2 + c;
+            moff = (x0 - 2) - floor16(x0 - 2);
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            yn_m2 = yn_m1 = b_m1 = l_m1 = u_m1 = l_m2 = u_m2 = gn_m2 = d_m3 = d_m2 = 0.0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const int q = kk * kBW + c;
+            // raw values; outside the readable rows / columns the bounds are 0 so yn = 0 (Dirichlet)
+            const bool in = col_ok && r >= A.rlo && r < A.rhi;
+            const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
+            const double bv = reinterpret_cast<const double*>(st + L::kB)[q];
+            const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
+            const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
+            double yn0;
+            if constexpr (HasDir) yn0 = trial(yv, reinterpret_cast<const double*>(st + L::kD)[q], sgn, alpha, lv, uv);
+            else yn0 = mid(lv, uv, yv);
+            const double ay = op.apply(A, r - 1, yn_m1, yn_m2, yn0);
+            const double gn1 = ay - b_m1;
+            const double d1 = pgrad(yn_m1, gn1, l_m1, u_m1);      // 0 outside the grid
+            const double ad = op.apply(A, r - 2, d_m2, d_m3, d1);
+            const int r2 = r - 2;
+            if (out_lane && col_ok && r2 >= y0 && r2 < y1) {
+                const long long v = (long long)gx + (long long)A.pitch * r2;
+                y_out[v] = yn_m2;
+                g_out[v] = gn_m2;
+                const bool act = (yn_m2 == l_m2) || (yn_m2 == u_m2);
+                const unsigned char m = act ? 0 : 1;
+                mask_out[v] = m;
+                acc[0] = fma(d_m2, d_m2, acc[0]);
+                acc[1] = fma(gn_m2, gn_m2, acc[1]);
+                acc[2] += act ? 1.0 : 0.0;
+                if (has_mp) acc[3] += (st[L::kMP + kk * kMW + c + moff] != m) ? 1.0 : 0.0;
+                const bool binding = (yn_m2 == l_m2 && gn_m2 >= 0.0) || (yn_m2 == u_m2 && gn_m2 <= 0.0);
+                acc[4] += (act && !binding) ? 1.0 : 0.0;
+                acc[5] = fma(d_m2, ad, acc[5]);
+            }
+            yn_m2 = yn_m1; yn_m1 = yn0;
+            l_m2 = l_m1; u_m2 = u_m1;
+            l_m1 = lv; u_m1 = uv; b_m1 = bv;
+            gn_m2 = gn1;
+            d_m3 = d_m2; d_m2 = d1;
+        });
+    reduce_and_finish<6>(acc, R, [&](double* t) { fin_accept(t, true, S); });
+}
+
+// ============================================================================
+// a3: projected search, K = 2 step sizes per sweep (as k2_search, H = 1; the
+// band's 2-lane halo is kept, only the 28 centre lanes accumulate).
+//   level 1  s_h(r) = mid(l, u, y + alpha_h sgn dir) - y
+//   level 2  sums <g, s_h>(r-1), <s_h, A s_h>(r-1)
+// Stage: y | dir | g (if dir != g) | l | u (if array bounds)
+// ============================================================================
+template <bool SB, bool DG>
+struct SrchLayout4 {
+    static constexpr int kY = 0;
+    static constexpr int kD = m4::kF;
+    static constexpr int kG = DG ? kD : kD + m4::kF;
+    static constexpr int kL = kG + m4::kF;
+    static constexpr int kU = kL + (SB ? 0 : m4::kF);
+    static constexpr int kStage = kU + (SB ? 0 : m4::kF);
+    static constexpr int kNST = 4;
+    static constexpr int kSmem = kNST * kStage + 64;
+};
+
+template <bool SB, bool DG>
+__global__ void __launch_bounds__(m4::kThreads, 2)
+k4_search(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMap m_y,
+          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_g,
+          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, double sgn,
+          int use_alpha0, int h0, double mu, Scal* S, RedScratch R) {
+    using namespace m4;
+    using L = SrchLayout4<SB, DG>;
+    constexpr int K = 2;
+    if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
+        if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
+        return;
+    }
+    const double base = use_alpha0 ? S->alpha0 : 1.0;
+    const double al0 = scalbn(base, -h0), al1 = scalbn(base, -(h0 + 1));
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 28 * wid + lane;
+    const bool out_lane = lane >= 2 && lane < 30;
+    double acc[2 * K] = {0.0, 0.0, 0.0, 0.0};
+    int gx = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double s0_m2 = 0.0, s0_m1 = 0.0, s1_m2 = 0.0, s1_m1 = 0.0, g_m1 = 0.0;
+    band_pipeline<L::kNST, L::kStage>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, L::kStage);
+            const int yt = yr - G.rlo;
+            tma_load_2d(st + L::kY, &m_y, x0 - 2, yt, bar);
+            tma_load_2d(st + L::kD, &m_dir, x0 - 2, yt, bar);
+            if (!DG) tma_load_2d(st + L::kG, &m_g, x0 - 2, yt, bar);
+            if (!SB) {
+                tma_load_2d(st + L::kL, &m_l, x0 - 2, yt, bar);
+                tma_load_2d(st + L::kU, &m_u, x0 - 2, yt, bar);
+            }
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 2 + c;
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            s0_m2 = s0_m1 = s1_m2 = s1_m1 = g_m1 = 0.0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const int q = kk * kBW + c;
+            const bool in = col_ok && r >= A.rlo && r < A.rhi;
+            const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
+            const double dv = reinterpret_cast<const double*>(st + L::kD)[q];
+            const double gv = reinterpret_cast<const double*>(st + L::kG)[q];
+            const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
+            const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
+            const double s0 = trial(yv, dv, sgn, al0, lv, uv) - yv;      // 0 outside
+            const double s1 = trial(yv, dv, sgn, al1, lv, uv) - yv;
+            const double a0 = op.apply(A, r - 1, s0_m1, s0_m2, s0);
+            const double a1 = op.apply(A, r - 1, s1_m1, s1_m2, s1);
+            const int r1 = r - 1;
+            if (out_lane && col_ok && r1 >= y0 && r1 < y1) {
+                acc[0] = fma(g_m1, s0_m1, acc[0]);
+                acc[1] = fma(s0_m1, a0, acc[1]);
+                acc[2] = fma(g_m1, s1_m1, acc[2]);
+                acc[3] = fma(s1_m1, a1, acc[3]);
+            }
+            s0_m2 = s0_m1; s0_m1 = s0;
+            s1_m2 = s1_m1; s1_m1 = s1;
+            g_m1 = gv;
+        });
+    reduce_and_finish<2 * K>(acc, R, [&](double* tt) { fin_search(tt, K, h0, base, mu, S); });
 }
 
 }  // namespace gpcg
