@@ -51,6 +51,8 @@ typedef struct {
     int64_t max_halvings; /* projected-search trials, 50 (R13)                                    */
     int64_t cg_cap;       /* 0 => m_k, the finite-termination bound P:444-447                     */
     double time_budget_s; /* 0 => none; else stop (NOT_CONVERGED) once exceeded (bounded samples) */
+    int64_t precond;      /* 0: plain CG (the hot path); 1: point-Jacobi PCG, M = diag(A_k)
+                             (the "diagonal Jacobi preconditioner" of P:1096-1098, Table 4)       */
 } ora_params;
 
 typedef struct {
@@ -288,26 +290,32 @@ int64_t ora_projected_search(int64_t n, const int64_t *rp, const int32_t *ci, co
 /* ------------------------------------------------------------------------ */
 
 /* Textbook CG (Hestenes-Stiefel) on A_k w = -r_k, w_0 = 0 (Alg. GPCG),
- * vectors embedded in R^n and zero off the free set.  Stops at the first j with
+ * vectors embedded in R^n and zero off the free set; with dinv != NULL the
+ * preconditioned (PCG) form with M^{-1} = diag(dinv) on the free set (point
+ * Jacobi: dinv_i = 1 / A_ii), z_j = M^{-1} rho_j.  Stops at the
+ * first j with
  *   (a) j >= 2 and q_k(w_{j-1}) - q_k(w_j) <= eta2 max_{l<j} (q_k(w_{l-1}) - q_k(w_l))
  *       (Eq. cgstop1; from j >= 2, reading R10), where the decrease of
- *       step j is 1/2 alpha_j rho_j'rho_j (reading R17);
- *   (b) ||rho_j|| <= 1e-14 (1 + ||r_k||)   (machine-precision guard);
+ *       step j is 1/2 alpha_j rho_j'z_j (reading R17; z = rho without M);
+ *   (b) sqrt(rho_j'z_j) <= 1e-14 (1 + sqrt(rho_0'z_0))   (machine-precision guard,
+ *       SPEC S:371; the M^{-1}-norm of the residual under PCG, reading R28);
  *   (c) j = cap.
  * Returns w_j at that j (reading R11).  Returns the iteration count, or
- * ORA_ENOTSPD (negative) on <p, A_k p> <= 0.  work: 3n doubles. decs (nullable,
+ * ORA_ENOTSPD (negative) on <p, A_k p> <= 0.  work: 4n doubles. decs (nullable,
  * length >= cap) receives the per-step decreases. */
-int64_t ora_cg(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
-               const unsigned char *free_, const double *r, double eta2, int64_t cap,
-               double *w, double *work, double *decs, double deadline)
+int64_t ora_pcg(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                const unsigned char *free_, const double *r, const double *dinv, double eta2, int64_t cap,
+                double *w, double *work, double *decs, double deadline)
 {
     double *rho = work, *p = work + n, *a = work + 2 * n;
+    double *z = dinv ? work + 3 * n : rho;
     for (int64_t i = 0; i < n; i++) {
         rho[i] = free_[i] ? -r[i] : 0.0;
-        p[i] = rho[i];
+        if (dinv) z[i] = free_[i] ? rho[i] * dinv[i] : 0.0;
+        p[i] = z[i];
         w[i] = 0.0;
     }
-    double rr = dot(n, rho, rho);
+    double rr = dot(n, rho, z);
     double rnorm0 = sqrt(rr);
     double maxdec = 0.0;
     int64_t it = 0;
@@ -322,17 +330,38 @@ int64_t ora_cg(int64_t n, const int64_t *rp, const int32_t *ci, const double *va
         double dec = 0.5 * alpha * rr;
         if (decs) decs[it - 1] = dec;
         for (int64_t i = 0; i < n; i++) rho[i] = rho[i] - alpha * a[i];
-        double rr_new = dot(n, rho, rho);
+        if (dinv)
+            for (int64_t i = 0; i < n; i++) z[i] = free_[i] ? rho[i] * dinv[i] : 0.0;
+        double rr_new = dot(n, rho, z);
         int stop = (it >= 2 && dec <= eta2 * maxdec) ||
                    (sqrt(rr_new) <= 1e-14 * (1.0 + rnorm0)) || (it >= cap) ||
                    (deadline > 0.0 && now_s() > deadline);  /* bounded-sample timing only */
         if (dec > maxdec) maxdec = dec;
         if (stop) break;
         double beta = rr_new / rr;
-        for (int64_t i = 0; i < n; i++) p[i] = rho[i] + beta * p[i];
+        for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
         rr = rr_new;
     }
     return it;
+}
+
+/* plain CG (the hot path's CG): ora_pcg without a preconditioner */
+int64_t ora_cg(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+               const unsigned char *free_, const double *r, double eta2, int64_t cap,
+               double *w, double *work, double *decs, double deadline)
+{
+    return ora_pcg(n, rp, ci, val, free_, r, NULL, eta2, cap, w, work, decs, deadline);
+}
+
+/* dinv_i = 1 / A_ii (the point-Jacobi preconditioner; A SPD => A_ii > 0) */
+void ora_jacobi_inverse(int64_t n, const int64_t *rp, const int32_t *ci, const double *val, double *dinv)
+{
+    for (int64_t i = 0; i < n; i++) {
+        double d = 0.0;
+        for (int64_t k = rp[i]; k < rp[i + 1]; k++)
+            if (ci[k] == i) d += val[k];
+        dinv[i] = 1.0 / d;
+    }
 }
 
 /* ------------------------------------------------------------------------ */
@@ -344,6 +373,7 @@ void ora_params_default(ora_params *p)
     p->mu = 0.1; p->eta1 = 0.1; p->eta2 = 0.05; p->eta2_shrink = 0.1; p->eta2_floor = 1e-12;
     p->gp_cap = 100; p->refine_cap = 30; p->max_halvings = 50; p->cg_cap = 0;
     p->time_budget_s = 0.0;
+    p->precond = 0;
 }
 
 /* Solve min q(x) s.t. l <= x <= u.  tol > 0: absolute tau on ||grad_Omega q||_2
@@ -363,15 +393,17 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
     double *g = (double *)malloc((size_t)n * sizeof(double));
     double *y = (double *)malloc((size_t)n * sizeof(double));
     double *w = (double *)malloc((size_t)n * sizeof(double));
-    double *work = (double *)malloc((size_t)3 * n * sizeof(double));
+    double *work = (double *)malloc((size_t)4 * n * sizeof(double));
+    double *dinv = prm->precond == 1 ? (double *)malloc((size_t)n * sizeof(double)) : NULL;
     unsigned char *act = (unsigned char *)malloc((size_t)n);
     unsigned char *fr = (unsigned char *)malloc((size_t)n);
-    if (!g || !y || !w || !work || !act || !fr) {
-        free(g); free(y); free(w); free(work); free(act); free(fr);
+    if (!g || !y || !w || !work || !act || !fr || (prm->precond == 1 && !dinv)) {
+        free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv);
         st->status = ORA_ENOMEM; return ORA_ENOMEM;
     }
     int status = ORA_NOT_CONVERGED;
 
+    if (dinv) ora_jacobi_inverse(n, rp, ci, val, dinv);
     /* Setup: x <- P[x0] (Alg. GPCG "Choose x0 in Omega" P:504) */
     ora_project(n, l, u, x0, x);
     gradient(n, rp, ci, val, b, x, g); st->full_spmvs++;
@@ -428,8 +460,8 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
             for (int64_t i = 0; i < n; i++) { fr[i] = !is_active(x[i], l[i], u[i]); m += fr[i]; }
             if (m == 0) break;              /* reading R26: next GP phase frees variables */
             int64_t cap = prm->cg_cap > 0 ? prm->cg_cap : m;
-            int64_t its = ora_cg(n, rp, ci, val, fr, g, eta2, cap, w, work, NULL,
-                                 prm->time_budget_s > 0.0 ? t0 + prm->time_budget_s : 0.0);
+            int64_t its = ora_pcg(n, rp, ci, val, fr, g, dinv, eta2, cap, w, work, NULL,
+                                  prm->time_budget_s > 0.0 ? t0 + prm->time_budget_s : 0.0);
             st->cg_calls++;
             if (its < 0) { status = (int)its; goto done; }
             st->cg_iters += its;
@@ -467,6 +499,6 @@ done:
         st->status = status;
         st->seconds = now_s() - t0;
     }
-    free(g); free(y); free(w); free(work); free(act); free(fr);
+    free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv);
     return status;
 }

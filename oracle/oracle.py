@@ -37,7 +37,7 @@ class Params(C.Structure):
                 ("eta2_shrink", C.c_double), ("eta2_floor", C.c_double),
                 ("gp_cap", C.c_int64), ("refine_cap", C.c_int64),
                 ("max_halvings", C.c_int64), ("cg_cap", C.c_int64),
-                ("time_budget_s", C.c_double)]
+                ("time_budget_s", C.c_double), ("precond", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -83,6 +83,10 @@ def lib():
                                            i64, P, P, P, P]
         L.ora_cg.restype = i64
         L.ora_cg.argtypes = [i64, P, P, P, P, P, C.c_double, i64, P, P, P, C.c_double]
+        L.ora_pcg.restype = i64
+        L.ora_pcg.argtypes = [i64, P, P, P, P, P, P, C.c_double, i64, P, P, P, C.c_double]
+        L.ora_jacobi_inverse.restype = None
+        L.ora_jacobi_inverse.argtypes = [i64, P, P, P, P]
         L.ora_params_default.restype = None
         L.ora_params_default.argtypes = [P]
         L.ora_gpcg_solve.restype = C.c_int
@@ -215,10 +219,32 @@ def cg(A: CSR, free, r, eta2, cap=0):
     m = int(fr.sum())
     cap = cap if cap > 0 else m
     w = np.empty(A.n)
-    work = np.empty(3 * A.n)
+    work = np.empty(4 * A.n)
     decs = np.zeros(max(cap, 1))
     it = lib().ora_cg(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), eta2, cap,
                       _p(w), _p(work), _p(decs), 0.0)
+    return it, w, decs[:max(it, 0)]
+
+
+def jacobi_inverse(A: CSR):
+    """1 / diag(A) (the point-Jacobi preconditioner, oracle routine)."""
+    d = np.empty(A.n)
+    lib().ora_jacobi_inverse(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(d))
+    return d
+
+
+def pcg(A: CSR, free, r, dinv, eta2, cap=0):
+    """Point-Jacobi PCG on A_F w = -r (M^-1 = diag(dinv) on F). -> (iterations, w, decreases)."""
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    r = _f64(r)
+    dinv = _f64(dinv)
+    m = int(fr.sum())
+    cap = cap if cap > 0 else m
+    w = np.empty(A.n)
+    work = np.empty(4 * A.n)
+    decs = np.zeros(max(cap, 1))
+    it = lib().ora_pcg(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), _p(dinv), eta2, cap,
+                       _p(w), _p(work), _p(decs), 0.0)
     return it, w, decs[:max(it, 0)]
 
 

@@ -252,6 +252,70 @@ def test_cg_progress_stop_rule(oracle):
     assert decs[it - 1] <= 0.05 * decs[:it - 1].max() or it == m
 
 
+# ---------------------------------------------------------------- point-Jacobi PCG
+def test_jacobi_inverse_is_inverse_diagonal(oracle):
+    Ad, b, l, u = P.random_dense_qp(9, seed=12, bounds="inf")
+    d = oracle.jacobi_inverse(csr_of(oracle, Ad))
+    assert np.array_equal(d, 1.0 / np.diag(Ad))
+
+
+def test_pcg_exact_for_diagonal_operator(oracle):
+    # M = diag(A) = A for a diagonal A: z_0 = A^-1 rho_0, one step solves (w = -A^-1 r)
+    dvals = np.linspace(0.5, 40.0, 11)
+    Ad = np.diag(dvals)
+    A = csr_of(oracle, Ad)
+    r = P.gaussian(13, 1, 11)
+    it, w, decs = oracle.pcg(A, np.ones(11, np.uint8), r, oracle.jacobi_inverse(A), 0.05)
+    assert it == 1
+    assert np.max(np.abs(w + r / dvals)) <= 1e-15 * np.max(np.abs(r / dvals))
+    # plain CG needs more than one step on the same system
+    assert oracle.cg(A, np.ones(11, np.uint8), r, 1e-300)[0] > 1
+
+
+def test_pcg_dense_solve_decreases_and_termination(oracle):
+    for seed, m in [(21, 10), (22, 17), (23, 30)]:
+        Ad, b, l, u = P.random_dense_qp(m, seed=seed, bounds="inf")
+        # badly scaled rows/cols: the case a diagonal preconditioner is for
+        sc = np.exp(2.0 * P.uniform(seed, 70, m))
+        Ad = (Ad * sc[:, None]) * sc[None, :]
+        A = csr_of(oracle, Ad)
+        r = P.gaussian(seed, 71, m)
+        ref = np.linalg.solve(Ad, -r)
+        it, w, decs = oracle.pcg(A, np.ones(m, np.uint8), r, oracle.jacobi_inverse(A), 1e-300)
+        assert 1 <= it <= m                                   # finite termination
+        assert np.max(np.abs(w - ref)) <= 1e-10 * np.linalg.cond(Ad) * np.max(np.abs(ref))
+        qk = 0.5 * w @ Ad @ w + r @ w
+        assert abs(decs.sum() + qk) <= 1e-10 * abs(qk)        # 1/2 alpha rho'z sums to -q_k(w)
+        assert np.all(decs >= 0)
+
+
+def test_pcg_masked_matches_reduced_dense(oracle):
+    Ad, b, l, u = P.random_dense_qp(14, seed=24, bounds="inf")
+    A = csr_of(oracle, Ad)
+    fr = (P.uniform(24, 91, 14) < 0.6).astype(np.uint8)
+    F = np.flatnonzero(fr)
+    r = P.gaussian(24, 92, 14)
+    it, w, decs = oracle.pcg(A, fr, r, oracle.jacobi_inverse(A), 1e-300)     # progress test off
+    assert it <= len(F) and np.all(w[fr == 0] == 0.0)
+    assert np.max(np.abs(w[F] - np.linalg.solve(Ad[np.ix_(F, F)], -r[F]))) <= 1e-12
+
+
+def test_gpcg_pcg_same_minimiser(oracle):
+    # x* is unique: the preconditioner changes the path, not the answer
+    for sd in range(40):
+        n = 2 + sd % 7
+        Ad, b, l, u = P.random_dense_qp(n, seed=4000 + sd, bounds="mixed")
+        A = csr_of(oracle, Ad)
+        rc, x, st = oracle.solve(A, b, l, u, 0.0, P.gaussian(sd, 1, n), -1e-12,
+                                 params=oracle.default_params(precond=1))
+        assert rc == 0 and np.max(np.abs(x - B.enum_solve(Ad, b, l, u))) <= 1e-6
+    prob = P.c0()
+    rc0, x0, st0 = oracle.solve_problem(prob, tol=-1e-12)
+    rc1, x1, st1 = oracle.solve_problem(prob, tol=-1e-12, params=oracle.default_params(precond=1))
+    assert rc0 == rc1 == 0 and np.max(np.abs(x0 - x1)) <= 1e-7
+    assert abs(st0["q"] - st1["q"]) <= 1e-10 * abs(st0["q"])
+
+
 # ---------------------------------------------------------------- whole GPCG
 def test_gpcg_two_var(oracle):
     g = GOLD["two_var_solution"]
