@@ -80,6 +80,9 @@ typedef struct {
     int64_t cg_cap;      /* CG iterations per call, 0 => m_k (finite termination P:444-447)*/
     int32_t search_k;    /* step sizes in the first search sweep: 2 (<=2 -> 2, else 8); retries use 8 */
     int32_t cg_chunk;    /* CG iterations per graph launch between host polls: 32          */
+    int32_t gp_chunk;    /* GP steps per graph launch between host polls: 8                */
+    int32_t precond;     /* 0: plain CG on A_k (the hot path); 1: point-Jacobi PCG with
+                            M = diag(A_k) (Table 4 "Diagonal")                 */
 } gpcg_params;
 
 typedef struct {

@@ -163,7 +163,12 @@ struct Scal {
     int cg_done, cg_reason;
     // generic dot products (objective)
     double r0, r1;
+    // a7: GP phase driven on the device (graph chunks of search + accept + k_gp_step)
+    double gp_tau, gp_eta1, gp_maxdec, gp_last_dec;
+    long long gp_j, gp_cap;
+    int gp_done, gp_reason;
 };
+enum GpReason : int { GP_RUNNING = 0, GP_STOP = 1, GP_CONV = 2, GP_HOST = 3 };
 
 // ----------------------------------------------------------------------------
 // deterministic two-stage reduction

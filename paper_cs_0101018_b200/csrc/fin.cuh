@@ -120,7 +120,7 @@ enum FinKind : int {
 
 struct FinArgs {
     int kind;
-    int K, h0, use_alpha0, has_dir;
+    int K, h0, use_alpha0, has_dir, gp;
     double mu, eta2;
     long long cap;
 };
@@ -139,6 +139,7 @@ __global__ void k_combine(const double* __restrict__ per_slab, int nslabs, int n
 // that did no work leaves the scalars untouched.
 __global__ void k_finalize(const double* __restrict__ t, Scal* S, FinArgs a) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (a.gp && S->gp_done) return;               // a sweep of a finished device-driven GP phase
     switch (a.kind) {
         case FIN_ACCEPT:
         case FIN_ACCEPT5:
@@ -164,6 +165,48 @@ __global__ void k_finalize(const double* __restrict__ t, Scal* S, FinArgs a) {
             S->r1 = t[1];
             break;
     }
+}
+
+// ---------------------------------------------------------------- a7 on the device: the GP phase
+// as graph chunks of [search, accept, k_gp_step]; the host polls once per chunk.
+__global__ void k_gp_begin(Scal* S, double tau, double eta1, long long gp_cap) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    S->gp_tau = tau;
+    S->gp_eta1 = eta1;
+    S->gp_cap = gp_cap;
+    S->gp_j = 0;
+    S->gp_maxdec = 0.0;
+    S->gp_last_dec = 0.0;
+    S->gp_done = 0;
+    S->gp_reason = GP_RUNNING;
+    if (sqrt(S->pg2) <= tau) { S->gp_done = 1; S->gp_reason = GP_CONV; }
+}
+
+// After search + accept of GP step j (Eq. next-y / gplsstop): the stop rules of the phase,
+// Eq. pgstop1 (no change of the active set, as index sets R9), Eq. pgstop2 (decrease <=
+// eta1 * the largest earlier decrease, from j >= 2: R10), the cap; then the convergence test
+// ||grad_Omega q|| <= tau (R13).  A first search batch without an acceptable step (or a
+// Cauchy step with <d,Ad> <= 0) hands the step back to the host (GP_HOST).
+__global__ void k_gp_step(Scal* S) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (S->gp_done) return;
+    if (S->s_h < 0) { S->gp_done = 1; S->gp_reason = GP_HOST; return; }
+    const long long j = ++S->gp_j;
+    const double dec = -S->s_delta;                      // q(y_{j-1}) - q(y_j)
+    S->gp_last_dec = dec;
+    const bool stop = (S->n_changed == 0.0) || (j >= 2 && dec <= S->gp_eta1 * S->gp_maxdec) || (j >= S->gp_cap);
+    if (dec > S->gp_maxdec) S->gp_maxdec = dec;
+    if (stop) { S->gp_done = 1; S->gp_reason = GP_STOP; }
+    else if (sqrt(S->pg2) <= S->gp_tau) { S->gp_done = 1; S->gp_reason = GP_CONV; }
+}
+
+// host-completed step: write back the phase state
+__global__ void k_gp_set(Scal* S, long long j, double maxdec, int done, int reason) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    S->gp_j = j;
+    S->gp_maxdec = maxdec;
+    S->gp_done = done;
+    S->gp_reason = reason;
 }
 
 }  // namespace gpcg

@@ -139,7 +139,8 @@ const NcclApi* nccl_api() {
     } while (0)
 
 // ---------------------------------------------------------------- vectors of a slab
-enum Vec : int { VY0, VY1, VG0, VG1, VW, VP, VRHO0, VRHO1, VQ0, VQ1, VS0, VS1, VIN, VOUT, VB, VL, VU, NVEC };
+enum Vec : int { VY0, VY1, VG0, VG1, VW, VP, VRHO0, VRHO1, VQ0, VQ1, VS0, VS1, VIN, VOUT, VB, VL, VU, VD, NVEC };
+// VD: 1 / diag(A) (point-Jacobi PCG, gpcg_params.precond = 1)
 enum Msk : int { MK0, MK1, MKCG, NMSK };
 constexpr int NO_VEC = -1;
 constexpr int NB_NONE = -1, NB_REMOTE = -2;
@@ -182,8 +183,8 @@ struct Slab {
     CUtensorMap t4[NVEC];
     CUtensorMap t4wo;
     CUtensorMap t4m[NMSK];
-    BandGeom bg{};
-    int grid4 = 1;
+    BandGeom bg_cg{}, bg_acc{}, bg_srch{};   // band x segment items sized to each kernel's residency
+    int grid4_cg = 1, grid4_acc = 1, grid4_srch = 1;
 };
 
 }  // namespace
@@ -222,6 +223,9 @@ struct gpcg_problem {
     int free_mask = -1;             // index of the recorded free set, -1 none
     cudaGraphExec_t cg_exec = nullptr;
     int cg_exec_chunk = 0;
+    cudaGraphExec_t gp_exec[2] = {nullptr, nullptr};   // GP chunk graphs starting from buffers 0 / 1
+    int gp_exec_chunk = 0;
+    bool gp_graph = true;           // GPCG_GP_GRAPH=0: host-driven GP steps (A/B)
     long long launches = 0;
     long long cg_iters_timed = 0, cg_free_iters_timed = 0;
     double t_cg_timed_ms = 0.0;
@@ -403,6 +407,8 @@ void free_all(gpcg_problem* h) {
         if (p) cudaFree(p);
     if (h->hS) cudaFreeHost(h->hS);
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
+    for (cudaGraphExec_t g : h->gp_exec)
+        if (g) cudaGraphExecDestroy(g);
     if (h->comm && nccl_api()) nccl_api()->CommDestroy(h->comm);
     for (cudaEvent_t e : {h->ev_sync, h->ev_a, h->ev_b, h->ev_c0, h->ev_c1})
         if (e) cudaEventDestroy(e);
@@ -471,7 +477,8 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k3_search<true, false>, SrchStage<true, false>::kSmem));
     RC(set_smem(k3_search<false, true>, SrchStage<false, true>::kSmem));
     RC(set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem));
-    RC(set_smem(k4_cg_iter, m4cg::kSmem));
+    RC(set_smem(k4_cg_iter<false>, m4cg::kSmem));
+    RC(set_smem(k4_cg_iter<true>, m4cg::kSmem));
     RC(set_smem(k4_accept<true, true>, AccLayout4<true, true>::kSmem));
     RC(set_smem(k4_accept<true, false>, AccLayout4<true, false>::kSmem));
     RC(set_smem(k4_accept<false, true>, AccLayout4<false, true>::kSmem));
@@ -490,9 +497,16 @@ int setup_tile(gpcg_problem* h) {
                             : resident(k3_accept<false>, AccStage<false>::kSmem);
     const int r_srch = h->sb ? resident(k3_search<true, true>, SrchStage<true, true>::kSmem)
                              : resident(k3_search<false, true>, SrchStage<false, true>::kSmem);
-    int nb4 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb4, k4_cg_iter, m4::kThreads, m4cg::kSmem);
-    const int r4 = std::max(1, nb4) * h->sms;
+    auto res4 = [&](auto kernel, int smem) {
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, m4::kThreads, smem);
+        return std::max(1, nb) * h->sms;
+    };
+    const int r4cg = res4(k4_cg_iter<false>, m4cg::kSmem);
+    const int r4acc = h->sb ? res4(k4_accept<true, true>, AccLayout4<true, true>::kSmem)
+                            : res4(k4_accept<false, true>, AccLayout4<false, true>::kSmem);
+    const int r4srch = h->sb ? res4(k4_search<true, true>, SrchLayout4<true, true>::kSmem)
+                             : res4(k4_search<false, true>, SrchLayout4<false, true>::kSmem);
     for (Slab& S : h->slabs) {
         for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
             RC(make_map(h, S, &S.tm[id], S.v[id], false, TBW, TBH));
@@ -506,12 +520,17 @@ int setup_tile(gpcg_problem* h) {
             RC(make_map(h, S, &S.t4[id], S.v[id], false, m4::kBW, m4::kBR));
         RC(make_map(h, S, &S.t4wo, S.v[VW], false, m4::kOut, m4::kBR));
         for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t4m[k], S.m[k], true, m4::kMW, m4::kBR));
-        S.bg.nbands = (h->nx + m4::kOut - 1) / m4::kOut;
-        S.bg.nsegs = std::max(1, std::min(r4 / S.bg.nbands, (S.rows + 15) / 16));
-        S.bg.seg = (S.rows + S.bg.nsegs - 1) / S.bg.nsegs;
-        S.bg.nsegs = (S.rows + S.bg.seg - 1) / S.bg.seg;
-        S.bg.rlo = -S.glo;
-        S.grid4 = std::min(S.bg.nbands * S.bg.nsegs, r4);
+        auto band = [&](int resident, BandGeom& G, int& grid) {
+            G.nbands = (h->nx + m4::kOut - 1) / m4::kOut;
+            G.nsegs = std::max(1, std::min(resident / G.nbands, (S.rows + 15) / 16));
+            G.seg = (S.rows + G.nsegs - 1) / G.nsegs;
+            G.nsegs = (S.rows + G.seg - 1) / G.seg;
+            G.rlo = -S.glo;
+            grid = std::min(G.nbands * G.nsegs, resident);
+        };
+        band(r4cg, S.bg_cg, S.grid4_cg);
+        band(r4acc, S.bg_acc, S.grid4_acc);
+        band(r4srch, S.bg_srch, S.grid4_srch);
         S.grid_t_cg = std::min(ntiles, r_cg);
         S.grid_t_acc = std::min(ntiles, r_acc);
         S.grid_t_srch = std::min(ntiles, r_srch);
@@ -551,6 +570,10 @@ int create_streams(gpcg_problem* h, void* stream) {
     CK(cudaGetDevice(&h->dev));
     CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
     h->user = (cudaStream_t)stream;
+    {
+        const char* e = getenv("GPCG_GP_GRAPH");
+        h->gp_graph = !(e && e[0] == '0');
+    }
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev_a));
@@ -669,7 +692,8 @@ int layout_slabs(gpcg_problem* h, long long rows_rank, int nsl, int ghost) {
 }
 
 // ---------------------------------------------------------------- launches (every slab)
-int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev, int y_out, int g_out, int m_out) {
+int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev, int y_out, int g_out, int m_out,
+                  int gp = 0) {
     const bool use_k4 = h->tile && (h->tile_mask & 16);
     const bool use_tile = h->tile && (h->tile_mask & (1 | 16));
     for (int s = 0; s < h->nslabs(); ++s) {
@@ -682,9 +706,9 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
             const int has_mp = mask_prev >= 0 ? 1 : 0;
             auto go = [&](auto sbt, auto hdt) {
                 constexpr bool SB = decltype(sbt)::value, HD = decltype(hdt)::value;
-                k4_accept<SB, HD><<<S.grid4, m4::kThreads, AccLayout4<SB, HD>::kSmem, h->st>>>(
-                    S.sop, S.bg, B, S.t4[y_in], md, S.t4[VB], S.t4[VL], S.t4[VU], mp, has_mp, sgn, S.v[y_out],
-                    S.v[g_out], S.m[m_out], h->dS, R);
+                k4_accept<SB, HD><<<S.grid4_acc, m4::kThreads, AccLayout4<SB, HD>::kSmem, h->st>>>(
+                    S.sop, S.bg_acc, B, S.t4[y_in], md, S.t4[VB], S.t4[VL], S.t4[VU], mp, has_mp, sgn, S.v[y_out],
+                    S.v[g_out], S.m[m_out], h->dS, R, gp);
             };
             if (h->sb) { if (dir >= 0) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (dir >= 0) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
@@ -694,18 +718,19 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
             if (h->sb)
                 k3_accept<true><<<S.grid_t_acc, kTileThreads, AccStage<true>::kSmem, h->st>>>(
                     S.sop, S.tg, B, S.tm[y_in], md, S.tm[VB], S.tm[VL], S.tm[VU], mp, dir >= 0 ? 1 : 0, sgn,
-                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R);
+                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
             else
                 k3_accept<false><<<S.grid_t_acc, kTileThreads, AccStage<false>::kSmem, h->st>>>(
                     S.sop, S.tg, B, S.tm[y_in], md, S.tm[VB], S.tm[VL], S.tm[VU], mp, dir >= 0 ? 1 : 0, sgn,
-                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R);
+                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
         } else if (!h->is_csr && !h->generic) {   // accept + regrad + mask + counts + next Cauchy step, one sweep
             const double* dp = dir >= 0 ? S.v[dir] : nullptr;
             const unsigned char* mp = mask_prev >= 0 ? S.m[mask_prev] : nullptr;
             auto go = [&](auto sbt, auto bct) {
                 constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value;
                 k2_accept<SB, BC><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, B, S.v[y_in], dp, sgn, S.v[VB],
-                                                                          mp, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R);
+                                                                          mp, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R,
+                                                                          gp);
             };
             if (h->sb) { if (h->bc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (h->bc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
@@ -716,7 +741,7 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
                 using Op = std::decay_t<decltype(op)>;
                 constexpr bool SB = decltype(sbt)::value;
                 k_accept<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y_in], dp, sgn, S.v[VB], mp, S.v[y_out],
-                                                                S.v[g_out], S.m[m_out], h->dS, R);
+                                                                S.v[g_out], S.m[m_out], h->dS, R, gp);
             };
             if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
             else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
@@ -726,13 +751,14 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
     }
     FinArgs a = fin((h->is_csr || h->generic) && !use_tile ? FIN_ACCEPT5 : FIN_ACCEPT);
     a.has_dir = dir >= 0 ? 1 : 0;
+    a.gp = gp;
     RC(finish_reduce(h, a, a.kind == FIN_ACCEPT ? 6 : 5));
     return exchange(h, {y_out, g_out}, {m_out});
 }
 
 bool fused_cauchy(const gpcg_problem* h) { return !h->is_csr && !h->generic; }
 
-int launch_cauchy(gpcg_problem* h, int y, int g) {
+int launch_cauchy(gpcg_problem* h, int y, int g, int gp = 0) {
     if (fused_cauchy(h)) return GPCG_OK;     // computed by the preceding accept sweep
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
@@ -740,21 +766,23 @@ int launch_cauchy(gpcg_problem* h, int y, int g) {
         auto go = [&](auto& op, auto sbt) {
             using Op = std::decay_t<decltype(op)>;
             constexpr bool SB = decltype(sbt)::value;
-            k_cauchy<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], h->dS, h->red(s));
+            k_cauchy<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], h->dS, h->red(s), gp);
         };
         if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
         else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
         h->launches++;
         CKLAUNCH();
     }
-    return finish_reduce(h, fin(FIN_CAUCHY), 2);
+    FinArgs a = fin(FIN_CAUCHY);
+    a.gp = gp;
+    return finish_reduce(h, a, 2);
 }
 
 // step sizes per projected-search sweep: the first sweep evaluates search_k
 // (2 or 8 instantiated), later sweeps 8
 int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
 
-int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_alpha0, int h0, int K) {
+int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_alpha0, int h0, int K, int gp = 0) {
     const double mu = h->prm.mu;
     const bool dg = (dir == g);
     const bool use_k4 = h->tile && (h->tile_mask & 32) && K == 2;  // retries use the column march
@@ -766,8 +794,8 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
         if (use_k4) {
             auto go = [&](auto sbt, auto dgt) {
                 constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
-                k4_search<SB, DG><<<S.grid4, m4::kThreads, SrchLayout4<SB, DG>::kSmem, h->st>>>(
-                    S.sop, S.bg, B, S.t4[y], S.t4[dir], S.t4[g], S.t4[VL], S.t4[VU], sgn, use_alpha0, h0, mu, h->dS, R);
+                k4_search<SB, DG><<<S.grid4_srch, m4::kThreads, SrchLayout4<SB, DG>::kSmem, h->st>>>(
+                    S.sop, S.bg_srch, B, S.t4[y], S.t4[dir], S.t4[g], S.t4[VL], S.t4[VU], sgn, use_alpha0, h0, mu, h->dS, R, gp);
             };
             if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
@@ -775,7 +803,7 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
             auto go = [&](auto sbt, auto dgt) {
                 constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
                 k3_search<SB, DG><<<S.grid_t_srch, kTileThreads, SrchStage<SB, DG>::kSmem, h->st>>>(
-                    S.sop, S.tg, B, S.tm[y], S.tm[dir], S.tm[g], S.tm[VL], S.tm[VU], sgn, use_alpha0, h0, mu, h->dS, R);
+                    S.sop, S.tg, B, S.tm[y], S.tm[dir], S.tm[g], S.tm[VL], S.tm[VU], sgn, use_alpha0, h0, mu, h->dS, R, gp);
             };
             if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
@@ -784,7 +812,7 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
                 constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value, DG = decltype(dgt)::value;
                 constexpr int KK = decltype(kt)::value;
                 k2_search<SB, BC, KK, DG><<<S.grid_m1, kMarchThreads, 0, h->st>>>(
-                    S.sop, S.mg1, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0, h0, mu, h->dS, R);
+                    S.sop, S.mg1, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0, h0, mu, h->dS, R, gp);
             };
             auto byk = [&](auto sbt, auto bct, auto dgt) {
                 if (K == 2) go(sbt, bct, std::integral_constant<int, 2>(), dgt);
@@ -803,10 +831,10 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
                 constexpr bool SB = decltype(sbt)::value;
                 if (K == 2)
                     k_search<Op, SB, 2><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0,
-                                                                        h0, mu, h->dS, R);
+                                                                        h0, mu, h->dS, R, gp);
                 else
                     k_search<Op, SB, 8><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0,
-                                                                        h0, mu, h->dS, R);
+                                                                        h0, mu, h->dS, R, gp);
             };
             if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
             else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
@@ -819,15 +847,16 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
     a.h0 = h0;
     a.use_alpha0 = use_alpha0;
     a.mu = mu;
+    a.gp = gp;
     return finish_reduce(h, a, 2 * K);
 }
 
 // one projected search + accept:  y' = P[y + alpha sgn dir], g' = A y' - b.
 // Host loops over batches of K step sizes until one is accepted.  Returns
 // GPCG_OK with *accepted_h >= 0, or GPCG_ESEARCH.
-int search_and_accept(gpcg_problem* h, int cur, int dir, double sgn, int use_alpha0, int* accepted_h) {
+int search_and_accept(gpcg_problem* h, int cur, int dir, double sgn, int use_alpha0, int* accepted_h, int h_start = 0) {
     const int nxt = cur ^ 1;
-    for (int h0 = 0, K = first_k(h); h0 < h->prm.max_halvings; h0 += K, K = 8) {
+    for (int h0 = h_start, K = h_start ? 8 : first_k(h); h0 < h->prm.max_halvings; h0 += K, K = 8) {
         RC(launch_search(h, vy(cur), vg(cur), dir, sgn, use_alpha0, h0, K));
         RC(launch_accept(h, vy(cur), dir, sgn, mk(cur), vy(nxt), vg(nxt), mk(nxt)));
         RC(sync_scal(h));
@@ -848,36 +877,44 @@ int search_and_accept(gpcg_problem* h, int cur, int dir, double sgn, int use_alp
 // one CG iteration on every slab (+ exchange + deferred finalize): captured into the graph
 int enqueue_cg_iter(gpcg_problem* h, int a) {
     const int bb = a ^ 1;
+    const bool pc = h->prm.precond == 1;
     const bool use_k4 = h->tile && (h->tile_mask & 8);
-    const bool use_tile = h->tile && (h->tile_mask & 4);
+    const bool use_tile = h->tile && (h->tile_mask & 4) && !pc;      // k3 has no PCG variant
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
         if (use_k4) {
-            k4_cg_iter<<<S.grid4, m4::kThreads, m4cg::kSmem, h->st>>>(S.sop, S.bg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo,
-                                                                     S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
-                                                                     h->dS, R);
+            if (pc)
+                k4_cg_iter<true><<<S.grid4_cg, m4::kThreads, m4cg::kSmem, h->st>>>(
+                    S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
+                    h->dS, R);
+            else
+                k4_cg_iter<false><<<S.grid4_cg, m4::kThreads, m4cg::kSmem, h->st>>>(
+                    S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
+                    h->dS, R);
         } else if (use_tile) {
             k3_cg_iter<2><<<S.grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
                 S.sop, S.tg, S.tm[vrho(a)], S.tm[vq(a)], S.tmWc, S.tmm[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
                 h->dS, R);
         } else if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
-            if (h->bc)
-                k2_cg_iter<true><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, S.m[MKCG], S.v[vrho(a)],
-                                                                         S.v[vq(a)], S.v[vrho(bb)], S.v[vq(bb)],
-                                                                         S.v[VW], h->dS, R);
-            else
-                k2_cg_iter<false><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, S.m[MKCG], S.v[vrho(a)],
-                                                                          S.v[vq(a)], S.v[vrho(bb)], S.v[vq(bb)],
-                                                                          S.v[VW], h->dS, R);
-        } else {
-            auto go = [&](auto& op) {
-                using Op = std::decay_t<decltype(op)>;
-                k_cg_iter<Op><<<S.grid, kThreads, 0, h->st>>>(op, S.m[MKCG], S.v[vrho(a)], S.v[vq(a)], S.v[vs(a)],
-                                                              S.v[vrho(bb)], S.v[vq(bb)], S.v[vs(bb)], S.v[VP],
-                                                              S.v[VW], h->dS, R);
+            auto go = [&](auto bct, auto pct) {
+                constexpr bool BC = decltype(bct)::value, PC = decltype(pct)::value;
+                k2_cg_iter<BC, PC><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, S.m[MKCG], S.v[vrho(a)],
+                                                                           S.v[vq(a)], S.v[vrho(bb)], S.v[vq(bb)],
+                                                                           S.v[VW], h->dS, R);
             };
-            if (h->is_csr) go(S.cop); else go(S.sop);
+            if (h->bc) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+            else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else {
+            auto go = [&](auto& op, auto pct) {
+                using Op = std::decay_t<decltype(op)>;
+                constexpr bool PC = decltype(pct)::value;
+                k_cg_iter<Op, PC><<<S.grid, kThreads, 0, h->st>>>(op, S.m[MKCG], S.v[vrho(a)], S.v[vq(a)], S.v[vs(a)],
+                                                                  S.v[vrho(bb)], S.v[vq(bb)], S.v[vs(bb)], S.v[VP],
+                                                                  S.v[VW], S.v[VD], h->dS, R);
+            };
+            if (h->is_csr) { if (pc) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
+            else { if (pc) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
         }
         h->launches++;
         CKLAUNCH();
@@ -912,6 +949,48 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
     return GPCG_OK;
 }
 
+// GP chunk: `chunk` steps of [Cauchy (generic kernels), first search batch, accept, k_gp_step]
+// starting from buffers c0, the buffers alternating per step (a finished phase makes the rest no-ops)
+int build_gp_graph(gpcg_problem* h, int chunk) {
+    if (h->gp_exec[0] && h->gp_exec_chunk == chunk) return GPCG_OK;
+    for (cudaGraphExec_t& g : h->gp_exec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (int c0 = 0; c0 < 2; ++c0) {
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+        const long long l0 = h->launches;
+        int rc = GPCG_OK;
+        for (int i = 0; i < chunk && !rc; ++i) {
+            const int cur = (c0 + i) & 1, nxt = cur ^ 1;
+            rc = launch_cauchy(h, vy(cur), vg(cur), 1);
+            if (!rc) rc = launch_search(h, vy(cur), vg(cur), vg(cur), -1.0, 1, 0, first_k(h), 1);
+            if (!rc) rc = launch_accept(h, vy(cur), vg(cur), -1.0, mk(cur), vy(nxt), vg(nxt), mk(nxt), 1);
+            if (!rc) {
+                k_gp_step<<<1, 32, 0, h->st>>>(h->dS);
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) rc = set_err(GPCG_ECUDA, "k_gp_step launch: %s", cudaGetErrorString(e));
+            }
+        }
+        h->launches = l0;
+        cudaError_t e = cudaStreamEndCapture(h->st, &graph);
+        if (rc) {
+            if (e == cudaSuccess) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&h->gp_exec[c0], graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    }
+    h->gp_exec_chunk = chunk;
+    return GPCG_OK;
+}
+
+int launches_per_gp_step(const gpcg_problem* h) {
+    const int fins = h->deferred ? (1 + (h->nslabs() > 1 ? 1 : 0)) : 0;
+    return (fused_cauchy(h) ? 0 : h->nslabs() + fins) + 2 * (h->nslabs() + fins) + 1;
+}
+
 // kernels per CG iteration (for the launch count)
 int launches_per_cg_iter(const gpcg_problem* h) {
     int n = h->nslabs();
@@ -924,23 +1003,26 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
+        const bool pc = h->prm.precond == 1;
         if (!h->is_csr && !h->generic) {
-            if (h->bc)
-                k2_cg_init<true><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.v[vg(cur)], S.m[cur],
-                                                                         S.m[MKCG], S.v[VRHO0], S.v[VQ0], S.v[VW],
-                                                                         eta2, cap, h->dS, R);
-            else
-                k2_cg_init<false><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.v[vg(cur)], S.m[cur],
-                                                                          S.m[MKCG], S.v[VRHO0], S.v[VQ0], S.v[VW],
-                                                                          eta2, cap, h->dS, R);
-        } else {
-            auto go = [&](auto& op) {
-                using Op = std::decay_t<decltype(op)>;
-                k_cg_init<Op><<<S.grid, kThreads, 0, h->st>>>(op, S.v[vg(cur)], S.m[cur], S.m[MKCG], S.v[VRHO0],
-                                                              S.v[VQ0], S.v[VS0], S.v[VRHO1], S.v[VQ1], S.v[VS1],
-                                                              S.v[VP], S.v[VW], eta2, cap, h->dS, R);
+            auto go = [&](auto bct, auto pct) {
+                constexpr bool BC = decltype(bct)::value, PC = decltype(pct)::value;
+                k2_cg_init<BC, PC><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.v[vg(cur)], S.m[cur],
+                                                                           S.m[MKCG], S.v[VRHO0], S.v[VQ0], S.v[VW],
+                                                                           eta2, cap, h->dS, R);
             };
-            if (h->is_csr) go(S.cop); else go(S.sop);
+            if (h->bc) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+            else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else {
+            auto go = [&](auto& op, auto pct) {
+                using Op = std::decay_t<decltype(op)>;
+                constexpr bool PC = decltype(pct)::value;
+                k_cg_init<Op, PC><<<S.grid, kThreads, 0, h->st>>>(op, S.v[vg(cur)], S.m[cur], S.m[MKCG], S.v[VRHO0],
+                                                                  S.v[VQ0], S.v[VS0], S.v[VRHO1], S.v[VQ1], S.v[VS1],
+                                                                  S.v[VP], S.v[VW], S.v[VD], eta2, cap, h->dS, R);
+            };
+            if (h->is_csr) { if (pc) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
+            else { if (pc) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
         }
         h->launches++;
         CKLAUNCH();
@@ -986,6 +1068,16 @@ int launch_objective(gpcg_problem* h, int x) {
         CKLAUNCH();
     }
     return finish_reduce(h, fin(FIN_R2), 2);
+}
+
+// 1 / diag(A) of every slab (+ ghosts): the point-Jacobi preconditioner
+int setup_jacobi(gpcg_problem* h) {
+    for (Slab& S : h->slabs) {
+        if (h->is_csr) k_jacobi_inverse<CsrOp><<<S.grid, kThreads, 0, h->st>>>(S.cop, S.v[VD]);
+        else k_jacobi_inverse<StencilOp><<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[VD]);
+        CKLAUNCH();
+    }
+    return exchange(h, {VD});
 }
 
 // ---------------------------------------------------------------- stencil slabs: operator
@@ -1109,6 +1201,7 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
     h->c = c;
     if ((rc = setup_stencil_slabs(h, wx, wy, shift))) return fail(rc);
     h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
+    if ((rc = setup_jacobi(h))) return fail(rc);
     {
         const char* e = getenv("GPCG_TILE");
         if (e && *e) h->tile_mask = atoi(e) & 63;
@@ -1251,6 +1344,7 @@ int create_csr(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t 
         S.cop = CsrOp{S.rows, S.rp, S.ci, S.val};
         S.grid = std::max(1, std::min((S.rows + kThreads - 1) / kThreads, h->sms * 16));
     }
+    if ((rc = setup_jacobi(h))) return fail(rc);
     {
         std::vector<const double*> arrs;
         std::vector<long long> cnts;
@@ -1287,6 +1381,8 @@ gpcg_params gpcg_params_default(void) {
     p.cg_cap = 0;
     p.search_k = 2;
     p.cg_chunk = 32;
+    p.gp_chunk = 8;
+    p.precond = 0;
     return p;
 }
 
@@ -1344,14 +1440,18 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
     if (!(p->eta2_shrink > 0.0 && p->eta2_shrink < 1.0) || !(p->eta2_floor > 0.0))
         return set_err(GPCG_EINVAL, "eta2_shrink in (0,1), eta2_floor > 0 required");
     if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 || p->cg_cap < 0 ||
-        p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096)
+        p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096 || p->gp_chunk < 1 ||
+        p->gp_chunk > 256 || (p->precond != 0 && p->precond != 1))
         return set_err(GPCG_EINVAL, "integer parameter out of range");
-    const int old_chunk = h->prm.cg_chunk;
+    const int old_chunk = h->prm.cg_chunk, old_pc = h->prm.precond;
     h->prm = *p;
-    if (old_chunk != p->cg_chunk && h->cg_exec) {
+    if ((old_chunk != p->cg_chunk || old_pc != p->precond) && h->cg_exec) {
         cudaGraphExecDestroy(h->cg_exec);
         h->cg_exec = nullptr;
     }
+    // the GP graphs bake in search_k / mu (and the chunk): rebuilt at the next solve
+    for (cudaGraphExec_t& g : h->gp_exec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     return GPCG_OK;
 }
 
@@ -1447,6 +1547,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     RC(launch_accept(h, VIN, NO_VEC, 0.0, NO_VEC, VY0, VG0, MK0));
     RC(sync_scal(h));
     st.full_spmvs++;
+    if (h->gp_graph) RC(build_gp_graph(h, std::max(1, h->prm.gp_chunk)));
     st.g0_norm = std::sqrt(S.g2);
     tau = tol > 0.0 ? tol : -tol * st.g0_norm;
     st.tau = tau;
@@ -1457,31 +1558,73 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
             st.outer_iters = k + 1;
             // ---- gradient projection phase, y_0 = x_k ------------
             CK(cudaEventRecord(h->ev_a, h->st));
-            long long j = 0;
-            double maxdec = 0.0;
             bool conv = false;
-            for (;;) {
-                if (std::sqrt(S.pg2) <= tau) { conv = true; break; }
-                if ((rc = launch_cauchy(h, vy(cur), vg(cur)))) goto fail;
-                st.full_spmvs++;
-                int hacc = -1;
-                // direction -grad q (Eq. next-y); trial points equal those of the
-                // -grad_Omega q reading for feasible y (reading R8)
-                if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc))) goto fail;
-                st.full_spmvs += 2;
-                cur ^= 1;
-                ++j;
-                st.gp_iters++;
-                const double dec = -S.s_delta;                      // q(y_{j-1}) - q(y_j)
+            if (h->gp_graph) {
+                // device-driven: graph chunks of GP steps, one poll per chunk (k_gp_step decides)
+                k_gp_begin<<<1, 32, 0, h->st>>>(h->dS, tau, prm.eta1, prm.gp_cap);
+                h->launches++;
+                CKLAUNCH();
+                long long jdone = 0;
+                for (;;) {
+                    CK(cudaGraphLaunch(h->gp_exec[cur], h->st));
+                    h->launches += (long long)h->gp_exec_chunk * launches_per_gp_step(h);
+                    if ((rc = sync_scal(h))) goto fail;
+                    const long long jn = S.gp_j;
+                    cur = (int)((cur + (jn - jdone)) & 1);
+                    st.gp_iters += jn - jdone;
+                    st.full_spmvs += 3 * (jn - jdone);
+                    jdone = jn;
+                    if (!S.gp_done) continue;
+                    if (S.gp_reason != GP_HOST) break;
+                    // the first search batch found no step: the host finishes this step
+                    int hacc = -1;
+                    if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc, first_k(h)))) goto fail;
+                    cur ^= 1;
+                    const long long j = jdone + 1;
+                    jdone = j;
+                    st.gp_iters++;
+                    st.full_spmvs += 3;
+                    const double dec = -S.s_delta;
+                    const bool stop = (S.n_changed == 0.0) || (j >= 2 && dec <= prm.eta1 * S.gp_maxdec) ||
+                                      (j >= prm.gp_cap);
+                    const double maxdec = std::max(S.gp_maxdec, dec);
+                    const bool cv = !stop && std::sqrt(S.pg2) <= tau;
+                    k_gp_set<<<1, 32, 0, h->st>>>(h->dS, j, maxdec, (stop || cv) ? 1 : 0,
+                                                  stop ? GP_STOP : (cv ? GP_CONV : GP_RUNNING));
+                    h->launches++;
+                    CKLAUNCH();
+                    if (stop || cv) { if ((rc = sync_scal(h))) goto fail; break; }
+                }
                 if (trace_on())
-                    fprintf(stderr, "[gpcg] k=%lld GP j=%lld h=%d alpha=%.3e dec=%.3e |A|=%.0f changed=%.0f pg=%.3e t=%.2fms\n",
-                            (long long)k, j, S.s_h, S.s_alpha, dec, S.n_active, S.n_changed, std::sqrt(S.pg2),
+                    fprintf(stderr, "[gpcg] k=%lld GP phase: %lld steps reason=%d |A|=%.0f pg=%.3e t=%.2fms\n",
+                            (long long)k, jdone, S.gp_reason, S.n_active, std::sqrt(S.pg2),
                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
-                const bool stop = (S.n_changed == 0.0) ||           // Eq. pgstop1 (index sets, R9)
-                                  (j >= 2 && dec <= prm.eta1 * maxdec) ||   // Eq. pgstop2 (R10)
-                                  (j >= prm.gp_cap);
-                if (dec > maxdec) maxdec = dec;
-                if (stop) break;
+            } else {
+                long long j = 0;
+                double maxdec = 0.0;
+                for (;;) {
+                    if (std::sqrt(S.pg2) <= tau) { conv = true; break; }
+                    if ((rc = launch_cauchy(h, vy(cur), vg(cur)))) goto fail;
+                    st.full_spmvs++;
+                    int hacc = -1;
+                    // direction -grad q (Eq. next-y); trial points equal those of the
+                    // -grad_Omega q reading for feasible y (reading R8)
+                    if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc))) goto fail;
+                    st.full_spmvs += 2;
+                    cur ^= 1;
+                    ++j;
+                    st.gp_iters++;
+                    const double dec = -S.s_delta;                      // q(y_{j-1}) - q(y_j)
+                    if (trace_on())
+                        fprintf(stderr, "[gpcg] k=%lld GP j=%lld h=%d alpha=%.3e dec=%.3e |A|=%.0f changed=%.0f pg=%.3e t=%.2fms\n",
+                                (long long)k, j, S.s_h, S.s_alpha, dec, S.n_active, S.n_changed, std::sqrt(S.pg2),
+                                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+                    const bool stop = (S.n_changed == 0.0) ||           // Eq. pgstop1 (index sets, R9)
+                                      (j >= 2 && dec <= prm.eta1 * maxdec) ||   // Eq. pgstop2 (R10)
+                                      (j >= prm.gp_cap);
+                    if (dec > maxdec) maxdec = dec;
+                    if (stop) break;
+                }
             }
             CK(cudaEventRecord(h->ev_b, h->st));
             CK(cudaEventSynchronize(h->ev_b));

@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(kThreads)
 k_accept(Op A, Bounds Bd, const double* __restrict__ y_in, const double* __restrict__ dir,
          double sgn, const double* __restrict__ b, const unsigned char* __restrict__ mask_prev,
          double* __restrict__ y_out, double* __restrict__ g_out, unsigned char* __restrict__ mask_out,
-         Scal* S, RedScratch R) {
+         Scal* S, RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     double alpha = 0.0;
     if (dir) {
         if (S->s_h < 0) return;          // uniform across the grid
@@ -73,7 +74,8 @@ k_accept(Op A, Bounds Bd, const double* __restrict__ y_in, const double* __restr
 template <class Op, bool SB>
 __global__ void __launch_bounds__(kThreads)
 k_cauchy(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
-         Scal* S, RedScratch R) {
+         Scal* S, RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     double acc[2] = {0.0, 0.0};
     A.for_each_point([&](const Pt& p) {
         double ad = 0.0, dv = 0.0;
@@ -100,7 +102,8 @@ template <class Op, bool SB, int K>
 __global__ void __launch_bounds__(kThreads)
 k_search(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
          const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu,
-         Scal* S, RedScratch R) {
+         Scal* S, RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
         if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
         return;
@@ -193,12 +196,14 @@ k_objective(Op A, const double* __restrict__ x, const double* __restrict__ b, Sc
 // rho, q, s ping-pong between two buffers (neighbours read the old values);
 // p and w are updated in place.  After cg_done every launch is a no-op.
 // ----------------------------------------------------------------------------
-template <class Op>
+// PC: point-Jacobi PCG with dinv = 1 / diag(A) (k_jacobi_inverse): u = dinv * rho, q = A_F u,
+// gamma = rho'u, delta = u'q; p_i = u_i + beta p_{i-1}.
+template <class Op, bool PC>
 __global__ void __launch_bounds__(kThreads)
 k_cg_init(Op A, const double* __restrict__ g, const unsigned char* __restrict__ mask,
           unsigned char* __restrict__ mask_cg, double* __restrict__ rho, double* __restrict__ q, double* __restrict__ s,
           double* __restrict__ rho2, double* __restrict__ q2, double* __restrict__ s2,
-          double* __restrict__ p, double* __restrict__ w, double eta2, long long cap,
+          double* __restrict__ p, double* __restrict__ w, const double* __restrict__ dinv, double eta2, long long cap,
           Scal* S, RedScratch R) {
     double acc[2] = {0.0, 0.0};
     A.for_each_point([&](const Pt& pt) {
@@ -208,26 +213,28 @@ k_cg_init(Op A, const double* __restrict__ g, const unsigned char* __restrict__ 
         p[v] = 0.0; w[v] = 0.0; s[v] = 0.0;
         rho2[v] = 0.0; q2[v] = 0.0; s2[v] = 0.0;
         if (!mv) { rho[v] = 0.0; q[v] = 0.0; return; }
-        double qv = 0.0, rv = 0.0;
+        double qv = 0.0, uv = 0.0;
         A.for_each_nbr(pt, [&](int c, double a) {
             const double rc = mask[c] ? -__ldg(g + c) : 0.0;
-            if (c == v) rv = rc;
-            qv = fma(a, rc, qv);
+            const double uc = PC ? rc * __ldg(dinv + c) : rc;
+            if (c == v) uv = uc;
+            qv = fma(a, uc, qv);
         });
+        const double rv = -__ldg(g + v);
         rho[v] = rv;
         q[v] = qv;
-        acc[0] = fma(rv, rv, acc[0]);
-        acc[1] = fma(rv, qv, acc[1]);
+        acc[0] = fma(rv, uv, acc[0]);
+        acc[1] = fma(uv, qv, acc[1]);
     });
     reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
 }
 
-template <class Op>
+template <class Op, bool PC>
 __global__ void __launch_bounds__(kThreads)
 k_cg_iter(Op A, const unsigned char* __restrict__ mask,
           const double* __restrict__ rho, const double* __restrict__ q, const double* __restrict__ s,
           double* __restrict__ rho_n, double* __restrict__ q_n, double* __restrict__ s_n,
-          double* __restrict__ p, double* __restrict__ w, Scal* S, RedScratch R) {
+          double* __restrict__ p, double* __restrict__ w, const double* __restrict__ dinv, Scal* S, RedScratch R) {
     if (*(volatile int*)&S->cg_done) return;
     const double alpha = S->cg_alpha, beta = S->cg_beta;
     double acc[2] = {0.0, 0.0};
@@ -235,29 +242,42 @@ k_cg_iter(Op A, const unsigned char* __restrict__ mask,
         const int v = pt.v;
         if (!mask[v]) return;
         const double rv = rho[v], qv = q[v], sv = s[v];
-        const double pn = fma(beta, p[v], rv);
+        const double pn = fma(beta, p[v], PC ? rv * __ldg(dinv + v) : rv);
         const double sn = fma(beta, sv, qv);
         w[v] = fma(alpha, pn, w[v]);
         p[v] = pn;
         s_n[v] = sn;
-        double rnv = 0.0, qn = 0.0;
+        double rnv = 0.0, unv = 0.0, qn = 0.0;
         A.for_each_nbr(pt, [&](int c, double a) {
-            double rc;
+            double uc;
             if (c == v) {
-                rc = fma(-alpha, sn, rv);
-                rnv = rc;
+                rnv = fma(-alpha, sn, rv);
+                unv = PC ? rnv * __ldg(dinv + v) : rnv;
+                uc = unv;
             } else {
                 if (!mask[c]) return;
-                rc = fma(-alpha, fma(beta, s[c], q[c]), rho[c]);
+                const double rc = fma(-alpha, fma(beta, s[c], q[c]), rho[c]);
+                uc = PC ? rc * __ldg(dinv + c) : rc;
             }
-            qn = fma(a, rc, qn);
+            qn = fma(a, uc, qn);
         });
         rho_n[v] = rnv;
         q_n[v] = qn;
-        acc[0] = fma(rnv, rnv, acc[0]);
-        acc[1] = fma(rnv, qn, acc[1]);
+        acc[0] = fma(rnv, unv, acc[0]);
+        acc[1] = fma(unv, qn, acc[1]);
     });
     reduce_and_finish<2>(acc, R, [&](double* t) { cg_finalize(t[0], t[1], S); });
+}
+
+// 1 / A_vv for every owned point (point-Jacobi preconditioner)
+template <class Op>
+__global__ void __launch_bounds__(kThreads)
+k_jacobi_inverse(Op A, double* __restrict__ dinv) {
+    A.for_each_point([&](const Pt& p) {
+        double d = 0.0;
+        A.for_each_nbr(p, [&](int c, double a) { if (c == p.v) d += a; });
+        dinv[p.v] = 1.0 / d;
+    });
 }
 
 // ----------------------------------------------------------------------------

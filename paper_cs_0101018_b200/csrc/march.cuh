@@ -60,6 +60,19 @@ struct Op5 {
             dg = (fw + fe) + (fs + fn);
         }
     }
+    // 1 / A_vv at row r of this lane (point-Jacobi preconditioner); BC: per column
+    __device__ __forceinline__ double dinv(const StencilOp& A, int r) const {
+        if constexpr (BC) {
+            return 1.0 / dg;
+        } else {
+            const int rc = min(max(r, A.rlo), A.rhi - 1);
+            const double* wxr = A.wx + (long long)rc * A.wx_ld + ic;
+            double d = (__ldg(wxr) + __ldg(wxr + 1)) +
+                       (__ldg(A.wy + (long long)rc * A.wy_ld + ic) + __ldg(A.wy + (long long)(rc + 1) * A.wy_ld + ic));
+            if (A.shift) d += __ldg(A.shift + ic + A.pitch * rc);
+            return 1.0 / d;
+        }
+    }
     // (A v) at row r of this lane: vc centre, vs / vn rows r-1 / r+1, west/east by shuffle
     __device__ __forceinline__ double apply(const StencilOp& A, int r, double vc, double vs, double vn) const {
         const double vw = __shfl_up_sync(0xffffffffu, vc, 1);
@@ -144,7 +157,8 @@ __global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_accept(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y_in, const double* __restrict__ dir,
           double sgn, const double* __restrict__ b, const unsigned char* __restrict__ mask_prev,
           double* __restrict__ y_out, double* __restrict__ g_out, unsigned char* __restrict__ mask_out,
-          Scal* S, RedScratch R) {
+          Scal* S, RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     double alpha = 0.0;
     if (dir) {
         if (S->s_h < 0) return;                   // uniform: no accepted step in this batch
@@ -231,7 +245,8 @@ template <bool SB, bool BC, int K, bool kDirIsG>
 __global__ void __launch_bounds__(kMarchThreads, (K <= 4 ? kMarchMinBlocks : 2))
 k2_search(StencilOp A, MarchGeom G, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
           const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu, Scal* S,
-          RedScratch R) {
+          RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
         if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
         return;
@@ -305,7 +320,8 @@ struct RawInit {
     unsigned char m;
 };
 
-template <bool BC>
+// PC: point-Jacobi PCG (u = rho / A_vv): gamma_0 = rho_0'u_0, delta_0 = u_0'A_F u_0.
+template <bool BC, bool PC>
 __global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigned char* __restrict__ mask,
            unsigned char* __restrict__ mask_cg, double* __restrict__ rho, double* __restrict__ p,
@@ -320,7 +336,7 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
         Op5<BC> op;
         op.init(A, i);
         const int rend = min(A.rhi, j1 + H);
-        double r_m2 = 0.0, r_m1 = 0.0;
+        double r_m2 = 0.0, r_m1 = 0.0, rho_m1 = 0.0;   // u (= rho without PC) at r-2, r-1; rho at r-1
         unsigned char m_m1 = 0;
         pipeline<NoPre, RawInit>(
             j0 - 1, j1 - j0 + 2, [&](int) { return NoPre{}; },
@@ -336,19 +352,20 @@ k2_cg_init(StencilOp A, MarchGeom G, const double* __restrict__ g, const unsigne
                 return x;
             },
             [&](int r, const RawInit& x) {
-                const double r0 = x.m ? x.rho : 0.0;
+                const double rho0 = x.m ? x.rho : 0.0;
+                const double r0 = PC ? rho0 * op.dinv(A, r) : rho0;
                 const int r1 = r - 1;
                 const double q = op.apply(A, r1, r_m1, r_m2, r0);
                 if (out_lane && col_ok && r1 >= j0 && r1 < j1) {
                     const int v = i + A.pitch * r1;
                     mask_cg[v] = m_m1;
-                    rho[v] = r_m1;
+                    rho[v] = rho_m1;
                     p[v] = 0.0;
                     w[v] = 0.0;
-                    acc[0] = fma(r_m1, r_m1, acc[0]);          // r_m1 = 0 off F
+                    acc[0] = fma(rho_m1, r_m1, acc[0]);        // 0 off F
                     acc[1] = m_m1 ? fma(r_m1, q, acc[1]) : acc[1];
                 }
-                r_m2 = r_m1; r_m1 = r0; m_m1 = x.m;
+                r_m2 = r_m1; r_m1 = r0; rho_m1 = rho0; m_m1 = x.m;
             });
     }
     reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
@@ -370,7 +387,9 @@ struct RawCg {
     unsigned char m;
 };
 
-template <bool BC>
+// PC: point-Jacobi PCG -- level 1 uses u = rho / A_vv, level 3 applies A to un = rn / A_vv and
+// accumulates gamma = rn'un, delta = un'A un (reading R19: Chronopoulos-Gear PCG).
+template <bool BC, bool PC>
 __global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
 k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
            const double* __restrict__ rho, const double* __restrict__ p,
@@ -392,7 +411,8 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
         double rho_m1 = 0.0;                       // rho(r-1)
         double w_m1 = 0.0, w_m2 = 0.0;             // w(r-1), w(r-2)
         unsigned char m_m1 = 0, m_m2 = 0;
-        double rn_m3 = 0.0, rn_m2 = 0.0;           // rn(r-3), rn(r-2)
+        double rn_m3 = 0.0, rn_m2 = 0.0;           // rn(r-3), rn(r-2)   (PC: un)
+        double rr_m2 = 0.0;                        // PC: rn(r-2)
         pipeline<unsigned char, RawCg>(
             j0 - 2, j1 - j0 + 4,
             [&](int r) -> unsigned char {
@@ -413,19 +433,22 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
                 return x;
             },
             [&](int r, const RawCg& x) {
-                const double pn0 = x.m ? fma(beta, x.p, x.rho) : 0.0;
+                const double u0 = PC ? x.rho * op.dinv(A, r) : x.rho;
+                const double pn0 = x.m ? fma(beta, x.p, u0) : 0.0;
                 // level 2 at row r-1
                 const double ap = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
-                const double rn1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
+                const double rr1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
+                const double rn1 = PC ? rr1 * op.dinv(A, r - 1) : rr1;
                 // level 3 at row r-2
                 const double q = op.apply(A, r - 2, rn_m2, rn_m3, rn1);
                 const int r2 = r - 2;
+                const double rres = PC ? rr_m2 : rn_m2;
                 if (out_lane && m_m2 && r2 >= j0 && r2 < j1) {   // m_m2 = 0 outside the grid
                     const int v = i + A.pitch * r2;
                     w[v] = fma(alpha, pn_m2, w_m2);
-                    rho_n[v] = rn_m2;
+                    rho_n[v] = rres;
                     p_n[v] = pn_m2;
-                    acc[0] = fma(rn_m2, rn_m2, acc[0]);
+                    acc[0] = fma(rres, rn_m2, acc[0]);
                     acc[1] = fma(rn_m2, q, acc[1]);
                 }
                 pn_m2 = pn_m1; pn_m1 = pn0;
@@ -433,6 +456,7 @@ k2_cg_iter(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask,
                 w_m2 = w_m1; w_m1 = x.w;
                 m_m2 = m_m1; m_m1 = x.m;
                 rn_m3 = rn_m2; rn_m2 = rn1;
+                rr_m2 = rr1;
             });
     }
     reduce_and_finish<2>(acc, R, [&](double* t) { cg_finalize(t[0], t[1], S); });

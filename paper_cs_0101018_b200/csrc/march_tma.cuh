@@ -34,12 +34,14 @@ constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kOut = 28 * kWarps;         // 112 output columns per band
 constexpr int kBW = kOut + 4;             // 116 box columns (2 halo each side)
-constexpr int kBR = 8;                    // rows per pipeline block
 constexpr int kMW = 144;                  // u8 mask box width (start floored to 16 B, 116 + 15 < 144)
-constexpr int kF = kBR * kBW * 8;         // 7424 B: one f64 band box
-constexpr int kFo = kBR * kOut * 8;       // 7168 B: one f64 box of the output columns only
-constexpr int kU = kBR * kMW;             // 1152 B: one u8 mask box
-static_assert(kF % 128 == 0 && kFo % 128 == 0 && kU % 128 == 0, "TMA destinations stay 128-byte aligned");
+constexpr int kBR = 4;                    // rows per pipeline block (small stages: 3-4 CTAs per SM)
+constexpr int r128(int b) { return (b + 127) / 128 * 128; }
+constexpr int kF = kBR * kBW * 8;         // 3712 B: one f64 band box
+constexpr int kFo = kBR * kOut * 8;       // 3584 B: one f64 box of the output columns only
+constexpr int kUt = kBR * kMW;            // 576 B delivered for one u8 mask box
+constexpr int kU = r128(kUt);             // 640 B reserved (stage arrays stay 128-byte aligned)
+static_assert(kF % 128 == 0 && kFo % 128 == 0, "TMA destinations stay 128-byte aligned");
 }  // namespace m4
 
 struct BandGeom {
@@ -104,12 +106,14 @@ __device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigne
 namespace m4cg {
 using namespace m4;
 constexpr int kRho = 0, kP = kF, kW = 2 * kF, kM = 2 * kF + kFo;
-constexpr int kStage = kM + kU;                       // 23168
+constexpr int kStage = kM + kU;                       // 11648
+constexpr int kTx = kM + kUt;                         // bytes the TMA delivers per stage
 constexpr int kNST = 4;
 constexpr int kSmem = kNST * kStage + 64;
 }  // namespace m4cg
 
-__global__ void __launch_bounds__(m4::kThreads, 2)
+template <bool PC>     // point-Jacobi PCG as in k2_cg_iter<BC, true>
+__global__ void __launch_bounds__(m4::kThreads, 4)
 k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, const __grid_constant__ CUtensorMap m_p,
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
            double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R) {
@@ -124,12 +128,12 @@ k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, c
     int gx = 0, moff = 0, y0 = 0, y1 = 0;
     bool col_ok = false;
     Op5<true> op;
-    double pn_m2 = 0.0, pn_m1 = 0.0, rho_m1 = 0.0, rn_m3 = 0.0, rn_m2 = 0.0;
+    double pn_m2 = 0.0, pn_m1 = 0.0, rho_m1 = 0.0, rn_m3 = 0.0, rn_m2 = 0.0, rr_m2 = 0.0, dinv = 0.0;
     unsigned char m_m1 = 0, m_m2 = 0;
     band_pipeline<kNST, kStage>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
-            mbar_expect_tx(bar, kStage);
+            mbar_expect_tx(bar, kTx);
             tma_load_2d(st + kRho, &m_rho, x0 - 2, yr - G.rlo, bar);
             tma_load_2d(st + kP, &m_p, x0 - 2, yr - G.rlo, bar);
             tma_load_2d(st + kW, &m_w, x0, yr - 2 - G.rlo, bar);      // w of the emitted rows (r - 2)
@@ -142,7 +146,8 @@ k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, c
             y1 = ye;
             col_ok = gx >= 0 && gx < A.nx;
             op.init(A, gx);
-            pn_m2 = pn_m1 = rho_m1 = rn_m3 = rn_m2 = 0.0;
+            dinv = op.dinv(A, 0);
+            pn_m2 = pn_m1 = rho_m1 = rn_m3 = rn_m2 = rr_m2 = 0.0;
             m_m1 = m_m2 = 0;
         },
         [&](const unsigned char* st, int kk, int r) {
@@ -151,23 +156,26 @@ k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, c
             const double* wS = reinterpret_cast<const double*>(st + kW);
             const unsigned char m = st[kM + kk * kMW + c + moff];
             const double rho = rhoS[kk * kBW + c];
-            const double pn0 = m ? fma(beta, pS[kk * kBW + c], rho) : 0.0;
+            const double pn0 = m ? fma(beta, pS[kk * kBW + c], PC ? rho * dinv : rho) : 0.0;
             const double ap = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
-            const double rn1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
+            const double rr1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
+            const double rn1 = PC ? rr1 * dinv : rr1;
             const double q = op.apply(A, r - 2, rn_m2, rn_m3, rn1);
             const int r2 = r - 2;
+            const double rres = PC ? rr_m2 : rn_m2;
             if (out_lane && m_m2 && col_ok && r2 >= y0 && r2 < y1) {
                 const long long v = (long long)gx + (long long)A.pitch * r2;
                 w_out[v] = fma(alpha, pn_m2, wS[kk * kOut + c - 2]);
-                rho_n[v] = rn_m2;
+                rho_n[v] = rres;
                 p_n[v] = pn_m2;
-                acc[0] = fma(rn_m2, rn_m2, acc[0]);
+                acc[0] = fma(rres, rn_m2, acc[0]);
                 acc[1] = fma(rn_m2, q, acc[1]);
             }
             pn_m2 = pn_m1; pn_m1 = pn0;
             rho_m1 = rho;
             m_m2 = m_m1; m_m1 = m;
             rn_m3 = rn_m2; rn_m2 = rn1;
+            rr_m2 = rr1;
         });
     reduce_and_finish<2>(acc, R, [&](double* tt) { cg_finalize(tt[0], tt[1], S); });
 }
@@ -189,19 +197,20 @@ struct AccLayout4 {
     static constexpr int kU = kL + (SB ? 0 : m4::kF);
     static constexpr int kMP = kU + (SB ? 0 : m4::kF);
     static constexpr int kStage = kMP + m4::kU;
-    static constexpr int kNST = SB ? 4 : 3;
+    static constexpr int kNST = 4;
     static constexpr int kSmem = kNST * kStage + 64;
 };
 
 template <bool SB, bool HasDir>
-__global__ void __launch_bounds__(m4::kThreads, 2)
+__global__ void __launch_bounds__(m4::kThreads, 4)
 k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
           const __grid_constant__ CUtensorMap m_mp, int has_mp, double sgn, double* __restrict__ y_out,
-          double* __restrict__ g_out, unsigned char* __restrict__ mask_out, Scal* S, RedScratch R) {
+          double* __restrict__ g_out, unsigned char* __restrict__ mask_out, Scal* S, RedScratch R, int gp) {
     using namespace m4;
     using L = AccLayout4<SB, HasDir>;
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     double alpha = 0.0;
     if (HasDir) {
         if (S->s_h < 0) return;                   // uniform: no accepted step in this batch
@@ -217,7 +226,7 @@ k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMa
     Op5<true> op;
     double yn_m2 = 0.0, yn_m1 = 0.0, b_m1 = 0.0, l_m1 = 0.0, u_m1 = 0.0, l_m2 = 0.0, u_m2 = 0.0;
     double gn_m2 = 0.0, d_m3 = 0.0, d_m2 = 0.0;
-    const uint32_t tx = L::kStage - (has_mp ? 0 : kU);
+    const uint32_t tx = L::kMP + (has_mp ? kUt : 0);
     band_pipeline<L::kNST, L::kStage>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
@@ -301,14 +310,15 @@ struct SrchLayout4 {
 };
 
 template <bool SB, bool DG>
-__global__ void __launch_bounds__(m4::kThreads, 2)
+__global__ void __launch_bounds__(m4::kThreads, 4)
 k4_search(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_g,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, double sgn,
-          int use_alpha0, int h0, double mu, Scal* S, RedScratch R) {
+          int use_alpha0, int h0, double mu, Scal* S, RedScratch R, int gp) {
     using namespace m4;
     using L = SrchLayout4<SB, DG>;
     constexpr int K = 2;
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
         if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
         return;

@@ -230,7 +230,8 @@ k3_accept(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMa
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
           const __grid_constant__ CUtensorMap m_mp, int has_dir, double sgn, int has_mp,
           double* __restrict__ y_out, double* __restrict__ g_out, unsigned char* __restrict__ mask_out,
-          Scal* S, RedScratch R) {
+          Scal* S, RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     double alpha = 0.0;
     if (has_dir) {
         if (S->s_h < 0) return;
@@ -350,8 +351,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 k3_search(StencilOp A, TileGeom T, Bounds Bd, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_g,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, double sgn,
-          int use_alpha0, int h0, double mu, Scal* S, RedScratch R) {
+          int use_alpha0, int h0, double mu, Scal* S, RedScratch R, int gp) {
     constexpr int K = 2;
+    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     if (use_alpha0 && !S->cauchy_ok) {
         if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
         return;

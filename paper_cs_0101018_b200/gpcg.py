@@ -31,7 +31,8 @@ class Params(C.Structure):
     _fields_ = [("mu", C.c_double), ("eta1", C.c_double), ("eta2", C.c_double),
                 ("eta2_shrink", C.c_double), ("eta2_floor", C.c_double),
                 ("gp_cap", C.c_int64), ("refine_cap", C.c_int64), ("max_halvings", C.c_int64),
-                ("cg_cap", C.c_int64), ("search_k", C.c_int32), ("cg_chunk", C.c_int32)]
+                ("cg_cap", C.c_int64), ("search_k", C.c_int32), ("cg_chunk", C.c_int32),
+                ("gp_chunk", C.c_int32), ("precond", C.c_int32)]
 
 
 class Stats(C.Structure):

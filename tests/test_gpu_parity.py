@@ -311,3 +311,39 @@ def test_solve_parity_vs_oracle_golden(G, name):
         free_val = x[i] if acto[k] else xo[k]
         assert min(abs(free_val - prob.l[i]), abs(free_val - prob.u[i])) <= 1e-7, (i, x[i], xo[k])
     assert abs(st["n_active"] - gold["n_active"]) <= gold["n_free_near_bound"] + 0.001 * prob.n
+
+
+# ------------------------------------------------------------------ point-Jacobi PCG
+PCG_CASES = ["C0", "C1", "jb80_eps0.9", "c4_family_m16", "ragged37x23", "dense8"]
+
+
+@pytest.mark.parametrize("case", PCG_CASES)
+def test_solve_parity_pcg(G, oracle, case):
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, params=oracle.default_params(precond=1))
+    assert rc_o == 0
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=1)
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0, (rc, st)
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
+    nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+    assert not nontie
+
+
+def test_pcg_fewer_cg_iterations_on_scaled_operator(G):
+    """Badly scaled rows (full faces with a wide spread): the diagonal preconditioner
+    must cut CG iterations (the point Jacobi method is the baseline of Table 4)."""
+    prob = ragged_stencil(60, 50, 9, bounds="inf")
+    sc = np.exp(3.0 * P.uniform(9, 50, prob.n))
+    prob.shift = prob.shift * 0 + sc            # diagonal shift spanning 3 decades
+    its = {}
+    for pc in (0, 1):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(precond=pc)
+            rc, x, st = s.solve(np.zeros(prob.n), -1e-10)
+        assert rc == 0
+        its[pc] = st["cg_iters"]
+    assert its[1] < its[0], its

@@ -92,3 +92,16 @@ def test_slab_errors(G):
     with pytest.raises(G.GpcgError) as e:
         G.Solver.from_problem(prob, slabs=2)          # a slab of < 2 stencil rows
     assert e.value.code == G.EINVAL
+
+
+@pytest.mark.parametrize("case", ["C1", "c4_family_m12", "ragged37x23_full_shift"])
+def test_slab_pcg_parity(G, oracle, case):
+    make, tol = CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, params=oracle.default_params(precond=1))
+    with G.Solver.from_problem(prob, slabs=3) as s:
+        s.set_params(precond=1)
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0 and rc_o == 0
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
