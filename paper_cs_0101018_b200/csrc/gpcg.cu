@@ -164,6 +164,7 @@ struct Slab {
     unsigned char* mb[NMSK] = {};
     unsigned char* m[NMSK] = {};
     double *wxb = nullptr, *wyb = nullptr, *shb = nullptr;   // face arrays / shift (bases)
+    double* brow = nullptr;         // global grid row 0 of b (nx), for the row-broadcast test / k4_accept
     long long* rp = nullptr;
     int* ci = nullptr;
     double* val = nullptr;
@@ -198,6 +199,7 @@ struct gpcg_problem {
     bool generic = false;           // GPCG_GENERIC=1: stencil problems use the flat generic kernels (A/B tests)
     bool sb = false;                // scalar (constant) bounds
     bool bc = false;                // stencil with broadcast faces and no shift
+    bool bb = false;                // stencil with b equal in every grid row (k4_accept reads brow)
     bool tile = false;              // TMA tile path built
     int tile_mask = 63;             // GPCG_TILE bits: TMA tile kernels (k3) 1 accept, 2 search, 4 CG
                                     // iteration; TMA-fed column march (k4, preferred) 8 CG, 16 accept,
@@ -399,7 +401,7 @@ void free_all(gpcg_problem* h) {
     for (Slab& S : h->slabs) {
         for (double* p : S.vb) if (p) cudaFree(p);
         for (unsigned char* p : S.mb) if (p) cudaFree(p);
-        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.rp, (void*)S.ci, (void*)S.val,
+        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.rp, (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             if (p) cudaFree(p);
     }
@@ -479,10 +481,14 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem));
     RC(set_smem(k4_cg_iter<false>, m4cg::kSmem));
     RC(set_smem(k4_cg_iter<true>, m4cg::kSmem));
-    RC(set_smem(k4_accept<true, true>, AccLayout4<true, true>::kSmem));
-    RC(set_smem(k4_accept<true, false>, AccLayout4<true, false>::kSmem));
-    RC(set_smem(k4_accept<false, true>, AccLayout4<false, true>::kSmem));
-    RC(set_smem(k4_accept<false, false>, AccLayout4<false, false>::kSmem));
+    RC(set_smem(k4_accept<true, true, false>, AccLayout4<true, true, false>::kSmem));
+    RC(set_smem(k4_accept<true, false, false>, AccLayout4<true, false, false>::kSmem));
+    RC(set_smem(k4_accept<false, true, false>, AccLayout4<false, true, false>::kSmem));
+    RC(set_smem(k4_accept<false, false, false>, AccLayout4<false, false, false>::kSmem));
+    RC(set_smem(k4_accept<true, true, true>, AccLayout4<true, true, true>::kSmem));
+    RC(set_smem(k4_accept<true, false, true>, AccLayout4<true, false, true>::kSmem));
+    RC(set_smem(k4_accept<false, true, true>, AccLayout4<false, true, true>::kSmem));
+    RC(set_smem(k4_accept<false, false, true>, AccLayout4<false, false, true>::kSmem));
     RC(set_smem(k4_search<true, true>, SrchLayout4<true, true>::kSmem));
     RC(set_smem(k4_search<true, false>, SrchLayout4<true, false>::kSmem));
     RC(set_smem(k4_search<false, true>, SrchLayout4<false, true>::kSmem));
@@ -503,8 +509,10 @@ int setup_tile(gpcg_problem* h) {
         return std::max(1, nb) * h->sms;
     };
     const int r4cg = res4(k4_cg_iter<false>, m4cg::kSmem);
-    const int r4acc = h->sb ? res4(k4_accept<true, true>, AccLayout4<true, true>::kSmem)
-                            : res4(k4_accept<false, true>, AccLayout4<false, true>::kSmem);
+    const int r4acc = h->sb ? (h->bb ? res4(k4_accept<true, true, true>, AccLayout4<true, true, true>::kSmem)
+                                     : res4(k4_accept<true, true, false>, AccLayout4<true, true, false>::kSmem))
+                            : (h->bb ? res4(k4_accept<false, true, true>, AccLayout4<false, true, true>::kSmem)
+                                     : res4(k4_accept<false, true, false>, AccLayout4<false, true, false>::kSmem));
     const int r4srch = h->sb ? res4(k4_search<true, true>, SrchLayout4<true, true>::kSmem)
                              : res4(k4_search<false, true>, SrchLayout4<false, true>::kSmem);
     for (Slab& S : h->slabs) {
@@ -704,14 +712,19 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
             const CUtensorMap& md = S.t4[dir >= 0 ? dir : y_in];
             const CUtensorMap& mp = S.t4m[mask_prev >= 0 ? mask_prev : MK0];
             const int has_mp = mask_prev >= 0 ? 1 : 0;
-            auto go = [&](auto sbt, auto hdt) {
-                constexpr bool SB = decltype(sbt)::value, HD = decltype(hdt)::value;
-                k4_accept<SB, HD><<<S.grid4_acc, m4::kThreads, AccLayout4<SB, HD>::kSmem, h->st>>>(
-                    S.sop, S.bg_acc, B, S.t4[y_in], md, S.t4[VB], S.t4[VL], S.t4[VU], mp, has_mp, sgn, S.v[y_out],
-                    S.v[g_out], S.m[m_out], h->dS, R, gp);
+            auto go = [&](auto sbt, auto hdt, auto bbt) {
+                constexpr bool SB = decltype(sbt)::value, HD = decltype(hdt)::value, BB = decltype(bbt)::value;
+                k4_accept<SB, HD, BB><<<S.grid4_acc, m4::kThreads, AccLayout4<SB, HD, BB>::kSmem, h->st>>>(
+                    S.sop, S.bg_acc, B, S.brow, S.t4[y_in], md, S.t4[VB], S.t4[VL], S.t4[VU], mp, has_mp, sgn,
+                    S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
             };
-            if (h->sb) { if (dir >= 0) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
-            else { if (dir >= 0) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+            auto bydir = [&](auto sbt, auto bbt) {
+                if (dir >= 0) go(sbt, std::true_type(), bbt); else go(sbt, std::false_type(), bbt);
+            };
+            auto bybb = [&](auto sbt) {
+                if (h->bb) bydir(sbt, std::true_type()); else bydir(sbt, std::false_type());
+            };
+            if (h->sb) bybb(std::true_type()); else bybb(std::false_type());
         } else if (use_tile) {
             const CUtensorMap& md = S.tm[dir >= 0 ? dir : y_in];
             const CUtensorMap& mp = S.tmm[mask_prev >= 0 ? mask_prev : MK0];
@@ -1070,6 +1083,29 @@ int launch_objective(gpcg_problem* h, int x) {
     return finish_reduce(h, fin(FIN_R2), 2);
 }
 
+// Is b the same in every grid row?  (global row 0 from slab 0 / rank 0, compared everywhere)
+int detect_b_rows(gpcg_problem* h) {
+    for (Slab& S : h->slabs) {
+        CK(cudaMalloc(&S.brow, (size_t)h->nx * sizeof(double)));
+        CK(cudaMemcpyAsync(S.brow, h->slabs[0].v[VB], (size_t)h->nx * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    }
+    if (h->nranks > 1)
+        NK(nccl_api()->Broadcast(h->slabs[0].brow, h->slabs[0].brow, (size_t)h->nx, ncclDouble, 0, h->comm, h->st));
+    for (int s = 1; s < h->nslabs(); ++s)
+        CK(cudaMemcpyAsync(h->slabs[s].brow, h->slabs[0].brow, (size_t)h->nx * sizeof(double),
+                           cudaMemcpyDeviceToDevice, h->st));
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const int g = std::max(1, std::min((int)(((long long)S.rows * h->nx + kThreads - 1) / kThreads), h->sms * 4));
+        k_count_row_mismatch<<<g, kThreads, 0, h->st>>>(h->nx, S.rows, h->pitch, S.v[VB], S.brow, h->dS, h->red(s));
+        CKLAUNCH();
+    }
+    RC(finish_reduce(h, fin(FIN_R2), 2));
+    RC(sync_scal(h));
+    h->bb = (h->hS->r0 == 0.0);
+    return GPCG_OK;
+}
+
 // 1 / diag(A) of every slab (+ ghosts): the point-Jacobi preconditioner
 int setup_jacobi(gpcg_problem* h) {
     for (Slab& S : h->slabs) {
@@ -1202,6 +1238,7 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
     if ((rc = setup_stencil_slabs(h, wx, wy, shift))) return fail(rc);
     h->bc = (wx_ld == 0 && wy_ld == 0 && shift == nullptr);
     if ((rc = setup_jacobi(h))) return fail(rc);
+    if ((rc = detect_b_rows(h))) return fail(rc);
     {
         const char* e = getenv("GPCG_TILE");
         if (e && *e) h->tile_mask = atoi(e) & 63;

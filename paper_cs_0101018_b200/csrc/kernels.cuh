@@ -280,6 +280,19 @@ k_jacobi_inverse(Op A, double* __restrict__ dinv) {
     });
 }
 
+// #entries of the owned rows that differ from row[] (the row-broadcast test for b)
+__global__ void __launch_bounds__(kThreads)
+k_count_row_mismatch(int cols, int rows, int pitch, const double* __restrict__ a, const double* __restrict__ row,
+                     Scal* S, RedScratch R) {
+    double acc[2] = {0.0, 0.0};
+    const long long n = (long long)cols * rows;
+    for (long long k = blockIdx.x * (long long)kThreads + threadIdx.x; k < n; k += (long long)gridDim.x * kThreads) {
+        const long long i = k % cols, v = i + (k / cols) * (long long)pitch;
+        acc[0] += (a[v] != row[i]) ? 1.0 : 0.0;
+    }
+    reduce_and_finish<2>(acc, R, [&](double* t) { S->r0 = t[0]; S->r1 = t[1]; });
+}
+
 // ----------------------------------------------------------------------------
 // input validation at create: #(l > u or NaN), #(b NaN), l / u constant?
 // ----------------------------------------------------------------------------

@@ -188,12 +188,14 @@ k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, c
 //   level 3  Ad(r-2) = (A d)(r-2);  emit row r-2
 // Stage: y | dir | b | l | u (band boxes, rows yr..; dir, l/u optional) | mask_prev (rows yr-2..)
 // ============================================================================
-template <bool SB, bool HasDir>
+// BB: b is the same in every grid row (detected at create; the journal-bearing b depends on xi_1
+// only) -> read once per column from brow, not streamed.
+template <bool SB, bool HasDir, bool BB>
 struct AccLayout4 {
     static constexpr int kY = 0;
     static constexpr int kD = m4::kF;
     static constexpr int kB = kD + (HasDir ? m4::kF : 0);
-    static constexpr int kL = kB + m4::kF;
+    static constexpr int kL = kB + (BB ? 0 : m4::kF);
     static constexpr int kU = kL + (SB ? 0 : m4::kF);
     static constexpr int kMP = kU + (SB ? 0 : m4::kF);
     static constexpr int kStage = kMP + m4::kU;
@@ -201,15 +203,15 @@ struct AccLayout4 {
     static constexpr int kSmem = kNST * kStage + 64;
 };
 
-template <bool SB, bool HasDir>
+template <bool SB, bool HasDir, bool BB>
 __global__ void __launch_bounds__(m4::kThreads, 4)
-k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMap m_y,
+k4_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
           const __grid_constant__ CUtensorMap m_mp, int has_mp, double sgn, double* __restrict__ y_out,
           double* __restrict__ g_out, unsigned char* __restrict__ mask_out, Scal* S, RedScratch R, int gp) {
     using namespace m4;
-    using L = AccLayout4<SB, HasDir>;
+    using L = AccLayout4<SB, HasDir, BB>;
     if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
     double alpha = 0.0;
     if (HasDir) {
@@ -225,7 +227,7 @@ k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMa
     bool col_ok = false;
     Op5<true> op;
     double yn_m2 = 0.0, yn_m1 = 0.0, b_m1 = 0.0, l_m1 = 0.0, u_m1 = 0.0, l_m2 = 0.0, u_m2 = 0.0;
-    double gn_m2 = 0.0, d_m3 = 0.0, d_m2 = 0.0;
+    double gn_m2 = 0.0, d_m3 = 0.0, d_m2 = 0.0, bcol = 0.0;
     const uint32_t tx = L::kMP + (has_mp ? kUt : 0);
     band_pipeline<L::kNST, L::kStage>(
         G, A.ny, smem,
@@ -234,7 +236,7 @@ k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMa
             const int yt = yr - G.rlo;
             tma_load_2d(st + L::kY, &m_y, x0 - 2, yt, bar);
             if (HasDir) tma_load_2d(st + L::kD, &m_dir, x0 - 2, yt, bar);
-            tma_load_2d(st + L::kB, &m_b, x0 - 2, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, &m_b, x0 - 2, yt, bar);
             if (!SB) {
                 tma_load_2d(st + L::kL, &m_l, x0 - 2, yt, bar);
                 tma_load_2d(st + L::kU, &m_u, x0 - 2, yt, bar);
@@ -248,6 +250,7 @@ k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMa
             y1 = ye;
             col_ok = gx >= 0 && gx < A.nx;
             op.init(A, gx);
+            if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
             yn_m2 = yn_m1 = b_m1 = l_m1 = u_m1 = l_m2 = u_m2 = gn_m2 = d_m3 = d_m2 = 0.0;
         },
         [&](const unsigned char* st, int kk, int r) {
@@ -255,7 +258,8 @@ k4_accept(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMa
             // raw values; outside the readable rows / columns the bounds are 0 so yn = 0 (Dirichlet)
             const bool in = col_ok && r >= A.rlo && r < A.rhi;
             const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
-            const double bv = reinterpret_cast<const double*>(st + L::kB)[q];
+            const double bv = BB ? ((r >= A.rlo && r < A.rhi) ? bcol : 0.0)
+                                 : reinterpret_cast<const double*>(st + L::kB)[q];
             const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
             const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
             double yn0;
