@@ -186,6 +186,11 @@ struct Slab {
     CUtensorMap t4m[NMSK];
     BandGeom bg_cg{}, bg_acc{}, bg_srch{};   // band x segment items sized to each kernel's residency
     int grid4_cg = 1, grid4_acc = 1, grid4_srch = 1;
+    // g-free sweeps (k5_*): 112-column boxes from x0 - 4, 128-byte mask boxes, 104-column bands
+    CUtensorMap t5[NVEC];
+    CUtensorMap t5m[NMSK];
+    BandGeom bg5_acc{}, bg5_srch{}, bg5_init{};
+    int grid5_acc = 1, grid5_srch = 1, grid5_init = 1;
 };
 
 }  // namespace
@@ -201,9 +206,11 @@ struct gpcg_problem {
     bool bc = false;                // stencil with broadcast faces and no shift
     bool bb = false;                // stencil with b equal in every grid row (k4_accept reads brow)
     bool tile = false;              // TMA tile path built
-    int tile_mask = 63;             // GPCG_TILE bits: TMA tile kernels (k3) 1 accept, 2 search, 4 CG
+    int tile_mask = 127;            // GPCG_TILE bits: TMA tile kernels (k3) 1 accept, 2 search, 4 CG
                                     // iteration; TMA-fed column march (k4, preferred) 8 CG, 16 accept,
-                                    // 32 search.  0 = column march (k2) only.
+                                    // 32 search; 64 g-free k5 accept / search / CG init (preferred,
+                                    // g is never stored).  0 = column march (k2) only.
+    bool gfree = false;             // k5 sweeps active: the G vectors are not maintained
     int nx = 0, pitch = 1;          // stencil: grid width and row pitch (nx rounded up to 32); CSR: 1
     long long wx_ld = 0, wy_ld = 0; // user face layout (0 = broadcast)
     long long n_local = 0;          // entries owned by this rank (the user's arrays)
@@ -489,6 +496,20 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k4_accept<true, false, true>, AccLayout4<true, false, true>::kSmem));
     RC(set_smem(k4_accept<false, true, true>, AccLayout4<false, true, true>::kSmem));
     RC(set_smem(k4_accept<false, false, true>, AccLayout4<false, false, true>::kSmem));
+#define K5ACC(SB, BB, M) RC(set_smem(k5_accept<SB, BB, M>, AccLayout5<SB, BB, M>::kSmem));
+#define K5ACC2(SB, BB) K5ACC(SB, BB, m5::GP) K5ACC(SB, BB, m5::CG) K5ACC(SB, BB, m5::PROJ)
+    K5ACC2(true, true) K5ACC2(true, false) K5ACC2(false, true) K5ACC2(false, false)
+#define K5S(SB, BB, M, K) RC(set_smem(k5_search<SB, BB, M, K>, SrchLayout5<SB, BB, M, K>::kSmem));
+#define K5S2(SB, BB) K5S(SB, BB, m5::GP, 2) K5S(SB, BB, m5::GP, 8) K5S(SB, BB, m5::CG, 2) K5S(SB, BB, m5::CG, 8)
+    K5S2(true, true) K5S2(true, false) K5S2(false, true) K5S2(false, false)
+    RC(set_smem(k5_cg_init<true, true>, CgInitLayout5<true>::kSmem));
+    RC(set_smem(k5_cg_init<true, false>, CgInitLayout5<true>::kSmem));
+    RC(set_smem(k5_cg_init<false, true>, CgInitLayout5<false>::kSmem));
+    RC(set_smem(k5_cg_init<false, false>, CgInitLayout5<false>::kSmem));
+#undef K5ACC
+#undef K5ACC2
+#undef K5S
+#undef K5S2
     RC(set_smem(k4_search<true, true>, SrchLayout4<true, true>::kSmem));
     RC(set_smem(k4_search<true, false>, SrchLayout4<true, false>::kSmem));
     RC(set_smem(k4_search<false, true>, SrchLayout4<false, true>::kSmem));
@@ -515,6 +536,18 @@ int setup_tile(gpcg_problem* h) {
                                      : res4(k4_accept<false, true, false>, AccLayout4<false, true, false>::kSmem));
     const int r4srch = h->sb ? res4(k4_search<true, true>, SrchLayout4<true, true>::kSmem)
                              : res4(k4_search<false, true>, SrchLayout4<false, true>::kSmem);
+    // k5: residency of the GP-mode variants of this problem's (SB, BB)
+    int r5acc, r5srch, r5init;
+    {
+        auto pick = [&](auto sbt, auto bbt) {
+            constexpr bool SB = decltype(sbt)::value, BB = decltype(bbt)::value;
+            r5acc = res4(k5_accept<SB, BB, m5::GP>, AccLayout5<SB, BB, m5::GP>::kSmem);
+            r5srch = res4(k5_search<SB, BB, m5::GP, 2>, SrchLayout5<SB, BB, m5::GP, 2>::kSmem);
+            r5init = res4(k5_cg_init<BB, false>, CgInitLayout5<BB>::kSmem);
+        };
+        if (h->sb) { if (h->bb) pick(std::true_type(), std::true_type()); else pick(std::true_type(), std::false_type()); }
+        else { if (h->bb) pick(std::false_type(), std::true_type()); else pick(std::false_type(), std::false_type()); }
+    }
     for (Slab& S : h->slabs) {
         for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
             RC(make_map(h, S, &S.tm[id], S.v[id], false, TBW, TBH));
@@ -528,8 +561,11 @@ int setup_tile(gpcg_problem* h) {
             RC(make_map(h, S, &S.t4[id], S.v[id], false, m4::kBW, m4::kBR));
         RC(make_map(h, S, &S.t4wo, S.v[VW], false, m4::kOut, m4::kBR));
         for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t4m[k], S.m[k], true, m4::kMW, m4::kBR));
-        auto band = [&](int resident, BandGeom& G, int& grid) {
-            G.nbands = (h->nx + m4::kOut - 1) / m4::kOut;
+        for (int id : {VY0, VY1, VW, VB, VL, VU, VIN})
+            RC(make_map(h, S, &S.t5[id], S.v[id], false, m5::kBW, m4::kBR));
+        for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t5m[k], S.m[k], true, m5::kMW, m4::kBR));
+        auto band = [&](int resident, BandGeom& G, int& grid, int out = m4::kOut) {
+            G.nbands = (h->nx + out - 1) / out;
             G.nsegs = std::max(1, std::min(resident / G.nbands, (S.rows + 15) / 16));
             G.seg = (S.rows + G.nsegs - 1) / G.nsegs;
             G.nsegs = (S.rows + G.seg - 1) / G.seg;
@@ -539,11 +575,15 @@ int setup_tile(gpcg_problem* h) {
         band(r4cg, S.bg_cg, S.grid4_cg);
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
+        band(r5acc, S.bg5_acc, S.grid5_acc, m5::kOut);
+        band(r5srch, S.bg5_srch, S.grid5_srch, m5::kOut);
+        band(r5init, S.bg5_init, S.grid5_init, m5::kOut);
         S.grid_t_cg = std::min(ntiles, r_cg);
         S.grid_t_acc = std::min(ntiles, r_acc);
         S.grid_t_srch = std::min(ntiles, r_srch);
     }
     h->tile = true;
+    h->gfree = (h->tile_mask & 64) != 0;
     return GPCG_OK;
 }
 
@@ -702,13 +742,35 @@ int layout_slabs(gpcg_problem* h, long long rows_rank, int nsl, int ghost) {
 // ---------------------------------------------------------------- launches (every slab)
 int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev, int y_out, int g_out, int m_out,
                   int gp = 0) {
+    const bool use_k5 = h->gfree;
     const bool use_k4 = h->tile && (h->tile_mask & 16);
     const bool use_tile = h->tile && (h->tile_mask & (1 | 16));
+    const int mode = dir < 0 ? m5::PROJ : ((dir == VG0 || dir == VG1) ? m5::GP : m5::CG);
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
         const RedScratch R = h->red(s);
-        if (use_k4) {
+        if (use_k5) {
+            const CUtensorMap& md = S.t5[dir >= 0 && mode == m5::CG ? dir : y_in];
+            const CUtensorMap& mp = S.t5m[mask_prev >= 0 ? mask_prev : MK0];
+            const int has_mp = mask_prev >= 0 ? 1 : 0;
+            auto go = [&](auto sbt, auto bbt, auto mt) {
+                constexpr bool SB = decltype(sbt)::value, BB = decltype(bbt)::value;
+                constexpr int M = decltype(mt)::value;
+                k5_accept<SB, BB, M><<<S.grid5_acc, m4::kThreads, AccLayout5<SB, BB, M>::kSmem, h->st>>>(
+                    S.sop, S.bg5_acc, B, S.brow, S.t5[y_in], md, S.t5[VB], S.t5[VL], S.t5[VU], mp, has_mp,
+                    S.v[y_out], S.m[m_out], h->dS, R, gp);
+            };
+            auto bymode = [&](auto sbt, auto bbt) {
+                if (mode == m5::GP) go(sbt, bbt, std::integral_constant<int, m5::GP>());
+                else if (mode == m5::CG) go(sbt, bbt, std::integral_constant<int, m5::CG>());
+                else go(sbt, bbt, std::integral_constant<int, m5::PROJ>());
+            };
+            auto bybb = [&](auto sbt) {
+                if (h->bb) bymode(sbt, std::true_type()); else bymode(sbt, std::false_type());
+            };
+            if (h->sb) bybb(std::true_type()); else bybb(std::false_type());
+        } else if (use_k4) {
             const CUtensorMap& md = S.t4[dir >= 0 ? dir : y_in];
             const CUtensorMap& mp = S.t4m[mask_prev >= 0 ? mask_prev : MK0];
             const int has_mp = mask_prev >= 0 ? 1 : 0;
@@ -766,6 +828,7 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
     a.has_dir = dir >= 0 ? 1 : 0;
     a.gp = gp;
     RC(finish_reduce(h, a, a.kind == FIN_ACCEPT ? 6 : 5));
+    if (use_k5) return exchange(h, {y_out}, {m_out});      // g is not stored
     return exchange(h, {y_out, g_out}, {m_out});
 }
 
@@ -798,13 +861,35 @@ int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
 int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_alpha0, int h0, int K, int gp = 0) {
     const double mu = h->prm.mu;
     const bool dg = (dir == g);
+    const bool use_k5 = h->gfree;                                  // K = 2 and the K = 8 retries
     const bool use_k4 = h->tile && (h->tile_mask & 32) && K == 2;  // retries use the column march
     const bool use_tile = h->tile && (h->tile_mask & 2) && K == 2;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
         const RedScratch R = h->red(s);
-        if (use_k4) {
+        if (use_k5) {
+            // GP: direction -g (recomputed from y); CG: direction w
+            auto go = [&](auto sbt, auto bbt, auto mt, auto kt) {
+                constexpr bool SB = decltype(sbt)::value, BB = decltype(bbt)::value;
+                constexpr int M = decltype(mt)::value, KK = decltype(kt)::value;
+                k5_search<SB, BB, M, KK><<<S.grid5_srch, m4::kThreads, SrchLayout5<SB, BB, M, KK>::kSmem, h->st>>>(
+                    S.sop, S.bg5_srch, B, S.brow, S.t5[y], S.t5[dg ? y : dir], S.t5[VB], S.t5[VL], S.t5[VU], h0, mu,
+                    h->dS, R, gp);
+            };
+            auto byk = [&](auto sbt, auto bbt, auto mt) {
+                if (K == 2) go(sbt, bbt, mt, std::integral_constant<int, 2>());
+                else go(sbt, bbt, mt, std::integral_constant<int, 8>());
+            };
+            auto bymode = [&](auto sbt, auto bbt) {
+                if (dg) byk(sbt, bbt, std::integral_constant<int, m5::GP>());
+                else byk(sbt, bbt, std::integral_constant<int, m5::CG>());
+            };
+            auto bybb = [&](auto sbt) {
+                if (h->bb) bymode(sbt, std::true_type()); else bymode(sbt, std::false_type());
+            };
+            if (h->sb) bybb(std::true_type()); else bybb(std::false_type());
+        } else if (use_k4) {
             auto go = [&](auto sbt, auto dgt) {
                 constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
                 k4_search<SB, DG><<<S.grid4_srch, m4::kThreads, SrchLayout4<SB, DG>::kSmem, h->st>>>(
@@ -1017,7 +1102,16 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
         const bool pc = h->prm.precond == 1;
-        if (!h->is_csr && !h->generic) {
+        if (h->gfree) {
+            auto go = [&](auto bbt, auto pct) {
+                constexpr bool BB = decltype(bbt)::value, PC = decltype(pct)::value;
+                k5_cg_init<BB, PC><<<S.grid5_init, m4::kThreads, CgInitLayout5<BB>::kSmem, h->st>>>(
+                    S.sop, S.bg5_init, S.brow, S.t5[vy(cur)], S.t5[VB], S.t5m[cur], S.m[MKCG], S.v[VRHO0], S.v[VQ0],
+                    S.v[VW], eta2, cap, h->dS, R);
+            };
+            if (h->bb) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
+            else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else if (!h->is_csr && !h->generic) {
             auto go = [&](auto bct, auto pct) {
                 constexpr bool BC = decltype(bct)::value, PC = decltype(pct)::value;
                 k2_cg_init<BC, PC><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.v[vg(cur)], S.m[cur],
@@ -1241,7 +1335,7 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
     if ((rc = detect_b_rows(h))) return fail(rc);
     {
         const char* e = getenv("GPCG_TILE");
-        if (e && *e) h->tile_mask = atoi(e) & 63;
+        if (e && *e) h->tile_mask = atoi(e) & 127;
         if (h->bc && !h->generic && h->tile_mask != 0 && (rc = setup_tile(h))) return fail(rc);
     }
     h->nnz = 5 * h->n_global - 2 * nx - 2 * ny;

@@ -51,21 +51,22 @@ struct BandGeom {
 
 // The pipeline engine.  issue(stage_ptr, x0, yr, bar): TMA loads of the block whose
 // first raw row is yr (band output columns start at x0); begin(x0, y0, y1): a new
-// item; row(stage_ptr, kk, r): one raw row (kk-th of the block).
-template <int NST, int STAGE, class Issue, class Begin, class Row>
+// item; row(stage_ptr, kk, r): one raw row (kk-th of the block).  OUT = output
+// columns per band; the raw rows of an item run from y0 - PRE to y1 - 1 + POST.
+template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
 __device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
                                               Begin&& begin, Row&& row) {
     using namespace m4;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     const int nitems = G.nbands * G.nsegs;
-    const int nblk = (G.seg + 4 + kBR - 1) / kBR;          // raw rows y0-2 .. y1+2
+    const int nblk = (G.seg + PRE + POST + kBR - 1) / kBR;
     auto issue = [&](int k) {
         const int i = k / nblk, b = k - i * nblk;
         const int t = blockIdx.x + i * (int)gridDim.x;
         if (t >= nitems) return;
         const int stage = k % NST;
-        const int x0 = (t % G.nbands) * kOut;
-        const int yr = (t / G.nbands) * G.seg - 2 + b * kBR;
+        const int x0 = (t % G.nbands) * OUT;
+        const int yr = (t / G.nbands) * G.seg - PRE + b * kBR;
         issue_loads(smem + stage * STAGE, x0, yr, &bar[stage]);
     };
     if (threadIdx.x == 0) {
@@ -76,14 +77,14 @@ __device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigne
     __syncthreads();
     int k = 0;
     for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
-        const int x0 = (t % G.nbands) * kOut;
+        const int x0 = (t % G.nbands) * OUT;
         const int y0 = (t / G.nbands) * G.seg, y1 = min(y0 + G.seg, ny);
         begin(x0, y0, y1);
         for (int b = 0; b < nblk; ++b, ++k) {
             const int stage = k % NST;
             unsigned char* st = smem + stage * STAGE;
             mbar_wait(&bar[stage], (k / NST) & 1);
-            const int yr = y0 - 2 + b * kBR;
+            const int yr = y0 - PRE + b * kBR;
 #pragma unroll
             for (int kk = 0; kk < kBR; ++kk) row(st, kk, yr + kk);
             __syncthreads();                              // every warp is done with this stage
@@ -383,6 +384,352 @@ k4_search(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMa
             g_m1 = gv;
         });
     reduce_and_finish<2 * K>(acc, R, [&](double* tt) { fin_search(tt, K, h0, base, mu, S); });
+}
+
+
+
+
+// ============================================================================
+// g-free GP / search sweeps (k5_*).  The gradient g = A y - b is never stored:
+// every sweep recomputes it from y at the rows and columns it needs, with the
+// arithmetic of the accept sweep that used to store it (op.apply(...) - b, so
+// the values are bitwise those of the stored-g kernels).  A GP step then
+// streams y (search) and y + masks (accept): 26 instead of 50 B per point.
+// The accept sweep of a GP step applies the operator three times (g of y, then
+// A yn, then A d), so the warps keep 26 output lanes with 3 halo lanes per
+// side; f64 boxes start at the even column x0 - 4 (16-byte aligned): lane L of
+// warp w <-> box column 26 w + L + 1 <-> grid column x0 - 3 + 26 w + L.
+// MODE: GP (direction -g, base alpha_0), CG (direction w, base 1), PROJ (no
+// direction: y_out = P[y]).
+// ============================================================================
+namespace m5 {
+constexpr int kOut = 26 * m4::kWarps;        // 104 output columns per band
+constexpr int kBW = 112;                     // f64 box columns (x0 - 4 .. x0 + 107)
+constexpr int kMW = 128;                     // u8 mask box width (start floored to 16 B)
+constexpr int kF = m4::kBR * kBW * 8;        // 3584 B
+constexpr int kUt = m4::kBR * kMW;           // 512 B
+static_assert(kF % 128 == 0 && kUt % 128 == 0, "TMA destinations stay 128-byte aligned");
+enum Mode : int { GP = 0, CG = 1, PROJ = 2 };
+}  // namespace m5
+
+// Stage: y | w (CG) | b (!BB) | l | u (!SB) | mask_prev
+template <bool SB, bool BB, int MODE>
+struct AccLayout5 {
+    static constexpr int kY = 0;
+    static constexpr int kD = m5::kF;
+    static constexpr int kB = kD + (MODE == m5::CG ? m5::kF : 0);
+    static constexpr int kL = kB + (BB ? 0 : m5::kF);
+    static constexpr int kU = kL + (SB ? 0 : m5::kF);
+    static constexpr int kMP = kU + (SB ? 0 : m5::kF);
+    static constexpr int kStage = kMP + m5::kUt;
+    static constexpr int kNST = 4;
+    static constexpr int kSmem = kNST * kStage + 64;
+    static constexpr int kLag = MODE == m5::GP ? 3 : 2;     // emitted row = raw row - kLag
+};
+
+// a1 + a2, g-free.  Per raw row r: (GP) g(r-1) = (A y)(r-1) - b, yn(r-1) = P[y - alpha g];
+// (CG) yn(r) = P[y + alpha w]; (PROJ) yn(r) = P[y].  With ry the yn row: gn(ry-1) = A yn - b,
+// d(ry-1) = grad_Omega q(yn); emit ry-2 with (A d)(ry-2).  y_out, mask_out, the six sums.
+template <bool SB, bool BB, int MODE>
+__global__ void __launch_bounds__(m4::kThreads, 4)
+k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
+          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
+          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
+          const __grid_constant__ CUtensorMap m_mp, int has_mp, double* __restrict__ y_out,
+          unsigned char* __restrict__ mask_out, Scal* S, RedScratch R, int gp) {
+    using namespace m4;
+    using L = AccLayout5<SB, BB, MODE>;
+    constexpr int LAG = L::kLag;
+    if (gp && *(volatile int*)&S->gp_done) return;
+    double alpha = 0.0;
+    if (MODE != m5::PROJ) {
+        if (S->s_h < 0) return;                   // uniform: no accepted step in this batch
+        alpha = S->s_alpha;
+    }
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 26 * wid + lane + 1;            // box column
+    const bool out_lane = lane >= 3 && lane < 29;
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int gx = 0, moff = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double bcol = 0.0;
+    double y_m1 = 0.0, y_m2 = 0.0, l_r1 = 0.0, u_r1 = 0.0, b_r1 = 0.0;   // GP: raw rows r-1, r-2
+    double yn_a = 0.0, yn_b = 0.0;                // yn(ry-1), yn(ry-2)
+    double l_a = 0.0, u_a = 0.0, b_a = 0.0;       // bounds / b of row ry-1
+    double d_a = 0.0, d_b = 0.0;                  // d(ry-2), d(ry-3)
+    double yn_e = 0.0, gn_e = 0.0, l_e = 0.0, u_e = 0.0;   // row ry-2 (emitted)
+    const uint32_t tx = L::kMP + (has_mp ? m5::kUt : 0);
+    band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, tx);
+            const int yt = yr - G.rlo;
+            tma_load_2d(st + L::kY, &m_y, x0 - 4, yt, bar);
+            if (MODE == m5::CG) tma_load_2d(st + L::kD, &m_dir, x0 - 4, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, &m_b, x0 - 4, yt, bar);
+            if (!SB) {
+                tma_load_2d(st + L::kL, &m_l, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kU, &m_u, x0 - 4, yt, bar);
+            }
+            if (has_mp) tma_load_2d(st + L::kMP, &m_mp, floor16(x0 - 4), yt - LAG, bar);
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 3 + 26 * wid + lane;
+            moff = (x0 - 4) - floor16(x0 - 4);
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
+            y_m1 = y_m2 = l_r1 = u_r1 = b_r1 = yn_a = yn_b = l_a = u_a = b_a = d_a = d_b = 0.0;
+            yn_e = gn_e = l_e = u_e = 0.0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const int q = kk * m5::kBW + c;
+            const bool rin = r >= A.rlo && r < A.rhi;
+            const bool in = col_ok && rin;
+            const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
+            const double bv = BB ? (rin ? bcol : 0.0) : reinterpret_cast<const double*>(st + L::kB)[q];
+            const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
+            const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
+            double yn, ln, un, bn;                // the new iterate and its row data, row ry
+            int ry;
+            if constexpr (MODE == m5::GP) {
+                ry = r - 1;
+                const double g1 = op.apply(A, r - 1, y_m1, y_m2, yv) - b_r1;   // g(r-1)
+                yn = trial(y_m1, g1, -1.0, alpha, l_r1, u_r1);
+                ln = l_r1; un = u_r1; bn = b_r1;
+                y_m2 = y_m1; y_m1 = yv;
+                l_r1 = lv; u_r1 = uv; b_r1 = bv;
+            } else {
+                ry = r;
+                if constexpr (MODE == m5::CG)
+                    yn = trial(yv, reinterpret_cast<const double*>(st + L::kD)[q], 1.0, alpha, lv, uv);
+                else
+                    yn = mid(lv, uv, yv);
+                ln = lv; un = uv; bn = bv;
+            }
+            const double gn1 = op.apply(A, ry - 1, yn_a, yn_b, yn) - b_a;        // gn(ry-1)
+            const double d1 = pgrad(yn_a, gn1, l_a, u_a);                       // d(ry-1)
+            const double ad = op.apply(A, ry - 2, d_a, d_b, d1);                // (A d)(ry-2)
+            const int re = ry - 2;
+            if (out_lane && col_ok && re >= y0 && re < y1) {
+                const long long v = (long long)gx + (long long)A.pitch * re;
+                y_out[v] = yn_e;
+                const bool act = (yn_e == l_e) || (yn_e == u_e);
+                const unsigned char m = act ? 0 : 1;
+                mask_out[v] = m;
+                acc[0] = fma(d_a, d_a, acc[0]);
+                acc[1] = fma(gn_e, gn_e, acc[1]);
+                acc[2] += act ? 1.0 : 0.0;
+                if (has_mp) acc[3] += (st[L::kMP + kk * m5::kMW + c + moff] != m) ? 1.0 : 0.0;
+                const bool binding = (yn_e == l_e && gn_e >= 0.0) || (yn_e == u_e && gn_e <= 0.0);
+                acc[4] += (act && !binding) ? 1.0 : 0.0;
+                acc[5] = fma(d_a, ad, acc[5]);
+            }
+            yn_e = yn_a; gn_e = gn1; l_e = l_a; u_e = u_a;
+            d_b = d_a; d_a = d1;
+            yn_b = yn_a; yn_a = yn;
+            l_a = ln; u_a = un; b_a = bn;
+        });
+    reduce_and_finish<6>(acc, R, [&](double* t) { fin_accept(t, true, S); });
+}
+
+// a3, g-free: K step sizes.  GP: g(r-1) from y, s_h(r-1) = P[y - alpha_h g] - y; CG: s_h(r) =
+// P[y + alpha_h w] - y, g(r-1) from y.  Emit <g, s_h>, <s_h, A s_h> one row behind the s row.
+template <bool SB, bool BB, int MODE, int K>
+struct SrchLayout5 {
+    static constexpr int kY = 0;
+    static constexpr int kD = m5::kF;
+    static constexpr int kB = kD + (MODE == m5::CG ? m5::kF : 0);
+    static constexpr int kL = kB + (BB ? 0 : m5::kF);
+    static constexpr int kU = kL + (SB ? 0 : m5::kF);
+    static constexpr int kStage = kU + (SB ? 0 : m5::kF);
+    static constexpr int kNST = 4;
+    static constexpr int kSmem = kNST * kStage + 64;
+};
+
+template <bool SB, bool BB, int MODE, int K>
+__global__ void __launch_bounds__(m4::kThreads, (K <= 2 ? 4 : 2))
+k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
+          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
+          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, int h0, double mu,
+          Scal* S, RedScratch R, int gp) {
+    using namespace m4;
+    using L = SrchLayout5<SB, BB, MODE, K>;
+    constexpr bool use_alpha0 = MODE == m5::GP;
+    if (gp && *(volatile int*)&S->gp_done) return;
+    if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
+        if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
+        return;
+    }
+    const double base = use_alpha0 ? S->alpha0 : 1.0;
+    double al[K];
+#pragma unroll
+    for (int h = 0; h < K; ++h) al[h] = scalbn(base, -(h0 + h));
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 26 * wid + lane + 1;
+    const bool out_lane = lane >= 3 && lane < 29;
+    double acc[2 * K];
+#pragma unroll
+    for (int s = 0; s < 2 * K; ++s) acc[s] = 0.0;
+    int gx = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double bcol = 0.0;
+    double y_m1 = 0.0, y_m2 = 0.0, l_r1 = 0.0, u_r1 = 0.0, b_r1 = 0.0;
+    double g_e = 0.0;                             // g of the emitted row
+    double s_a[K], s_b[K];                        // s_h at the s row - 1, - 2
+#pragma unroll
+    for (int h = 0; h < K; ++h) { s_a[h] = 0.0; s_b[h] = 0.0; }
+    band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, L::kStage);
+            const int yt = yr - G.rlo;
+            tma_load_2d(st + L::kY, &m_y, x0 - 4, yt, bar);
+            if (MODE == m5::CG) tma_load_2d(st + L::kD, &m_dir, x0 - 4, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, &m_b, x0 - 4, yt, bar);
+            if (!SB) {
+                tma_load_2d(st + L::kL, &m_l, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kU, &m_u, x0 - 4, yt, bar);
+            }
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 3 + 26 * wid + lane;
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
+            y_m1 = y_m2 = l_r1 = u_r1 = b_r1 = g_e = 0.0;
+#pragma unroll
+            for (int h = 0; h < K; ++h) { s_a[h] = 0.0; s_b[h] = 0.0; }
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const int q = kk * m5::kBW + c;
+            const bool rin = r >= A.rlo && r < A.rhi;
+            const bool in = col_ok && rin;
+            const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
+            const double bv = BB ? (rin ? bcol : 0.0) : reinterpret_cast<const double*>(st + L::kB)[q];
+            const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
+            const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
+            const double g1 = op.apply(A, r - 1, y_m1, y_m2, yv) - b_r1;     // g(r-1)
+            double sn[K];                         // s_h at the s row rs
+            int rs;
+            if constexpr (MODE == m5::GP) {
+                rs = r - 1;
+#pragma unroll
+                for (int h = 0; h < K; ++h) sn[h] = trial(y_m1, g1, -1.0, al[h], l_r1, u_r1) - y_m1;
+            } else {
+                rs = r;
+                const double dv = reinterpret_cast<const double*>(st + L::kD)[q];
+#pragma unroll
+                for (int h = 0; h < K; ++h) sn[h] = trial(yv, dv, 1.0, al[h], lv, uv) - yv;
+            }
+            // emit row rs-1: <g, s_h>, <s_h, A s_h>;  g(rs-1) is g1 (CG) or the previous g1 (GP)
+            const int re = rs - 1;
+            const double ge = (MODE == m5::GP) ? g_e : g1;
+            const bool emit = out_lane && col_ok && re >= y0 && re < y1;
+#pragma unroll
+            for (int h = 0; h < K; ++h) {
+                const double as = op.apply(A, re, s_a[h], s_b[h], sn[h]);
+                if (emit) {
+                    acc[2 * h] = fma(ge, s_a[h], acc[2 * h]);
+                    acc[2 * h + 1] = fma(s_a[h], as, acc[2 * h + 1]);
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < K; ++h) { s_b[h] = s_a[h]; s_a[h] = sn[h]; }
+            g_e = g1;
+            y_m2 = y_m1; y_m1 = yv;
+            l_r1 = lv; u_r1 = uv; b_r1 = bv;
+        });
+    reduce_and_finish<2 * K>(acc, R, [&](double* tt) { fin_search(tt, K, h0, base, mu, S); });
+}
+
+// a5 init, g-free: rho_0 = -[v in F] (A y - b)_v, u_0 = rho_0 (/ A_vv with PC); q_0 = A_F u_0;
+// gamma_0 = rho_0'u_0, delta_0 = u_0'q_0.  Writes rho, p = 0, w = 0 and the CG mask copy.
+// Stage: y | b (!BB) | mask
+template <bool BB>
+struct CgInitLayout5 {
+    static constexpr int kY = 0;
+    static constexpr int kB = m5::kF;
+    static constexpr int kM = kB + (BB ? 0 : m5::kF);
+    static constexpr int kStage = kM + m5::kUt;
+    static constexpr int kNST = 4;
+    static constexpr int kSmem = kNST * kStage + 64;
+};
+
+template <bool BB, bool PC>
+__global__ void __launch_bounds__(m4::kThreads, 4)
+k5_cg_init(StencilOp A, BandGeom G, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
+           const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_mask,
+           unsigned char* __restrict__ mask_cg, double* __restrict__ rho, double* __restrict__ p,
+           double* __restrict__ w, double eta2, long long cap, Scal* S, RedScratch R) {
+    using namespace m4;
+    using L = CgInitLayout5<BB>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 26 * wid + lane + 1;
+    const bool out_lane = lane >= 3 && lane < 29;
+    double acc[2] = {0.0, 0.0};
+    int gx = 0, moff = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double bcol = 0.0, dinv = 0.0;
+    double y_m1 = 0.0, y_m2 = 0.0, b_r1 = 0.0;
+    unsigned char m_r1 = 0, m_a = 0;
+    double u_a = 0.0, u_b = 0.0, rho_a = 0.0;     // u at rows r-2, r-3; rho at r-2
+    const uint32_t tx = L::kM + m5::kUt;
+    band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, tx);
+            const int yt = yr - G.rlo;
+            tma_load_2d(st + L::kY, &m_y, x0 - 4, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, &m_b, x0 - 4, yt, bar);
+            tma_load_2d(st + L::kM, &m_mask, floor16(x0 - 4), yt, bar);
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 3 + 26 * wid + lane;
+            moff = (x0 - 4) - floor16(x0 - 4);
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            dinv = op.dinv(A, 0);
+            if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
+            y_m1 = y_m2 = b_r1 = u_a = u_b = rho_a = 0.0;
+            m_r1 = m_a = 0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const int q = kk * m5::kBW + c;
+            const bool rin = r >= A.rlo && r < A.rhi;
+            const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
+            const double bv = BB ? (rin ? bcol : 0.0) : reinterpret_cast<const double*>(st + L::kB)[q];
+            const unsigned char mv = st[L::kM + kk * m5::kMW + c + moff];
+            const double g1 = op.apply(A, r - 1, y_m1, y_m2, yv) - b_r1;     // g(r-1)
+            const double rho1 = m_r1 ? -g1 : 0.0;                            // rho_0(r-1)
+            const double u1 = PC ? rho1 * dinv : rho1;
+            const double qv = op.apply(A, r - 2, u_a, u_b, u1);              // (A_F u_0)(r-2) on F
+            const int re = r - 2;
+            if (out_lane && col_ok && re >= y0 && re < y1) {
+                const long long v = (long long)gx + (long long)A.pitch * re;
+                mask_cg[v] = m_a;
+                rho[v] = rho_a;
+                p[v] = 0.0;
+                w[v] = 0.0;
+                acc[0] = fma(rho_a, u_a, acc[0]);
+                acc[1] = m_a ? fma(u_a, qv, acc[1]) : acc[1];
+            }
+            u_b = u_a; u_a = u1; rho_a = rho1; m_a = m_r1;
+            y_m2 = y_m1; y_m1 = yv; b_r1 = bv; m_r1 = mv;
+        });
+    reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
 }
 
 }  // namespace gpcg
