@@ -188,6 +188,27 @@ GPCG_API int gpcg_create_stencil2d_dist(gpcg_problem **out, const gpcg_dist *dis
                                const double *shift, const double *b, const double *l, const double *u, double c);
 
 /*
+ * gpcg_create_stencil3d -- A is the 3-D 7-point face-weight operator on an
+ * nx x ny x nz grid (C4's operator without CSR
+ * storage), the 3-D analogue of gpcg_create_stencil2d: A = sum over faces of
+ * w_f (e_a - e_b)(e_a - e_b)', boundary faces w_f e_a e_a', plus diag(shift).
+ * Point (i, j, k) <-> v = i + nx (j + ny k).  Full face arrays:
+ *   wx[(k ny + j)(nx+1) + i'] joins (i'-1, j, k)-(i', j, k), i' = 0..nx;
+ *   wy[(k (ny+1) + j') nx + i] joins (i, j'-1, k)-(i, j', k), j' = 0..ny;
+ *   wz[k' nx ny + j nx + i]   joins (i, j, k'-1)-(i, j, k'), k' = 0..nz.
+ * shift nullable (n).  b, l, u: n.  Errors as gpcg_create_stencil2d.
+ * gpcg_create_stencil3d_dist: slabs of z-planes (gpcg_dist rows = planes; one
+ * ghost plane per side); wx, wy, b, l, u, shift hold the rank's planes, wz its
+ * face planes row_begin .. row_end inclusive.
+ */
+GPCG_API int gpcg_create_stencil3d(gpcg_problem **out, void *cuda_stream, int64_t nx, int64_t ny, int64_t nz,
+                          const double *wx, const double *wy, const double *wz, const double *shift,
+                          const double *b, const double *l, const double *u, double c);
+GPCG_API int gpcg_create_stencil3d_dist(gpcg_problem **out, const gpcg_dist *dist, void *cuda_stream, int64_t nx,
+                               int64_t ny, int64_t nz, const double *wx, const double *wy, const double *wz,
+                               const double *shift, const double *b, const double *l, const double *u, double c);
+
+/*
  * gpcg_create_csr -- A given in CSR with BOTH triangles stored:
  * row_ptr[n+1] (int64, row_ptr[0] = 0), col[nnz] (int32, sorted within each
  * row, 0 <= col < n), val[nnz] (fp64).  The paper's PETSc "standard

@@ -106,6 +106,50 @@ int ora_stencil2d_to_csr(int64_t nx, int64_t ny, const double *wx, int64_t wx_ld
     return ORA_OK;
 }
 
+/* 3-D 7-point face-weight operator (the 3-D analogue of
+ * the definition above: A = sum over faces of w_f (e_a - e_b)(e_a - e_b)', boundary
+ * faces w_f e_a e_a', plus diag(shift)).  Point (i, j, k) <-> v = i + nx (j + ny k).
+ * wx[(k ny + j)(nx+1) + i'] joins (i'-1, j, k)-(i', j, k), i' = 0..nx;
+ * wy[(k (ny+1) + j') nx + i] joins (i, j'-1, k)-(i, j', k), j' = 0..ny;
+ * wz[k' nx ny + j nx + i] joins (i, j, k'-1)-(i, j, k'), k' = 0..nz.
+ * Columns in increasing order: -z, -y, -x, diag, +x, +y, +z. */
+int64_t ora_stencil3d_nnz(int64_t nx, int64_t ny, int64_t nz)
+{
+    return 7 * nx * ny * nz - 2 * (ny * nz + nx * nz + nx * ny);
+}
+
+int ora_stencil3d_to_csr(int64_t nx, int64_t ny, int64_t nz, const double *wx, const double *wy,
+                         const double *wz, const double *shift, int64_t *rp, int32_t *ci, double *val)
+{
+    if (nx <= 0 || ny <= 0 || nz <= 0) return ORA_EINVAL;
+    int64_t p = 0;
+    rp[0] = 0;
+    for (int64_t k = 0; k < nz; k++) {
+        for (int64_t j = 0; j < ny; j++) {
+            for (int64_t i = 0; i < nx; i++) {
+                int64_t v = i + nx * (j + ny * k);
+                double w_w = wx[(k * ny + j) * (nx + 1) + i];
+                double w_e = wx[(k * ny + j) * (nx + 1) + i + 1];
+                double w_s = wy[(k * (ny + 1) + j) * nx + i];
+                double w_n = wy[(k * (ny + 1) + j + 1) * nx + i];
+                double w_d = wz[k * nx * ny + j * nx + i];
+                double w_u = wz[(k + 1) * nx * ny + j * nx + i];
+                double d = w_w + w_e + w_s + w_n + w_d + w_u;
+                if (shift) d = d + shift[v];
+                if (k > 0)      { ci[p] = (int32_t)(v - nx * ny); val[p] = -w_d; p++; }
+                if (j > 0)      { ci[p] = (int32_t)(v - nx);      val[p] = -w_s; p++; }
+                if (i > 0)      { ci[p] = (int32_t)(v - 1);       val[p] = -w_w; p++; }
+                ci[p] = (int32_t)v; val[p] = d; p++;
+                if (i < nx - 1) { ci[p] = (int32_t)(v + 1);       val[p] = -w_e; p++; }
+                if (j < ny - 1) { ci[p] = (int32_t)(v + nx);      val[p] = -w_n; p++; }
+                if (k < nz - 1) { ci[p] = (int32_t)(v + nx * ny); val[p] = -w_u; p++; }
+                rp[v + 1] = p;
+            }
+        }
+    }
+    return ORA_OK;
+}
+
 /* y = A x  (row-wise left-to-right sums) -- "Mat-Vec Multiply", T3 P:999-1005 */
 void ora_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
               const double *x, double *y)

@@ -64,6 +64,10 @@ def lib():
         L.ora_stencil2d_nnz.argtypes = [i64, i64]
         L.ora_stencil2d_to_csr.restype = C.c_int
         L.ora_stencil2d_to_csr.argtypes = [i64, i64, P, i64, P, i64, P, P, P, P]
+        L.ora_stencil3d_nnz.restype = i64
+        L.ora_stencil3d_nnz.argtypes = [i64, i64, i64]
+        L.ora_stencil3d_to_csr.restype = C.c_int
+        L.ora_stencil3d_to_csr.argtypes = [i64, i64, i64, P, P, P, P, P, P, P]
         L.ora_spmv.restype = None
         L.ora_spmv.argtypes = [i64, P, P, P, P, P]
         L.ora_spmv_masked.restype = None
@@ -134,10 +138,27 @@ def stencil2d_to_csr(nx, ny, wx, wx_ld, wy, wy_ld, shift=None) -> CSR:
     return CSR(n, rp, ci, va)
 
 
+def stencil3d_to_csr(nx, ny, nz, wx, wy, wz, shift=None) -> CSR:
+    L = lib()
+    n = nx * ny * nz
+    nnz = L.ora_stencil3d_nnz(nx, ny, nz)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    ci = np.zeros(nnz, dtype=np.int32)
+    va = np.zeros(nnz, dtype=np.float64)
+    wx = _f64(wx); wy = _f64(wy); wz = _f64(wz)
+    sh = _f64(shift) if shift is not None else None
+    rc = L.ora_stencil3d_to_csr(nx, ny, nz, _p(wx), _p(wy), _p(wz), _p(sh), _p(rp), _p(ci), _p(va))
+    if rc != 0:
+        raise ValueError("ora_stencil3d_to_csr failed")
+    return CSR(n, rp, ci, va)
+
+
 def problem_csr(prob) -> CSR:
     """The oracle's own CSR of a problems.Problem (assembled here for stencils)."""
     if prob.kind == "stencil2d":
         return stencil2d_to_csr(prob.nx, prob.ny, prob.wx, prob.wx_ld, prob.wy, prob.wy_ld, prob.shift)
+    if prob.kind == "stencil3d":
+        return stencil3d_to_csr(prob.nx, prob.ny, prob.nz, prob.wx, prob.wy, prob.wz, prob.shift)
     return CSR(prob.n, np.ascontiguousarray(prob.row_ptr, dtype=np.int64),
                np.ascontiguousarray(prob.col, dtype=np.int32), _f64(prob.val))
 

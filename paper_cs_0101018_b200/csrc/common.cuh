@@ -23,7 +23,7 @@ constexpr int kMaxK = 16;          // projected-search step sizes per sweep
 // point / neighbour iteration
 // ----------------------------------------------------------------------------
 struct Pt {
-    int v, i, j;
+    int v, i, j, k;
 };
 
 // 5-point face-weight operator (gpcg.h, gpcg_create_stencil2d).  ld 0 means a
@@ -55,7 +55,7 @@ struct StencilOp {
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
             const int bj = t / ntx, bi = t - bj * ntx;
             const int i = (bi << 5) + tx, j = (bj << 3) + ty;
-            if (i < nx && j < ny) body(Pt{i + pitch * j, i, j});
+            if (i < nx && j < ny) body(Pt{i + pitch * j, i, j, 0});
         }
     }
 
@@ -91,13 +91,63 @@ struct CsrOp {
     template <class Body>
     __device__ __forceinline__ void for_each_point(Body&& body) const {
         for (int v = blockIdx.x * kThreads + threadIdx.x; v < n; v += gridDim.x * kThreads)
-            body(Pt{v, 0, 0});
+            body(Pt{v, 0, 0, 0});
     }
 
     template <class CB>
     __device__ __forceinline__ void for_each_nbr(const Pt& p, CB&& cb) const {
         const long long e = __ldg(rp + p.v + 1);
         for (long long k = __ldg(rp + p.v); k < e; ++k) cb(__ldg(ci + k), __ldg(val + k));
+    }
+};
+
+// 3-D 7-point face-weight operator (gpcg_create_stencil3d), for the
+// generic kernels.  Point (i, j, k) of the slab at v = i + nx j + plane k (plane = nx ny, no
+// padding); k in [0, nz) owned, [klo, khi) readable (ghost planes of a slab), outside: zero.
+// wx: (nx+1) per (j, k) line; wy: nx per face line, ny+1 face lines per plane; wz: one plane
+// of nx ny per face plane (face plane k joins planes k-1, k).
+struct Stencil3Op {
+    int nx, ny, nz;
+    long long plane;
+    const double* __restrict__ wx;
+    const double* __restrict__ wy;
+    const double* __restrict__ wz;
+    const double* __restrict__ shift;
+    int klo, khi;
+
+    __device__ __forceinline__ int num_units() const {
+        return (int)((plane * nz + kThreads - 1) / kThreads);
+    }
+
+    template <class Body>
+    __device__ __forceinline__ void for_each_point(Body&& body) const {
+        const int n = (int)(plane * nz);
+        for (int v = blockIdx.x * kThreads + threadIdx.x; v < n; v += gridDim.x * kThreads) {
+            const int k = v / (int)plane, r = v - k * (int)plane;
+            const int j = r / nx, i = r - j * nx;
+            body(Pt{v, i, j, k});
+        }
+    }
+
+    template <class CB>
+    __device__ __forceinline__ void for_each_nbr(const Pt& p, CB&& cb) const {
+        const long long line = (long long)p.k * ny + p.j;
+        const double ww = __ldg(wx + line * (nx + 1) + p.i);
+        const double we = __ldg(wx + line * (nx + 1) + p.i + 1);
+        const double ws = __ldg(wy + ((long long)p.k * (ny + 1) + p.j) * nx + p.i);
+        const double wn = __ldg(wy + ((long long)p.k * (ny + 1) + p.j + 1) * nx + p.i);
+        const long long ip = (long long)p.j * nx + p.i;
+        const double wd = __ldg(wz + (long long)p.k * plane + ip);
+        const double wu = __ldg(wz + (long long)(p.k + 1) * plane + ip);
+        double d = ((ww + we) + (ws + wn)) + (wd + wu);
+        if (shift) d += __ldg(shift + p.v);
+        cb(p.v, d);
+        if (p.i > 0) cb(p.v - 1, -ww);
+        if (p.i < nx - 1) cb(p.v + 1, -we);
+        if (p.j > 0) cb(p.v - nx, -ws);
+        if (p.j < ny - 1) cb(p.v + nx, -wn);
+        if (p.k - 1 >= klo) cb(p.v - (int)plane, -wd);
+        if (p.k + 1 < khi) cb(p.v + (int)plane, -wu);
     }
 };
 

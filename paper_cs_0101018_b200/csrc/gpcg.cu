@@ -170,6 +170,7 @@ struct Slab {
     double* val = nullptr;
     StencilOp sop{};
     CsrOp cop{};
+    Stencil3Op s3op{};
     double* partials = nullptr;
     unsigned int* counter = nullptr;
     MarchGeom mg1{}, mg2{};
@@ -201,6 +202,8 @@ struct gpcg_problem {
     cudaStream_t st = nullptr;      // private work stream (capturable)
     cudaEvent_t ev_sync = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c0 = nullptr, ev_c1 = nullptr;
     bool is_csr = false;
+    bool is3d = false;              // 3-D 7-point stencil (generic kernels; rows = z-planes)
+    int rowlen = 1;                 // elements of one user row: 2-D nx, 3-D nx*ny, CSR 1
     bool generic = false;           // GPCG_GENERIC=1: stencil problems use the flat generic kernels (A/B tests)
     bool sb = false;                // scalar (constant) bounds
     bool bc = false;                // stencil with broadcast faces and no shift
@@ -365,6 +368,22 @@ int exchange_arrays(gpcg_problem* h, const RowArray* arr, int na) {
 
 bool has_ghosts(const gpcg_problem* h) { return h->nslabs() > 1 || h->nranks > 1; }
 
+// 2-D stencil with its specialised sweeps (march / tile kernels); otherwise the generic kernels
+bool spec2d(const gpcg_problem* h) { return !h->is_csr && !h->is3d && !h->generic; }
+
+// f(op) with the slab's operator policy (generic kernels)
+template <class F>
+void with_gop(const gpcg_problem* h, Slab& S, F&& f) {
+    if (h->is_csr) f(S.cop);
+    else if (h->is3d) f(S.s3op);
+    else f(S.sop);
+}
+template <class F>
+void with_gop_sb(const gpcg_problem* h, Slab& S, F&& f) {
+    if (h->sb) with_gop(h, S, [&](auto& op) { f(op, std::true_type()); });
+    else with_gop(h, S, [&](auto& op) { f(op, std::false_type()); });
+}
+
 int exchange(gpcg_problem* h, std::initializer_list<int> vecs, std::initializer_list<int> msks = {}) {
     if (!has_ghosts(h)) return GPCG_OK;
     RowArray arr[8];
@@ -386,7 +405,7 @@ int copy_kind(const void* p, bool to_device) {
 // the rank's contiguous user vector (n_local entries) -> vector id of every slab (owned rows)
 int upload_vec(gpcg_problem* h, int id, const double* src) {
     const cudaMemcpyKind k = (cudaMemcpyKind)copy_kind(src, true);
-    const size_t cols = h->is_csr ? 1 : (size_t)h->nx;
+    const size_t cols = (size_t)h->rowlen;
     for (Slab& S : h->slabs)
         CK(cudaMemcpy2DAsync(S.v[id], (size_t)h->pitch * sizeof(double), src + (long long)S.uoff * cols,
                              cols * sizeof(double), cols * sizeof(double), S.rows, k, h->st));
@@ -394,7 +413,7 @@ int upload_vec(gpcg_problem* h, int id, const double* src) {
 }
 int download_vec(gpcg_problem* h, double* dst, int id) {
     const cudaMemcpyKind k = (cudaMemcpyKind)copy_kind(dst, false);
-    const size_t cols = h->is_csr ? 1 : (size_t)h->nx;
+    const size_t cols = (size_t)h->rowlen;
     for (Slab& S : h->slabs)
         CK(cudaMemcpy2DAsync(dst + (long long)S.uoff * cols, cols * sizeof(double), S.v[id],
                              (size_t)h->pitch * sizeof(double), cols * sizeof(double), S.rows, k, h->st));
@@ -652,7 +671,7 @@ int create_vectors(gpcg_problem* h, const double* b, const double* l, const doub
         // partial sums of the largest grid any kernel of this slab uses (grid-stride generic kernels
         // are capped at 16 blocks/SM; march grids are one warp per item)
         long long gmax = (long long)h->sms * 16;
-        if (!h->is_csr) {
+        if (!h->is_csr && !h->is3d) {
             S.mg1 = march_geom(h->nx, S.rows, 1);
             S.mg2 = march_geom(h->nx, S.rows, 2);
             S.grid_m1 = march_grid(S.mg1);
@@ -681,8 +700,8 @@ int create_vectors(gpcg_problem* h, const double* b, const double* l, const doub
     if (h->nranks > 1) NK(nccl_api()->Broadcast(h->lu0, h->lu0, 2, ncclDouble, 0, h->comm, h->st));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        const int cols = h->is_csr ? S.rows : h->nx, rows = h->is_csr ? 1 : S.rows;
-        const int g = std::max(1, (int)std::min<long long>(((long long)S.rows * (h->is_csr ? 1 : h->nx) + kThreads - 1) / kThreads,
+        const int cols = h->is_csr ? S.rows : h->rowlen, rows = h->is_csr ? 1 : S.rows;
+        const int g = std::max(1, (int)std::min<long long>(((long long)S.rows * h->rowlen + kThreads - 1) / kThreads,
                                                            (long long)h->sms * 4));
         k_check_inputs<<<g, kThreads, 0, h->st>>>(cols, rows, h->is_csr ? S.rows : h->pitch, S.v[VB], S.v[VL], S.v[VU],
                                                   h->lu0, h->dS, h->red(s));
@@ -798,7 +817,7 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
                 k3_accept<false><<<S.grid_t_acc, kTileThreads, AccStage<false>::kSmem, h->st>>>(
                     S.sop, S.tg, B, S.tm[y_in], md, S.tm[VB], S.tm[VL], S.tm[VU], mp, dir >= 0 ? 1 : 0, sgn,
                     mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
-        } else if (!h->is_csr && !h->generic) {   // accept + regrad + mask + counts + next Cauchy step, one sweep
+        } else if (spec2d(h)) {   // accept + regrad + mask + counts + next Cauchy step, one sweep
             const double* dp = dir >= 0 ? S.v[dir] : nullptr;
             const unsigned char* mp = mask_prev >= 0 ? S.m[mask_prev] : nullptr;
             auto go = [&](auto sbt, auto bct) {
@@ -812,19 +831,17 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
         } else {
             const double* dp = dir >= 0 ? S.v[dir] : nullptr;
             const unsigned char* mp = mask_prev >= 0 ? S.m[mask_prev] : nullptr;
-            auto go = [&](auto& op, auto sbt) {
+            with_gop_sb(h, S, [&](auto& op, auto sbt) {
                 using Op = std::decay_t<decltype(op)>;
                 constexpr bool SB = decltype(sbt)::value;
                 k_accept<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y_in], dp, sgn, S.v[VB], mp, S.v[y_out],
                                                                 S.v[g_out], S.m[m_out], h->dS, R, gp);
-            };
-            if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
-            else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+            });
         }
         h->launches++;
         CKLAUNCH();
     }
-    FinArgs a = fin((h->is_csr || h->generic) && !use_tile ? FIN_ACCEPT5 : FIN_ACCEPT);
+    FinArgs a = fin(spec2d(h) ? FIN_ACCEPT : FIN_ACCEPT5);
     a.has_dir = dir >= 0 ? 1 : 0;
     a.gp = gp;
     RC(finish_reduce(h, a, a.kind == FIN_ACCEPT ? 6 : 5));
@@ -832,20 +849,18 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
     return exchange(h, {y_out, g_out}, {m_out});
 }
 
-bool fused_cauchy(const gpcg_problem* h) { return !h->is_csr && !h->generic; }
+bool fused_cauchy(const gpcg_problem* h) { return spec2d(h); }
 
 int launch_cauchy(gpcg_problem* h, int y, int g, int gp = 0) {
     if (fused_cauchy(h)) return GPCG_OK;     // computed by the preceding accept sweep
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
-        auto go = [&](auto& op, auto sbt) {
+        with_gop_sb(h, S, [&](auto& op, auto sbt) {
             using Op = std::decay_t<decltype(op)>;
             constexpr bool SB = decltype(sbt)::value;
             k_cauchy<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], h->dS, h->red(s), gp);
-        };
-        if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
-        else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+        });
         h->launches++;
         CKLAUNCH();
     }
@@ -905,7 +920,7 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
             };
             if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
-        } else if (!h->is_csr && !h->generic) {
+        } else if (spec2d(h)) {
             auto go = [&](auto sbt, auto bct, auto kt, auto dgt) {
                 constexpr bool SB = decltype(sbt)::value, BC = decltype(bct)::value, DG = decltype(dgt)::value;
                 constexpr int KK = decltype(kt)::value;
@@ -924,7 +939,7 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
             };
             if (h->sb) bybc(std::true_type()); else bybc(std::false_type());
         } else {
-            auto go = [&](auto& op, auto sbt) {
+            with_gop_sb(h, S, [&](auto& op, auto sbt) {
                 using Op = std::decay_t<decltype(op)>;
                 constexpr bool SB = decltype(sbt)::value;
                 if (K == 2)
@@ -933,9 +948,7 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
                 else
                     k_search<Op, SB, 8><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[y], S.v[g], S.v[dir], sgn, use_alpha0,
                                                                         h0, mu, h->dS, R, gp);
-            };
-            if (h->is_csr) { if (h->sb) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
-            else { if (h->sb) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+            });
         }
         h->launches++;
         CKLAUNCH();
@@ -994,7 +1007,7 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
             k3_cg_iter<2><<<S.grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
                 S.sop, S.tg, S.tm[vrho(a)], S.tm[vq(a)], S.tmWc, S.tmm[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
                 h->dS, R);
-        } else if (!h->is_csr && !h->generic) {   // stencil: rho, p ping-pong (p in Q[]), w in place
+        } else if (spec2d(h)) {   // stencil: rho, p ping-pong (p in Q[]), w in place
             auto go = [&](auto bct, auto pct) {
                 constexpr bool BC = decltype(bct)::value, PC = decltype(pct)::value;
                 k2_cg_iter<BC, PC><<<S.grid_m2, kMarchThreads, 0, h->st>>>(S.sop, S.mg2, S.m[MKCG], S.v[vrho(a)],
@@ -1004,20 +1017,21 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
             if (h->bc) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
         } else {
-            auto go = [&](auto& op, auto pct) {
+            with_gop(h, S, [&](auto& op) {
                 using Op = std::decay_t<decltype(op)>;
-                constexpr bool PC = decltype(pct)::value;
-                k_cg_iter<Op, PC><<<S.grid, kThreads, 0, h->st>>>(op, S.m[MKCG], S.v[vrho(a)], S.v[vq(a)], S.v[vs(a)],
-                                                                  S.v[vrho(bb)], S.v[vq(bb)], S.v[vs(bb)], S.v[VP],
-                                                                  S.v[VW], S.v[VD], h->dS, R);
-            };
-            if (h->is_csr) { if (pc) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
-            else { if (pc) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+                auto go = [&](auto pct) {
+                    constexpr bool PC = decltype(pct)::value;
+                    k_cg_iter<Op, PC><<<S.grid, kThreads, 0, h->st>>>(op, S.m[MKCG], S.v[vrho(a)], S.v[vq(a)],
+                                                                      S.v[vs(a)], S.v[vrho(bb)], S.v[vq(bb)],
+                                                                      S.v[vs(bb)], S.v[VP], S.v[VW], S.v[VD], h->dS, R);
+                };
+                if (pc) go(std::true_type()); else go(std::false_type());
+            });
         }
         h->launches++;
         CKLAUNCH();
     }
-    if (h->is_csr || h->generic) RC(exchange(h, {vrho(bb), vq(bb), vs(bb)}));
+    if (!spec2d(h)) RC(exchange(h, {vrho(bb), vq(bb), vs(bb)}));
     else RC(exchange(h, {vrho(bb), vq(bb)}));
     return finish_reduce(h, fin(FIN_CG_ITER), 2);
 }
@@ -1111,7 +1125,7 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
             };
             if (h->bb) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
-        } else if (!h->is_csr && !h->generic) {
+        } else if (spec2d(h)) {
             auto go = [&](auto bct, auto pct) {
                 constexpr bool BC = decltype(bct)::value, PC = decltype(pct)::value;
                 k2_cg_init<BC, PC><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.v[vg(cur)], S.m[cur],
@@ -1121,15 +1135,17 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
             if (h->bc) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
         } else {
-            auto go = [&](auto& op, auto pct) {
+            with_gop(h, S, [&](auto& op) {
                 using Op = std::decay_t<decltype(op)>;
-                constexpr bool PC = decltype(pct)::value;
-                k_cg_init<Op, PC><<<S.grid, kThreads, 0, h->st>>>(op, S.v[vg(cur)], S.m[cur], S.m[MKCG], S.v[VRHO0],
-                                                                  S.v[VQ0], S.v[VS0], S.v[VRHO1], S.v[VQ1], S.v[VS1],
-                                                                  S.v[VP], S.v[VW], S.v[VD], eta2, cap, h->dS, R);
-            };
-            if (h->is_csr) { if (pc) go(S.cop, std::true_type()); else go(S.cop, std::false_type()); }
-            else { if (pc) go(S.sop, std::true_type()); else go(S.sop, std::false_type()); }
+                auto go = [&](auto pct) {
+                    constexpr bool PC = decltype(pct)::value;
+                    k_cg_init<Op, PC><<<S.grid, kThreads, 0, h->st>>>(op, S.v[vg(cur)], S.m[cur], S.m[MKCG],
+                                                                      S.v[VRHO0], S.v[VQ0], S.v[VS0], S.v[VRHO1],
+                                                                      S.v[VQ1], S.v[VS1], S.v[VP], S.v[VW], S.v[VD],
+                                                                      eta2, cap, h->dS, R);
+                };
+                if (pc) go(std::true_type()); else go(std::false_type());
+            });
         }
         h->launches++;
         CKLAUNCH();
@@ -1138,7 +1154,7 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     a.eta2 = eta2;
     a.cap = cap;
     RC(finish_reduce(h, a, 2));
-    if (h->is_csr || h->generic) RC(exchange(h, {VRHO0, VQ0, VS0}, {MKCG}));
+    if (!spec2d(h)) RC(exchange(h, {VRHO0, VQ0, VS0}, {MKCG}));
     else RC(exchange(h, {VRHO0, VQ0}, {MKCG}));
     const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
     RC(build_cg_graph(h, chunk));
@@ -1167,10 +1183,10 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
 int launch_objective(gpcg_problem* h, int x) {
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        if (h->is_csr)
-            k_objective<CsrOp><<<S.grid, kThreads, 0, h->st>>>(S.cop, S.v[x], S.v[VB], h->dS, h->red(s));
-        else
-            k_objective<StencilOp><<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[x], S.v[VB], h->dS, h->red(s));
+        with_gop(h, S, [&](auto& op) {
+            using Op = std::decay_t<decltype(op)>;
+            k_objective<Op><<<S.grid, kThreads, 0, h->st>>>(op, S.v[x], S.v[VB], h->dS, h->red(s));
+        });
         h->launches++;
         CKLAUNCH();
     }
@@ -1203,8 +1219,10 @@ int detect_b_rows(gpcg_problem* h) {
 // 1 / diag(A) of every slab (+ ghosts): the point-Jacobi preconditioner
 int setup_jacobi(gpcg_problem* h) {
     for (Slab& S : h->slabs) {
-        if (h->is_csr) k_jacobi_inverse<CsrOp><<<S.grid, kThreads, 0, h->st>>>(S.cop, S.v[VD]);
-        else k_jacobi_inverse<StencilOp><<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[VD]);
+        with_gop(h, S, [&](auto& op) {
+            using Op = std::decay_t<decltype(op)>;
+            k_jacobi_inverse<Op><<<S.grid, kThreads, 0, h->st>>>(op, S.v[VD]);
+        });
         CKLAUNCH();
     }
     return exchange(h, {VD});
@@ -1316,6 +1334,7 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
     auto fail = [&](int r) { free_all(h); return r; };
     h->is_csr = false;
     h->nx = (int)nx;
+    h->rowlen = (int)nx;
     h->pitch = (int)pitch;
     h->wx_ld = wx_ld;
     h->wy_ld = wy_ld;
@@ -1339,6 +1358,117 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
         if (h->bc && !h->generic && h->tile_mask != 0 && (rc = setup_tile(h))) return fail(rc);
     }
     h->nnz = 5 * h->n_global - 2 * nx - 2 * ny;
+    if ((rc = leave(h))) return fail(rc);
+    *out = h;
+    return GPCG_OK;
+}
+
+// ---------------------------------------------------------------- 3-D stencil slabs (z-planes)
+int create_stencil3(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t nx, int64_t ny, int64_t nz,
+                    const double* wx, const double* wy, const double* wz, const double* shift, const double* b,
+                    const double* l, const double* u, double c) {
+    g_err.clear();
+    if (!out) return set_err(GPCG_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (nx <= 0 || ny <= 0 || nz <= 0 || nx * ny * nz >= (1LL << 31))
+        return set_err(GPCG_EINVAL, "grid %lld x %lld x %lld out of range (need 0 < n < 2^31)", (long long)nx,
+                       (long long)ny, (long long)nz);
+    if (!wx || !wy || !wz || !b || !l || !u) return set_err(GPCG_EINVAL, "NULL array argument");
+    if (!std::isfinite(c)) return set_err(GPCG_EINVAL, "c is not finite");
+    long long rb = 0, re = nz;
+    int nsl = 1;
+    if (dist) {
+        if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)
+            return set_err(GPCG_EINVAL, "bad rank %d / nranks %d", dist->rank, dist->nranks);
+        rb = dist->row_begin;
+        re = dist->row_end;
+        nsl = dist->local_slabs > 0 ? dist->local_slabs : 1;
+        if (rb < 0 || re > nz || re <= rb) return set_err(GPCG_EINVAL, "bad plane range [%lld, %lld)", rb, re);
+        if ((dist->rank == 0) != (rb == 0) || (dist->rank == dist->nranks - 1) != (re == nz))
+            return set_err(GPCG_EINVAL, "plane range [%lld, %lld) inconsistent with rank %d of %d", rb, re,
+                           dist->rank, dist->nranks);
+    }
+    const long long plane = nx * ny;
+    if (plane * (re - rb + 2 * nsl + 1) >= (1LL << 31)) return set_err(GPCG_EINVAL, "slab too large");
+    gpcg_problem* h = new gpcg_problem();
+    auto fail = [&](int r) { free_all(h); return r; };
+    h->is3d = true;
+    h->nx = (int)nx;
+    h->rowlen = (int)plane;
+    h->pitch = (int)plane;
+    h->n_global = plane * nz;
+    h->n_local = plane * (re - rb);
+    h->rank_row0 = rb;
+    int rc;
+    if ((rc = create_streams(h, stream))) return fail(rc);
+    if ((rc = setup_comm(h, dist))) return fail(rc);
+    if ((rc = layout_slabs(h, re - rb, nsl, 1))) return fail(rc);
+    if ((rc = create_vectors(h, b, l, u))) return fail(rc);
+    h->c = c;
+    const long long lx = (nx + 1) * ny, ly = nx * (ny + 1), lz = plane;   // elements per (face) plane
+    std::vector<const double*> arrs(h->nslabs());
+    std::vector<long long> cnts(h->nslabs());
+    double bad = 0.0;
+    for (Slab& S : h->slabs) {
+        const long long planes = S.glo + S.rows + S.ghi;
+        double *wxo, *wyo, *wzo, *sho = nullptr;
+        // reuse the 2-D face slots: wxb <- wx, wyb <- wy, brow <- wz
+        if (cudaMalloc(&S.wxb, (size_t)(planes * lx) * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&S.wyb, (size_t)(planes * ly) * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&S.brow, (size_t)((planes + 1) * lz) * sizeof(double)) != cudaSuccess)
+            return fail(set_err(GPCG_ENOMEM, "3-D face arrays"));
+        cudaMemsetAsync(S.wxb, 0, (size_t)(planes * lx) * sizeof(double), h->st);
+        cudaMemsetAsync(S.wyb, 0, (size_t)(planes * ly) * sizeof(double), h->st);
+        cudaMemsetAsync(S.brow, 0, (size_t)((planes + 1) * lz) * sizeof(double), h->st);
+        wxo = S.wxb + S.glo * lx;
+        wyo = S.wyb + S.glo * ly;
+        wzo = S.brow + S.glo * lz;
+        if (cudaMemcpyAsync(wxo, wx + (long long)S.uoff * lx, (size_t)(S.rows * lx) * sizeof(double),
+                            (cudaMemcpyKind)copy_kind(wx, true), h->st) != cudaSuccess ||
+            cudaMemcpyAsync(wyo, wy + (long long)S.uoff * ly, (size_t)(S.rows * ly) * sizeof(double),
+                            (cudaMemcpyKind)copy_kind(wy, true), h->st) != cudaSuccess ||
+            cudaMemcpyAsync(wzo, wz + (long long)S.uoff * lz, (size_t)((S.rows + 1) * lz) * sizeof(double),
+                            (cudaMemcpyKind)copy_kind(wz, true), h->st) != cudaSuccess)
+            return fail(set_err(GPCG_ECUDA, "3-D face upload"));
+        if (shift) {
+            if (cudaMalloc(&S.shb, (size_t)S.nalloc * sizeof(double)) != cudaSuccess)
+                return fail(set_err(GPCG_ENOMEM, "shift"));
+            cudaMemsetAsync(S.shb, 0, (size_t)S.nalloc * sizeof(double), h->st);
+            sho = S.shb + S.glo * plane;
+            if (cudaMemcpyAsync(sho, shift + (long long)S.uoff * plane, (size_t)(S.rows * plane) * sizeof(double),
+                                (cudaMemcpyKind)copy_kind(shift, true), h->st) != cudaSuccess)
+                return fail(set_err(GPCG_ECUDA, "shift upload"));
+        }
+        S.s3op = Stencil3Op{(int)nx, (int)ny, S.rows, plane, wxo, wyo, wzo, sho, -S.glo, S.rows + S.ghi};
+        S.grid = std::max(1, (int)std::min<long long>((plane * S.rows + kThreads - 1) / kThreads, (long long)h->sms * 16));
+    }
+    for (int pass = 0; pass < 4; ++pass) {
+        if (pass == 3 && !shift) break;
+        for (int s = 0; s < h->nslabs(); ++s) {
+            Slab& S = h->slabs[s];
+            const double* a[4] = {S.s3op.wx, S.s3op.wy, S.s3op.wz, S.s3op.shift};
+            const long long n[4] = {S.rows * lx, S.rows * ly, (S.rows + 1) * lz, S.rows * plane};
+            arrs[s] = a[pass];
+            cnts[s] = n[pass];
+        }
+        double t = 0.0;
+        if ((rc = count_nonfinite(h, arrs.data(), cnts.data(), &t))) return fail(rc);
+        bad += t;
+    }
+    if (bad != 0.0) return fail(set_err(GPCG_EINVAL, "%.0f non-finite stencil weights", bad));
+    if (has_ghosts(h)) {
+        auto bx = [](gpcg_problem*, Slab& S, int) { return reinterpret_cast<char*>(const_cast<double*>(S.s3op.wx)); };
+        auto by = [](gpcg_problem*, Slab& S, int) { return reinterpret_cast<char*>(const_cast<double*>(S.s3op.wy)); };
+        auto bz = [](gpcg_problem*, Slab& S, int) { return reinterpret_cast<char*>(const_cast<double*>(S.s3op.wz)); };
+        auto bs = [](gpcg_problem*, Slab& S, int) { return reinterpret_cast<char*>(const_cast<double*>(S.s3op.shift)); };
+        RowArray arr[4] = {RowArray{bx, 0, (size_t)lx, sizeof(double), ncclDouble, 0, 0},
+                           RowArray{by, 0, (size_t)ly, sizeof(double), ncclDouble, 0, 0},
+                           RowArray{bz, 0, (size_t)lz, sizeof(double), ncclDouble, 1, 1},
+                           RowArray{bs, 0, (size_t)plane, sizeof(double), ncclDouble, 0, 0}};
+        if ((rc = exchange_arrays(h, arr, shift ? 4 : 3))) return fail(rc);
+    }
+    if ((rc = setup_jacobi(h))) return fail(rc);
+    h->nnz = 7 * h->n_global - 2 * (ny * nz + nx * nz + nx * ny);
     if ((rc = leave(h))) return fail(rc);
     *out = h;
     return GPCG_OK;
@@ -1397,6 +1527,7 @@ int create_csr(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t 
     auto fail = [&](int r) { free_all(h); return r; };
     h->is_csr = true;
     h->pitch = 1;
+    h->rowlen = 1;
     h->n_global = n_global;
     h->n_local = nloc;
     h->rank_row0 = rb;
@@ -1551,6 +1682,18 @@ int gpcg_create_stencil2d_dist(gpcg_problem** out, const gpcg_dist* dist, void* 
     return create_stencil(out, dist, cuda_stream, nx, ny, wx, wx_ld, wy, wy_ld, shift, b, l, u, c);
 }
 
+int gpcg_create_stencil3d(gpcg_problem** out, void* cuda_stream, int64_t nx, int64_t ny, int64_t nz, const double* wx,
+                          const double* wy, const double* wz, const double* shift, const double* b, const double* l,
+                          const double* u, double c) {
+    return create_stencil3(out, nullptr, cuda_stream, nx, ny, nz, wx, wy, wz, shift, b, l, u, c);
+}
+
+int gpcg_create_stencil3d_dist(gpcg_problem** out, const gpcg_dist* dist, void* cuda_stream, int64_t nx, int64_t ny,
+                               int64_t nz, const double* wx, const double* wy, const double* wz, const double* shift,
+                               const double* b, const double* l, const double* u, double c) {
+    return create_stencil3(out, dist, cuda_stream, nx, ny, nz, wx, wy, wz, shift, b, l, u, c);
+}
+
 int gpcg_create_csr(gpcg_problem** out, void* cuda_stream, int64_t n, const int64_t* row_ptr, const int32_t* col,
                     const double* val, const double* b, const double* l, const double* u, double c) {
     return create_csr(out, nullptr, cuda_stream, n, row_ptr, col, val, b, l, u, c);
@@ -1613,7 +1756,7 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
         return set_err(GPCG_ESTATE, "reduced hessvec needs a free set: call gpcg_project or gpcg_solve first");
     RC(enter(h));
     // direct device access only for one slab with a contiguous layout (CSR, or nx a multiple of 32)
-    const bool direct = h->nslabs() == 1 && !has_ghosts(h) && (h->is_csr || h->pitch == h->nx);
+    const bool direct = h->nslabs() == 1 && !has_ghosts(h) && (h->is_csr || h->pitch == h->rowlen);
     const bool vdev = direct && is_device_ptr(v), ydev = direct && is_device_ptr(y);
     if (!vdev) {
         RC(upload_vec(h, VIN, v));
@@ -1628,7 +1771,7 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
             if (reduced) k_hessvec<Op, true><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
             else k_hessvec<Op, false><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
         };
-        if (h->is_csr) go(S.cop); else go(S.sop);
+        with_gop(h, S, go);
         h->launches++;
         CKLAUNCH();
     }

@@ -21,7 +21,8 @@ STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "ENOMEM", -3: "EC
                 -5: "ENOTSPD", -6: "ESEARCH", -7: "ESTATE"}
 
 # every symbol include/gpcg.h declares (checked by tests/test_abi.py)
-SYMBOLS = ["gpcg_params_default", "gpcg_create_stencil2d", "gpcg_create_stencil2d_dist", "gpcg_create_csr",
+SYMBOLS = ["gpcg_params_default", "gpcg_create_stencil2d", "gpcg_create_stencil2d_dist",
+           "gpcg_create_stencil3d", "gpcg_create_stencil3d_dist", "gpcg_create_csr",
            "gpcg_create_csr_dist", "gpcg_set_params", "gpcg_solve", "gpcg_hessvec", "gpcg_project",
            "gpcg_objective", "gpcg_size", "gpcg_destroy", "gpcg_last_error", "gpcg_partition_rows",
            "gpcg_nccl_unique_id"]
@@ -83,6 +84,11 @@ def load():
     L.gpcg_create_stencil2d_dist.restype = i32
     L.gpcg_create_stencil2d_dist.argtypes = [C.POINTER(P), C.POINTER(Dist), P, i64, i64, P, i64, P, i64, P, P, P,
                                              P, dbl]
+    L.gpcg_create_stencil3d.restype = i32
+    L.gpcg_create_stencil3d.argtypes = [C.POINTER(P), P, i64, i64, i64, P, P, P, P, P, P, P, dbl]
+    L.gpcg_create_stencil3d_dist.restype = i32
+    L.gpcg_create_stencil3d_dist.argtypes = [C.POINTER(P), C.POINTER(Dist), P, i64, i64, i64, P, P, P, P, P, P, P,
+                                             dbl]
     L.gpcg_create_csr_dist.restype = i32
     L.gpcg_create_csr_dist.argtypes = [C.POINTER(P), C.POINTER(Dist), P, i64, P, P, P, P, P, P, dbl]
     L.gpcg_partition_rows.restype = None
@@ -172,8 +178,8 @@ def nccl_unique_id() -> bytes:
 
 
 def problem_rows(prob):
-    """Rows the slab split runs over: grid rows (stencil2d) or matrix rows (CSR)."""
-    return prob.ny if prob.kind == "stencil2d" else prob.n
+    """Rows the slab split runs over: grid rows (stencil2d), z-planes (stencil3d), matrix rows (CSR)."""
+    return {"stencil2d": prob.ny, "stencil3d": prob.nz}.get(prob.kind, prob.n)
 
 
 def local_part(prob, row_begin, row_end):
@@ -196,6 +202,17 @@ def local_part(prob, row_begin, row_end):
         out["wy"] = wy if not prob.wy_ld else np.ascontiguousarray(
             wy[row_begin * prob.wy_ld:row_end * prob.wy_ld + nx])
         out["n"] = (row_end - row_begin) * nx
+    elif prob.kind == "stencil3d":
+        nx, ny = prob.nx, prob.ny
+        pl = nx * ny
+        sl = slice(row_begin * pl, row_end * pl)
+        for k in ("b", "l", "u", "x0"):
+            out[k] = np.ascontiguousarray(np.asarray(getattr(prob, k))[sl])
+        out["shift"] = None if prob.shift is None else np.ascontiguousarray(np.asarray(prob.shift)[sl])
+        out["wx"] = np.ascontiguousarray(np.asarray(prob.wx)[row_begin * (nx + 1) * ny:row_end * (nx + 1) * ny])
+        out["wy"] = np.ascontiguousarray(np.asarray(prob.wy)[row_begin * nx * (ny + 1):row_end * nx * (ny + 1)])
+        out["wz"] = np.ascontiguousarray(np.asarray(prob.wz)[row_begin * pl:(row_end + 1) * pl])   # face planes rb..re
+        out["n"] = (row_end - row_begin) * pl
     else:
         rp = np.asarray(prob.row_ptr, dtype=np.int64)
         k0, k1 = int(rp[row_begin]), int(rp[row_end])
@@ -230,6 +247,20 @@ class Solver:
                                      wy_ld, args[2], args[3], args[4], args[5], float(c))
         _check(rc)
         return cls(h, nx * ny)
+
+    @classmethod
+    def stencil3d(cls, nx, ny, nz, wx, wy, wz, b, l, u, c=0.0, shift=None, stream=None):
+        L = load()
+        h = C.c_void_p()
+        keep = []
+        args = []
+        for a in (wx, wy, wz, shift, b, l, u):
+            p, k = _ptr(a, np.float64)
+            args.append(p)
+            keep.append(k)
+        rc = L.gpcg_create_stencil3d(C.byref(h), _stream_ptr(stream), nx, ny, nz, *args, float(c))
+        _check(rc)
+        return cls(h, nx * ny * nz)
 
     @classmethod
     def csr(cls, n, row_ptr, col, val, b, l, u, c=0.0, stream=None):
@@ -269,6 +300,10 @@ class Solver:
             rc = L.gpcg_create_stencil2d_dist(C.byref(h), C.byref(d), _stream_ptr(stream), prob.nx, prob.ny,
                                               P(loc["wx"]), prob.wx_ld, P(loc["wy"]), prob.wy_ld, P(loc["shift"]),
                                               P(loc["b"]), P(loc["l"]), P(loc["u"]), float(prob.c))
+        elif prob.kind == "stencil3d":
+            rc = L.gpcg_create_stencil3d_dist(C.byref(h), C.byref(d), _stream_ptr(stream), prob.nx, prob.ny,
+                                              prob.nz, P(loc["wx"]), P(loc["wy"]), P(loc["wz"]), P(loc["shift"]),
+                                              P(loc["b"]), P(loc["l"]), P(loc["u"]), float(prob.c))
         else:
             rc = L.gpcg_create_csr_dist(C.byref(h), C.byref(d), _stream_ptr(stream), prob.n,
                                         P(loc["row_ptr"], np.int64), P(loc["col"], np.int32), P(loc["val"]),
@@ -284,6 +319,10 @@ class Solver:
         if slabs > 1:
             return cls.dist(prob, local_slabs=slabs, stream=stream, device=device)[0]
         conv = (lambda a: a) if device is None else _to_device(device)
+        if prob.kind == "stencil3d":
+            return cls.stencil3d(prob.nx, prob.ny, prob.nz, conv(prob.wx), conv(prob.wy), conv(prob.wz),
+                                 conv(prob.b), conv(prob.l), conv(prob.u), prob.c,
+                                 shift=None if prob.shift is None else conv(prob.shift), stream=stream)
         if prob.kind == "stencil2d":
             return cls.stencil2d(prob.nx, prob.ny, conv(prob.wx), prob.wx_ld, conv(prob.wy), prob.wy_ld,
                                  conv(prob.b), conv(prob.l), conv(prob.u), prob.c,

@@ -92,6 +92,8 @@ class Problem:
     # stencil2d
     nx: int = 0
     ny: int = 0
+    nz: int = 0
+    wz: Optional[np.ndarray] = None          # stencil3d z-face weights
     wx: Optional[np.ndarray] = None
     wx_ld: int = 0
     wy: Optional[np.ndarray] = None
@@ -105,7 +107,7 @@ class Problem:
 
     def input_bytes(self) -> int:
         """Bytes of all host arrays a create+solve call uploads (operator, b, l, u, x0)."""
-        arrs = [self.b, self.l, self.u, self.x0, self.wx, self.wy, self.shift,
+        arrs = [self.b, self.l, self.u, self.x0, self.wx, self.wy, self.wz, self.shift,
                 self.row_ptr, self.col, self.val]
         return int(sum(a.nbytes for a in arrs if a is not None))
 
@@ -281,6 +283,25 @@ def c4_family(m: int = 256, seed: int = 4, box: float = 0.01, name: str = "C4") 
                    meta=dict(m=m, seed=seed, family="c4"))
 
 
+def c4_stencil_family(m: int = 256, seed: int = 4, box: float = 0.01, name: str = "C4s") -> Problem:
+    """The C4 problem as a 3-D 7-point face-weight stencil (kind "stencil3d", SURVEY.md
+    8(f) NEXT-2): the same edge weights (streams 11/12/13), b (14) and bounds as
+    c4_family, laid out as face arrays (include/gpcg.h, gpcg_create_stencil3d); there
+    are no boundary faces and the 1e-3 of the diagonal is the shift."""
+    n = m ** 3
+    ex = np.exp(0.5 * gaussian(seed, 11, n)).reshape(m, m, m)     # [k, j, i]: edge (i,j,k)-(i+1,j,k)
+    ey = np.exp(0.5 * gaussian(seed, 12, n)).reshape(m, m, m)
+    ez = np.exp(0.5 * gaussian(seed, 13, n)).reshape(m, m, m)
+    wx = np.zeros((m, m, m + 1)); wx[:, :, 1:m] = ex[:, :, :m - 1]   # face i' joins i'-1, i'
+    wy = np.zeros((m, m + 1, m)); wy[:, 1:m, :] = ey[:, :m - 1, :]
+    wz = np.zeros((m + 1, m, m)); wz[1:m, :, :] = ez[:m - 1, :, :]
+    del ex, ey, ez
+    b = gaussian(seed, 14, n)
+    return Problem(name=name, kind="stencil3d", n=n, b=b, l=np.full(n, -box), u=np.full(n, box),
+                   x0=np.zeros(n), tol=-1e-8, nx=m, ny=m, nz=m, wx=wx.reshape(-1), wy=wy.reshape(-1),
+                   wz=wz.reshape(-1), shift=np.full(n, 1e-3), meta=dict(m=m, seed=seed, family="c4"))
+
+
 def c4() -> Problem:
     return c4_family()
 
@@ -332,4 +353,15 @@ CONFIGS = {"C0": c0, "C1": c1, "C2": c2, "C3": c3, "C4": c4}
 
 
 def get(name: str) -> Problem:
-    return CONFIGS[name]()
+    """A config by name; family members as e.g. C3_1600 (1600^2 member of C3's family),
+    C4_128 (128^3 member of C4's)."""
+    if name in CONFIGS:
+        return CONFIGS[name]()
+    fam, _, size = name.partition("_")
+    if fam == "C3" and size:
+        return c3_family(int(size), int(size))
+    if fam == "C4" and size:
+        return c4_family(m=int(size))
+    if fam == "C4s":
+        return c4_stencil_family(m=int(size) if size else 256)
+    raise KeyError(name)

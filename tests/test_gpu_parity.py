@@ -347,3 +347,64 @@ def test_pcg_fewer_cg_iterations_on_scaled_operator(G):
         assert rc == 0
         its[pc] = st["cg_iters"]
     assert its[1] < its[0], its
+
+
+# ------------------------------------------------------------------ every stencil kernel family
+# GPCG_TILE selects the sweep implementations (gpcg.cu): 0 column march (k2), 7 TMA tiles (k3),
+# 63 TMA-fed march with stored g (k4), 127 g-free TMA-fed march (k5, the default).  Each must
+# reach the oracle's solution on its own.
+@pytest.mark.parametrize("tile", ["0", "7", "63", "127"])
+@pytest.mark.parametrize("case", ["C0", "c3_family_160", "jb80_eps0.9"])
+def test_kernel_families_parity(G, oracle, monkeypatch, tile, case):
+    monkeypatch.setenv("GPCG_TILE", tile)
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    for pc in (0, 1):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(precond=pc)
+            rc, x, st = s.solve(prob.x0, tol)
+        assert rc == 0, (tile, pc, st)
+        assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+        assert np.max(np.abs(x - x_o)) <= 1e-7
+    # the GP phase on the host (GPCG_GP_GRAPH=0) reaches the same point
+    monkeypatch.setenv("GPCG_GP_GRAPH", "0")
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0 and np.max(np.abs(x - x_o)) <= 1e-7
+
+
+# ------------------------------------------------------------------ 3-D 7-point stencil (NEXT-2)
+@pytest.mark.parametrize("m", [5, 12, 16])
+def test_stencil3d_spmv_and_solve_parity(G, oracle, m):
+    prob = P.c4_stencil_family(m=m)
+    A = oracle.problem_csr(prob)
+    p = 2.0 * P.uniform(97, 1, prob.n) - 1.0
+    with G.Solver.from_problem(prob) as s:
+        spmv_close(s.hessvec(p), oracle.spmv(A, p), abs_op(A, p))
+        rc, x, st = s.solve(prob.x0, -1e-11)
+        yr = s.hessvec(p, reduced=True)
+    free = (x > prob.l) & (x < prob.u)
+    spmv_close(yr, oracle.spmv_masked(A, free, p), abs_op(A, p * free))
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=-1e-11)
+    assert rc == 0 and rc_o == 0
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
+    nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+    assert not nontie
+
+
+def test_stencil3d_full_c4_matches_csr_golden(G):
+    """Full-size C4 (256^3) through gpcg_create_stencil3d against the oracle's CSR golden:
+    the same matrix (face assembly == the edge-list CSR, pinned in test_oracle_pins)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "oracle_C4.json")
+    gold = json.load(open(path))
+    prob = P.c4_stencil_family(m=256)
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(prob.x0, gold["tol"])
+    assert rc == 0
+    assert abs(st["q"] - gold["q"]) <= 1e-10 * abs(gold["q"])
+    idx = np.asarray(gold["idx"])
+    assert np.max(np.abs(x[idx] - np.asarray(gold["x"]))) <= 1e-7

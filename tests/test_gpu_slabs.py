@@ -105,3 +105,18 @@ def test_slab_pcg_parity(G, oracle, case):
     assert rc == 0 and rc_o == 0
     assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
     assert np.max(np.abs(x - x_o)) <= 1e-7
+
+
+@pytest.mark.parametrize("slabs", [2, 3])
+def test_slab_stencil3d_parity(G, oracle, slabs):
+    prob = P.c4_stencil_family(m=10)
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=-1e-11)
+    with G.Solver.from_problem(prob, slabs=slabs) as s:
+        rc, x, st = s.solve(prob.x0, -1e-11)
+        p = 2.0 * P.uniform(96, 1, prob.n) - 1.0
+        y = s.hessvec(p)
+    A = oracle.problem_csr(prob)
+    spmv_close(y, oracle.spmv(A, p), abs_op(A, p))
+    assert rc == 0 and rc_o == 0
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7

@@ -467,3 +467,29 @@ def test_rng_determinism():
     assert np.array_equal(a[5:], b)
     z = P.gaussian(4, 14, 100000)
     assert abs(z.mean()) < 0.02 and abs(z.std() - 1) < 0.02
+
+
+# ---------------------------------------------------------------- 3-D 7-point stencil (NEXT-2)
+def test_stencil3d_assembly_matches_edge_list_csr(oracle):
+    # two independent routes to C4's matrix: face assembly (oracle) vs the generator's edge-list CSR
+    for m in (4, 7, 12):
+        A = oracle.problem_csr(P.c4_family(m=m))
+        S = oracle.problem_csr(P.c4_stencil_family(m=m))
+        assert np.array_equal(A.rp, S.rp) and np.array_equal(A.ci, S.ci)
+        assert np.max(np.abs(A.val - S.val)) <= 1e-14 * np.max(np.abs(A.val))
+
+
+def test_stencil3d_constant_coefficient_eigenpairs(oracle):
+    # unit faces incl. Dirichlet boundary faces: A = Laplacian_x + _y + _z with the textbook
+    # eigenvectors sin(p pi i/(n+1)) ... and eigenvalues sum_d 4 sin^2(p_d pi / (2(n_d+1)))
+    nx, ny, nz = 5, 4, 3
+    A = oracle.stencil3d_to_csr(nx, ny, nz, np.ones((nx + 1) * ny * nz), np.ones(nx * (ny + 1) * nz),
+                                np.ones(nx * ny * (nz + 1)))
+    i, j, k = np.meshgrid(np.arange(1, nx + 1), np.arange(1, ny + 1), np.arange(1, nz + 1), indexing="ij")
+    for p, q, r in [(1, 1, 1), (2, 3, 1), (5, 4, 3)]:
+        v = (np.sin(p * np.pi * i / (nx + 1)) * np.sin(q * np.pi * j / (ny + 1)) *
+             np.sin(r * np.pi * k / (nz + 1))).transpose(2, 1, 0).reshape(-1)     # v = i + nx (j + ny k)
+        lam = sum(4 * np.sin(a * np.pi / (2 * (m + 1))) ** 2 for a, m in [(p, nx), (q, ny), (r, nz)])
+        assert np.max(np.abs(oracle.spmv(A, v) - lam * v)) <= 1e-13
+    D = A.todense()
+    assert np.array_equal(D, D.T)
