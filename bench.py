@@ -57,13 +57,20 @@ def load_peaks():
 
 
 def cg_kernel_name(prob):
-    if prob.kind != "stencil2d":
+    """The CG-iteration kernel libgpcg.so selects for this problem (gpcg.cu enqueue_cg_iter)."""
+    if prob.kind == "csr":
         return "k_cg_iter<CsrOp>"
+    if prob.kind == "stencil3d":
+        return "k_cg_iter<Stencil3Op>"
     bc = not prob.wx_ld and not prob.wy_ld and prob.shift is None
-    tile = int(os.environ.get("GPCG_TILE", "7") or 7) & 4
+    tile = int(os.environ.get("GPCG_TILE", "127") or 127)
     if os.environ.get("GPCG_GENERIC") == "1":
         return "k_cg_iter<StencilOp>"
-    return "k3_cg_iter<2> (TMA tile)" if (bc and tile) else "k2_cg_iter (column march)"
+    if bc and tile & 8:
+        return "k4_cg_iter (TMA-fed column march)"
+    if bc and tile & 4:
+        return "k3_cg_iter<2> (TMA tile)"
+    return "k2_cg_iter (column march)"
 
 
 def cg_min_bytes_per_free_point(prob):
@@ -291,6 +298,7 @@ def run_ours(args):
     s_e2e.solve(x0h, prob.tol, x_out=xh)
     s_e2e.close()
     e2e_s, e2e_hvps = 0.0, 0
+    t_parts = {"create_s": 0.0, "solve_s": 0.0, "destroy_s": 0.0}
     for _ in range(e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -298,10 +306,16 @@ def run_ours(args):
             dist.barrier()
         t0 = time.perf_counter()
         s2 = make()
+        t1 = time.perf_counter()
         rc, _, st2 = s2.solve(x0h, prob.tol, x_out=xh)
+        t2 = time.perf_counter()
         s2.close()
         torch.cuda.synchronize()
-        e2e_s += time.perf_counter() - t0
+        t3 = time.perf_counter()
+        e2e_s += t3 - t0
+        t_parts["create_s"] += (t1 - t0) / e2e_steps
+        t_parts["solve_s"] += (t2 - t1) / e2e_steps
+        t_parts["destroy_s"] += (t3 - t2) / e2e_steps
         e2e_hvps += st2["cg_iters"]
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -348,7 +362,8 @@ def run_ours(args):
                     "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": int(x0.numel() * 8),
                     "what": "gpcg_create (H2D operator,b,l,u from pinned host) + gpcg_solve (H2D x0, "
-                            "D2H x) + gpcg_destroy, wall clock, %d steps" % e2e_steps},
+                            "D2H x) + gpcg_destroy, wall clock, %d steps" % e2e_steps,
+                    "per_step": t_parts},
             "gpu_launches": agg["kernel_launches"],
             "clocks": clk,
         }
