@@ -159,7 +159,8 @@ struct Slab {
     int send_lo = 0, send_hi = 0;   // rows the lower / upper neighbour reads from this slab
     int nb_lo = NB_NONE, nb_hi = NB_NONE;
     long long nalloc = 0;           // elements per vector = (glo + rows + ghi) * pitch
-    double* vb[NVEC] = {};          // allocation bases
+    void* arena = nullptr;          // one allocation holding every vector and mask of the slab
+    double* vb[NVEC] = {};          // allocation bases (inside the arena)
     double* v[NVEC] = {};           // origins (owned row 0)
     unsigned char* mb[NMSK] = {};
     unsigned char* m[NMSK] = {};
@@ -238,6 +239,8 @@ struct gpcg_problem {
     cudaGraphExec_t gp_exec[2] = {nullptr, nullptr};   // GP chunk graphs starting from buffers 0 / 1
     int gp_exec_chunk = 0;
     bool gp_graph = true;           // GPCG_GP_GRAPH=0: host-driven GP steps (A/B)
+    bool cg_persistent = true;      // GPCG_CG_PERSIST=0: CG as graph chunks instead of k6_cg_loop
+    unsigned int* gbar = nullptr;   // grid-barrier counter of the persistent kernels
     long long launches = 0;
     long long cg_iters_timed = 0, cg_free_iters_timed = 0;
     double t_cg_timed_ms = 0.0;
@@ -425,13 +428,12 @@ void free_all(gpcg_problem* h) {
     cudaSetDevice(h->dev);
     if (h->st) cudaStreamSynchronize(h->st);
     for (Slab& S : h->slabs) {
-        for (double* p : S.vb) if (p) cudaFree(p);
-        for (unsigned char* p : S.mb) if (p) cudaFree(p);
+        if (S.arena) cudaFree(S.arena);
         for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.rp, (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             if (p) cudaFree(p);
     }
-    for (void* p : {(void*)h->red_all, (void*)h->red_tot, (void*)h->lu0, (void*)h->dS})
+    for (void* p : {(void*)h->red_all, (void*)h->red_tot, (void*)h->lu0, (void*)h->dS, (void*)h->gbar})
         if (p) cudaFree(p);
     if (h->hS) cudaFreeHost(h->hS);
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
@@ -507,6 +509,8 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem));
     RC(set_smem(k4_cg_iter<false>, m4cg::kSmem));
     RC(set_smem(k4_cg_iter<true>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop<false>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop<true>, m4cg::kSmem));
     RC(set_smem(k4_accept<true, true, false>, AccLayout4<true, true, false>::kSmem));
     RC(set_smem(k4_accept<true, false, false>, AccLayout4<true, false, false>::kSmem));
     RC(set_smem(k4_accept<false, true, false>, AccLayout4<false, true, false>::kSmem));
@@ -548,7 +552,9 @@ int setup_tile(gpcg_problem* h) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, m4::kThreads, smem);
         return std::max(1, nb) * h->sms;
     };
-    const int r4cg = res4(k4_cg_iter<false>, m4cg::kSmem);
+    int nbcg = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbcg, k4_cg_iter<false>, m4::kThreadsWS, m4cg::kSmem);
+    const int r4cg = std::max(1, nbcg) * h->sms;
     const int r4acc = h->sb ? (h->bb ? res4(k4_accept<true, true, true>, AccLayout4<true, true, true>::kSmem)
                                      : res4(k4_accept<true, true, false>, AccLayout4<true, true, false>::kSmem))
                             : (h->bb ? res4(k4_accept<false, true, true>, AccLayout4<false, true, true>::kSmem)
@@ -640,7 +646,10 @@ int create_streams(gpcg_problem* h, void* stream) {
     {
         const char* e = getenv("GPCG_GP_GRAPH");
         h->gp_graph = !(e && e[0] == '0');
+        const char* e2 = getenv("GPCG_CG_PERSIST");
+        h->cg_persistent = !(e2 && e2[0] == '0');
     }
+    CK(cudaMalloc(&h->gbar, sizeof(unsigned int)));
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev_a));
@@ -656,16 +665,21 @@ int create_streams(gpcg_problem* h, void* stream) {
 int create_vectors(gpcg_problem* h, const double* b, const double* l, const double* u) {
     for (Slab& S : h->slabs) {
         S.nalloc = (long long)(S.glo + S.rows + S.ghi) * h->pitch;
-        const size_t nb = (size_t)S.nalloc * sizeof(double);
+        const size_t nb = ((size_t)S.nalloc * sizeof(double) + 255) / 256 * 256;
+        const size_t mbytes = ((size_t)S.nalloc + 255) / 256 * 256;
         const long long off = (long long)S.glo * h->pitch;
+        // one arena per slab (few large allocations keep create / destroy cheap); 256-byte aligned
+        // sub-arrays; zeroed: padding columns and boundary ghosts stay 0
+        const size_t total = NVEC * nb + NMSK * mbytes;
+        CK(cudaMalloc(&S.arena, total));
+        CK(cudaMemsetAsync(S.arena, 0, total, h->st));
+        char* base = static_cast<char*>(S.arena);
         for (int k = 0; k < NVEC; ++k) {
-            CK(cudaMalloc(&S.vb[k], nb));
-            CK(cudaMemsetAsync(S.vb[k], 0, nb, h->st));     // padding columns and boundary ghosts stay 0
+            S.vb[k] = reinterpret_cast<double*>(base + k * nb);
             S.v[k] = S.vb[k] + off;
         }
         for (int k = 0; k < NMSK; ++k) {
-            CK(cudaMalloc(&S.mb[k], (size_t)S.nalloc));
-            CK(cudaMemsetAsync(S.mb[k], 0, (size_t)S.nalloc, h->st));
+            S.mb[k] = reinterpret_cast<unsigned char*>(base + NVEC * nb + k * mbytes);
             S.m[k] = S.mb[k] + off;
         }
         // partial sums of the largest grid any kernel of this slab uses (grid-stride generic kernels
@@ -996,11 +1010,11 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
         const RedScratch R = h->red(s);
         if (use_k4) {
             if (pc)
-                k4_cg_iter<true><<<S.grid4_cg, m4::kThreads, m4cg::kSmem, h->st>>>(
+                k4_cg_iter<true><<<S.grid4_cg, m4::kThreadsWS, m4cg::kSmem, h->st>>>(
                     S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
                     h->dS, R);
             else
-                k4_cg_iter<false><<<S.grid4_cg, m4::kThreads, m4cg::kSmem, h->st>>>(
+                k4_cg_iter<false><<<S.grid4_cg, m4::kThreadsWS, m4cg::kSmem, h->st>>>(
                     S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
                     h->dS, R);
         } else if (use_tile) {
@@ -1156,6 +1170,31 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     RC(finish_reduce(h, a, 2));
     if (!spec2d(h)) RC(exchange(h, {VRHO0, VQ0, VS0}, {MKCG}));
     else RC(exchange(h, {VRHO0, VQ0}, {MKCG}));
+    if (h->cg_persistent && h->tile && (h->tile_mask & 8) && !has_ghosts(h)) {
+        // one cooperative launch runs the whole CG call (k6_cg_loop)
+        Slab& S = h->slabs[0];
+        CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
+        CK(cudaEventRecord(h->ev_c0, h->st));
+        void* args[] = {(void*)&S.sop, (void*)&S.bg_cg, (void*)&S.t4[VRHO0], (void*)&S.t4[VRHO1], (void*)&S.t4[VQ0],
+                        (void*)&S.t4[VQ1], (void*)&S.t4wo, (void*)&S.t4m[MKCG], (void*)&S.v[VRHO0],
+                        (void*)&S.v[VRHO1], (void*)&S.v[VQ0], (void*)&S.v[VQ1], (void*)&S.v[VW], (void*)&h->dS,
+                        (void*)&S.partials, (void*)&h->gbar};
+        const void* fn = h->prm.precond == 1 ? (const void*)k6_cg_loop<true> : (const void*)k6_cg_loop<false>;
+        CK(cudaLaunchCooperativeKernel(fn, dim3(S.grid4_cg), dim3(m4::kThreadsWS), args, (size_t)m4cg::kSmem, h->st));
+        CK(cudaEventRecord(h->ev_c1, h->st));
+        h->launches++;
+        RC(sync_scal(h));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_c0, h->ev_c1));
+        h->t_cg_timed_ms += ms;
+        h->cg_iters_timed += h->hS->cg_it;
+        h->cg_free_iters_timed += h->hS->cg_it * m;
+        *iters = h->hS->cg_it;
+        if (h->hS->cg_reason == CG_NOTSPD)
+            return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
+                           (long long)h->hS->cg_it);
+        return GPCG_OK;    // one slab: no ghosts of w to refresh
+    }
     const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
     RC(build_cg_graph(h, chunk));
     for (;;) {

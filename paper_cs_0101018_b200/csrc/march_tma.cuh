@@ -30,8 +30,9 @@
 namespace gpcg {
 
 namespace m4 {
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
+constexpr int kWarps = 4;                 // consumer warps (one per 28 / 26-column strip)
+constexpr int kThreads = 32 * kWarps;     // lock-step engine: thread 0 also issues the TMA loads
+constexpr int kThreadsWS = 32 * (kWarps + 1);  // warp-specialised engine: + one TMA producer warp
 constexpr int kOut = 28 * kWarps;         // 112 output columns per band
 constexpr int kBW = kOut + 4;             // 116 box columns (2 halo each side)
 constexpr int kMW = 144;                  // u8 mask box width (start floored to 16 B, 116 + 15 < 144)
@@ -49,10 +50,81 @@ struct BandGeom {
     int rlo;                    // first tensor row (StencilOp::rlo)
 };
 
-// The pipeline engine.  issue(stage_ptr, x0, yr, bar): TMA loads of the block whose
-// first raw row is yr (band output columns start at x0); begin(x0, y0, y1): a new
-// item; row(stage_ptr, kk, r): one raw row (kk-th of the block).  OUT = output
-// columns per band; the raw rows of an item run from y0 - PRE to y1 - 1 + POST.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// The pipeline engine (warp-specialised).  Warp kWarps is the producer: its lane 0 walks
+// the CTA's block sequence and, once the consumers have released a stage (empty
+// mbarrier, one arrival per consumer warp), issues the TMA loads of the next block into
+// it (full mbarrier, transaction bytes).  The consumer warps wait on the full barrier,
+// march their rows and release the stage -- no CTA-wide barrier per block, so warps
+// drift up to NST blocks apart.  issue(stage_ptr, x0, yr, bar): the loads of the block
+// whose first raw row is yr (band output columns start at x0); begin(x0, y0, y1): a new
+// item (consumers); row(stage_ptr, kk, r): one raw row.  OUT = output columns per band;
+// the raw rows of an item run from y0 - PRE to y1 - 1 + POST.  The producer warp leaves
+// with nothing accumulated and joins the block reduction afterwards.
+// k0: blocks this CTA already streamed through the same barriers (a persistent kernel
+// calls the engine once per sweep; the mbarriers are initialised at k0 = 0 only and
+// their phases continue).  Returns the CTA's block count after the sweep.
+template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
+__device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
+                                                Begin&& begin, Row&& row, int k0 = 0) {
+    using namespace m4;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+    uint64_t* empty = full + NST;
+    const int nitems = G.nbands * G.nsegs;
+    const int nblk = (G.seg + PRE + POST + kBR - 1) / kBR;
+    int nmine = 0;
+    for (int t = blockIdx.x; t < nitems; t += gridDim.x) nmine += nblk;
+    if (k0 == 0) {
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < NST; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], kWarps);
+            }
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kWarps) {                                 // producer
+        if (lane == 0) {
+            int k = k0;
+            for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
+                const int x0 = (t % G.nbands) * OUT;
+                const int yb = (t / G.nbands) * G.seg - PRE;
+                for (int b = 0; b < nblk; ++b, ++k) {
+                    const int stage = k % NST;
+                    if (k >= NST) mbar_wait(&empty[stage], ((k / NST) - 1) & 1);
+                    issue_loads(smem + stage * STAGE, x0, yb + b * kBR, &full[stage]);
+                }
+            }
+        }
+        return k0 + nmine;
+    }
+    int k = k0;
+    for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
+        const int x0 = (t % G.nbands) * OUT;
+        const int y0 = (t / G.nbands) * G.seg, y1 = min(y0 + G.seg, ny);
+        begin(x0, y0, y1);
+        for (int b = 0; b < nblk; ++b, ++k) {
+            const int stage = k % NST;
+            unsigned char* st = smem + stage * STAGE;
+            mbar_wait(&full[stage], (k / NST) & 1);
+            const int yr = y0 - PRE + b * kBR;
+#pragma unroll
+            for (int kk = 0; kk < kBR; ++kk) row(st, kk, yr + kk);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);    // this warp is done with the stage
+        }
+    }
+    return k0 + nmine;
+}
+
+// Lock-step variant (kThreads = 4 warps): thread 0 issues the loads of block k + NST
+// after a CTA-wide barrier that retires block k.  Fewer threads per CTA (more CTAs per
+// SM at the register budget of the accept / search sweeps).
 template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
 __device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
                                               Begin&& begin, Row&& row) {
@@ -113,32 +185,30 @@ constexpr int kNST = 4;
 constexpr int kSmem = kNST * kStage + 64;
 }  // namespace m4cg
 
-template <bool PC>     // point-Jacobi PCG as in k2_cg_iter<BC, true>
-__global__ void __launch_bounds__(m4::kThreads, 4)
-k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, const __grid_constant__ CUtensorMap m_p,
-           const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
-           double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R) {
+// One CG sweep on this CTA's items: rho_n, p_n, w written for the free points; acc = this
+// thread's (gamma, delta) contributions.  Returns the CTA's running TMA block count.
+template <bool PC>
+__device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, const CUtensorMap* m_rho,
+                                         const CUtensorMap* m_p, const CUtensorMap* m_w, const CUtensorMap* m_mask,
+                                         double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out,
+                                         double alpha, double beta, unsigned char* smem, double (&acc)[2], int k0) {
     using namespace m4cg;
-    if (*(volatile int*)&S->cg_done) return;
-    const double alpha = S->cg_alpha, beta = S->cg_beta;
-    extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int c = 28 * wid + lane;                        // box column of this lane
     const bool out_lane = lane >= 2 && lane < 30;
-    double acc[2] = {0.0, 0.0};
     int gx = 0, moff = 0, y0 = 0, y1 = 0;
     bool col_ok = false;
     Op5<true> op;
     double pn_m2 = 0.0, pn_m1 = 0.0, rho_m1 = 0.0, rn_m3 = 0.0, rn_m2 = 0.0, rr_m2 = 0.0, dinv = 0.0;
     unsigned char m_m1 = 0, m_m2 = 0;
-    band_pipeline<kNST, kStage>(
+    return band_pipeline_ws<kNST, kStage>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, kTx);
-            tma_load_2d(st + kRho, &m_rho, x0 - 2, yr - G.rlo, bar);
-            tma_load_2d(st + kP, &m_p, x0 - 2, yr - G.rlo, bar);
-            tma_load_2d(st + kW, &m_w, x0, yr - 2 - G.rlo, bar);      // w of the emitted rows (r - 2)
-            tma_load_2d(st + kM, &m_mask, floor16(x0 - 2), yr - G.rlo, bar);
+            tma_load_2d(st + kRho, m_rho, x0 - 2, yr - G.rlo, bar);
+            tma_load_2d(st + kP, m_p, x0 - 2, yr - G.rlo, bar);
+            tma_load_2d(st + kW, m_w, x0, yr - 2 - G.rlo, bar);      // w of the emitted rows (r - 2)
+            tma_load_2d(st + kM, m_mask, floor16(x0 - 2), yr - G.rlo, bar);
         },
         [&](int x0, int yb, int ye) {
             gx = x0 - 2 + c;
@@ -177,8 +247,119 @@ k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, c
             m_m2 = m_m1; m_m1 = m;
             rn_m3 = rn_m2; rn_m2 = rn1;
             rr_m2 = rr1;
-        });
+        },
+        k0);
+}
+
+template <bool PC>     // point-Jacobi PCG as in k2_cg_iter<BC, true>
+__global__ void __launch_bounds__(m4::kThreadsWS, 4)
+k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, const __grid_constant__ CUtensorMap m_p,
+           const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
+           double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R) {
+    if (*(volatile int*)&S->cg_done) return;
+    const double alpha = S->cg_alpha, beta = S->cg_beta;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double acc[2] = {0.0, 0.0};
+    cg_sweep4<PC>(A, G, &m_rho, &m_p, &m_w, &m_mask, rho_n, p_n, w_out, alpha, beta, smem, acc, 0);
     reduce_and_finish<2>(acc, R, [&](double* tt) { cg_finalize(tt[0], tt[1], S); });
+}
+
+// ============================================================================
+// a5 as ONE persistent cooperative launch per CG call (single slab, single rank): every
+// iteration is a sweep, a block reduction, a grid barrier, and the finaliser evaluated
+// redundantly by every CTA on the same fixed-order sum of the block partials (so every
+// CTA takes the same decision without a second barrier).  No launch per iteration, no
+// host poll; the loop stops at cgstop1 / the exact-solve guard / the cap / breakdown.
+// rho and p ping-pong between buffers 0 / 1 by iteration parity (same as the graph path).
+// ============================================================================
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
+    // this thread's global writes become visible to the async proxy (the next sweep's TMA loads)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();                                  // release the CTA's writes at gpu scope
+        const unsigned int target = (gen + 1) * nblocks;
+        atomicAdd(bar, 1u);
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+        ++gen;
+    }
+    __syncthreads();
+}
+
+template <bool PC>
+__global__ void __launch_bounds__(m4::kThreadsWS, 4)
+k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, const __grid_constant__ CUtensorMap m_rho1,
+           const __grid_constant__ CUtensorMap m_p0, const __grid_constant__ CUtensorMap m_p1,
+           const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
+           double* __restrict__ rho0, double* __restrict__ rho1, double* __restrict__ p0, double* __restrict__ p1,
+           double* __restrict__ w_out, Scal* S, double* __restrict__ part, unsigned int* gbar) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[2 * 32];
+    __shared__ double tot[2];
+    // CG state (identical in every CTA)
+    double alpha = S->cg_alpha, beta = S->cg_beta, gamma_old = S->cg_gamma, maxdec = S->cg_maxdec;
+    const double eta2 = S->cg_eta2, rnorm0 = S->cg_rnorm0;
+    long long it = S->cg_it;
+    const long long cap = S->cg_cap;
+    int done = S->cg_done, reason = S->cg_reason;
+    unsigned int gen = 0;
+    int k = 0;
+    const unsigned int G_ = gridDim.x;
+    while (!done) {
+        const int a = (int)(it & 1);
+        double acc[2] = {0.0, 0.0};
+        k = cg_sweep4<PC>(A, G, a ? &m_rho1 : &m_rho0, a ? &m_p1 : &m_p0, &m_w, &m_mask, a ? rho0 : rho1,
+                          a ? p0 : p1, w_out, alpha, beta, smem, acc, k);
+        // block partials -> part[parity][s][block]
+        block_reduce<2>(acc, red);
+        double* pp = part + (it & 1) * 2 * G_;
+        if (threadIdx.x == 0) {
+            pp[blockIdx.x] = acc[0];
+            pp[G_ + blockIdx.x] = acc[1];
+        }
+        grid_barrier(gbar, G_, gen);
+        // fixed-order sum of the partials, same in every CTA
+        double t[2] = {0.0, 0.0};
+        for (unsigned int b = threadIdx.x; b < G_; b += blockDim.x) {
+            t[0] += __ldcg(pp + b);
+            t[1] += __ldcg(pp + G_ + b);
+        }
+        block_reduce<2>(t, red);
+        if (threadIdx.x == 0) { tot[0] = t[0]; tot[1] = t[1]; }
+        __syncthreads();
+        const double gamma = tot[0], delta = tot[1];
+        // cg_finalize (fin.cuh), evaluated in every CTA
+        const double dec = 0.5 * alpha * gamma_old;
+        ++it;
+        reason = CG_RUNNING;
+        if (it >= 2 && dec <= eta2 * maxdec) reason = CG_PROGRESS;
+        else if (sqrt(gamma) <= 1e-14 * (1.0 + rnorm0)) reason = CG_EXACT;
+        else if (it >= cap) reason = CG_CAP;
+        if (dec > maxdec) maxdec = dec;
+        if (reason == CG_RUNNING) {
+            const double beta_n = gamma / gamma_old;
+            const double pap = delta - beta_n * gamma / alpha;
+            beta = beta_n;
+            if (!(pap > 0.0)) reason = CG_NOTSPD;
+            else alpha = gamma / pap;
+        }
+        gamma_old = gamma;
+        if (reason != CG_RUNNING) done = 1;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            S->cg_it = it;
+            S->cg_dec = dec;
+            S->cg_maxdec = maxdec;
+            S->cg_gamma = gamma;
+            S->cg_beta = beta;
+            S->cg_alpha = alpha;
+            S->cg_reason = reason;
+            S->cg_done = done;
+        }
+    }
+    // the host zeroes the barrier counter before each launch
 }
 
 // ============================================================================
