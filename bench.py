@@ -67,6 +67,8 @@ def cg_kernel_name(prob):
     if os.environ.get("GPCG_GENERIC") == "1":
         return "k_cg_iter<StencilOp>"
     if bc and tile & 8:
+        if os.environ.get("GPCG_CG_PERSIST", "1") != "0":
+            return "k6_cg_loop (persistent cooperative CG, TMA-fed column march; per-iteration time)"
         return "k4_cg_iter (TMA-fed column march)"
     if bc and tile & 4:
         return "k3_cg_iter<2> (TMA tile)"

@@ -240,6 +240,9 @@ struct gpcg_problem {
     int gp_exec_chunk = 0;
     bool gp_graph = true;           // GPCG_GP_GRAPH=0: host-driven GP steps (A/B)
     bool cg_persistent = true;      // GPCG_CG_PERSIST=0: CG as graph chunks instead of k6_cg_loop
+    bool gp_persistent = true;      // GPCG_GP_PERSIST=0: GP phase as graph chunks instead of k6_gp_loop
+    int grid6_gp = 1;
+    size_t smem6_gp = 0;
     unsigned int* gbar = nullptr;   // grid-barrier counter of the persistent kernels
     long long launches = 0;
     long long cg_iters_timed = 0, cg_free_iters_timed = 0;
@@ -609,6 +612,23 @@ int setup_tile(gpcg_problem* h) {
     }
     h->tile = true;
     h->gfree = (h->tile_mask & 64) != 0;
+    {
+        // persistent GP phase: smem of the larger (accept) layout; grid within co-residency
+        auto cfg = [&](auto sbt, auto bbt) {
+            constexpr bool SB = decltype(sbt)::value, BB = decltype(bbt)::value;
+            const size_t sm = std::max<size_t>(AccLayout5<SB, BB, m5::GP>::kSmem, SrchLayout5<SB, BB, m5::GP, 2>::kSmem);
+            h->smem6_gp = sm;
+            cudaFuncSetAttribute(k6_gp_loop<SB, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k6_gp_loop<SB, BB>, m4::kThreads, sm);
+            return std::max(1, nb) * h->sms;
+        };
+        int r6;
+        if (h->sb) r6 = h->bb ? cfg(std::true_type(), std::true_type()) : cfg(std::true_type(), std::false_type());
+        else r6 = h->bb ? cfg(std::false_type(), std::true_type()) : cfg(std::false_type(), std::false_type());
+        const Slab& S0 = h->slabs[0];
+        h->grid6_gp = std::max(1, std::min({r6, S0.grid5_srch, S0.grid5_acc}));
+    }
     return GPCG_OK;
 }
 
@@ -648,6 +668,8 @@ int create_streams(gpcg_problem* h, void* stream) {
         h->gp_graph = !(e && e[0] == '0');
         const char* e2 = getenv("GPCG_CG_PERSIST");
         h->cg_persistent = !(e2 && e2[0] == '0');
+        const char* e3 = getenv("GPCG_GP_PERSIST");
+        h->gp_persistent = !(e3 && e3[0] == '0');
     }
     CK(cudaMalloc(&h->gbar, sizeof(unsigned int)));
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
@@ -1115,6 +1137,24 @@ int build_gp_graph(gpcg_problem* h, int chunk) {
 int launches_per_gp_step(const gpcg_problem* h) {
     const int fins = h->deferred ? (1 + (h->nslabs() > 1 ? 1 : 0)) : 0;
     return (fused_cauchy(h) ? 0 : h->nslabs() + fins) + 2 * (h->nslabs() + fins) + 1;
+}
+
+// The whole GP phase (until it stops or hands a step back) as one cooperative launch.
+int launch_gp_loop(gpcg_problem* h, int cur) {
+    Slab& S = h->slabs[0];
+    CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
+    Bounds B = h->bounds(S);
+    double mu = h->prm.mu;
+    void* args[] = {(void*)&S.sop, (void*)&S.bg5_srch, (void*)&S.bg5_acc, (void*)&B, (void*)&S.brow,
+                    (void*)&S.t5[VY0], (void*)&S.t5[VY1], (void*)&S.t5[VB], (void*)&S.t5[VL], (void*)&S.t5[VU],
+                    (void*)&S.t5m[MK0], (void*)&S.t5m[MK1], (void*)&S.v[VY0], (void*)&S.v[VY1], (void*)&S.m[MK0],
+                    (void*)&S.m[MK1], (void*)&cur, (void*)&mu, (void*)&h->dS, (void*)&S.partials, (void*)&h->gbar};
+    const void* fn;
+    if (h->sb) fn = h->bb ? (const void*)k6_gp_loop<true, true> : (const void*)k6_gp_loop<true, false>;
+    else fn = h->bb ? (const void*)k6_gp_loop<false, true> : (const void*)k6_gp_loop<false, false>;
+    CK(cudaLaunchCooperativeKernel(fn, dim3(h->grid6_gp), dim3(m4::kThreads), args, h->smem6_gp, h->st));
+    h->launches++;
+    return GPCG_OK;
 }
 
 // kernels per CG iteration (for the launch count)
@@ -1860,7 +1900,8 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     RC(launch_accept(h, VIN, NO_VEC, 0.0, NO_VEC, VY0, VG0, MK0));
     RC(sync_scal(h));
     st.full_spmvs++;
-    if (h->gp_graph) RC(build_gp_graph(h, std::max(1, h->prm.gp_chunk)));
+    if (h->gp_graph && !(h->gp_persistent && h->gfree && !has_ghosts(h)))
+        RC(build_gp_graph(h, std::max(1, h->prm.gp_chunk)));
     st.g0_norm = std::sqrt(S.g2);
     tau = tol > 0.0 ? tol : -tol * st.g0_norm;
     st.tau = tau;
@@ -1878,9 +1919,14 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 h->launches++;
                 CKLAUNCH();
                 long long jdone = 0;
+                const bool persist = h->gp_persistent && h->gfree && !has_ghosts(h);
                 for (;;) {
-                    CK(cudaGraphLaunch(h->gp_exec[cur], h->st));
-                    h->launches += (long long)h->gp_exec_chunk * launches_per_gp_step(h);
+                    if (persist) {
+                        if ((rc = launch_gp_loop(h, cur))) goto fail;
+                    } else {
+                        CK(cudaGraphLaunch(h->gp_exec[cur], h->st));
+                        h->launches += (long long)h->gp_exec_chunk * launches_per_gp_step(h);
+                    }
                     if ((rc = sync_scal(h))) goto fail;
                     const long long jn = S.gp_j;
                     cur = (int)((cur + (jn - jdone)) & 1);

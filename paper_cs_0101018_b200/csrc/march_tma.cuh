@@ -125,25 +125,30 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
 // Lock-step variant (kThreads = 4 warps): thread 0 issues the loads of block k + NST
 // after a CTA-wide barrier that retires block k.  Fewer threads per CTA (more CTAs per
 // SM at the register budget of the accept / search sweeps).
+// bars: NST mbarriers (null: after the stages); k0 as in band_pipeline_ws (init at 0 only).
 template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
-__device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
-                                              Begin&& begin, Row&& row) {
+__device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
+                                             Begin&& begin, Row&& row, uint64_t* bars = nullptr, int k0 = 0) {
     using namespace m4;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+    uint64_t* bar = bars ? bars : reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     const int nitems = G.nbands * G.nsegs;
     const int nblk = (G.seg + PRE + POST + kBR - 1) / kBR;
-    auto issue = [&](int k) {
+    int nmine = 0;
+    for (int t = blockIdx.x; t < nitems; t += gridDim.x) nmine += nblk;
+    auto issue = [&](int k) {                            // k: this sweep's local block index
         const int i = k / nblk, b = k - i * nblk;
         const int t = blockIdx.x + i * (int)gridDim.x;
         if (t >= nitems) return;
-        const int stage = k % NST;
+        const int stage = (k0 + k) % NST;
         const int x0 = (t % G.nbands) * OUT;
         const int yr = (t / G.nbands) * G.seg - PRE + b * kBR;
         issue_loads(smem + stage * STAGE, x0, yr, &bar[stage]);
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
-        fence_mbar_init();
+        if (k0 == 0) {
+            for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+            fence_mbar_init();
+        }
         for (int k = 0; k < NST; ++k) issue(k);
     }
     __syncthreads();
@@ -153,9 +158,9 @@ __device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigne
         const int y0 = (t / G.nbands) * G.seg, y1 = min(y0 + G.seg, ny);
         begin(x0, y0, y1);
         for (int b = 0; b < nblk; ++b, ++k) {
-            const int stage = k % NST;
+            const int stage = (k0 + k) % NST;
             unsigned char* st = smem + stage * STAGE;
-            mbar_wait(&bar[stage], (k / NST) & 1);
+            mbar_wait(&bar[stage], ((k0 + k) / NST) & 1);
             const int yr = y0 - PRE + b * kBR;
 #pragma unroll
             for (int kk = 0; kk < kBR; ++kk) row(st, kk, yr + kk);
@@ -166,6 +171,7 @@ __device__ __forceinline__ void band_pipeline(const BandGeom& G, int ny, unsigne
             }
         }
     }
+    return k0 + nmine;
 }
 
 // ============================================================================
@@ -612,26 +618,18 @@ struct AccLayout5 {
 // (CG) yn(r) = P[y + alpha w]; (PROJ) yn(r) = P[y].  With ry the yn row: gn(ry-1) = A yn - b,
 // d(ry-1) = grad_Omega q(yn); emit ry-2 with (A d)(ry-2).  y_out, mask_out, the six sums.
 template <bool SB, bool BB, int MODE>
-__global__ void __launch_bounds__(m4::kThreads, 4)
-k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
-          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
-          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
-          const __grid_constant__ CUtensorMap m_mp, int has_mp, double* __restrict__ y_out,
-          unsigned char* __restrict__ mask_out, Scal* S, RedScratch R, int gp) {
+__device__ __forceinline__ int accept_sweep5(const StencilOp& A, const BandGeom& G, const Bounds& Bd,
+                                             const double* __restrict__ brow, const CUtensorMap* m_y,
+                                             const CUtensorMap* m_dir, const CUtensorMap* m_b, const CUtensorMap* m_l,
+                                             const CUtensorMap* m_u, const CUtensorMap* m_mp, int has_mp, double alpha,
+                                             double* __restrict__ y_out, unsigned char* __restrict__ mask_out,
+                                             unsigned char* smem, double (&acc)[6], uint64_t* bars, int k0) {
     using namespace m4;
     using L = AccLayout5<SB, BB, MODE>;
     constexpr int LAG = L::kLag;
-    if (gp && *(volatile int*)&S->gp_done) return;
-    double alpha = 0.0;
-    if (MODE != m5::PROJ) {
-        if (S->s_h < 0) return;                   // uniform: no accepted step in this batch
-        alpha = S->s_alpha;
-    }
-    extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int c = 26 * wid + lane + 1;            // box column
     const bool out_lane = lane >= 3 && lane < 29;
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     int gx = 0, moff = 0, y0 = 0, y1 = 0;
     bool col_ok = false;
     Op5<true> op;
@@ -642,19 +640,19 @@ k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, c
     double d_a = 0.0, d_b = 0.0;                  // d(ry-2), d(ry-3)
     double yn_e = 0.0, gn_e = 0.0, l_e = 0.0, u_e = 0.0;   // row ry-2 (emitted)
     const uint32_t tx = L::kMP + (has_mp ? m5::kUt : 0);
-    band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, tx);
             const int yt = yr - G.rlo;
-            tma_load_2d(st + L::kY, &m_y, x0 - 4, yt, bar);
-            if (MODE == m5::CG) tma_load_2d(st + L::kD, &m_dir, x0 - 4, yt, bar);
-            if (!BB) tma_load_2d(st + L::kB, &m_b, x0 - 4, yt, bar);
+            tma_load_2d(st + L::kY, m_y, x0 - 4, yt, bar);
+            if (MODE == m5::CG) tma_load_2d(st + L::kD, m_dir, x0 - 4, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, m_b, x0 - 4, yt, bar);
             if (!SB) {
-                tma_load_2d(st + L::kL, &m_l, x0 - 4, yt, bar);
-                tma_load_2d(st + L::kU, &m_u, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kL, m_l, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kU, m_u, x0 - 4, yt, bar);
             }
-            if (has_mp) tma_load_2d(st + L::kMP, &m_mp, floor16(x0 - 4), yt - LAG, bar);
+            if (has_mp) tma_load_2d(st + L::kMP, m_mp, floor16(x0 - 4), yt - LAG, bar);
         },
         [&](int x0, int yb, int ye) {
             gx = x0 - 3 + 26 * wid + lane;
@@ -714,7 +712,27 @@ k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, c
             d_b = d_a; d_a = d1;
             yn_b = yn_a; yn_a = yn;
             l_a = ln; u_a = un; b_a = bn;
-        });
+        },
+        bars, k0);
+}
+
+template <bool SB, bool BB, int MODE>
+__global__ void __launch_bounds__(m4::kThreads, 4)
+k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
+          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
+          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
+          const __grid_constant__ CUtensorMap m_mp, int has_mp, double* __restrict__ y_out,
+          unsigned char* __restrict__ mask_out, Scal* S, RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;
+    double alpha = 0.0;
+    if (MODE != m5::PROJ) {
+        if (S->s_h < 0) return;                   // uniform: no accepted step in this batch
+        alpha = S->s_alpha;
+    }
+    extern __shared__ __align__(128) unsigned char smem[];
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    accept_sweep5<SB, BB, MODE>(A, G, Bd, brow, &m_y, &m_dir, &m_b, &m_l, &m_u, &m_mp, has_mp, alpha, y_out, mask_out,
+                                smem, acc, nullptr, 0);
     reduce_and_finish<6>(acc, R, [&](double* t) { fin_accept(t, true, S); });
 }
 
@@ -733,30 +751,16 @@ struct SrchLayout5 {
 };
 
 template <bool SB, bool BB, int MODE, int K>
-__global__ void __launch_bounds__(m4::kThreads, (K <= 2 ? 4 : 2))
-k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
-          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
-          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, int h0, double mu,
-          Scal* S, RedScratch R, int gp) {
+__device__ __forceinline__ int search_sweep5(const StencilOp& A, const BandGeom& G, const Bounds& Bd,
+                                             const double* __restrict__ brow, const CUtensorMap* m_y,
+                                             const CUtensorMap* m_dir, const CUtensorMap* m_b, const CUtensorMap* m_l,
+                                             const CUtensorMap* m_u, const double (&al)[K], unsigned char* smem,
+                                             double (&acc)[2 * K], uint64_t* bars, int k0) {
     using namespace m4;
     using L = SrchLayout5<SB, BB, MODE, K>;
-    constexpr bool use_alpha0 = MODE == m5::GP;
-    if (gp && *(volatile int*)&S->gp_done) return;
-    if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
-        if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
-        return;
-    }
-    const double base = use_alpha0 ? S->alpha0 : 1.0;
-    double al[K];
-#pragma unroll
-    for (int h = 0; h < K; ++h) al[h] = scalbn(base, -(h0 + h));
-    extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int c = 26 * wid + lane + 1;
     const bool out_lane = lane >= 3 && lane < 29;
-    double acc[2 * K];
-#pragma unroll
-    for (int s = 0; s < 2 * K; ++s) acc[s] = 0.0;
     int gx = 0, y0 = 0, y1 = 0;
     bool col_ok = false;
     Op5<true> op;
@@ -766,17 +770,17 @@ k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, c
     double s_a[K], s_b[K];                        // s_h at the s row - 1, - 2
 #pragma unroll
     for (int h = 0; h < K; ++h) { s_a[h] = 0.0; s_b[h] = 0.0; }
-    band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2>(
+    return band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, L::kStage);
             const int yt = yr - G.rlo;
-            tma_load_2d(st + L::kY, &m_y, x0 - 4, yt, bar);
-            if (MODE == m5::CG) tma_load_2d(st + L::kD, &m_dir, x0 - 4, yt, bar);
-            if (!BB) tma_load_2d(st + L::kB, &m_b, x0 - 4, yt, bar);
+            tma_load_2d(st + L::kY, m_y, x0 - 4, yt, bar);
+            if (MODE == m5::CG) tma_load_2d(st + L::kD, m_dir, x0 - 4, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, m_b, x0 - 4, yt, bar);
             if (!SB) {
-                tma_load_2d(st + L::kL, &m_l, x0 - 4, yt, bar);
-                tma_load_2d(st + L::kU, &m_u, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kL, m_l, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kU, m_u, x0 - 4, yt, bar);
             }
         },
         [&](int x0, int yb, int ye) {
@@ -828,7 +832,31 @@ k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, c
             g_e = g1;
             y_m2 = y_m1; y_m1 = yv;
             l_r1 = lv; u_r1 = uv; b_r1 = bv;
-        });
+        },
+        bars, k0);
+}
+
+template <bool SB, bool BB, int MODE, int K>
+__global__ void __launch_bounds__(m4::kThreads, (K <= 2 ? 4 : 2))
+k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
+          const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
+          const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, int h0, double mu,
+          Scal* S, RedScratch R, int gp) {
+    constexpr bool use_alpha0 = MODE == m5::GP;
+    if (gp && *(volatile int*)&S->gp_done) return;
+    if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
+        if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
+        return;
+    }
+    const double base = use_alpha0 ? S->alpha0 : 1.0;
+    double al[K];
+#pragma unroll
+    for (int h = 0; h < K; ++h) al[h] = scalbn(base, -(h0 + h));
+    extern __shared__ __align__(128) unsigned char smem[];
+    double acc[2 * K];
+#pragma unroll
+    for (int s = 0; s < 2 * K; ++s) acc[s] = 0.0;
+    search_sweep5<SB, BB, MODE, K>(A, G, Bd, brow, &m_y, &m_dir, &m_b, &m_l, &m_u, al, smem, acc, nullptr, 0);
     reduce_and_finish<2 * K>(acc, R, [&](double* tt) { fin_search(tt, K, h0, base, mu, S); });
 }
 
@@ -911,6 +939,118 @@ k5_cg_init(StencilOp A, BandGeom G, const double* __restrict__ brow, const __gri
             y_m2 = y_m1; y_m1 = yv; b_r1 = bv; m_r1 = mv;
         });
     reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
+}
+
+
+// ============================================================================
+// a1-a3 + a7: the whole GP phase as ONE persistent cooperative launch
+// (single slab, single rank, g-free sweeps).  Per GP step: search sweep (K = 2) ->
+// grid barrier -> every CTA sums the block partials in the same fixed order and takes
+// the Eq. gplsstop decision -> accept sweep -> grid barrier -> fin_accept sums ->
+// k_gp_step's stop rules (pgstop1, pgstop2, cap, convergence).  A first batch without
+// an acceptable step (or <d,Ad> <= 0) hands the step back to the host (GP_HOST), as the
+// graph path does.  y, mask ping-pong between buffers 0 / 1 starting from cur0.
+// ============================================================================
+template <int NS>
+__device__ __forceinline__ void grid_sum(double (&acc)[NS], double* part, unsigned int G_, unsigned int* gbar,
+                                         unsigned int& gen, double* red, double* tot) {
+    block_reduce<NS>(acc, red);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < NS; ++q) part[q * G_ + blockIdx.x] = acc[q];
+    grid_barrier(gbar, G_, gen);
+    double t[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) t[q] = 0.0;
+    for (unsigned int b = threadIdx.x; b < G_; b += blockDim.x)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) t[q] += __ldcg(part + q * G_ + b);
+    block_reduce<NS>(t, red);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < NS; ++q) tot[q] = t[q];
+    __syncthreads();
+}
+
+template <bool SB, bool BB>
+__global__ void __launch_bounds__(m4::kThreads, 4)
+k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __restrict__ brow,
+           const __grid_constant__ CUtensorMap m_y0, const __grid_constant__ CUtensorMap m_y1,
+           const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_l,
+           const __grid_constant__ CUtensorMap m_u, const __grid_constant__ CUtensorMap m_m0,
+           const __grid_constant__ CUtensorMap m_m1, double* __restrict__ y0p, double* __restrict__ y1p,
+           unsigned char* __restrict__ mk0, unsigned char* __restrict__ mk1, int cur0, double mu, Scal* S,
+           double* __restrict__ part, unsigned int* gbar) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[4];
+    __shared__ double red[6 * 32];
+    __shared__ double tot[6];
+    if (S->gp_done) return;
+    const double tau = S->gp_tau, eta1 = S->gp_eta1;
+    const long long gp_cap = S->gp_cap;
+    long long j = S->gp_j;
+    double maxdec = S->gp_maxdec, last_dec = S->gp_last_dec;
+    double alpha0 = S->alpha0;
+    int cauchy_ok = S->cauchy_ok;
+    double pg2 = S->pg2, g2 = S->g2, n_active = S->n_active, n_changed = S->n_changed, n_nb = S->n_nonbinding;
+    double dd = S->dd, dAd = S->dAd;
+    int s_h = S->s_h;
+    double s_alpha = S->s_alpha, s_delta = S->s_delta, s_gs = S->s_gs;
+    int done = 0, reason = GP_RUNNING;
+    const unsigned int G_ = gridDim.x;
+    unsigned int gen = 0;
+    int k = 0, red_i = 0;
+    int cur = cur0;
+    while (!done) {
+        if (!cauchy_ok) { s_h = -1; done = 1; reason = GP_HOST; break; }
+        // ---- search, alpha_h = alpha_0 2^-h, h = 0, 1
+        {
+            const double al[2] = {alpha0, scalbn(alpha0, -1)};
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            k = search_sweep5<SB, BB, m5::GP, 2>(A, Gs, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b,
+                                                 &m_l, &m_u, al, smem, acc, bars, k);
+            grid_sum<4>(acc, part + (red_i++ & 1) * 6 * G_, G_, gbar, gen, red, tot);
+            s_h = -1;
+            for (int h = 0; h < 2; ++h) {
+                const double gs = tot[2 * h], sAs = tot[2 * h + 1];
+                const double dq = gs + 0.5 * sAs;
+                if (dq <= mu * gs) {
+                    s_h = h;
+                    s_alpha = al[h];
+                    s_delta = dq;
+                    s_gs = gs;
+                    break;
+                }
+            }
+        }
+        if (s_h < 0) { done = 1; reason = GP_HOST; break; }
+        // ---- accept y' = P[y - s_alpha g], regrad sums, free mask, next Cauchy form
+        {
+            double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            k = accept_sweep5<SB, BB, m5::GP>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b, &m_l,
+                                              &m_u, cur ? &m_m1 : &m_m0, 1, s_alpha, cur ? y0p : y1p,
+                                              cur ? mk0 : mk1, smem, acc, bars, k);
+            grid_sum<6>(acc, part + (red_i++ & 1) * 6 * G_, G_, gbar, gen, red, tot);
+            pg2 = tot[0]; g2 = tot[1]; n_active = tot[2]; n_changed = tot[3]; n_nb = tot[4];
+            dd = tot[0]; dAd = tot[5];
+            cauchy_ok = (tot[5] > 0.0) ? 1 : 0;
+            alpha0 = (tot[5] > 0.0) ? tot[0] / tot[5] : 0.0;
+        }
+        cur ^= 1;
+        // ---- k_gp_step
+        ++j;
+        const double dec = -s_delta;
+        last_dec = dec;
+        const bool stop = (n_changed == 0.0) || (j >= 2 && dec <= eta1 * maxdec) || (j >= gp_cap);
+        if (dec > maxdec) maxdec = dec;
+        if (stop) { done = 1; reason = GP_STOP; }
+        else if (sqrt(pg2) <= tau) { done = 1; reason = GP_CONV; }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        S->pg2 = pg2; S->g2 = g2; S->n_active = n_active; S->n_changed = n_changed; S->n_nonbinding = n_nb;
+        S->dd = dd; S->dAd = dAd; S->cauchy_ok = cauchy_ok; S->alpha0 = alpha0;
+        S->s_h = s_h; S->s_alpha = s_alpha; S->s_delta = s_delta; S->s_gs = s_gs;
+        S->gp_j = j; S->gp_maxdec = maxdec; S->gp_last_dec = last_dec;
+        S->gp_done = done; S->gp_reason = reason;
+    }
 }
 
 }  // namespace gpcg
