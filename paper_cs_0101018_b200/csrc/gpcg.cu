@@ -187,6 +187,7 @@ struct Slab {
     CUtensorMap t4wo;
     CUtensorMap t4m[NMSK];
     BandGeom bg_cg{}, bg_acc{}, bg_srch{};   // band x segment items sized to each kernel's residency
+    unsigned char* cgflags = nullptr;         // k_cg_block_flags of the running CG call (bg_cg geometry)
     int grid4_cg = 1, grid4_acc = 1, grid4_srch = 1;
     // g-free sweeps (k5_*): 112-column boxes from x0 - 4, 128-byte mask boxes, 104-column bands
     CUtensorMap t5[NVEC];
@@ -241,6 +242,8 @@ struct gpcg_problem {
     bool gp_graph = true;           // GPCG_GP_GRAPH=0: host-driven GP steps (A/B)
     bool cg_persistent = true;      // GPCG_CG_PERSIST=0: CG as graph chunks instead of k6_cg_loop
     bool gp_persistent = true;      // GPCG_GP_PERSIST=0: GP phase as graph chunks instead of k6_gp_loop
+    bool cg_skip = true;            // GPCG_CG_SKIP=0: the CG sweep loads every block (no active-block skip)
+    bool gp_spec = true;            // GPCG_GP_SPEC=0: no speculative h = 0 accept in k6_gp_loop
     int grid6_gp = 1;
     size_t smem6_gp = 0;
     unsigned int* gbar = nullptr;   // grid-barrier counter of the persistent kernels
@@ -432,7 +435,8 @@ void free_all(gpcg_problem* h) {
     if (h->st) cudaStreamSynchronize(h->st);
     for (Slab& S : h->slabs) {
         if (S.arena) cudaFree(S.arena);
-        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.rp, (void*)S.ci, (void*)S.val,
+        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, (void*)S.rp,
+                        (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             if (p) cudaFree(p);
     }
@@ -601,6 +605,10 @@ int setup_tile(gpcg_problem* h) {
             grid = std::min(G.nbands * G.nsegs, resident);
         };
         band(r4cg, S.bg_cg, S.grid4_cg);
+        {
+            const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
+            CK(cudaMalloc(&S.cgflags, (size_t)std::max<long long>(nf, 1)));
+        }
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
         band(r5acc, S.bg5_acc, S.grid5_acc, m5::kOut);
@@ -670,6 +678,10 @@ int create_streams(gpcg_problem* h, void* stream) {
         h->cg_persistent = !(e2 && e2[0] == '0');
         const char* e3 = getenv("GPCG_GP_PERSIST");
         h->gp_persistent = !(e3 && e3[0] == '0');
+        const char* e4 = getenv("GPCG_CG_SKIP");
+        h->cg_skip = !(e4 && e4[0] == '0');
+        const char* e5 = getenv("GPCG_GP_SPEC");
+        h->gp_spec = !(e5 && e5[0] == '0');
     }
     CK(cudaMalloc(&h->gbar, sizeof(unsigned int)));
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
@@ -1027,6 +1039,7 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
     const bool pc = h->prm.precond == 1;
     const bool use_k4 = h->tile && (h->tile_mask & 8);
     const bool use_tile = h->tile && (h->tile_mask & 4) && !pc;      // k3 has no PCG variant
+    const bool skip = h->cg_skip;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
@@ -1034,11 +1047,11 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
             if (pc)
                 k4_cg_iter<true><<<S.grid4_cg, m4::kThreadsWS, m4cg::kSmem, h->st>>>(
                     S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
-                    h->dS, R);
+                    h->dS, R, skip ? S.cgflags : nullptr);
             else
                 k4_cg_iter<false><<<S.grid4_cg, m4::kThreadsWS, m4cg::kSmem, h->st>>>(
                     S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
-                    h->dS, R);
+                    h->dS, R, skip ? S.cgflags : nullptr);
         } else if (use_tile) {
             k3_cg_iter<2><<<S.grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
                 S.sop, S.tg, S.tm[vrho(a)], S.tm[vq(a)], S.tmWc, S.tmm[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
@@ -1145,10 +1158,12 @@ int launch_gp_loop(gpcg_problem* h, int cur) {
     CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
     Bounds B = h->bounds(S);
     double mu = h->prm.mu;
+    int spec = h->gp_spec ? 1 : 0;
     void* args[] = {(void*)&S.sop, (void*)&S.bg5_srch, (void*)&S.bg5_acc, (void*)&B, (void*)&S.brow,
                     (void*)&S.t5[VY0], (void*)&S.t5[VY1], (void*)&S.t5[VB], (void*)&S.t5[VL], (void*)&S.t5[VU],
                     (void*)&S.t5m[MK0], (void*)&S.t5m[MK1], (void*)&S.v[VY0], (void*)&S.v[VY1], (void*)&S.m[MK0],
-                    (void*)&S.m[MK1], (void*)&cur, (void*)&mu, (void*)&h->dS, (void*)&S.partials, (void*)&h->gbar};
+                    (void*)&S.m[MK1], (void*)&cur, (void*)&mu, (void*)&h->dS, (void*)&S.partials, (void*)&h->gbar,
+                    (void*)&spec};
     const void* fn;
     if (h->sb) fn = h->bb ? (const void*)k6_gp_loop<true, true> : (const void*)k6_gp_loop<true, false>;
     else fn = h->bb ? (const void*)k6_gp_loop<false, true> : (const void*)k6_gp_loop<false, false>;
@@ -1210,15 +1225,26 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     RC(finish_reduce(h, a, 2));
     if (!spec2d(h)) RC(exchange(h, {VRHO0, VQ0, VS0}, {MKCG}));
     else RC(exchange(h, {VRHO0, VQ0}, {MKCG}));
+    if (h->tile && (h->tile_mask & 8) && h->cg_skip) {
+        for (Slab& S : h->slabs) {
+            const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
+            const int g = (int)std::min<long long>((nf + 255) / 256, (long long)h->sms * 8);
+            k_cg_block_flags<<<std::max(g, 1), 256, 0, h->st>>>(h->nx, h->pitch, S.bg_cg, S.m[MKCG], S.rows + S.ghi,
+                                                                S.cgflags);
+            h->launches++;
+            CKLAUNCH();
+        }
+    }
     if (h->cg_persistent && h->tile && (h->tile_mask & 8) && !has_ghosts(h)) {
         // one cooperative launch runs the whole CG call (k6_cg_loop)
         Slab& S = h->slabs[0];
+        const unsigned char* flags = h->cg_skip ? S.cgflags : nullptr;
         CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
         CK(cudaEventRecord(h->ev_c0, h->st));
         void* args[] = {(void*)&S.sop, (void*)&S.bg_cg, (void*)&S.t4[VRHO0], (void*)&S.t4[VRHO1], (void*)&S.t4[VQ0],
                         (void*)&S.t4[VQ1], (void*)&S.t4wo, (void*)&S.t4m[MKCG], (void*)&S.v[VRHO0],
                         (void*)&S.v[VRHO1], (void*)&S.v[VQ0], (void*)&S.v[VQ1], (void*)&S.v[VW], (void*)&h->dS,
-                        (void*)&S.partials, (void*)&h->gbar};
+                        (void*)&S.partials, (void*)&h->gbar, (void*)&flags};
         const void* fn = h->prm.precond == 1 ? (const void*)k6_cg_loop<true> : (const void*)k6_cg_loop<false>;
         CK(cudaLaunchCooperativeKernel(fn, dim3(S.grid4_cg), dim3(m4::kThreadsWS), args, (size_t)m4cg::kSmem, h->st));
         CK(cudaEventRecord(h->ev_c1, h->st));
@@ -1935,9 +1961,11 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                     jdone = jn;
                     if (!S.gp_done) continue;
                     if (S.gp_reason != GP_HOST) break;
-                    // the first search batch found no step: the host finishes this step
+                    // the first search batch found no step: the host finishes this step (the persistent
+                    // kernel reports the first step size index it has not tried in s_pad)
                     int hacc = -1;
-                    if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc, first_k(h)))) goto fail;
+                    const int hstart = persist ? std::max(S.s_pad, 0) : first_k(h);
+                    if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc, hstart))) goto fail;
                     cur ^= 1;
                     const long long j = jdone + 1;
                     jdone = j;

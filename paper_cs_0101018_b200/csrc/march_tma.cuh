@@ -67,9 +67,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // k0: blocks this CTA already streamed through the same barriers (a persistent kernel
 // calls the engine once per sweep; the mbarriers are initialised at k0 = 0 only and
 // their phases continue).  Returns the CTA's block count after the sweep.
+// flags (nullable): one byte per (item, block) -- bit 0: the block's raw rows hold a free
+// point, bit 1: its emitted rows do -- passed to issue_loads so that all-active blocks skip
+// the loads their rows never read (3 = load everything).
 template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
 __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
-                                                Begin&& begin, Row&& row, int k0 = 0) {
+                                                Begin&& begin, Row&& row, int k0 = 0,
+                                                const unsigned char* __restrict__ flags = nullptr) {
     using namespace m4;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     uint64_t* empty = full + NST;
@@ -88,17 +92,19 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
         __syncthreads();
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == kWarps) {                                 // producer
-        if (lane == 0) {
-            int k = k0;
-            for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
-                const int x0 = (t % G.nbands) * OUT;
-                const int yb = (t / G.nbands) * G.seg - PRE;
-                for (int b = 0; b < nblk; ++b, ++k) {
-                    const int stage = k % NST;
-                    if (k >= NST) mbar_wait(&empty[stage], ((k / NST) - 1) & 1);
-                    issue_loads(smem + stage * STAGE, x0, yb + b * kBR, &full[stage]);
-                }
+    if (warp == kWarps) {                                 // producer (lane 0 issues; the warp fetches flags)
+        int k = k0;
+        for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
+            const int x0 = (t % G.nbands) * OUT;
+            const int yb = (t / G.nbands) * G.seg - PRE;
+            int f = 3;
+            for (int b = 0; b < nblk; ++b, ++k) {
+                if (flags && (b & 31) == 0) f = (b + lane < nblk) ? __ldg(flags + (long long)t * nblk + b + lane) : 3;
+                const int fb = flags ? __shfl_sync(0xffffffffu, f, b & 31) : 3;
+                const int stage = k % NST;
+                if (k >= NST) mbar_wait(&empty[stage], ((k / NST) - 1) & 1);
+                if (lane == 0) issue_loads(smem + stage * STAGE, x0, yb + b * kBR, &full[stage], fb);
+                __syncwarp();
             }
         }
         return k0 + nmine;
@@ -197,7 +203,8 @@ template <bool PC>
 __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, const CUtensorMap* m_rho,
                                          const CUtensorMap* m_p, const CUtensorMap* m_w, const CUtensorMap* m_mask,
                                          double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out,
-                                         double alpha, double beta, unsigned char* smem, double (&acc)[2], int k0) {
+                                         double alpha, double beta, unsigned char* smem, double (&acc)[2], int k0,
+                                         const unsigned char* __restrict__ flags = nullptr) {
     using namespace m4cg;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int c = 28 * wid + lane;                        // box column of this lane
@@ -209,11 +216,15 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
     unsigned char m_m1 = 0, m_m2 = 0;
     return band_pipeline_ws<kNST, kStage>(
         G, A.ny, smem,
-        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
-            mbar_expect_tx(bar, kTx);
-            tma_load_2d(st + kRho, m_rho, x0 - 2, yr - G.rlo, bar);
-            tma_load_2d(st + kP, m_p, x0 - 2, yr - G.rlo, bar);
-            tma_load_2d(st + kW, m_w, x0, yr - 2 - G.rlo, bar);      // w of the emitted rows (r - 2)
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar, int fb) {
+            // rho / p are read only at free points of the raw rows, w only at free emitted rows:
+            // blocks without any (flags bit 0 / bit 1) skip those loads (stale smem is never read)
+            mbar_expect_tx(bar, kUt + ((fb & 1) ? 2 * kF : 0) + ((fb & 2) ? kFo : 0));
+            if (fb & 1) {
+                tma_load_2d(st + kRho, m_rho, x0 - 2, yr - G.rlo, bar);
+                tma_load_2d(st + kP, m_p, x0 - 2, yr - G.rlo, bar);
+            }
+            if (fb & 2) tma_load_2d(st + kW, m_w, x0, yr - 2 - G.rlo, bar);      // w of the emitted rows (r - 2)
             tma_load_2d(st + kM, m_mask, floor16(x0 - 2), yr - G.rlo, bar);
         },
         [&](int x0, int yb, int ye) {
@@ -254,19 +265,47 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
             rn_m3 = rn_m2; rn_m2 = rn1;
             rr_m2 = rr1;
         },
-        k0);
+        k0, flags);
+}
+
+// Block flags of the CG sweep geometry G for the fixed CG mask: bit 0 if rows [yr, yr+4) of
+// the block's box columns [x0-2, x0+114) hold a free point, bit 1 if rows [yr-2, yr+2) of its
+// output columns [x0, x0+112) do.  One thread per (item, block).
+__global__ void k_cg_block_flags(int nx, int pitch, BandGeom G, const unsigned char* __restrict__ mask, int rhi,
+                                 unsigned char* __restrict__ flags) {
+    using namespace m4;
+    const int nblk = (G.seg + 4 + kBR - 1) / kBR;
+    const long long total = (long long)G.nbands * G.nsegs * nblk;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total; q += (long long)gridDim.x * blockDim.x) {
+        const int t = (int)(q / nblk), b = (int)(q - (long long)t * nblk);
+        const int x0 = (t % G.nbands) * kOut;
+        const int yr = (t / G.nbands) * G.seg - 2 + b * kBR;
+        int f = 0;
+        for (int r = max(yr - 2, G.rlo); r < min(yr + kBR, rhi); ++r) {
+            const unsigned char* row = mask + (long long)r * pitch;
+            const bool in_data = r >= yr, in_w = r < yr + kBR - 2;
+            for (int c = max(x0 - 2, 0); c < min(x0 + kOut + 2, nx); ++c) {
+                if (!row[c]) continue;
+                if (in_data) f |= 1;
+                if (in_w && c >= x0 && c < x0 + kOut) f |= 2;
+            }
+            if (f == 3) break;
+        }
+        flags[q] = (unsigned char)f;
+    }
 }
 
 template <bool PC>     // point-Jacobi PCG as in k2_cg_iter<BC, true>
 __global__ void __launch_bounds__(m4::kThreadsWS, 4)
 k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, const __grid_constant__ CUtensorMap m_p,
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
-           double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R) {
+           double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R,
+           const unsigned char* __restrict__ flags) {
     if (*(volatile int*)&S->cg_done) return;
     const double alpha = S->cg_alpha, beta = S->cg_beta;
     extern __shared__ __align__(128) unsigned char smem[];
     double acc[2] = {0.0, 0.0};
-    cg_sweep4<PC>(A, G, &m_rho, &m_p, &m_w, &m_mask, rho_n, p_n, w_out, alpha, beta, smem, acc, 0);
+    cg_sweep4<PC>(A, G, &m_rho, &m_p, &m_w, &m_mask, rho_n, p_n, w_out, alpha, beta, smem, acc, 0, flags);
     reduce_and_finish<2>(acc, R, [&](double* tt) { cg_finalize(tt[0], tt[1], S); });
 }
 
@@ -301,7 +340,8 @@ k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, 
            const __grid_constant__ CUtensorMap m_p0, const __grid_constant__ CUtensorMap m_p1,
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
            double* __restrict__ rho0, double* __restrict__ rho1, double* __restrict__ p0, double* __restrict__ p1,
-           double* __restrict__ w_out, Scal* S, double* __restrict__ part, unsigned int* gbar) {
+           double* __restrict__ w_out, Scal* S, double* __restrict__ part, unsigned int* gbar,
+           const unsigned char* __restrict__ flags) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[2 * 32];
     __shared__ double tot[2];
@@ -318,7 +358,7 @@ k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, 
         const int a = (int)(it & 1);
         double acc[2] = {0.0, 0.0};
         k = cg_sweep4<PC>(A, G, a ? &m_rho1 : &m_rho0, a ? &m_p1 : &m_p0, &m_w, &m_mask, a ? rho0 : rho1,
-                          a ? p0 : p1, w_out, alpha, beta, smem, acc, k);
+                          a ? p0 : p1, w_out, alpha, beta, smem, acc, k, flags);
         // block partials -> part[parity][s][block]
         block_reduce<2>(acc, red);
         double* pp = part + (it & 1) * 2 * G_;
@@ -942,6 +982,105 @@ k5_cg_init(StencilOp A, BandGeom G, const double* __restrict__ brow, const __gri
 }
 
 
+// Speculative GP step (used by k6_gp_loop): the accept sweep of the GP mode at the first
+// step size alpha_0, which also accumulates the h = 0 search sums <g, s> and <s, A s>
+// (s = yn - y, A s applied to s exactly as search_sweep5 does).  If Eq. gplsstop accepts
+// h = 0 -- the common case -- the step costs one sweep instead of two; otherwise the caller
+// discards y_out / mask_out and runs search (h >= 1) + accept.  acc: the six accept sums,
+// then <g, s>, <s, A s>.
+template <bool SB, bool BB>
+__device__ __forceinline__ int spec_sweep5(const StencilOp& A, const BandGeom& G, const Bounds& Bd,
+                                           const double* __restrict__ brow, const CUtensorMap* m_y,
+                                           const CUtensorMap* m_b, const CUtensorMap* m_l, const CUtensorMap* m_u,
+                                           const CUtensorMap* m_mp, double alpha, double* __restrict__ y_out,
+                                           unsigned char* __restrict__ mask_out, unsigned char* smem,
+                                           double (&acc)[8], uint64_t* bars, int k0) {
+    using namespace m4;
+    using L = AccLayout5<SB, BB, m5::GP>;
+    constexpr int LAG = L::kLag;                  // 3: emitted row = raw row - 3
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 26 * wid + lane + 1;
+    const bool out_lane = lane >= 3 && lane < 29;
+    int gx = 0, moff = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double bcol = 0.0;
+    double y_m1 = 0.0, y_m2 = 0.0, l_r1 = 0.0, u_r1 = 0.0, b_r1 = 0.0;
+    double yn_a = 0.0, yn_b = 0.0, l_a = 0.0, u_a = 0.0, b_a = 0.0, d_a = 0.0, d_b = 0.0;
+    double yn_e = 0.0, gn_e = 0.0, l_e = 0.0, u_e = 0.0;
+    double s_a = 0.0, s_b = 0.0;                  // s(r-2), s(r-3)
+    double g_a = 0.0, g_b = 0.0;                  // g(r-2), g(r-3)
+    double as_p = 0.0;                            // (A s)(r-3), from the previous row step
+    const uint32_t tx = L::kMP + m5::kUt;
+    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, tx);
+            const int yt = yr - G.rlo;
+            tma_load_2d(st + L::kY, m_y, x0 - 4, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, m_b, x0 - 4, yt, bar);
+            if (!SB) {
+                tma_load_2d(st + L::kL, m_l, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kU, m_u, x0 - 4, yt, bar);
+            }
+            tma_load_2d(st + L::kMP, m_mp, floor16(x0 - 4), yt - LAG, bar);
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 3 + 26 * wid + lane;
+            moff = (x0 - 4) - floor16(x0 - 4);
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
+            y_m1 = y_m2 = l_r1 = u_r1 = b_r1 = yn_a = yn_b = l_a = u_a = b_a = d_a = d_b = 0.0;
+            yn_e = gn_e = l_e = u_e = s_a = s_b = g_a = g_b = as_p = 0.0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const int q = kk * m5::kBW + c;
+            const bool rin = r >= A.rlo && r < A.rhi;
+            const bool in = col_ok && rin;
+            const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
+            const double bv = BB ? (rin ? bcol : 0.0) : reinterpret_cast<const double*>(st + L::kB)[q];
+            const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
+            const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
+            const double g1 = op.apply(A, r - 1, y_m1, y_m2, yv) - b_r1;     // g(r-1)
+            const double yn = trial(y_m1, g1, -1.0, alpha, l_r1, u_r1);      // yn(r-1)
+            const double s1 = yn - y_m1;                                      // s(r-1)
+            const double as2 = op.apply(A, r - 2, s_a, s_b, s1);              // (A s)(r-2)
+            const double gn1 = op.apply(A, r - 2, yn_a, yn_b, yn) - b_a;      // gn(r-2)
+            const double d1 = pgrad(yn_a, gn1, l_a, u_a);                     // d(r-2)
+            const double ad = op.apply(A, r - 3, d_a, d_b, d1);               // (A d)(r-3)
+            const int re = r - 3;
+            if (out_lane && col_ok && re >= y0 && re < y1) {
+                const long long v = (long long)gx + (long long)A.pitch * re;
+                y_out[v] = yn_e;
+                const bool act = (yn_e == l_e) || (yn_e == u_e);
+                const unsigned char m = act ? 0 : 1;
+                mask_out[v] = m;
+                acc[0] = fma(d_a, d_a, acc[0]);
+                acc[1] = fma(gn_e, gn_e, acc[1]);
+                acc[2] += act ? 1.0 : 0.0;
+                acc[3] += (st[L::kMP + kk * m5::kMW + c + moff] != m) ? 1.0 : 0.0;
+                const bool binding = (yn_e == l_e && gn_e >= 0.0) || (yn_e == u_e && gn_e <= 0.0);
+                acc[4] += (act && !binding) ? 1.0 : 0.0;
+                acc[5] = fma(d_a, ad, acc[5]);
+                acc[6] = fma(g_b, s_b, acc[6]);                               // <g, s>(r-3)
+                acc[7] = fma(s_b, as_p, acc[7]);                              // <s, A s>(r-3)
+            }
+            yn_e = yn_a; gn_e = gn1; l_e = l_a; u_e = u_a;
+            d_b = d_a; d_a = d1;
+            yn_b = yn_a; yn_a = yn;
+            l_a = l_r1; u_a = u_r1; b_a = b_r1;
+            s_b = s_a; s_a = s1;
+            g_b = g_a; g_a = g1;
+            as_p = as2;
+            y_m2 = y_m1; y_m1 = yv;
+            l_r1 = lv; u_r1 = uv; b_r1 = bv;
+        },
+        bars, k0);
+}
+
 // ============================================================================
 // a1-a3 + a7: the whole GP phase as ONE persistent cooperative launch
 // (single slab, single rank, g-free sweeps).  Per GP step: search sweep (K = 2) ->
@@ -978,11 +1117,11 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
            const __grid_constant__ CUtensorMap m_u, const __grid_constant__ CUtensorMap m_m0,
            const __grid_constant__ CUtensorMap m_m1, double* __restrict__ y0p, double* __restrict__ y1p,
            unsigned char* __restrict__ mk0, unsigned char* __restrict__ mk1, int cur0, double mu, Scal* S,
-           double* __restrict__ part, unsigned int* gbar) {
+           double* __restrict__ part, unsigned int* gbar, int spec) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[4];
-    __shared__ double red[6 * 32];
-    __shared__ double tot[6];
+    __shared__ double red[8 * 32];
+    __shared__ double tot[8];
     if (S->gp_done) return;
     const double tau = S->gp_tau, eta1 = S->gp_eta1;
     const long long gp_cap = S->gp_cap;
@@ -995,45 +1134,59 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
     int s_h = S->s_h;
     double s_alpha = S->s_alpha, s_delta = S->s_delta, s_gs = S->s_gs;
     int done = 0, reason = GP_RUNNING;
+    int s_spec = 0;                               // GP_HOST: the first step size index still to try
     const unsigned int G_ = gridDim.x;
     unsigned int gen = 0;
     int k = 0, red_i = 0;
     int cur = cur0;
     while (!done) {
         if (!cauchy_ok) { s_h = -1; done = 1; reason = GP_HOST; break; }
-        // ---- search, alpha_h = alpha_0 2^-h, h = 0, 1
-        {
-            const double al[2] = {alpha0, scalbn(alpha0, -1)};
+        bool have_accept = false;
+        if (spec) {
+            // speculative accept at alpha_0 with the h = 0 search sums (one sweep when accepted)
+            double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            k = spec_sweep5<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u, cur ? &m_m1 : &m_m0,
+                                    alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc, bars, k);
+            grid_sum<8>(acc, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
+            const double gs = tot[6], sAs = tot[7];
+            const double dq = gs + 0.5 * sAs;
+            if (dq <= mu * gs) {                         // Eq. gplsstop at h = 0
+                s_h = 0; s_alpha = alpha0; s_delta = dq; s_gs = gs;
+                have_accept = true;
+            }
+        }
+        if (!have_accept) {
+            // ---- search, alpha_h = alpha_0 2^-h for the next two h
+            const int h0 = spec ? 1 : 0;
+            const double al[2] = {scalbn(alpha0, -h0), scalbn(alpha0, -(h0 + 1))};
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             k = search_sweep5<SB, BB, m5::GP, 2>(A, Gs, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b,
                                                  &m_l, &m_u, al, smem, acc, bars, k);
-            grid_sum<4>(acc, part + (red_i++ & 1) * 6 * G_, G_, gbar, gen, red, tot);
+            grid_sum<4>(acc, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
             s_h = -1;
             for (int h = 0; h < 2; ++h) {
                 const double gs = tot[2 * h], sAs = tot[2 * h + 1];
                 const double dq = gs + 0.5 * sAs;
                 if (dq <= mu * gs) {
-                    s_h = h;
+                    s_h = h0 + h;
                     s_alpha = al[h];
                     s_delta = dq;
                     s_gs = gs;
                     break;
                 }
             }
-        }
-        if (s_h < 0) { done = 1; reason = GP_HOST; break; }
-        // ---- accept y' = P[y - s_alpha g], regrad sums, free mask, next Cauchy form
-        {
-            double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            if (s_h < 0) { s_h = -1; s_spec = h0 + 2; done = 1; reason = GP_HOST; break; }
+            // ---- accept y' = P[y - s_alpha g], regrad sums, free mask, next Cauchy form
+            double acc6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             k = accept_sweep5<SB, BB, m5::GP>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b, &m_l,
                                               &m_u, cur ? &m_m1 : &m_m0, 1, s_alpha, cur ? y0p : y1p,
-                                              cur ? mk0 : mk1, smem, acc, bars, k);
-            grid_sum<6>(acc, part + (red_i++ & 1) * 6 * G_, G_, gbar, gen, red, tot);
-            pg2 = tot[0]; g2 = tot[1]; n_active = tot[2]; n_changed = tot[3]; n_nb = tot[4];
-            dd = tot[0]; dAd = tot[5];
-            cauchy_ok = (tot[5] > 0.0) ? 1 : 0;
-            alpha0 = (tot[5] > 0.0) ? tot[0] / tot[5] : 0.0;
+                                              cur ? mk0 : mk1, smem, acc6, bars, k);
+            grid_sum<6>(acc6, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
         }
+        pg2 = tot[0]; g2 = tot[1]; n_active = tot[2]; n_changed = tot[3]; n_nb = tot[4];
+        dd = tot[0]; dAd = tot[5];
+        cauchy_ok = (tot[5] > 0.0) ? 1 : 0;
+        alpha0 = (tot[5] > 0.0) ? tot[0] / tot[5] : 0.0;
         cur ^= 1;
         // ---- k_gp_step
         ++j;
@@ -1050,6 +1203,7 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
         S->s_h = s_h; S->s_alpha = s_alpha; S->s_delta = s_delta; S->s_gs = s_gs;
         S->gp_j = j; S->gp_maxdec = maxdec; S->gp_last_dec = last_dec;
         S->gp_done = done; S->gp_reason = reason;
+        S->s_pad = s_spec;                         // GP_HOST after a search: resume the search at h = s_spec
     }
 }
 

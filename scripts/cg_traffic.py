@@ -3,7 +3,7 @@
 progress test effectively off (eta2 = 1e-10), so `ncu -k regex:k6_cg_loop -c 1` sees a
 launch of exactly CAP iterations (checked: the first call's count is printed).
 
-usage: python scripts/cg_traffic.py [CAP]
+usage: python scripts/cg_traffic.py [CAP] [CONFIG]
 """
 import os
 import sys
@@ -13,7 +13,7 @@ import torch  # noqa: E402
 from paper_cs_0101018_b200 import problems as P, gpcg  # noqa: E402
 
 CAP = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-prob = P.c2()
+prob = P.get(sys.argv[2] if len(sys.argv) > 2 else "C2")
 s = gpcg.Solver.from_problem(prob, device="cuda")
 s.set_params(cg_cap=CAP, eta2=1e-10, refine_cap=1)
 x0 = torch.zeros(prob.n, dtype=torch.float64, device="cuda")

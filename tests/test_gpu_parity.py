@@ -408,3 +408,23 @@ def test_stencil3d_full_c4_matches_csr_golden(G):
     assert abs(st["q"] - gold["q"]) <= 1e-10 * abs(gold["q"])
     idx = np.asarray(gold["idx"])
     assert np.max(np.abs(x[idx] - np.asarray(gold["x"]))) <= 1e-7
+
+
+# ------------------------------------------------------------------ edge grids for the band kernels
+# (bands of 112 / 104 columns, row segments, persistent cooperative loops): widths that leave a
+# partial band, a single column / row, fewer rows than a pipeline block.
+@pytest.mark.parametrize("nx,ny", [(1, 37), (37, 1), (2, 2), (113, 9), (105, 41), (230, 3), (224, 17)])
+def test_band_kernels_edge_grids(G, oracle, nx, ny):
+    prob = P.journal_bearing(nx, ny, eps=0.5)
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=-1e-12)
+    for pc in (0, 1):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(precond=pc)
+            rc, x, st = s.solve(prob.x0, -1e-12)
+            p = 2.0 * P.uniform(95, 1, prob.n) - 1.0
+            y = s.hessvec(p)
+        assert rc == 0 and rc_o == 0, (rc, st)
+        A = oracle.problem_csr(prob)
+        spmv_close(y, oracle.spmv(A, p), abs_op(A, p))
+        assert abs(st["q"] - st_o["q"]) <= 1e-10 * max(abs(st_o["q"]), 1e-300)
+        assert np.max(np.abs(x - x_o)) <= 1e-7
