@@ -7,6 +7,6 @@ timeout 300 python scripts/diag.py C2 > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python scripts/diag.py C2 > gpurun_out/ncu_ll.log 2>&1
 echo "ll rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k6_" -s 40 -c 2 -o gpurun_out/prof_${TAG} \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k6_" -s 60 -c 2 -o gpurun_out/prof_${TAG} \
     python scripts/diag.py C2 > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
