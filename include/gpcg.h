@@ -118,7 +118,7 @@ GPCG_API gpcg_params gpcg_params_default(void);
  * rows in rank order (rank 0 first).  Every rank calls every function with its
  * own slab (same sequence on all ranks); user arrays hold the rank's rows only.
  * Each operator application reads ghost rows of the neighbouring ranks
- * (stencil: 2 grid rows; CSR: the band of rows its columns reach -- columns of
+ * (stencil2d: 3 grid rows; stencil3d: 1 plane; CSR: the band of rows its columns reach -- columns of
  * a rank may only refer to rows of itself and of ranks r-1, r+1), exchanged by
  * NCCL send/recv after every sweep that writes a vector a neighbour reads, and
  * every global sum is one ncclAllReduce (one per CG iteration, one per search
@@ -132,8 +132,8 @@ GPCG_API gpcg_params gpcg_params_default(void);
  *                 copies and summing slab totals in slab order -- the same
  *                 arithmetic as nranks * local_slabs ranks (used to test the
  *                 slab path on one GPU).
- * Errors: GPCG_EINVAL for a bad range or a slab of < 2 stencil rows (< 1 CSR
- * row) or a CSR band beyond the neighbouring slab; GPCG_ENCCL if NCCL fails.
+ * Errors: GPCG_EINVAL for a bad range or a slab of < 3 stencil2d rows (< 1 plane
+ * / CSR row) or a CSR band beyond the neighbouring slab; GPCG_ENCCL if NCCL fails.
  */
 typedef struct {
     int32_t rank, nranks;

@@ -1228,7 +1228,7 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     if (h->tile && (h->tile_mask & 8) && h->cg_skip) {
         for (Slab& S : h->slabs) {
             const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
-            const int g = (int)std::min<long long>((nf + 255) / 256, (long long)h->sms * 8);
+            const int g = (int)std::min<long long>((nf * 32 + 255) / 256, (long long)h->sms * 8);
             k_cg_block_flags<<<std::max(g, 1), 256, 0, h->st>>>(h->nx, h->pitch, S.bg_cg, S.m[MKCG], S.rows + S.ghi,
                                                                 S.cgflags);
             h->launches++;
@@ -1450,7 +1450,9 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
     int rc;
     if ((rc = create_streams(h, stream))) return fail(rc);
     if ((rc = setup_comm(h, dist))) return fail(rc);
-    if ((rc = layout_slabs(h, re - rb, nsl, 2))) return fail(rc);
+    // ghost rows: 3 -- the g-free GP accept sweep (k5, march_tma.cuh) applies the operator three
+    // times on top of y (g, A yn, A d), the other sweeps twice
+    if ((rc = layout_slabs(h, re - rb, nsl, 3))) return fail(rc);
     if ((rc = create_vectors(h, b, l, u))) return fail(rc);
     h->c = c;
     if ((rc = setup_stencil_slabs(h, wx, wy, shift))) return fail(rc);

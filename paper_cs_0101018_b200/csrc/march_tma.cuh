@@ -270,28 +270,31 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
 
 // Block flags of the CG sweep geometry G for the fixed CG mask: bit 0 if rows [yr, yr+4) of
 // the block's box columns [x0-2, x0+114) hold a free point, bit 1 if rows [yr-2, yr+2) of its
-// output columns [x0, x0+112) do.  One thread per (item, block).
+// output columns [x0, x0+112) do.  One warp per (item, block); lanes stride the columns.
 __global__ void k_cg_block_flags(int nx, int pitch, BandGeom G, const unsigned char* __restrict__ mask, int rhi,
                                  unsigned char* __restrict__ flags) {
     using namespace m4;
     const int nblk = (G.seg + 4 + kBR - 1) / kBR;
     const long long total = (long long)G.nbands * G.nsegs * nblk;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total; q += (long long)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long q = w0; q < total; q += nw) {
         const int t = (int)(q / nblk), b = (int)(q - (long long)t * nblk);
         const int x0 = (t % G.nbands) * kOut;
         const int yr = (t / G.nbands) * G.seg - 2 + b * kBR;
-        int f = 0;
+        int fd = 0, fw = 0;
         for (int r = max(yr - 2, G.rlo); r < min(yr + kBR, rhi); ++r) {
             const unsigned char* row = mask + (long long)r * pitch;
-            const bool in_data = r >= yr, in_w = r < yr + kBR - 2;
-            for (int c = max(x0 - 2, 0); c < min(x0 + kOut + 2, nx); ++c) {
-                if (!row[c]) continue;
-                if (in_data) f |= 1;
-                if (in_w && c >= x0 && c < x0 + kOut) f |= 2;
+            for (int c = x0 - 2 + lane; c < x0 + kOut + 2; c += 32) {
+                if (c < 0 || c >= nx || !row[c]) continue;
+                if (r >= yr) fd = 1;
+                if (r < yr + kBR - 2 && c >= x0 && c < x0 + kOut) fw = 1;
             }
-            if (f == 3) break;
         }
-        flags[q] = (unsigned char)f;
+        fd = __any_sync(0xffffffffu, fd);
+        fw = __any_sync(0xffffffffu, fw);
+        if (lane == 0) flags[q] = (unsigned char)(fd | (fw << 1));
     }
 }
 
