@@ -83,6 +83,10 @@ typedef struct {
     int32_t gp_chunk;    /* GP steps per graph launch between host polls: 8                */
     int32_t precond;     /* 0: plain CG on A_k (the hot path); 1: point-Jacobi PCG with
                             M = diag(A_k) (Table 4 "Diagonal")                 */
+    int32_t cg_mode;     /* 0: A_k applied in place on masked full-length vectors (the hot
+                            path, P:680-683's "alternative technique"); 1: A_k extracted
+                            as a compact CSR matrix each CG call, as the paper does with
+                            PETSc -- the extraction ablation; one slab / rank */
 } gpcg_params;
 
 typedef struct {
@@ -105,6 +109,7 @@ typedef struct {
      * t_cg_timed_ms of device time; cg_free_iters_timed = sum of |F| over them. */
     int64_t cg_iters_timed, cg_free_iters_timed;
     double t_cg_timed_ms;
+    double t_extract_ms;   /* cg_mode = 1: device time spent building A_F and r_F          */
 } gpcg_stats;
 
 GPCG_API gpcg_params gpcg_params_default(void);

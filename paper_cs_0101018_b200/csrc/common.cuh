@@ -46,6 +46,7 @@ struct StencilOp {
     int rlo, rhi;                      // readable rows (owned + ghost); outside: Dirichlet zero
 
     __device__ __forceinline__ int num_units() const { return ((nx + 31) >> 5) * ((ny + 7) >> 3); }
+    __device__ __forceinline__ Pt point(int v) const { return Pt{v, v % pitch, v / pitch, 0}; }
 
     template <class Body>
     __device__ __forceinline__ void for_each_point(Body&& body) const {
@@ -87,6 +88,7 @@ struct CsrOp {
     const double* __restrict__ val;
 
     __device__ __forceinline__ int num_units() const { return (n + kThreads - 1) / kThreads; }
+    __device__ __forceinline__ Pt point(int v) const { return Pt{v, 0, 0, 0}; }
 
     template <class Body>
     __device__ __forceinline__ void for_each_point(Body&& body) const {
@@ -117,6 +119,10 @@ struct Stencil3Op {
 
     __device__ __forceinline__ int num_units() const {
         return (int)((plane * nz + kThreads - 1) / kThreads);
+    }
+    __device__ __forceinline__ Pt point(int v) const {
+        const int k = v / (int)plane, r = v - k * (int)plane;
+        return Pt{v, r % nx, r / nx, k};
     }
 
     template <class Body>

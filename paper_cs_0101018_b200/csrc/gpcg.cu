@@ -40,6 +40,7 @@
 #include "march.cuh"
 #include "tile.cuh"
 #include "march_tma.cuh"
+#include "extract.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -188,6 +189,13 @@ struct Slab {
     CUtensorMap t4m[NMSK];
     BandGeom bg_cg{}, bg_acc{}, bg_srch{};   // band x segment items sized to each kernel's residency
     unsigned char* cgflags = nullptr;         // k_cg_block_flags of the running CG call (bg_cg geometry)
+    // explicit extraction (cg_mode = 1): compact numbering, A_F in CSR, compact CG vectors
+    void* xarena = nullptr;
+    int *xidx = nullptr, *xpos = nullptr, *xcnt = nullptr, *xcol = nullptr;
+    long long *xblk = nullptr, *xtot = nullptr, *xrp = nullptr;
+    double* xval = nullptr;
+    double* xv[12] = {};                      // gF, dinvF, rho x2, q x2, s x2, p, w, (spare)
+    unsigned char *xmask = nullptr, *xmaskcg = nullptr;
     int grid4_cg = 1, grid4_acc = 1, grid4_srch = 1;
     // g-free sweeps (k5_*): 112-column boxes from x0 - 4, 128-byte mask boxes, 104-column bands
     CUtensorMap t5[NVEC];
@@ -250,6 +258,7 @@ struct gpcg_problem {
     long long launches = 0;
     long long cg_iters_timed = 0, cg_free_iters_timed = 0;
     double t_cg_timed_ms = 0.0;
+    double t_extract_ms = 0.0;
 
     int nslabs() const { return (int)slabs.size(); }
     RedScratch red(int s) const {
@@ -435,7 +444,7 @@ void free_all(gpcg_problem* h) {
     if (h->st) cudaStreamSynchronize(h->st);
     for (Slab& S : h->slabs) {
         if (S.arena) cudaFree(S.arena);
-        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, (void*)S.rp,
+        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, S.xarena, (void*)S.rp,
                         (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             if (p) cudaFree(p);
@@ -1179,8 +1188,143 @@ int launches_per_cg_iter(const gpcg_problem* h) {
     return n;
 }
 
+// ---------------------------------------------------------------- explicit extraction (cg_mode = 1)
+// The extraction ablation (the paper's MatGetSubMatrix route):
+// build A_F = Z'AZ as an m x m CSR and r_F, run CG on the compact system with the CSR kernels,
+// scatter w back.  One slab, one rank.
+int ensure_extract_buffers(gpcg_problem* h, Slab& S) {
+    if (S.xarena) return GPCG_OK;
+    const long long n = S.rows * (long long)h->rowlen;
+    long long nnzmax = 0;                     // stored entries of the operator bound those of A_F
+    if (h->is_csr) {
+        long long last = 0;
+        CK(cudaMemcpy(&last, S.rp + S.rows, sizeof(long long), cudaMemcpyDeviceToHost));
+        nnzmax = last;
+    } else {
+        nnzmax = (h->is3d ? 7 : 5) * n;
+    }
+    const long long nblk = (n + kScanBlock - 1) / kScanBlock;
+    auto r256 = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t b_idx = r256((size_t)S.nalloc * 4), b_pos = r256((size_t)n * 4), b_cnt = r256((size_t)n * 4);
+    const size_t b_col = r256((size_t)nnzmax * 4), b_blk = r256((size_t)(nblk + 1) * 8), b_tot = 256;
+    const size_t b_rp = r256((size_t)(n + 1) * 8), b_val = r256((size_t)nnzmax * 8), b_vec = r256((size_t)n * 8);
+    const size_t b_msk = r256((size_t)n);
+    const size_t total = b_idx + b_pos + b_cnt + b_col + b_blk + b_tot + b_rp + b_val + 12 * b_vec + 2 * b_msk;
+    CK(cudaMalloc(&S.xarena, total));
+    CK(cudaMemsetAsync(S.xarena, 0, total, h->st));
+    char* p = static_cast<char*>(S.xarena);
+    S.xidx = reinterpret_cast<int*>(p) + (long long)S.glo * h->pitch; p += b_idx;   // indexed by v (ghosts incl.)
+    S.xpos = reinterpret_cast<int*>(p); p += b_pos;
+    S.xcnt = reinterpret_cast<int*>(p); p += b_cnt;
+    S.xcol = reinterpret_cast<int*>(p); p += b_col;
+    S.xblk = reinterpret_cast<long long*>(p); p += b_blk;
+    S.xtot = reinterpret_cast<long long*>(p); p += b_tot;
+    S.xrp = reinterpret_cast<long long*>(p); p += b_rp;
+    S.xval = reinterpret_cast<double*>(p); p += b_val;
+    for (int k = 0; k < 12; ++k) { S.xv[k] = reinterpret_cast<double*>(p); p += b_vec; }
+    S.xmask = reinterpret_cast<unsigned char*>(p); p += b_msk;
+    S.xmaskcg = reinterpret_cast<unsigned char*>(p);
+    CK(cudaMemsetAsync(S.xmask, 1, (size_t)n, h->st));                     // every compact row is free
+    return GPCG_OK;
+}
+
+int run_cg_extract(gpcg_problem* h, int cur, double eta2, long long cap, long long* iters) {
+    if (h->nslabs() != 1 || h->nranks != 1)
+        return set_err(GPCG_EINVAL, "cg_mode = 1 (explicit extraction) supports one slab on one rank");
+    Slab& S = h->slabs[0];
+    RC(ensure_extract_buffers(h, S));
+    const long long n = S.rows * (long long)h->rowlen;
+    const long long nblk = (n + kScanBlock - 1) / kScanBlock;
+    const unsigned char* mask = S.m[cur];
+    CK(cudaEventRecord(h->ev_c0, h->st));
+    // compact numbering of F
+    k_scan_count<true><<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, mask, nullptr, S.xblk);
+    k_scan_blocks<<<1, 1024, 0, h->st>>>(nblk, S.xblk, S.xtot);
+    k_scan_assign<<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, mask, S.xblk, S.xidx, S.xpos);
+    CKLAUNCH();
+    long long mm = 0;
+    CK(cudaMemcpyAsync(&mm, S.xtot, sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (mm <= 0) { *iters = 0; return GPCG_OK; }
+    const int g = (int)std::min<long long>((mm + kThreads - 1) / kThreads, (long long)h->sms * 16);
+    // row pointers of A_F
+    with_gop(h, S, [&](auto& op) {
+        using Op = std::decay_t<decltype(op)>;
+        k_extract_count<Op><<<g, kThreads, 0, h->st>>>(op, mm, S.xpos, mask, S.xcnt);
+    });
+    const long long mblk = (mm + kScanBlock - 1) / kScanBlock;
+    k_scan_count<false><<<(unsigned)mblk, 256, 0, h->st>>>(mm, 1, 1, nullptr, S.xcnt, S.xblk);
+    k_scan_blocks<<<1, 1024, 0, h->st>>>(mblk, S.xblk, S.xtot);
+    k_scan_assign_vals<<<(unsigned)mblk, 256, 0, h->st>>>(mm, S.xcnt, S.xblk, S.xrp);
+    CK(cudaMemcpyAsync(S.xrp + mm, S.xtot, sizeof(long long), cudaMemcpyDeviceToDevice, h->st));
+    // A_F, r_F (recomputed from y: works with or without stored g), 1/diag on F
+    with_gop(h, S, [&](auto& op) {
+        using Op = std::decay_t<decltype(op)>;
+        k_extract_fill<Op><<<g, kThreads, 0, h->st>>>(op, mm, S.xpos, mask, S.xidx, S.xrp, S.xcol, S.xval,
+                                                      S.v[vy(cur)], S.v[VB], S.v[VD], S.xv[0], S.xv[1]);
+    });
+    CKLAUNCH();
+    CK(cudaEventRecord(h->ev_c1, h->st));
+    h->launches += 8;
+    // CG on the compact system (CSR kernels, all rows free)
+    const CsrOp cop{(int)mm, S.xrp, S.xcol, S.xval};
+    const bool pc = h->prm.precond == 1;
+    const RedScratch R = h->red(0);
+    double* rho[2] = {S.xv[2], S.xv[3]};
+    double* q[2] = {S.xv[4], S.xv[5]};
+    double* sv[2] = {S.xv[6], S.xv[7]};
+    double* pv = S.xv[8];
+    double* wv = S.xv[9];
+    if (pc)
+        k_cg_init<CsrOp, true><<<g, kThreads, 0, h->st>>>(cop, S.xv[0], S.xmask, S.xmaskcg, rho[0], q[0], sv[0], rho[1],
+                                                          q[1], sv[1], pv, wv, S.xv[1], eta2, cap, h->dS, R);
+    else
+        k_cg_init<CsrOp, false><<<g, kThreads, 0, h->st>>>(cop, S.xv[0], S.xmask, S.xmaskcg, rho[0], q[0], sv[0], rho[1],
+                                                           q[1], sv[1], pv, wv, S.xv[1], eta2, cap, h->dS, R);
+    CKLAUNCH();
+    h->launches++;
+    const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
+    float ms_x = 0.f;
+    CK(cudaEventSynchronize(h->ev_c1));
+    CK(cudaEventElapsedTime(&ms_x, h->ev_c0, h->ev_c1));
+    h->t_extract_ms += ms_x;
+    for (;;) {
+        CK(cudaEventRecord(h->ev_c0, h->st));
+        for (int i = 0; i < chunk; ++i) {
+            const int a = i & 1, bb = a ^ 1;
+            if (pc)
+                k_cg_iter<CsrOp, true><<<g, kThreads, 0, h->st>>>(cop, S.xmaskcg, rho[a], q[a], sv[a], rho[bb], q[bb],
+                                                                  sv[bb], pv, wv, S.xv[1], h->dS, R);
+            else
+                k_cg_iter<CsrOp, false><<<g, kThreads, 0, h->st>>>(cop, S.xmaskcg, rho[a], q[a], sv[a], rho[bb], q[bb],
+                                                                   sv[bb], pv, wv, S.xv[1], h->dS, R);
+        }
+        CKLAUNCH();
+        CK(cudaEventRecord(h->ev_c1, h->st));
+        h->launches += chunk;
+        RC(sync_scal(h));
+        if (h->hS->cg_done) break;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_c0, h->ev_c1));
+        h->t_cg_timed_ms += ms;
+        h->cg_iters_timed += chunk;
+        h->cg_free_iters_timed += chunk * mm;
+    }
+    *iters = h->hS->cg_it;
+    if (h->hS->cg_reason == CG_NOTSPD)
+        return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
+                       (long long)h->hS->cg_it);
+    // w = Z w_F
+    const int gs = (int)std::min<long long>((n + kThreads - 1) / kThreads, (long long)h->sms * 16);
+    k_scatter<<<gs, kThreads, 0, h->st>>>(n, h->rowlen, h->pitch, mask, S.xidx, wv, S.v[VW]);
+    CKLAUNCH();
+    h->launches++;
+    return GPCG_OK;
+}
+
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
+    if (h->prm.cg_mode == 1) return run_cg_extract(h, cur, eta2, cap, iters);
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
@@ -1752,6 +1896,7 @@ gpcg_params gpcg_params_default(void) {
     p.cg_chunk = 32;
     p.gp_chunk = 8;
     p.precond = 0;
+    p.cg_mode = 0;
     return p;
 }
 
@@ -1822,7 +1967,7 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
         return set_err(GPCG_EINVAL, "eta2_shrink in (0,1), eta2_floor > 0 required");
     if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 || p->cg_cap < 0 ||
         p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096 || p->gp_chunk < 1 ||
-        p->gp_chunk > 256 || (p->precond != 0 && p->precond != 1))
+        p->gp_chunk > 256 || (p->precond != 0 && p->precond != 1) || (p->cg_mode != 0 && p->cg_mode != 1))
         return set_err(GPCG_EINVAL, "integer parameter out of range");
     const int old_chunk = h->prm.cg_chunk, old_pc = h->prm.precond;
     h->prm = *p;
@@ -1913,6 +2058,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     h->launches = 0;
     h->cg_iters_timed = h->cg_free_iters_timed = 0;
     h->t_cg_timed_ms = 0.0;
+    h->t_extract_ms = 0.0;
     int rc;
     RC(enter(h));
     const gpcg_params& prm = h->prm;
@@ -2076,6 +2222,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     st.cg_iters_timed = h->cg_iters_timed;
     st.cg_free_iters_timed = h->cg_free_iters_timed;
     st.t_cg_timed_ms = h->t_cg_timed_ms;
+    st.t_extract_ms = h->t_extract_ms;
     st.t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     if (stats) *stats = st;
     RC(leave(h));

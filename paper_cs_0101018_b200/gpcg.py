@@ -33,7 +33,7 @@ class Params(C.Structure):
                 ("eta2_shrink", C.c_double), ("eta2_floor", C.c_double),
                 ("gp_cap", C.c_int64), ("refine_cap", C.c_int64), ("max_halvings", C.c_int64),
                 ("cg_cap", C.c_int64), ("search_k", C.c_int32), ("cg_chunk", C.c_int32),
-                ("gp_chunk", C.c_int32), ("precond", C.c_int32)]
+                ("gp_chunk", C.c_int32), ("precond", C.c_int32), ("cg_mode", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -44,7 +44,7 @@ class Stats(C.Structure):
                 ("t_total_ms", C.c_double), ("t_cg_ms", C.c_double), ("t_gp_ms", C.c_double),
                 ("status", C.c_int32), ("kernel_launches", C.c_int32),
                 ("cg_iters_timed", C.c_int64), ("cg_free_iters_timed", C.c_int64),
-                ("t_cg_timed_ms", C.c_double)]
+                ("t_cg_timed_ms", C.c_double), ("t_extract_ms", C.c_double)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -428,3 +428,37 @@ def test_band_kernels_edge_grids(G, oracle, nx, ny):
         spmv_close(y, oracle.spmv(A, p), abs_op(A, p))
         assert abs(st["q"] - st_o["q"]) <= 1e-10 * max(abs(st_o["q"]), 1e-300)
         assert np.max(np.abs(x - x_o)) <= 1e-7
+
+
+# ------------------------------------------------------------------ extraction ablation (NEXT-4)
+@pytest.mark.parametrize("case", ["C0", "C1", "c4_family_m16", "ragged37x23", "dense8", "jb80_eps0.9"])
+def test_solve_parity_explicit_extraction(G, oracle, case):
+    """cg_mode = 1: A_k extracted as a compact CSR matrix each CG call (the paper's PETSc
+    route) reaches the oracle's solution too, with and without the Jacobi preconditioner."""
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    for pc in (0, 1):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(cg_mode=1, precond=pc)
+            rc, x, st = s.solve(prob.x0, tol)
+        assert rc == 0, (rc, st)
+        assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+        assert np.max(np.abs(x - x_o)) <= 1e-7
+        assert st["cg_iters"] == 0 or st["t_extract_ms"] > 0.0
+
+
+def test_explicit_extraction_same_cg_iterates(G):
+    """The compact CG runs the same recurrences on the same numbers (A_F's rows in the
+    operator's neighbour order): one CG call from the same point gives w to rounding."""
+    prob = P.c1()
+    out = {}
+    for mode in (0, 1):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(cg_mode=mode, cg_cap=40, eta2=1e-10, refine_cap=1)
+            rc, x, st = s.solve(prob.x0, -1e-12, max_it=1)
+        out[mode] = (x, st)
+    x0, st0 = out[0]
+    x1, st1 = out[1]
+    assert st0["cg_iters"] == st1["cg_iters"] and st0["gp_iters"] == st1["gp_iters"]
+    assert np.max(np.abs(x0 - x1)) <= 1e-10 * np.max(np.abs(x0))

@@ -129,10 +129,15 @@ def test_slab_first_outer_iteration_matches_single_slab(G, case):
     deep enough for the operator applications a sweep chains -- a missing ghost row shows up
     as a wrong Cauchy step alpha_0 at the slab boundary and a visibly different iterate)."""
     prob = CASES[case][0]()
+    # one CG iteration per CG call: the iterate is then dominated by the GP phase, whose
+    # steps differ between slab counts only by the reduction order (~1e-16 relative) -- a
+    # Krylov run would amplify those rounding differences and hide a real discrepancy
     with G.Solver.from_problem(prob) as s1:
+        s1.set_params(cg_cap=1)
         rc1, x1, st1 = s1.solve(prob.x0, -1e-12, max_it=1)
     with G.Solver.from_problem(prob, slabs=3) as s3:
+        s3.set_params(cg_cap=1)
         rc3, x3, st3 = s3.solve(prob.x0, -1e-12, max_it=1)
     assert (st1["gp_iters"], st1["cg_iters"]) == (st3["gp_iters"], st3["cg_iters"])
     scale = max(np.max(np.abs(x1)), 1e-300)
-    assert np.max(np.abs(x1 - x3)) <= 1e-11 * scale, np.max(np.abs(x1 - x3)) / scale
+    assert np.max(np.abs(x1 - x3)) <= 1e-12 * scale, np.max(np.abs(x1 - x3)) / scale
