@@ -86,7 +86,8 @@ typedef struct {
     int32_t cg_mode;     /* 0: A_k applied in place on masked full-length vectors (the hot
                             path, P:680-683's "alternative technique"); 1: A_k extracted
                             as a compact CSR matrix each CG call, as the paper does with
-                            PETSc -- the extraction ablation; one slab / rank */
+                            PETSc -- the extraction ablation; one slab / rank;
+                            2: extract only for CSR / 3-D operators with |F| < 0.3 n      */
 } gpcg_params;
 
 typedef struct {

@@ -1324,7 +1324,11 @@ int run_cg_extract(gpcg_problem* h, int cur, double eta2, long long cap, long lo
 
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
-    if (h->prm.cg_mode == 1) return run_cg_extract(h, cur, eta2, cap, iters);
+    // cg_mode 1: always extract; 2 (auto): extract for the generic kernels (CSR, 3-D) when the
+    // free set is small (m < 0.3 n), where the compact system wins
+    if (h->prm.cg_mode == 1 ||
+        (h->prm.cg_mode == 2 && !spec2d(h) && h->nslabs() == 1 && h->nranks == 1 && 10 * m < 3 * h->n_global))
+        return run_cg_extract(h, cur, eta2, cap, iters);
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
@@ -1967,7 +1971,7 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
         return set_err(GPCG_EINVAL, "eta2_shrink in (0,1), eta2_floor > 0 required");
     if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 || p->cg_cap < 0 ||
         p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096 || p->gp_chunk < 1 ||
-        p->gp_chunk > 256 || (p->precond != 0 && p->precond != 1) || (p->cg_mode != 0 && p->cg_mode != 1))
+        p->gp_chunk > 256 || (p->precond != 0 && p->precond != 1) || (p->cg_mode < 0 || p->cg_mode > 2))
         return set_err(GPCG_EINVAL, "integer parameter out of range");
     const int old_chunk = h->prm.cg_chunk, old_pc = h->prm.precond;
     h->prm = *p;
