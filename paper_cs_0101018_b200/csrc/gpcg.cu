@@ -613,15 +613,20 @@ int setup_tile(gpcg_problem* h) {
             G.rlo = -S.glo;
             grid = std::min(G.nbands * G.nsegs, resident);
         };
-        band(r4cg, S.bg_cg, S.grid4_cg);
+        // GPCG_CG_CTAS_PER_SM / GPCG_GP_CTAS_PER_SM (tuning): cap the CTAs per SM of the CG / GP bands
+        auto cap_env = [&](const char* name, int r) {
+            const char* e = getenv(name);
+            return (e && atoi(e) > 0) ? std::min(r, atoi(e) * h->sms) : r;
+        };
+        band(cap_env("GPCG_CG_CTAS_PER_SM", r4cg), S.bg_cg, S.grid4_cg);
         {
             const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
             CK(cudaMalloc(&S.cgflags, (size_t)std::max<long long>(nf, 1)));
         }
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
-        band(r5acc, S.bg5_acc, S.grid5_acc, m5::kOut);
-        band(r5srch, S.bg5_srch, S.grid5_srch, m5::kOut);
+        band(cap_env("GPCG_GP_CTAS_PER_SM", r5acc), S.bg5_acc, S.grid5_acc, m5::kOut);
+        band(cap_env("GPCG_GP_CTAS_PER_SM", r5srch), S.bg5_srch, S.grid5_srch, m5::kOut);
         band(r5init, S.bg5_init, S.grid5_init, m5::kOut);
         S.grid_t_cg = std::min(ntiles, r_cg);
         S.grid_t_acc = std::min(ntiles, r_acc);
