@@ -360,6 +360,10 @@ def run_ours(args):
                          "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_launch": min_bytes_per_launch, "us_per_launch": launch_s * 1e6,
                          "launch": "one CG iteration (reduced HVP + vector updates + reduction)",
+                         "note": ("traffic = ncu DRAM bytes per CG iteration (profiles/traffic_<config>.json): at C2 the "
+                                  "CG working set (~105 MB) stays in the 126 MB L2 between iterations, so the sweep is "
+                                  "issue/L2-bound and 'achieved' counts the bytes the kernel must touch, mostly L2 hits; "
+                                  "the HBM-bound regime is C3 (DESIGN.md 9)"),
                          "algorithmic_bytes": f"{cg_min_bytes_per_free_point(prob):.0f} B per free point + 1 B mask "
                                               f"per point (DESIGN.md 6: the kernel's three-vector recurrence)",
                          "survey_8d_80B": {"bytes_per_launch": bytes_per_launch, "achieved": achieved,

@@ -235,6 +235,8 @@ struct gpcg_problem {
     std::vector<Slab> slabs;
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
+    bool use_nccl = false;          // collectives go through NCCL (nranks > 1, or GPCG_FORCE_NCCL=1: a
+                                    // 1-rank communicator, to exercise the NCCL path on one GPU)
     bool deferred = false;          // several slabs or ranks: reductions go through k_finalize
     double* red_all = nullptr;      // [nslabs][kMaxSums] per-slab totals
     double* red_tot = nullptr;      // [kMaxSums] global totals
@@ -300,7 +302,7 @@ int finish_reduce(gpcg_problem* h, const FinArgs& a, int ns) {
         h->launches++;
         CKLAUNCH();
     }
-    if (h->nranks > 1)
+    if (h->use_nccl)
         NK(nccl_api()->AllReduce(h->red_tot, h->red_tot, (size_t)ns, ncclDouble, ncclSum, h->comm, h->st));
     k_finalize<<<1, 32, 0, h->st>>>(h->red_tot, h->dS, a);
     h->launches++;
@@ -672,6 +674,14 @@ int setup_comm(gpcg_problem* h, const gpcg_dist* d) {
         ncclUniqueId id;
         memcpy(&id, d->nccl_id, sizeof id);
         NK(N->CommInitRank(&h->comm, h->nranks, id, h->rank));
+        h->use_nccl = true;
+    } else if (getenv("GPCG_FORCE_NCCL") && getenv("GPCG_FORCE_NCCL")[0] == '1') {
+        const NcclApi* N = nccl_api();
+        if (!N) return set_err(GPCG_ENCCL, "GPCG_FORCE_NCCL=1 but libnccl.so.2 is not loadable");
+        ncclUniqueId id;
+        NK(N->GetUniqueId(&id));
+        NK(N->CommInitRank(&h->comm, 1, id, 0));
+        h->use_nccl = true;
     }
     return GPCG_OK;
 }
@@ -759,7 +769,7 @@ int create_vectors(gpcg_problem* h, const double* b, const double* l, const doub
     // first pair, broadcast from rank 0)?
     CK(cudaMemcpyAsync(h->lu0, h->slabs[0].v[VL], sizeof(double), cudaMemcpyDeviceToDevice, h->st));
     CK(cudaMemcpyAsync(h->lu0 + 1, h->slabs[0].v[VU], sizeof(double), cudaMemcpyDeviceToDevice, h->st));
-    if (h->nranks > 1) NK(nccl_api()->Broadcast(h->lu0, h->lu0, 2, ncclDouble, 0, h->comm, h->st));
+    if (h->use_nccl) NK(nccl_api()->Broadcast(h->lu0, h->lu0, 2, ncclDouble, 0, h->comm, h->st));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const int cols = h->is_csr ? S.rows : h->rowlen, rows = h->is_csr ? 1 : S.rows;
@@ -816,7 +826,7 @@ int layout_slabs(gpcg_problem* h, long long rows_rank, int nsl, int ghost) {
         const int need = (S.nb_lo != NB_NONE || S.nb_hi != NB_NONE) ? std::max(ghost, 1) : 1;
         if (S.rows < need) return set_err(GPCG_EINVAL, "slab %d has %d rows (need >= %d)", s, S.rows, need);
     }
-    h->deferred = has_ghosts(h);
+    h->deferred = has_ghosts(h) || h->use_nccl;
     return GPCG_OK;
 }
 
@@ -1234,7 +1244,7 @@ int ensure_extract_buffers(gpcg_problem* h, Slab& S) {
 }
 
 int run_cg_extract(gpcg_problem* h, int cur, double eta2, long long cap, long long* iters) {
-    if (h->nslabs() != 1 || h->nranks != 1)
+    if (h->nslabs() != 1 || h->nranks != 1 || h->deferred)
         return set_err(GPCG_EINVAL, "cg_mode = 1 (explicit extraction) supports one slab on one rank");
     Slab& S = h->slabs[0];
     RC(ensure_extract_buffers(h, S));
@@ -1332,7 +1342,7 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     // cg_mode 1: always extract; 2 (auto): extract for the generic kernels (CSR, 3-D) when the
     // free set is small (m < 0.3 n), where the compact system wins
     if (h->prm.cg_mode == 1 ||
-        (h->prm.cg_mode == 2 && !spec2d(h) && h->nslabs() == 1 && h->nranks == 1 && 10 * m < 3 * h->n_global))
+        (h->prm.cg_mode == 2 && !spec2d(h) && !h->deferred && 10 * m < 3 * h->n_global))
         return run_cg_extract(h, cur, eta2, cap, iters);
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
@@ -1388,7 +1398,7 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
             CKLAUNCH();
         }
     }
-    if (h->cg_persistent && h->tile && (h->tile_mask & 8) && !has_ghosts(h)) {
+    if (h->cg_persistent && h->tile && (h->tile_mask & 8) && !h->deferred) {
         // one cooperative launch runs the whole CG call (k6_cg_loop)
         Slab& S = h->slabs[0];
         const unsigned char* flags = h->cg_skip ? S.cgflags : nullptr;
@@ -1457,7 +1467,7 @@ int detect_b_rows(gpcg_problem* h) {
         CK(cudaMalloc(&S.brow, (size_t)h->nx * sizeof(double)));
         CK(cudaMemcpyAsync(S.brow, h->slabs[0].v[VB], (size_t)h->nx * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
     }
-    if (h->nranks > 1)
+    if (h->use_nccl)
         NK(nccl_api()->Broadcast(h->slabs[0].brow, h->slabs[0].brow, (size_t)h->nx, ncclDouble, 0, h->comm, h->st));
     for (int s = 1; s < h->nslabs(); ++s)
         CK(cudaMemcpyAsync(h->slabs[s].brow, h->slabs[0].brow, (size_t)h->nx * sizeof(double),
@@ -2083,7 +2093,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     RC(launch_accept(h, VIN, NO_VEC, 0.0, NO_VEC, VY0, VG0, MK0));
     RC(sync_scal(h));
     st.full_spmvs++;
-    if (h->gp_graph && !(h->gp_persistent && h->gfree && !has_ghosts(h)))
+    if (h->gp_graph && !(h->gp_persistent && h->gfree && !h->deferred))
         RC(build_gp_graph(h, std::max(1, h->prm.gp_chunk)));
     st.g0_norm = std::sqrt(S.g2);
     tau = tol > 0.0 ? tol : -tol * st.g0_norm;
@@ -2102,7 +2112,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 h->launches++;
                 CKLAUNCH();
                 long long jdone = 0;
-                const bool persist = h->gp_persistent && h->gfree && !has_ghosts(h);
+                const bool persist = h->gp_persistent && h->gfree && !h->deferred;
                 for (;;) {
                     if (persist) {
                         if ((rc = launch_gp_loop(h, cur))) goto fail;

@@ -141,3 +141,21 @@ def test_slab_first_outer_iteration_matches_single_slab(G, case):
     assert (st1["gp_iters"], st1["cg_iters"]) == (st3["gp_iters"], st3["cg_iters"])
     scale = max(np.max(np.abs(x1)), 1e-300)
     assert np.max(np.abs(x1 - x3)) <= 1e-12 * scale, np.max(np.abs(x1 - x3)) / scale
+
+
+@pytest.mark.parametrize("slabs", [1, 2])
+@pytest.mark.parametrize("case", ["C0", "C1", "c4_family_m12"])
+def test_nccl_collectives_one_rank(G, oracle, monkeypatch, case, slabs):
+    """The NCCL path on one GPU: GPCG_FORCE_NCCL=1 gives the handle a 1-rank communicator, so
+    every global sum is an ncclAllReduce (inside the captured CG / GP graphs) and the create-time
+    broadcasts go through ncclBroadcast, with the deferred k_finalize decisions -- the collective
+    sequence of a multi-rank run, minus the send/recv halos (no neighbouring rank)."""
+    monkeypatch.setenv("GPCG_FORCE_NCCL", "1")
+    make, tol = CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    with G.Solver.from_problem(prob, slabs=slabs) as s:
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0 and rc_o == 0, (rc, st)
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
