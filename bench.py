@@ -56,8 +56,9 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def cg_kernel_name(prob):
-    """The CG-iteration kernel libgpcg.so selects for this problem (gpcg.cu enqueue_cg_iter)."""
+def cg_kernel_name(prob, slabs_total=1):
+    """The CG-iteration kernel libgpcg.so selects for this problem (gpcg.cu run_cg /
+    enqueue_cg_iter); slabs_total > 1 (ranks x local slabs) uses the graph-chunk path."""
     if prob.kind == "csr":
         return "k_cg_iter<CsrOp>"
     if prob.kind == "stencil3d":
@@ -67,7 +68,7 @@ def cg_kernel_name(prob):
     if os.environ.get("GPCG_GENERIC") == "1":
         return "k_cg_iter<StencilOp>"
     if bc and tile & 8:
-        if os.environ.get("GPCG_CG_PERSIST", "1") != "0":
+        if os.environ.get("GPCG_CG_PERSIST", "1") != "0" and slabs_total == 1:
             return "k6_cg_loop (persistent cooperative CG, TMA-fed column march; per-iteration time)"
         return "k4_cg_iter (TMA-fed column march)"
     if bc and tile & 4:
@@ -353,7 +354,7 @@ def run_ours(args):
             # the five-vector C-G form for CSR = SURVEY 8(d)'s figure); SURVEY 8(d)'s 80 B figure
             # (which also streams A p and A rho) beside it -- against that count the kernel exceeds
             # the copy peak, because it recomputes A p and A rho from neighbours instead of streaming them.
-            "roofline": {"bound": "hbm", "kernel": cg_kernel_name(prob),
+            "roofline": {"bound": "hbm", "kernel": cg_kernel_name(prob, world * args.slabs),
                          "achieved": achieved_min, "peak": peak, "unit": "GB/s",
                          "frac": (achieved_min / peak) if achieved_min else None,
                          "frac_of_8TBs": (achieved_min / 8000.0) if achieved_min else None,
