@@ -29,6 +29,12 @@
 
 namespace gpcg {
 
+#ifndef GPCG_CG_NST
+#define GPCG_CG_NST 4       // CG sweep pipeline stages (tuning)
+#endif
+#ifndef GPCG_CG_MINB
+#define GPCG_CG_MINB 4      // CG sweep CTAs per SM the register budget is sized for (tuning)
+#endif
 namespace m4 {
 constexpr int kWarps = 4;                 // consumer warps (one per 28 / 26-column strip)
 constexpr int kThreads = 32 * kWarps;     // lock-step engine: thread 0 also issues the TMA loads
@@ -193,7 +199,7 @@ using namespace m4;
 constexpr int kRho = 0, kP = kF, kW = 2 * kF, kM = 2 * kF + kFo;
 constexpr int kStage = kM + kU;                       // 11648
 constexpr int kTx = kM + kUt;                         // bytes the TMA delivers per stage
-constexpr int kNST = 4;
+constexpr int kNST = GPCG_CG_NST;
 constexpr int kSmem = kNST * kStage + 64;
 }  // namespace m4cg
 
@@ -299,7 +305,7 @@ __global__ void k_cg_block_flags(int nx, int pitch, BandGeom G, const unsigned c
 }
 
 template <bool PC>     // point-Jacobi PCG as in k2_cg_iter<BC, true>
-__global__ void __launch_bounds__(m4::kThreadsWS, 4)
+__global__ void __launch_bounds__(m4::kThreadsWS, GPCG_CG_MINB)
 k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, const __grid_constant__ CUtensorMap m_p,
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
            double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R,
@@ -338,7 +344,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
 }
 
 template <bool PC>
-__global__ void __launch_bounds__(m4::kThreadsWS, 4)
+__global__ void __launch_bounds__(m4::kThreadsWS, GPCG_CG_MINB)
 k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, const __grid_constant__ CUtensorMap m_rho1,
            const __grid_constant__ CUtensorMap m_p0, const __grid_constant__ CUtensorMap m_p1,
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,

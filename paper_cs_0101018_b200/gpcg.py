@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgpcg.so")
+LIB_PATH = os.environ.get("GPCG_LIB") or os.path.join(_HERE, "libgpcg.so")   # GPCG_LIB: A/B builds
 
 OK, NOT_CONVERGED, EINVAL, ENOMEM, ECUDA, ENCCL, ENOTSPD, ESEARCH, ESTATE = 0, 1, -1, -2, -3, -4, -5, -6, -7
 STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL",
