@@ -52,7 +52,10 @@ typedef struct {
     int64_t cg_cap;       /* 0 => m_k, the finite-termination bound P:444-447                     */
     double time_budget_s; /* 0 => none; else stop (NOT_CONVERGED) once exceeded (bounded samples) */
     int64_t precond;      /* 0: plain CG (the hot path); 1: point-Jacobi PCG, M = diag(A_k)
-                             (the "diagonal Jacobi preconditioner" of P:1096-1098, Table 4)       */
+                             (the "diagonal Jacobi preconditioner" of P:1096-1098, Table 4);
+                             2: block-Jacobi ILU(0) on tiles of a 2-D grid          */
+    int64_t grid_nx, grid_ny;   /* precond 2: the 2-D grid (v = i + nx j)                          */
+    int64_t tile_x, tile_y;     /* precond 2: block = tile_x x tile_y tile of the grid              */
 } ora_params;
 
 typedef struct {
@@ -347,18 +350,45 @@ int64_t ora_projected_search(int64_t n, const int64_t *rp, const int32_t *ci, co
  * Returns w_j at that j (reading R11).  Returns the iteration count, or
  * ORA_ENOTSPD (negative) on <p, A_k p> <= 0.  work: 4n doubles. decs (nullable,
  * length >= cap) receives the per-step decreases. */
-int64_t ora_pcg(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
-                const unsigned char *free_, const double *r, const double *dinv, double eta2, int64_t cap,
-                double *w, double *work, double *decs, double deadline)
+void ora_bjilu_factor(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                      const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, double *d);
+void ora_bjilu_apply(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                     const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, const double *d,
+                     const double *r, double *t, double *z);
+
+/* preconditioner of ora_pcg_m: kind 0 none, 1 point Jacobi (dinv), 2 block-Jacobi ILU(0)
+ * (grid nx, tiles tx x ty; pivots factored at the start of every CG call on its free set) */
+typedef struct {
+    int kind;
+    const double *dinv;
+    int64_t nx, tx, ty;
+    double *d, *t;              /* kind 2: pivots and forward-solve scratch (n each) */
+} ora_prec;
+
+static void prec_apply(const ora_prec *M, int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                       const unsigned char *free_, const double *r, double *z)
 {
+    if (M->kind == 1) {
+        for (int64_t i = 0; i < n; i++) z[i] = free_[i] ? r[i] * M->dinv[i] : 0.0;
+    } else {
+        ora_bjilu_apply(n, rp, ci, val, free_, M->nx, M->tx, M->ty, M->d, r, M->t, z);
+    }
+}
+
+int64_t ora_pcg_m(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                  const unsigned char *free_, const double *r, const ora_prec *M, double eta2, int64_t cap,
+                  double *w, double *work, double *decs, double deadline)
+{
+    const int pc = M && M->kind != 0;
     double *rho = work, *p = work + n, *a = work + 2 * n;
-    double *z = dinv ? work + 3 * n : rho;
+    double *z = pc ? work + 3 * n : rho;
+    if (M && M->kind == 2) ora_bjilu_factor(n, rp, ci, val, free_, M->nx, M->tx, M->ty, M->d);
     for (int64_t i = 0; i < n; i++) {
         rho[i] = free_[i] ? -r[i] : 0.0;
-        if (dinv) z[i] = free_[i] ? rho[i] * dinv[i] : 0.0;
-        p[i] = z[i];
         w[i] = 0.0;
     }
+    if (pc) prec_apply(M, n, rp, ci, val, free_, rho, z);
+    for (int64_t i = 0; i < n; i++) p[i] = z[i];
     double rr = dot(n, rho, z);
     double rnorm0 = sqrt(rr);
     double maxdec = 0.0;
@@ -374,8 +404,7 @@ int64_t ora_pcg(int64_t n, const int64_t *rp, const int32_t *ci, const double *v
         double dec = 0.5 * alpha * rr;
         if (decs) decs[it - 1] = dec;
         for (int64_t i = 0; i < n; i++) rho[i] = rho[i] - alpha * a[i];
-        if (dinv)
-            for (int64_t i = 0; i < n; i++) z[i] = free_[i] ? rho[i] * dinv[i] : 0.0;
+        if (pc) prec_apply(M, n, rp, ci, val, free_, rho, z);
         double rr_new = dot(n, rho, z);
         int stop = (it >= 2 && dec <= eta2 * maxdec) ||
                    (sqrt(rr_new) <= 1e-14 * (1.0 + rnorm0)) || (it >= cap) ||
@@ -389,12 +418,90 @@ int64_t ora_pcg(int64_t n, const int64_t *rp, const int32_t *ci, const double *v
     return it;
 }
 
+/* point-Jacobi form (dinv nullable: plain CG) */
+int64_t ora_pcg(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                const unsigned char *free_, const double *r, const double *dinv, double eta2, int64_t cap,
+                double *w, double *work, double *decs, double deadline)
+{
+    ora_prec M = {dinv ? 1 : 0, dinv, 0, 0, 0, NULL, NULL};
+    return ora_pcg_m(n, rp, ci, val, free_, r, &M, eta2, cap, w, work, decs, deadline);
+}
+
+/* block-Jacobi ILU(0) form (tiles tx x ty of an nx-wide grid); work: 4n, scratch: 2n */
+int64_t ora_pcg_bjilu(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                      const unsigned char *free_, const double *r, int64_t nx, int64_t tx, int64_t ty,
+                      double eta2, int64_t cap, double *w, double *work, double *scratch, double *decs)
+{
+    ora_prec M = {2, NULL, nx, tx, ty, scratch, scratch + n};
+    return ora_pcg_m(n, rp, ci, val, free_, r, &M, eta2, cap, w, work, decs, 0.0);
+}
+
 /* plain CG (the hot path's CG): ora_pcg without a preconditioner */
 int64_t ora_cg(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
                const unsigned char *free_, const double *r, double eta2, int64_t cap,
                double *w, double *work, double *decs, double deadline)
 {
     return ora_pcg(n, rp, ci, val, free_, r, NULL, eta2, cap, w, work, decs, deadline);
+}
+
+/* ------------------------------------------------------------------------ */
+/* block-Jacobi ILU(0) ("a block Jacobi preconditioner ... ILU(0),  */
+/* which produced a factored matrix that maintained the same sparsity pattern")  */
+/* ------------------------------------------------------------------------ */
+/* Blocks: the tiles of tile_x x tile_y points of an nx x ny grid (v = i + nx j); within a
+ * block the rows of A_k = Z'AZ (free points only) in natural order.  ILU(0) keeps A's
+ * pattern: M = (D + L) D^-1 (D + U), L / U the strict lower / upper parts of the block of
+ * A_k, D the pivots
+ *     d_v = a_vv - sum_{u < v in the block, u free, a_vu != 0} a_vu a_uv / d_u
+ * (for a pattern in which no product l_vk u_ku lands on a pattern entry other than the
+ * diagonal -- true for the 5-point stencil in natural order -- this is exactly ILU(0)).
+ * Entries coupling different blocks are dropped (block Jacobi).  Symmetric A: a_uv = a_vu. */
+static int same_tile(int64_t u, int64_t v, int64_t nx, int64_t tx, int64_t ty)
+{
+    return (u % nx) / tx == (v % nx) / tx && (u / nx) / ty == (v / nx) / ty;
+}
+
+void ora_bjilu_factor(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                      const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, double *d)
+{
+    /* natural order is a valid elimination order inside every block: u < v globally and in
+     * the same tile <=> u precedes v in the tile's row-major order */
+    for (int64_t v = 0; v < n; v++) {
+        if (!free_[v]) { d[v] = 1.0; continue; }
+        double dv = 0.0;
+        for (int64_t k = rp[v]; k < rp[v + 1]; k++)
+            if (ci[k] == v) dv += val[k];
+        for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
+            int64_t u = ci[k];
+            if (u < v && free_[u] && same_tile(u, v, nx, tx, ty)) dv = dv - val[k] * val[k] / d[u];
+        }
+        d[v] = dv;
+    }
+}
+
+/* z = M^-1 r on the free set: (D + L) t = r forward, then D^-1 (D + U) z = t backward */
+void ora_bjilu_apply(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                     const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, const double *d,
+                     const double *r, double *t, double *z)
+{
+    for (int64_t v = 0; v < n; v++) {
+        if (!free_[v]) { t[v] = 0.0; continue; }
+        double s = r[v];
+        for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
+            int64_t u = ci[k];
+            if (u < v && free_[u] && same_tile(u, v, nx, tx, ty)) s = s - val[k] * t[u];
+        }
+        t[v] = s / d[v];
+    }
+    for (int64_t v = n - 1; v >= 0; v--) {
+        if (!free_[v]) { z[v] = 0.0; continue; }
+        double s = 0.0;
+        for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
+            int64_t u = ci[k];
+            if (u > v && free_[u] && same_tile(u, v, nx, tx, ty)) s = s + val[k] * z[u];
+        }
+        z[v] = t[v] - s / d[v];
+    }
 }
 
 /* dinv_i = 1 / A_ii (the point-Jacobi preconditioner; A SPD => A_ii > 0) */
@@ -418,6 +525,7 @@ void ora_params_default(ora_params *p)
     p->gp_cap = 100; p->refine_cap = 30; p->max_halvings = 50; p->cg_cap = 0;
     p->time_budget_s = 0.0;
     p->precond = 0;
+    p->grid_nx = 0; p->grid_ny = 0; p->tile_x = 32; p->tile_y = 32;
 }
 
 /* Solve min q(x) s.t. l <= x <= u.  tol > 0: absolute tau on ||grad_Omega q||_2
@@ -439,10 +547,16 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
     double *w = (double *)malloc((size_t)n * sizeof(double));
     double *work = (double *)malloc((size_t)4 * n * sizeof(double));
     double *dinv = prm->precond == 1 ? (double *)malloc((size_t)n * sizeof(double)) : NULL;
+    double *ilu = prm->precond == 2 ? (double *)malloc((size_t)2 * n * sizeof(double)) : NULL;
+    if (prm->precond == 2 && (prm->grid_nx <= 0 || prm->grid_nx * prm->grid_ny != n || prm->tile_x <= 0 ||
+                              prm->tile_y <= 0)) {
+        free(dinv); free(ilu);
+        st->status = ORA_EINVAL; return ORA_EINVAL;
+    }
     unsigned char *act = (unsigned char *)malloc((size_t)n);
     unsigned char *fr = (unsigned char *)malloc((size_t)n);
-    if (!g || !y || !w || !work || !act || !fr || (prm->precond == 1 && !dinv)) {
-        free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv);
+    if (!g || !y || !w || !work || !act || !fr || (prm->precond == 1 && !dinv) || (prm->precond == 2 && !ilu)) {
+        free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv); free(ilu);
         st->status = ORA_ENOMEM; return ORA_ENOMEM;
     }
     int status = ORA_NOT_CONVERGED;
@@ -504,8 +618,9 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
             for (int64_t i = 0; i < n; i++) { fr[i] = !is_active(x[i], l[i], u[i]); m += fr[i]; }
             if (m == 0) break;              /* reading R26: next GP phase frees variables */
             int64_t cap = prm->cg_cap > 0 ? prm->cg_cap : m;
-            int64_t its = ora_pcg(n, rp, ci, val, fr, g, dinv, eta2, cap, w, work, NULL,
-                                  prm->time_budget_s > 0.0 ? t0 + prm->time_budget_s : 0.0);
+            ora_prec M = {(int)prm->precond, dinv, prm->grid_nx, prm->tile_x, prm->tile_y, ilu, ilu ? ilu + n : NULL};
+            int64_t its = ora_pcg_m(n, rp, ci, val, fr, g, &M, eta2, cap, w, work, NULL,
+                                    prm->time_budget_s > 0.0 ? t0 + prm->time_budget_s : 0.0);
             st->cg_calls++;
             if (its < 0) { status = (int)its; goto done; }
             st->cg_iters += its;
@@ -543,6 +658,6 @@ done:
         st->status = status;
         st->seconds = now_s() - t0;
     }
-    free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv);
+    free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv); free(ilu);
     return status;
 }

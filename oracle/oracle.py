@@ -37,7 +37,8 @@ class Params(C.Structure):
                 ("eta2_shrink", C.c_double), ("eta2_floor", C.c_double),
                 ("gp_cap", C.c_int64), ("refine_cap", C.c_int64),
                 ("max_halvings", C.c_int64), ("cg_cap", C.c_int64),
-                ("time_budget_s", C.c_double), ("precond", C.c_int64)]
+                ("time_budget_s", C.c_double), ("precond", C.c_int64),
+                ("grid_nx", C.c_int64), ("grid_ny", C.c_int64), ("tile_x", C.c_int64), ("tile_y", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -89,6 +90,12 @@ def lib():
         L.ora_cg.argtypes = [i64, P, P, P, P, P, C.c_double, i64, P, P, P, C.c_double]
         L.ora_pcg.restype = i64
         L.ora_pcg.argtypes = [i64, P, P, P, P, P, P, C.c_double, i64, P, P, P, C.c_double]
+        L.ora_pcg_bjilu.restype = i64
+        L.ora_pcg_bjilu.argtypes = [i64, P, P, P, P, P, i64, i64, i64, C.c_double, i64, P, P, P, P]
+        L.ora_bjilu_factor.restype = None
+        L.ora_bjilu_factor.argtypes = [i64, P, P, P, P, i64, i64, i64, P]
+        L.ora_bjilu_apply.restype = None
+        L.ora_bjilu_apply.argtypes = [i64, P, P, P, P, i64, i64, i64, P, P, P, P]
         L.ora_jacobi_inverse.restype = None
         L.ora_jacobi_inverse.argtypes = [i64, P, P, P, P]
         L.ora_params_default.restype = None
@@ -252,6 +259,38 @@ def jacobi_inverse(A: CSR):
     d = np.empty(A.n)
     lib().ora_jacobi_inverse(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(d))
     return d
+
+
+def bjilu_factor(A: CSR, free, nx, tx, ty):
+    """Block-Jacobi ILU(0) pivots on tiles tx x ty of an nx-wide grid (oracle routine)."""
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    d = np.empty(A.n)
+    lib().ora_bjilu_factor(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), nx, tx, ty, _p(d))
+    return d
+
+
+def bjilu_apply(A: CSR, free, nx, tx, ty, d, r):
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    r = _f64(r)
+    t = np.empty(A.n)
+    z = np.empty(A.n)
+    lib().ora_bjilu_apply(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), nx, tx, ty, _p(d), _p(r), _p(t), _p(z))
+    return z
+
+
+def pcg_bjilu(A: CSR, free, r, nx, tx, ty, eta2, cap=0):
+    """Block-Jacobi ILU(0) PCG on A_F w = -r. -> (iterations, w, decreases)."""
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    r = _f64(r)
+    m = int(fr.sum())
+    cap = cap if cap > 0 else m
+    w = np.empty(A.n)
+    work = np.empty(4 * A.n)
+    scratch = np.empty(2 * A.n)
+    decs = np.zeros(max(cap, 1))
+    it = lib().ora_pcg_bjilu(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), nx, tx, ty, eta2, cap,
+                             _p(w), _p(work), _p(scratch), _p(decs))
+    return it, w, decs[:max(it, 0)]
 
 
 def pcg(A: CSR, free, r, dinv, eta2, cap=0):

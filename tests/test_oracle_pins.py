@@ -493,3 +493,71 @@ def test_stencil3d_constant_coefficient_eigenpairs(oracle):
         assert np.max(np.abs(oracle.spmv(A, v) - lam * v)) <= 1e-13
     D = A.todense()
     assert np.array_equal(D, D.T)
+
+
+# ---------------------------------------------------------------- block-Jacobi ILU(0) (NEXT-3)
+def _grid_csr(oracle, nx, ny, seed):
+    wx = 0.5 + P.uniform(seed, 1, ny * (nx + 1))
+    wy = 0.5 + P.uniform(seed, 2, (ny + 1) * nx)
+    return oracle.stencil2d_to_csr(nx, ny, wx, nx + 1, wy, nx, 0.01 * P.uniform(seed, 3, nx * ny))
+
+
+def test_bjilu_reproduces_a_on_its_pattern(oracle):
+    # ILU(0): M = (D+L) D^-1 (D+U) equals A on A's pattern inside every block (and the
+    # inter-block entries are dropped); checked densely on a 7 x 6 grid with 3 x 4 tiles
+    nx, ny, tx, ty = 7, 6, 3, 4
+    A = _grid_csr(oracle, nx, ny, 31)
+    n = nx * ny
+    free = (P.uniform(31, 9, n) < 0.8).astype(np.uint8)
+    d = oracle.bjilu_factor(A, free, nx, tx, ty)
+    Ad = A.todense()
+    F = np.flatnonzero(free)
+    tile = lambda v: ((v % nx) // tx, (v // nx) // ty)   # noqa: E731
+    L = np.zeros((n, n)); U = np.zeros((n, n)); D = np.diag(np.where(free == 1, d, 1.0))
+    for v in F:
+        for u in F:
+            if u != v and Ad[v, u] != 0 and tile(u) == tile(v):
+                (L if u < v else U)[v, u] = Ad[v, u]
+    M = (D + L) @ np.linalg.inv(D) @ (D + U)
+    for v in F:
+        for u in F:
+            if Ad[v, u] != 0 and tile(u) == tile(v):
+                assert abs(M[v, u] - Ad[v, u]) <= 1e-12 * abs(Ad[v, v])
+    # and M^-1 r through the oracle's triangular solves equals the dense solve on F
+    r = P.gaussian(31, 10, n)
+    z = oracle.bjilu_apply(A, free, nx, tx, ty, d, r)
+    MF = M[np.ix_(F, F)]
+    assert np.max(np.abs(z[F] - np.linalg.solve(MF, r[F]))) <= 1e-12 * np.max(np.abs(z[F]))
+    assert np.all(z[free == 0] == 0.0)
+
+
+def test_bjilu_exact_on_a_single_row(oracle):
+    # one grid row inside one tile: A_F tridiagonal, ILU(0) = exact LDL' -> one PCG step solves
+    nx = 24
+    A = _grid_csr(oracle, nx, 1, 32)
+    free = np.ones(nx, np.uint8)
+    r = P.gaussian(32, 11, nx)
+    it, w, decs = oracle.pcg_bjilu(A, free, r, nx, 32, 32, 1e-300)
+    assert it == 1
+    assert np.max(np.abs(w + np.linalg.solve(A.todense(), r))) <= 1e-12 * np.max(np.abs(w))
+
+
+def test_bjilu_1x1_tiles_is_jacobi(oracle):
+    nx, ny = 9, 7
+    A = _grid_csr(oracle, nx, ny, 33)
+    free = (P.uniform(33, 9, nx * ny) < 0.7).astype(np.uint8)
+    r = P.gaussian(33, 12, nx * ny)
+    it_b, w_b, dec_b = oracle.pcg_bjilu(A, free, r, nx, 1, 1, 1e-300)
+    it_j, w_j, dec_j = oracle.pcg(A, free, r, oracle.jacobi_inverse(A), 1e-300)
+    assert it_b == it_j
+    assert np.max(np.abs(w_b - w_j)) <= 1e-12 * np.max(np.abs(w_j))
+
+
+def test_gpcg_bjilu_same_minimiser_fewer_cg_iterations(oracle):
+    prob = P.c0()
+    base = oracle.solve_problem(prob, tol=-1e-12, params=oracle.default_params(precond=1))
+    ilu = oracle.solve_problem(prob, tol=-1e-12, params=oracle.default_params(
+        precond=2, grid_nx=50, grid_ny=50, tile_x=32, tile_y=32))
+    assert base[0] == ilu[0] == 0
+    assert np.max(np.abs(base[1] - ilu[1])) <= 1e-7
+    assert ilu[2]["cg_iters"] < base[2]["cg_iters"]      # fewer CG iterations than Jacobi
