@@ -82,7 +82,9 @@ typedef struct {
     int32_t cg_chunk;    /* CG iterations per graph launch between host polls: 32          */
     int32_t gp_chunk;    /* GP steps per graph launch between host polls: 8                */
     int32_t precond;     /* 0: plain CG on A_k (the hot path); 1: point-Jacobi PCG with
-                            M = diag(A_k) (Table 4 "Diagonal")                 */
+                            M = diag(A_k) (Table 4 "Diagonal"); 2: block-
+                            Jacobi ILU(0) on 32 x 32 tiles of each slab (
+                            2-D stencils only, textbook PCG, two sweeps per iteration)     */
     int32_t cg_mode;     /* 0: A_k applied in place on masked full-length vectors (the hot
                             path, P:680-683's "alternative technique"); 1: A_k extracted
                             as a compact CSR matrix each CG call, as the paper does with

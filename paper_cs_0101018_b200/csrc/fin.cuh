@@ -107,6 +107,43 @@ __device__ __forceinline__ void cg_finalize(double gamma, double delta, Scal* S)
     S->cg_alpha = gamma / pap;
 }
 
+// ---------------------------------------------------------------- textbook PCG (block-Jacobi ILU, bjilu.cuh)
+__device__ __forceinline__ void pcg2_init_fin(double gamma, double eta2, long long cap, Scal* S) {
+    S->cg_it = 0;
+    S->cg_cap = cap;
+    S->cg_eta2 = eta2;
+    S->cg_maxdec = 0.0;
+    S->cg_dec = 0.0;
+    S->cg_gamma = gamma;
+    S->cg_rnorm0 = sqrt(gamma);
+    S->cg_beta = 0.0;
+    S->cg_alpha = 0.0;
+    S->cg_done = 0;
+    S->cg_reason = CG_RUNNING;
+    if (gamma == 0.0 || cap <= 0) { S->cg_done = 1; S->cg_reason = CG_EXACT; }
+}
+__device__ __forceinline__ void pcg2_alpha_fin(double pq, Scal* S) {
+    if (S->cg_done) return;
+    if (!(pq > 0.0)) { S->cg_done = 1; S->cg_reason = CG_NOTSPD; return; }
+    S->cg_alpha = S->cg_gamma / pq;
+}
+// after w += alpha p, r -= alpha q, z = M^-1 r: same order of tests as the oracle
+__device__ __forceinline__ void pcg2_beta_fin(double gamma_new, Scal* S) {
+    if (S->cg_done) return;
+    const double dec = 0.5 * S->cg_alpha * S->cg_gamma;
+    const long long j = S->cg_it + 1;
+    S->cg_it = j;
+    S->cg_dec = dec;
+    int reason = CG_RUNNING;
+    if (j >= 2 && dec <= S->cg_eta2 * S->cg_maxdec) reason = CG_PROGRESS;
+    else if (sqrt(gamma_new) <= 1e-14 * (1.0 + S->cg_rnorm0)) reason = CG_EXACT;
+    else if (j >= S->cg_cap) reason = CG_CAP;
+    if (dec > S->cg_maxdec) S->cg_maxdec = dec;
+    if (reason != CG_RUNNING) { S->cg_reason = reason; S->cg_done = 1; return; }
+    S->cg_beta = gamma_new / S->cg_gamma;
+    S->cg_gamma = gamma_new;
+}
+
 // ---------------------------------------------------------------- deferred mode
 enum FinKind : int {
     FIN_ACCEPT = 0,      // 6 sums (stencil kernels: + Cauchy form)
@@ -116,6 +153,9 @@ enum FinKind : int {
     FIN_CG_INIT = 4,
     FIN_CG_ITER = 5,
     FIN_R2 = 6,          // plain sums -> r0, r1 (objective, validation)
+    FIN_PCG2_INIT = 7,   // block-Jacobi ILU PCG (bjilu.cuh): gamma_0
+    FIN_PCG2_ALPHA = 8,  //   p'A p -> alpha
+    FIN_PCG2_BETA = 9,   //   r'z -> decrease, stop tests, beta
 };
 
 struct FinArgs {
@@ -163,6 +203,15 @@ __global__ void k_finalize(const double* __restrict__ t, Scal* S, FinArgs a) {
         case FIN_R2:
             S->r0 = t[0];
             S->r1 = t[1];
+            break;
+        case FIN_PCG2_INIT:
+            pcg2_init_fin(t[0], a.eta2, a.cap, S);
+            break;
+        case FIN_PCG2_ALPHA:
+            pcg2_alpha_fin(t[0], S);
+            break;
+        case FIN_PCG2_BETA:
+            pcg2_beta_fin(t[0], S);
             break;
     }
 }

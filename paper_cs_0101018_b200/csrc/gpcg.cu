@@ -41,6 +41,7 @@
 #include "tile.cuh"
 #include "march_tma.cuh"
 #include "extract.cuh"
+#include "bjilu.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -248,6 +249,8 @@ struct gpcg_problem {
     cudaGraphExec_t cg_exec = nullptr;
     int cg_exec_chunk = 0;
     cudaGraphExec_t gp_exec[2] = {nullptr, nullptr};   // GP chunk graphs starting from buffers 0 / 1
+    cudaGraphExec_t bj_exec = nullptr;  // block-Jacobi ILU PCG chunk graph (precond = 2)
+    int bj_exec_chunk = 0;
     int gp_exec_chunk = 0;
     bool gp_graph = true;           // GPCG_GP_GRAPH=0: host-driven GP steps (A/B)
     bool cg_persistent = true;      // GPCG_CG_PERSIST=0: CG as graph chunks instead of k6_cg_loop
@@ -455,6 +458,7 @@ void free_all(gpcg_problem* h) {
         if (p) cudaFree(p);
     if (h->hS) cudaFreeHost(h->hS);
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
+    if (h->bj_exec) cudaGraphExecDestroy(h->bj_exec);
     for (cudaGraphExec_t g : h->gp_exec)
         if (g) cudaGraphExecDestroy(g);
     if (h->comm && nccl_api()) nccl_api()->CommDestroy(h->comm);
@@ -1337,8 +1341,97 @@ int run_cg_extract(gpcg_problem* h, int cur, double eta2, long long cap, long lo
     return GPCG_OK;
 }
 
+// ---------------------------------------------------------------- block-Jacobi ILU(0) PCG (precond = 2)
+// Vectors: r = RHO0, z = RHO1, p = Q0 / Q1 (ping-pong), q = S0, 1/d = S1, w = W.
+int bj_grid_tiles(const gpcg_problem* h, const Slab& S, int warps_per_cta = 8) {
+    const long long nt = (long long)((h->nx + kTile - 1) / kTile) * ((S.rows + kTile - 1) / kTile);
+    return (int)std::max<long long>(1, std::min<long long>((nt + warps_per_cta - 1) / warps_per_cta,
+                                                           (long long)h->sms * 16));
+}
+
+int enqueue_bj_iter(gpcg_problem* h, int a) {
+    const int bb = a ^ 1;
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        k_pcg2_matvec<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VRHO1], S.v[vq(a)], S.v[vq(bb)], S.v[VS0],
+                                                      h->dS, h->red(s));
+        CKLAUNCH();
+    }
+    RC(finish_reduce(h, fin(FIN_PCG2_ALPHA), 1));
+    RC(exchange(h, {vq(bb)}));
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        k_pcg2_solve<1><<<bj_grid_tiles(h, S, 4), kSolveThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
+                                                                 S.v[vq(bb)], S.v[VW], S.v[VRHO1], 0.0, 0, h->dS,
+                                                                 h->red(s));
+        CKLAUNCH();
+    }
+    RC(finish_reduce(h, fin(FIN_PCG2_BETA), 1));
+    return exchange(h, {VRHO1});
+}
+
+int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
+    if (h->is_csr || h->is3d)
+        return set_err(GPCG_EINVAL, "precond = 2 (block-Jacobi ILU(0)) is implemented for 2-D stencils");
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        k_pcg2_init<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vy(cur)], S.v[VB], S.m[cur], S.m[MKCG], S.v[VRHO0],
+                                                    S.v[VQ0], S.v[VQ1], S.v[VW]);
+        CKLAUNCH();
+        k_bjilu_factor<<<bj_grid_tiles(h, S), 256, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VS1]);
+        CKLAUNCH();
+        k_pcg2_solve<0><<<bj_grid_tiles(h, S, 4), kSolveThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
+                                                                 S.v[VQ0], S.v[VW], S.v[VRHO1], eta2, cap, h->dS,
+                                                                 h->red(s));
+        CKLAUNCH();
+        h->launches += 3;
+    }
+    FinArgs a = fin(FIN_PCG2_INIT);
+    a.eta2 = eta2;
+    a.cap = cap;
+    RC(finish_reduce(h, a, 1));
+    RC(exchange(h, {VRHO1, VQ0, VQ1}, {MKCG}));
+    const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
+    if (!h->bj_exec || h->bj_exec_chunk != chunk) {
+        if (h->bj_exec) { cudaGraphExecDestroy(h->bj_exec); h->bj_exec = nullptr; }
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+        const long long l0 = h->launches;
+        int rc = GPCG_OK;
+        for (int i = 0; i < chunk && !rc; ++i) rc = enqueue_bj_iter(h, i & 1);
+        h->launches = l0;
+        cudaError_t e = cudaStreamEndCapture(h->st, &graph);
+        if (rc) { if (e == cudaSuccess) cudaGraphDestroy(graph); return rc; }
+        if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&h->bj_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+        h->bj_exec_chunk = chunk;
+    }
+    const int per_iter = 2 * h->nslabs() + (h->deferred ? 2 * (1 + (h->nslabs() > 1 ? 1 : 0)) : 0);
+    for (;;) {
+        CK(cudaEventRecord(h->ev_c0, h->st));
+        CK(cudaGraphLaunch(h->bj_exec, h->st));
+        CK(cudaEventRecord(h->ev_c1, h->st));
+        h->launches += (long long)chunk * per_iter;
+        RC(sync_scal(h));
+        if (h->hS->cg_done) break;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_c0, h->ev_c1));
+        h->t_cg_timed_ms += ms;
+        h->cg_iters_timed += chunk;
+        h->cg_free_iters_timed += chunk * m;
+    }
+    *iters = h->hS->cg_it;
+    if (h->hS->cg_reason == CG_NOTSPD)
+        return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
+                       (long long)h->hS->cg_it);
+    return exchange(h, {VW});
+}
+
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
+    if (h->prm.precond == 2) return run_cg_bjilu(h, cur, m, eta2, cap, iters);
     // cg_mode 1: always extract; 2 (auto): extract for the generic kernels (CSR, 3-D) when the
     // free set is small (m < 0.3 n), where the compact system wins
     if (h->prm.cg_mode == 1 ||
@@ -1986,7 +2079,7 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
         return set_err(GPCG_EINVAL, "eta2_shrink in (0,1), eta2_floor > 0 required");
     if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 || p->cg_cap < 0 ||
         p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096 || p->gp_chunk < 1 ||
-        p->gp_chunk > 256 || (p->precond != 0 && p->precond != 1) || (p->cg_mode < 0 || p->cg_mode > 2))
+        p->gp_chunk > 256 || p->precond < 0 || p->precond > 2 || (p->cg_mode < 0 || p->cg_mode > 2))
         return set_err(GPCG_EINVAL, "integer parameter out of range");
     const int old_chunk = h->prm.cg_chunk, old_pc = h->prm.precond;
     h->prm = *p;

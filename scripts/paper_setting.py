@@ -30,6 +30,9 @@ PAPER = {
 }
 
 
+PRECOND_NAMES = {0: "none", 1: "jacobi", 2: "bj-ilu0 (32x32 tiles)"}
+
+
 def run(grid, eps, precond):
     prob = P.journal_bearing(grid, grid, eps)
     s = gpcg.Solver.from_problem(prob, device="cuda")
@@ -42,7 +45,7 @@ def run(grid, eps, precond):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     s.close()
-    return {"grid": grid, "n": prob.n, "eps": eps, "precond": "jacobi" if precond else "none", "rc": rc,
+    return {"grid": grid, "n": prob.n, "eps": eps, "precond": PRECOND_NAMES[precond], "rc": rc,
             "iters": st["outer_iters"], "n_GP": st["gp_iters"], "cg_iters": st["cg_iters"],
             "t_cg_pct": round(100.0 * st["t_cg_ms"] / max(st["t_total_ms"], 1e-9), 1), "seconds": dt,
             "free_fraction": st["n_free"] / prob.n, "q": st["q"], "pg_norm": st["pg_norm"]}
@@ -54,7 +57,7 @@ def main():
     args = ap.parse_args()
     rows = []
     for grid, eps in [(800, 0.1), (800, 0.9), (1600, 0.1), (1600, 0.9)]:
-        for pc in (0, 1):
+        for pc in (0, 1, 2):
             r = run(grid, eps, pc)
             r["paper"] = PAPER[(grid, eps)]
             rows.append(r)

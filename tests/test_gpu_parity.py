@@ -462,3 +462,56 @@ def test_explicit_extraction_same_cg_iterates(G):
     x1, st1 = out[1]
     assert st0["cg_iters"] == st1["cg_iters"] and st0["gp_iters"] == st1["gp_iters"]
     assert np.max(np.abs(x0 - x1)) <= 1e-10 * np.max(np.abs(x0))
+
+
+# ------------------------------------------------------------------ block-Jacobi ILU(0) PCG (NEXT-3)
+BJ_CASES = ["C0", "C1", "jb80_eps0.9", "c3_family_160", "ragged37x23"]
+
+
+def _bj_params(oracle, prob):
+    return oracle.default_params(precond=2, grid_nx=prob.nx, grid_ny=prob.ny, tile_x=32, tile_y=32)
+
+
+@pytest.mark.parametrize("case", BJ_CASES)
+def test_solve_parity_bjilu(G, oracle, case):
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, params=_bj_params(oracle, prob))
+    assert rc_o == 0
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=2)
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0, (rc, st)
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
+    nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+    assert not nontie
+
+
+@pytest.mark.parametrize("case", ["C0", "ragged37x23"])
+def test_bjilu_first_outer_iteration_matches_oracle(G, oracle, case):
+    """One outer iteration (GP phase + one block-Jacobi ILU(0) PCG call + search) on the GPU
+    and in the oracle: the same algorithm on the same numbers, equal to rounding; and fewer
+    CG iterations than the point-Jacobi PCG from the same point."""
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    prm = _bj_params(oracle, prob)
+    prm.refine_cap = 1
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, max_it=1, params=prm)
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=2, refine_cap=1)
+        rc, x, st = s.solve(prob.x0, tol, max_it=1)
+    assert st["gp_iters"] == st_o["gp_iters"] and st["cg_iters"] == st_o["cg_iters"]
+    assert np.max(np.abs(x - x_o)) <= 1e-9 * max(np.max(np.abs(x_o)), 1e-300)
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=1, refine_cap=1)
+        rc1, x1, st1 = s.solve(prob.x0, tol, max_it=1)
+    assert st["cg_iters"] <= st1["cg_iters"]
+
+
+def test_bjilu_rejected_for_csr(G):
+    prob = dense_problem(8, 21)
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=2)
+        rc, x, st = s.solve(prob.x0, -1e-10, allow_error=True)
+    assert rc == G.EINVAL

@@ -159,3 +159,18 @@ def test_nccl_collectives_one_rank(G, oracle, monkeypatch, case, slabs):
     assert rc == 0 and rc_o == 0, (rc, st)
     assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
     assert np.max(np.abs(x - x_o)) <= 1e-7
+
+
+@pytest.mark.parametrize("case", ["C0", "ragged37x23_full_shift"])
+def test_slab_bjilu_reaches_the_minimiser(G, oracle, case):
+    """Block-Jacobi ILU with blocks inside each slab (the paper's one block per processor,
+    here tiles per slab): a different preconditioner per slab layout, the same x*."""
+    make, tol = CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    with G.Solver.from_problem(prob, slabs=2) as s:
+        s.set_params(precond=2)
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0 and rc_o == 0
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
