@@ -83,53 +83,87 @@ k_bjilu_factor(StencilOp A, const unsigned char* __restrict__ mask, double* __re
 }
 
 // z = M^-1 r on one tile (r already updated): forward (D + L) t = r, backward D^-1 (D + U) z = t.
-// t is kept in shared memory (32 x 32 per warp); returns this lane's sum of r z.
+// The tile's r, 1/d and mask are first staged in shared memory by coalesced row loads (the
+// wavefront steps then wait on shared memory, not on dependent global loads); z overwrites t
+// in place during the backward sweep and is stored row by row.  Returns this lane's r'z.
+struct TileSmem {
+    double r[kTile * kTile], dinv[kTile * kTile], t[kTile * kTile];
+    unsigned char m[kTile * kTile];
+};
+
 __device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0, const unsigned char* __restrict__ mask,
                                              const double* __restrict__ dinv, const double* __restrict__ r,
-                                             double* __restrict__ z, double* tsm) {
+                                             double* __restrict__ z, TileSmem& T) {
     const int lane = threadIdx.x & 31;
     const int i = x0 + lane;
+    const bool col_ok = i < A.nx;
+    for (int jl = 0; jl < kTile; ++jl) {                  // stage (coalesced rows)
+        const int j = y0 + jl;
+        const int q = jl * kTile + lane;
+        if (col_ok && j < A.ny) {
+            const long long v = i + (long long)A.pitch * j;
+            const unsigned char mv = mask[v];
+            T.m[q] = mv;
+            T.r[q] = mv ? r[v] : 0.0;
+            T.dinv[q] = mv ? dinv[v] : 0.0;
+        } else {
+            T.m[q] = 0;
+            T.r[q] = 0.0;
+            T.dinv[q] = 0.0;
+        }
+    }
+    __syncwarp();
     double t_prev = 0.0;                                  // t of (i, j-1)
     for (int l = 0; l < 2 * kTile - 1; ++l) {
         const double t_west = __shfl_up_sync(0xffffffffu, t_prev, 1);
-        const int jl = l - lane, j = y0 + jl;
+        const int jl = l - lane;
         double t_new = t_prev;
-        if (jl >= 0 && jl < kTile && i < A.nx && j < A.ny) {
-            const long long v = i + (long long)A.pitch * j;
+        if (jl >= 0 && jl < kTile) {
+            const int q = jl * kTile + lane;
             double tv = 0.0;
-            if (mask[v]) {
-                const Faces5 f = faces_at(A, i, j);
-                double s = r[v];
-                if (jl > 0 && mask[v - A.pitch]) s = s + f.s * t_prev;      // a_vs = -w_s
-                if (lane > 0 && mask[v - 1]) s = s + f.w * t_west;          // a_vw = -w_w
-                tv = s * dinv[v];
+            if (T.m[q]) {
+                const int j = y0 + jl;
+                double s = T.r[q];
+                if (jl > 0 && T.m[q - kTile]) s = s + __ldg(A.wy + (long long)j * A.wy_ld + i) * t_prev;   // a_vs = -w_s
+                if (lane > 0 && T.m[q - 1]) s = s + __ldg(A.wx + (long long)j * A.wx_ld + i) * t_west;     // a_vw = -w_w
+                tv = s * T.dinv[q];
             }
-            tsm[jl * kTile + lane] = tv;
+            T.t[q] = tv;
             t_new = tv;
         }
         t_prev = t_new;
     }
     __syncwarp();
-    double rz = 0.0, z_prev = 0.0;                        // z of (i, j+1)
+    double z_prev = 0.0;                                  // z of (i, j+1)
     for (int l = 2 * kTile - 2; l >= 0; --l) {
         const double z_east = __shfl_down_sync(0xffffffffu, z_prev, 1);
-        const int jl = l - lane, j = y0 + jl;
+        const int jl = l - lane;
         double z_new = z_prev;
-        if (jl >= 0 && jl < kTile && i < A.nx && j < A.ny) {
-            const long long v = i + (long long)A.pitch * j;
+        if (jl >= 0 && jl < kTile) {
+            const int q = jl * kTile + lane;
             double zv = 0.0;
-            if (mask[v]) {
-                const Faces5 f = faces_at(A, i, j);
+            if (T.m[q]) {
+                const int j = y0 + jl;
                 double s = 0.0;
-                if (jl < kTile - 1 && j + 1 < A.ny && mask[v + A.pitch]) s = s - f.n * z_prev;   // a_vn = -w_n
-                if (lane < kTile - 1 && i + 1 < A.nx && mask[v + 1]) s = s - f.e * z_east;       // a_ve = -w_e
-                zv = tsm[jl * kTile + lane] - s * dinv[v];
-                rz = fma(r[v], zv, rz);
+                if (jl < kTile - 1 && T.m[q + kTile]) s = s - __ldg(A.wy + (long long)(j + 1) * A.wy_ld + i) * z_prev;  // a_vn
+                if (lane < kTile - 1 && T.m[q + 1]) s = s - __ldg(A.wx + (long long)j * A.wx_ld + i + 1) * z_east;     // a_ve
+                zv = T.t[q] - s * T.dinv[q];
             }
-            z[v] = zv;
+            T.t[q] = zv;                                  // z overwrites t (t_v is not read again)
             z_new = zv;
         }
         z_prev = z_new;
+    }
+    __syncwarp();
+    double rz = 0.0;
+    for (int jl = 0; jl < kTile; ++jl) {                  // store z (coalesced rows), r'z
+        const int j = y0 + jl;
+        if (col_ok && j < A.ny) {
+            const int q = jl * kTile + lane;
+            const double zv = T.t[q];
+            z[i + (long long)A.pitch * j] = zv;
+            rz = fma(T.r[q], zv, rz);
+        }
     }
     __syncwarp();
     return rz;
@@ -154,19 +188,20 @@ k_pcg2_init(StencilOp A, const double* __restrict__ y, const double* __restrict_
     });
 }
 
-constexpr int kSolveThreads = 128;      // 4 tiles per CTA (8 KB of forward-solve scratch each)
+constexpr int kSolveThreads = 128;      // 4 tiles per CTA, one warp each
+constexpr int kSolveSmem = (kSolveThreads / 32) * (int)sizeof(TileSmem);
 
 template <int KIND>   // 0: init solve (gamma_0), 1: iteration update + solve (gamma_{j+1})
 __global__ void __launch_bounds__(kSolveThreads)
 k_pcg2_solve(StencilOp A, const unsigned char* __restrict__ mask, const double* __restrict__ dinv,
              double* __restrict__ r, const double* __restrict__ q, const double* __restrict__ p,
              double* __restrict__ w, double* __restrict__ z, double eta2, long long cap, Scal* S, RedScratch R) {
-    __shared__ double tsm[kSolveThreads / 32][kTile * kTile];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     if (KIND == 1 && *(volatile int*)&S->cg_done) return;
     const double alpha = KIND == 1 ? S->cg_alpha : 0.0;
     double acc[1] = {0.0};
     const int lane = threadIdx.x & 31;
-    double* my = tsm[threadIdx.x >> 5];
+    TileSmem& T = reinterpret_cast<TileSmem*>(smem_raw)[threadIdx.x >> 5];
     for_each_tile(A, [&](int x0, int y0) {
         if (KIND == 1) {                                  // w += alpha p, r -= alpha q on the tile
             const int i = x0 + lane;
@@ -180,7 +215,7 @@ k_pcg2_solve(StencilOp A, const unsigned char* __restrict__ mask, const double* 
                 }
             __syncwarp();
         }
-        acc[0] += tile_solve(A, x0, y0, mask, dinv, r, z, my);
+        acc[0] += tile_solve(A, x0, y0, mask, dinv, r, z, T);
     });
     reduce_and_finish<1>(acc, R, [&](double* t) {
         if (KIND == 0) pcg2_init_fin(t[0], eta2, cap, S);

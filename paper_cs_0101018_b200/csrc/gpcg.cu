@@ -1361,7 +1361,7 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
     RC(exchange(h, {vq(bb)}));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        k_pcg2_solve<1><<<bj_grid_tiles(h, S, 4), kSolveThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
+        k_pcg2_solve<1><<<bj_grid_tiles(h, S, 4), kSolveThreads, kSolveSmem, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
                                                                  S.v[vq(bb)], S.v[VW], S.v[VRHO1], 0.0, 0, h->dS,
                                                                  h->red(s));
         CKLAUNCH();
@@ -1373,6 +1373,8 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
 int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     if (h->is_csr || h->is3d)
         return set_err(GPCG_EINVAL, "precond = 2 (block-Jacobi ILU(0)) is implemented for 2-D stencils");
+    RC(set_smem(k_pcg2_solve<0>, kSolveSmem));
+    RC(set_smem(k_pcg2_solve<1>, kSolveSmem));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         k_pcg2_init<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vy(cur)], S.v[VB], S.m[cur], S.m[MKCG], S.v[VRHO0],
@@ -1380,7 +1382,7 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
         CKLAUNCH();
         k_bjilu_factor<<<bj_grid_tiles(h, S), 256, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VS1]);
         CKLAUNCH();
-        k_pcg2_solve<0><<<bj_grid_tiles(h, S, 4), kSolveThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
+        k_pcg2_solve<0><<<bj_grid_tiles(h, S, 4), kSolveThreads, kSolveSmem, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
                                                                  S.v[VQ0], S.v[VW], S.v[VRHO1], eta2, cap, h->dS,
                                                                  h->red(s));
         CKLAUNCH();

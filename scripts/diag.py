@@ -14,6 +14,8 @@ for name in sys.argv[1:]:
     prob = P.get(name)
     t1 = time.time()
     s = gpcg.Solver.from_problem(prob, device="cuda")
+    if os.environ.get("GPCG_PRECOND"):
+        s.set_params(precond=int(os.environ["GPCG_PRECOND"]))
     x0 = torch.from_numpy(prob.x0).cuda()
     torch.cuda.synchronize()
     t2 = time.time()
