@@ -97,20 +97,19 @@ __device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0,
     const int lane = threadIdx.x & 31;
     const int i = x0 + lane;
     const bool col_ok = i < A.nx;
-    for (int jl = 0; jl < kTile; ++jl) {                  // stage (coalesced rows)
+    // stage (coalesced rows; unrolled so that many rows' loads are in flight at once)
+    const int ic = col_ok ? i : x0;                       // in-grid address for the predicated-off lanes
+#pragma unroll 8
+    for (int jl = 0; jl < kTile; ++jl) {
         const int j = y0 + jl;
+        const bool in = col_ok && j < A.ny;
+        const long long v = ic + (long long)A.pitch * min(j, A.ny - 1);
+        const unsigned char mv = in ? mask[v] : 0;
+        const double rv = r[v], dv = dinv[v];
         const int q = jl * kTile + lane;
-        if (col_ok && j < A.ny) {
-            const long long v = i + (long long)A.pitch * j;
-            const unsigned char mv = mask[v];
-            T.m[q] = mv;
-            T.r[q] = mv ? r[v] : 0.0;
-            T.dinv[q] = mv ? dinv[v] : 0.0;
-        } else {
-            T.m[q] = 0;
-            T.r[q] = 0.0;
-            T.dinv[q] = 0.0;
-        }
+        T.m[q] = mv;
+        T.r[q] = mv ? rv : 0.0;
+        T.dinv[q] = mv ? dv : 0.0;
     }
     __syncwarp();
     double t_prev = 0.0;                                  // t of (i, j-1)
@@ -156,6 +155,7 @@ __device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0,
     }
     __syncwarp();
     double rz = 0.0;
+#pragma unroll 8
     for (int jl = 0; jl < kTile; ++jl) {                  // store z (coalesced rows), r'z
         const int j = y0 + jl;
         if (col_ok && j < A.ny) {
@@ -205,14 +205,19 @@ k_pcg2_solve(StencilOp A, const unsigned char* __restrict__ mask, const double* 
     for_each_tile(A, [&](int x0, int y0) {
         if (KIND == 1) {                                  // w += alpha p, r -= alpha q on the tile
             const int i = x0 + lane;
-            if (i < A.nx)
-                for (int jl = 0; jl < kTile && y0 + jl < A.ny; ++jl) {
-                    const long long v = i + (long long)A.pitch * (y0 + jl);
-                    if (mask[v]) {
-                        w[v] = fma(alpha, p[v], w[v]);
-                        r[v] = fma(-alpha, q[v], r[v]);
-                    }
+            const int ic = i < A.nx ? i : x0;
+#pragma unroll 8
+            for (int jl = 0; jl < kTile; ++jl) {          // unconditional loads: rows in flight together
+                const int j = y0 + jl;
+                const bool in = i < A.nx && j < A.ny;
+                const long long v = ic + (long long)A.pitch * min(j, A.ny - 1);
+                const unsigned char mv = mask[v];
+                const double pv = p[v], wv = w[v], qv = q[v], rv = r[v];
+                if (in && mv) {
+                    w[v] = fma(alpha, pv, wv);
+                    r[v] = fma(-alpha, qv, rv);
                 }
+            }
             __syncwarp();
         }
         acc[0] += tile_solve(A, x0, y0, mask, dinv, r, z, T);
