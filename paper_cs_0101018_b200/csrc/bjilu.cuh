@@ -7,25 +7,33 @@
 // A_k in natural order; ILU(0) keeps the 5-point pattern, so only the pivots change:
 //     d_v = a_vv - a_vs^2 / d_s - a_vw^2 / d_w      (south / west neighbour in the tile, free)
 // and M = (D + L) D^-1 (D + U) (oracle/gpcg_oracle.c ora_bjilu_*).  One warp owns a tile:
-// lane i is column i, and anti-diagonal l = i + j is step l of a 63-step wavefront -- the
-// west neighbour of (i, j) was computed by lane i-1 one step earlier (warp shuffle), the
-// south neighbour by the same lane one step earlier (register) -- so the factorisation and
-// both triangular solves run in registers with no barrier.
+// lane i is column i, and anti-diagonal l = i + jl is step l of a 63-step wavefront -- the
+// west neighbour of (i, jl) was computed by lane i-1 one step earlier (warp shuffle), the
+// south neighbour by the same lane one step earlier (register).  The factor is stored, and
+// the tile staged, in a skewed layout (sk() below) in which every wavefront step is one
+// contiguous row, so a step costs a shared-memory access, two FMAs and a shuffle; the factor
+// loads are independent of the recurrence and run ahead of it.
 //
 // PCG (textbook form, the oracle's ora_pcg_m): per iteration
-//   k_pcg2_matvec: p = z + beta p (at the point and its neighbours), q = A_F p, sum p'q
+//   k_pcg2_matvec: w += alpha_prev p_old, p = z + beta p (at the point and its neighbours),
+//                  q = A_F p, sum p'q
 //                  -> alpha = gamma / p'q
-//   k_pcg2_update: w += alpha p, r -= alpha q, z = M^-1 r (tile wavefronts), sum r'z
+//   k_pcg2_solve<1>: r -= alpha q, z = M^-1 r (tile wavefronts), sum r'z
 //                  -> decrease 1/2 alpha gamma, cgstop1 / exact guard / cap, beta
-// Vectors (full length, zero off F): r, z, p (ping-pong), q, w, 1/d.
+// Vectors (full length, zero off F): r, z, p (ping-pong), q; the factor (BjFactor) per slab.
 #pragma once
 
 #include "common.cuh"
 #include "fin.cuh"
+#include "march.cuh"
 
 namespace gpcg {
 
 constexpr int kTile = 32;
+#ifndef GPCG_BJ_UNROLL
+#define GPCG_BJ_UNROLL 8
+#endif
+constexpr int kBjUnroll = GPCG_BJ_UNROLL;                 // wavefront steps unrolled (factor loads in flight)
 
 // face weights / diagonal of point (i, j) of the slab (StencilOp layout)
 struct Faces5 {
@@ -42,128 +50,148 @@ __device__ __forceinline__ Faces5 faces_at(const StencilOp& A, int i, int j) {
     return f;
 }
 
-// tiles of the slab, one per warp (grid-stride over tiles)
+// tiles of the slab, one per warp (grid-stride over tiles); body(x0, y0, tile index)
 template <class Body>
 __device__ __forceinline__ void for_each_tile(const StencilOp& A, Body&& body) {
     const int ntx = (A.nx + kTile - 1) / kTile, nty = (A.ny + kTile - 1) / kTile;
     const int nt = ntx * nty;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int t = warp; t < nt; t += nw) body((t % ntx) * kTile, (t / ntx) * kTile);
+    for (int t = warp; t < nt; t += nw) body((t % ntx) * kTile, (t / ntx) * kTile, t);
 }
 
-// ILU(0) pivots of every tile on the CG mask -> dinv = 1 / d (1 off F)
-__global__ void __launch_bounds__(256)
-k_bjilu_factor(StencilOp A, const unsigned char* __restrict__ mask, double* __restrict__ dinv) {
-    const int lane = threadIdx.x & 31;
-    for_each_tile(A, [&](int x0, int y0) {
+// Skewed tile layout of the factor (and of the per-warp shared-memory staging): element
+// (i, jl) of a tile sits at row (i + jl) mod 32, column i.  Wavefront step l touches the
+// points with i + jl = l, i.e. row l mod 32 -- 32 consecutive doubles (lanes with
+// i + jl = l and i + jl = l - 32 never coexist in one step, so the map is a bijection and
+// each step is one coalesced 256-byte access); a row-major pass over the tile (fixed jl,
+// lane i) hits 32 distinct bank pairs.
+__device__ __forceinline__ int sk(int i, int jl) { return ((i + jl) & (kTile - 1)) * kTile + i; }
+
+// The factor of every tile in the skewed layout, kTile^2 doubles per tile and array:
+//   dinv = 1 / d_v on F, 0 off F (so the solves need no mask: off F every t, z is 0),
+//   cs   = w_s (the coupling -a_vs) if v, s in F and s in the tile, else 0,
+//   cw   = w_w likewise for the west neighbour.
+// The backward solve reads the north / east couplings as cs of (i, jl + 1) and cw of (i + 1, jl)
+// (A symmetric; cs of a tile's row 0 and cw of its column 0 are 0, which drops the couplings
+// across tile edges).
+struct BjFactor {
+    double *dinv, *cs, *cw;
+};
+
+constexpr int kBjThreads = 64;                                        // 2 tiles per CTA
+constexpr int kBjMinBlocks = 10;                                      // 20 tiles / SM in flight
+constexpr int kFactorSmem = (kBjThreads / 32) * kTile * kTile * (3 * 8 + 1);
+constexpr int kSolveSmem = (kBjThreads / 32) * kTile * kTile * 8;
+
+// ILU(0) pivots of every tile on the CG mask: d_v = a_vv - cs^2 / d_s - cw^2 / d_w (south first,
+// the oracle's column order).  Staged per warp in shared memory (skewed), then one 63-step
+// wavefront; cs / cw go out as soon as they are formed, dinv at its wavefront step.
+__global__ void __launch_bounds__(kBjThreads)
+k_bjilu_factor(StencilOp A, const unsigned char* __restrict__ mask, BjFactor F) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double* Da = reinterpret_cast<double*>(smem_raw) + wid * 3 * kTile * kTile;
+    double* Ds = Da + kTile * kTile;
+    double* Dw = Ds + kTile * kTile;
+    unsigned char* Mf = smem_raw + (kBjThreads / 32) * 3 * kTile * kTile * 8 + wid * kTile * kTile;
+    for_each_tile(A, [&](int x0, int y0, int tt) {
+        const long long tb = (long long)tt * kTile * kTile;
         const int i = x0 + lane;
-        double d_prev = 1.0;                              // d of (i, j-1): this lane, previous step
-        for (int l = 0; l < 2 * kTile - 1; ++l) {
-            const double d_west = __shfl_up_sync(0xffffffffu, d_prev, 1);   // (i-1, j) from step l-1
-            const int j = y0 + l - lane;
-            double d_new = d_prev;
-            if (l - lane >= 0 && l - lane < kTile && i < A.nx && j < A.ny) {
+        for (int jl = 0; jl < kTile; ++jl) {
+            const int j = y0 + jl;
+            const int q = sk(lane, jl);
+            double a = 0.0, cs = 0.0, cw = 0.0;
+            unsigned char f = 0;
+            if (i < A.nx && j < A.ny) {
                 const long long v = i + (long long)A.pitch * j;
                 if (mask[v]) {
-                    const Faces5 f = faces_at(A, i, j);
-                    double dv = f.d;
-                    if (j > y0 && mask[v - A.pitch]) dv = dv - f.s * f.s / d_prev;          // south
-                    if (lane > 0 && mask[v - 1]) dv = dv - f.w * f.w / d_west;              // west
-                    d_new = dv;
-                    dinv[v] = 1.0 / dv;
-                } else {
-                    d_new = 1.0;
-                    dinv[v] = 1.0;
+                    const Faces5 fc = faces_at(A, i, j);
+                    a = fc.d;
+                    if (jl > 0 && mask[v - A.pitch]) cs = fc.s;
+                    if (lane > 0 && mask[v - 1]) cw = fc.w;
+                    f = 1;
                 }
             }
-            d_prev = d_new;
+            Da[q] = a;
+            Ds[q] = cs;
+            Dw[q] = cw;
+            Mf[q] = f;
+            F.cs[tb + q] = cs;
+            F.cw[tb + q] = cw;
         }
+        __syncwarp();
+        double d_prev = 1.0;                              // d of (i, jl - 1): this lane, previous step
+        for (int l = 0; l < 2 * kTile - 1; ++l) {
+            const double d_west = __shfl_up_sync(0xffffffffu, d_prev, 1);   // (i - 1, jl), step l - 1
+            if ((unsigned)(l - lane) < (unsigned)kTile) {
+                const int q = (l & (kTile - 1)) * kTile + lane;
+                double dn = 1.0, di = 0.0;
+                if (Mf[q]) {
+                    const double cs = Ds[q], cw = Dw[q];
+                    dn = Da[q] - cs * cs / d_prev - cw * cw / d_west;
+                    di = 1.0 / dn;
+                }
+                F.dinv[tb + q] = di;
+                d_prev = dn;
+            }
+        }
+        __syncwarp();
     });
 }
 
-// z = M^-1 r on one tile (r already updated): forward (D + L) t = r, backward D^-1 (D + U) z = t.
-// The tile's r, 1/d and mask are first staged in shared memory by coalesced row loads (the
-// wavefront steps then wait on shared memory, not on dependent global loads); z overwrites t
-// in place during the backward sweep and is stored row by row.  Returns this lane's r'z.
-struct TileSmem {
-    double r[kTile * kTile], dinv[kTile * kTile], t[kTile * kTile];
-    unsigned char m[kTile * kTile];
-};
-
-__device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0, const unsigned char* __restrict__ mask,
-                                             const double* __restrict__ dinv, const double* __restrict__ r,
-                                             double* __restrict__ z, TileSmem& T) {
+// z = M^-1 r on one tile whose r is staged (skewed) in T: forward (D + L) t = r, backward
+// D^-1 (D + U) z = t, both in place in T; then z is stored row by row.  Returns this lane's
+// share of r'z, formed in the forward sweep as t'D t = sum t_v (D t)_v: with U = L^T,
+// r'z = r'(D + U)^-1 D t = ((D + L)^-1 r)' D t = t'D t, and (D t)_v is the sum the step
+// forms before scaling by 1/d_v (so r need not be kept or re-read).  The factor rows of each
+// step are chain-independent loads, hoisted ahead of the dependent t / z recurrences by the
+// full unroll; the recurrences touch only registers, shuffles and T.
+__device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0, long long tb, const BjFactor& F,
+                                             double* __restrict__ z, double* T) {
     const int lane = threadIdx.x & 31;
-    const int i = x0 + lane;
-    const bool col_ok = i < A.nx;
-    // stage (coalesced rows; unrolled so that many rows' loads are in flight at once)
-    const int ic = col_ok ? i : x0;                       // in-grid address for the predicated-off lanes
-#pragma unroll 8
-    for (int jl = 0; jl < kTile; ++jl) {
-        const int j = y0 + jl;
-        const bool in = col_ok && j < A.ny;
-        const long long v = ic + (long long)A.pitch * min(j, A.ny - 1);
-        const unsigned char mv = in ? mask[v] : 0;
-        const double rv = r[v], dv = dinv[v];
-        const int q = jl * kTile + lane;
-        T.m[q] = mv;
-        T.r[q] = mv ? rv : 0.0;
-        T.dinv[q] = mv ? dv : 0.0;
-    }
+    const double* Fd = F.dinv + tb + lane;
+    const double* Fs = F.cs + tb + lane;
+    const double* Fw = F.cw + tb + lane;
     __syncwarp();
-    double t_prev = 0.0;                                  // t of (i, j-1)
-    for (int l = 0; l < 2 * kTile - 1; ++l) {
-        const double t_west = __shfl_up_sync(0xffffffffu, t_prev, 1);
-        const int jl = l - lane;
-        double t_new = t_prev;
-        if (jl >= 0 && jl < kTile) {
-            const int q = jl * kTile + lane;
-            double tv = 0.0;
-            if (T.m[q]) {
-                const int j = y0 + jl;
-                double s = T.r[q];
-                if (jl > 0 && T.m[q - kTile]) s = s + __ldg(A.wy + (long long)j * A.wy_ld + i) * t_prev;   // a_vs = -w_s
-                if (lane > 0 && T.m[q - 1]) s = s + __ldg(A.wx + (long long)j * A.wx_ld + i) * t_west;     // a_vw = -w_w
-                tv = s * T.dinv[q];
-            }
-            T.t[q] = tv;
-            t_new = tv;
-        }
-        t_prev = t_new;
-    }
-    __syncwarp();
-    double z_prev = 0.0;                                  // z of (i, j+1)
-    for (int l = 2 * kTile - 2; l >= 0; --l) {
-        const double z_east = __shfl_down_sync(0xffffffffu, z_prev, 1);
-        const int jl = l - lane;
-        double z_new = z_prev;
-        if (jl >= 0 && jl < kTile) {
-            const int q = jl * kTile + lane;
-            double zv = 0.0;
-            if (T.m[q]) {
-                const int j = y0 + jl;
-                double s = 0.0;
-                if (jl < kTile - 1 && T.m[q + kTile]) s = s - __ldg(A.wy + (long long)(j + 1) * A.wy_ld + i) * z_prev;  // a_vn
-                if (lane < kTile - 1 && T.m[q + 1]) s = s - __ldg(A.wx + (long long)j * A.wx_ld + i + 1) * z_east;     // a_ve
-                zv = T.t[q] - s * T.dinv[q];
-            }
-            T.t[q] = zv;                                  // z overwrites t (t_v is not read again)
-            z_new = zv;
-        }
-        z_prev = z_new;
-    }
-    __syncwarp();
+    double t_prev = 0.0;                                  // t of (i, jl - 1)
     double rz = 0.0;
-#pragma unroll 8
-    for (int jl = 0; jl < kTile; ++jl) {                  // store z (coalesced rows), r'z
-        const int j = y0 + jl;
-        if (col_ok && j < A.ny) {
-            const int q = jl * kTile + lane;
-            const double zv = T.t[q];
-            z[i + (long long)A.pitch * j] = zv;
-            rz = fma(T.r[q], zv, rz);
+#pragma unroll kBjUnroll
+    for (int l = 0; l < 2 * kTile - 1; ++l) {
+        const int row = (l & (kTile - 1)) * kTile;
+        const double dv = __ldg(Fd + row), cs = __ldg(Fs + row), cw = __ldg(Fw + row);
+        const double t_west = __shfl_up_sync(0xffffffffu, t_prev, 1);   // (i - 1, jl), step l - 1
+        const double sv = T[row + lane] + cs * t_prev + cw * t_west;    // (D t)_v
+        const double tv = sv * dv;
+        if ((unsigned)(l - lane) < (unsigned)kTile) {
+            T[row + lane] = tv;
+            t_prev = tv;
+            rz = fma(tv, sv, rz);
         }
+    }
+    __syncwarp();
+    double z_prev = 0.0;                                  // z of (i, jl + 1)
+#pragma unroll kBjUnroll
+    for (int l = 2 * kTile - 2; l >= 0; --l) {
+        const int row = (l & (kTile - 1)) * kTile, nrow = ((l + 1) & (kTile - 1)) * kTile;
+        const double dv = __ldg(Fd + row);
+        const double cn = __ldg(Fs + nrow);               // cs of (i, jl + 1); 0 when jl = 31
+        const double cwn = __ldg(Fw + nrow);              // lane i+1's value is cw of (i + 1, jl)
+        const double z_east = __shfl_down_sync(0xffffffffu, z_prev, 1);  // (i + 1, jl), step l + 1
+        const double cwe = __shfl_down_sync(0xffffffffu, cwn, 1);           // all lanes take part
+        const double ce = lane < kTile - 1 ? cwe : 0.0;
+        const double zv = T[row + lane] + (ce * z_east + cn * z_prev) * dv;
+        if ((unsigned)(l - lane) < (unsigned)kTile) {
+            T[row + lane] = zv;
+            z_prev = zv;
+        }
+    }
+    __syncwarp();
+    const int i = x0 + lane;
+#pragma unroll 8
+    for (int jl = 0; jl < kTile; ++jl) {                  // store z (coalesced rows)
+        const int j = y0 + jl;
+        if (i < A.nx && j < A.ny) z[i + (long long)A.pitch * j] = T[sk(lane, jl)];
     }
     __syncwarp();
     return rz;
@@ -188,39 +216,35 @@ k_pcg2_init(StencilOp A, const double* __restrict__ y, const double* __restrict_
     });
 }
 
-constexpr int kSolveThreads = 128;      // 4 tiles per CTA, one warp each
-constexpr int kSolveSmem = (kSolveThreads / 32) * (int)sizeof(TileSmem);
-
 template <int KIND>   // 0: init solve (gamma_0), 1: iteration update + solve (gamma_{j+1})
-__global__ void __launch_bounds__(kSolveThreads)
-k_pcg2_solve(StencilOp A, const unsigned char* __restrict__ mask, const double* __restrict__ dinv,
-             double* __restrict__ r, const double* __restrict__ q, const double* __restrict__ p,
-             double* __restrict__ w, double* __restrict__ z, double eta2, long long cap, Scal* S, RedScratch R) {
+__global__ void __launch_bounds__(kBjThreads, kBjMinBlocks)
+k_pcg2_solve(StencilOp A, BjFactor F, double* __restrict__ r, const double* __restrict__ q,
+             double* __restrict__ z, double eta2, long long cap, Scal* S, RedScratch R) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (KIND == 1 && *(volatile int*)&S->cg_done) return;
     const double alpha = KIND == 1 ? S->cg_alpha : 0.0;
     double acc[1] = {0.0};
     const int lane = threadIdx.x & 31;
-    TileSmem& T = reinterpret_cast<TileSmem*>(smem_raw)[threadIdx.x >> 5];
-    for_each_tile(A, [&](int x0, int y0) {
-        if (KIND == 1) {                                  // w += alpha p, r -= alpha q on the tile
-            const int i = x0 + lane;
-            const int ic = i < A.nx ? i : x0;
+    double* T = reinterpret_cast<double*>(smem_raw) + (threadIdx.x >> 5) * kTile * kTile;
+    for_each_tile(A, [&](int x0, int y0, int tt) {
+        const int i = x0 + lane;
+        const int ic = i < A.nx ? i : x0;
+        // KIND 1: r -= alpha q (r and q are 0 off F, so no mask); stage r skewed in T (0 outside
+        // the grid).  w += alpha p is deferred to the next k_pcg2_matvec (k_pcg2_wlast after the
+        // last iteration).
 #pragma unroll 8
-            for (int jl = 0; jl < kTile; ++jl) {          // unconditional loads: rows in flight together
-                const int j = y0 + jl;
-                const bool in = i < A.nx && j < A.ny;
-                const long long v = ic + (long long)A.pitch * min(j, A.ny - 1);
-                const unsigned char mv = mask[v];
-                const double pv = p[v], wv = w[v], qv = q[v], rv = r[v];
-                if (in && mv) {
-                    w[v] = fma(alpha, pv, wv);
-                    r[v] = fma(-alpha, qv, rv);
-                }
+        for (int jl = 0; jl < kTile; ++jl) {
+            const int j = y0 + jl;
+            const bool in = i < A.nx && j < A.ny;
+            const long long v = ic + (long long)A.pitch * min(j, A.ny - 1);
+            double rv = r[v];
+            if (KIND == 1) {
+                rv = fma(-alpha, q[v], rv);
+                if (in) r[v] = rv;
             }
-            __syncwarp();
+            T[sk(lane, jl)] = in ? rv : 0.0;
         }
-        acc[0] += tile_solve(A, x0, y0, mask, dinv, r, z, T);
+        acc[0] += tile_solve(A, x0, y0, (long long)tt * kTile * kTile, F, z, T);
     });
     reduce_and_finish<1>(acc, R, [&](double* t) {
         if (KIND == 0) pcg2_init_fin(t[0], eta2, cap, S);
@@ -231,14 +255,16 @@ k_pcg2_solve(StencilOp A, const unsigned char* __restrict__ mask, const double* 
 // p_new = z + beta p_old (zero off F; formed at the neighbours too), q = A_F p_new, sum p'q
 __global__ void __launch_bounds__(kThreads)
 k_pcg2_matvec(StencilOp A, const unsigned char* __restrict__ mask, const double* __restrict__ z,
-              const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q, Scal* S,
-              RedScratch R) {
+              const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
+              double* __restrict__ w, Scal* S, RedScratch R) {
     if (*(volatile int*)&S->cg_done) return;
     const double beta = S->cg_beta;
+    const double alpha_prev = S->cg_alpha;                // alpha of the previous iteration (0 at the first)
     double acc[1] = {0.0};
     A.for_each_point([&](const Pt& pt) {
         const int v = pt.v;
         if (!mask[v]) { p_new[v] = 0.0; q[v] = 0.0; return; }
+        w[v] = fma(alpha_prev, p_old[v], w[v]);           // the previous iteration's w += alpha p
         double qv = 0.0, pv = 0.0;
         A.for_each_nbr(pt, [&](int c, double a) {
             if (!mask[c]) return;
@@ -251,6 +277,81 @@ k_pcg2_matvec(StencilOp A, const unsigned char* __restrict__ mask, const double*
         acc[0] = fma(pv, qv, acc[0]);
     });
     reduce_and_finish<1>(acc, R, [&](double* t) { pcg2_alpha_fin(t[0], S); });
+}
+
+// The same step on the column march (march.cuh, H = 1): level 1 forms p(r) once per point,
+// level 2 applies A at row r - 1 from registers and shuffles; w, p_new, q written at r - 1.
+struct RawPm {
+    double z, p;
+    unsigned char m;
+};
+
+template <bool BC>
+__global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
+k2_pcg2_matvec(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask, const double* __restrict__ z,
+               const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
+               double* __restrict__ w, Scal* S, RedScratch R) {
+    if (*(volatile int*)&S->cg_done) return;
+    const double beta = S->cg_beta;
+    const double alpha_prev = S->cg_alpha;                // alpha of the previous iteration (0 at the first)
+    constexpr int H = 1;
+    const int lane = threadIdx.x & 31;
+    const bool out_lane = lane >= H && lane < 32 - H;
+    double acc[1] = {0.0};
+    int i, j0, j1;
+    if (march_item<H>(A, G, i, j0, j1)) {
+        const bool col_ok = (i >= 0 && i < A.nx);
+        Op5<BC> op;
+        op.init(A, i);
+        const int rend = min(A.rhi, j1 + H);
+        double pn_m2 = 0.0, pn_m1 = 0.0;                  // p_new(r-2), p_new(r-1)
+        double po_m1 = 0.0;                               // p_old(r-1)
+        unsigned char m_m1 = 0;
+        pipeline<unsigned char, RawPm>(
+            j0 - 1, j1 - j0 + 2,
+            [&](int r) -> unsigned char {
+                unsigned char m = 0;
+                if (r >= A.rlo && r < rend && col_ok) m = __ldg(mask + i + A.pitch * r);
+                return m;
+            },
+            [&](int r, unsigned char m) {
+                RawPm x{0.0, 0.0, m};
+                if (m) {
+                    const int v = i + A.pitch * r;
+                    x.z = z[v];
+                    x.p = p_old[v];
+                }
+                return x;
+            },
+            [&](int r, const RawPm& x) {
+                const double pn0 = x.m ? fma(beta, x.p, x.z) : 0.0;
+                const double qv = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
+                const int r1 = r - 1;
+                if (out_lane && col_ok && r1 >= j0 && r1 < j1) {
+                    const int v = i + A.pitch * r1;
+                    if (m_m1) {
+                        w[v] = fma(alpha_prev, po_m1, w[v]);
+                        p_new[v] = pn_m1;
+                        q[v] = qv;
+                        acc[0] = fma(pn_m1, qv, acc[0]);
+                    } else {
+                        p_new[v] = 0.0;
+                        q[v] = 0.0;
+                    }
+                }
+                pn_m2 = pn_m1; pn_m1 = pn0;
+                po_m1 = x.p;
+                m_m1 = x.m;
+            });
+    }
+    reduce_and_finish<1>(acc, R, [&](double* t) { pcg2_alpha_fin(t[0], S); });
+}
+
+// after the last iteration j: w += alpha_j p_j (p is 0 off F)
+__global__ void __launch_bounds__(kThreads)
+k_pcg2_wlast(StencilOp A, const double* __restrict__ p, double* __restrict__ w, const Scal* S) {
+    const double alpha = S->cg_alpha;
+    A.for_each_point([&](const Pt& pt) { w[pt.v] = fma(alpha, p[pt.v], w[pt.v]); });
 }
 
 }  // namespace gpcg

@@ -197,6 +197,7 @@ struct Slab {
     double* xval = nullptr;
     double* xv[12] = {};                      // gF, dinvF, rho x2, q x2, s x2, p, w, (spare)
     unsigned char *xmask = nullptr, *xmaskcg = nullptr;
+    double* bjf = nullptr;                    // block-Jacobi ILU(0) factor (precond = 2): 3 x tiles x 32^2
     int grid4_cg = 1, grid4_acc = 1, grid4_srch = 1;
     // g-free sweeps (k5_*): 112-column boxes from x0 - 4, 128-byte mask boxes, 104-column bands
     CUtensorMap t5[NVEC];
@@ -449,7 +450,7 @@ void free_all(gpcg_problem* h) {
     if (h->st) cudaStreamSynchronize(h->st);
     for (Slab& S : h->slabs) {
         if (S.arena) cudaFree(S.arena);
-        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, S.xarena, (void*)S.rp,
+        for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, S.xarena, (void*)S.bjf, (void*)S.rp,
                         (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             if (p) cudaFree(p);
@@ -1342,28 +1343,42 @@ int run_cg_extract(gpcg_problem* h, int cur, double eta2, long long cap, long lo
 }
 
 // ---------------------------------------------------------------- block-Jacobi ILU(0) PCG (precond = 2)
-// Vectors: r = RHO0, z = RHO1, p = Q0 / Q1 (ping-pong), q = S0, 1/d = S1, w = W.
-int bj_grid_tiles(const gpcg_problem* h, const Slab& S, int warps_per_cta = 8) {
-    const long long nt = (long long)((h->nx + kTile - 1) / kTile) * ((S.rows + kTile - 1) / kTile);
-    return (int)std::max<long long>(1, std::min<long long>((nt + warps_per_cta - 1) / warps_per_cta,
-                                                           (long long)h->sms * 16));
+// Vectors: r = RHO0, z = RHO1, p = Q0 / Q1 (ping-pong), q = S0, w = W; the factor in Slab::bjf.
+long long bj_tiles(const gpcg_problem* h, const Slab& S) {
+    return (long long)((h->nx + kTile - 1) / kTile) * ((S.rows + kTile - 1) / kTile);
+}
+
+int bj_grid_tiles(const gpcg_problem* h, const Slab& S) {
+    const int wpc = kBjThreads / 32;
+    return (int)std::max<long long>(1, std::min<long long>((bj_tiles(h, S) + wpc - 1) / wpc, (long long)h->sms * 16));
+}
+
+BjFactor bj_factor(const Slab& S, long long nt) {
+    const long long e = nt * kTile * kTile;
+    return BjFactor{S.bjf, S.bjf + e, S.bjf + 2 * e};
 }
 
 int enqueue_bj_iter(gpcg_problem* h, int a) {
     const int bb = a ^ 1;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        k_pcg2_matvec<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VRHO1], S.v[vq(a)], S.v[vq(bb)], S.v[VS0],
-                                                      h->dS, h->red(s));
+        if (h->generic)
+            k_pcg2_matvec<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VRHO1], S.v[vq(a)], S.v[vq(bb)],
+                                                          S.v[VS0], S.v[VW], h->dS, h->red(s));
+        else if (h->bc)
+            k2_pcg2_matvec<true><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.m[MKCG], S.v[VRHO1], S.v[vq(a)],
+                                                                         S.v[vq(bb)], S.v[VS0], S.v[VW], h->dS, h->red(s));
+        else
+            k2_pcg2_matvec<false><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.m[MKCG], S.v[VRHO1], S.v[vq(a)],
+                                                                          S.v[vq(bb)], S.v[VS0], S.v[VW], h->dS, h->red(s));
         CKLAUNCH();
     }
     RC(finish_reduce(h, fin(FIN_PCG2_ALPHA), 1));
     RC(exchange(h, {vq(bb)}));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        k_pcg2_solve<1><<<bj_grid_tiles(h, S, 4), kSolveThreads, kSolveSmem, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
-                                                                 S.v[vq(bb)], S.v[VW], S.v[VRHO1], 0.0, 0, h->dS,
-                                                                 h->red(s));
+        k_pcg2_solve<1><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, bj_tiles(h, S)), S.v[VRHO0],
+                                                                              S.v[VS0], S.v[VRHO1], 0.0, 0, h->dS, h->red(s));
         CKLAUNCH();
     }
     RC(finish_reduce(h, fin(FIN_PCG2_BETA), 1));
@@ -1373,18 +1388,20 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
 int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     if (h->is_csr || h->is3d)
         return set_err(GPCG_EINVAL, "precond = 2 (block-Jacobi ILU(0)) is implemented for 2-D stencils");
+    RC(set_smem(k_bjilu_factor, kFactorSmem));
     RC(set_smem(k_pcg2_solve<0>, kSolveSmem));
     RC(set_smem(k_pcg2_solve<1>, kSolveSmem));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
+        const long long nt = bj_tiles(h, S);
+        if (!S.bjf) CK(cudaMalloc(&S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double)));
         k_pcg2_init<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vy(cur)], S.v[VB], S.m[cur], S.m[MKCG], S.v[VRHO0],
                                                     S.v[VQ0], S.v[VQ1], S.v[VW]);
         CKLAUNCH();
-        k_bjilu_factor<<<bj_grid_tiles(h, S), 256, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VS1]);
+        k_bjilu_factor<<<bj_grid_tiles(h, S), kBjThreads, kFactorSmem, h->st>>>(S.sop, S.m[MKCG], bj_factor(S, nt));
         CKLAUNCH();
-        k_pcg2_solve<0><<<bj_grid_tiles(h, S, 4), kSolveThreads, kSolveSmem, h->st>>>(S.sop, S.m[MKCG], S.v[VS1], S.v[VRHO0], S.v[VS0],
-                                                                 S.v[VQ0], S.v[VW], S.v[VRHO1], eta2, cap, h->dS,
-                                                                 h->red(s));
+        k_pcg2_solve<0><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, nt), S.v[VRHO0], S.v[VS0],
+                                                                              S.v[VRHO1], eta2, cap, h->dS, h->red(s));
         CKLAUNCH();
         h->launches += 3;
     }
@@ -1428,6 +1445,13 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
     if (h->hS->cg_reason == CG_NOTSPD)
         return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
                        (long long)h->hS->cg_it);
+    // the last iteration's w += alpha p (iteration j wrote p_j into Q[j & 1]; chunks are even)
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        k_pcg2_wlast<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vq((int)(h->hS->cg_it & 1))], S.v[VW], h->dS);
+        CKLAUNCH();
+        h->launches++;
+    }
     return exchange(h, {VW});
 }
 

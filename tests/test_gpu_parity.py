@@ -472,8 +472,10 @@ def _bj_params(oracle, prob):
     return oracle.default_params(precond=2, grid_nx=prob.nx, grid_ny=prob.ny, tile_x=32, tile_y=32)
 
 
+@pytest.mark.parametrize("generic", ["0", "1"])   # PCG matvec: column march (k2) / generic kernel
 @pytest.mark.parametrize("case", BJ_CASES)
-def test_solve_parity_bjilu(G, oracle, case):
+def test_solve_parity_bjilu(G, oracle, monkeypatch, case, generic):
+    monkeypatch.setenv("GPCG_GENERIC", generic)
     make, tol = SOLVE_CASES[case]
     prob = make()
     rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, params=_bj_params(oracle, prob))
