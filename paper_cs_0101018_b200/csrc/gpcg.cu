@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <initializer_list>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -210,6 +211,7 @@ struct Slab {
 
 struct gpcg_problem {
     int dev = 0, sms = 148;
+    cudaMemPool_t pool = nullptr;   // device allocations (mem_pool); null: cudaMalloc / cudaFree
     cudaStream_t user = nullptr;    // caller's stream
     cudaStream_t st = nullptr;      // private work stream (capturable)
     cudaEvent_t ev_sync = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c0 = nullptr, ev_c1 = nullptr;
@@ -276,6 +278,44 @@ struct gpcg_problem {
 };
 
 namespace {
+
+// Device memory of a handle comes from one stream-ordered pool per device and process that
+// keeps freed blocks reserved (release threshold = max): a create / solve / destroy cycle
+// per request then costs no cudaMalloc / cudaFree (page mapping, implicit device-wide
+// synchronisation) after the first.  GPCG_POOL=0 at create: plain cudaMalloc / cudaFree.
+cudaMemPool_t mem_pool(int dev) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!pools[dev]) {
+        cudaMemPoolProps pp = {};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &pp) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[dev] = pool;
+    }
+    return pools[dev];
+}
+
+// (allocations happen at create and lazily at the first solve needing a buffer; the stream is
+// synchronised so the block may be used from any stream or by synchronous copies at once)
+template <class T>
+cudaError_t dalloc(gpcg_problem* h, T** p, size_t bytes) {
+    if (!h->pool) return cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    const cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, h->pool, h->st);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(h->st);
+}
+
+void dfree(gpcg_problem* h, void* p) {
+    if (!p) return;
+    if (h->pool) cudaFreeAsync(p, h->st);
+    else cudaFree(p);
+}
 
 int sync_scal(gpcg_problem* h) {
     CK(cudaMemcpyAsync(h->hS, h->dS, sizeof(Scal), cudaMemcpyDeviceToHost, h->st));
@@ -449,14 +489,14 @@ void free_all(gpcg_problem* h) {
     cudaSetDevice(h->dev);
     if (h->st) cudaStreamSynchronize(h->st);
     for (Slab& S : h->slabs) {
-        if (S.arena) cudaFree(S.arena);
+        dfree(h, S.arena);
         for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, S.xarena, (void*)S.bjf, (void*)S.rp,
                         (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
-            if (p) cudaFree(p);
+            dfree(h, p);
     }
     for (void* p : {(void*)h->red_all, (void*)h->red_tot, (void*)h->lu0, (void*)h->dS, (void*)h->gbar})
-        if (p) cudaFree(p);
+        dfree(h, p);
     if (h->hS) cudaFreeHost(h->hS);
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
     if (h->bj_exec) cudaGraphExecDestroy(h->bj_exec);
@@ -628,7 +668,7 @@ int setup_tile(gpcg_problem* h) {
         band(cap_env("GPCG_CG_CTAS_PER_SM", r4cg), S.bg_cg, S.grid4_cg);
         {
             const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
-            CK(cudaMalloc(&S.cgflags, (size_t)std::max<long long>(nf, 1)));
+            CK(dalloc(h, &S.cgflags, (size_t)std::max<long long>(nf, 1)));
         }
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
@@ -712,8 +752,12 @@ int create_streams(gpcg_problem* h, void* stream) {
         const char* e5 = getenv("GPCG_GP_SPEC");
         h->gp_spec = !(e5 && e5[0] == '0');
     }
-    CK(cudaMalloc(&h->gbar, sizeof(unsigned int)));
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    {
+        const char* e6 = getenv("GPCG_POOL");
+        h->pool = (e6 && e6[0] == '0') ? nullptr : mem_pool(h->dev);
+    }
+    CK(dalloc(h, &h->gbar, sizeof(unsigned int)));
     CK(cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev_a));
     CK(cudaEventCreate(&h->ev_b));
@@ -734,7 +778,7 @@ int create_vectors(gpcg_problem* h, const double* b, const double* l, const doub
         // one arena per slab (few large allocations keep create / destroy cheap); 256-byte aligned
         // sub-arrays; zeroed: padding columns and boundary ghosts stay 0
         const size_t total = NVEC * nb + NMSK * mbytes;
-        CK(cudaMalloc(&S.arena, total));
+        CK(dalloc(h, &S.arena, total));
         CK(cudaMemsetAsync(S.arena, 0, total, h->st));
         char* base = static_cast<char*>(S.arena);
         for (int k = 0; k < NVEC; ++k) {
@@ -755,15 +799,15 @@ int create_vectors(gpcg_problem* h, const double* b, const double* l, const doub
             S.grid_m2 = march_grid(S.mg2);
             gmax = std::max<long long>(gmax, std::max(S.grid_m1, S.grid_m2));
         }
-        CK(cudaMalloc(&S.partials, (size_t)kMaxSums * gmax * sizeof(double)));
-        CK(cudaMalloc(&S.counter, sizeof(unsigned int)));
+        CK(dalloc(h, &S.partials, (size_t)kMaxSums * gmax * sizeof(double)));
+        CK(dalloc(h, &S.counter, sizeof(unsigned int)));
         CK(cudaMemsetAsync(S.counter, 0, sizeof(unsigned int), h->st));
     }
-    CK(cudaMalloc(&h->red_all, (size_t)kMaxSums * h->nslabs() * sizeof(double)));
-    CK(cudaMalloc(&h->red_tot, (size_t)kMaxSums * sizeof(double)));
+    CK(dalloc(h, &h->red_all, (size_t)kMaxSums * h->nslabs() * sizeof(double)));
+    CK(dalloc(h, &h->red_tot, (size_t)kMaxSums * sizeof(double)));
     CK(cudaMemsetAsync(h->red_tot, 0, (size_t)kMaxSums * sizeof(double), h->st));
-    CK(cudaMalloc(&h->lu0, 2 * sizeof(double)));
-    CK(cudaMalloc(&h->dS, sizeof(Scal)));
+    CK(dalloc(h, &h->lu0, 2 * sizeof(double)));
+    CK(dalloc(h, &h->dS, sizeof(Scal)));
     CK(cudaMemsetAsync(h->dS, 0, sizeof(Scal), h->st));
     CK(cudaMallocHost(&h->hS, sizeof(Scal)));
     RC(upload_vec(h, VB, b));
@@ -1230,7 +1274,7 @@ int ensure_extract_buffers(gpcg_problem* h, Slab& S) {
     const size_t b_rp = r256((size_t)(n + 1) * 8), b_val = r256((size_t)nnzmax * 8), b_vec = r256((size_t)n * 8);
     const size_t b_msk = r256((size_t)n);
     const size_t total = b_idx + b_pos + b_cnt + b_col + b_blk + b_tot + b_rp + b_val + 12 * b_vec + 2 * b_msk;
-    CK(cudaMalloc(&S.xarena, total));
+    CK(dalloc(h, &S.xarena, total));
     CK(cudaMemsetAsync(S.xarena, 0, total, h->st));
     char* p = static_cast<char*>(S.xarena);
     S.xidx = reinterpret_cast<int*>(p) + (long long)S.glo * h->pitch; p += b_idx;   // indexed by v (ghosts incl.)
@@ -1394,7 +1438,7 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const long long nt = bj_tiles(h, S);
-        if (!S.bjf) CK(cudaMalloc(&S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double)));
+        if (!S.bjf) CK(dalloc(h, &S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double)));
         k_pcg2_init<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vy(cur)], S.v[VB], S.m[cur], S.m[MKCG], S.v[VRHO0],
                                                     S.v[VQ0], S.v[VQ1], S.v[VW]);
         CKLAUNCH();
@@ -1583,7 +1627,7 @@ int launch_objective(gpcg_problem* h, int x) {
 // Is b the same in every grid row?  (global row 0 from slab 0 / rank 0, compared everywhere)
 int detect_b_rows(gpcg_problem* h) {
     for (Slab& S : h->slabs) {
-        CK(cudaMalloc(&S.brow, (size_t)h->nx * sizeof(double)));
+        CK(dalloc(h, &S.brow, (size_t)h->nx * sizeof(double)));
         CK(cudaMemcpyAsync(S.brow, h->slabs[0].v[VB], (size_t)h->nx * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
     }
     if (h->use_nccl)
@@ -1626,8 +1670,8 @@ int setup_stencil_slabs(gpcg_problem* h, const double* wx, const double* wy, con
         // wx: (glo + rows + ghi) rows of nx+1 (or one broadcast row); wy: face rows [-glo, rows + ghi]
         const long long wxr = h->wx_ld ? (S.glo + S.rows + S.ghi) : 1;
         const long long wyr = h->wy_ld ? (S.glo + S.rows + 1 + S.ghi) : 1;
-        CK(cudaMalloc(&S.wxb, (size_t)(wxr * (nx + 1)) * sizeof(double)));
-        CK(cudaMalloc(&S.wyb, (size_t)(wyr * nx) * sizeof(double)));
+        CK(dalloc(h, &S.wxb, (size_t)(wxr * (nx + 1)) * sizeof(double)));
+        CK(dalloc(h, &S.wyb, (size_t)(wyr * nx) * sizeof(double)));
         CK(cudaMemsetAsync(S.wxb, 0, (size_t)(wxr * (nx + 1)) * sizeof(double), h->st));
         CK(cudaMemsetAsync(S.wyb, 0, (size_t)(wyr * nx) * sizeof(double), h->st));
         double* wxo = S.wxb + (h->wx_ld ? (long long)S.glo * (nx + 1) : 0);
@@ -1645,7 +1689,7 @@ int setup_stencil_slabs(gpcg_problem* h, const double* wx, const double* wy, con
             CK(cudaMemcpyAsync(wyo, wy, (size_t)nx * sizeof(double), ky, h->st));
         double* sho = nullptr;
         if (shift) {
-            CK(cudaMalloc(&S.shb, (size_t)S.nalloc * sizeof(double)));
+            CK(dalloc(h, &S.shb, (size_t)S.nalloc * sizeof(double)));
             CK(cudaMemsetAsync(S.shb, 0, (size_t)S.nalloc * sizeof(double), h->st));
             sho = S.shb + (long long)S.glo * h->pitch;
             CK(cudaMemcpy2DAsync(sho, (size_t)h->pitch * sizeof(double), shift + (long long)S.uoff * nx,
@@ -1802,9 +1846,9 @@ int create_stencil3(gpcg_problem** out, const gpcg_dist* dist, void* stream, int
         const long long planes = S.glo + S.rows + S.ghi;
         double *wxo, *wyo, *wzo, *sho = nullptr;
         // reuse the 2-D face slots: wxb <- wx, wyb <- wy, brow <- wz
-        if (cudaMalloc(&S.wxb, (size_t)(planes * lx) * sizeof(double)) != cudaSuccess ||
-            cudaMalloc(&S.wyb, (size_t)(planes * ly) * sizeof(double)) != cudaSuccess ||
-            cudaMalloc(&S.brow, (size_t)((planes + 1) * lz) * sizeof(double)) != cudaSuccess)
+        if (dalloc(h, &S.wxb, (size_t)(planes * lx) * sizeof(double)) != cudaSuccess ||
+            dalloc(h, &S.wyb, (size_t)(planes * ly) * sizeof(double)) != cudaSuccess ||
+            dalloc(h, &S.brow, (size_t)((planes + 1) * lz) * sizeof(double)) != cudaSuccess)
             return fail(set_err(GPCG_ENOMEM, "3-D face arrays"));
         cudaMemsetAsync(S.wxb, 0, (size_t)(planes * lx) * sizeof(double), h->st);
         cudaMemsetAsync(S.wyb, 0, (size_t)(planes * ly) * sizeof(double), h->st);
@@ -1820,7 +1864,7 @@ int create_stencil3(gpcg_problem** out, const gpcg_dist* dist, void* stream, int
                             (cudaMemcpyKind)copy_kind(wz, true), h->st) != cudaSuccess)
             return fail(set_err(GPCG_ECUDA, "3-D face upload"));
         if (shift) {
-            if (cudaMalloc(&S.shb, (size_t)S.nalloc * sizeof(double)) != cudaSuccess)
+            if (dalloc(h, &S.shb, (size_t)S.nalloc * sizeof(double)) != cudaSuccess)
                 return fail(set_err(GPCG_ENOMEM, "shift"));
             cudaMemsetAsync(S.shb, 0, (size_t)S.nalloc * sizeof(double), h->st);
             sho = S.shb + S.glo * plane;
@@ -1952,7 +1996,7 @@ int create_csr(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t 
     if (h->nranks > 1) {
         // exchange band widths with the neighbouring ranks: my glo is what rank-1 sends me
         long long* dbuf = nullptr;
-        if (cudaMalloc(&dbuf, 4 * sizeof(long long)) != cudaSuccess) return fail(set_err(GPCG_ENOMEM, "band buffer"));
+        if (dalloc(h, &dbuf, 4 * sizeof(long long)) != cudaSuccess) return fail(set_err(GPCG_ENOMEM, "band buffer"));
         long long hb[4] = {h->slabs.front().glo, h->slabs.back().ghi, 0, 0};
         cudaMemcpy(dbuf, hb, 4 * sizeof(long long), cudaMemcpyHostToDevice);
         const NcclApi* N = nccl_api();
@@ -1965,7 +2009,7 @@ int create_csr(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t 
         ok = nk(N->GroupEnd()) && ok;
         cudaStreamSynchronize(h->st);
         cudaMemcpy(hb, dbuf, 4 * sizeof(long long), cudaMemcpyDeviceToHost);
-        cudaFree(dbuf);
+        dfree(h, dbuf);
         if (!ok) return fail(set_err(GPCG_ENCCL, "band-width exchange failed"));
         h->slabs.front().send_lo = h->rank > 0 ? (int)hb[2] : 0;            // rank-1's ghi
         h->slabs.back().send_hi = h->rank < h->nranks - 1 ? (int)hb[3] : 0; // rank+1's glo
@@ -1984,9 +2028,9 @@ int create_csr(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t 
         for (int i = 0; i <= S.rows; ++i) rps[i] = rp[S.row0 + i] - k0;
         cis.resize(k1 - k0);
         for (long long k = k0; k < k1; ++k) cis[k - k0] = (int32_t)(cols[k] - g0);
-        if (cudaMalloc(&S.rp, (S.rows + 1) * sizeof(long long)) != cudaSuccess ||
-            cudaMalloc(&S.ci, std::max<long long>(1, k1 - k0) * sizeof(int)) != cudaSuccess ||
-            cudaMalloc(&S.val, std::max<long long>(1, k1 - k0) * sizeof(double)) != cudaSuccess)
+        if (dalloc(h, &S.rp, (S.rows + 1) * sizeof(long long)) != cudaSuccess ||
+            dalloc(h, &S.ci, std::max<long long>(1, k1 - k0) * sizeof(int)) != cudaSuccess ||
+            dalloc(h, &S.val, std::max<long long>(1, k1 - k0) * sizeof(double)) != cudaSuccess)
             return fail(set_err(GPCG_ENOMEM, "CSR arrays (nnz = %lld)", k1 - k0));
         if (cudaMemcpy(S.rp, rps.data(), (S.rows + 1) * sizeof(long long), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(S.ci, cis.data(), (k1 - k0) * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||

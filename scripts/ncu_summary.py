@@ -40,10 +40,8 @@ def report(path):
         tu = units[idx["gpu__time_duration.sum"]]
         t_ns = g("gpu__time_duration.sum") * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3,
                                                "msecond": 1e6, "ms": 1e6}.get(tu, 1)
-        bu = units[idx["dram__bytes_read.sum"]]
-        bscale = {"byte": 1, "B": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6,
-                  "Gbyte": 1e9, "GB": 1e9}.get(bu, 1)
-        byt = (g("dram__bytes_read.sum") + g("dram__bytes_write.sum")) * bscale
+        bsc = {"byte": 1, "B": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 1e9, "GB": 1e9}
+        byt = sum(g(m) * bsc.get(units[idx[m]], 1) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         print(f"{short(r[ki])[:38]:38s} {t_ns/1e3:8.2f} {byt/1e6:9.2f} {byt/t_ns:8.1f} "
               f"{g('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):6.1f} "
               f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):6.1f} {g('launch__registers_per_thread'):5.0f} "

@@ -203,6 +203,28 @@ def test_device_pointers_and_determinism(G):
     assert st1["cg_iters"] == st2["cg_iters"]
 
 
+@pytest.mark.parametrize("pool", ["1", "0"])
+def test_create_destroy_cycles_reuse_memory(G, monkeypatch, pool):
+    """Handles allocate from a retained stream-ordered pool (GPCG_POOL=0: cudaMalloc): repeated
+    create / solve / destroy cycles, with a live handle in between, give bitwise the same result."""
+    import torch
+    monkeypatch.setenv("GPCG_POOL", pool)
+    prob = P.c1()
+    x0 = torch.from_numpy(prob.x0).cuda()
+    ref = None
+    keep = G.Solver.from_problem(P.c0(), device="cuda")
+    for _ in range(3):
+        with G.Solver.from_problem(prob, device="cuda") as s:
+            rc, x, st = s.solve(x0, -1e-8)
+        assert rc == 0
+        if ref is None:
+            ref = x.clone()
+        assert torch.equal(x, ref)
+    rc0, _, _ = keep.solve(torch.zeros(P.c0().n, dtype=torch.float64, device="cuda"), -1e-8)
+    keep.close()
+    assert rc0 == 0
+
+
 # ------------------------------------------------------------------ edge cases
 def test_edge_tiny_grids(G, oracle):
     for nx, ny in [(1, 1), (1, 2), (3, 1)]:
