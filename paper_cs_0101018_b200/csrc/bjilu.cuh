@@ -26,14 +26,14 @@
 #include "common.cuh"
 #include "fin.cuh"
 #include "march.cuh"
+#include "tile.cuh"
 
 namespace gpcg {
 
 constexpr int kTile = 32;
 #ifndef GPCG_BJ_UNROLL
-#define GPCG_BJ_UNROLL 8
+#define GPCG_BJ_UNROLL 4
 #endif
-constexpr int kBjUnroll = GPCG_BJ_UNROLL;                 // wavefront steps unrolled (factor loads in flight)
 
 // face weights / diagonal of point (i, j) of the slab (StencilOp layout)
 struct Faces5 {
@@ -80,9 +80,9 @@ struct BjFactor {
 };
 
 constexpr int kBjThreads = 64;                                        // 2 tiles per CTA
-constexpr int kBjMinBlocks = 10;                                      // 20 tiles / SM in flight
+constexpr int kBjMinBlocks = 9;                                       // 18 tiles / SM in flight
 constexpr int kFactorSmem = (kBjThreads / 32) * kTile * kTile * (3 * 8 + 1);
-constexpr int kSolveSmem = (kBjThreads / 32) * kTile * kTile * 8;
+constexpr int kSolveSmem = (kBjThreads / 32) * kTile * kTile * 8 + 128;   // + alignment pad
 
 // ILU(0) pivots of every tile on the CG mask: d_v = a_vv - cs^2 / d_s - cw^2 / d_w (south first,
 // the oracle's column order).  Staged per warp in shared memory (skewed), then one 63-step
@@ -140,58 +140,94 @@ k_bjilu_factor(StencilOp A, const unsigned char* __restrict__ mask, BjFactor F) 
     });
 }
 
-// z = M^-1 r on one tile whose r is staged (skewed) in T: forward (D + L) t = r, backward
-// D^-1 (D + U) z = t, both in place in T; then z is stored row by row.  Returns this lane's
-// share of r'z, formed in the forward sweep as t'D t = sum t_v (D t)_v: with U = L^T,
+// z = M^-1 r on one tile whose r is staged in T (natural layout: (i, jl) at jl * 32 + i):
+// forward (D + L) t = r, backward D^-1 (D + U) z = t, both in place in T; then z is stored
+// row by row.  Wavefront step l touches T at (l - i) * 32 + i: 32 distinct bank pairs
+// (-31 = 1 mod 16), so the diagonal access is conflict-free without skewing T.  Returns this
+// lane's share of r'z, formed in the forward sweep as t'D t = sum t_v (D t)_v: with U = L^T,
 // r'z = r'(D + U)^-1 D t = ((D + L)^-1 r)' D t = t'D t, and (D t)_v is the sum the step
-// forms before scaling by 1/d_v (so r need not be kept or re-read).  The factor rows of each
-// step are chain-independent loads, hoisted ahead of the dependent t / z recurrences by the
-// full unroll; the recurrences touch only registers, shuffles and T.
+// forms before scaling by 1/d_v (so r need not be kept or re-read).
+// The factor rows (skewed, one contiguous 256-byte row per step) are loaded in groups of
+// kBjGroup steps, double-buffered: group g + 1 is in flight while group g runs, so the
+// recurrence waits on shared memory and shuffles, not on the loads.
+constexpr int kBjGroup = GPCG_BJ_UNROLL;
+constexpr int kBjSteps = 2 * kTile;                      // 63 wavefront steps + 1 idle (no active lane)
+
+struct FacGroup {
+    double d[kBjGroup], s[kBjGroup], w[kBjGroup];
+};
+
+template <bool BWD>
+__device__ __forceinline__ void load_group(FacGroup& G, const double* Fd, const double* Fs, const double* Fw, int g) {
+#pragma unroll
+    for (int k = 0; k < kBjGroup; ++k) {
+        const int l = BWD ? kBjSteps - 1 - (g * kBjGroup + k) : g * kBjGroup + k;
+        const int row = (l & (kTile - 1)) * kTile;
+        const int nrow = BWD ? ((l + 1) & (kTile - 1)) * kTile : row;
+        G.d[k] = __ldg(Fd + row);
+        G.s[k] = __ldg(Fs + nrow);                       // fwd: cs of (i, jl); bwd: cs of (i, jl + 1)
+        G.w[k] = __ldg(Fw + nrow);                       // fwd: cw of (i, jl); bwd: lane i+1 has cw of (i+1, jl)
+    }
+}
+
 __device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0, long long tb, const BjFactor& F,
                                              double* __restrict__ z, double* T) {
     const int lane = threadIdx.x & 31;
     const double* Fd = F.dinv + tb + lane;
     const double* Fs = F.cs + tb + lane;
     const double* Fw = F.cw + tb + lane;
+    constexpr int NG = kBjSteps / kBjGroup;
     __syncwarp();
     double t_prev = 0.0;                                  // t of (i, jl - 1)
     double rz = 0.0;
-#pragma unroll kBjUnroll
-    for (int l = 0; l < 2 * kTile - 1; ++l) {
-        const int row = (l & (kTile - 1)) * kTile;
-        const double dv = __ldg(Fd + row), cs = __ldg(Fs + row), cw = __ldg(Fw + row);
-        const double t_west = __shfl_up_sync(0xffffffffu, t_prev, 1);   // (i - 1, jl), step l - 1
-        const double sv = T[row + lane] + cs * t_prev + cw * t_west;    // (D t)_v
-        const double tv = sv * dv;
-        if ((unsigned)(l - lane) < (unsigned)kTile) {
-            T[row + lane] = tv;
-            t_prev = tv;
-            rz = fma(tv, sv, rz);
+    FacGroup cur, nxt;
+    load_group<false>(cur, Fd, Fs, Fw, 0);
+#pragma unroll 1
+    for (int g = 0; g < NG; ++g) {
+        if (g + 1 < NG) load_group<false>(nxt, Fd, Fs, Fw, g + 1);
+#pragma unroll
+        for (int k = 0; k < kBjGroup; ++k) {
+            const int l = g * kBjGroup + k;
+            const int q = ((l - lane) & (kTile - 1)) * kTile + lane;
+            const double t_west = __shfl_up_sync(0xffffffffu, t_prev, 1);   // (i - 1, jl), step l - 1
+            const double sv = T[q] + cur.s[k] * t_prev + cur.w[k] * t_west;  // (D t)_v
+            const double tv = sv * cur.d[k];
+            if ((unsigned)(l - lane) < (unsigned)kTile) {
+                T[q] = tv;
+                t_prev = tv;
+                rz = fma(tv, sv, rz);
+            }
         }
+        cur = nxt;
     }
     __syncwarp();
     double z_prev = 0.0;                                  // z of (i, jl + 1)
-#pragma unroll kBjUnroll
-    for (int l = 2 * kTile - 2; l >= 0; --l) {
-        const int row = (l & (kTile - 1)) * kTile, nrow = ((l + 1) & (kTile - 1)) * kTile;
-        const double dv = __ldg(Fd + row);
-        const double cn = __ldg(Fs + nrow);               // cs of (i, jl + 1); 0 when jl = 31
-        const double cwn = __ldg(Fw + nrow);              // lane i+1's value is cw of (i + 1, jl)
-        const double z_east = __shfl_down_sync(0xffffffffu, z_prev, 1);  // (i + 1, jl), step l + 1
-        const double cwe = __shfl_down_sync(0xffffffffu, cwn, 1);           // all lanes take part
-        const double ce = lane < kTile - 1 ? cwe : 0.0;
-        const double zv = T[row + lane] + (ce * z_east + cn * z_prev) * dv;
-        if ((unsigned)(l - lane) < (unsigned)kTile) {
-            T[row + lane] = zv;
-            z_prev = zv;
+    load_group<true>(cur, Fd, Fs, Fw, 0);
+#pragma unroll 1
+    for (int g = 0; g < NG; ++g) {
+        if (g + 1 < NG) load_group<true>(nxt, Fd, Fs, Fw, g + 1);
+#pragma unroll
+        for (int k = 0; k < kBjGroup; ++k) {
+            const int l = kBjSteps - 1 - (g * kBjGroup + k);
+            const int q = ((l - lane) & (kTile - 1)) * kTile + lane;
+            const double z_east = __shfl_down_sync(0xffffffffu, z_prev, 1);  // (i + 1, jl), step l + 1
+            const double cwe = __shfl_down_sync(0xffffffffu, cur.w[k], 1);   // all lanes take part
+            const double ce = lane < kTile - 1 ? cwe : 0.0;
+            const double cn = cur.s[k];                                     // 0 when jl = 31 (row 0's cs)
+            const double zv = T[q] + (ce * z_east + cn * z_prev) * cur.d[k];
+            if ((unsigned)(l - lane) < (unsigned)kTile) {
+                T[q] = zv;
+                z_prev = zv;
+            }
         }
+        cur = nxt;
     }
     __syncwarp();
     const int i = x0 + lane;
 #pragma unroll 8
     for (int jl = 0; jl < kTile; ++jl) {                  // store z (coalesced rows)
         const int j = y0 + jl;
-        if (i < A.nx && j < A.ny) z[i + (long long)A.pitch * j] = T[sk(lane, jl)];
+        if (i < A.nx && j < A.ny) z[i + (long long)A.pitch * j] = T[jl * kTile + lane];
     }
     __syncwarp();
     return rz;
@@ -218,31 +254,49 @@ k_pcg2_init(StencilOp A, const double* __restrict__ y, const double* __restrict_
 
 template <int KIND>   // 0: init solve (gamma_0), 1: iteration update + solve (gamma_{j+1})
 __global__ void __launch_bounds__(kBjThreads, kBjMinBlocks)
-k_pcg2_solve(StencilOp A, BjFactor F, double* __restrict__ r, const double* __restrict__ q,
-             double* __restrict__ z, double eta2, long long cap, Scal* S, RedScratch R) {
+k_pcg2_solve(StencilOp A, BjFactor F, const __grid_constant__ CUtensorMap m_r, int row0, double* __restrict__ r,
+             const double* __restrict__ q, double* __restrict__ z, double eta2, long long cap, Scal* S,
+             RedScratch R) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint64_t bars[kBjThreads / 32];
     if (KIND == 1 && *(volatile int*)&S->cg_done) return;
     const double alpha = KIND == 1 ? S->cg_alpha : 0.0;
     double acc[1] = {0.0};
-    const int lane = threadIdx.x & 31;
-    double* T = reinterpret_cast<double*>(smem_raw) + (threadIdx.x >> 5) * kTile * kTile;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // TMA destinations must be 128-byte aligned; the dynamic block is padded by 128 for this
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    double* T = reinterpret_cast<double*>(base) + wid * kTile * kTile;
+    uint64_t* bar = &bars[wid];
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;
     for_each_tile(A, [&](int x0, int y0, int tt) {
+        // r tile -> T by TMA (zero outside the stored grid)
+        if (lane == 0) {
+            fence_proxy_async();                          // T's previous generic accesses before the async write
+            mbar_expect_tx(bar, kTile * kTile * 8);
+            tma_load_2d(T, &m_r, x0, y0 + row0, bar);
+        }
         const int i = x0 + lane;
         const int ic = i < A.nx ? i : x0;
-        // KIND 1: r -= alpha q (r and q are 0 off F, so no mask); stage r skewed in T (0 outside
-        // the grid).  w += alpha p is deferred to the next k_pcg2_matvec (k_pcg2_wlast after the
-        // last iteration).
-#pragma unroll 8
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        // KIND 1: r -= alpha q (r and q are 0 off F, so no mask), written back; rows / columns
+        // outside the slab's owned grid are zeroed in T (the tile is the owned part).  w += alpha p
+        // is deferred to the next matvec (k_pcg2_wlast after the last iteration).
+#pragma unroll 16
         for (int jl = 0; jl < kTile; ++jl) {
             const int j = y0 + jl;
             const bool in = i < A.nx && j < A.ny;
-            const long long v = ic + (long long)A.pitch * min(j, A.ny - 1);
-            double rv = r[v];
+            double rv = T[jl * kTile + lane];
             if (KIND == 1) {
-                rv = fma(-alpha, q[v], rv);
-                if (in) r[v] = rv;
+                rv = fma(-alpha, q[ic + (long long)A.pitch * min(j, A.ny - 1)], rv);
+                if (in) r[i + (long long)A.pitch * j] = rv;
             }
-            T[sk(lane, jl)] = in ? rv : 0.0;
+            T[jl * kTile + lane] = in ? rv : 0.0;
         }
         acc[0] += tile_solve(A, x0, y0, (long long)tt * kTile * kTile, F, z, T);
     });
@@ -277,6 +331,72 @@ k_pcg2_matvec(StencilOp A, const unsigned char* __restrict__ mask, const double*
         acc[0] = fma(pv, qv, acc[0]);
     });
     reduce_and_finish<1>(acc, R, [&](double* t) { pcg2_alpha_fin(t[0], S); });
+}
+
+// The same step as a 2-D tile sweep (the default): a 256-thread CTA owns a 32 x 32 output
+// tile; p = z + beta p_old is formed once per point on the 34 x 34 tile + halo in shared
+// memory (z and p_old are 0 off F, so no mask there; the loads of the fill are independent),
+// then every thread applies the 5-point operator to 4 points from shared memory, in the
+// order of Op5::apply.  w += alpha_prev p_old, p_new, q written at the owned points.
+constexpr int kMvThreads = 256;
+constexpr int kMvH = kTile + 2;
+
+__global__ void __launch_bounds__(kMvThreads)
+k_pcg2_matvec_tile(StencilOp A, const unsigned char* __restrict__ mask, const double* __restrict__ z,
+                   const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
+                   double* __restrict__ w, Scal* S, RedScratch R) {
+    __shared__ double P[kMvH][kMvH + 1];
+    if (*(volatile int*)&S->cg_done) return;
+    const double beta = S->cg_beta;
+    const double alpha_prev = S->cg_alpha;                // alpha of the previous iteration (0 at the first)
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int ntx = (A.nx + kTile - 1) / kTile, nty = (A.ny + kTile - 1) / kTile;
+    double acc[1] = {0.0};
+    for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
+        const int x0 = (t % ntx) * kTile, y0 = (t / ntx) * kTile;
+        for (int e = threadIdx.x; e < kMvH * kMvH; e += kMvThreads) {
+            const int ry = e / kMvH, rx = e - ry * kMvH;
+            const int i = x0 - 1 + rx, j = y0 - 1 + ry;
+            double pv = 0.0;
+            if (i >= 0 && i < A.nx && j >= A.rlo && j < A.rhi) {
+                const long long v = i + (long long)A.pitch * j;
+                pv = fma(beta, p_old[v], z[v]);
+            }
+            P[ry][rx] = pv;
+        }
+        __syncthreads();
+        const int i = x0 + tx;
+#pragma unroll
+        for (int m = 0; m < kTile / 8; ++m) {
+            const int jl = ty + 8 * m, j = y0 + jl;
+            if (i < A.nx && j < A.ny) {
+                const long long v = i + (long long)A.pitch * j;
+                const double pc = P[jl + 1][tx + 1];
+                if (mask[v]) {
+                    const double* wxr = A.wx + (long long)j * A.wx_ld + i;
+                    const double fw = __ldg(wxr), fe = __ldg(wxr + 1);
+                    const double fs = __ldg(A.wy + (long long)j * A.wy_ld + i);
+                    const double fn = __ldg(A.wy + (long long)(j + 1) * A.wy_ld + i);
+                    double d = (fw + fe) + (fs + fn);
+                    if (A.shift) d += __ldg(A.shift + v);
+                    double qv = d * pc;
+                    qv = fma(-fw, P[jl + 1][tx], qv);
+                    qv = fma(-fe, P[jl + 1][tx + 2], qv);
+                    qv = fma(-fs, P[jl][tx + 1], qv);
+                    qv = fma(-fn, P[jl + 2][tx + 1], qv);
+                    w[v] = fma(alpha_prev, p_old[v], w[v]);
+                    p_new[v] = pc;
+                    q[v] = qv;
+                    acc[0] = fma(pc, qv, acc[0]);
+                } else {
+                    p_new[v] = 0.0;
+                    q[v] = 0.0;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    reduce_and_finish<1>(acc, R, [&](double* tt) { pcg2_alpha_fin(tt[0], S); });
 }
 
 // The same step on the column march (march.cuh, H = 1): level 1 forms p(r) once per point,

@@ -199,6 +199,7 @@ struct Slab {
     double* xv[12] = {};                      // gF, dinvF, rho x2, q x2, s x2, p, w, (spare)
     unsigned char *xmask = nullptr, *xmaskcg = nullptr;
     double* bjf = nullptr;                    // block-Jacobi ILU(0) factor (precond = 2): 3 x tiles x 32^2
+    CUtensorMap tbr;                          // r (RHO0) in 32 x 32 boxes for the BJ-ILU tile solves
     int grid4_cg = 1, grid4_acc = 1, grid4_srch = 1;
     // g-free sweeps (k5_*): 112-column boxes from x0 - 4, 128-byte mask boxes, 104-column bands
     CUtensorMap t5[NVEC];
@@ -212,6 +213,7 @@ struct Slab {
 struct gpcg_problem {
     int dev = 0, sms = 148;
     cudaMemPool_t pool = nullptr;   // device allocations (mem_pool); null: cudaMalloc / cudaFree
+    int bj_matvec = 0;              // GPCG_BJ_MATVEC: BJ-ILU PCG matvec 0 = 2-D tile sweep, 1 = column march
     cudaStream_t user = nullptr;    // caller's stream
     cudaStream_t st = nullptr;      // private work stream (capturable)
     cudaEvent_t ev_sync = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c0 = nullptr, ev_c1 = nullptr;
@@ -754,6 +756,8 @@ int create_streams(gpcg_problem* h, void* stream) {
     }
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     {
+        const char* e7 = getenv("GPCG_BJ_MATVEC");
+        h->bj_matvec = (e7 && e7[0] == '1') ? 1 : 0;
         const char* e6 = getenv("GPCG_POOL");
         h->pool = (e6 && e6[0] == '0') ? nullptr : mem_pool(h->dev);
     }
@@ -1397,6 +1401,10 @@ int bj_grid_tiles(const gpcg_problem* h, const Slab& S) {
     return (int)std::max<long long>(1, std::min<long long>((bj_tiles(h, S) + wpc - 1) / wpc, (long long)h->sms * 16));
 }
 
+int bj_grid_mv(const gpcg_problem* h, const Slab& S) {
+    return (int)std::max<long long>(1, std::min<long long>(bj_tiles(h, S), (long long)h->sms * 8));
+}
+
 BjFactor bj_factor(const Slab& S, long long nt) {
     const long long e = nt * kTile * kTile;
     return BjFactor{S.bjf, S.bjf + e, S.bjf + 2 * e};
@@ -1406,9 +1414,14 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
     const int bb = a ^ 1;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
+        const int tile_mode = h->bj_matvec;
         if (h->generic)
             k_pcg2_matvec<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VRHO1], S.v[vq(a)], S.v[vq(bb)],
                                                           S.v[VS0], S.v[VW], h->dS, h->red(s));
+        else if (tile_mode == 0)
+            k_pcg2_matvec_tile<<<bj_grid_mv(h, S), kMvThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VRHO1], S.v[vq(a)],
+                                                                          S.v[vq(bb)], S.v[VS0], S.v[VW], h->dS,
+                                                                          h->red(s));
         else if (h->bc)
             k2_pcg2_matvec<true><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.m[MKCG], S.v[VRHO1], S.v[vq(a)],
                                                                          S.v[vq(bb)], S.v[VS0], S.v[VW], h->dS, h->red(s));
@@ -1421,8 +1434,9 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
     RC(exchange(h, {vq(bb)}));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        k_pcg2_solve<1><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, bj_tiles(h, S)), S.v[VRHO0],
-                                                                              S.v[VS0], S.v[VRHO1], 0.0, 0, h->dS, h->red(s));
+        k_pcg2_solve<1><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, bj_tiles(h, S)), S.tbr,
+                                                                              S.glo, S.v[VRHO0], S.v[VS0], S.v[VRHO1],
+                                                                              0.0, 0, h->dS, h->red(s));
         CKLAUNCH();
     }
     RC(finish_reduce(h, fin(FIN_PCG2_BETA), 1));
@@ -1438,14 +1452,18 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const long long nt = bj_tiles(h, S);
-        if (!S.bjf) CK(dalloc(h, &S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double)));
+        if (!S.bjf) {
+            CK(dalloc(h, &S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double)));
+            RC(make_map(h, S, &S.tbr, S.v[VRHO0], false, kTile, kTile));
+        }
         k_pcg2_init<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vy(cur)], S.v[VB], S.m[cur], S.m[MKCG], S.v[VRHO0],
                                                     S.v[VQ0], S.v[VQ1], S.v[VW]);
         CKLAUNCH();
         k_bjilu_factor<<<bj_grid_tiles(h, S), kBjThreads, kFactorSmem, h->st>>>(S.sop, S.m[MKCG], bj_factor(S, nt));
         CKLAUNCH();
-        k_pcg2_solve<0><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, nt), S.v[VRHO0], S.v[VS0],
-                                                                              S.v[VRHO1], eta2, cap, h->dS, h->red(s));
+        k_pcg2_solve<0><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, nt), S.tbr, S.glo,
+                                                                              S.v[VRHO0], S.v[VS0], S.v[VRHO1], eta2,
+                                                                              cap, h->dS, h->red(s));
         CKLAUNCH();
         h->launches += 3;
     }
