@@ -43,6 +43,7 @@
 #include "march_tma.cuh"
 #include "extract.cuh"
 #include "bjilu.cuh"
+#include "march3.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -179,6 +180,7 @@ struct Slab {
     unsigned int* counter = nullptr;
     MarchGeom mg1{}, mg2{};
     int grid_m1 = 1, grid_m2 = 1, grid = 1;
+    int grid7 = 1;                            // 3-D plane-march kernels (march3.cuh)
     TileGeom tg{};
     int grid_t_cg = 1, grid_t_acc = 1, grid_t_srch = 1;
     CUtensorMap tm[NVEC];
@@ -438,6 +440,9 @@ bool has_ghosts(const gpcg_problem* h) { return h->nslabs() > 1 || h->nranks > 1
 bool spec2d(const gpcg_problem* h) { return !h->is_csr && !h->is3d && !h->generic; }
 
 // f(op) with the slab's operator policy (generic kernels)
+// 3-D stencils run the plane-march kernels (march3.cuh) unless GPCG_GENERIC=1
+bool use_m3(const gpcg_problem* h) { return h->is3d && !h->generic; }
+
 template <class F>
 void with_gop(const gpcg_problem* h, Slab& S, F&& f) {
     if (h->is_csr) f(S.cop);
@@ -956,6 +961,14 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
         } else {
             const double* dp = dir >= 0 ? S.v[dir] : nullptr;
             const unsigned char* mp = mask_prev >= 0 ? S.m[mask_prev] : nullptr;
+            if (use_m3(h)) {
+                if (h->sb)
+                    k7_accept<true><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, B, S.v[y_in], dp, sgn, S.v[VB], mp,
+                                                                         S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
+                else
+                    k7_accept<false><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, B, S.v[y_in], dp, sgn, S.v[VB], mp,
+                                                                          S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
+            } else
             with_gop_sb(h, S, [&](auto& op, auto sbt) {
                 using Op = std::decay_t<decltype(op)>;
                 constexpr bool SB = decltype(sbt)::value;
@@ -981,6 +994,10 @@ int launch_cauchy(gpcg_problem* h, int y, int g, int gp = 0) {
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
+        if (use_m3(h)) {
+            if (h->sb) k7_cauchy<true><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, B, S.v[y], S.v[g], h->dS, h->red(s), gp);
+            else k7_cauchy<false><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, B, S.v[y], S.v[g], h->dS, h->red(s), gp);
+        } else
         with_gop_sb(h, S, [&](auto& op, auto sbt) {
             using Op = std::decay_t<decltype(op)>;
             constexpr bool SB = decltype(sbt)::value;
@@ -1063,6 +1080,13 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
                 if (h->bc) bydg(sbt, std::true_type()); else bydg(sbt, std::false_type());
             };
             if (h->sb) bybc(std::true_type()); else bybc(std::false_type());
+        } else if (use_m3(h) && K == 2) {
+            if (h->sb)
+                k7_search<true, 2><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, B, S.v[y], S.v[g], S.v[dir], sgn,
+                                                                        use_alpha0, h0, mu, h->dS, R, gp);
+            else
+                k7_search<false, 2><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, B, S.v[y], S.v[g], S.v[dir], sgn,
+                                                                         use_alpha0, h0, mu, h->dS, R, gp);
         } else {
             with_gop_sb(h, S, [&](auto& op, auto sbt) {
                 using Op = std::decay_t<decltype(op)>;
@@ -1142,6 +1166,14 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
             };
             if (h->bc) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else if (use_m3(h)) {
+            auto go = [&](auto pct) {
+                constexpr bool PC = decltype(pct)::value;
+                k7_cg_iter<PC><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, S.m[MKCG], S.v[vrho(a)], S.v[vq(a)],
+                                                                    S.v[vs(a)], S.v[vrho(bb)], S.v[vq(bb)], S.v[vs(bb)],
+                                                                    S.v[VP], S.v[VW], S.v[VD], h->dS, R);
+            };
+            if (pc) go(std::true_type()); else go(std::false_type());
         } else {
             with_gop(h, S, [&](auto& op) {
                 using Op = std::decay_t<decltype(op)>;
@@ -1547,6 +1579,14 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
             };
             if (h->bc) { if (pc) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (pc) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
+        } else if (use_m3(h)) {
+            auto go = [&](auto pct) {
+                constexpr bool PC = decltype(pct)::value;
+                k7_cg_init<PC><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, S.v[vg(cur)], S.m[cur], S.m[MKCG], S.v[VRHO0],
+                                                                    S.v[VQ0], S.v[VS0], S.v[VRHO1], S.v[VQ1], S.v[VS1],
+                                                                    S.v[VP], S.v[VW], S.v[VD], eta2, cap, h->dS, R);
+            };
+            if (pc) go(std::true_type()); else go(std::false_type());
         } else {
             with_gop(h, S, [&](auto& op) {
                 using Op = std::decay_t<decltype(op)>;
@@ -1892,6 +1932,9 @@ int create_stencil3(gpcg_problem** out, const gpcg_dist* dist, void* stream, int
         }
         S.s3op = Stencil3Op{(int)nx, (int)ny, S.rows, plane, wxo, wyo, wzo, sho, -S.glo, S.rows + S.ghi};
         S.grid = std::max(1, (int)std::min<long long>((plane * S.rows + kThreads - 1) / kThreads, (long long)h->sms * 16));
+        const long long items7 = ((nx + m3::OX - 1) / m3::OX) * ((ny + m3::OY - 1) / m3::OY) *
+                                 (((long long)S.rows + m3::KZ - 1) / m3::KZ);
+        S.grid7 = (int)std::max<long long>(1, std::min<long long>(items7, (long long)h->sms * 8));
     }
     for (int pass = 0; pass < 4; ++pass) {
         if (pass == 3 && !shift) break;
@@ -2223,7 +2266,12 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
             if (reduced) k_hessvec<Op, true><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
             else k_hessvec<Op, false><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
         };
-        with_gop(h, S, go);
+        if (use_m3(h)) {
+            if (reduced) k7_hessvec<true><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, vin, yout, mask);
+            else k7_hessvec<false><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, vin, yout, mask);
+        } else {
+            with_gop(h, S, go);
+        }
         h->launches++;
         CKLAUNCH();
     }

@@ -416,6 +416,75 @@ def test_stencil3d_spmv_and_solve_parity(G, oracle, m):
     assert not nontie
 
 
+def ragged_stencil3d(nx, ny, nz, seed, shift=True, bounds="two"):
+    """3-D 7-point face-weight stencil with every face (boundary faces too) positive, so the
+    diagonal carries the Dirichlet boundary faces; sizes chosen off the plane-march tiles."""
+    wx = 0.5 + P.uniform(seed, 1, nz * ny * (nx + 1))
+    wy = 0.5 + P.uniform(seed, 2, nz * (ny + 1) * nx)
+    wz = 0.5 + P.uniform(seed, 3, (nz + 1) * ny * nx)
+    n = nx * ny * nz
+    sh = 0.01 * P.uniform(seed, 4, n) if shift else None
+    b = P.gaussian(seed, 5, n)
+    if bounds == "two":
+        l = -0.2 * P.uniform(seed, 6, n)
+        u = 0.2 * P.uniform(seed, 7, n)
+    else:
+        l = np.full(n, -0.05); u = np.full(n, 0.05)      # scalar bounds (the SB kernels)
+    return P.Problem(name=f"r3d_{nx}x{ny}x{nz}", kind="stencil3d", n=n, b=b, l=l, u=u,
+                     x0=P.gaussian(seed, 8, n) * 0.1, tol=-1e-10, nx=nx, ny=ny, nz=nz, wx=wx, wy=wy, wz=wz,
+                     shift=sh)
+
+
+R3D_CASES = {
+    "31x7x33": lambda: ragged_stencil3d(31, 7, 33, 11),
+    "45x13x65_sb": lambda: ragged_stencil3d(45, 13, 65, 12, shift=False, bounds="scalar"),
+    "1x1x9": lambda: ragged_stencil3d(1, 1, 9, 13),
+    "2x3x1": lambda: ragged_stencil3d(2, 3, 1, 14),
+    "61x6x5_sb": lambda: ragged_stencil3d(61, 6, 5, 15, bounds="scalar"),
+}
+
+
+@pytest.mark.parametrize("generic", ["0", "1"])   # plane-march kernels (march3.cuh) / generic kernels
+@pytest.mark.parametrize("case", list(R3D_CASES))
+def test_stencil3d_ragged_parity(G, oracle, monkeypatch, case, generic):
+    monkeypatch.setenv("GPCG_GENERIC", generic)
+    prob = R3D_CASES[case]()
+    A = oracle.problem_csr(prob)
+    p = 2.0 * P.uniform(98, 1, prob.n) - 1.0
+    with G.Solver.from_problem(prob) as s:
+        spmv_close(s.hessvec(p), oracle.spmv(A, p), abs_op(A, p))
+        rc, x, st = s.solve(prob.x0, prob.tol)
+        yr = s.hessvec(p, reduced=True)
+        for pc in (1,):
+            s.set_params(precond=pc)
+            rc1, x1, st1 = s.solve(prob.x0, prob.tol)
+    free = (x > prob.l) & (x < prob.u)
+    spmv_close(yr, oracle.spmv_masked(A, free, p), abs_op(A, p * free))
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=prob.tol)
+    assert rc == 0 and rc_o == 0 and rc1 == 0
+    for xx, stt in ((x, st), (x1, st1)):
+        assert abs(stt["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+        assert np.max(np.abs(xx - x_o)) <= 1e-7
+    nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+    assert not nontie
+
+
+def test_stencil3d_march_first_outer_iteration_matches_generic(G, monkeypatch):
+    """One outer iteration through the plane-march kernels and through the generic kernels:
+    the same per-point arithmetic, so the same GP / CG iteration counts and x to rounding."""
+    prob = ragged_stencil3d(47, 19, 41, 16)
+    out = {}
+    for generic in ("0", "1"):
+        monkeypatch.setenv("GPCG_GENERIC", generic)
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(refine_cap=1)
+            rc, x, st = s.solve(prob.x0, prob.tol, max_it=1)
+        out[generic] = (x, st)
+    (x0, st0), (x1, st1) = out["0"], out["1"]
+    assert st0["gp_iters"] == st1["gp_iters"] and st0["cg_iters"] == st1["cg_iters"]
+    assert np.max(np.abs(x0 - x1)) <= 1e-12 * np.max(np.abs(x1))
+
+
 def test_stencil3d_full_c4_matches_csr_golden(G):
     """Full-size C4 (256^3) through gpcg_create_stencil3d against the oracle's CSR golden:
     the same matrix (face assembly == the edge-list CSR, pinned in test_oracle_pins)."""
