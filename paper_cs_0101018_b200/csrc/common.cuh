@@ -223,6 +223,7 @@ struct Scal {
     double gp_tau, gp_eta1, gp_maxdec, gp_last_dec;
     long long gp_j, gp_cap;
     int gp_done, gp_reason;
+    int gp_fb, gp_pad;               // k6_gp_loop: steps whose speculative sweep was rejected (diagnostic)
 };
 enum GpReason : int { GP_RUNNING = 0, GP_STOP = 1, GP_CONV = 2, GP_HOST = 3 };
 

@@ -2379,8 +2379,8 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                     if (stop || cv) { if ((rc = sync_scal(h))) goto fail; break; }
                 }
                 if (trace_on())
-                    fprintf(stderr, "[gpcg] k=%lld GP phase: %lld steps reason=%d |A|=%.0f pg=%.3e t=%.2fms\n",
-                            (long long)k, jdone, S.gp_reason, S.n_active, std::sqrt(S.pg2),
+                    fprintf(stderr, "[gpcg] k=%lld GP phase: %lld steps (%d speculative sweeps rejected) reason=%d |A|=%.0f pg=%.3e t=%.2fms\n",
+                            (long long)k, jdone, S.gp_fb, S.gp_reason, S.n_active, std::sqrt(S.pg2),
                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
             } else {
                 long long j = 0;

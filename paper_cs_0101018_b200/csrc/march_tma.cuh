@@ -1144,6 +1144,7 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
     double s_alpha = S->s_alpha, s_delta = S->s_delta, s_gs = S->s_gs;
     int done = 0, reason = GP_RUNNING;
     int s_spec = 0;                               // GP_HOST: the first step size index still to try
+    int nfb = 0;                                  // rejected speculative sweeps (diagnostic)
     const unsigned int G_ = gridDim.x;
     unsigned int gen = 0;
     int k = 0, red_i = 0;
@@ -1165,6 +1166,7 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
             }
         }
         if (!have_accept) {
+            nfb += spec ? 1 : 0;
             // ---- search, alpha_h = alpha_0 2^-h for the next two h
             const int h0 = spec ? 1 : 0;
             const double al[2] = {scalbn(alpha0, -h0), scalbn(alpha0, -(h0 + 1))};
@@ -1213,6 +1215,7 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
         S->gp_j = j; S->gp_maxdec = maxdec; S->gp_last_dec = last_dec;
         S->gp_done = done; S->gp_reason = reason;
         S->s_pad = s_spec;                         // GP_HOST after a search: resume the search at h = s_spec
+        S->gp_fb = nfb;
     }
 }
 
