@@ -2266,7 +2266,19 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
             if (reduced) k_hessvec<Op, true><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
             else k_hessvec<Op, false><<<S.grid, kThreads, 0, h->st>>>(op, vin, yout, mask);
         };
-        if (use_m3(h)) {
+        // broadcast-face 2-D stencils: the TMA-fed march (needs a 16-byte aligned input for its map)
+        const bool k4 = h->tile && !h->generic && (reinterpret_cast<uintptr_t>(vin) & 15) == 0;
+        if (k4) {
+            CUtensorMap mv;
+            if (vin == S.v[VIN]) mv = S.t4[VIN];
+            else RC(make_map(h, S, &mv, vin, false, m4::kBW, m4::kBR));
+            if (reduced)
+                k4_hessvec<true><<<S.grid4_cg, m4::kThreadsWS, m4hv::kSmem, h->st>>>(S.sop, S.bg_cg, mv,
+                                                                                     S.t4m[h->free_mask], yout);
+            else
+                k4_hessvec<false><<<S.grid4_cg, m4::kThreadsWS, m4hv::kSmem, h->st>>>(S.sop, S.bg_cg, mv, S.t4m[0],
+                                                                                      yout);
+        } else if (use_m3(h)) {
             if (reduced) k7_hessvec<true><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, vin, yout, mask);
             else k7_hessvec<false><<<S.grid7, m3::kThreads, 0, h->st>>>(S.s3op, vin, yout, mask);
         } else {

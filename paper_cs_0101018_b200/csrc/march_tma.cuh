@@ -274,6 +274,63 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
         k0, flags);
 }
 
+// ============================================================================
+// a4: y = A v (full) or y = Z Z' A Z Z' v on the free mask (reduced), as k_hessvec, on the
+// TMA-fed march (broadcast faces): level 1 u(r) = [r in F] v(r) (reduced) or v(r); level 2
+// y(r-1) = (A u)(r-1), 0 off F (reduced).  Stage: v band box | mask box.
+// ============================================================================
+namespace m4hv {
+using namespace m4;
+constexpr int kV = 0, kM = kF;
+constexpr int kStage = kF + kU;                       // 4352
+constexpr int kNST = 8;
+constexpr int kSmem = kNST * kStage + 64;
+}  // namespace m4hv
+
+template <bool RED>
+__global__ void __launch_bounds__(m4::kThreadsWS, 4)
+k4_hessvec(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_v, const __grid_constant__ CUtensorMap m_mask,
+           double* __restrict__ y) {
+    using namespace m4hv;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 28 * wid + lane;
+    const bool out_lane = lane >= 2 && lane < 30;
+    int gx = 0, moff = 0, y0 = 0, y1 = 0;
+    bool col_ok = false;
+    Op5<true> op;
+    double u_m1 = 0.0, u_m2 = 0.0;
+    unsigned char m_m1 = 0;
+    band_pipeline_ws<kNST, kStage, kOut, 1, 1>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar, int) {
+            mbar_expect_tx(bar, kF + (RED ? kUt : 0));
+            tma_load_2d(st + kV, &m_v, x0 - 2, yr - G.rlo, bar);
+            if (RED) tma_load_2d(st + kM, &m_mask, floor16(x0 - 2), yr - G.rlo, bar);
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 2 + c;
+            moff = (x0 - 2) - floor16(x0 - 2);
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            op.init(A, gx);
+            u_m1 = u_m2 = 0.0;
+            m_m1 = 0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const unsigned char m = RED ? st[kM + kk * kMW + c + moff] : 1;
+            const double vv = reinterpret_cast<const double*>(st + kV)[kk * kBW + c];
+            const double u0 = m ? vv : 0.0;
+            const double q = op.apply(A, r - 1, u_m1, u_m2, u0);
+            const int r1 = r - 1;
+            if (out_lane && col_ok && r1 >= y0 && r1 < y1)
+                y[(long long)gx + (long long)A.pitch * r1] = m_m1 ? q : 0.0;
+            u_m2 = u_m1; u_m1 = u0;
+            m_m1 = m;
+        });
+}
+
 // Block flags of the CG sweep geometry G for the fixed CG mask: bit 0 if rows [yr, yr+4) of
 // the block's box columns [x0-2, x0+114) hold a free point, bit 1 if rows [yr-2, yr+2) of its
 // output columns [x0, x0+112) do.  One warp per (item, block); lanes stride the columns.
