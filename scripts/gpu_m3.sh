@@ -1,7 +1,7 @@
-# 3-D plane march: parity tests, C4s timing (march TY=8 / TY=16 / generic)
+# 3-D plane march: C4s timing (depth 2 / depth 3 / generic) + ncu of the depth-3 cauchy sweep
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "stencil3d" 2>&1 | tail -3
 export GPCG_TRACE_OFF=1
-echo "TY=8";  timeout 300 python scripts/diag.py C4s C4s 2>&1 | tail -1
-echo "TY=16"; GPCG_LIB=build_variants/libgpcg_m3ty16.so timeout 300 python scripts/diag.py C4s C4s 2>&1 | tail -1
-echo "generic"; GPCG_GENERIC=1 timeout 300 python scripts/diag.py C4s C4s 2>&1 | tail -1
+echo "depth2";  timeout 300 python scripts/diag.py C4s C4s 2>&1 | tail -1
+echo "depth3"; GPCG_LIB=build_variants/libgpcg_m3d3.so timeout 300 python scripts/diag.py C4s C4s 2>&1 | tail -1
+GPCG_LIB=build_variants/libgpcg_m3d3.so timeout 600 ncu --set full --clock-control none -k regex:"k7_" -c 3 -o gpurun_out/prof_m3d3 python scripts/diag.py C4s > /dev/null 2>&1
+python scripts/ncu_summary.py gpurun_out/prof_m3d3.ncu-rep
