@@ -396,6 +396,35 @@ def test_kernel_families_parity(G, oracle, monkeypatch, tile, case):
     assert rc == 0 and np.max(np.abs(x - x_o)) <= 1e-7
 
 
+# ------------------------------------------------------------------ the GP-phase cap (reading R13)
+@pytest.mark.parametrize("cap", [2, 5])
+@pytest.mark.parametrize("case", ["C0", "c3_family_160", "jb80_eps0.9"])
+def test_gp_cap_parity(G, oracle, monkeypatch, case, cap):
+    """GP phases that stop at gpcg_params.gp_cap (persistent GP loop and host-driven path)
+    follow the oracle with the same cap: same first-outer-iteration counts, same x*."""
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    prm = oracle.default_params(gp_cap=cap, refine_cap=1)
+    rc_o1, x_o1, st_o1 = oracle.solve_problem(prob, tol=tol, max_it=1, params=prm)
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, params=oracle.default_params(gp_cap=cap))
+    for graph in ("1", "0"):
+        monkeypatch.setenv("GPCG_GP_GRAPH", graph)
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(gp_cap=cap, refine_cap=1)
+            rc1, x1, st1 = s.solve(prob.x0, tol, max_it=1, allow_error=True)
+            s.set_params(gp_cap=cap, refine_cap=30)
+            rc, x, st = s.solve(prob.x0, tol)
+        assert st1["gp_iters"] == st_o1["gp_iters"], (graph, st1["gp_iters"], st_o1["gp_iters"])
+        # after a capped GP phase the CG call starts far from the face minimiser and runs long
+        # on a flat decrease profile, so the C-G vs textbook rounding can move the cgstop1
+        # iteration by a few (C0: 1e-7 relative in x; jb80: 213 vs 210 iterations)
+        assert abs(st1["cg_iters"] - st_o1["cg_iters"]) <= 1 + 0.03 * st_o1["cg_iters"], \
+            (st1["cg_iters"], st_o1["cg_iters"])
+        assert rc == 0 and rc_o == 0
+        assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+        assert np.max(np.abs(x - x_o)) <= 1e-7
+
+
 # ------------------------------------------------------------------ 3-D 7-point stencil (NEXT-2)
 @pytest.mark.parametrize("m", [5, 12, 16])
 def test_stencil3d_spmv_and_solve_parity(G, oracle, m):
