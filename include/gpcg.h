@@ -107,8 +107,9 @@ typedef struct {
     double t_total_ms, t_cg_ms, t_gp_ms;  /* CUDA-event times (CG chunks, GP sweeps) */
     int32_t status;
     int32_t kernel_launches; /* library kernels launched during the call (low 31 bits) */
-    /* steady-state CG timing: CUDA events around every CG graph chunk in which no
-     * iteration had finished, i.e. cg_iters_timed real iterations took
+    /* CG timing: CUDA events around every persistent CG launch (one slab, one rank:
+     * the whole call) or, on the graph-chunk path (slabs / ranks), around every chunk
+     * in which no iteration had finished; cg_iters_timed iterations took
      * t_cg_timed_ms of device time; cg_free_iters_timed = sum of |F| over them. */
     int64_t cg_iters_timed, cg_free_iters_timed;
     double t_cg_timed_ms;

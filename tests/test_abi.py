@@ -89,3 +89,19 @@ def test_product_path_does_not_import_oracle():
         if f.endswith(".py"):
             txt = open(os.path.join(pkg, f)).read()
             assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def example_binary(tmp_dir):
+    """Compile examples/solve_bearing.c (plain C against include/gpcg.h and libgpcg.so)."""
+    import subprocess
+    out = os.path.join(tmp_dir, "solve_bearing")
+    libdir = os.path.join(ROOT, "paper_cs_0101018_b200")
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "solve_bearing.c"), "-L", libdir, "-lgpcg",
+                           "-Wl,-rpath," + libdir, "-lm", "-o", out])
+    return out
+
+
+def test_c_example_builds_against_the_abi(lib, tmp_path):
+    """The boundary is usable from C alone: the example compiles and links with -Werror."""
+    assert os.path.exists(example_binary(str(tmp_path)))

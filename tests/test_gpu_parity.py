@@ -191,6 +191,20 @@ def test_solve_enumeration_small(G):
         assert np.max(np.abs(x - B.enum_solve(A, b, l, u))) <= 1e-6
 
 
+def test_c_example_matches_oracle(G, oracle, tmp_path):
+    """examples/solve_bearing.c -- the ABI from plain C, host arrays -- solves C0 to the oracle's q*."""
+    import subprocess
+    from tests.test_abi import example_binary
+    exe = example_binary(str(tmp_path))
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    fields = dict(kv.split("=") for kv in out.stdout.split())
+    rc_o, x_o, st_o = oracle.solve_problem(P.c0(), tol=-1e-8)
+    assert fields["status"] == "0" and rc_o == 0
+    assert abs(float(fields["q"]) - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert abs(int(fields["free"]) - int(np.sum(x_o > 0.0))) <= 2      # degenerate ties aside
+
+
 def test_device_pointers_and_determinism(G):
     import torch
     prob = P.c1()
