@@ -75,8 +75,14 @@ __device__ __forceinline__ int sk(int i, int jl) { return ((i + jl) & (kTile - 1
 // The backward solve reads the north / east couplings as cs of (i, jl + 1) and cw of (i + 1, jl)
 // (A symmetric; cs of a tile's row 0 and cw of its column 0 are 0, which drops the couplings
 // across tile edges).
+// Broadcast faces (journal bearing: the couplings of column i are the same in every row):
+// instead of cs / cw the factor stores one code byte per element -- bit 0: the south
+// coupling is present (v, s in F, s in the tile), bit 1: the west one -- and the solve forms
+// cs = bit0 ? w_s(i) : 0, cw = bit1 ? w_w(i) : 0 from the lane's column faces held in
+// registers: 9 instead of 24 bytes of factor per element and wavefront step.
 struct BjFactor {
     double *dinv, *cs, *cw;
+    unsigned char* code;
 };
 
 constexpr int kBjThreads = 64;                                        // 2 tiles per CTA
@@ -117,8 +123,12 @@ k_bjilu_factor(StencilOp A, const unsigned char* __restrict__ mask, BjFactor F) 
             Ds[q] = cs;
             Dw[q] = cw;
             Mf[q] = f;
-            F.cs[tb + q] = cs;
-            F.cw[tb + q] = cw;
+            if (F.code) {
+                F.code[tb + q] = (unsigned char)((cs != 0.0 ? 1 : 0) | (cw != 0.0 ? 2 : 0));
+            } else {
+                F.cs[tb + q] = cs;
+                F.cw[tb + q] = cw;
+            }
         }
         __syncwarp();
         double d_prev = 1.0;                              // d of (i, jl - 1): this lane, previous step
@@ -153,38 +163,65 @@ k_bjilu_factor(StencilOp A, const unsigned char* __restrict__ mask, BjFactor F) 
 constexpr int kBjGroup = GPCG_BJ_UNROLL;
 constexpr int kBjSteps = 2 * kTile;                      // 63 wavefront steps + 1 idle (no active lane)
 
+template <bool BC>
 struct FacGroup {
     double d[kBjGroup], s[kBjGroup], w[kBjGroup];
+    unsigned int c[BC ? kBjGroup : 1];
 };
 
-template <bool BWD>
-__device__ __forceinline__ void load_group(FacGroup& G, const double* Fd, const double* Fs, const double* Fw, int g) {
+// BC: s / w are formed from the code byte and the lane's column faces fs / fw (0 when absent)
+template <bool BWD, bool BC>
+__device__ __forceinline__ void load_group(FacGroup<BC>& G, const double* Fd, const double* Fs, const double* Fw,
+                                           const unsigned char* Fc, int g) {
 #pragma unroll
     for (int k = 0; k < kBjGroup; ++k) {
         const int l = BWD ? kBjSteps - 1 - (g * kBjGroup + k) : g * kBjGroup + k;
         const int row = (l & (kTile - 1)) * kTile;
         const int nrow = BWD ? ((l + 1) & (kTile - 1)) * kTile : row;
         G.d[k] = __ldg(Fd + row);
-        G.s[k] = __ldg(Fs + nrow);                       // fwd: cs of (i, jl); bwd: cs of (i, jl + 1)
-        G.w[k] = __ldg(Fw + nrow);                       // fwd: cw of (i, jl); bwd: lane i+1 has cw of (i+1, jl)
+        if constexpr (BC) {
+            G.c[k] = __ldg(Fc + nrow);                   // fwd: code of (i, jl); bwd: of (i, jl + 1)
+        } else {
+            G.s[k] = __ldg(Fs + nrow);                   // fwd: cs of (i, jl); bwd: cs of (i, jl + 1)
+            G.w[k] = __ldg(Fw + nrow);                   // fwd: cw of (i, jl); bwd: lane i+1 has cw of (i+1, jl)
+        }
     }
 }
 
+template <bool BC>
+__device__ __forceinline__ void decode_group(FacGroup<BC>& G, double fs, double fw) {
+    if constexpr (BC) {
+#pragma unroll
+        for (int k = 0; k < kBjGroup; ++k) {
+            G.s[k] = (G.c[k] & 1u) ? fs : 0.0;
+            G.w[k] = (G.c[k] & 2u) ? fw : 0.0;
+        }
+    }
+}
+
+template <bool BC>
 __device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0, long long tb, const BjFactor& F,
                                              double* __restrict__ z, double* T) {
     const int lane = threadIdx.x & 31;
     const double* Fd = F.dinv + tb + lane;
-    const double* Fs = F.cs + tb + lane;
-    const double* Fw = F.cw + tb + lane;
+    const double* Fs = BC ? nullptr : F.cs + tb + lane;
+    const double* Fw = BC ? nullptr : F.cw + tb + lane;
+    const unsigned char* Fc = BC ? F.code + tb + lane : nullptr;
+    double fs = 0.0, fw = 0.0;                            // BC: this column's south / west faces
+    if (BC && x0 + lane < A.nx) {
+        fs = __ldg(A.wy + x0 + lane);
+        fw = __ldg(A.wx + x0 + lane);
+    }
     constexpr int NG = kBjSteps / kBjGroup;
     __syncwarp();
     double t_prev = 0.0;                                  // t of (i, jl - 1)
     double rz = 0.0;
-    FacGroup cur, nxt;
-    load_group<false>(cur, Fd, Fs, Fw, 0);
+    FacGroup<BC> cur, nxt;
+    load_group<false, BC>(cur, Fd, Fs, Fw, Fc, 0);
 #pragma unroll 1
     for (int g = 0; g < NG; ++g) {
-        if (g + 1 < NG) load_group<false>(nxt, Fd, Fs, Fw, g + 1);
+        if (g + 1 < NG) load_group<false, BC>(nxt, Fd, Fs, Fw, Fc, g + 1);
+        decode_group<BC>(cur, fs, fw);
 #pragma unroll
         for (int k = 0; k < kBjGroup; ++k) {
             const int l = g * kBjGroup + k;
@@ -202,10 +239,11 @@ __device__ __forceinline__ double tile_solve(const StencilOp& A, int x0, int y0,
     }
     __syncwarp();
     double z_prev = 0.0;                                  // z of (i, jl + 1)
-    load_group<true>(cur, Fd, Fs, Fw, 0);
+    load_group<true, BC>(cur, Fd, Fs, Fw, Fc, 0);
 #pragma unroll 1
     for (int g = 0; g < NG; ++g) {
-        if (g + 1 < NG) load_group<true>(nxt, Fd, Fs, Fw, g + 1);
+        if (g + 1 < NG) load_group<true, BC>(nxt, Fd, Fs, Fw, Fc, g + 1);
+        decode_group<BC>(cur, fs, fw);
 #pragma unroll
         for (int k = 0; k < kBjGroup; ++k) {
             const int l = kBjSteps - 1 - (g * kBjGroup + k);
@@ -252,7 +290,7 @@ k_pcg2_init(StencilOp A, const double* __restrict__ y, const double* __restrict_
     });
 }
 
-template <int KIND>   // 0: init solve (gamma_0), 1: iteration update + solve (gamma_{j+1})
+template <int KIND, bool BC>   // KIND 0: init solve (gamma_0), 1: iteration update + solve (gamma_{j+1})
 __global__ void __launch_bounds__(kBjThreads, kBjMinBlocks)
 k_pcg2_solve(StencilOp A, BjFactor F, const __grid_constant__ CUtensorMap m_r, int row0, double* __restrict__ r,
              const double* __restrict__ q, double* __restrict__ z, double eta2, long long cap, Scal* S,
@@ -298,7 +336,7 @@ k_pcg2_solve(StencilOp A, BjFactor F, const __grid_constant__ CUtensorMap m_r, i
             }
             T[jl * kTile + lane] = in ? rv : 0.0;
         }
-        acc[0] += tile_solve(A, x0, y0, (long long)tt * kTile * kTile, F, z, T);
+        acc[0] += tile_solve<BC>(A, x0, y0, (long long)tt * kTile * kTile, F, z, T);
     });
     reduce_and_finish<1>(acc, R, [&](double* t) {
         if (KIND == 0) pcg2_init_fin(t[0], eta2, cap, S);

@@ -1437,9 +1437,11 @@ int bj_grid_mv(const gpcg_problem* h, const Slab& S) {
     return (int)std::max<long long>(1, std::min<long long>(bj_tiles(h, S), (long long)h->sms * 8));
 }
 
-BjFactor bj_factor(const Slab& S, long long nt) {
+// broadcast faces: dinv + code bytes (the cs / cw arrays unused); else dinv, cs, cw
+BjFactor bj_factor(const gpcg_problem* h, const Slab& S, long long nt) {
     const long long e = nt * kTile * kTile;
-    return BjFactor{S.bjf, S.bjf + e, S.bjf + 2 * e};
+    unsigned char* code = h->bc ? reinterpret_cast<unsigned char*>(S.bjf + 3 * e) : nullptr;
+    return BjFactor{S.bjf, S.bjf + e, S.bjf + 2 * e, code};
 }
 
 int enqueue_bj_iter(gpcg_problem* h, int a) {
@@ -1466,7 +1468,12 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
     RC(exchange(h, {vq(bb)}));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        k_pcg2_solve<1><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, bj_tiles(h, S)), S.tbr,
+        if (h->bc)
+            k_pcg2_solve<1, true><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(h, S, bj_tiles(h, S)), S.tbr,
+                                                                              S.glo, S.v[VRHO0], S.v[VS0], S.v[VRHO1],
+                                                                              0.0, 0, h->dS, h->red(s));
+        else
+            k_pcg2_solve<1, false><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(h, S, bj_tiles(h, S)), S.tbr,
                                                                               S.glo, S.v[VRHO0], S.v[VS0], S.v[VRHO1],
                                                                               0.0, 0, h->dS, h->red(s));
         CKLAUNCH();
@@ -1479,21 +1486,28 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
     if (h->is_csr || h->is3d)
         return set_err(GPCG_EINVAL, "precond = 2 (block-Jacobi ILU(0)) is implemented for 2-D stencils");
     RC(set_smem(k_bjilu_factor, kFactorSmem));
-    RC(set_smem(k_pcg2_solve<0>, kSolveSmem));
-    RC(set_smem(k_pcg2_solve<1>, kSolveSmem));
+    RC(set_smem(k_pcg2_solve<0, false>, kSolveSmem));
+    RC(set_smem(k_pcg2_solve<1, false>, kSolveSmem));
+    RC(set_smem(k_pcg2_solve<0, true>, kSolveSmem));
+    RC(set_smem(k_pcg2_solve<1, true>, kSolveSmem));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const long long nt = bj_tiles(h, S);
         if (!S.bjf) {
-            CK(dalloc(h, &S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double)));
+            CK(dalloc(h, &S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double) + (size_t)nt * kTile * kTile));
             RC(make_map(h, S, &S.tbr, S.v[VRHO0], false, kTile, kTile));
         }
         k_pcg2_init<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vy(cur)], S.v[VB], S.m[cur], S.m[MKCG], S.v[VRHO0],
                                                     S.v[VQ0], S.v[VQ1], S.v[VW]);
         CKLAUNCH();
-        k_bjilu_factor<<<bj_grid_tiles(h, S), kBjThreads, kFactorSmem, h->st>>>(S.sop, S.m[MKCG], bj_factor(S, nt));
+        k_bjilu_factor<<<bj_grid_tiles(h, S), kBjThreads, kFactorSmem, h->st>>>(S.sop, S.m[MKCG], bj_factor(h, S, nt));
         CKLAUNCH();
-        k_pcg2_solve<0><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(S, nt), S.tbr, S.glo,
+        if (h->bc)
+            k_pcg2_solve<0, true><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(h, S, nt), S.tbr, S.glo,
+                                                                              S.v[VRHO0], S.v[VS0], S.v[VRHO1], eta2,
+                                                                              cap, h->dS, h->red(s));
+        else
+            k_pcg2_solve<0, false><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(h, S, nt), S.tbr, S.glo,
                                                                               S.v[VRHO0], S.v[VS0], S.v[VRHO1], eta2,
                                                                               cap, h->dS, h->red(s));
         CKLAUNCH();
