@@ -1,0 +1,58 @@
+// Microbenchmark: DRAM bandwidth of reading S fp64 arrays of 16.8M elements (C4s-sized) with
+// each warp reading 256-byte row segments of a 2-D (x 256, y) tiling (the 3-D plane march's
+// pattern: a CTA of 8 warps takes 8 consecutive rows of one 32-column strip) versus plain
+// contiguous grid-stride streaming of the same arrays.  Sum written to avoid dead code.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 streams.cu -o streams.bin
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int S>
+__global__ void k_tiled(const double* const* a, long long n, int nx, double* out) {
+    // block = 32 x 8 threads, blocks tile (x strips of 32) x (y rows of 8); rows are nx long
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int strips = nx / 32;
+    const long long rows = n / nx;
+    double acc = 0.0;
+    for (long long blk = blockIdx.x; blk < (rows / 8) * strips; blk += gridDim.x) {
+        const long long r = (blk / strips) * 8 + ty;
+        const long long v = r * nx + (blk % strips) * 32 + tx;
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc += __ldg(a[s] + v);
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
+template <int S>
+__global__ void k_flat(const double* const* a, long long n, double* out) {
+    double acc = 0.0;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc += __ldg(a[s] + v);
+    if (acc == 1.2345) out[0] = acc;
+}
+
+int main() {
+    const long long n = 256LL * 256 * 256;
+    const int S = 6;
+    double* h[S];
+    for (int s = 0; s < S; ++s) { cudaMalloc(&h[s], n * 8); cudaMemset(h[s], 0, n * 8); }
+    double** d; cudaMalloc(&d, sizeof(h)); cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
+    double* out; cudaMalloc(&out, 8);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int mode = 0; mode < 2; ++mode)
+        for (int grid : {148 * 4, 148 * 8, 148 * 16}) {
+            float best = 1e9;
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaEventRecord(a);
+                if (mode == 0) k_tiled<S><<<grid, 256>>>(d, n, 256, out);
+                else k_flat<S><<<grid, 256>>>(d, n, out);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms; cudaEventElapsedTime(&ms, a, b);
+                if (ms < best) best = ms;
+            }
+            printf("%s grid %d: %.1f us, %.0f GB/s\n", mode ? "flat " : "tiled", grid, best * 1e3,
+                   S * n * 8.0 / (best * 1e-3) / 1e9);
+        }
+    return 0;
+}
