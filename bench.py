@@ -151,10 +151,11 @@ def dist_env():
     return rank, world, local
 
 
-def oracle_sample(prob, budget_s):
-    """Oracle GPCG on prob for at most budget_s seconds -> (cg_iters, seconds, stats)."""
+def oracle_sample(prob, budget_s, A=None):
+    """Oracle GPCG on prob for at most budget_s seconds -> (cg_iters, seconds, stats).
+    A: the oracle's CSR of prob (built here when not given)."""
     from oracle import oracle as O
-    A = O.problem_csr(prob)
+    A = O.problem_csr(prob) if A is None else A
     params = O.default_params(time_budget_s=float(budget_s))
     rc, x, st = O.solve(A, prob.b, prob.l, prob.u, prob.c, prob.x0, prob.tol, 500, params)
     return st["cg_iters"], st["seconds"], st
@@ -167,14 +168,16 @@ def run_reference(args):
         return 0
     from paper_cs_0101018_b200 import problems as P
     prob = P.get(args.config)
+    from oracle import oracle as O
+    A = O.problem_csr(prob)                      # assembled once (not part of a step)
     total = args.steps + args.warmup
     budget = max(5.0, min(20.0, 150.0 / max(total, 1)))
     for _ in range(args.warmup):
-        oracle_sample(prob, budget)
+        oracle_sample(prob, budget, A)
     iters, secs = 0, 0.0
     last = None
     for _ in range(args.steps):
-        it, s, st = oracle_sample(prob, budget)
+        it, s, st = oracle_sample(prob, budget, A)
         iters += it
         secs += s
         last = st
