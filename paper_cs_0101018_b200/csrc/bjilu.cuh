@@ -25,7 +25,6 @@
 
 #include "common.cuh"
 #include "fin.cuh"
-#include "march.cuh"
 #include "tile.cuh"
 
 namespace gpcg {
@@ -435,74 +434,6 @@ k_pcg2_matvec_tile(StencilOp A, const unsigned char* __restrict__ mask, const do
         __syncthreads();
     }
     reduce_and_finish<1>(acc, R, [&](double* tt) { pcg2_alpha_fin(tt[0], S); });
-}
-
-// The same step on the column march (march.cuh, H = 1): level 1 forms p(r) once per point,
-// level 2 applies A at row r - 1 from registers and shuffles; w, p_new, q written at r - 1.
-struct RawPm {
-    double z, p;
-    unsigned char m;
-};
-
-template <bool BC>
-__global__ void __launch_bounds__(kMarchThreads, kMarchMinBlocks)
-k2_pcg2_matvec(StencilOp A, MarchGeom G, const unsigned char* __restrict__ mask, const double* __restrict__ z,
-               const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
-               double* __restrict__ w, Scal* S, RedScratch R) {
-    if (*(volatile int*)&S->cg_done) return;
-    const double beta = S->cg_beta;
-    const double alpha_prev = S->cg_alpha;                // alpha of the previous iteration (0 at the first)
-    constexpr int H = 1;
-    const int lane = threadIdx.x & 31;
-    const bool out_lane = lane >= H && lane < 32 - H;
-    double acc[1] = {0.0};
-    int i, j0, j1;
-    if (march_item<H>(A, G, i, j0, j1)) {
-        const bool col_ok = (i >= 0 && i < A.nx);
-        Op5<BC> op;
-        op.init(A, i);
-        const int rend = min(A.rhi, j1 + H);
-        double pn_m2 = 0.0, pn_m1 = 0.0;                  // p_new(r-2), p_new(r-1)
-        double po_m1 = 0.0;                               // p_old(r-1)
-        unsigned char m_m1 = 0;
-        pipeline<unsigned char, RawPm>(
-            j0 - 1, j1 - j0 + 2,
-            [&](int r) -> unsigned char {
-                unsigned char m = 0;
-                if (r >= A.rlo && r < rend && col_ok) m = __ldg(mask + i + A.pitch * r);
-                return m;
-            },
-            [&](int r, unsigned char m) {
-                RawPm x{0.0, 0.0, m};
-                if (m) {
-                    const int v = i + A.pitch * r;
-                    x.z = z[v];
-                    x.p = p_old[v];
-                }
-                return x;
-            },
-            [&](int r, const RawPm& x) {
-                const double pn0 = x.m ? fma(beta, x.p, x.z) : 0.0;
-                const double qv = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
-                const int r1 = r - 1;
-                if (out_lane && col_ok && r1 >= j0 && r1 < j1) {
-                    const int v = i + A.pitch * r1;
-                    if (m_m1) {
-                        w[v] = fma(alpha_prev, po_m1, w[v]);
-                        p_new[v] = pn_m1;
-                        q[v] = qv;
-                        acc[0] = fma(pn_m1, qv, acc[0]);
-                    } else {
-                        p_new[v] = 0.0;
-                        q[v] = 0.0;
-                    }
-                }
-                pn_m2 = pn_m1; pn_m1 = pn0;
-                po_m1 = x.p;
-                m_m1 = x.m;
-            });
-    }
-    reduce_and_finish<1>(acc, R, [&](double* t) { pcg2_alpha_fin(t[0], S); });
 }
 
 // after the last iteration j: w += alpha_j p_j (p is 0 off F)

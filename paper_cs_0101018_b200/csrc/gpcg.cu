@@ -215,7 +215,6 @@ struct Slab {
 struct gpcg_problem {
     int dev = 0, sms = 148;
     cudaMemPool_t pool = nullptr;   // device allocations (mem_pool); null: cudaMalloc / cudaFree
-    int bj_matvec = 0;              // GPCG_BJ_MATVEC: BJ-ILU PCG matvec 0 = 2-D tile sweep, 1 = column march
     cudaStream_t user = nullptr;    // caller's stream
     cudaStream_t st = nullptr;      // private work stream (capturable)
     cudaEvent_t ev_sync = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c0 = nullptr, ev_c1 = nullptr;
@@ -761,8 +760,6 @@ int create_streams(gpcg_problem* h, void* stream) {
     }
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     {
-        const char* e7 = getenv("GPCG_BJ_MATVEC");
-        h->bj_matvec = (e7 && e7[0] == '1') ? 1 : 0;
         const char* e6 = getenv("GPCG_POOL");
         h->pool = (e6 && e6[0] == '0') ? nullptr : mem_pool(h->dev);
     }
@@ -1448,20 +1445,13 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
     const int bb = a ^ 1;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        const int tile_mode = h->bj_matvec;
         if (h->generic)
             k_pcg2_matvec<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VRHO1], S.v[vq(a)], S.v[vq(bb)],
                                                           S.v[VS0], S.v[VW], h->dS, h->red(s));
-        else if (tile_mode == 0)
+        else
             k_pcg2_matvec_tile<<<bj_grid_mv(h, S), kMvThreads, 0, h->st>>>(S.sop, S.m[MKCG], S.v[VRHO1], S.v[vq(a)],
                                                                           S.v[vq(bb)], S.v[VS0], S.v[VW], h->dS,
                                                                           h->red(s));
-        else if (h->bc)
-            k2_pcg2_matvec<true><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.m[MKCG], S.v[VRHO1], S.v[vq(a)],
-                                                                         S.v[vq(bb)], S.v[VS0], S.v[VW], h->dS, h->red(s));
-        else
-            k2_pcg2_matvec<false><<<S.grid_m1, kMarchThreads, 0, h->st>>>(S.sop, S.mg1, S.m[MKCG], S.v[VRHO1], S.v[vq(a)],
-                                                                          S.v[vq(bb)], S.v[VS0], S.v[VW], h->dS, h->red(s));
         CKLAUNCH();
     }
     RC(finish_reduce(h, fin(FIN_PCG2_ALPHA), 1));
