@@ -439,6 +439,25 @@ def test_gp_cap_parity(G, oracle, monkeypatch, case, cap):
         assert np.max(np.abs(x - x_o)) <= 1e-7
 
 
+# ------------------------------------------------------------------ A/B switches of the single-slab path
+@pytest.mark.parametrize("switch", ["GPCG_CG_PERSIST", "GPCG_GP_PERSIST", "GPCG_CG_SKIP", "GPCG_GP_SPEC"])
+@pytest.mark.parametrize("case", ["C0", "jb80_eps0.9", "c3_family_160"])
+def test_path_switches_parity(G, oracle, monkeypatch, switch, case):
+    """Each switch turns one device-side optimisation off (graph-chunk CG / GP instead of the
+    persistent loops, no all-active block skipping, no speculative GP step): the same x*."""
+    monkeypatch.setenv(switch, "0")
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    for pc in (0, 1):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(precond=pc)
+            rc, x, st = s.solve(prob.x0, tol)
+        assert rc == 0 and rc_o == 0
+        assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+        assert np.max(np.abs(x - x_o)) <= 1e-7
+
+
 # ------------------------------------------------------------------ 3-D 7-point stencil (NEXT-2)
 @pytest.mark.parametrize("m", [5, 12, 16])
 def test_stencil3d_spmv_and_solve_parity(G, oracle, m):
