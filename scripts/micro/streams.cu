@@ -22,6 +22,24 @@ __global__ void k_tiled(const double* const* a, long long n, int nx, double* out
     if (acc == 1.2345) out[0] = acc;
 }
 
+// the plane march's order: block = (x strip of 32, y block of 8, z chunk of 32 planes), marching k
+template <int S>
+__global__ void k_zmarch(const double* const* a, long long n, int nx, double* out) {
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int ny = nx, nz = (int)(n / ((long long)nx * ny));
+    const int strips = nx / 32, yb = ny / 8, zc = nz / 32;
+    double acc = 0.0;
+    for (int item = blockIdx.x; item < strips * yb * zc; item += gridDim.x) {
+        const int bx = item % strips, by = (item / strips) % yb, bz = item / (strips * yb);
+        for (int k = bz * 32; k < bz * 32 + 32; ++k) {
+            const long long v = ((long long)k * ny + by * 8 + ty) * nx + bx * 32 + tx;
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc += __ldg(a[s] + v);
+        }
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
 template <int S>
 __global__ void k_flat(const double* const* a, long long n, double* out) {
     double acc = 0.0;
@@ -39,19 +57,20 @@ int main() {
     double** d; cudaMalloc(&d, sizeof(h)); cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
     double* out; cudaMalloc(&out, 8);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-    for (int mode = 0; mode < 2; ++mode)
+    for (int mode = 0; mode < 3; ++mode)
         for (int grid : {148 * 4, 148 * 8, 148 * 16}) {
             float best = 1e9;
             for (int rep = 0; rep < 5; ++rep) {
                 cudaEventRecord(a);
                 if (mode == 0) k_tiled<S><<<grid, 256>>>(d, n, 256, out);
-                else k_flat<S><<<grid, 256>>>(d, n, out);
+                else if (mode == 1) k_flat<S><<<grid, 256>>>(d, n, out);
+                else k_zmarch<S><<<grid, 256>>>(d, n, 256, out);
                 cudaEventRecord(b);
                 cudaEventSynchronize(b);
                 float ms; cudaEventElapsedTime(&ms, a, b);
                 if (ms < best) best = ms;
             }
-            printf("%s grid %d: %.1f us, %.0f GB/s\n", mode ? "flat " : "tiled", grid, best * 1e3,
+            printf("%s grid %d: %.1f us, %.0f GB/s\n", mode == 0 ? "tiled " : (mode == 1 ? "flat  " : "zmarch"), grid, best * 1e3,
                    S * n * 8.0 / (best * 1e-3) / 1e9);
         }
     return 0;
