@@ -1,16 +1,18 @@
 // gpcg.cu -- libgpcg.so: the C ABI of include/gpcg.h and the host state machine
 // of Algorithm GPCG driving the sm_100a kernels.
 //
-// Control: the host runs the outer / GP logic from a few
-// device scalars read once per GP sub-step (one pinned readback); the CG inner
-// solve runs as CUDA-graph chunks of `cg_chunk` single-reduction iterations
-// whose device-side finaliser sets a done flag (later launches are no-ops),
-// polled once per chunk.  The decisions follow, step by step, the same
-// algorithm as oracle/gpcg_oracle.c (written independently; no shared code).
+// Control: the host runs the outer logic from a few device
+// scalars (one pinned readback per phase).  One slab on one rank with a 2-D
+// broadcast-face stencil: a whole GP phase and a whole CG call are one persistent
+// cooperative kernel each (march_tma.cuh k6_*), deciding on the device.  Otherwise
+// the GP phase and the CG solve run as CUDA-graph chunks whose device-side
+// finalisers set done flags (later launches are no-ops), polled once per chunk.
+// The decisions follow, step by step, the same algorithm as oracle/gpcg_oracle.c
+// (written independently; no shared code).
 //
 // Slabs: a handle owns one or more contiguous row slabs of
-// the problem.  Each slab stores its vectors with ghost rows (stencil: 2 grid
-// rows per side, CSR: the band of neighbour rows its columns reach), refreshed
+// the problem.  Each slab stores its vectors with ghost rows (2-D stencil: 3 grid
+// rows per side, 3-D: 1 plane, CSR: the band of neighbour rows its columns reach), refreshed
 // after every sweep that writes a vector some neighbour reads -- by a device
 // copy between slabs of this process, or by NCCL send/recv between ranks.
 // With more than one slab (or rank) every reducing kernel DEFERS its decision
