@@ -2278,6 +2278,10 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
             CUtensorMap mv;
             if (vin == S.v[VIN]) mv = S.t4[VIN];
             else RC(make_map(h, S, &mv, vin, false, m4::kBW, m4::kBR));
+            if (m4hv::kSmem > 48 * 1024) {               // wide bands (GPCG_M4_WARPS = 8)
+                RC(set_smem(k4_hessvec<true>, m4hv::kSmem));
+                RC(set_smem(k4_hessvec<false>, m4hv::kSmem));
+            }
             if (reduced)
                 k4_hessvec<true><<<S.grid4_cg, m4::kThreadsWS, m4hv::kSmem, h->st>>>(S.sop, S.bg_cg, mv,
                                                                                      S.t4m[h->free_mask], yout);

@@ -32,22 +32,27 @@ namespace gpcg {
 #ifndef GPCG_CG_NST
 #define GPCG_CG_NST 4       // CG sweep pipeline stages (tuning)
 #endif
+#ifndef GPCG_M4_WARPS
+#define GPCG_M4_WARPS 8     // consumer warps per CTA of the band engines: 8 halves the CTAs of the
+                            // persistent loops (grid barrier and partial sums) against 4 (-5 % per step)
+#endif
 #ifndef GPCG_CG_MINB
-#define GPCG_CG_MINB 4      // CG sweep CTAs per SM the register budget is sized for (tuning)
+#define GPCG_CG_MINB (16 / GPCG_M4_WARPS)   // CG sweep CTAs per SM the register budget is sized for
 #endif
 namespace m4 {
-constexpr int kWarps = 4;                 // consumer warps (one per 28 / 26-column strip)
+constexpr int kWarps = GPCG_M4_WARPS;     // consumer warps (one per 28 / 26-column strip)
+constexpr int kMinB = 16 / kWarps;        // CTAs per SM the register budgets are sized for (64 warps)
 constexpr int kThreads = 32 * kWarps;     // lock-step engine: thread 0 also issues the TMA loads
 constexpr int kThreadsWS = 32 * (kWarps + 1);  // warp-specialised engine: + one TMA producer warp
-constexpr int kOut = 28 * kWarps;         // 112 output columns per band
-constexpr int kBW = kOut + 4;             // 116 box columns (2 halo each side)
-constexpr int kMW = 144;                  // u8 mask box width (start floored to 16 B, 116 + 15 < 144)
+constexpr int kOut = 28 * kWarps;         // output columns per band (224 at 8 warps)
+constexpr int kBW = kOut + 4;             // box columns (2 halo each side)
+constexpr int kMW = (kBW + 15 + 15) / 16 * 16;   // u8 mask box width (start floored to 16 B): 144 at 4 warps
 constexpr int kBR = 4;                    // rows per pipeline block (small stages: 3-4 CTAs per SM)
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
-constexpr int kF = kBR * kBW * 8;         // 3712 B: one f64 band box
-constexpr int kFo = kBR * kOut * 8;       // 3584 B: one f64 box of the output columns only
-constexpr int kUt = kBR * kMW;            // 576 B delivered for one u8 mask box
-constexpr int kU = r128(kUt);             // 640 B reserved (stage arrays stay 128-byte aligned)
+constexpr int kF = kBR * kBW * 8;         // one f64 band box
+constexpr int kFo = kBR * kOut * 8;       // one f64 box of the output columns only
+constexpr int kUt = kBR * kMW;            // bytes delivered for one u8 mask box
+constexpr int kU = r128(kUt);             // reserved (stage arrays stay 128-byte aligned)
 static_assert(kF % 128 == 0 && kFo % 128 == 0, "TMA destinations stay 128-byte aligned");
 }  // namespace m4
 
@@ -197,7 +202,7 @@ __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned
 namespace m4cg {
 using namespace m4;
 constexpr int kRho = 0, kP = kF, kW = 2 * kF, kM = 2 * kF + kFo;
-constexpr int kStage = kM + kU;                       // 11648
+constexpr int kStage = kM + kU;
 constexpr int kTx = kM + kUt;                         // bytes the TMA delivers per stage
 constexpr int kNST = GPCG_CG_NST;
 constexpr int kSmem = kNST * kStage + 64;
@@ -282,13 +287,13 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
 namespace m4hv {
 using namespace m4;
 constexpr int kV = 0, kM = kF;
-constexpr int kStage = kF + kU;                       // 4352
+constexpr int kStage = kF + kU;
 constexpr int kNST = 8;
 constexpr int kSmem = kNST * kStage + 64;
 }  // namespace m4hv
 
 template <bool RED>
-__global__ void __launch_bounds__(m4::kThreadsWS, 4)
+__global__ void __launch_bounds__(m4::kThreadsWS, m4::kMinB)
 k4_hessvec(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_v, const __grid_constant__ CUtensorMap m_mask,
            double* __restrict__ y) {
     using namespace m4hv;
@@ -498,7 +503,7 @@ struct AccLayout4 {
 };
 
 template <bool SB, bool HasDir, bool BB>
-__global__ void __launch_bounds__(m4::kThreads, 4)
+__global__ void __launch_bounds__(m4::kThreads, m4::kMinB)
 k4_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
@@ -608,7 +613,7 @@ struct SrchLayout4 {
 };
 
 template <bool SB, bool DG>
-__global__ void __launch_bounds__(m4::kThreads, 4)
+__global__ void __launch_bounds__(m4::kThreads, m4::kMinB)
 k4_search(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_g,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, double sgn,
@@ -696,11 +701,11 @@ k4_search(StencilOp A, BandGeom G, Bounds Bd, const __grid_constant__ CUtensorMa
 // direction: y_out = P[y]).
 // ============================================================================
 namespace m5 {
-constexpr int kOut = 26 * m4::kWarps;        // 104 output columns per band
-constexpr int kBW = 112;                     // f64 box columns (x0 - 4 .. x0 + 107)
-constexpr int kMW = 128;                     // u8 mask box width (start floored to 16 B)
-constexpr int kF = m4::kBR * kBW * 8;        // 3584 B
-constexpr int kUt = m4::kBR * kMW;           // 512 B
+constexpr int kOut = 26 * m4::kWarps;        // output columns per band (208 at 8 warps)
+constexpr int kBW = kOut + 8;                // f64 box columns (x0 - 4 .. x0 + kOut + 3): 112 at 4 warps
+constexpr int kMW = (kBW + 15 + 31) / 32 * 32;  // u8 mask box width (start floored to 16 B): 128 at 4 warps
+constexpr int kF = m4::kBR * kBW * 8;
+constexpr int kUt = m4::kBR * kMW;
 static_assert(kF % 128 == 0 && kUt % 128 == 0, "TMA destinations stay 128-byte aligned");
 enum Mode : int { GP = 0, CG = 1, PROJ = 2 };
 }  // namespace m5
@@ -823,7 +828,7 @@ __device__ __forceinline__ int accept_sweep5(const StencilOp& A, const BandGeom&
 }
 
 template <bool SB, bool BB, int MODE>
-__global__ void __launch_bounds__(m4::kThreads, 4)
+__global__ void __launch_bounds__(m4::kThreads, m4::kMinB)
 k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
@@ -943,7 +948,7 @@ __device__ __forceinline__ int search_sweep5(const StencilOp& A, const BandGeom&
 }
 
 template <bool SB, bool BB, int MODE, int K>
-__global__ void __launch_bounds__(m4::kThreads, (K <= 2 ? 4 : 2))
+__global__ void __launch_bounds__(m4::kThreads, (K <= 2 ? m4::kMinB : (m4::kMinB > 1 ? m4::kMinB / 2 : 1)))
 k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, int h0, double mu,
@@ -980,7 +985,7 @@ struct CgInitLayout5 {
 };
 
 template <bool BB, bool PC>
-__global__ void __launch_bounds__(m4::kThreads, 4)
+__global__ void __launch_bounds__(m4::kThreads, m4::kMinB)
 k5_cg_init(StencilOp A, BandGeom G, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
            const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_mask,
            unsigned char* __restrict__ mask_cg, double* __restrict__ rho, double* __restrict__ p,
@@ -1176,7 +1181,7 @@ __device__ __forceinline__ void grid_sum(double (&acc)[NS], double* part, unsign
 }
 
 template <bool SB, bool BB>
-__global__ void __launch_bounds__(m4::kThreads, 4)
+__global__ void __launch_bounds__(m4::kThreads, m4::kMinB)
 k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __restrict__ brow,
            const __grid_constant__ CUtensorMap m_y0, const __grid_constant__ CUtensorMap m_y1,
            const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_l,
