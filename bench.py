@@ -236,7 +236,7 @@ def run_ours(args):
     clocks.start()
     tot_ms = 0.0
     agg = {"cg_iters": 0, "gp_iters": 0, "outer_iters": 0, "kernel_launches": 0, "cg_iters_timed": 0,
-           "cg_free_iters_timed": 0, "t_cg_timed_ms": 0.0, "t_cg_ms": 0.0}
+           "cg_free_iters_timed": 0, "t_cg_timed_ms": 0.0, "t_cg_ms": 0.0, "t_gp_ms": 0.0}
     last = None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(args.steps):
@@ -329,6 +329,22 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e_val = e2e_hvps / e2e_s
 
+    # the other persistent loop (k6_gp_loop: about half of the device time): one GP
+    # step = one speculative accept sweep over the grid; its kernel bytes are 18 B per point
+    # (y, mask read; y, mask written; b row-broadcast, bounds scalar, g recomputed), but the sweep
+    # applies the operator four times per point and is instruction-issue bound
+    gp_roof = None
+    if agg["gp_iters"] and prob.kind == "stencil2d":
+        gp_step_s = (agg["t_gp_ms"] / 1e3) / agg["gp_iters"]
+        gp_bytes = 18.0 * prob.n / world
+        gp_roof = {"bound": "hbm", "kernel": "k6_gp_loop (persistent GP phase; speculative accept sweep per step)",
+                   "achieved": gp_bytes / gp_step_s / 1e9, "peak": peak, "unit": "GB/s",
+                   "frac": gp_bytes / gp_step_s / 1e9 / peak, "traffic": None,
+                   "bytes_per_launch": gp_bytes, "us_per_launch": gp_step_s * 1e6,
+                   "launch": "one GP step (sweep + grid reduction + stop tests), CUDA events around each GP phase",
+                   "note": "issue-bound, not byte-bound: ~250 thread instructions per grid point per step "
+                           "(4 stencil applications) at ~56 % issue efficiency (profiles/r1g_ncu_full_k6_C2.txt)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         it, secs, stc = oracle_sample(prob, args.cpu_budget)
@@ -367,13 +383,16 @@ def run_ours(args):
                          "note": ("traffic = ncu DRAM bytes per CG iteration (profiles/traffic_<config>.json): at C2 the "
                                   "CG working set (~105 MB) stays in the 126 MB L2 between iterations, so the sweep is "
                                   "issue/L2-bound and 'achieved' counts the bytes the kernel must touch, mostly L2 hits; "
-                                  "the HBM-bound regime is C3 (DESIGN.md 9)"),
+                                  "the HBM-bound regime is C3 (DESIGN.md 9). The CG and GP persistent loops each take "
+                                  "about half of the device time (profiles/r1j_launches_bench_C2_summary.txt); the GP "
+                                  "loop is in roofline_gp"),
                          "algorithmic_bytes": f"{cg_min_bytes_per_free_point(prob):.0f} B per free point + 1 B mask "
                                               f"per point (DESIGN.md 6: the kernel's three-vector recurrence)",
                          "survey_8d_80B": {"bytes_per_launch": bytes_per_launch, "achieved": achieved,
                                            "frac": (achieved / peak) if achieved else None,
                                            "what": f"{bpp:.0f} B per free point + 1 B mask per point (SURVEY.md "
                                                    f"8(d) fused C-G CG iteration, 5 vectors)"}},
+            "roofline_gp": gp_roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT,
                     "h2d_bytes_per_step": h2d,
