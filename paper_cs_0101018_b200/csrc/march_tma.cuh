@@ -352,10 +352,16 @@ __global__ void k_cg_block_flags(int nx, int pitch, BandGeom G, const unsigned c
         const int x0 = (t % G.nbands) * kOut;
         const int yr = (t / G.nbands) * G.seg - 2 + b * kBR;
         int fd = 0, fw = 0;
-        for (int r = max(yr - 2, G.rlo); r < min(yr + kBR, rhi); ++r) {
+        // all the block's mask bytes are independent loads: unrolled so they are in flight together
+#pragma unroll
+        for (int rr = 0; rr < kBR + 2; ++rr) {
+            const int r = yr - 2 + rr;
+            if (r < G.rlo || r >= rhi) continue;
             const unsigned char* row = mask + (long long)r * pitch;
-            for (int c = x0 - 2 + lane; c < x0 + kOut + 2; c += 32) {
-                if (c < 0 || c >= nx || !row[c]) continue;
+#pragma unroll
+            for (int cc = 0; cc < (kOut + 4 + 31) / 32; ++cc) {
+                const int c = x0 - 2 + lane + 32 * cc;
+                if (c >= x0 + kOut + 2 || c < 0 || c >= nx || !row[c]) continue;
                 if (r >= yr) fd = 1;
                 if (r < yr + kBR - 2 && c >= x0 && c < x0 + kOut) fw = 1;
             }
