@@ -578,6 +578,8 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k3_search<true, false>, SrchStage<true, false>::kSmem));
     RC(set_smem(k3_search<false, true>, SrchStage<false, true>::kSmem));
     RC(set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem));
+    RC(set_smem(k4_hessvec<true>, m4hv::kSmem));
+    RC(set_smem(k4_hessvec<false>, m4hv::kSmem));
     RC(set_smem(k4_cg_iter<false>, m4cg::kSmem));
     RC(set_smem(k4_cg_iter<true>, m4cg::kSmem));
     RC(set_smem(k6_cg_loop<false>, m4cg::kSmem));
@@ -2278,10 +2280,6 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
             CUtensorMap mv;
             if (vin == S.v[VIN]) mv = S.t4[VIN];
             else RC(make_map(h, S, &mv, vin, false, m4::kBW, m4::kBR));
-            if (m4hv::kSmem > 48 * 1024) {               // wide bands (GPCG_M4_WARPS = 8)
-                RC(set_smem(k4_hessvec<true>, m4hv::kSmem));
-                RC(set_smem(k4_hessvec<false>, m4hv::kSmem));
-            }
             if (reduced)
                 k4_hessvec<true><<<S.grid4_cg, m4::kThreadsWS, m4hv::kSmem, h->st>>>(S.sop, S.bg_cg, mv,
                                                                                      S.t4m[h->free_mask], yout);
