@@ -20,6 +20,12 @@
  * fusion, no reordering.  Build with -O2 -ffp-contract=off so that every
  * a*b+c rounds twice, as written.
  *
+ * OpenMP build ("the OpenMP build of the same source, all host cores"):
+ * compiled with -fopenmp, the row loops of the SpMVs and the elementwise vector loops
+ * (no reductions) are split over threads; every sum (dot products, norms, counts) stays a
+ * single left-to-right loop, so both builds return bitwise-identical results.  Without
+ * -fopenmp the pragmas are ignored and the file is the plain single-threaded oracle.
+ *
  * Pins (tests/test_oracle_*.py): dense brute-force products, the eps=0
  * Laplacian eigenpairs, 3^n active-set enumeration, Cholesky solves with
  * infinite bounds, KKT certificates, SPEC.md hand values, the paper's free
@@ -46,7 +52,7 @@ typedef struct {
     double eta2;          /* Eq. cgstop1, P:790 eta2 = 0.05                                       */
     double eta2_shrink;   /* Eq. cgstop3 "reduce eta2" P:491: x0.1 (R12)                          */
     double eta2_floor;    /* 1e-12 (R12)                                                          */
-    int64_t gp_cap;       /* GP iterates per phase, 100 (R13)                                     */
+    int64_t gp_cap;       /* GP iterates per phase: safety net only, 100000 (R13; the paper has none) */
     int64_t refine_cap;   /* cgstop3 repetitions per outer iterate, 30 (R12)                      */
     int64_t max_halvings; /* projected-search trials, 50 (R13)                                    */
     int64_t cg_cap;       /* 0 => m_k, the finite-termination bound P:444-447                     */
@@ -56,6 +62,8 @@ typedef struct {
                              2: block-Jacobi ILU(0) on tiles of a 2-D grid          */
     int64_t grid_nx, grid_ny;   /* precond 2: the 2-D grid (v = i + nx j)                          */
     int64_t tile_x, tile_y;     /* precond 2: block = tile_x x tile_y tile of the grid              */
+    double *trace;              /* nullable: per-step record of the control path (test pins only),  */
+    int64_t trace_cap;          /* trace_cap records of ORA_TREC doubles, see trace_put()           */
 } ora_params;
 
 typedef struct {
@@ -63,7 +71,28 @@ typedef struct {
     int64_t n_free, n_active, n_active_nonbinding;
     double pg_norm, q, g0_norm, tau, seconds;
     int64_t status;
+    int64_t trace_len;    /* records written to prm->trace (may exceed trace_cap: then truncated) */
 } ora_stats;
+
+/* Control-path trace (test infrastructure: lets the pins check the GP-phase stop rules and
+ * the eta2 refinement step by step).  One record = ORA_TREC doubles
+ *   {kind, k, i1, i2, v1, v2}
+ *   kind 1  GP step        i1 = j (1-based),   i2 = h (accepted halving), v1 = q(y_{j-1}) - q(y_j), v2 = alpha
+ *   kind 2  GP phase end   i1 = j_k (steps),   i2 = reason: 0 converged, 1 Eq. pgstop1, 2 Eq. pgstop2,
+ *                                                           3 gp_cap,   v1 = max decrease, v2 = alpha_0 of step 1
+ *   kind 3  CG call        i1 = rep,           i2 = iterations,          v1 = eta2 used, v2 = m_k = |F|
+ *   kind 4  CG search      i1 = rep,           i2 = h,                   v1 = q(x_k) - q(x_{k+1}),
+ *                                                                        v2 = |A(x_{k+1}) \ B(x_{k+1})|     */
+#define ORA_TREC 6
+static void trace_put(const ora_params *prm, ora_stats *st, int kind, int64_t k, int64_t i1, int64_t i2,
+                      double v1, double v2)
+{
+    if (prm->trace && st->trace_len < prm->trace_cap) {
+        double *r = prm->trace + ORA_TREC * st->trace_len;
+        r[0] = kind; r[1] = (double)k; r[2] = (double)i1; r[3] = (double)i2; r[4] = v1; r[5] = v2;
+    }
+    st->trace_len++;
+}
 
 /* ------------------------------------------------------------------------ */
 /* operator                                                                  */
@@ -157,6 +186,7 @@ int ora_stencil3d_to_csr(int64_t nx, int64_t ny, int64_t nz, const double *wx, c
 void ora_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
               const double *x, double *y)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) {
         double s = 0.0;
         for (int64_t k = rp[i]; k < rp[i + 1]; k++) s += val[k] * x[ci[k]];
@@ -170,6 +200,7 @@ void ora_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *val
 void ora_spmv_masked(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
                      const unsigned char *free_, const double *x, double *y)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) {
         double s = 0.0;
         if (free_[i]) {
@@ -274,6 +305,7 @@ static void gradient(int64_t n, const int64_t *rp, const int32_t *ci, const doub
                      const double *b, const double *x, double *g)
 {
     ora_spmv(n, rp, ci, val, x, g);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) g[i] = g[i] - b[i];
 }
 
@@ -315,6 +347,7 @@ int64_t ora_projected_search(int64_t n, const int64_t *rp, const int32_t *ci, co
     double *s = work, *As = work + n;
     for (int64_t h = 0; h < max_halvings; h++) {
         double alpha = ldexp(alpha_base, (int)-h);
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) {
             ynew[i] = mid(l[i], u[i], y[i] + alpha * dir[i]);
             s[i] = ynew[i] - y[i];
@@ -400,9 +433,11 @@ int64_t ora_pcg_m(int64_t n, const int64_t *rp, const int32_t *ci, const double 
         double pAp = dot(n, p, a);
         if (!(pAp > 0.0)) return ORA_ENOTSPD;
         double alpha = rr / pAp;
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) w[i] = w[i] + alpha * p[i];
         double dec = 0.5 * alpha * rr;
         if (decs) decs[it - 1] = dec;
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) rho[i] = rho[i] - alpha * a[i];
         if (pc) prec_apply(M, n, rp, ci, val, free_, rho, z);
         double rr_new = dot(n, rho, z);
@@ -412,6 +447,7 @@ int64_t ora_pcg_m(int64_t n, const int64_t *rp, const int32_t *ci, const double 
         if (dec > maxdec) maxdec = dec;
         if (stop) break;
         double beta = rr_new / rr;
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
         rr = rr_new;
     }
@@ -522,10 +558,11 @@ void ora_jacobi_inverse(int64_t n, const int64_t *rp, const int32_t *ci, const d
 void ora_params_default(ora_params *p)
 {
     p->mu = 0.1; p->eta1 = 0.1; p->eta2 = 0.05; p->eta2_shrink = 0.1; p->eta2_floor = 1e-12;
-    p->gp_cap = 100; p->refine_cap = 30; p->max_halvings = 50; p->cg_cap = 0;
+    p->gp_cap = 100000; p->refine_cap = 30; p->max_halvings = 50; p->cg_cap = 0;
     p->time_budget_s = 0.0;
     p->precond = 0;
     p->grid_nx = 0; p->grid_ny = 0; p->tile_x = 32; p->tile_y = 32;
+    p->trace = NULL; p->trace_cap = 0;
 }
 
 /* Solve min q(x) s.t. l <= x <= u.  tol > 0: absolute tau on ||grad_Omega q||_2
@@ -574,10 +611,13 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
         st->outer_iters = k + 1;
         /* ---- gradient projection phase : y_0 = x_k ---------- */
         int64_t j = 0;
-        double maxdec = 0.0;
+        double maxdec = 0.0, alpha_first = 0.0;
         for (;;) {
             /* g = A y_j - b holds here */
-            if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
+            if (pgnorm(n, x, g, l, u) <= tau) {
+                trace_put(prm, st, 2, k, j, 0, maxdec, alpha_first);
+                status = ORA_OK; goto done;
+            }
             int cs;
             double alpha0 = ora_cauchy_alpha(n, rp, ci, val, x, g, l, u, work, &cs);
             st->full_spmvs++;
@@ -602,11 +642,13 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
             st->gp_iters++;
             gradient(n, rp, ci, val, b, x, g); st->full_spmvs++;
             double dec = -delta;                            /* q(y_{j-1}) - q(y_j) */
-            int stop = same ||                               /* Eq. pgstop1 */
-                       (j >= 2 && dec <= prm->eta1 * maxdec) ||  /* Eq. pgstop2 (R10) */
-                       (j >= prm->gp_cap);
+            if (j == 1) alpha_first = alpha0;
+            trace_put(prm, st, 1, k, j, h, dec, alpha);
+            int reason = same ? 1 :                                      /* Eq. pgstop1 */
+                         (j >= 2 && dec <= prm->eta1 * maxdec) ? 2 :     /* Eq. pgstop2 (R10) */
+                         (j >= prm->gp_cap) ? 3 : 0;                     /* safety net (R13) */
             if (dec > maxdec) maxdec = dec;
-            if (stop) break;
+            if (reason) { trace_put(prm, st, 2, k, j, reason, maxdec, alpha_first); break; }
         }
         /* x_k = y_{j_k}; convergence test (R13) */
         if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
@@ -624,6 +666,7 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
             st->cg_calls++;
             if (its < 0) { status = (int)its; goto done; }
             st->cg_iters += its;
+            trace_put(prm, st, 3, k, rep, its, eta2, (double)m);
             /* d_k = Z_k w_{j_k} is w itself (zero off F) */
             double delta, alpha;
             int64_t h = ora_projected_search(n, rp, ci, val, x, g, w, l, u, 1.0, prm->mu,
@@ -632,11 +675,12 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
             st->full_spmvs += h + 1;
             memcpy(x, y, (size_t)n * sizeof(double));
             gradient(n, rp, ci, val, b, x, g); st->full_spmvs++;
-            if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
             /* Eq. cgstop3: B(x_{k+1}) = A(x_{k+1}) -> reduce eta2, continue CG */
             int64_t nonbinding = 0;
             for (int64_t i = 0; i < n; i++)
                 if (is_active(x[i], l[i], u[i]) && !is_binding(x[i], g[i], l[i], u[i])) nonbinding++;
+            trace_put(prm, st, 4, k, rep, h, -delta, (double)nonbinding);
+            if (pgnorm(n, x, g, l, u) <= tau) { status = ORA_OK; goto done; }
             if (nonbinding != 0) break;
             eta2 = eta2 * prm->eta2_shrink;
             if (eta2 < prm->eta2_floor) eta2 = prm->eta2_floor;

@@ -17,19 +17,23 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "gpcg_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
+LIB_OMP = os.path.join(HERE, "liboracle_omp.so")
 
 OK, NOT_CONVERGED, EINVAL, ENOMEM, ENOTSPD, ESEARCH = 0, 1, -1, -2, -5, -6
 
 
-def build(force: bool = False) -> str:
-    """Compile liboracle.so (gcc -O2 -ffp-contract=off; no OpenMP, single thread)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        tmp = LIB + f".tmp{os.getpid()}"
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile liboracle.so (gcc -O2 -ffp-contract=off; single thread) or, omp=True,
+    liboracle_omp.so: the same source with -fopenmp (row / elementwise loops threaded, every
+    sum serial: bitwise-identical results; SURVEY.md 8(d)'s all-core baseline)."""
+    out = LIB_OMP if omp else LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(SRC):
+        tmp = out + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c99",
-                               "-D_POSIX_C_SOURCE=199309L", "-fPIC", "-shared",
-                               "-o", tmp, SRC, "-lm"])
-        os.replace(tmp, LIB)
-    return LIB
+                               "-D_POSIX_C_SOURCE=199309L", "-fPIC", "-shared"] +
+                              (["-fopenmp"] if omp else []) + ["-o", tmp, SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
 
 
 class Params(C.Structure):
@@ -38,7 +42,8 @@ class Params(C.Structure):
                 ("gp_cap", C.c_int64), ("refine_cap", C.c_int64),
                 ("max_halvings", C.c_int64), ("cg_cap", C.c_int64),
                 ("time_budget_s", C.c_double), ("precond", C.c_int64),
-                ("grid_nx", C.c_int64), ("grid_ny", C.c_int64), ("tile_x", C.c_int64), ("tile_y", C.c_int64)]
+                ("grid_nx", C.c_int64), ("grid_ny", C.c_int64), ("tile_x", C.c_int64), ("tile_y", C.c_int64),
+                ("trace", C.c_void_p), ("trace_cap", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -46,19 +51,39 @@ class Stats(C.Structure):
                 ("cg_calls", C.c_int64), ("refinements", C.c_int64), ("full_spmvs", C.c_int64),
                 ("n_free", C.c_int64), ("n_active", C.c_int64), ("n_active_nonbinding", C.c_int64),
                 ("pg_norm", C.c_double), ("q", C.c_double), ("g0_norm", C.c_double),
-                ("tau", C.c_double), ("seconds", C.c_double), ("status", C.c_int64)]
+                ("tau", C.c_double), ("seconds", C.c_double), ("status", C.c_int64),
+                ("trace_len", C.c_int64)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+TREC = 6   # doubles per control-path trace record (ORA_TREC in gpcg_oracle.c)
+
+
 _lib = None
+_lib_omp = None
 
 
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(build())
+        # ORACLE_LIB: load another build of the same source (mutation testing of the pins,
+        # scripts/oracle_mutants.py); default: the in-tree build
+        _lib = _bind(C.CDLL(os.environ.get("ORACLE_LIB") or build()))
+    return _lib
+
+
+def lib_omp():
+    """The OpenMP build (all host cores unless OMP_NUM_THREADS says otherwise)."""
+    global _lib_omp
+    if _lib_omp is None:
+        _lib_omp = _bind(C.CDLL(build(omp=True)))
+    return _lib_omp
+
+
+def _bind(L):
+    if True:
         P = C.c_void_p
         i64 = C.c_int64
         L.ora_stencil2d_nnz.restype = i64
@@ -103,8 +128,7 @@ def lib():
         L.ora_gpcg_solve.restype = C.c_int
         L.ora_gpcg_solve.argtypes = [i64, P, P, P, P, P, P, C.c_double, P, C.c_double, i64,
                                      P, P, P]
-        _lib = L
-    return _lib
+    return L
 
 
 def _p(a):
@@ -240,8 +264,9 @@ def projected_search(A: CSR, y, g, direction, l, u, alpha_base, mu=0.1, max_halv
     return h, ynew, delta.value, alpha.value
 
 
-def cg(A: CSR, free, r, eta2, cap=0):
-    """Textbook CG on A_F w = -r.  -> (iterations or error code, w, decreases)."""
+def cg(A: CSR, free, r, eta2, cap=0, omp=False):
+    """Textbook CG on A_F w = -r.  -> (iterations or error code, w, decreases).
+    omp: run the OpenMP build (same results bitwise)."""
     fr = np.ascontiguousarray(free, dtype=np.uint8)
     r = _f64(r)
     m = int(fr.sum())
@@ -249,7 +274,7 @@ def cg(A: CSR, free, r, eta2, cap=0):
     w = np.empty(A.n)
     work = np.empty(4 * A.n)
     decs = np.zeros(max(cap, 1))
-    it = lib().ora_cg(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), eta2, cap,
+    it = (lib_omp() if omp else lib()).ora_cg(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), eta2, cap,
                       _p(w), _p(work), _p(decs), 0.0)
     return it, w, decs[:max(it, 0)]
 
@@ -331,3 +356,20 @@ def solve_problem(prob, tol=None, max_it=500, params: Params = None):
     A = problem_csr(prob)
     return solve(A, prob.b, prob.l, prob.u, prob.c, prob.x0,
                  prob.tol if tol is None else tol, max_it, params)
+
+
+def solve_trace(A: CSR, b, l, u, c, x0, tol, max_it=500, params: Params = None, cap=200000):
+    """Algorithm GPCG with the control-path trace (see gpcg_oracle.c, trace_put).
+    -> (status, x, stats dict, trace as an (records, 6) array)."""
+    params = params or default_params()
+    buf = np.zeros(cap * TREC)
+    params.trace = buf.ctypes.data
+    params.trace_cap = cap
+    try:
+        rc, x, st = solve(A, b, l, u, c, x0, tol, max_it, params)
+    finally:
+        params.trace = None
+        params.trace_cap = 0
+    if st["trace_len"] > cap:
+        raise RuntimeError("oracle trace truncated")
+    return rc, x, st, buf[: st["trace_len"] * TREC].reshape(-1, TREC).copy()
