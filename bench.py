@@ -3,20 +3,29 @@
 
 A "step" is one full GPCG solve (Algorithm GPCG: every row of
 SURVEY.md 8(a) -- GP sweeps a1/a2/a3, CG a4/a5, reductions a6, control a7) of
-the configured workload from x0 to tol, inputs resident in HBM.
+the configured workload from x0 to tol, inputs resident in HBM.  Default
+workload: C3 (BASELINE.json configs[3], 8000^2 = 64M variables, the north_star's
+strong-scaling grid; its working set is far larger than the 126 MB L2, so the
+sweeps are measured in the HBM regime).  --config C2 runs the paper-size grid.
 
   value   = reduced Hessian-vector products per second over the K timed solves
-            (one per CG iteration: the masked SpMV A_F rho inside k_cg_iter),
+            (one per CG iteration: the masked SpMV A_F rho of the CG sweep),
             aggregated over ranks; solve seconds are reported beside it.
   e2e     = the same metric through the C ABI with HOST (pinned) buffers:
             create (H2D of operator, b, l, u) + solve (H2D x0, D2H x) + destroy.
-  roofline: dominant kernel k_cg_iter; algorithmic bytes per launch
-            (80 + coef) B per free point + 1 B mask per point, over
-            its CUDA-event-timed steady-state launch duration.
-  cpu_baseline / --impl reference: the plain-C oracle (oracle/) on the same
-            workload, bounded by a time budget, on the host cores (1 thread).
+  roofline: the persistent loop with the larger device time (CG or GP), its
+            algorithmic bytes per launch (the bytes THIS kernel's
+            algorithm must move -- CG: 48 B per free point + 1 B mask per point;
+            GP: the speculative sweep's bytes per point, + search and accept
+            sweeps for rejected steps) over its CUDA-event-timed duration; SURVEY
+            8(d)'s count and the ncu DRAM bytes (profiles/traffic_<config>.json)
+            beside it.
+  cpu_baseline / --impl reference: the plain-C oracle (oracle/), unmodified, on
+            the same workload: reduced HVPs/s of its textbook CG (ora_cg, the
+            masked operator Z Z' A Z Z') for a fixed number of iterations -- the
+            same unit of work as `value`, independent of the solve's phase.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference] [--slabs S]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference] [--slabs S]
 N > 1 runs under torchrun (one process per GPU): the SAME problem split into N row
 slabs (gpcg_create_*_dist: NCCL halo exchange + one allreduce per CG iteration),
 i.e. strong scaling; see DESIGN.md "Multi-GPU".  --slabs S (N = 1) splits the
@@ -151,18 +160,45 @@ def dist_env():
     return rank, world, local
 
 
-def oracle_sample(prob, budget_s, A=None):
-    """Oracle GPCG on prob for at most budget_s seconds -> (cg_iters, seconds, stats).
-    A: the oracle's CSR of prob (built here when not given)."""
+def oracle_free_set(prob):
+    """The free set the oracle's CG rate is measured on: F = {l < P[x0] < u}, or every point if
+    that is empty (C2's x0 = 0 = l) -- the masked operator costs the same per row either way."""
+    x = np.minimum(np.maximum(prob.x0, prob.l), prob.u)
+    fr = ((x > prob.l) & (x < prob.u)).astype(np.uint8)
+    if not fr.any():
+        fr[:] = 1
+    return x, fr
+
+
+def oracle_cg_rate(prob, iters, A=None, omp=False):
+    """The oracle's reduced-HVP rate: `iters` iterations of its textbook CG (ora_cg, one masked
+    SpMV Z Z' A Z Z' p per iteration plus the vector updates) on A_F w = -g_F at P[x0], the
+    progress test switched off so every call does exactly `iters` iterations.
+    -> (iterations, seconds, threads)."""
     from oracle import oracle as O
     A = O.problem_csr(prob) if A is None else A
-    params = O.default_params(time_budget_s=float(budget_s))
-    rc, x, st = O.solve(A, prob.b, prob.l, prob.u, prob.c, prob.x0, prob.tol, 500, params)
-    return st["cg_iters"], st["seconds"], st
+    x, fr = oracle_free_set(prob)
+    g = O.gradient(A, prob.b, x)
+    t0 = time.perf_counter()
+    it, w, decs = O.cg(A, fr, g, 1e-300, cap=iters, omp=omp)
+    secs = time.perf_counter() - t0
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)) if omp else 1
+    return it, secs, threads
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
-    """--impl reference: the oracle (plain C, 1 thread) timed on the host, same workload/metric."""
+    """--impl reference: the oracle (plain C, 1 thread) timed on the host, same workload/metric:
+    each step = a fixed number of its CG iterations (reduced HVPs) on the workload."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
@@ -170,27 +206,28 @@ def run_reference(args):
     prob = P.get(args.config)
     from oracle import oracle as O
     A = O.problem_csr(prob)                      # assembled once (not part of a step)
+    # iterations per step: about min(6 s, 150 s / steps) of oracle work, so warm-up + timed steps
+    # stay within a few minutes
+    _, s1, _ = oracle_cg_rate(prob, 1, A)
     total = args.steps + args.warmup
-    budget = max(5.0, min(20.0, 150.0 / max(total, 1)))
+    iters = max(1, int(min(6.0, 150.0 / max(total, 1)) / max(s1, 1e-6)))
     for _ in range(args.warmup):
-        oracle_sample(prob, budget, A)
-    iters, secs = 0, 0.0
-    last = None
+        oracle_cg_rate(prob, iters, A)
+    its, secs = 0, 0.0
     for _ in range(args.steps):
-        it, s, st = oracle_sample(prob, budget, A)
-        iters += it
-        secs += s
-        last = st
-    value = iters / secs if secs > 0 else 0.0
+        it, sec, _ = oracle_cg_rate(prob, iters, A)
+        its += it
+        secs += sec
+    value = its / secs if secs > 0 else 0.0
+    sample = (f"each step: {iters} iterations of the oracle's textbook CG (ora_cg: masked SpMV + vector "
+              f"updates) on A_F w = -g_F of {args.config} at P[x0] (F = {int(oracle_free_set(prob)[1].sum())} "
+              f"points), progress test off; 1 thread, {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "n": prob.n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"each step: the first {budget:.0f} s of the {args.config} GPCG solve "
-                                   f"(oracle stops at the time budget; last step: {last['outer_iters']} outer, "
-                                   f"{last['gp_iters']} GP, {last['cg_iters']} CG iterations)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -205,17 +242,22 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def fresh_nccl_id():
+        """A new ncclUniqueId for every communicator this process creates (an id's bootstrap root
+        serves one ncclCommInitRank round): rank 0 draws it, torch.distributed broadcasts it."""
+        if world == 1:
+            return None
         obj = [gpcg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
     dev = torch.device("cuda", local)
     prob = P.get(args.config)
     stream = torch.cuda.current_stream()
     if world > 1 or args.slabs > 1:
-        solver, rb, re, loc = gpcg.Solver.dist(prob, rank, world, nccl_id, local_slabs=args.slabs,
+        solver, rb, re, loc = gpcg.Solver.dist(prob, rank, world, fresh_nccl_id(), local_slabs=args.slabs,
                                                stream=stream, device=dev)
         x0_host = loc["x0"]
     else:
@@ -236,7 +278,8 @@ def run_ours(args):
     clocks.start()
     tot_ms = 0.0
     agg = {"cg_iters": 0, "gp_iters": 0, "outer_iters": 0, "kernel_launches": 0, "cg_iters_timed": 0,
-           "cg_free_iters_timed": 0, "t_cg_timed_ms": 0.0, "t_cg_ms": 0.0, "t_gp_ms": 0.0}
+           "cg_free_iters_timed": 0, "t_cg_timed_ms": 0.0, "t_cg_ms": 0.0, "t_gp_ms": 0.0,
+           "gp_spec_rejected": 0}
     last = None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(args.steps):
@@ -275,15 +318,20 @@ def run_ours(args):
     launch_s = (agg["t_cg_timed_ms"] / 1e3) / it_t
     achieved = bytes_per_launch / launch_s / 1e9 if agg["cg_iters_timed"] else None
     achieved_min = min_bytes_per_launch / launch_s / 1e9 if agg["cg_iters_timed"] else None
-    traffic = None
+    # ncu DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per CG iteration / per GP step
+    # on this config, from one `ncu --set full` capture (profiles/traffic_<config>.json)
+    traffic = {}
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tr_path):
-        traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+        tj = json.load(open(tr_path))
+        traffic = {"cg": tj.get("cg", {}).get("dram_bytes_per_launch", tj.get("dram_bytes_per_launch")),
+                   "gp": tj.get("gp", {}).get("dram_bytes_per_launch")}
 
     # e2e: through the C ABI with host (pinned) buffers, H2D/D2H inside the timed region
     def pinned(a):
         return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-    e2e_steps = max(1, min(args.steps, 3))
+    # e2e steps: 3, or 1 when a solve takes seconds (C3) so that the default run stays minutes long
+    e2e_steps = max(1, min(args.steps, 3 if tot_ms / args.steps < 3000.0 else 1))
     if loc is None:
         hp = P.Problem(**{**prob.__dict__})
         for k in ("b", "l", "u", "x0", "wx", "wy", "shift", "row_ptr", "col", "val"):
@@ -296,12 +344,11 @@ def run_ours(args):
         hp = P.Problem(**{**prob.__dict__})
         lp = {k: (pinned(v) if isinstance(v, np.ndarray) else v) for k, v in loc.items()}
         xh = torch.empty(loc["n"], dtype=torch.float64).pin_memory()
-        make = lambda: gpcg.Solver.dist(prob, rank, world, nccl_id, local_slabs=args.slabs,   # noqa: E731
+        make = lambda: gpcg.Solver.dist(prob, rank, world, fresh_nccl_id(), local_slabs=args.slabs,  # noqa: E731
                                         stream=stream, local=lp)[0]
         h2d = int(sum(v.numel() * v.element_size() for v in lp.values() if hasattr(v, "numel")))
     x0h = pinned(np.ascontiguousarray(x0_host))
-    s_e2e = make()                                               # warm-up of the e2e path
-    s_e2e.solve(x0h, prob.tol, x_out=xh)
+    s_e2e = make()                                # warm-up of the e2e path (memory pool, module state)
     s_e2e.close()
     e2e_s, e2e_hvps = 0.0, 0
     t_parts = {"create_s": 0.0, "solve_s": 0.0, "destroy_s": 0.0}
@@ -329,29 +376,60 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e_val = e2e_hvps / e2e_s
 
-    # the other persistent loop (k6_gp_loop: about half of the device time): one GP
-    # step = one speculative accept sweep over the grid; its kernel bytes are 18 B per point
-    # (y, mask read; y, mask written; b row-broadcast, bounds scalar, g recomputed), but the sweep
-    # applies the operator four times per point and is instruction-issue bound
+    # the GP phase: one GP step = one speculative accept sweep at alpha_0 (k6_gp_loop, 2-D broadcast
+    # faces, one slab) whose bytes per point are those the sweep must move: y and the
+    # previous mask read, y and the mask written (18 B) + l, u unless both are constants (16 B) + b
+    # unless every grid row holds the same b (8 B); g is recomputed, never stored.  A step whose
+    # speculative sweep was rejected (stats gp_spec_rejected) also ran a search sweep (y [+ l, u]
+    # [+ b]) and an accept sweep (the speculative sweep's bytes).
     gp_roof = None
     if agg["gp_iters"] and prob.kind == "stencil2d":
+        sb = bool(np.all(prob.l == prob.l[0]) and np.all(prob.u == prob.u[0]))
+        bb = bool(np.all(prob.b.reshape(prob.ny, prob.nx) == prob.b[: prob.nx][None, :]))
+        spec_b = 18.0 + (0.0 if sb else 16.0) + (0.0 if bb else 8.0)
+        srch_b = 8.0 + (0.0 if sb else 16.0) + (0.0 if bb else 8.0)
+        persist = (world * args.slabs == 1 and not prob.wx_ld and not prob.wy_ld and prob.shift is None
+                   and os.environ.get("GPCG_GP_PERSIST", "1") != "0")
+        rej = agg["gp_spec_rejected"]
         gp_step_s = (agg["t_gp_ms"] / 1e3) / agg["gp_iters"]
-        gp_bytes = 18.0 * prob.n / world
-        gp_roof = {"bound": "hbm", "kernel": "k6_gp_loop (persistent GP phase; speculative accept sweep per step)",
-                   "achieved": gp_bytes / gp_step_s / 1e9, "peak": peak, "unit": "GB/s",
-                   "frac": gp_bytes / gp_step_s / 1e9 / peak, "traffic": None,
+        gp_bytes = (spec_b * agg["gp_iters"] + (srch_b + spec_b) * rej) * prob.n / agg["gp_iters"] / world
+        ach = gp_bytes / gp_step_s / 1e9
+        gp_roof = {"bound": "hbm",
+                   "kernel": ("k6_gp_loop (persistent GP phase; speculative accept sweep per step)" if persist
+                              else "k5_search / k5_accept GP graph chunks"),
+                   "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                   "frac_of_8TBs": ach / 8000.0, "traffic": traffic.get("gp"), "peak_source": peak_src,
                    "bytes_per_launch": gp_bytes, "us_per_launch": gp_step_s * 1e6,
-                   "launch": "one GP step (sweep + grid reduction + stop tests), CUDA events around each GP phase",
-                   "note": "issue-bound, not byte-bound: ~250 thread instructions per grid point per step "
-                           "(4 stencil applications) at ~56 % issue efficiency (profiles/r1g_ncu_full_k6_C2.txt)"}
+                   "launch": "one GP step (sweep(s) + grid reduction + stop tests), CUDA events around each GP phase",
+                   "algorithmic_bytes": f"{spec_b:.0f} B per point per speculative sweep (sb={sb}, bb={bb}); "
+                                        f"+{srch_b + spec_b:.0f} B per point for each of {rej} rejected steps",
+                   "survey_8d": {"bytes_per_launch": (74.0 if sb else 122.0) * prob.n / world,
+                                 "frac": (74.0 if sb else 122.0) * prob.n / world / gp_step_s / 1e9 / peak,
+                                 "what": "SURVEY 8(d): 3 sweeps per GP sub-step (a2, a3, a1)"}}
+        if traffic.get("gp"):
+            gp_roof["dram_over_algorithmic"] = traffic["gp"] / gp_bytes
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        it, secs, stc = oracle_sample(prob, args.cpu_budget)
-        cpu = {"value": it / secs if secs > 0 else 0.0, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"first {args.cpu_budget:.0f} s of the {args.config} GPCG solve on 1 host core "
-                         f"({stc['outer_iters']} outer, {stc['gp_iters']} GP, {stc['cg_iters']} CG iterations "
-                         f"done; oracle stops at the time budget)"}
+        from oracle import oracle as O
+        A_o = O.problem_csr(prob)
+        _, s1, _ = oracle_cg_rate(prob, 1, A_o)
+        iters = max(2, int(args.cpu_budget / max(s1, 1e-6)))
+        it1, sec1, _ = oracle_cg_rate(prob, iters, A_o)
+        _, s1o, _ = oracle_cg_rate(prob, 1, A_o, omp=True)
+        iters_o = max(2, int(args.cpu_budget / max(s1o, 1e-6)))
+        ito, seco, thr = oracle_cg_rate(prob, iters_o, A_o, omp=True)
+        del A_o
+        nf = int(oracle_free_set(prob)[1].sum())
+        cpu = {"value": it1 / sec1, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{it1} iterations of the oracle's textbook CG (ora_cg: masked SpMV Z Z' A Z Z' p + "
+                         f"vector updates, progress test off) on A_F w = -g_F of {args.config} at P[x0] "
+                         f"(|F| = {nf}), 1 host thread; {cpu_model()}",
+               "openmp": {"value": ito / seco, "unit": UNIT, "cores": thr, "nproc": os.cpu_count(),
+                          "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+                          "sample": f"{ito} iterations, same call, liboracle_omp.so (the same source with "
+                                    f"-fopenmp: row and elementwise loops threaded, sums serial; bitwise-equal "
+                                    f"results)"}}
 
     if rank == 0:
         line = {
@@ -360,7 +438,8 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, paper_cs_0101018_b200/problems.py)",
             "config": {"workload": WORKLOADS[args.config], "n": prob.n,
-                       "l2": "flushed (256 MB write) between timed solves",
+                       "l2": "flushed (256 MB write) between timed solves; C3's vectors (512 MB each) exceed "
+                             "the 126 MB L2 anyway",
                        "parallelism": ("1 GPU, 1 slab" if world == 1 and args.slabs == 1 else
                                        f"{world} GPU(s) x {args.slabs} row slab(s) of one problem "
                                        f"(halo exchange + one allreduce per CG iteration)")},
@@ -377,21 +456,17 @@ def run_ours(args):
                          "achieved": achieved_min, "peak": peak, "unit": "GB/s",
                          "frac": (achieved_min / peak) if achieved_min else None,
                          "frac_of_8TBs": (achieved_min / 8000.0) if achieved_min else None,
-                         "traffic": traffic, "peak_source": peak_src,
+                         "traffic": traffic.get("cg"), "peak_source": peak_src,
                          "bytes_per_launch": min_bytes_per_launch, "us_per_launch": launch_s * 1e6,
+                         "dram_over_algorithmic": (traffic["cg"] / min_bytes_per_launch) if traffic.get("cg") else None,
                          "launch": "one CG iteration (reduced HVP + vector updates + reduction)",
-                         "note": ("traffic = ncu DRAM bytes per CG iteration (profiles/traffic_<config>.json): at C2 the "
-                                  "CG working set (~105 MB) stays in the 126 MB L2 between iterations, so the sweep is "
-                                  "issue/L2-bound and 'achieved' counts the bytes the kernel must touch, mostly L2 hits; "
-                                  "the HBM-bound regime is C3 (DESIGN.md 9). The CG and GP persistent loops each take "
-                                  "about half of the device time (profiles/r1j_launches_bench_C2_summary.txt); the GP "
-                                  "loop is in roofline_other"),
                          "algorithmic_bytes": f"{cg_min_bytes_per_free_point(prob):.0f} B per free point + 1 B mask "
                                               f"per point (DESIGN.md 6: the kernel's three-vector recurrence)",
-                         "survey_8d_80B": {"bytes_per_launch": bytes_per_launch, "achieved": achieved,
-                                           "frac": (achieved / peak) if achieved else None,
-                                           "what": f"{bpp:.0f} B per free point + 1 B mask per point (SURVEY.md "
-                                                   f"8(d) fused C-G CG iteration, 5 vectors)"}},
+                         "survey_8d": {"bytes_per_launch": bytes_per_launch, "achieved": achieved,
+                                       "frac": (achieved / peak) if achieved else None,
+                                       "what": f"{bpp:.0f} B per free point + 1 B mask per point (SURVEY.md 8(d) "
+                                               f"fused C-G CG iteration, 5 vectors; this kernel recomputes A p and "
+                                               f"A rho from neighbours instead of streaming them)"}},
             "roofline_gp": gp_roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT,
@@ -427,7 +502,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -74,7 +74,7 @@ typedef struct {
     double eta2;         /* Eq. cgstop1: 0.05                                              */
     double eta2_shrink;  /* Eq. cgstop3 refinement factor: 0.1                             */
     double eta2_floor;   /* 1e-12                                                          */
-    int64_t gp_cap;      /* GP iterates per phase: 100                                     */
+    int64_t gp_cap;      /* GP iterates per phase: 100000, a safety net (the paper has none)*/
     int64_t refine_cap;  /* cgstop3 repetitions per outer iterate: 30                      */
     int64_t max_halvings;/* projected-search trials: 50                                    */
     int64_t cg_cap;      /* CG iterations per call, 0 => m_k (finite termination P:444-447)*/
@@ -84,7 +84,10 @@ typedef struct {
     int32_t precond;     /* 0: plain CG on A_k (the hot path); 1: point-Jacobi PCG with
                             M = diag(A_k) (Table 4 "Diagonal"); 2: block-
                             Jacobi ILU(0) on 32 x 32 tiles of each slab (
-                            2-D stencils only, textbook PCG, two sweeps per iteration)     */
+                            2-D stencils only, textbook PCG, two sweeps per iteration);
+                            3: block-Jacobi ILU(2) on the same tiles (the
+                            subdomain solver of the paper's Tables 1-3, "two levels of
+                            fill"; 2-D stencils only)                                      */
     int32_t cg_mode;     /* 0: A_k applied in place on masked full-length vectors (the hot
                             path, P:680-683's "alternative technique"); 1: A_k extracted
                             as a compact CSR matrix each CG call, as the paper does with
@@ -114,6 +117,10 @@ typedef struct {
     int64_t cg_iters_timed, cg_free_iters_timed;
     double t_cg_timed_ms;
     double t_extract_ms;   /* cg_mode = 1: device time spent building A_F and r_F          */
+    /* GP phase sweeps (2-D persistent GP loop): gp_spec_rejected = GP steps whose speculative
+     * accept sweep at alpha_0 was rejected by Eq. gplsstop (each then ran a search sweep and
+     * an accept sweep as well); 0 on the other paths. */
+    int64_t gp_spec_rejected;
 } gpcg_stats;
 
 GPCG_API gpcg_params gpcg_params_default(void);

@@ -59,11 +59,13 @@ typedef struct {
     double time_budget_s; /* 0 => none; else stop (NOT_CONVERGED) once exceeded (bounded samples) */
     int64_t precond;      /* 0: plain CG (the hot path); 1: point-Jacobi PCG, M = diag(A_k)
                              (the "diagonal Jacobi preconditioner" of P:1096-1098, Table 4);
-                             2: block-Jacobi ILU(0) on tiles of a 2-D grid          */
+                             2: block-Jacobi ILU(0) on tiles of a 2-D grid;
+                             3: block-Jacobi ILU(ilu_level) on the same tiles       */
     int64_t grid_nx, grid_ny;   /* precond 2: the 2-D grid (v = i + nx j)                          */
     int64_t tile_x, tile_y;     /* precond 2: block = tile_x x tile_y tile of the grid              */
     double *trace;              /* nullable: per-step record of the control path (test pins only),  */
     int64_t trace_cap;          /* trace_cap records of ORA_TREC doubles, see trace_put()           */
+    int64_t ilu_level;          /* precond 3: block-Jacobi ILU(ilu_level), 2 = the paper's ILU(2)   */
 } ora_params;
 
 typedef struct {
@@ -389,13 +391,31 @@ void ora_bjilu_apply(int64_t n, const int64_t *rp, const int32_t *ci, const doub
                      const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, const double *d,
                      const double *r, double *t, double *z);
 
-/* preconditioner of ora_pcg_m: kind 0 none, 1 point Jacobi (dinv), 2 block-Jacobi ILU(0)
- * (grid nx, tiles tx x ty; pivots factored at the start of every CG call on its free set) */
+/* block-Jacobi ILU(k) factor (kind 3, below): rows of L (unit, strictly lower) and U (upper,
+ * with the diagonal) of every block, in natural order; row v holds ent[beg[v] .. beg[v+1]) */
+typedef struct {
+    int64_t n, cap, used;
+    int64_t *beg;               /* n + 1 */
+    int64_t *col;
+    int64_t *lev;
+    double *val;                /* L entries (col < v): l_vc;  U entries (col >= v): u_vc */
+} ora_iluk;
+
+int ora_bjiluk_factor(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                      const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, int64_t level, ora_iluk *F);
+void ora_bjiluk_apply(const ora_iluk *F, const unsigned char *free_, const double *r, double *t, double *z);
+void ora_iluk_free(ora_iluk *F);
+
+/* preconditioner of ora_pcg_m: kind 0 none, 1 point Jacobi (dinv), 2 block-Jacobi ILU(0),
+ * 3 block-Jacobi ILU(level) (grid nx, tiles tx x ty; factored at the start of every CG call
+ * on its free set) */
 typedef struct {
     int kind;
     const double *dinv;
     int64_t nx, tx, ty;
-    double *d, *t;              /* kind 2: pivots and forward-solve scratch (n each) */
+    double *d, *t;              /* kind 2: pivots and forward-solve scratch (n each); kind 3: t only */
+    int64_t level;              /* kind 3 */
+    ora_iluk *F;                /* kind 3 */
 } ora_prec;
 
 static void prec_apply(const ora_prec *M, int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
@@ -403,6 +423,8 @@ static void prec_apply(const ora_prec *M, int64_t n, const int64_t *rp, const in
 {
     if (M->kind == 1) {
         for (int64_t i = 0; i < n; i++) z[i] = free_[i] ? r[i] * M->dinv[i] : 0.0;
+    } else if (M->kind == 3) {
+        ora_bjiluk_apply(M->F, free_, r, M->t, z);
     } else {
         ora_bjilu_apply(n, rp, ci, val, free_, M->nx, M->tx, M->ty, M->d, r, M->t, z);
     }
@@ -416,6 +438,9 @@ int64_t ora_pcg_m(int64_t n, const int64_t *rp, const int32_t *ci, const double 
     double *rho = work, *p = work + n, *a = work + 2 * n;
     double *z = pc ? work + 3 * n : rho;
     if (M && M->kind == 2) ora_bjilu_factor(n, rp, ci, val, free_, M->nx, M->tx, M->ty, M->d);
+    if (M && M->kind == 3 &&
+        ora_bjiluk_factor(n, rp, ci, val, free_, M->nx, M->tx, M->ty, M->level, M->F) != ORA_OK)
+        return ORA_ENOMEM;
     for (int64_t i = 0; i < n; i++) {
         rho[i] = free_[i] ? -r[i] : 0.0;
         w[i] = 0.0;
@@ -459,7 +484,7 @@ int64_t ora_pcg(int64_t n, const int64_t *rp, const int32_t *ci, const double *v
                 const unsigned char *free_, const double *r, const double *dinv, double eta2, int64_t cap,
                 double *w, double *work, double *decs, double deadline)
 {
-    ora_prec M = {dinv ? 1 : 0, dinv, 0, 0, 0, NULL, NULL};
+    ora_prec M = {dinv ? 1 : 0, dinv, 0, 0, 0, NULL, NULL, 0, NULL};
     return ora_pcg_m(n, rp, ci, val, free_, r, &M, eta2, cap, w, work, decs, deadline);
 }
 
@@ -468,8 +493,22 @@ int64_t ora_pcg_bjilu(int64_t n, const int64_t *rp, const int32_t *ci, const dou
                       const unsigned char *free_, const double *r, int64_t nx, int64_t tx, int64_t ty,
                       double eta2, int64_t cap, double *w, double *work, double *scratch, double *decs)
 {
-    ora_prec M = {2, NULL, nx, tx, ty, scratch, scratch + n};
+    ora_prec M = {2, NULL, nx, tx, ty, scratch, scratch + n, 0, NULL};
     return ora_pcg_m(n, rp, ci, val, free_, r, &M, eta2, cap, w, work, decs, 0.0);
+}
+
+/* block-Jacobi ILU(level) form (tiles tx x ty of an nx-wide grid); work: 4n, scratch: n */
+int64_t ora_pcg_bjiluk(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                       const unsigned char *free_, const double *r, int64_t nx, int64_t tx, int64_t ty,
+                       int64_t level, double eta2, int64_t cap, double *w, double *work, double *scratch,
+                       double *decs)
+{
+    ora_iluk F;
+    memset(&F, 0, sizeof F);
+    ora_prec M = {3, NULL, nx, tx, ty, NULL, scratch, level, &F};
+    int64_t it = ora_pcg_m(n, rp, ci, val, free_, r, &M, eta2, cap, w, work, decs, 0.0);
+    ora_iluk_free(&F);
+    return it;
 }
 
 /* plain CG (the hot path's CG): ora_pcg without a preconditioner */
@@ -540,6 +579,167 @@ void ora_bjilu_apply(int64_t n, const int64_t *rp, const int32_t *ci, const doub
     }
 }
 
+/* ------------------------------------------------------------------------ */
+/* block-Jacobi ILU(k) ("ILU(2), which allowed two levels of fill")  */
+/* ------------------------------------------------------------------------ */
+/* ILU(p) with levels of fill, row by row in the IKJ form (the textbook ILU(p) algorithm):
+ * on each block (tile) of A_k = Z'AZ in natural order, row v starts as the free, same-tile
+ * entries of A, all of level 0; then for every k < v of the row with lev(v,k) <= p, in
+ * increasing k:   l_vk = a_vk / u_kk;   a_vj -= l_vk u_kj  for every j > k of U's row k,
+ * lev(v,j) = min(lev(v,j), lev(v,k) + lev(k,j) + 1)   (a new position starts at that
+ * level); finally the positions with lev(v,j) > p are dropped.  M = L U, L unit lower.
+ * ILU(0) keeps A's pattern (= ora_bjilu_* above); p large enough gives the complete LU
+ * factorisation of every block. */
+static int iluk_reserve(ora_iluk *F, int64_t need)
+{
+    if (F->used + need <= F->cap) return ORA_OK;
+    int64_t c = F->cap ? F->cap : 1024;
+    while (c < F->used + need) c *= 2;
+    int64_t *col = (int64_t *)realloc(F->col, (size_t)c * sizeof(int64_t));
+    if (!col) return ORA_ENOMEM;
+    F->col = col;
+    int64_t *lev = (int64_t *)realloc(F->lev, (size_t)c * sizeof(int64_t));
+    if (!lev) return ORA_ENOMEM;
+    F->lev = lev;
+    double *v = (double *)realloc(F->val, (size_t)c * sizeof(double));
+    if (!v) return ORA_ENOMEM;
+    F->val = v;
+    F->cap = c;
+    return ORA_OK;
+}
+
+void ora_iluk_free(ora_iluk *F)
+{
+    free(F->beg); free(F->col); free(F->lev); free(F->val);
+    memset(F, 0, sizeof *F);
+}
+
+int ora_bjiluk_factor(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                      const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, int64_t level, ora_iluk *F)
+{
+    if (F->n != n) {
+        free(F->beg);
+        F->beg = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
+        if (!F->beg) return ORA_ENOMEM;
+        F->n = n;
+    }
+    F->used = 0;
+    /* the working row: positions (col, lev, val) in insertion order, scanned linearly */
+    int64_t wcap = 64, wn;
+    for (int64_t v = 0; v < n; v++)
+        if (4 * (rp[v + 1] - rp[v]) > wcap) wcap = 4 * (rp[v + 1] - rp[v]);
+    int64_t *wc = (int64_t *)malloc((size_t)wcap * sizeof(int64_t));
+    int64_t *wl = (int64_t *)malloc((size_t)wcap * sizeof(int64_t));
+    double *wv = (double *)malloc((size_t)wcap * sizeof(double));
+    unsigned char *wd = (unsigned char *)malloc((size_t)wcap);
+    if (!wc || !wl || !wv || !wd) { free(wc); free(wl); free(wv); free(wd); return ORA_ENOMEM; }
+    for (int64_t v = 0; v < n; v++) {
+        F->beg[v] = F->used;
+        if (!free_[v]) continue;
+        wn = 0;
+        for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
+            int64_t u = ci[k];
+            if (!free_[u] || !same_tile(u, v, nx, tx, ty)) continue;
+            int64_t f = -1;
+            for (int64_t q = 0; q < wn; q++) if (wc[q] == u) { f = q; break; }
+            if (f >= 0) { wv[f] += val[k]; continue; }
+            wc[wn] = u; wl[wn] = 0; wv[wn] = val[k]; wd[wn] = 0; wn++;   /* wcap >= 4 x row length */
+        }
+        for (;;) {
+            /* the smallest not yet eliminated k < v with lev(v,k) <= level */
+            int64_t qk = -1;
+            for (int64_t q = 0; q < wn; q++)
+                if (wc[q] < v && !wd[q] && wl[q] <= level && (qk < 0 || wc[q] < wc[qk])) qk = q;
+            if (qk < 0) break;
+            wd[qk] = 1;
+            int64_t k = wc[qk];
+            double ukk = 0.0;
+            for (int64_t e = F->beg[k]; e < F->beg[k + 1]; e++) if (F->col[e] == k) ukk = F->val[e];
+            double lvk = wv[qk] / ukk;
+            wv[qk] = lvk;
+            for (int64_t e = F->beg[k]; e < F->beg[k + 1]; e++) {
+                int64_t j = F->col[e];
+                if (j <= k) continue;                       /* U's row k: j > k */
+                int64_t nl = wl[qk] + F->lev[e] + 1;
+                int64_t f = -1;
+                for (int64_t q = 0; q < wn; q++) if (wc[q] == j) { f = q; break; }
+                if (f < 0) {
+                    if (wn == wcap) {
+                        wcap *= 2;
+                        int64_t *a = (int64_t *)realloc(wc, (size_t)wcap * sizeof(int64_t)); if (a) wc = a;
+                        int64_t *b = (int64_t *)realloc(wl, (size_t)wcap * sizeof(int64_t)); if (b) wl = b;
+                        double *c = (double *)realloc(wv, (size_t)wcap * sizeof(double)); if (c) wv = c;
+                        unsigned char *d = (unsigned char *)realloc(wd, (size_t)wcap); if (d) wd = d;
+                        if (!a || !b || !c || !d) { free(wc); free(wl); free(wv); free(wd); return ORA_ENOMEM; }
+                    }
+                    f = wn++;
+                    wc[f] = j; wl[f] = nl; wv[f] = 0.0; wd[f] = 0;
+                }
+                wv[f] = wv[f] - lvk * F->val[e];
+                if (nl < wl[f]) wl[f] = nl;
+            }
+        }
+        /* keep the positions of level <= p, in increasing column order */
+        int64_t keep = 0;
+        for (int64_t q = 0; q < wn; q++) keep += wl[q] <= level;
+        if (iluk_reserve(F, keep) != ORA_OK) { free(wc); free(wl); free(wv); free(wd); return ORA_ENOMEM; }
+        int64_t last = -1;
+        for (int64_t m = 0; m < keep; m++) {
+            int64_t qb = -1;
+            for (int64_t q = 0; q < wn; q++)
+                if (wl[q] <= level && wc[q] > last && (qb < 0 || wc[q] < wc[qb])) qb = q;
+            F->col[F->used] = wc[qb]; F->lev[F->used] = wl[qb]; F->val[F->used] = wv[qb];
+            F->used++;
+            last = wc[qb];
+        }
+    }
+    F->beg[n] = F->used;
+    free(wc); free(wl); free(wv); free(wd);
+    return ORA_OK;
+}
+
+/* z = M^-1 r = U^-1 L^-1 r on the free set (forward L t = r, L unit; backward U z = t) */
+void ora_bjiluk_apply(const ora_iluk *F, const unsigned char *free_, const double *r, double *t, double *z)
+{
+    int64_t n = F->n;
+    for (int64_t v = 0; v < n; v++) {
+        if (!free_[v]) { t[v] = 0.0; continue; }
+        double s = r[v];
+        for (int64_t e = F->beg[v]; e < F->beg[v + 1]; e++)
+            if (F->col[e] < v) s = s - F->val[e] * t[F->col[e]];
+        t[v] = s;
+    }
+    for (int64_t v = n - 1; v >= 0; v--) {
+        if (!free_[v]) { z[v] = 0.0; continue; }
+        double s = t[v], d = 0.0;
+        for (int64_t e = F->beg[v]; e < F->beg[v + 1]; e++) {
+            if (F->col[e] > v) s = s - F->val[e] * z[F->col[e]];
+            else if (F->col[e] == v) d = F->val[e];
+        }
+        z[v] = s / d;
+    }
+}
+
+/* The factor of ora_bjiluk_factor as dense-able triplets (tests): L and U entries with their
+ * levels.  Returns the entry count; with out arrays NULL only counts. */
+int64_t ora_bjiluk_export(int64_t n, const int64_t *rp, const int32_t *ci, const double *val,
+                          const unsigned char *free_, int64_t nx, int64_t tx, int64_t ty, int64_t level,
+                          int64_t *rows, int64_t *cols, int64_t *levs, double *vals, int64_t cap)
+{
+    ora_iluk F;
+    memset(&F, 0, sizeof F);
+    if (ora_bjiluk_factor(n, rp, ci, val, free_, nx, tx, ty, level, &F) != ORA_OK) return -1;
+    int64_t m = F.used;
+    if (rows && m <= cap) {
+        for (int64_t v = 0; v < n; v++)
+            for (int64_t e = F.beg[v]; e < F.beg[v + 1]; e++) {
+                rows[e] = v; cols[e] = F.col[e]; levs[e] = F.lev[e]; vals[e] = F.val[e];
+            }
+    }
+    ora_iluk_free(&F);
+    return m;
+}
+
 /* dinv_i = 1 / A_ii (the point-Jacobi preconditioner; A SPD => A_ii > 0) */
 void ora_jacobi_inverse(int64_t n, const int64_t *rp, const int32_t *ci, const double *val, double *dinv)
 {
@@ -563,6 +763,7 @@ void ora_params_default(ora_params *p)
     p->precond = 0;
     p->grid_nx = 0; p->grid_ny = 0; p->tile_x = 32; p->tile_y = 32;
     p->trace = NULL; p->trace_cap = 0;
+    p->ilu_level = 2;
 }
 
 /* Solve min q(x) s.t. l <= x <= u.  tol > 0: absolute tau on ||grad_Omega q||_2
@@ -584,15 +785,17 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
     double *w = (double *)malloc((size_t)n * sizeof(double));
     double *work = (double *)malloc((size_t)4 * n * sizeof(double));
     double *dinv = prm->precond == 1 ? (double *)malloc((size_t)n * sizeof(double)) : NULL;
-    double *ilu = prm->precond == 2 ? (double *)malloc((size_t)2 * n * sizeof(double)) : NULL;
-    if (prm->precond == 2 && (prm->grid_nx <= 0 || prm->grid_nx * prm->grid_ny != n || prm->tile_x <= 0 ||
+    double *ilu = prm->precond >= 2 ? (double *)malloc((size_t)2 * n * sizeof(double)) : NULL;
+    ora_iluk iluk;
+    memset(&iluk, 0, sizeof iluk);
+    if (prm->precond >= 2 && (prm->grid_nx <= 0 || prm->grid_nx * prm->grid_ny != n || prm->tile_x <= 0 ||
                               prm->tile_y <= 0)) {
         free(dinv); free(ilu);
         st->status = ORA_EINVAL; return ORA_EINVAL;
     }
     unsigned char *act = (unsigned char *)malloc((size_t)n);
     unsigned char *fr = (unsigned char *)malloc((size_t)n);
-    if (!g || !y || !w || !work || !act || !fr || (prm->precond == 1 && !dinv) || (prm->precond == 2 && !ilu)) {
+    if (!g || !y || !w || !work || !act || !fr || (prm->precond == 1 && !dinv) || (prm->precond >= 2 && !ilu)) {
         free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv); free(ilu);
         st->status = ORA_ENOMEM; return ORA_ENOMEM;
     }
@@ -660,7 +863,8 @@ int ora_gpcg_solve(int64_t n, const int64_t *rp, const int32_t *ci, const double
             for (int64_t i = 0; i < n; i++) { fr[i] = !is_active(x[i], l[i], u[i]); m += fr[i]; }
             if (m == 0) break;              /* reading R26: next GP phase frees variables */
             int64_t cap = prm->cg_cap > 0 ? prm->cg_cap : m;
-            ora_prec M = {(int)prm->precond, dinv, prm->grid_nx, prm->tile_x, prm->tile_y, ilu, ilu ? ilu + n : NULL};
+            ora_prec M = {(int)prm->precond, dinv, prm->grid_nx, prm->tile_x, prm->tile_y, ilu, ilu ? ilu + n : NULL,
+                          prm->ilu_level, &iluk};
             int64_t its = ora_pcg_m(n, rp, ci, val, fr, g, &M, eta2, cap, w, work, NULL,
                                     prm->time_budget_s > 0.0 ? t0 + prm->time_budget_s : 0.0);
             st->cg_calls++;
@@ -703,5 +907,6 @@ done:
         st->seconds = now_s() - t0;
     }
     free(g); free(y); free(w); free(work); free(act); free(fr); free(dinv); free(ilu);
+    ora_iluk_free(&iluk);
     return status;
 }

@@ -43,7 +43,7 @@ class Params(C.Structure):
                 ("max_halvings", C.c_int64), ("cg_cap", C.c_int64),
                 ("time_budget_s", C.c_double), ("precond", C.c_int64),
                 ("grid_nx", C.c_int64), ("grid_ny", C.c_int64), ("tile_x", C.c_int64), ("tile_y", C.c_int64),
-                ("trace", C.c_void_p), ("trace_cap", C.c_int64)]
+                ("trace", C.c_void_p), ("trace_cap", C.c_int64), ("ilu_level", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -117,6 +117,10 @@ def _bind(L):
         L.ora_pcg.argtypes = [i64, P, P, P, P, P, P, C.c_double, i64, P, P, P, C.c_double]
         L.ora_pcg_bjilu.restype = i64
         L.ora_pcg_bjilu.argtypes = [i64, P, P, P, P, P, i64, i64, i64, C.c_double, i64, P, P, P, P]
+        L.ora_pcg_bjiluk.restype = i64
+        L.ora_pcg_bjiluk.argtypes = [i64, P, P, P, P, P, i64, i64, i64, i64, C.c_double, i64, P, P, P, P]
+        L.ora_bjiluk_export.restype = i64
+        L.ora_bjiluk_export.argtypes = [i64, P, P, P, P, i64, i64, i64, i64, P, P, P, P, i64]
         L.ora_bjilu_factor.restype = None
         L.ora_bjilu_factor.argtypes = [i64, P, P, P, P, i64, i64, i64, P]
         L.ora_bjilu_apply.restype = None
@@ -315,6 +319,35 @@ def pcg_bjilu(A: CSR, free, r, nx, tx, ty, eta2, cap=0):
     decs = np.zeros(max(cap, 1))
     it = lib().ora_pcg_bjilu(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), nx, tx, ty, eta2, cap,
                              _p(w), _p(work), _p(scratch), _p(decs))
+    return it, w, decs[:max(it, 0)]
+
+
+def bjiluk_factor(A: CSR, free, nx, tx, ty, level):
+    """Block-Jacobi ILU(level) factor (oracle routine) -> (rows, cols, levels, values): the L
+    (col < row, unit diagonal implied) and U (col >= row) entries of every tile."""
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    L = lib()
+    m = L.ora_bjiluk_export(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), nx, tx, ty, level,
+                            None, None, None, None, 0)
+    rows = np.empty(m, np.int64); cols = np.empty(m, np.int64); levs = np.empty(m, np.int64)
+    vals = np.empty(m)
+    L.ora_bjiluk_export(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), nx, tx, ty, level,
+                        _p(rows), _p(cols), _p(levs), _p(vals), m)
+    return rows, cols, levs, vals
+
+
+def pcg_bjiluk(A: CSR, free, r, nx, tx, ty, level, eta2, cap=0):
+    """Block-Jacobi ILU(level) PCG on A_F w = -r. -> (iterations, w, decreases)."""
+    fr = np.ascontiguousarray(free, dtype=np.uint8)
+    r = _f64(r)
+    m = int(fr.sum())
+    cap = cap if cap > 0 else m
+    w = np.empty(A.n)
+    work = np.empty(4 * A.n)
+    scratch = np.empty(A.n)
+    decs = np.zeros(max(cap, 1))
+    it = lib().ora_pcg_bjiluk(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(fr), _p(r), nx, tx, ty, level, eta2, cap,
+                              _p(w), _p(work), _p(scratch), _p(decs))
     return it, w, decs[:max(it, 0)]
 
 

@@ -45,6 +45,7 @@
 #include "march_tma.cuh"
 #include "extract.cuh"
 #include "bjilu.cuh"
+#include "bjilu2.cuh"
 #include "march3.cuh"
 
 #include <cudaTypedefs.h>
@@ -202,7 +203,8 @@ struct Slab {
     double* xval = nullptr;
     double* xv[12] = {};                      // gF, dinvF, rho x2, q x2, s x2, p, w, (spare)
     unsigned char *xmask = nullptr, *xmaskcg = nullptr;
-    double* bjf = nullptr;                    // block-Jacobi ILU(0) factor (precond = 2): 3 x tiles x 32^2
+    double* bjf = nullptr;                    // block-Jacobi ILU factor (precond 2 / 3): 5 x tiles x 32^2 doubles
+                                              // + tiles x 32^2 code bytes
     CUtensorMap tbr;                          // r (RHO0) in 32 x 32 boxes for the BJ-ILU tile solves
     int grid4_cg = 1, grid4_acc = 1, grid4_srch = 1;
     // g-free sweeps (k5_*): 112-column boxes from x0 - 4, 128-byte mask boxes, 104-column bands
@@ -257,8 +259,8 @@ struct gpcg_problem {
     cudaGraphExec_t cg_exec = nullptr;
     int cg_exec_chunk = 0;
     cudaGraphExec_t gp_exec[2] = {nullptr, nullptr};   // GP chunk graphs starting from buffers 0 / 1
-    cudaGraphExec_t bj_exec = nullptr;  // block-Jacobi ILU PCG chunk graph (precond = 2)
-    int bj_exec_chunk = 0;
+    cudaGraphExec_t bj_exec = nullptr;  // block-Jacobi ILU PCG chunk graph (precond = 2 / 3)
+    int bj_exec_chunk = 0, bj_exec_pc = 0;
     int gp_exec_chunk = 0;
     bool gp_graph = true;           // GPCG_GP_GRAPH=0: host-driven GP steps (A/B)
     bool cg_persistent = true;      // GPCG_CG_PERSIST=0: CG as graph chunks instead of k6_cg_loop
@@ -1441,8 +1443,14 @@ int bj_grid_mv(const gpcg_problem* h, const Slab& S) {
 // broadcast faces: dinv + code bytes (the cs / cw arrays unused); else dinv, cs, cw
 BjFactor bj_factor(const gpcg_problem* h, const Slab& S, long long nt) {
     const long long e = nt * kTile * kTile;
-    unsigned char* code = h->bc ? reinterpret_cast<unsigned char*>(S.bjf + 3 * e) : nullptr;
+    unsigned char* code = h->bc ? reinterpret_cast<unsigned char*>(S.bjf + 5 * e) : nullptr;
     return BjFactor{S.bjf, S.bjf + e, S.bjf + 2 * e, code};
+}
+
+// ILU(2): l_S, l_SE, l_SEE, l_W, 1/d in the same storage
+Bj2Factor bj2_factor(const Slab& S, long long nt) {
+    const long long e = nt * kTile * kTile;
+    return Bj2Factor{S.bjf, S.bjf + e, S.bjf + 2 * e, S.bjf + 3 * e, S.bjf + 4 * e};
 }
 
 int enqueue_bj_iter(gpcg_problem* h, int a) {
@@ -1462,7 +1470,11 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
     RC(exchange(h, {vq(bb)}));
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
-        if (h->bc)
+        if (h->prm.precond == 3)
+            k_pcg3_solve<1><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj2_factor(S, bj_tiles(h, S)), S.tbr,
+                                                                                 S.glo, S.v[VRHO0], S.v[VS0], S.v[VRHO1],
+                                                                                 0.0, 0, h->dS, h->red(s));
+        else if (h->bc)
             k_pcg2_solve<1, true><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(h, S, bj_tiles(h, S)), S.tbr,
                                                                               S.glo, S.v[VRHO0], S.v[VS0], S.v[VRHO1],
                                                                               0.0, 0, h->dS, h->red(s));
@@ -1478,8 +1490,12 @@ int enqueue_bj_iter(gpcg_problem* h, int a) {
 
 int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
     if (h->is_csr || h->is3d)
-        return set_err(GPCG_EINVAL, "precond = 2 (block-Jacobi ILU(0)) is implemented for 2-D stencils");
+        return set_err(GPCG_EINVAL, "precond = 2 / 3 (block-Jacobi ILU(0) / ILU(2)) is implemented for 2-D stencils");
+    const bool ilu2 = h->prm.precond == 3;
     RC(set_smem(k_bjilu_factor, kFactorSmem));
+    RC(set_smem(k_bjilu2_factor, kBj2FactorSmem));
+    RC(set_smem(k_pcg3_solve<0>, kSolveSmem));
+    RC(set_smem(k_pcg3_solve<1>, kSolveSmem));
     RC(set_smem(k_pcg2_solve<0, false>, kSolveSmem));
     RC(set_smem(k_pcg2_solve<1, false>, kSolveSmem));
     RC(set_smem(k_pcg2_solve<0, true>, kSolveSmem));
@@ -1488,12 +1504,21 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
         Slab& S = h->slabs[s];
         const long long nt = bj_tiles(h, S);
         if (!S.bjf) {
-            CK(dalloc(h, &S.bjf, (size_t)3 * nt * kTile * kTile * sizeof(double) + (size_t)nt * kTile * kTile));
+            CK(dalloc(h, &S.bjf, (size_t)5 * nt * kTile * kTile * sizeof(double) + (size_t)nt * kTile * kTile));
             RC(make_map(h, S, &S.tbr, S.v[VRHO0], false, kTile, kTile));
         }
         k_pcg2_init<<<S.grid, kThreads, 0, h->st>>>(S.sop, S.v[vy(cur)], S.v[VB], S.m[cur], S.m[MKCG], S.v[VRHO0],
                                                     S.v[VQ0], S.v[VQ1], S.v[VW]);
         CKLAUNCH();
+        if (ilu2) {
+            const int gw = (int)std::max<long long>(1, std::min<long long>((nt + kBj2FactorWarps - 1) / kBj2FactorWarps,
+                                                                           (long long)h->sms * 8));
+            k_bjilu2_factor<<<gw, 32 * kBj2FactorWarps, kBj2FactorSmem, h->st>>>(S.sop, S.m[MKCG], bj2_factor(S, nt));
+            CKLAUNCH();
+            k_pcg3_solve<0><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj2_factor(S, nt), S.tbr, S.glo,
+                                                                                 S.v[VRHO0], S.v[VS0], S.v[VRHO1], eta2,
+                                                                                 cap, h->dS, h->red(s));
+        } else {
         k_bjilu_factor<<<bj_grid_tiles(h, S), kBjThreads, kFactorSmem, h->st>>>(S.sop, S.m[MKCG], bj_factor(h, S, nt));
         CKLAUNCH();
         if (h->bc)
@@ -1504,6 +1529,7 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
             k_pcg2_solve<0, false><<<bj_grid_tiles(h, S), kBjThreads, kSolveSmem, h->st>>>(S.sop, bj_factor(h, S, nt), S.tbr, S.glo,
                                                                               S.v[VRHO0], S.v[VS0], S.v[VRHO1], eta2,
                                                                               cap, h->dS, h->red(s));
+        }
         CKLAUNCH();
         h->launches += 3;
     }
@@ -1513,7 +1539,7 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
     RC(finish_reduce(h, a, 1));
     RC(exchange(h, {VRHO1, VQ0, VQ1}, {MKCG}));
     const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
-    if (!h->bj_exec || h->bj_exec_chunk != chunk) {
+    if (!h->bj_exec || h->bj_exec_chunk != chunk || h->bj_exec_pc != h->prm.precond) {
         if (h->bj_exec) { cudaGraphExecDestroy(h->bj_exec); h->bj_exec = nullptr; }
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
@@ -1528,6 +1554,7 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
         cudaGraphDestroy(graph);
         if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
         h->bj_exec_chunk = chunk;
+        h->bj_exec_pc = h->prm.precond;
     }
     const int per_iter = 2 * h->nslabs() + (h->deferred ? 2 * (1 + (h->nslabs() > 1 ? 1 : 0)) : 0);
     for (;;) {
@@ -1559,7 +1586,7 @@ int run_cg_bjilu(gpcg_problem* h, int cur, long long m, double eta2, long long c
 
 // CG on the free set of M[cur].  On return W holds w_{j_k}.
 int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, long long* iters) {
-    if (h->prm.precond == 2) return run_cg_bjilu(h, cur, m, eta2, cap, iters);
+    if (h->prm.precond >= 2) return run_cg_bjilu(h, cur, m, eta2, cap, iters);
     // cg_mode 1: always extract; 2 (auto): extract for the generic kernels (CSR, 3-D) when the
     // free set is small (m < 0.3 n), where the compact system wins
     if (h->prm.cg_mode == 1 ||
@@ -2139,7 +2166,7 @@ gpcg_params gpcg_params_default(void) {
     p.eta2 = 0.05;
     p.eta2_shrink = 0.1;
     p.eta2_floor = 1e-12;
-    p.gp_cap = 100;
+    p.gp_cap = 100000;  // safety net only: the paper's GP phase has no cap (R13)
     p.refine_cap = 30;
     p.max_halvings = 50;
     p.cg_cap = 0;
@@ -2218,7 +2245,7 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
         return set_err(GPCG_EINVAL, "eta2_shrink in (0,1), eta2_floor > 0 required");
     if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 || p->cg_cap < 0 ||
         p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096 || p->gp_chunk < 1 ||
-        p->gp_chunk > 256 || p->precond < 0 || p->precond > 2 || (p->cg_mode < 0 || p->cg_mode > 2))
+        p->gp_chunk > 256 || p->precond < 0 || p->precond > 3 || (p->cg_mode < 0 || p->cg_mode > 2))
         return set_err(GPCG_EINVAL, "integer parameter out of range");
     const int old_chunk = h->prm.cg_chunk, old_pc = h->prm.precond;
     h->prm = *p;
@@ -2371,6 +2398,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                     }
                     if ((rc = sync_scal(h))) goto fail;
                     const long long jn = S.gp_j;
+                    if (persist) st.gp_spec_rejected += S.gp_fb;
                     cur = (int)((cur + (jn - jdone)) & 1);
                     st.gp_iters += jn - jdone;
                     st.full_spmvs += 3 * (jn - jdone);

@@ -44,7 +44,8 @@ class Stats(C.Structure):
                 ("t_total_ms", C.c_double), ("t_cg_ms", C.c_double), ("t_gp_ms", C.c_double),
                 ("status", C.c_int32), ("kernel_launches", C.c_int32),
                 ("cg_iters_timed", C.c_int64), ("cg_free_iters_timed", C.c_int64),
-                ("t_cg_timed_ms", C.c_double), ("t_extract_ms", C.c_double)]
+                ("t_cg_timed_ms", C.c_double), ("t_extract_ms", C.c_double),
+                ("gp_spec_rejected", C.c_int64)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -48,7 +48,7 @@ def test_params_default(lib):
     p = gpcg.default_params()
     # P:789-791 eta1 = 0.1, eta2 = 0.05; readings R6/R12/R13 for the rest
     assert (p.mu, p.eta1, p.eta2, p.eta2_shrink, p.eta2_floor) == (0.1, 0.1, 0.05, 0.1, 1e-12)
-    assert (p.gp_cap, p.refine_cap, p.max_halvings, p.cg_cap) == (100, 30, 50, 0)
+    assert (p.gp_cap, p.refine_cap, p.max_halvings, p.cg_cap) == (100000, 30, 50, 0)
 
 
 def test_no_cpu_fallback_without_device(lib):

@@ -31,6 +31,15 @@ def abs_op(A, p):
     return np.bincount(rows, weights=np.abs(A.val) * np.abs(p[A.ci]), minlength=A.n)
 
 
+def abs_op_rows(A, p, idx):
+    """|A| |p| on the rows idx only (sampled checks at full size)."""
+    out = np.zeros(len(idx))
+    for t, i in enumerate(idx):
+        k0, k1 = A.rp[i], A.rp[i + 1]
+        out[t] = np.sum(np.abs(A.val[k0:k1]) * np.abs(p[A.ci[k0:k1]]))
+    return out
+
+
 def spmv_close(y, yref, scale):
     d = np.abs(np.asarray(y) - yref)
     assert d.max() <= 1e-13 * max(scale.max(), 1e-300), (d.max(), scale.max())
@@ -324,11 +333,11 @@ GOLDEN = {
 
 @pytest.mark.parametrize("name", list(GOLDEN))
 def test_solve_parity_vs_oracle_golden(G, name):
+    import base64
     import json
     import os
+    import zlib
     path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_{name}.json")
-    if not os.path.exists(path):
-        pytest.skip(f"{path} not generated yet (python scripts/golden_oracle.py {name})")
     gold = json.load(open(path))
     prob = GOLDEN[name]()
     assert prob.n == gold["n"] and gold["rc"] == 0
@@ -339,14 +348,67 @@ def test_solve_parity_vs_oracle_golden(G, name):
     idx = np.asarray(gold["idx"])
     xo = np.asarray(gold["x"])
     assert np.max(np.abs(x[idx] - xo)) <= 1e-7, np.max(np.abs(x[idx] - xo))
-    # active sets: identical away from ties (the free copy within 1e-7 of the bound)
-    act = (x[idx] == prob.l[idx]) | (x[idx] == prob.u[idx])
-    acto = np.asarray(gold["active_sample"], dtype=bool)
-    for k in np.flatnonzero(act != acto):
-        i = idx[k]
-        free_val = x[i] if acto[k] else xo[k]
-        assert min(abs(free_val - prob.l[i]), abs(free_val - prob.u[i])) <= 1e-7, (i, x[i], xo[k])
-    assert abs(st["n_active"] - gold["n_active"]) <= gold["n_free_near_bound"] + 0.001 * prob.n
+    # active sets over ALL n points (the oracle's set is stored bit-packed): identical away from
+    # degenerate ties: a point active on one side only must be free on the other
+    # side within 1e-7 of the bound -- the GPU's x is at hand; the oracle's free points near a
+    # bound are stored with their x (near_idx / near_x)
+    acto = np.unpackbits(np.frombuffer(zlib.decompress(base64.b64decode(gold["active_packbits_zlib_b64"])),
+                                       dtype=np.uint8))[: prob.n].astype(bool)
+    assert int(acto.sum()) == gold["n_active"]
+    act = (x == prob.l) | (x == prob.u)
+    mism = np.flatnonzero(act != acto)
+    near = dict(zip(gold["near_idx"], gold["near_x"]))
+    nontie = []
+    for i in mism:
+        if acto[i]:      # oracle active, GPU free: the GPU's value must sit within 1e-7 of a bound
+            ok = min(abs(x[i] - prob.l[i]), abs(x[i] - prob.u[i])) <= 1e-7
+        else:            # GPU active, oracle free: the oracle's point must be a stored near-bound tie
+            ok = int(i) in near
+        if not ok:
+            nontie.append(int(i))
+    assert not nontie, (len(mism), nontie[:10])
+    ties = [int(i) for i in mism]
+    print(f"[parity] {name}: active-set mismatches {len(mism)} (all ties within 1e-7 of the bound); "
+          f"oracle near-bound free points {gold['n_free_near_bound']}; "
+          f"min |g_i| over the oracle's ties {min(gold['near_absg'], default=float('nan')):.3e}; "
+          f"tie indices {ties[:8]}")
+    assert st["n_active"] == int(act.sum())
+
+
+# ------------------------------------------------------------------ C3 at full size (BASELINE.json configs[3],
+# 8000^2 = 64M variables): no oracle solve fits a test run, so the GPU solution is certified by the
+# oracle's own code (SURVEY 8(c) "at full C3 size"): one CPU SpMV gives g, then the KKT conditions,
+# ||grad_Omega q|| <= tau (to 1 %) and B = A; plus the reduced HVP at 1e-13 on sampled rows.
+def test_c3_full_size_solve_certified_by_oracle(G, oracle):
+    import time
+    prob = P.c3()
+    assert prob.n == 64_000_000
+    t0 = time.perf_counter()
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(prob.x0, prob.tol)          # default parameters, tau = 1e-8 ||g(x0)||
+        t_solve = time.perf_counter() - t0
+        p = 2.0 * P.uniform(33, 1, prob.n) - 1.0
+        yr = s.hessvec(p, reduced=True)                 # on the solution's free set
+    assert rc == 0, (rc, st)
+    A = oracle.problem_csr(prob)
+    g = oracle.gradient(A, prob.b, x)
+    assert np.all(x >= prob.l) and np.all(x <= prob.u)
+    pg = np.linalg.norm(oracle.proj_grad(x, g, prob.l, prob.u))
+    assert pg <= 1.01 * st["tau"], (pg, st["tau"])
+    act, bnd, na, nb = oracle.sets(x, g, prob.l, prob.u)
+    assert na == nb, (na, nb)                            # B = A
+    assert na == st["n_active"]
+    assert 0.47 <= na / prob.n <= 0.53                   # calibrated ~50 % active (configs[3])
+    free = ~act
+    idx = np.unique((P.uniform(33, 2, 20000) * prob.n).astype(np.int64))
+    ysub = oracle.spmv_masked(A, free, p)
+    spmv_close(yr[idx], ysub[idx], abs_op_rows(A, p * free, idx))
+    # a-posteriori bound E = ||grad_Omega q|| / lambda_lb (SURVEY 8(c) parity protocol)
+    hx, hy = prob.meta["hx"], prob.meta["hy"]
+    lam = (0.9 ** 3) * ((hy / hx) * 4 * np.sin(np.pi / (2 * (prob.nx + 1))) ** 2 +
+                        (hx / hy) * 4 * np.sin(np.pi / (2 * (prob.ny + 1))) ** 2)
+    print(f"[C3] solve {t_solve:.1f} s outer={st['outer_iters']} gp={st['gp_iters']} cg={st['cg_iters']} "
+          f"|A|/n={na / prob.n:.4f} pg={pg:.3e} tau={st['tau']:.3e} E=pg/lambda_lb={pg / lam:.3e}")
 
 
 # ------------------------------------------------------------------ point-Jacobi PCG
@@ -670,6 +732,49 @@ def test_bjilu_first_outer_iteration_matches_oracle(G, oracle, case):
         s.set_params(precond=1, refine_cap=1)
         rc1, x1, st1 = s.solve(prob.x0, tol, max_it=1)
     assert st["cg_iters"] <= st1["cg_iters"]
+
+
+# ------------------------------------------------------------------ block-Jacobi ILU(2) PCG (NEXT-3, the paper's
+# subdomain solver)
+def _bj2_params(oracle, prob, **kw):
+    return oracle.default_params(precond=3, ilu_level=2, grid_nx=prob.nx, grid_ny=prob.ny, tile_x=32, tile_y=32,
+                                 **kw)
+
+
+@pytest.mark.parametrize("case", BJ_CASES)
+def test_solve_parity_bjilu2(G, oracle, case):
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, params=_bj2_params(oracle, prob))
+    assert rc_o == 0
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=3)
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0, (rc, st)
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
+    nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+    assert not nontie
+
+
+@pytest.mark.parametrize("case", ["C0", "ragged37x23", "jb80_eps0.9"])
+def test_bjilu2_first_outer_iteration_matches_oracle(G, oracle, case):
+    """One outer iteration (GP phase + one block-Jacobi ILU(2) PCG call + search): the same
+    algorithm on the same numbers as the oracle's generic ILU(k), equal to rounding; and no
+    more CG iterations than ILU(0) from the same point (Table 4)."""
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    prm = _bj2_params(oracle, prob, refine_cap=1)
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol, max_it=1, params=prm)
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=3, refine_cap=1)
+        rc, x, st = s.solve(prob.x0, tol, max_it=1)
+    assert st["gp_iters"] == st_o["gp_iters"] and st["cg_iters"] == st_o["cg_iters"], (st, st_o)
+    assert np.max(np.abs(x - x_o)) <= 1e-9 * max(np.max(np.abs(x_o)), 1e-300)
+    with G.Solver.from_problem(prob) as s:
+        s.set_params(precond=2, refine_cap=1)
+        rc0, x0, st0 = s.solve(prob.x0, tol, max_it=1)
+    assert st["cg_iters"] <= st0["cg_iters"]
 
 
 def test_bjilu_rejected_for_csr(G):
