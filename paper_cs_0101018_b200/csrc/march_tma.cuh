@@ -39,6 +39,12 @@ namespace gpcg {
 #ifndef GPCG_CG_MINB
 #define GPCG_CG_MINB (16 / GPCG_M4_WARPS)   // CG sweep CTAs per SM the register budget is sized for
 #endif
+#ifndef GPCG_GP_NST
+#define GPCG_GP_NST 4       // pipeline stages of the g-free GP sweeps (k5 / k6_gp_loop; tuning)
+#endif
+#ifndef GPCG_GP_MINB
+#define GPCG_GP_MINB (16 / GPCG_M4_WARPS)   // CTAs per SM the GP sweeps' register budget is sized for
+#endif
 namespace m4 {
 constexpr int kWarps = GPCG_M4_WARPS;     // consumer warps (one per 28 / 26-column strip)
 constexpr int kMinB = 16 / kWarps;        // CTAs per SM the register budgets are sized for (64 warps)
@@ -726,7 +732,7 @@ struct AccLayout5 {
     static constexpr int kU = kL + (SB ? 0 : m5::kF);
     static constexpr int kMP = kU + (SB ? 0 : m5::kF);
     static constexpr int kStage = kMP + m5::kUt;
-    static constexpr int kNST = 4;
+    static constexpr int kNST = GPCG_GP_NST;
     static constexpr int kSmem = kNST * kStage + 64;
     static constexpr int kLag = MODE == m5::GP ? 3 : 2;     // emitted row = raw row - kLag
 };
@@ -834,7 +840,7 @@ __device__ __forceinline__ int accept_sweep5(const StencilOp& A, const BandGeom&
 }
 
 template <bool SB, bool BB, int MODE>
-__global__ void __launch_bounds__(m4::kThreads, m4::kMinB)
+__global__ void __launch_bounds__(m4::kThreads, GPCG_GP_MINB)
 k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
@@ -863,7 +869,7 @@ struct SrchLayout5 {
     static constexpr int kL = kB + (BB ? 0 : m5::kF);
     static constexpr int kU = kL + (SB ? 0 : m5::kF);
     static constexpr int kStage = kU + (SB ? 0 : m5::kF);
-    static constexpr int kNST = 4;
+    static constexpr int kNST = GPCG_GP_NST;
     static constexpr int kSmem = kNST * kStage + 64;
 };
 
@@ -954,7 +960,7 @@ __device__ __forceinline__ int search_sweep5(const StencilOp& A, const BandGeom&
 }
 
 template <bool SB, bool BB, int MODE, int K>
-__global__ void __launch_bounds__(m4::kThreads, (K <= 2 ? m4::kMinB : (m4::kMinB > 1 ? m4::kMinB / 2 : 1)))
+__global__ void __launch_bounds__(m4::kThreads, (K <= 2 ? GPCG_GP_MINB : (m4::kMinB > 1 ? m4::kMinB / 2 : 1)))
 k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
           const __grid_constant__ CUtensorMap m_dir, const __grid_constant__ CUtensorMap m_b,
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, int h0, double mu,
@@ -1158,6 +1164,114 @@ __device__ __forceinline__ int spec_sweep5(const StencilOp& A, const BandGeom& G
         bars, k0);
 }
 
+// The speculative GP step with one operator application less and a 2-row lag (default;
+// GPCG_GP_SPEC6=0 selects spec_sweep5 above).  Same sums, evaluated as
+//   g(r-1)  = (A y)(r-1) - b,   yn(r-1) = P[y - alpha_0 g],   s(r-1) = yn - y
+//   As(r-2) = (A s)(r-2),       gn(r-2) = g(r-2) + As(r-2)       (A yn - b = A y - b + A s)
+//   d(r-2)  = grad_Omega q(yn)(r-2)
+//   <d, A d> as its face form  sum_faces w_f (d_a - d_b)^2  (+ w_f d^2 on boundary faces;
+//            A = sum_f w_f (e_a - e_b)(e_a - e_b)' + boundary terms, BASELINE configs[0]):
+//            each point adds its west and south faces, the last column / row its east /
+//            north boundary face, so only the west neighbour (shuffle) and the row below
+//            (register) are needed -- no A d, no third row of lag.
+// gn and <d, A d> differ from spec_sweep5's only in rounding (one add instead of a fresh
+// stencil application; a sum of squares instead of d'(A d)); the iterate yn is the same.
+template <bool SB, bool BB>
+__device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G, const Bounds& Bd,
+                                           const double* __restrict__ brow, const CUtensorMap* m_y,
+                                           const CUtensorMap* m_b, const CUtensorMap* m_l, const CUtensorMap* m_u,
+                                           const CUtensorMap* m_mp, double alpha, double* __restrict__ y_out,
+                                           unsigned char* __restrict__ mask_out, unsigned char* smem,
+                                           double (&acc)[8], uint64_t* bars, int k0) {
+    using namespace m4;
+    using L = AccLayout5<SB, BB, m5::GP>;
+    constexpr int LAG = 2;                        // emitted row = raw row - 2
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = 26 * wid + lane + 1;
+    const bool out_lane = lane >= 3 && lane < 29;
+    int gx = 0, moff = 0, y0 = 0, y1 = 0;
+    bool col_ok = false, east_bd = false;
+    Op5<true> op;
+    double bcol = 0.0;
+    double y_m1 = 0.0, y_m2 = 0.0, l_r1 = 0.0, u_r1 = 0.0, b_r1 = 0.0;   // raw rows r-1, r-2
+    double g_a = 0.0, yn_a = 0.0, l_a = 0.0, u_a = 0.0;                 // row r-2
+    double s_a = 0.0, s_b = 0.0;                                        // s(r-2), s(r-3)
+    double d_b = 0.0;                                                   // d(r-3)
+    const uint32_t tx = L::kMP + m5::kUt;
+    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+        G, A.ny, smem,
+        [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
+            mbar_expect_tx(bar, tx);
+            const int yt = yr - G.rlo;
+            tma_load_2d(st + L::kY, m_y, x0 - 4, yt, bar);
+            if (!BB) tma_load_2d(st + L::kB, m_b, x0 - 4, yt, bar);
+            if (!SB) {
+                tma_load_2d(st + L::kL, m_l, x0 - 4, yt, bar);
+                tma_load_2d(st + L::kU, m_u, x0 - 4, yt, bar);
+            }
+            tma_load_2d(st + L::kMP, m_mp, floor16(x0 - 4), yt - LAG, bar);
+        },
+        [&](int x0, int yb, int ye) {
+            gx = x0 - 3 + 26 * wid + lane;
+            moff = (x0 - 4) - floor16(x0 - 4);
+            y0 = yb;
+            y1 = ye;
+            col_ok = gx >= 0 && gx < A.nx;
+            east_bd = gx == A.nx - 1;
+            op.init(A, gx);
+            if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
+            y_m1 = y_m2 = l_r1 = u_r1 = b_r1 = g_a = yn_a = l_a = u_a = s_a = s_b = d_b = 0.0;
+        },
+        [&](const unsigned char* st, int kk, int r) {
+            const int q = kk * m5::kBW + c;
+            const bool rin = r >= A.rlo && r < A.rhi;
+            const bool in = col_ok && rin;
+            const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
+            const double bv = BB ? (rin ? bcol : 0.0) : reinterpret_cast<const double*>(st + L::kB)[q];
+            const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
+            const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
+            const double g1 = op.apply(A, r - 1, y_m1, y_m2, yv) - b_r1;     // g(r-1)
+            const double yn1 = trial(y_m1, g1, -1.0, alpha, l_r1, u_r1);     // yn(r-1)
+            const double s1 = yn1 - y_m1;                                     // s(r-1)
+            const double as2 = op.apply(A, r - 2, s_a, s_b, s1);              // (A s)(r-2)
+            const double gn2 = g_a + as2;                                     // gn(r-2)
+            const double d2 = pgrad(yn_a, gn2, l_a, u_a);                     // d(r-2)
+            const double dw = __shfl_up_sync(0xffffffffu, d2, 1);             // d(r-2) one column west
+            const int re = r - 2;
+            if (out_lane && col_ok && re >= y0 && re < y1) {
+                const long long v = (long long)gx + (long long)A.pitch * re;
+                y_out[v] = yn_a;
+                const bool act = (yn_a == l_a) || (yn_a == u_a);
+                const unsigned char m = act ? 0 : 1;
+                mask_out[v] = m;
+                const double ew = d2 - dw, es = d2 - d_b;
+                double e = op.fw * ew * ew;
+                e = fma(op.fs * es, es, e);
+                if (east_bd) e = fma(op.fe * d2, d2, e);                       // east boundary face
+                if (r - 1 >= A.rhi) e = fma(op.fn * d2, d2, e);                // north boundary face
+                acc[0] = fma(d2, d2, acc[0]);
+                acc[1] = fma(gn2, gn2, acc[1]);
+                acc[2] += act ? 1.0 : 0.0;
+                acc[3] += (st[L::kMP + kk * m5::kMW + c + moff] != m) ? 1.0 : 0.0;
+                const bool binding = (yn_a == l_a && gn2 >= 0.0) || (yn_a == u_a && gn2 <= 0.0);
+                acc[4] += (act && !binding) ? 1.0 : 0.0;
+                acc[5] += e;                                                  // <d, A d>
+                acc[6] = fma(g_a, s_a, acc[6]);                               // <g, s>(r-2)
+                acc[7] = fma(s_a, as2, acc[7]);                               // <s, A s>(r-2)
+            }
+            d_b = d2;
+            s_b = s_a; s_a = s1;
+            g_a = g1; yn_a = yn1; l_a = l_r1; u_a = u_r1;
+            y_m2 = y_m1; y_m1 = yv;
+            l_r1 = lv; u_r1 = uv; b_r1 = bv;
+        },
+        bars, k0);
+}
+
+#ifndef GPCG_GP_SPEC6
+#define GPCG_GP_SPEC6 1
+#endif
+
 // ============================================================================
 // a1-a3 + a7: the whole GP phase as ONE persistent cooperative launch
 // (single slab, single rank, g-free sweeps).  Per GP step: search sweep (K = 2) ->
@@ -1187,7 +1301,7 @@ __device__ __forceinline__ void grid_sum(double (&acc)[NS], double* part, unsign
 }
 
 template <bool SB, bool BB>
-__global__ void __launch_bounds__(m4::kThreads, m4::kMinB)
+__global__ void __launch_bounds__(m4::kThreads, GPCG_GP_MINB)
 k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __restrict__ brow,
            const __grid_constant__ CUtensorMap m_y0, const __grid_constant__ CUtensorMap m_y1,
            const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_l,
@@ -1223,8 +1337,12 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
         if (spec) {
             // speculative accept at alpha_0 with the h = 0 search sums (one sweep when accepted)
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            k = spec_sweep5<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u, cur ? &m_m1 : &m_m0,
-                                    alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc, bars, k);
+            if (GPCG_GP_SPEC6)
+                k = spec_sweep6<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u, cur ? &m_m1 : &m_m0,
+                                        alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc, bars, k);
+            else
+                k = spec_sweep5<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u, cur ? &m_m1 : &m_m0,
+                                        alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc, bars, k);
             grid_sum<8>(acc, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
             const double gs = tot[6], sAs = tot[7];
             const double dq = gs + 0.5 * sAs;

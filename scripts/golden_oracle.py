@@ -9,10 +9,12 @@ usage: python scripts/golden_oracle.py NAME [NAME ...]
   NAME in: C2 (1600^2, configs[2]), C3_1600 (C3 family, 1600^2 member),
            C4_128 (C4 family, 128^3 member)
 """
+import base64
 import json
 import os
 import sys
 import time
+import zlib
 
 import numpy as np
 
@@ -30,7 +32,7 @@ CASES = {
     "C4_128": (lambda: P.c4_family(m=128), -1e-10),
     "C4": (lambda: P.c4(), -1e-10),
 }
-NSAMPLE = 4096
+NSAMPLE = 16384
 
 
 def sample_indices(n, k=NSAMPLE):
@@ -51,6 +53,10 @@ def main():
         idx = sample_indices(prob.n)
         # 1e-7 window around each bound, for the tie rule of the active-set comparison
         near = np.flatnonzero((~act) & ((np.abs(x - prob.l) <= 1e-7) | (np.abs(x - prob.u) <= 1e-7)))
+        # the whole active set (bit-packed, zlib, base64): the GPU test compares it point by point
+        act_z = base64.b64encode(zlib.compress(np.packbits(act.astype(np.uint8)).tobytes(), 9)).decode()
+        # ties: the oracle's free points within 1e-7 of a bound, with x and |g| there
+        gnear = np.abs(g[near])
         out = {
             "name": name, "problem": prob.name, "n": int(prob.n), "tol": tol, "rc": int(rc),
             "oracle_seconds": secs, "stats": {k: (float(v) if isinstance(v, float) else int(v))
@@ -60,6 +66,9 @@ def main():
             "idx": idx.tolist(), "x": [float(v) for v in x[idx]],
             "active_sample": [int(v) for v in act[idx]],
             "n_free_near_bound": int(near.size),
+            "near_idx": near.tolist(), "near_x": [float(v) for v in x[near]],
+            "near_absg": [float(v) for v in gnear],
+            "active_packbits_zlib_b64": act_z,
             "active_sum_index": int(np.sum(np.flatnonzero(act) % 1000003)),
             "source": "scripts/golden_oracle.py -> oracle/gpcg_oracle.c (plain C, fp64, 1 thread)",
         }
