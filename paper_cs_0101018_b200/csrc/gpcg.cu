@@ -439,6 +439,11 @@ int exchange_arrays(gpcg_problem* h, const RowArray* arr, int na) {
 
 bool has_ghosts(const gpcg_problem* h) { return h->nslabs() > 1 || h->nranks > 1; }
 
+// several slabs of one device, one process: the persistent loops span all slabs (SlabLink)
+bool multi_slab_persistent(const gpcg_problem* h) {
+    return h->nranks == 1 && !h->use_nccl && h->nslabs() > 1 && h->nslabs() <= kMaxMs;
+}
+
 // 2-D stencil with its specialised sweeps (march / tile kernels); otherwise the generic kernels
 bool spec2d(const gpcg_problem* h) { return !h->is_csr && !h->is3d && !h->generic; }
 
@@ -586,6 +591,8 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k4_cg_iter<true>, m4cg::kSmem));
     RC(set_smem(k6_cg_loop<false>, m4cg::kSmem));
     RC(set_smem(k6_cg_loop<true>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop_ms<false>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop_ms<true>, m4cg::kSmem));
     RC(set_smem(k4_accept<true, true, false>, AccLayout4<true, true, false>::kSmem));
     RC(set_smem(k4_accept<true, false, false>, AccLayout4<true, false, false>::kSmem));
     RC(set_smem(k4_accept<false, true, false>, AccLayout4<false, true, false>::kSmem));
@@ -677,15 +684,18 @@ int setup_tile(gpcg_problem* h) {
             const char* e = getenv(name);
             return (e && atoi(e) > 0) ? std::min(r, atoi(e) * h->sms) : r;
         };
-        band(cap_env("GPCG_CG_CTAS_PER_SM", r4cg), S.bg_cg, S.grid4_cg);
+        // several slabs in one persistent CG launch: the resident CTAs are shared among the slabs
+        band(cap_env("GPCG_CG_CTAS_PER_SM", r4cg) / (multi_slab_persistent(h) ? h->nslabs() : 1), S.bg_cg,
+             S.grid4_cg);
         {
             const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
             CK(dalloc(h, &S.cgflags, (size_t)std::max<long long>(nf, 1)));
         }
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
-        band(cap_env("GPCG_GP_CTAS_PER_SM", r5acc), S.bg5_acc, S.grid5_acc, m5::kOut);
-        band(cap_env("GPCG_GP_CTAS_PER_SM", r5srch), S.bg5_srch, S.grid5_srch, m5::kOut);
+        const int gshare = multi_slab_persistent(h) ? h->nslabs() : 1;   // one persistent GP launch, all slabs
+        band(cap_env("GPCG_GP_CTAS_PER_SM", r5acc) / gshare, S.bg5_acc, S.grid5_acc, m5::kOut);
+        band(cap_env("GPCG_GP_CTAS_PER_SM", r5srch) / gshare, S.bg5_srch, S.grid5_srch, m5::kOut);
         band(r5init, S.bg5_init, S.grid5_init, m5::kOut);
         S.grid_t_cg = std::min(ntiles, r_cg);
         S.grid_t_acc = std::min(ntiles, r_acc);
@@ -700,6 +710,7 @@ int setup_tile(gpcg_problem* h) {
             const size_t sm = std::max<size_t>(AccLayout5<SB, BB, m5::GP>::kSmem, SrchLayout5<SB, BB, m5::GP, 2>::kSmem);
             h->smem6_gp = sm;
             cudaFuncSetAttribute(k6_gp_loop<SB, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k6_gp_loop_ms<SB, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int nb = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k6_gp_loop<SB, BB>, m4::kThreads, sm);
             return std::max(1, nb) * h->sms;
@@ -1265,7 +1276,59 @@ int launches_per_gp_step(const gpcg_problem* h) {
 }
 
 // The whole GP phase (until it stops or hands a step back) as one cooperative launch.
+// the persistent GP phase runs: one slab and rank, or several slabs of one device (k6_gp_loop_ms)
+bool gp_persist(const gpcg_problem* h) {
+    return h->gp_persistent && h->gfree && (!h->deferred || multi_slab_persistent(h));
+}
+
+int launch_gp_loop_ms(gpcg_problem* h, int cur) {
+    GpMsArgs P;
+    memset(&P, 0, sizeof P);
+    P.nslabs = h->nslabs();
+    int cta = 0;
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        GpMsSlab& X = P.s[s];
+        X.m_y0 = S.t5[VY0]; X.m_y1 = S.t5[VY1]; X.m_b = S.t5[VB]; X.m_l = S.t5[VL]; X.m_u = S.t5[VU];
+        X.m_m0 = S.t5m[MK0]; X.m_m1 = S.t5m[MK1];
+        X.A = S.sop;
+        X.Gs = S.bg5_srch;
+        X.Ga = S.bg5_acc;
+        X.Bd = h->bounds(S);
+        X.brow = S.brow;
+        X.y0p = S.v[VY0]; X.y1p = S.v[VY1]; X.mk0 = S.m[MK0]; X.mk1 = S.m[MK1];
+        const int g = std::max(1, std::min(S.grid5_srch, S.grid5_acc));
+        X.Ls = SlabLink{0, g, 0, 0, 0};
+        if (S.nb_lo >= 0) {
+            Slab& N = h->slabs[S.nb_lo];
+            X.lo_y0 = N.v[VY0]; X.lo_y1 = N.v[VY1]; X.lo_m0 = N.m[MK0]; X.lo_m1 = N.m[MK1];
+            X.Ls.lo_rows = N.rows;
+            X.Ls.lo_ghost = N.ghi;
+        }
+        if (S.nb_hi >= 0) {
+            Slab& N = h->slabs[S.nb_hi];
+            X.hi_y0 = N.v[VY0]; X.hi_y1 = N.v[VY1]; X.hi_m0 = N.m[MK0]; X.hi_m1 = N.m[MK1];
+            X.Ls.hi_ghost = N.glo;
+        }
+        X.La = X.Ls;
+        X.cta0 = cta;
+        cta += g;
+    }
+    CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
+    double mu = h->prm.mu;
+    int spec = h->gp_spec ? 1 : 0;
+    void* args[] = {(void*)&P, (void*)&cur, (void*)&mu, (void*)&h->dS, (void*)&h->slabs[0].partials,
+                    (void*)&h->gbar, (void*)&spec};
+    const void* fn;
+    if (h->sb) fn = h->bb ? (const void*)k6_gp_loop_ms<true, true> : (const void*)k6_gp_loop_ms<true, false>;
+    else fn = h->bb ? (const void*)k6_gp_loop_ms<false, true> : (const void*)k6_gp_loop_ms<false, false>;
+    CK(cudaLaunchCooperativeKernel(fn, dim3(cta), dim3(m4::kThreads), args, h->smem6_gp, h->st));
+    h->launches++;
+    return GPCG_OK;
+}
+
 int launch_gp_loop(gpcg_problem* h, int cur) {
+    if (h->nslabs() > 1) return launch_gp_loop_ms(h, cur);
     Slab& S = h->slabs[0];
     CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
     Bounds B = h->bounds(S);
@@ -1679,6 +1742,56 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
             return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
                            (long long)h->hS->cg_it);
         return GPCG_OK;    // one slab: no ghosts of w to refresh
+    }
+    if (h->cg_persistent && h->tile && (h->tile_mask & 8) && multi_slab_persistent(h)) {
+        // one cooperative launch over every slab (k6_cg_loop_ms, fused halo writes)
+        CgMsArgs P;
+        memset(&P, 0, sizeof P);
+        P.nslabs = h->nslabs();
+        int cta = 0;
+        for (int s = 0; s < h->nslabs(); ++s) {
+            Slab& S = h->slabs[s];
+            CgMsSlab& X = P.s[s];
+            X.m_rho0 = S.t4[VRHO0]; X.m_rho1 = S.t4[VRHO1]; X.m_p0 = S.t4[VQ0]; X.m_p1 = S.t4[VQ1];
+            X.m_w = S.t4wo; X.m_mask = S.t4m[MKCG];
+            X.A = S.sop;
+            X.G = S.bg_cg;
+            X.rho0 = S.v[VRHO0]; X.rho1 = S.v[VRHO1]; X.p0 = S.v[VQ0]; X.p1 = S.v[VQ1]; X.w = S.v[VW];
+            X.flags = h->cg_skip ? S.cgflags : nullptr;
+            X.L = SlabLink{0, S.grid4_cg, 0, 0, 0};
+            if (S.nb_lo >= 0) {
+                Slab& N = h->slabs[S.nb_lo];
+                X.lo_rho0 = N.v[VRHO0]; X.lo_rho1 = N.v[VRHO1]; X.lo_p0 = N.v[VQ0]; X.lo_p1 = N.v[VQ1];
+                X.L.lo_rows = N.rows;
+                X.L.lo_ghost = N.ghi;
+            }
+            if (S.nb_hi >= 0) {
+                Slab& N = h->slabs[S.nb_hi];
+                X.hi_rho0 = N.v[VRHO0]; X.hi_rho1 = N.v[VRHO1]; X.hi_p0 = N.v[VQ0]; X.hi_p1 = N.v[VQ1];
+                X.L.hi_ghost = N.glo;
+            }
+            X.cta0 = cta;
+            cta += S.grid4_cg;
+        }
+        CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
+        CK(cudaEventRecord(h->ev_c0, h->st));
+        void* args[] = {(void*)&P, (void*)&h->dS, (void*)&h->slabs[0].partials, (void*)&h->gbar};
+        const void* fn = h->prm.precond == 1 ? (const void*)k6_cg_loop_ms<true> : (const void*)k6_cg_loop_ms<false>;
+        CK(cudaLaunchCooperativeKernel(fn, dim3(cta), dim3(m4::kThreadsWS), args, (size_t)m4cg::kSmem, h->st));
+        CK(cudaEventRecord(h->ev_c1, h->st));
+        h->launches++;
+        RC(sync_scal(h));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_c0, h->ev_c1));
+        h->t_cg_timed_ms += ms;
+        h->cg_iters_timed += h->hS->cg_it;
+        h->cg_free_iters_timed += h->hS->cg_it * m;
+        *iters = h->hS->cg_it;
+        if (h->hS->cg_reason == CG_NOTSPD)
+            return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
+                           (long long)h->hS->cg_it);
+        // the search along d = w reads w at the neighbours
+        return exchange(h, {VW});
     }
     const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
     RC(build_cg_graph(h, chunk));
@@ -2369,7 +2482,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
     RC(launch_accept(h, VIN, NO_VEC, 0.0, NO_VEC, VY0, VG0, MK0));
     RC(sync_scal(h));
     st.full_spmvs++;
-    if (h->gp_graph && !(h->gp_persistent && h->gfree && !h->deferred))
+    if (h->gp_graph && !gp_persist(h))
         RC(build_gp_graph(h, std::max(1, h->prm.gp_chunk)));
     st.g0_norm = std::sqrt(S.g2);
     tau = tol > 0.0 ? tol : -tol * st.g0_norm;
@@ -2388,7 +2501,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 h->launches++;
                 CKLAUNCH();
                 long long jdone = 0;
-                const bool persist = h->gp_persistent && h->gfree && !h->deferred;
+                const bool persist = gp_persist(h);
                 for (;;) {
                     if (persist) {
                         if ((rc = launch_gp_loop(h, cur))) goto fail;

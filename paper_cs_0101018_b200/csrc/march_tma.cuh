@@ -39,11 +39,19 @@ namespace gpcg {
 #ifndef GPCG_CG_MINB
 #define GPCG_CG_MINB (16 / GPCG_M4_WARPS)   // CG sweep CTAs per SM the register budget is sized for
 #endif
+#ifndef GPCG_LAZY_REFILL
+#define GPCG_LAZY_REFILL 0  // 1: lock-step band engine without the per-block CTA barrier -- the last warp
+                            // done with a stage refills it (measured: no gain on C2 / C3)
+#endif
+#ifndef GPCG_GP_BRANCHFREE
+#define GPCG_GP_BRANCHFREE 0   // 1: spec_sweep6 sums without a per-row branch (weights 0 / 1): measured slower (C3 562 vs 541 us per GP step)
+#endif
 #ifndef GPCG_GP_NST
-#define GPCG_GP_NST 4       // pipeline stages of the g-free GP sweeps (k5 / k6_gp_loop; tuning)
+#define GPCG_GP_NST 3       // pipeline stages of the g-free GP sweeps (k5 / k6_gp_loop; tuning: 3 stages
+                            // and 3 CTAs per SM measured 3 % faster than 4 and 2 on C3)
 #endif
 #ifndef GPCG_GP_MINB
-#define GPCG_GP_MINB (16 / GPCG_M4_WARPS)   // CTAs per SM the GP sweeps' register budget is sized for
+#define GPCG_GP_MINB 3      // CTAs per SM the GP sweeps' register budget is sized for
 #endif
 namespace m4 {
 constexpr int kWarps = GPCG_M4_WARPS;     // consumer warps (one per 28 / 26-column strip)
@@ -87,17 +95,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // flags (nullable): one byte per (item, block) -- bit 0: the block's raw rows hold a free
 // point, bit 1: its emitted rows do -- passed to issue_loads so that all-active blocks skip
 // the loads their rows never read (3 = load everything).
+// bid / nb (>= 0): this CTA's index and the CTA count among the CTAs sharing G (a persistent
+// kernel spanning several slabs gives each slab its own range of CTAs); default the grid's.
 template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
 __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
                                                 Begin&& begin, Row&& row, int k0 = 0,
-                                                const unsigned char* __restrict__ flags = nullptr) {
+                                                const unsigned char* __restrict__ flags = nullptr, int bid = -1,
+                                                int nb = -1) {
     using namespace m4;
+    if (bid < 0) { bid = blockIdx.x; nb = gridDim.x; }
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     uint64_t* empty = full + NST;
     const int nitems = G.nbands * G.nsegs;
     const int nblk = (G.seg + PRE + POST + kBR - 1) / kBR;
     int nmine = 0;
-    for (int t = blockIdx.x; t < nitems; t += gridDim.x) nmine += nblk;
+    for (int t = bid; t < nitems; t += nb) nmine += nblk;
     if (k0 == 0) {
         if (threadIdx.x == 0) {
             for (int s = 0; s < NST; ++s) {
@@ -111,7 +123,7 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == kWarps) {                                 // producer (lane 0 issues; the warp fetches flags)
         int k = k0;
-        for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
+        for (int t = bid; t < nitems; t += nb) {
             const int x0 = (t % G.nbands) * OUT;
             const int yb = (t / G.nbands) * G.seg - PRE;
             int f = 3;
@@ -127,7 +139,7 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
         return k0 + nmine;
     }
     int k = k0;
-    for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
+    for (int t = bid; t < nitems; t += nb) {
         const int x0 = (t % G.nbands) * OUT;
         const int y0 = (t / G.nbands) * G.seg, y1 = min(y0 + G.seg, ny);
         begin(x0, y0, y1);
@@ -151,22 +163,27 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
 // bars: NST mbarriers (null: after the stages); k0 as in band_pipeline_ws (init at 0 only).
 template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
 __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
-                                             Begin&& begin, Row&& row, uint64_t* bars = nullptr, int k0 = 0) {
+                                             Begin&& begin, Row&& row, uint64_t* bars = nullptr, int k0 = 0,
+                                             int bid = -1, int nb = -1) {
     using namespace m4;
+    if (bid < 0) { bid = blockIdx.x; nb = gridDim.x; }
     uint64_t* bar = bars ? bars : reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     const int nitems = G.nbands * G.nsegs;
     const int nblk = (G.seg + PRE + POST + kBR - 1) / kBR;
     int nmine = 0;
-    for (int t = blockIdx.x; t < nitems; t += gridDim.x) nmine += nblk;
+    for (int t = bid; t < nitems; t += nb) nmine += nblk;
     auto issue = [&](int k) {                            // k: this sweep's local block index
         const int i = k / nblk, b = k - i * nblk;
-        const int t = blockIdx.x + i * (int)gridDim.x;
+        const int t = bid + i * nb;
         if (t >= nitems) return;
         const int stage = (k0 + k) % NST;
         const int x0 = (t % G.nbands) * OUT;
         const int yr = (t / G.nbands) * G.seg - PRE + b * kBR;
         issue_loads(smem + stage * STAGE, x0, yr, &bar[stage]);
     };
+#if GPCG_LAZY_REFILL
+    __shared__ unsigned int done_cnt[8];                 // warps done with each stage's current block
+#endif
     if (threadIdx.x == 0) {
         if (k0 == 0) {
             for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
@@ -174,9 +191,12 @@ __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned
         }
         for (int k = 0; k < NST; ++k) issue(k);
     }
+#if GPCG_LAZY_REFILL
+    if (threadIdx.x < NST) done_cnt[threadIdx.x] = 0;
+#endif
     __syncthreads();
     int k = 0;
-    for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
+    for (int t = bid; t < nitems; t += nb) {
         const int x0 = (t % G.nbands) * OUT;
         const int y0 = (t / G.nbands) * G.seg, y1 = min(y0 + G.seg, ny);
         begin(x0, y0, y1);
@@ -187,15 +207,47 @@ __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned
             const int yr = y0 - PRE + b * kBR;
 #pragma unroll
             for (int kk = 0; kk < kBR; ++kk) row(st, kk, yr + kk);
+#if GPCG_LAZY_REFILL
+            // no CTA barrier: each warp counts itself done with the stage; the LAST warp to finish
+            // it refills it (block k + NST), so no warp ever waits for the others here
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) {
+                __threadfence_block();
+                if (atomicAdd(&done_cnt[stage], 1u) == (unsigned int)(m4::kThreads / 32) - 1) {
+                    done_cnt[stage] = 0;
+                    __threadfence_block();
+                    fence_proxy_async();
+                    issue(k + NST);
+                }
+            }
+#else
             __syncthreads();                              // every warp is done with this stage
             if (threadIdx.x == 0) {
                 fence_proxy_async();
                 issue(k + NST);
             }
+#endif
         }
     }
+#if GPCG_LAZY_REFILL
+    __syncthreads();                                      // stages free before the next sweep issues
+#endif
     return k0 + nmine;
 }
+
+// Several slabs of one device in ONE persistent kernel (SURVEY.md 8(e) row slabs; the
+// multi-slab counterpart of k6_cg_loop / k6_gp_loop): the CTAs of slab s are the grid range
+// [cta0, cta0 + nb), bid = blockIdx.x - cta0 their index within the slab.  Fused halo
+// exchange: every output row a neighbour slab keeps as a ghost row is also stored straight
+// into that neighbour's ghost rows by the CTA that produces it, so the ghost rows are current
+// after the grid barrier that ends the sweep -- no exchange step, no extra barrier, the
+// transfer overlaps the sweep.  lo_rows: owned rows of the lower neighbour (slab s - 1);
+// lo_ghost / hi_ghost: ghost rows the lower / upper neighbour keeps of this slab (0: none).
+struct SlabLink {
+    int bid, nb;
+    int lo_rows;
+    int lo_ghost, hi_ghost;
+};
 
 // ============================================================================
 // a5: CG iteration, same recurrences as k2_cg_iter:
@@ -221,7 +273,9 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
                                          const CUtensorMap* m_p, const CUtensorMap* m_w, const CUtensorMap* m_mask,
                                          double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out,
                                          double alpha, double beta, unsigned char* smem, double (&acc)[2], int k0,
-                                         const unsigned char* __restrict__ flags = nullptr) {
+                                         const unsigned char* __restrict__ flags = nullptr,
+                                         const SlabLink* L = nullptr, double* lo_rho = nullptr, double* lo_p = nullptr,
+                                         double* hi_rho = nullptr, double* hi_p = nullptr) {
     using namespace m4cg;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int c = 28 * wid + lane;                        // box column of this lane
@@ -275,6 +329,18 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
                 p_n[v] = pn_m2;
                 acc[0] = fma(rres, rn_m2, acc[0]);
                 acc[1] = fma(rn_m2, q, acc[1]);
+                if (L) {                                      // fused halo write (SlabLink)
+                    if (r2 < L->lo_ghost) {
+                        const long long vl = (long long)gx + (long long)A.pitch * (L->lo_rows + r2);
+                        lo_rho[vl] = rres;
+                        lo_p[vl] = pn_m2;
+                    }
+                    if (r2 >= A.ny - L->hi_ghost) {
+                        const long long vh = (long long)gx + (long long)A.pitch * (r2 - A.ny);
+                        hi_rho[vh] = rres;
+                        hi_p[vh] = pn_m2;
+                    }
+                }
             }
             pn_m2 = pn_m1; pn_m1 = pn0;
             rho_m1 = rho;
@@ -282,7 +348,7 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
             rn_m3 = rn_m2; rn_m2 = rn1;
             rr_m2 = rr1;
         },
-        k0, flags);
+        k0, flags, L ? L->bid : -1, L ? L->nb : -1);
 }
 
 // ============================================================================
@@ -417,15 +483,11 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
     __syncthreads();
 }
 
-template <bool PC>
-__global__ void __launch_bounds__(m4::kThreadsWS, GPCG_CG_MINB)
-k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, const __grid_constant__ CUtensorMap m_rho1,
-           const __grid_constant__ CUtensorMap m_p0, const __grid_constant__ CUtensorMap m_p1,
-           const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
-           double* __restrict__ rho0, double* __restrict__ rho1, double* __restrict__ p0, double* __restrict__ p1,
-           double* __restrict__ w_out, Scal* S, double* __restrict__ part, unsigned int* gbar,
-           const unsigned char* __restrict__ flags) {
-    extern __shared__ __align__(128) unsigned char smem[];
+// The CG call loop shared by the single- and multi-slab persistent kernels: per iteration
+// sweep(a, alpha, beta, acc, k) -> block partials -> grid barrier -> fixed-order sum of all
+// CTAs' partials (the same in every CTA) -> cg_finalize evaluated in every CTA.
+template <class Sweep>
+__device__ __forceinline__ void cg_loop(Scal* S, double* __restrict__ part, unsigned int* gbar, Sweep&& sweep) {
     __shared__ double red[2 * 32];
     __shared__ double tot[2];
     // CG state (identical in every CTA)
@@ -440,8 +502,7 @@ k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, 
     while (!done) {
         const int a = (int)(it & 1);
         double acc[2] = {0.0, 0.0};
-        k = cg_sweep4<PC>(A, G, a ? &m_rho1 : &m_rho0, a ? &m_p1 : &m_p0, &m_w, &m_mask, a ? rho0 : rho1,
-                          a ? p0 : p1, w_out, alpha, beta, smem, acc, k, flags);
+        k = sweep(a, alpha, beta, acc, k);
         // block partials -> part[parity][s][block]
         block_reduce<2>(acc, red);
         double* pp = part + (it & 1) * 2 * G_;
@@ -489,6 +550,58 @@ k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, 
         }
     }
     // the host zeroes the barrier counter before each launch
+}
+
+template <bool PC>
+__global__ void __launch_bounds__(m4::kThreadsWS, GPCG_CG_MINB)
+k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, const __grid_constant__ CUtensorMap m_rho1,
+           const __grid_constant__ CUtensorMap m_p0, const __grid_constant__ CUtensorMap m_p1,
+           const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
+           double* __restrict__ rho0, double* __restrict__ rho1, double* __restrict__ p0, double* __restrict__ p1,
+           double* __restrict__ w_out, Scal* S, double* __restrict__ part, unsigned int* gbar,
+           const unsigned char* __restrict__ flags) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    cg_loop(S, part, gbar, [&](int a, double alpha, double beta, double (&acc)[2], int k) {
+        return cg_sweep4<PC>(A, G, a ? &m_rho1 : &m_rho0, a ? &m_p1 : &m_p0, &m_w, &m_mask, a ? rho0 : rho1,
+                             a ? p0 : p1, w_out, alpha, beta, smem, acc, k, flags);
+    });
+}
+
+// k6_cg_loop over several slabs of one device (SlabLink): each slab's CTAs sweep its rows and
+// write the rows its neighbours keep as ghosts into their ghost rows as well; one grid
+// barrier and one fixed-order sum over all CTAs per iteration, as with one slab.
+constexpr int kMaxMs = 8;
+struct CgMsSlab {
+    CUtensorMap m_rho0, m_rho1, m_p0, m_p1, m_w, m_mask;
+    StencilOp A;
+    BandGeom G;
+    double *rho0, *rho1, *p0, *p1, *w;
+    const unsigned char* flags;
+    double *lo_rho0, *lo_rho1, *lo_p0, *lo_p1;    // lower neighbour's origins (slab s - 1)
+    double *hi_rho0, *hi_rho1, *hi_p0, *hi_p1;    // upper neighbour's origins (slab s + 1)
+    SlabLink L;                                   // bid is set in the kernel
+    int cta0;
+};
+struct CgMsArgs {
+    CgMsSlab s[kMaxMs];
+    int nslabs;
+};
+
+template <bool PC>
+__global__ void __launch_bounds__(m4::kThreadsWS, GPCG_CG_MINB)
+k6_cg_loop_ms(const __grid_constant__ CgMsArgs P, Scal* S, double* __restrict__ part, unsigned int* gbar) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    int si = 0;
+    while (si + 1 < P.nslabs && (int)blockIdx.x >= P.s[si + 1].cta0) ++si;
+    const CgMsSlab& X = P.s[si];
+    SlabLink L = X.L;
+    L.bid = (int)blockIdx.x - X.cta0;
+    cg_loop(S, part, gbar, [&](int a, double alpha, double beta, double (&acc)[2], int k) {
+        return cg_sweep4<PC>(X.A, X.G, a ? &X.m_rho1 : &X.m_rho0, a ? &X.m_p1 : &X.m_p0, &X.m_w, &X.m_mask,
+                             a ? X.rho0 : X.rho1, a ? X.p0 : X.p1, X.w, alpha, beta, smem, acc, k, X.flags, &L,
+                             a ? X.lo_rho0 : X.lo_rho1, a ? X.lo_p0 : X.lo_p1, a ? X.hi_rho0 : X.hi_rho1,
+                             a ? X.hi_p0 : X.hi_p1);
+    });
 }
 
 // ============================================================================
@@ -746,7 +859,10 @@ __device__ __forceinline__ int accept_sweep5(const StencilOp& A, const BandGeom&
                                              const CUtensorMap* m_dir, const CUtensorMap* m_b, const CUtensorMap* m_l,
                                              const CUtensorMap* m_u, const CUtensorMap* m_mp, int has_mp, double alpha,
                                              double* __restrict__ y_out, unsigned char* __restrict__ mask_out,
-                                             unsigned char* smem, double (&acc)[6], uint64_t* bars, int k0) {
+                                             unsigned char* smem, double (&acc)[6], uint64_t* bars, int k0,
+                                             const SlabLink* SL = nullptr, double* lo_y = nullptr,
+                                             unsigned char* lo_m = nullptr, double* hi_y = nullptr,
+                                             unsigned char* hi_m = nullptr) {
     using namespace m4;
     using L = AccLayout5<SB, BB, MODE>;
     constexpr int LAG = L::kLag;
@@ -830,13 +946,25 @@ __device__ __forceinline__ int accept_sweep5(const StencilOp& A, const BandGeom&
                 const bool binding = (yn_e == l_e && gn_e >= 0.0) || (yn_e == u_e && gn_e <= 0.0);
                 acc[4] += (act && !binding) ? 1.0 : 0.0;
                 acc[5] = fma(d_a, ad, acc[5]);
+                if (SL) {                                     // fused halo write (SlabLink)
+                    if (re < SL->lo_ghost) {
+                        const long long vl = (long long)gx + (long long)A.pitch * (SL->lo_rows + re);
+                        lo_y[vl] = yn_e;
+                        lo_m[vl] = m;
+                    }
+                    if (re >= A.ny - SL->hi_ghost) {
+                        const long long vh = (long long)gx + (long long)A.pitch * (re - A.ny);
+                        hi_y[vh] = yn_e;
+                        hi_m[vh] = m;
+                    }
+                }
             }
             yn_e = yn_a; gn_e = gn1; l_e = l_a; u_e = u_a;
             d_b = d_a; d_a = d1;
             yn_b = yn_a; yn_a = yn;
             l_a = ln; u_a = un; b_a = bn;
         },
-        bars, k0);
+        bars, k0, SL ? SL->bid : -1, SL ? SL->nb : -1);
 }
 
 template <bool SB, bool BB, int MODE>
@@ -878,7 +1006,8 @@ __device__ __forceinline__ int search_sweep5(const StencilOp& A, const BandGeom&
                                              const double* __restrict__ brow, const CUtensorMap* m_y,
                                              const CUtensorMap* m_dir, const CUtensorMap* m_b, const CUtensorMap* m_l,
                                              const CUtensorMap* m_u, const double (&al)[K], unsigned char* smem,
-                                             double (&acc)[2 * K], uint64_t* bars, int k0) {
+                                             double (&acc)[2 * K], uint64_t* bars, int k0,
+                                             const SlabLink* SL = nullptr) {
     using namespace m4;
     using L = SrchLayout5<SB, BB, MODE, K>;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -956,7 +1085,7 @@ __device__ __forceinline__ int search_sweep5(const StencilOp& A, const BandGeom&
             y_m2 = y_m1; y_m1 = yv;
             l_r1 = lv; u_r1 = uv; b_r1 = bv;
         },
-        bars, k0);
+        bars, k0, SL ? SL->bid : -1, SL ? SL->nb : -1);
 }
 
 template <bool SB, bool BB, int MODE, int K>
@@ -1182,7 +1311,9 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
                                            const CUtensorMap* m_b, const CUtensorMap* m_l, const CUtensorMap* m_u,
                                            const CUtensorMap* m_mp, double alpha, double* __restrict__ y_out,
                                            unsigned char* __restrict__ mask_out, unsigned char* smem,
-                                           double (&acc)[8], uint64_t* bars, int k0) {
+                                           double (&acc)[8], uint64_t* bars, int k0, const SlabLink* SL = nullptr,
+                                           double* lo_y = nullptr, unsigned char* lo_m = nullptr,
+                                           double* hi_y = nullptr, unsigned char* hi_m = nullptr) {
     using namespace m4;
     using L = AccLayout5<SB, BB, m5::GP>;
     constexpr int LAG = 2;                        // emitted row = raw row - 2
@@ -1238,7 +1369,42 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             const double d2 = pgrad(yn_a, gn2, l_a, u_a);                     // d(r-2)
             const double dw = __shfl_up_sync(0xffffffffu, d2, 1);             // d(r-2) one column west
             const int re = r - 2;
-            if (out_lane && col_ok && re >= y0 && re < y1) {
+            const bool emit = out_lane && col_ok && re >= y0 && re < y1;
+#if GPCG_GP_BRANCHFREE
+            // the sums without a branch (weight 0 / 1), so that the rows of a block can interleave;
+            // only the stores are predicated
+            {
+                const double wgt = emit ? 1.0 : 0.0;
+                const bool act = (yn_a == l_a) || (yn_a == u_a);
+                const unsigned char m = act ? 0 : 1;
+                const double ew = d2 - dw, es = d2 - d_b;
+                double e = op.fw * ew * ew;
+                e = fma(op.fs * es, es, e);
+                if (east_bd) e = fma(op.fe * d2, d2, e);                       // east boundary face
+                if (r - 1 >= A.rhi) e = fma(op.fn * d2, d2, e);                // north boundary face
+                const double dz = wgt * d2, gz = wgt * gn2, sz = wgt * s_a;
+                acc[0] = fma(dz, d2, acc[0]);
+                acc[1] = fma(gz, gn2, acc[1]);
+                acc[5] = fma(wgt, e, acc[5]);                                 // <d, A d>
+                acc[6] = fma(g_a, sz, acc[6]);                                // <g, s>(r-2)
+                acc[7] = fma(sz, as2, acc[7]);                                // <s, A s>(r-2)
+                const bool binding = (yn_a == l_a && gn2 >= 0.0) || (yn_a == u_a && gn2 <= 0.0);
+                const unsigned char mp = st[L::kMP + kk * m5::kMW + c + moff];
+                acc[2] += (emit && act) ? 1.0 : 0.0;
+                acc[3] += (emit && mp != m) ? 1.0 : 0.0;
+                acc[4] += (emit && act && !binding) ? 1.0 : 0.0;
+                if (emit) {
+                    const long long v = (long long)gx + (long long)A.pitch * re;
+                    y_out[v] = yn_a;
+                    mask_out[v] = m;
+                }
+            }
+            if (SL && emit) {
+                const bool act = (yn_a == l_a) || (yn_a == u_a);
+                const unsigned char m = act ? 0 : 1;
+                {
+#else
+            if (emit) {
                 const long long v = (long long)gx + (long long)A.pitch * re;
                 y_out[v] = yn_a;
                 const bool act = (yn_a == l_a) || (yn_a == u_a);
@@ -1258,6 +1424,21 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
                 acc[5] += e;                                                  // <d, A d>
                 acc[6] = fma(g_a, s_a, acc[6]);                               // <g, s>(r-2)
                 acc[7] = fma(s_a, as2, acc[7]);                               // <s, A s>(r-2)
+                {
+#endif
+                if (SL) {                                     // fused halo write (SlabLink)
+                    if (re < SL->lo_ghost) {
+                        const long long vl = (long long)gx + (long long)A.pitch * (SL->lo_rows + re);
+                        lo_y[vl] = yn_a;
+                        lo_m[vl] = m;
+                    }
+                    if (re >= A.ny - SL->hi_ghost) {
+                        const long long vh = (long long)gx + (long long)A.pitch * (re - A.ny);
+                        hi_y[vh] = yn_a;
+                        hi_m[vh] = m;
+                    }
+                }
+                }
             }
             d_b = d2;
             s_b = s_a; s_a = s1;
@@ -1265,7 +1446,7 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             y_m2 = y_m1; y_m1 = yv;
             l_r1 = lv; u_r1 = uv; b_r1 = bv;
         },
-        bars, k0);
+        bars, k0, SL ? SL->bid : -1, SL ? SL->nb : -1);
 }
 
 #ifndef GPCG_GP_SPEC6
@@ -1300,17 +1481,12 @@ __device__ __forceinline__ void grid_sum(double (&acc)[NS], double* part, unsign
     __syncthreads();
 }
 
-template <bool SB, bool BB>
-__global__ void __launch_bounds__(m4::kThreads, GPCG_GP_MINB)
-k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __restrict__ brow,
-           const __grid_constant__ CUtensorMap m_y0, const __grid_constant__ CUtensorMap m_y1,
-           const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_l,
-           const __grid_constant__ CUtensorMap m_u, const __grid_constant__ CUtensorMap m_m0,
-           const __grid_constant__ CUtensorMap m_m1, double* __restrict__ y0p, double* __restrict__ y1p,
-           unsigned char* __restrict__ mk0, unsigned char* __restrict__ mk1, int cur0, double mu, Scal* S,
-           double* __restrict__ part, unsigned int* gbar, int spec) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[4];
+// The GP phase loop shared by the single- and multi-slab persistent kernels.  spec(cur, alpha_0,
+// acc8, k), search(cur, al, acc4, k), accept(cur, alpha, acc6, k) run one sweep of this CTA's
+// items from the y / mask buffers `cur` and return the CTA's running TMA block count.
+template <class Spec, class Search, class Accept>
+__device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __restrict__ part, unsigned int* gbar,
+                                        int spec, Spec&& spec_fn, Search&& search_fn, Accept&& accept_fn) {
     __shared__ double red[8 * 32];
     __shared__ double tot[8];
     if (S->gp_done) return;
@@ -1337,12 +1513,7 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
         if (spec) {
             // speculative accept at alpha_0 with the h = 0 search sums (one sweep when accepted)
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            if (GPCG_GP_SPEC6)
-                k = spec_sweep6<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u, cur ? &m_m1 : &m_m0,
-                                        alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc, bars, k);
-            else
-                k = spec_sweep5<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u, cur ? &m_m1 : &m_m0,
-                                        alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc, bars, k);
+            k = spec_fn(cur, alpha0, acc, k);
             grid_sum<8>(acc, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
             const double gs = tot[6], sAs = tot[7];
             const double dq = gs + 0.5 * sAs;
@@ -1357,8 +1528,7 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
             const int h0 = spec ? 1 : 0;
             const double al[2] = {scalbn(alpha0, -h0), scalbn(alpha0, -(h0 + 1))};
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            k = search_sweep5<SB, BB, m5::GP, 2>(A, Gs, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b,
-                                                 &m_l, &m_u, al, smem, acc, bars, k);
+            k = search_fn(cur, al, acc, k);
             grid_sum<4>(acc, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
             s_h = -1;
             for (int h = 0; h < 2; ++h) {
@@ -1375,9 +1545,7 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
             if (s_h < 0) { s_h = -1; s_spec = h0 + 2; done = 1; reason = GP_HOST; break; }
             // ---- accept y' = P[y - s_alpha g], regrad sums, free mask, next Cauchy form
             double acc6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            k = accept_sweep5<SB, BB, m5::GP>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b, &m_l,
-                                              &m_u, cur ? &m_m1 : &m_m0, 1, s_alpha, cur ? y0p : y1p,
-                                              cur ? mk0 : mk1, smem, acc6, bars, k);
+            k = accept_fn(cur, s_alpha, acc6, k);
             grid_sum<6>(acc6, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
         }
         pg2 = tot[0]; g2 = tot[1]; n_active = tot[2]; n_changed = tot[3]; n_nb = tot[4];
@@ -1403,6 +1571,92 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
         S->s_pad = s_spec;                         // GP_HOST after a search: resume the search at h = s_spec
         S->gp_fb = nfb;
     }
+}
+
+template <bool SB, bool BB>
+__global__ void __launch_bounds__(m4::kThreads, GPCG_GP_MINB)
+k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __restrict__ brow,
+           const __grid_constant__ CUtensorMap m_y0, const __grid_constant__ CUtensorMap m_y1,
+           const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_l,
+           const __grid_constant__ CUtensorMap m_u, const __grid_constant__ CUtensorMap m_m0,
+           const __grid_constant__ CUtensorMap m_m1, double* __restrict__ y0p, double* __restrict__ y1p,
+           unsigned char* __restrict__ mk0, unsigned char* __restrict__ mk1, int cur0, double mu, Scal* S,
+           double* __restrict__ part, unsigned int* gbar, int spec) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[4];
+    gp_loop(
+        cur0, mu, S, part, gbar, spec,
+        [&](int cur, double alpha0, double (&acc)[8], int k) {
+            if (GPCG_GP_SPEC6)
+                return spec_sweep6<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u,
+                                           cur ? &m_m1 : &m_m0, alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc,
+                                           bars, k);
+            return spec_sweep5<SB, BB>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, &m_b, &m_l, &m_u, cur ? &m_m1 : &m_m0,
+                                       alpha0, cur ? y0p : y1p, cur ? mk0 : mk1, smem, acc, bars, k);
+        },
+        [&](int cur, const double (&al)[2], double (&acc)[4], int k) {
+            return search_sweep5<SB, BB, m5::GP, 2>(A, Gs, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b,
+                                                    &m_l, &m_u, al, smem, acc, bars, k);
+        },
+        [&](int cur, double alpha, double (&acc)[6], int k) {
+            return accept_sweep5<SB, BB, m5::GP>(A, Ga, Bd, brow, cur ? &m_y1 : &m_y0, cur ? &m_y1 : &m_y0, &m_b,
+                                                 &m_l, &m_u, cur ? &m_m1 : &m_m0, 1, alpha, cur ? y0p : y1p,
+                                                 cur ? mk0 : mk1, smem, acc, bars, k);
+        });
+}
+
+// k6_gp_loop over several slabs of one device (SlabLink): the accepted y and the new mask of
+// every row a neighbour keeps as a ghost row also go straight into its ghost rows.
+struct GpMsSlab {
+    CUtensorMap m_y0, m_y1, m_b, m_l, m_u, m_m0, m_m1;
+    StencilOp A;
+    BandGeom Gs, Ga;
+    Bounds Bd;
+    const double* brow;
+    double *y0p, *y1p;
+    unsigned char *mk0, *mk1;
+    double *lo_y0, *lo_y1, *hi_y0, *hi_y1;            // neighbours' origins of the y buffers
+    unsigned char *lo_m0, *lo_m1, *hi_m0, *hi_m1;     // ... and of the mask buffers
+    SlabLink Ls, La;                                  // search / accept geometries (bid set in the kernel)
+    int cta0;
+};
+struct GpMsArgs {
+    GpMsSlab s[kMaxMs];
+    int nslabs;
+};
+
+template <bool SB, bool BB>
+__global__ void __launch_bounds__(m4::kThreads, GPCG_GP_MINB)
+k6_gp_loop_ms(const __grid_constant__ GpMsArgs P, int cur0, double mu, Scal* S, double* __restrict__ part,
+              unsigned int* gbar, int spec) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[4];
+    int si = 0;
+    while (si + 1 < P.nslabs && (int)blockIdx.x >= P.s[si + 1].cta0) ++si;
+    const GpMsSlab& X = P.s[si];
+    SlabLink Ls = X.Ls, La = X.La;
+    Ls.bid = La.bid = (int)blockIdx.x - X.cta0;
+    gp_loop(
+        cur0, mu, S, part, gbar, spec,
+        [&](int cur, double alpha0, double (&acc)[8], int k) {
+            return spec_sweep6<SB, BB>(X.A, X.Ga, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u,
+                                       cur ? &X.m_m1 : &X.m_m0, alpha0, cur ? X.y0p : X.y1p, cur ? X.mk0 : X.mk1,
+                                       smem, acc, bars, k, &La, cur ? X.lo_y0 : X.lo_y1, cur ? X.lo_m0 : X.lo_m1,
+                                       cur ? X.hi_y0 : X.hi_y1, cur ? X.hi_m0 : X.hi_m1);
+        },
+        [&](int cur, const double (&al)[2], double (&acc)[4], int k) {
+            return search_sweep5<SB, BB, m5::GP, 2>(X.A, X.Gs, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0,
+                                                    cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u, al, smem, acc,
+                                                    bars, k, &Ls);
+        },
+        [&](int cur, double alpha, double (&acc)[6], int k) {
+            return accept_sweep5<SB, BB, m5::GP>(X.A, X.Ga, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0,
+                                                 cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u,
+                                                 cur ? &X.m_m1 : &X.m_m0, 1, alpha, cur ? X.y0p : X.y1p,
+                                                 cur ? X.mk0 : X.mk1, smem, acc, bars, k, &La,
+                                                 cur ? X.lo_y0 : X.lo_y1, cur ? X.lo_m0 : X.lo_m1,
+                                                 cur ? X.hi_y0 : X.hi_y1, cur ? X.hi_m0 : X.hi_m1);
+        });
 }
 
 }  // namespace gpcg

@@ -42,6 +42,9 @@ if __name__ == "__main__":
         print(f"C1_OBSTACLE_A = {a:.4g}  (check: {active_fraction(P.c1_family(a=float(f'{a:.4g}'))):.4f})")
     if which in ("c3", "all"):
         nx = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+        lo = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-3      # optional bracket
+        hi = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
+        its = int(sys.argv[5]) if len(sys.argv) > 5 else 14
         print(f"C3: c such that |A(x*)|/n = 0.50 at {nx}x{nx}")
-        c = bisect(lambda c: P.c3_family(nx, nx, c=c), 1e-3, 1.0, 0.50, increasing=False)
+        c = bisect(lambda c: P.c3_family(nx, nx, c=c), lo, hi, 0.50, increasing=False, iters=its)
         print(f"C3_OBSTACLE_C = {c:.4g}  (check: {active_fraction(P.c3_family(nx, nx, c=float(f'{c:.4g}'))):.4f})")
