@@ -198,7 +198,8 @@ def c1() -> Problem:
 # C3: journal bearing with mesh-independent two-sided obstacles
 # --------------------------------------------------------------------------
 C3_X = 0.133            # max of the l=0 solution
-C3_OBSTACLE_C = 0.01514  # frozen by scripts/calibrate.py c3 400 (oracle solves only): 0.500 active
+C3_OBSTACLE_C = 0.01045  # frozen by scripts/calibrate.py c3 1600 (oracle solves only): 0.500 active at 1600^2
+                         # (round 1 froze 0.01514 at 400^2, which leaves only 43 % active at 8000^2)
 
 
 def c3_family(nx: int = 8000, ny: int = 8000, c: float = None, seed: int = 3,
