@@ -92,7 +92,10 @@ typedef struct {
                             path, P:680-683's "alternative technique"); 1: A_k extracted
                             as a compact CSR matrix each CG call, as the paper does with
                             PETSc -- the extraction ablation; one slab / rank;
-                            2: extract only for CSR / 3-D operators with |F| < 0.3 n      */
+                            3: A_k applied in place over the compacted free-row list (the
+                            CG and the reduced hessvec touch only the free rows; CSR / 3-D
+                            operators, one slab / rank); 2 (default): 3 for CSR / 3-D
+                            operators with |F| < 0.3 n on one slab and rank, else 0       */
 } gpcg_params;
 
 typedef struct {

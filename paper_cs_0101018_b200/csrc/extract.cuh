@@ -109,7 +109,7 @@ k_scan_assign(long long n, int rowlen, int pitch, const unsigned char* __restric
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         if (f[q]) {
-            idx[v[q]] = (int)run;
+            if (idx) idx[v[q]] = (int)run;
             pos[run] = (int)v[q];
             ++run;
         }

@@ -44,6 +44,7 @@
 #include "tile.cuh"
 #include "march_tma.cuh"
 #include "extract.cuh"
+#include "compact.cuh"
 #include "bjilu.cuh"
 #include "bjilu2.cuh"
 #include "march3.cuh"
@@ -203,6 +204,11 @@ struct Slab {
     double* xval = nullptr;
     double* xv[12] = {};                      // gF, dinvF, rho x2, q x2, s x2, p, w, (spare)
     unsigned char *xmask = nullptr, *xmaskcg = nullptr;
+    // compacted free-row list (compact.cuh; CSR / 3-D operators, one slab): rows of mask fmask
+    int* flist = nullptr;
+    long long *fblk = nullptr, *ftot = nullptr;
+    long long fcount = -1;
+    int fmask = -1;
     double* bjf = nullptr;                    // block-Jacobi ILU factor (precond 2 / 3): 5 x tiles x 32^2 doubles
                                               // + tiles x 32^2 code bytes
     CUtensorMap tbr;                          // r (RHO0) in 32 x 32 boxes for the BJ-ILU tile solves
@@ -506,6 +512,7 @@ void free_all(gpcg_problem* h) {
     for (Slab& S : h->slabs) {
         dfree(h, S.arena);
         for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, S.xarena, (void*)S.bjf, (void*)S.rp,
+                        (void*)S.flist, (void*)S.fblk, (void*)S.ftot,
                         (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             dfree(h, p);
@@ -1394,6 +1401,105 @@ int ensure_extract_buffers(gpcg_problem* h, Slab& S) {
     return GPCG_OK;
 }
 
+// ---------------------------------------------------------------- compacted free-row list (a4 (iii))
+// F of mask mk, in owned-point order, by the deterministic scans of extract.cuh; S.fcount = |F|
+// (read back: the callers synchronise anyway).
+int build_free_list(gpcg_problem* h, Slab& S, int mk) {
+    const long long n = S.rows * (long long)h->rowlen;
+    const long long nblk = (n + kScanBlock - 1) / kScanBlock;
+    if (!S.flist) {
+        CK(dalloc(h, &S.flist, (size_t)std::max<long long>(n, 1) * sizeof(int)));
+        CK(dalloc(h, &S.fblk, (size_t)(nblk + 1) * sizeof(long long)));
+        CK(dalloc(h, &S.ftot, sizeof(long long)));
+    }
+    k_scan_count<true><<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, S.m[mk], nullptr, S.fblk);
+    k_scan_blocks<<<1, 1024, 0, h->st>>>(nblk, S.fblk, S.ftot);
+    k_scan_assign<<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, S.m[mk], S.fblk, nullptr, S.flist);
+    CKLAUNCH();
+    h->launches += 3;
+    long long m = 0;
+    CK(cudaMemcpyAsync(&m, S.ftot, sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    S.fcount = m;
+    S.fmask = mk;
+    return GPCG_OK;
+}
+
+// the compact (free-row list) regime: CSR / 3-D operator, one slab on one rank, |F| < 0.3 n
+bool compact_ok(const gpcg_problem* h) { return !spec2d(h) && h->nslabs() == 1 && h->nranks == 1 && !h->deferred; }
+
+// CG on A_F applied in place over the free-row list (cg_mode 3, and cg_mode 2 for small free
+// sets): the C-G recurrences of k_cg_init / k_cg_iter on the free rows only; vectors full-length
+// (zero off F), no copy of A's values.  On return W holds w (zero off F).
+int run_cg_compact(gpcg_problem* h, int cur, double eta2, long long cap, long long* iters) {
+    if (!compact_ok(h))
+        return set_err(GPCG_EINVAL, "cg_mode = 3 (free-row list) supports CSR / 3-D operators on one slab and rank");
+    Slab& S = h->slabs[0];
+    CK(cudaEventRecord(h->ev_c0, h->st));
+    RC(build_free_list(h, S, cur));
+    const long long n = S.rows * (long long)h->rowlen;
+    const long long mm = S.fcount;
+    CK(cudaMemsetAsync(S.v[VW], 0, (size_t)n * sizeof(double), h->st));       // w = 0 off F
+    CK(cudaMemcpyAsync(S.m[MKCG], S.m[cur], (size_t)n, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaEventRecord(h->ev_c1, h->st));
+    CK(cudaEventSynchronize(h->ev_c1));
+    float ms_x = 0.f;
+    CK(cudaEventElapsedTime(&ms_x, h->ev_c0, h->ev_c1));
+    h->t_extract_ms += ms_x;
+    if (mm <= 0) { *iters = 0; return GPCG_OK; }
+    const int g = (int)std::max<long long>(1, std::min<long long>((mm + kThreads - 1) / kThreads, (long long)h->sms * 16));
+    const bool pc = h->prm.precond == 1;
+    const RedScratch R = h->red(0);
+    with_gop(h, S, [&](auto& op) {
+        using Op = std::decay_t<decltype(op)>;
+        if (pc)
+            k_cg_init_rows<Op, true><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.v[vg(cur)], S.m[MKCG], S.v[VRHO0],
+                                                                S.v[VQ0], S.v[VS0], S.v[VP], S.v[VW], S.v[VD], eta2,
+                                                                cap, h->dS, R);
+        else
+            k_cg_init_rows<Op, false><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.v[vg(cur)], S.m[MKCG], S.v[VRHO0],
+                                                                 S.v[VQ0], S.v[VS0], S.v[VP], S.v[VW], S.v[VD], eta2,
+                                                                 cap, h->dS, R);
+    });
+    CKLAUNCH();
+    h->launches++;
+    const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
+    for (;;) {
+        CK(cudaEventRecord(h->ev_c0, h->st));
+        for (int i = 0; i < chunk; ++i) {
+            const int a = i & 1, bb = a ^ 1;
+            with_gop(h, S, [&](auto& op) {
+                using Op = std::decay_t<decltype(op)>;
+                if (pc)
+                    k_cg_iter_rows<Op, true><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.m[MKCG], S.v[vrho(a)],
+                                                                        S.v[vq(a)], S.v[vs(a)], S.v[vrho(bb)],
+                                                                        S.v[vq(bb)], S.v[vs(bb)], S.v[VP], S.v[VW],
+                                                                        S.v[VD], h->dS, R);
+                else
+                    k_cg_iter_rows<Op, false><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.m[MKCG], S.v[vrho(a)],
+                                                                         S.v[vq(a)], S.v[vs(a)], S.v[vrho(bb)],
+                                                                         S.v[vq(bb)], S.v[vs(bb)], S.v[VP], S.v[VW],
+                                                                         S.v[VD], h->dS, R);
+            });
+        }
+        CKLAUNCH();
+        CK(cudaEventRecord(h->ev_c1, h->st));
+        h->launches += chunk;
+        RC(sync_scal(h));
+        if (h->hS->cg_done) break;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_c0, h->ev_c1));
+        h->t_cg_timed_ms += ms;
+        h->cg_iters_timed += chunk;
+        h->cg_free_iters_timed += chunk * mm;
+    }
+    *iters = h->hS->cg_it;
+    if (h->hS->cg_reason == CG_NOTSPD)
+        return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
+                       (long long)h->hS->cg_it);
+    return GPCG_OK;
+}
+
 int run_cg_extract(gpcg_problem* h, int cur, double eta2, long long cap, long long* iters) {
     if (h->nslabs() != 1 || h->nranks != 1 || h->deferred)
         return set_err(GPCG_EINVAL, "cg_mode = 1 (explicit extraction) supports one slab on one rank");
@@ -1652,9 +1758,9 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     if (h->prm.precond >= 2) return run_cg_bjilu(h, cur, m, eta2, cap, iters);
     // cg_mode 1: always extract; 2 (auto): extract for the generic kernels (CSR, 3-D) when the
     // free set is small (m < 0.3 n), where the compact system wins
-    if (h->prm.cg_mode == 1 ||
-        (h->prm.cg_mode == 2 && !spec2d(h) && !h->deferred && 10 * m < 3 * h->n_global))
-        return run_cg_extract(h, cur, eta2, cap, iters);
+    if (h->prm.cg_mode == 1) return run_cg_extract(h, cur, eta2, cap, iters);
+    if (h->prm.cg_mode == 3 || (h->prm.cg_mode == 2 && compact_ok(h) && 10 * m < 3 * h->n_global))
+        return run_cg_compact(h, cur, eta2, cap, iters);
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const RedScratch R = h->red(s);
@@ -2287,7 +2393,7 @@ gpcg_params gpcg_params_default(void) {
     p.cg_chunk = 32;
     p.gp_chunk = 8;
     p.precond = 0;
-    p.cg_mode = 0;
+    p.cg_mode = 2;      // in place; CSR / 3-D with |F| < 0.3 n over the compacted free-row list
     return p;
 }
 
@@ -2358,7 +2464,7 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
         return set_err(GPCG_EINVAL, "eta2_shrink in (0,1), eta2_floor > 0 required");
     if (p->gp_cap < 1 || p->refine_cap < 1 || p->max_halvings < 1 || p->max_halvings > 1000 || p->cg_cap < 0 ||
         p->search_k < 1 || p->search_k > kMaxK || p->cg_chunk < 1 || p->cg_chunk > 4096 || p->gp_chunk < 1 ||
-        p->gp_chunk > 256 || p->precond < 0 || p->precond > 3 || (p->cg_mode < 0 || p->cg_mode > 2))
+        p->gp_chunk > 256 || p->precond < 0 || p->precond > 3 || (p->cg_mode < 0 || p->cg_mode > 3))
         return set_err(GPCG_EINVAL, "integer parameter out of range");
     const int old_chunk = h->prm.cg_chunk, old_pc = h->prm.precond;
     h->prm = *p;
@@ -2385,6 +2491,7 @@ int gpcg_project(gpcg_problem* h, const double* x, double* px, double* pg_norm2,
     RC(download_vec(h, px, VY0));
     RC(sync_scal(h));
     h->free_mask = 0;
+    if (compact_ok(h)) RC(build_free_list(h, h->slabs[0], 0));
     if (pg_norm2) *pg_norm2 = h->hS->pg2;
     if (n_active) *n_active = (int64_t)h->hS->n_active;
     if (n_active_nonbinding) *n_active_nonbinding = (int64_t)h->hS->n_nonbinding;
@@ -2416,7 +2523,21 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
         };
         // broadcast-face 2-D stencils: the TMA-fed march (needs a 16-byte aligned input for its map)
         const bool k4 = h->tile && !h->generic && (reinterpret_cast<uintptr_t>(vin) & 15) == 0;
-        if (k4) {
+        // CSR / 3-D with a small free set: only the free rows (compacted list of the recorded set)
+        const long long nown = S.rows * (long long)h->rowlen;
+        const bool rows = reduced && compact_ok(h) && S.fmask == h->free_mask && S.fcount >= 0 &&
+                          10 * S.fcount < 3 * nown && h->prm.cg_mode != 0;
+        if (rows) {
+            CK(cudaMemsetAsync(yout, 0, (size_t)nown * sizeof(double), h->st));
+            if (S.fcount > 0) {
+                const int g = (int)std::max<long long>(
+                    1, std::min<long long>((S.fcount + kThreads - 1) / kThreads, (long long)h->sms * 16));
+                with_gop(h, S, [&](auto& op) {
+                    using Op = std::decay_t<decltype(op)>;
+                    k_hessvec_rows<Op><<<g, kThreads, 0, h->st>>>(op, S.fcount, S.flist, mask, vin, yout);
+                });
+            }
+        } else if (k4) {
             CUtensorMap mv;
             if (vin == S.v[VIN]) mv = S.t4[VIN];
             else RC(make_map(h, S, &mv, vin, false, m4::kBW, m4::kBR));
@@ -2618,6 +2739,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
         RC(launch_objective(h, vy(cur)));
         RC(sync_scal(h));
         h->free_mask = cur;
+        if (compact_ok(h)) RC(build_free_list(h, h->slabs[0], cur));
         st.q = 0.5 * S.r0 - S.r1 + h->c;
         st.pg_norm = std::sqrt(pg2);
         st.n_active = (int64_t)na;

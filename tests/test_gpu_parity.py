@@ -783,3 +783,45 @@ def test_bjilu_rejected_for_csr(G):
         s.set_params(precond=2)
         rc, x, st = s.solve(prob.x0, -1e-10, allow_error=True)
     assert rc == G.EINVAL
+
+
+# ------------------------------------------------------------------ compacted free-row list
+COMPACT_CASES = {"c4_family_m16": lambda: P.c4_family(m=16), "c4_family_m24": lambda: P.c4_family(m=24),
+                 "c4s_family_16": lambda: P.c4_stencil_family(m=16), "dense8": lambda: dense_problem(8, 21)}
+
+
+@pytest.mark.parametrize("case", list(COMPACT_CASES))
+def test_compact_free_rows_solve_and_hessvec(G, oracle, case):
+    """cg_mode 3 (CG applied in place over the compacted free-row list) and the default (2)
+    reach the oracle's solution; the reduced HVP over the list equals ora_spmv_masked on the
+    recorded free set (the masked full-length kernel, cg_mode 0, beside it)."""
+    prob = COMPACT_CASES[case]()
+    tol = -1e-11
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    A = oracle.problem_csr(prob)
+    p = 2.0 * P.uniform(77, 1, prob.n) - 1.0
+    for mode in (3, 2, 0):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(cg_mode=mode)
+            rc, x, st = s.solve(prob.x0, tol)
+            yr = s.hessvec(p, reduced=True)
+        assert rc == 0 and rc_o == 0, (mode, rc, st)
+        assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+        assert np.max(np.abs(x - x_o)) <= 1e-7
+        free = (x > prob.l) & (x < prob.u)
+        spmv_close(yr, oracle.spmv_masked(A, free, p), abs_op(A, p * free))
+
+
+def test_compact_free_rows_same_cg_iterates(G):
+    """One CG call from the same point over the free-row list and over the masked full-length
+    vectors: the same recurrences on the same numbers -> the same w to rounding."""
+    prob = P.c4_family(m=24)
+    out = {}
+    for mode in (0, 3):
+        with G.Solver.from_problem(prob) as s:
+            s.set_params(cg_mode=mode, cg_cap=30, eta2=1e-10, refine_cap=1)
+            rc, x, st = s.solve(prob.x0, -1e-12, max_it=1)
+        out[mode] = (x, st)
+    (x0, st0), (x3, st3) = out[0], out[3]
+    assert st0["cg_iters"] == st3["cg_iters"] and st0["gp_iters"] == st3["gp_iters"]
+    assert np.max(np.abs(x0 - x3)) <= 1e-12 * np.max(np.abs(x0))
