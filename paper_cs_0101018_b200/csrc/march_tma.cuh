@@ -43,9 +43,6 @@ namespace gpcg {
 #define GPCG_LAZY_REFILL 0  // 1: lock-step band engine without the per-block CTA barrier -- the last warp
                             // done with a stage refills it (measured: no gain on C2 / C3)
 #endif
-#ifndef GPCG_GP_BRANCHFREE
-#define GPCG_GP_BRANCHFREE 0   // 1: spec_sweep6 sums without a per-row branch (weights 0 / 1): measured slower (C3 562 vs 541 us per GP step)
-#endif
 #ifndef GPCG_GP_NST
 #define GPCG_GP_NST 3       // pipeline stages of the g-free GP sweeps (k5 / k6_gp_loop; tuning: 3 stages
                             // and 3 CTAs per SM measured 3 % faster than 4 and 2 on C3)
@@ -1321,15 +1318,17 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
     const int c = 26 * wid + lane + 1;
     const bool out_lane = lane >= 3 && lane < 29;
     int gx = 0, moff = 0, y0 = 0, y1 = 0;
-    bool col_ok = false, east_bd = false;
+    bool col_ok = false;
     Op5<true> op;
-    double bcol = 0.0;
+    double bcol = 0.0, fe_bd = 0.0;               // b of the column; east boundary face weight (last column)
+    long long vrow = 0;                           // storage index of (gx, emitted row), advanced per row
+    int n_act = 0, n_chg = 0, n_nb = 0;           // the three set counts, as integers (exact)
     double y_m1 = 0.0, y_m2 = 0.0, l_r1 = 0.0, u_r1 = 0.0, b_r1 = 0.0;   // raw rows r-1, r-2
     double g_a = 0.0, yn_a = 0.0, l_a = 0.0, u_a = 0.0;                 // row r-2
     double s_a = 0.0, s_b = 0.0;                                        // s(r-2), s(r-3)
     double d_b = 0.0;                                                   // d(r-3)
     const uint32_t tx = L::kMP + m5::kUt;
-    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+    const int k = band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, tx);
@@ -1348,19 +1347,21 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             y0 = yb;
             y1 = ye;
             col_ok = gx >= 0 && gx < A.nx;
-            east_bd = gx == A.nx - 1;
             op.init(A, gx);
+            fe_bd = gx == A.nx - 1 ? op.fe : 0.0;
             if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
+            vrow = (long long)gx + (long long)A.pitch * (yb - (LAG + 1) - LAG);
             y_m1 = y_m2 = l_r1 = u_r1 = b_r1 = g_a = yn_a = l_a = u_a = s_a = s_b = d_b = 0.0;
         },
         [&](const unsigned char* st, int kk, int r) {
             const int q = kk * m5::kBW + c;
-            const bool rin = r >= A.rlo && r < A.rhi;
-            const bool in = col_ok && rin;
+            const bool in = col_ok && r >= A.rlo && r < A.rhi;
             const double yv = reinterpret_cast<const double*>(st + L::kY)[q];
-            const double bv = BB ? (rin ? bcol : 0.0) : reinterpret_cast<const double*>(st + L::kB)[q];
-            const double lv = in ? (SB ? Bd.lc : reinterpret_cast<const double*>(st + L::kL)[q]) : 0.0;
-            const double uv = in ? (SB ? Bd.uc : reinterpret_cast<const double*>(st + L::kU)[q]) : 0.0;
+            // b is not masked outside the grid rows: there y = l = u = 0, so yn = s = d = 0 whatever g is;
+            // array bounds need no mask either: the TMA unit zero-fills everything outside the tensor
+            const double bv = BB ? bcol : reinterpret_cast<const double*>(st + L::kB)[q];
+            const double lv = SB ? (in ? Bd.lc : 0.0) : reinterpret_cast<const double*>(st + L::kL)[q];
+            const double uv = SB ? (in ? Bd.uc : 0.0) : reinterpret_cast<const double*>(st + L::kU)[q];
             const double g1 = op.apply(A, r - 1, y_m1, y_m2, yv) - b_r1;     // g(r-1)
             const double yn1 = trial(y_m1, g1, -1.0, alpha, l_r1, u_r1);     // yn(r-1)
             const double s1 = yn1 - y_m1;                                     // s(r-1)
@@ -1369,63 +1370,30 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             const double d2 = pgrad(yn_a, gn2, l_a, u_a);                     // d(r-2)
             const double dw = __shfl_up_sync(0xffffffffu, d2, 1);             // d(r-2) one column west
             const int re = r - 2;
-            const bool emit = out_lane && col_ok && re >= y0 && re < y1;
-#if GPCG_GP_BRANCHFREE
-            // the sums without a branch (weight 0 / 1), so that the rows of a block can interleave;
-            // only the stores are predicated
-            {
-                const double wgt = emit ? 1.0 : 0.0;
-                const bool act = (yn_a == l_a) || (yn_a == u_a);
-                const unsigned char m = act ? 0 : 1;
-                const double ew = d2 - dw, es = d2 - d_b;
-                double e = op.fw * ew * ew;
-                e = fma(op.fs * es, es, e);
-                if (east_bd) e = fma(op.fe * d2, d2, e);                       // east boundary face
-                if (r - 1 >= A.rhi) e = fma(op.fn * d2, d2, e);                // north boundary face
-                const double dz = wgt * d2, gz = wgt * gn2, sz = wgt * s_a;
-                acc[0] = fma(dz, d2, acc[0]);
-                acc[1] = fma(gz, gn2, acc[1]);
-                acc[5] = fma(wgt, e, acc[5]);                                 // <d, A d>
-                acc[6] = fma(g_a, sz, acc[6]);                                // <g, s>(r-2)
-                acc[7] = fma(sz, as2, acc[7]);                                // <s, A s>(r-2)
-                const bool binding = (yn_a == l_a && gn2 >= 0.0) || (yn_a == u_a && gn2 <= 0.0);
-                const unsigned char mp = st[L::kMP + kk * m5::kMW + c + moff];
-                acc[2] += (emit && act) ? 1.0 : 0.0;
-                acc[3] += (emit && mp != m) ? 1.0 : 0.0;
-                acc[4] += (emit && act && !binding) ? 1.0 : 0.0;
-                if (emit) {
-                    const long long v = (long long)gx + (long long)A.pitch * re;
-                    y_out[v] = yn_a;
-                    mask_out[v] = m;
-                }
-            }
-            if (SL && emit) {
-                const bool act = (yn_a == l_a) || (yn_a == u_a);
-                const unsigned char m = act ? 0 : 1;
-                {
-#else
-            if (emit) {
-                const long long v = (long long)gx + (long long)A.pitch * re;
+            const long long v = vrow;
+            vrow += A.pitch;
+            if (out_lane && col_ok && re >= y0 && re < y1) {
                 y_out[v] = yn_a;
-                const bool act = (yn_a == l_a) || (yn_a == u_a);
+                const bool al = yn_a == l_a, au = yn_a == u_a;
+                const bool act = al || au;
                 const unsigned char m = act ? 0 : 1;
                 mask_out[v] = m;
+                // face form of <d, A d>: west and south faces, + the boundary faces of the last
+                // column / row (coefficient fe_bd, and fn on the last grid row)
                 const double ew = d2 - dw, es = d2 - d_b;
+                const double kb = fe_bd + ((r - 1 >= A.rhi) ? op.fn : 0.0);
                 double e = op.fw * ew * ew;
                 e = fma(op.fs * es, es, e);
-                if (east_bd) e = fma(op.fe * d2, d2, e);                       // east boundary face
-                if (r - 1 >= A.rhi) e = fma(op.fn * d2, d2, e);                // north boundary face
+                e = fma(kb * d2, d2, e);
                 acc[0] = fma(d2, d2, acc[0]);
                 acc[1] = fma(gn2, gn2, acc[1]);
-                acc[2] += act ? 1.0 : 0.0;
-                acc[3] += (st[L::kMP + kk * m5::kMW + c + moff] != m) ? 1.0 : 0.0;
-                const bool binding = (yn_a == l_a && gn2 >= 0.0) || (yn_a == u_a && gn2 <= 0.0);
-                acc[4] += (act && !binding) ? 1.0 : 0.0;
+                n_act += act ? 1 : 0;
+                n_chg += (st[L::kMP + kk * m5::kMW + c + moff] != m) ? 1 : 0;
+                const bool binding = (al && gn2 >= 0.0) || (au && gn2 <= 0.0);
+                n_nb += (act && !binding) ? 1 : 0;
                 acc[5] += e;                                                  // <d, A d>
                 acc[6] = fma(g_a, s_a, acc[6]);                               // <g, s>(r-2)
                 acc[7] = fma(s_a, as2, acc[7]);                               // <s, A s>(r-2)
-                {
-#endif
                 if (SL) {                                     // fused halo write (SlabLink)
                     if (re < SL->lo_ghost) {
                         const long long vl = (long long)gx + (long long)A.pitch * (SL->lo_rows + re);
@@ -1438,7 +1406,6 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
                         hi_m[vh] = m;
                     }
                 }
-                }
             }
             d_b = d2;
             s_b = s_a; s_a = s1;
@@ -1447,6 +1414,10 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             l_r1 = lv; u_r1 = uv; b_r1 = bv;
         },
         bars, k0, SL ? SL->bid : -1, SL ? SL->nb : -1);
+    acc[2] += (double)n_act;
+    acc[3] += (double)n_chg;
+    acc[4] += (double)n_nb;
+    return k;
 }
 
 #ifndef GPCG_GP_SPEC6
