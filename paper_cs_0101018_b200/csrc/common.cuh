@@ -191,12 +191,12 @@ __device__ __forceinline__ double trial(double y, double dir, double sgn, double
 }
 
 // Eq. proj-gradient; fixed variables give 0 (R16).
+// Branch-free: the component is 0 at a lower bound unless g < 0, at an upper bound unless
+// g > 0 (both at once for l = u: always 0), else g -- the same values as the case analysis.
 __device__ __forceinline__ double pgrad(double x, double g, double l, double u) {
     const bool al = (x == l), au = (x == u);
-    if (al && au) return 0.0;
-    if (al) return g < 0.0 ? g : 0.0;
-    if (au) return g > 0.0 ? g : 0.0;
-    return g;
+    const bool zero = (al && !(g < 0.0)) || (au && !(g > 0.0));
+    return zero ? 0.0 : g;
 }
 
 // ----------------------------------------------------------------------------

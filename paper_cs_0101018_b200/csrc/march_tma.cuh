@@ -39,10 +39,6 @@ namespace gpcg {
 #ifndef GPCG_CG_MINB
 #define GPCG_CG_MINB (16 / GPCG_M4_WARPS)   // CG sweep CTAs per SM the register budget is sized for
 #endif
-#ifndef GPCG_LAZY_REFILL
-#define GPCG_LAZY_REFILL 0  // 1: lock-step band engine without the per-block CTA barrier -- the last warp
-                            // done with a stage refills it (measured: no gain on C2 / C3)
-#endif
 #ifndef GPCG_GP_NST
 #define GPCG_GP_NST 3       // pipeline stages of the g-free GP sweeps (k5 / k6_gp_loop; tuning: 3 stages
                             // and 3 CTAs per SM measured 3 % faster than 4 and 2 on C3)
@@ -154,43 +150,47 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
     return k0 + nmine;
 }
 
-// Lock-step variant (kThreads = 4 warps): thread 0 issues the loads of block k + NST
-// after a CTA-wide barrier that retires block k.  Fewer threads per CTA (more CTAs per
-// SM at the register budget of the accept / search sweeps).
+// Lock-step variant: after the CTA barrier that retires block k, ONE lane issues the loads of
+// block k + NST into the freed stage.  The issuing warp rotates with k (warp k mod W), so the
+// refill work -- a few dozen instructions a block -- is spread over the warps instead of
+// putting warp 0 behind the others at every barrier, and the block to issue next is kept as a
+// cursor in shared memory (item, block, its x0 and first row), advanced without divisions.
 // bars: NST mbarriers (null: after the stages); k0 as in band_pipeline_ws (init at 0 only).
 template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
 __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
                                              Begin&& begin, Row&& row, uint64_t* bars = nullptr, int k0 = 0,
                                              int bid = -1, int nb = -1) {
     using namespace m4;
+    constexpr int NW = m4::kThreads / 32;
     if (bid < 0) { bid = blockIdx.x; nb = gridDim.x; }
     uint64_t* bar = bars ? bars : reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     const int nitems = G.nbands * G.nsegs;
     const int nblk = (G.seg + PRE + POST + kBR - 1) / kBR;
     int nmine = 0;
     for (int t = bid; t < nitems; t += nb) nmine += nblk;
-    auto issue = [&](int k) {                            // k: this sweep's local block index
-        const int i = k / nblk, b = k - i * nblk;
-        const int t = bid + i * nb;
+    __shared__ int cur[4];                               // next block to issue: item t, block b, x0, row
+    // issue the block at the cursor into the stage of local block index k; advance the cursor
+    auto issue_next = [&](int k, int& t, int& b, int& x0, int& yr) {
         if (t >= nitems) return;
         const int stage = (k0 + k) % NST;
-        const int x0 = (t % G.nbands) * OUT;
-        const int yr = (t / G.nbands) * G.seg - PRE + b * kBR;
         issue_loads(smem + stage * STAGE, x0, yr, &bar[stage]);
+        yr += kBR;
+        if (++b == nblk) {
+            b = 0;
+            t += nb;
+            x0 = (t % G.nbands) * OUT;
+            yr = (t / G.nbands) * G.seg - PRE;
+        }
     };
-#if GPCG_LAZY_REFILL
-    __shared__ unsigned int done_cnt[8];                 // warps done with each stage's current block
-#endif
     if (threadIdx.x == 0) {
         if (k0 == 0) {
             for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
             fence_mbar_init();
         }
-        for (int k = 0; k < NST; ++k) issue(k);
+        int t = bid, b = 0, x0 = (t % G.nbands) * OUT, yr = (t / G.nbands) * G.seg - PRE;
+        for (int k = 0; k < NST; ++k) issue_next(k, t, b, x0, yr);
+        cur[0] = t; cur[1] = b; cur[2] = x0; cur[3] = yr;
     }
-#if GPCG_LAZY_REFILL
-    if (threadIdx.x < NST) done_cnt[threadIdx.x] = 0;
-#endif
     __syncthreads();
     int k = 0;
     for (int t = bid; t < nitems; t += nb) {
@@ -204,31 +204,15 @@ __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned
             const int yr = y0 - PRE + b * kBR;
 #pragma unroll
             for (int kk = 0; kk < kBR; ++kk) row(st, kk, yr + kk);
-#if GPCG_LAZY_REFILL
-            // no CTA barrier: each warp counts itself done with the stage; the LAST warp to finish
-            // it refills it (block k + NST), so no warp ever waits for the others here
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) {
-                __threadfence_block();
-                if (atomicAdd(&done_cnt[stage], 1u) == (unsigned int)(m4::kThreads / 32) - 1) {
-                    done_cnt[stage] = 0;
-                    __threadfence_block();
-                    fence_proxy_async();
-                    issue(k + NST);
-                }
-            }
-#else
             __syncthreads();                              // every warp is done with this stage
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == (k % NW) * 32) {
                 fence_proxy_async();
-                issue(k + NST);
+                int ct = cur[0], cb = cur[1], cx = cur[2], cy = cur[3];
+                issue_next(k + NST, ct, cb, cx, cy);
+                cur[0] = ct; cur[1] = cb; cur[2] = cx; cur[3] = cy;
             }
-#endif
         }
     }
-#if GPCG_LAZY_REFILL
-    __syncthreads();                                      // stages free before the next sweep issues
-#endif
     return k0 + nmine;
 }
 
