@@ -105,42 +105,107 @@ k_bjilu2_factor(StencilOp A, const unsigned char* __restrict__ mask, Bj2Factor F
     }
 }
 
-// z = M^-1 r on one tile staged in T (natural layout), in place; returns this lane's part of r'z
+// z = M^-1 r on one tile staged in T (natural layout), in place; returns this lane's part of r'z.
+// The wavefront step t = i + 3 jl is run as groups G = t / 3 of three sub-steps s = t mod 3:
+// in group G lane i handles its single point jl = G - i / 3 at sub-step i mod 3, so the five
+// factor values it needs in a group are known in advance -- they are loaded kIlu2Pre groups
+// ahead (a register ring) and the recurrence waits on shared memory and shuffles only.
+constexpr int kIlu2Groups = 42;                    // (31 + 3 * 31) / 3 + 1
+constexpr int kIlu2Pre = 4;                        // groups of factor loads in flight
+struct F5 {
+    double a, b, c, d, e;
+};
+
 __device__ __forceinline__ double tile_solve_ilu2(const StencilOp& A, int x0, int y0, long long tb,
                                                   const Bj2Factor& F, double* __restrict__ z, double* T) {
     const int lane = threadIdx.x & 31;
+    const int i3 = lane / 3, sl = lane - 3 * i3;
+    // forward L y = r: values of the lane's point of group G (lS, lSE, lSEE, lW, 1/d)
+    auto ldf = [&](int G) {
+        const int jl = G - i3;
+        F5 v{0.0, 0.0, 0.0, 0.0, 0.0};
+        if (jl >= 0 && jl < kTile) {
+            const long long q = tb + jl * kTile + lane;
+            v.a = __ldg(F.lS + q); v.b = __ldg(F.lSE + q); v.c = __ldg(F.lSEE + q);
+            v.d = __ldg(F.lW + q); v.e = __ldg(F.dinv + q);
+        }
+        return v;
+    };
     double rz = 0.0;
+    F5 ring[kIlu2Pre];
+#pragma unroll
+    for (int d = 0; d < kIlu2Pre; ++d) ring[d] = ldf(d);
     __syncwarp();
-    for (int t = 0; t < kIlu2Steps; ++t) {
-        int jl;
-        if (ilu2_step(t, lane, jl)) {
-            const int q = jl * kTile + lane;
-            double y = T[q];
-            if (jl > 0) {
-                y = fma(-__ldg(F.lS + tb + q), T[q - kTile], y);
-                if (lane + 1 < kTile) y = fma(-__ldg(F.lSE + tb + q), T[q - kTile + 1], y);
-                if (lane + 2 < kTile) y = fma(-__ldg(F.lSEE + tb + q), T[q - kTile + 2], y);
+#pragma unroll 1
+    for (int G0 = 0; G0 < kIlu2Groups; G0 += kIlu2Pre) {
+#pragma unroll
+        for (int d = 0; d < kIlu2Pre; ++d) {
+            const int G = G0 + d;
+            const F5 f = ring[d];
+            ring[d] = ldf(G + kIlu2Pre);
+            const int jl = G - i3;
+            const bool act = jl >= 0 && jl < kTile;
+#pragma unroll
+            for (int s3 = 0; s3 < 3; ++s3) {
+                if (act && sl == s3) {
+                    const int q = jl * kTile + lane;
+                    double y = T[q];
+                    if (jl > 0) {
+                        y = fma(-f.a, T[q - kTile], y);
+                        if (lane + 1 < kTile) y = fma(-f.b, T[q - kTile + 1], y);
+                        if (lane + 2 < kTile) y = fma(-f.c, T[q - kTile + 2], y);
+                    }
+                    if (lane > 0) y = fma(-f.d, T[q - 1], y);
+                    T[q] = y;
+                    rz = fma(y * y, f.e, rz);
+                }
+                __syncwarp();
             }
-            if (lane > 0) y = fma(-__ldg(F.lW + tb + q), T[q - 1], y);
-            T[q] = y;
-            rz = fma(y * y, __ldg(F.dinv + tb + q), rz);
         }
-        __syncwarp();
     }
-    for (int t = kIlu2Steps - 1; t >= 0; --t) {
-        int jl;
-        if (ilu2_step(t, lane, jl)) {
-            const int q = jl * kTile + lane;
-            double s = 0.0;
-            if (lane + 1 < kTile) s = fma(__ldg(F.lW + tb + q + 1), T[q + 1], s);               // E
+    // backward: z_v = y_v / d_v - (l_{E,W} z_E + l_{N,S} z_N + l_{NW,SE} z_NW + l_{NWW,SEE} z_NWW)
+    auto ldb = [&](int G) {
+        const int jl = G - i3;
+        F5 v{0.0, 0.0, 0.0, 0.0, 0.0};
+        if (jl >= 0 && jl < kTile) {
+            const long long q = tb + jl * kTile + lane;
+            if (lane + 1 < kTile) v.a = __ldg(F.lW + q + 1);                    // E
             if (jl + 1 < kTile) {
-                s = fma(__ldg(F.lS + tb + q + kTile), T[q + kTile], s);                        // N
-                if (lane > 0) s = fma(__ldg(F.lSE + tb + q + kTile - 1), T[q + kTile - 1], s);  // NW
-                if (lane > 1) s = fma(__ldg(F.lSEE + tb + q + kTile - 2), T[q + kTile - 2], s); // NWW
+                v.b = __ldg(F.lS + q + kTile);                                  // N
+                if (lane > 0) v.c = __ldg(F.lSE + q + kTile - 1);               // NW
+                if (lane > 1) v.d = __ldg(F.lSEE + q + kTile - 2);              // NWW
             }
-            T[q] = fma(T[q], __ldg(F.dinv + tb + q), -s);
+            v.e = __ldg(F.dinv + q);
         }
-        __syncwarp();
+        return v;
+    };
+#pragma unroll
+    for (int d = 0; d < kIlu2Pre; ++d) ring[d] = ldb(kIlu2Groups - 1 - d);
+#pragma unroll 1
+    for (int G0 = kIlu2Groups - 1; G0 >= 0; G0 -= kIlu2Pre) {
+#pragma unroll
+        for (int d = 0; d < kIlu2Pre; ++d) {
+            const int G = G0 - d;
+            const F5 f = ring[d];
+            ring[d] = ldb(G - kIlu2Pre);
+            const int jl = G - i3;
+            const bool act = jl >= 0 && jl < kTile;
+#pragma unroll
+            for (int s3 = 2; s3 >= 0; --s3) {
+                if (act && sl == s3) {
+                    const int q = jl * kTile + lane;
+                    double sacc = 0.0;
+                    if (lane + 1 < kTile) sacc = fma(f.a, T[q + 1], sacc);
+                    if (jl + 1 < kTile) {
+                        sacc = fma(f.b, T[q + kTile], sacc);
+                        if (lane > 0) sacc = fma(f.c, T[q + kTile - 1], sacc);
+                        if (lane > 1) sacc = fma(f.d, T[q + kTile - 2], sacc);
+                    }
+                    T[q] = fma(T[q], f.e, -sacc);
+                }
+                __syncwarp();
+            }
+        }
     }
     const int i = x0 + lane;
 #pragma unroll 8

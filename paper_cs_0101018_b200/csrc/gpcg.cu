@@ -194,9 +194,11 @@ struct Slab {
     // w box of the CG iteration, 144-byte mask boxes
     CUtensorMap t4[NVEC];
     CUtensorMap t4wo;
+    CUtensorMap t4c[4];             // CG sweep per-warp boxes: rho0, rho1, p0 (Q0), p1 (Q1), 32 x 4
+    CUtensorMap t4cw;               // CG sweep per-warp w box, 28 x 4
     CUtensorMap t4m[NMSK];
     BandGeom bg_cg{}, bg_acc{}, bg_srch{};   // band x segment items sized to each kernel's residency
-    unsigned char* cgflags = nullptr;         // k_cg_block_flags of the running CG call (bg_cg geometry)
+    unsigned short* cgflags = nullptr;        // k_cg_block_flags of the running CG call (bg_cg geometry)
     // explicit extraction (cg_mode = 1): compact numbering, A_F in CSR, compact CG vectors
     void* xarena = nullptr;
     int *xidx = nullptr, *xpos = nullptr, *xcnt = nullptr, *xcol = nullptr;
@@ -272,6 +274,7 @@ struct gpcg_problem {
     bool cg_persistent = true;      // GPCG_CG_PERSIST=0: CG as graph chunks instead of k6_cg_loop
     bool gp_persistent = true;      // GPCG_GP_PERSIST=0: GP phase as graph chunks instead of k6_gp_loop
     bool cg_skip = true;            // GPCG_CG_SKIP=0: the CG sweep loads every block (no active-block skip)
+    bool cg_pw = false;             // CG sweep with per-warp boxes (large grids; GPCG_CG_PW=0/1 overrides)
     bool gp_spec = true;            // GPCG_GP_SPEC=0: no speculative h = 0 accept in k6_gp_loop
     int grid6_gp = 1;
     size_t smem6_gp = 0;
@@ -674,6 +677,11 @@ int setup_tile(gpcg_problem* h) {
         for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
             RC(make_map(h, S, &S.t4[id], S.v[id], false, m4::kBW, m4::kBR));
         RC(make_map(h, S, &S.t4wo, S.v[VW], false, m4::kOut, m4::kBR));
+        {
+            const int ids[4] = {VRHO0, VRHO1, VQ0, VQ1};
+            for (int i = 0; i < 4; ++i) RC(make_map(h, S, &S.t4c[i], S.v[ids[i]], false, m4cg::kPW, m4::kBR));
+            RC(make_map(h, S, &S.t4cw, S.v[VW], false, m4cg::kWW, m4::kBR));
+        }
         for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t4m[k], S.m[k], true, m4::kMW, m4::kBR));
         for (int id : {VY0, VY1, VW, VB, VL, VU, VIN})
             RC(make_map(h, S, &S.t5[id], S.v[id], false, m5::kBW, m4::kBR));
@@ -696,7 +704,7 @@ int setup_tile(gpcg_problem* h) {
              S.grid4_cg);
         {
             const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
-            CK(dalloc(h, &S.cgflags, (size_t)std::max<long long>(nf, 1)));
+            CK(dalloc(h, &S.cgflags, (size_t)std::max<long long>(nf, 1) * sizeof(unsigned short)));
         }
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
@@ -710,6 +718,14 @@ int setup_tile(gpcg_problem* h) {
     }
     h->tile = true;
     h->gfree = (h->tile_mask & 64) != 0;
+    {
+        // per-warp CG boxes pay off once the CG vectors (rho x2, p x2, w: 40 B per point) leave
+        // the 126 MB L2 (C3: 64M points); below that the band boxes' 3 TMA operations a block win
+        long long pts = 0;
+        for (const Slab& S : h->slabs) pts += (long long)S.rows * h->nx;
+        h->cg_pw = 40LL * pts > 256LL * 1024 * 1024;
+        if (const char* e = getenv("GPCG_CG_PW")) h->cg_pw = atoi(e) != 0;
+    }
     {
         // persistent GP phase: smem of the larger (accept) layout; grid within co-residency
         auto cfg = [&](auto sbt, auto bbt) {
@@ -1168,12 +1184,14 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
         if (use_k4) {
             if (pc)
                 k4_cg_iter<true><<<S.grid4_cg, m4::kThreadsWS, m4cg::kSmem, h->st>>>(
-                    S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
-                    h->dS, R, skip ? S.cgflags : nullptr);
+                    S.sop, S.bg_cg, h->cg_pw ? S.t4c[a] : S.t4[vrho(a)], h->cg_pw ? S.t4c[2 + a] : S.t4[vq(a)],
+                    h->cg_pw ? S.t4cw : S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
+                    h->dS, R, skip ? S.cgflags : nullptr, h->cg_pw ? 1 : 0);
             else
                 k4_cg_iter<false><<<S.grid4_cg, m4::kThreadsWS, m4cg::kSmem, h->st>>>(
-                    S.sop, S.bg_cg, S.t4[vrho(a)], S.t4[vq(a)], S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
-                    h->dS, R, skip ? S.cgflags : nullptr);
+                    S.sop, S.bg_cg, h->cg_pw ? S.t4c[a] : S.t4[vrho(a)], h->cg_pw ? S.t4c[2 + a] : S.t4[vq(a)],
+                    h->cg_pw ? S.t4cw : S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
+                    h->dS, R, skip ? S.cgflags : nullptr, h->cg_pw ? 1 : 0);
         } else if (use_tile) {
             k3_cg_iter<2><<<S.grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
                 S.sop, S.tg, S.tm[vrho(a)], S.tm[vq(a)], S.tmWc, S.tmm[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
@@ -1826,13 +1844,17 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
     if (h->cg_persistent && h->tile && (h->tile_mask & 8) && !h->deferred) {
         // one cooperative launch runs the whole CG call (k6_cg_loop)
         Slab& S = h->slabs[0];
-        const unsigned char* flags = h->cg_skip ? S.cgflags : nullptr;
+        const unsigned short* flags = h->cg_skip ? S.cgflags : nullptr;
         CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
         CK(cudaEventRecord(h->ev_c0, h->st));
-        void* args[] = {(void*)&S.sop, (void*)&S.bg_cg, (void*)&S.t4[VRHO0], (void*)&S.t4[VRHO1], (void*)&S.t4[VQ0],
-                        (void*)&S.t4[VQ1], (void*)&S.t4wo, (void*)&S.t4m[MKCG], (void*)&S.v[VRHO0],
+        const bool pw = h->cg_pw;
+        int pwi = pw ? 1 : 0;
+        void* args[] = {(void*)&S.sop, (void*)&S.bg_cg, (void*)(pw ? &S.t4c[0] : &S.t4[VRHO0]),
+                        (void*)(pw ? &S.t4c[1] : &S.t4[VRHO1]), (void*)(pw ? &S.t4c[2] : &S.t4[VQ0]),
+                        (void*)(pw ? &S.t4c[3] : &S.t4[VQ1]), (void*)(pw ? &S.t4cw : &S.t4wo), (void*)&S.t4m[MKCG],
+                        (void*)&S.v[VRHO0],
                         (void*)&S.v[VRHO1], (void*)&S.v[VQ0], (void*)&S.v[VQ1], (void*)&S.v[VW], (void*)&h->dS,
-                        (void*)&S.partials, (void*)&h->gbar, (void*)&flags};
+                        (void*)&S.partials, (void*)&h->gbar, (void*)&flags, (void*)&pwi};
         const void* fn = h->prm.precond == 1 ? (const void*)k6_cg_loop<true> : (const void*)k6_cg_loop<false>;
         CK(cudaLaunchCooperativeKernel(fn, dim3(S.grid4_cg), dim3(m4::kThreadsWS), args, (size_t)m4cg::kSmem, h->st));
         CK(cudaEventRecord(h->ev_c1, h->st));
@@ -1854,12 +1876,19 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
         CgMsArgs P;
         memset(&P, 0, sizeof P);
         P.nslabs = h->nslabs();
+        P.pw = h->cg_pw ? 1 : 0;
         int cta = 0;
         for (int s = 0; s < h->nslabs(); ++s) {
             Slab& S = h->slabs[s];
             CgMsSlab& X = P.s[s];
-            X.m_rho0 = S.t4[VRHO0]; X.m_rho1 = S.t4[VRHO1]; X.m_p0 = S.t4[VQ0]; X.m_p1 = S.t4[VQ1];
-            X.m_w = S.t4wo; X.m_mask = S.t4m[MKCG];
+            if (h->cg_pw) {
+                X.m_rho0 = S.t4c[0]; X.m_rho1 = S.t4c[1]; X.m_p0 = S.t4c[2]; X.m_p1 = S.t4c[3];
+                X.m_w = S.t4cw;
+            } else {
+                X.m_rho0 = S.t4[VRHO0]; X.m_rho1 = S.t4[VRHO1]; X.m_p0 = S.t4[VQ0]; X.m_p1 = S.t4[VQ1];
+                X.m_w = S.t4wo;
+            }
+            X.m_mask = S.t4m[MKCG];
             X.A = S.sop;
             X.G = S.bg_cg;
             X.rho0 = S.v[VRHO0]; X.rho1 = S.v[VRHO1]; X.p0 = S.v[VQ0]; X.p1 = S.v[VQ1]; X.w = S.v[VW];

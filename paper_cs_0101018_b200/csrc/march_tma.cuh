@@ -85,15 +85,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // k0: blocks this CTA already streamed through the same barriers (a persistent kernel
 // calls the engine once per sweep; the mbarriers are initialised at k0 = 0 only and
 // their phases continue).  Returns the CTA's block count after the sweep.
-// flags (nullable): one byte per (item, block) -- bit 0: the block's raw rows hold a free
-// point, bit 1: its emitted rows do -- passed to issue_loads so that all-active blocks skip
-// the loads their rows never read (3 = load everything).
-// bid / nb (>= 0): this CTA's index and the CTA count among the CTAs sharing G (a persistent
-// kernel spanning several slabs gives each slab its own range of CTAs); default the grid's.
+// flags (nullable): 16 bits per (item, block) -- bit w: the block's raw rows hold a free point
+// in consumer warp w's input columns, bit 8 + w: its emitted rows do in warp w's output columns
+// -- passed to issue_loads so that warps whose rows are all active skip the loads they never
+// read (0xffff = load everything).  Every lane of the producer warp calls issue_loads.
 template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
 __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
                                                 Begin&& begin, Row&& row, int k0 = 0,
-                                                const unsigned char* __restrict__ flags = nullptr, int bid = -1,
+                                                const unsigned short* __restrict__ flags = nullptr, int bid = -1,
                                                 int nb = -1) {
     using namespace m4;
     if (bid < 0) { bid = blockIdx.x; nb = gridDim.x; }
@@ -114,18 +113,19 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
         __syncthreads();
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == kWarps) {                                 // producer (lane 0 issues; the warp fetches flags)
+    if (warp == kWarps) {                                 // producer (the warp fetches flags, issues loads)
         int k = k0;
         for (int t = bid; t < nitems; t += nb) {
             const int x0 = (t % G.nbands) * OUT;
             const int yb = (t / G.nbands) * G.seg - PRE;
-            int f = 3;
+            int f = 0xffff;
             for (int b = 0; b < nblk; ++b, ++k) {
-                if (flags && (b & 31) == 0) f = (b + lane < nblk) ? __ldg(flags + (long long)t * nblk + b + lane) : 3;
-                const int fb = flags ? __shfl_sync(0xffffffffu, f, b & 31) : 3;
+                if (flags && (b & 31) == 0)
+                    f = (b + lane < nblk) ? __ldg(flags + (long long)t * nblk + b + lane) : 0xffff;
+                const int fb = flags ? __shfl_sync(0xffffffffu, f, b & 31) : 0xffff;
                 const int stage = k % NST;
                 if (k >= NST) mbar_wait(&empty[stage], ((k / NST) - 1) & 1);
-                if (lane == 0) issue_loads(smem + stage * STAGE, x0, yb + b * kBR, &full[stage], fb);
+                issue_loads(smem + stage * STAGE, x0, yb + b * kBR, &full[stage], fb);
                 __syncwarp();
             }
         }
@@ -238,13 +238,27 @@ struct SlabLink {
 //            gamma += rn^2, delta += rn q
 // Stage: rho | p (band boxes, rows yr..) | w (output columns, rows yr-2..) | mask (rows yr..)
 // ============================================================================
+// Two stage layouts (a run-time choice, `pw`): band boxes (one 228-column box per array and
+// block: 3 TMA operations a block, best when the vectors stay in L2, C2) or per-warp boxes
+// (warp w's rho / p box holds its 32 input columns, 28 outputs + 2 halo each side, its w box
+// its 28 output columns), so that a warp whose rows hold no free point skips its loads (the
+// band's other warps still load theirs): fewer DRAM bytes on large grids with large active
+// regions (C3), 8x the TMA operations.
 namespace m4cg {
 using namespace m4;
-constexpr int kRho = 0, kP = kF, kW = 2 * kF, kM = 2 * kF + kFo;
-constexpr int kStage = kM + kU;
-constexpr int kTx = kM + kUt;                         // bytes the TMA delivers per stage
+// band layout
+constexpr int kRhoB = 0, kPB = kF, kWBd = 2 * kF, kMB = 2 * kF + kFo;
+// per-warp layout
+constexpr int kPW = 32, kWW = 28;                     // per-warp rho / p and w box columns
+constexpr int kFW = kBR * kPW * 8;                    // one per-warp rho / p box (1 KB)
+constexpr int kWB = kBR * kWW * 8;                    // one per-warp w box (896 B)
+constexpr int kRho = 0, kP = kWarps * kFW, kW = 2 * kWarps * kFW;
+constexpr int kM = r128(kW + kWarps * kWB);
+constexpr int kStage = (kM > kMB ? kM : kMB) + kU;
 constexpr int kNST = GPCG_CG_NST;
 constexpr int kSmem = kNST * kStage + 64;
+static_assert(kFW % 128 == 0 && kWB % 128 == 0 && kW % 128 == 0 && kMB % 128 == 0,
+              "TMA destinations stay 128-byte aligned");
 }  // namespace m4cg
 
 // One CG sweep on this CTA's items: rho_n, p_n, w written for the free points; acc = this
@@ -254,7 +268,7 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
                                          const CUtensorMap* m_p, const CUtensorMap* m_w, const CUtensorMap* m_mask,
                                          double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out,
                                          double alpha, double beta, unsigned char* smem, double (&acc)[2], int k0,
-                                         const unsigned char* __restrict__ flags = nullptr,
+                                         const unsigned short* __restrict__ flags = nullptr, bool pw = false,
                                          const SlabLink* L = nullptr, double* lo_rho = nullptr, double* lo_p = nullptr,
                                          double* hi_rho = nullptr, double* hi_p = nullptr) {
     using namespace m4cg;
@@ -269,15 +283,36 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
     return band_pipeline_ws<kNST, kStage>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar, int fb) {
-            // rho / p are read only at free points of the raw rows, w only at free emitted rows:
-            // blocks without any (flags bit 0 / bit 1) skip those loads (stale smem is never read)
-            mbar_expect_tx(bar, kUt + ((fb & 1) ? 2 * kF : 0) + ((fb & 2) ? kFo : 0));
-            if (fb & 1) {
-                tma_load_2d(st + kRho, m_rho, x0 - 2, yr - G.rlo, bar);
-                tma_load_2d(st + kP, m_p, x0 - 2, yr - G.rlo, bar);
+            // (every producer lane) rho / p are read only at free points of the raw rows, w only
+            // at free emitted rows: per warp strip, boxes without any (flags bits w / 8 + w)
+            // are skipped (stale smem is never read: every use is masked)
+            const int plane = threadIdx.x & 31;
+            const unsigned fd = fb & 0xff, fw = (fb >> 8) & 0xff;
+            if (!pw) {                                        // band boxes, one lane
+                if (plane == 0) {
+                    mbar_expect_tx(bar, kUt + (fd ? 2 * kF : 0) + (fw ? kFo : 0));
+                    if (fd) {
+                        tma_load_2d(st + kRhoB, m_rho, x0 - 2, yr - G.rlo, bar);
+                        tma_load_2d(st + kPB, m_p, x0 - 2, yr - G.rlo, bar);
+                    }
+                    if (fw) tma_load_2d(st + kWBd, m_w, x0, yr - 2 - G.rlo, bar);
+                    tma_load_2d(st + kMB, m_mask, floor16(x0 - 2), yr - G.rlo, bar);
+                }
+                return;
             }
-            if (fb & 2) tma_load_2d(st + kW, m_w, x0, yr - 2 - G.rlo, bar);      // w of the emitted rows (r - 2)
-            tma_load_2d(st + kM, m_mask, floor16(x0 - 2), yr - G.rlo, bar);
+            if (plane == 0) mbar_expect_tx(bar, kUt + __popc(fd) * 2 * kFW + __popc(fw) * kWB);
+            __syncwarp();
+            if (plane < kWarps) {
+                if ((fd >> plane) & 1) {
+                    tma_load_2d(st + kRho + plane * kFW, m_rho, x0 - 2 + 28 * plane, yr - G.rlo, bar);
+                    tma_load_2d(st + kP + plane * kFW, m_p, x0 - 2 + 28 * plane, yr - G.rlo, bar);
+                }
+            } else if (plane < 2 * kWarps) {
+                const int w = plane - kWarps;                 // w of the emitted rows (r - 2)
+                if ((fw >> w) & 1) tma_load_2d(st + kW + w * kWB, m_w, x0 + 28 * w, yr - 2 - G.rlo, bar);
+            } else if (plane == 2 * kWarps) {
+                tma_load_2d(st + kM, m_mask, floor16(x0 - 2), yr - G.rlo, bar);
+            }
         },
         [&](int x0, int yb, int ye) {
             gx = x0 - 2 + c;
@@ -291,12 +326,12 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
             m_m1 = m_m2 = 0;
         },
         [&](const unsigned char* st, int kk, int r) {
-            const double* rhoS = reinterpret_cast<const double*>(st + kRho);
-            const double* pS = reinterpret_cast<const double*>(st + kP);
-            const double* wS = reinterpret_cast<const double*>(st + kW);
-            const unsigned char m = st[kM + kk * kMW + c + moff];
-            const double rho = rhoS[kk * kBW + c];
-            const double pn0 = m ? fma(beta, pS[kk * kBW + c], PC ? rho * dinv : rho) : 0.0;
+            const double* rhoS = reinterpret_cast<const double*>(st + (pw ? kRho + wid * kFW : kRhoB));
+            const double* pS = reinterpret_cast<const double*>(st + (pw ? kP + wid * kFW : kPB));
+            const int qi = pw ? kk * kPW + lane : kk * kBW + c;
+            const unsigned char m = st[(pw ? kM : kMB) + kk * kMW + c + moff];
+            const double rho = m ? rhoS[qi] : 0.0;
+            const double pn0 = m ? fma(beta, pS[qi], PC ? rho * dinv : rho) : 0.0;
             const double ap = op.apply(A, r - 1, pn_m1, pn_m2, pn0);
             const double rr1 = m_m1 ? fma(-alpha, ap, rho_m1) : 0.0;
             const double rn1 = PC ? rr1 * dinv : rr1;
@@ -305,7 +340,8 @@ __device__ __forceinline__ int cg_sweep4(const StencilOp& A, const BandGeom& G, 
             const double rres = PC ? rr_m2 : rn_m2;
             if (out_lane && m_m2 && col_ok && r2 >= y0 && r2 < y1) {
                 const long long v = (long long)gx + (long long)A.pitch * r2;
-                w_out[v] = fma(alpha, pn_m2, wS[kk * kOut + c - 2]);
+                const double* wS = reinterpret_cast<const double*>(st + (pw ? kW + wid * kWB : kWBd));
+                w_out[v] = fma(alpha, pn_m2, wS[pw ? kk * kWW + lane - 2 : kk * kOut + c - 2]);
                 rho_n[v] = rres;
                 p_n[v] = pn_m2;
                 acc[0] = fma(rres, rn_m2, acc[0]);
@@ -362,6 +398,7 @@ k4_hessvec(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_v, con
     band_pipeline_ws<kNST, kStage, kOut, 1, 1>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar, int) {
+            if ((threadIdx.x & 31) != 0) return;          // one producer lane issues
             mbar_expect_tx(bar, kF + (RED ? kUt : 0));
             tma_load_2d(st + kV, &m_v, x0 - 2, yr - G.rlo, bar);
             if (RED) tma_load_2d(st + kM, &m_mask, floor16(x0 - 2), yr - G.rlo, bar);
@@ -389,11 +426,12 @@ k4_hessvec(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_v, con
         });
 }
 
-// Block flags of the CG sweep geometry G for the fixed CG mask: bit 0 if rows [yr, yr+4) of
-// the block's box columns [x0-2, x0+114) hold a free point, bit 1 if rows [yr-2, yr+2) of its
-// output columns [x0, x0+112) do.  One warp per (item, block); lanes stride the columns.
+// Block flags of the CG sweep geometry G for the fixed CG mask, 16 bits per (item, block):
+// bit w if rows [yr, yr+4) of consumer warp w's input columns [x0 + 28 w - 2, x0 + 28 w + 30)
+// hold a free point, bit 8 + w if rows [yr-2, yr+2) of its output columns [x0 + 28 w,
+// x0 + 28 w + 28) do.  One warp per (item, block); lanes stride the columns.
 __global__ void k_cg_block_flags(int nx, int pitch, BandGeom G, const unsigned char* __restrict__ mask, int rhi,
-                                 unsigned char* __restrict__ flags) {
+                                 unsigned short* __restrict__ flags) {
     using namespace m4;
     const int nblk = (G.seg + 4 + kBR - 1) / kBR;
     const long long total = (long long)G.nbands * G.nsegs * nblk;
@@ -404,7 +442,7 @@ __global__ void k_cg_block_flags(int nx, int pitch, BandGeom G, const unsigned c
         const int t = (int)(q / nblk), b = (int)(q - (long long)t * nblk);
         const int x0 = (t % G.nbands) * kOut;
         const int yr = (t / G.nbands) * G.seg - 2 + b * kBR;
-        int fd = 0, fw = 0;
+        unsigned int bits = 0;
         // all the block's mask bytes are independent loads: unrolled so they are in flight together
 #pragma unroll
         for (int rr = 0; rr < kBR + 2; ++rr) {
@@ -413,15 +451,19 @@ __global__ void k_cg_block_flags(int nx, int pitch, BandGeom G, const unsigned c
             const unsigned char* row = mask + (long long)r * pitch;
 #pragma unroll
             for (int cc = 0; cc < (kOut + 4 + 31) / 32; ++cc) {
-                const int c = x0 - 2 + lane + 32 * cc;
-                if (c >= x0 + kOut + 2 || c < 0 || c >= nx || !row[c]) continue;
-                if (r >= yr) fd = 1;
-                if (r < yr + kBR - 2 && c >= x0 && c < x0 + kOut) fw = 1;
+                const int o = lane + 32 * cc - 2;             // column offset from x0: -2 .. kOut + 1
+                const int c = x0 + o;
+                if (o >= kOut + 2 || c < 0 || c >= nx || !row[c]) continue;
+                if (r >= yr) {                                // raw rows: input strips holding o
+                    const int ws = (o + 2) / 28;
+                    if (ws < kWarps) bits |= 1u << ws;
+                    if (ws >= 1 && o < 28 * ws + 2) bits |= 1u << (ws - 1);
+                }
+                if (r < yr + kBR - 2 && o >= 0 && o < kOut) bits |= 1u << (8 + o / 28);   // emitted rows
             }
         }
-        fd = __any_sync(0xffffffffu, fd);
-        fw = __any_sync(0xffffffffu, fw);
-        if (lane == 0) flags[q] = (unsigned char)(fd | (fw << 1));
+        bits = __reduce_or_sync(0xffffffffu, bits);
+        if (lane == 0) flags[q] = (unsigned short)bits;
     }
 }
 
@@ -430,12 +472,12 @@ __global__ void __launch_bounds__(m4::kThreadsWS, GPCG_CG_MINB)
 k4_cg_iter(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho, const __grid_constant__ CUtensorMap m_p,
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
            double* __restrict__ rho_n, double* __restrict__ p_n, double* __restrict__ w_out, Scal* S, RedScratch R,
-           const unsigned char* __restrict__ flags) {
+           const unsigned short* __restrict__ flags, int pw) {
     if (*(volatile int*)&S->cg_done) return;
     const double alpha = S->cg_alpha, beta = S->cg_beta;
     extern __shared__ __align__(128) unsigned char smem[];
     double acc[2] = {0.0, 0.0};
-    cg_sweep4<PC>(A, G, &m_rho, &m_p, &m_w, &m_mask, rho_n, p_n, w_out, alpha, beta, smem, acc, 0, flags);
+    cg_sweep4<PC>(A, G, &m_rho, &m_p, &m_w, &m_mask, rho_n, p_n, w_out, alpha, beta, smem, acc, 0, flags, pw != 0);
     reduce_and_finish<2>(acc, R, [&](double* tt) { cg_finalize(tt[0], tt[1], S); });
 }
 
@@ -540,11 +582,11 @@ k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, 
            const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_mask,
            double* __restrict__ rho0, double* __restrict__ rho1, double* __restrict__ p0, double* __restrict__ p1,
            double* __restrict__ w_out, Scal* S, double* __restrict__ part, unsigned int* gbar,
-           const unsigned char* __restrict__ flags) {
+           const unsigned short* __restrict__ flags, int pw) {
     extern __shared__ __align__(128) unsigned char smem[];
     cg_loop(S, part, gbar, [&](int a, double alpha, double beta, double (&acc)[2], int k) {
         return cg_sweep4<PC>(A, G, a ? &m_rho1 : &m_rho0, a ? &m_p1 : &m_p0, &m_w, &m_mask, a ? rho0 : rho1,
-                             a ? p0 : p1, w_out, alpha, beta, smem, acc, k, flags);
+                             a ? p0 : p1, w_out, alpha, beta, smem, acc, k, flags, pw != 0);
     });
 }
 
@@ -557,7 +599,7 @@ struct CgMsSlab {
     StencilOp A;
     BandGeom G;
     double *rho0, *rho1, *p0, *p1, *w;
-    const unsigned char* flags;
+    const unsigned short* flags;
     double *lo_rho0, *lo_rho1, *lo_p0, *lo_p1;    // lower neighbour's origins (slab s - 1)
     double *hi_rho0, *hi_rho1, *hi_p0, *hi_p1;    // upper neighbour's origins (slab s + 1)
     SlabLink L;                                   // bid is set in the kernel
@@ -566,6 +608,7 @@ struct CgMsSlab {
 struct CgMsArgs {
     CgMsSlab s[kMaxMs];
     int nslabs;
+    int pw;                                       // per-warp boxes (cg_sweep4)
 };
 
 template <bool PC>
@@ -579,7 +622,8 @@ k6_cg_loop_ms(const __grid_constant__ CgMsArgs P, Scal* S, double* __restrict__ 
     L.bid = (int)blockIdx.x - X.cta0;
     cg_loop(S, part, gbar, [&](int a, double alpha, double beta, double (&acc)[2], int k) {
         return cg_sweep4<PC>(X.A, X.G, a ? &X.m_rho1 : &X.m_rho0, a ? &X.m_p1 : &X.m_p0, &X.m_w, &X.m_mask,
-                             a ? X.rho0 : X.rho1, a ? X.p0 : X.p1, X.w, alpha, beta, smem, acc, k, X.flags, &L,
+                             a ? X.rho0 : X.rho1, a ? X.p0 : X.p1, X.w, alpha, beta, smem, acc, k, X.flags,
+                             P.pw != 0, &L,
                              a ? X.lo_rho0 : X.lo_rho1, a ? X.lo_p0 : X.lo_p1, a ? X.hi_rho0 : X.hi_rho1,
                              a ? X.hi_p0 : X.hi_p1);
     });

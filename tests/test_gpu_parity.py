@@ -825,3 +825,32 @@ def test_compact_free_rows_same_cg_iterates(G):
     (x0, st0), (x3, st3) = out[0], out[3]
     assert st0["cg_iters"] == st3["cg_iters"] and st0["gp_iters"] == st3["gp_iters"]
     assert np.max(np.abs(x0 - x3)) <= 1e-12 * np.max(np.abs(x0))
+
+
+# ------------------------------------------------------------------ CG sweep stage layouts (band / per-warp boxes)
+@pytest.mark.parametrize("pw", ["0", "1"])
+@pytest.mark.parametrize("case", ["C0", "jb80_eps0.9", "c3_family_160"])
+def test_cg_sweep_box_layouts(G, oracle, monkeypatch, case, pw):
+    """The persistent CG sweep with band boxes and with per-warp boxes (+ per-warp skip flags;
+    the default for grids whose CG vectors exceed L2): same solution as the oracle, and the
+    same CG iterates as each other from the same point."""
+    monkeypatch.setenv("GPCG_CG_PW", pw)
+    make, tol = SOLVE_CASES[case]
+    prob = make()
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    with G.Solver.from_problem(prob) as s:
+        rc, x, st = s.solve(prob.x0, tol)
+    assert rc == 0 and rc_o == 0, (rc, st)
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
+    for slabs in (1, 2):
+        with G.Solver.from_problem(prob, slabs=slabs) as s:
+            s.set_params(cg_cap=25, eta2=1e-10, refine_cap=1)
+            rc1, x1, st1 = s.solve(prob.x0, tol, max_it=1)
+        monkeypatch.setenv("GPCG_CG_PW", "1" if pw == "0" else "0")
+        with G.Solver.from_problem(prob, slabs=slabs) as s:
+            s.set_params(cg_cap=25, eta2=1e-10, refine_cap=1)
+            rc2, x2, st2 = s.solve(prob.x0, tol, max_it=1)
+        monkeypatch.setenv("GPCG_CG_PW", pw)
+        assert st1["cg_iters"] == st2["cg_iters"]
+        assert np.array_equal(x1, x2)
