@@ -25,7 +25,7 @@
 
 #include "common.cuh"
 #include "fin.cuh"
-#include "tile.cuh"
+#include "tma.cuh"
 
 namespace gpcg {
 

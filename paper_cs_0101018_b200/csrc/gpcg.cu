@@ -41,7 +41,7 @@
 #include "fin.cuh"
 #include "kernels.cuh"
 #include "march.cuh"
-#include "tile.cuh"
+#include "tma.cuh"
 #include "march_tma.cuh"
 #include "extract.cuh"
 #include "compact.cuh"
@@ -185,11 +185,6 @@ struct Slab {
     MarchGeom mg1{}, mg2{};
     int grid_m1 = 1, grid_m2 = 1, grid = 1;
     int grid7 = 1;                            // 3-D plane-march kernels (march3.cuh)
-    TileGeom tg{};
-    int grid_t_cg = 1, grid_t_acc = 1, grid_t_srch = 1;
-    CUtensorMap tm[NVEC];
-    CUtensorMap tmm[NMSK];
-    CUtensorMap tmWc;               // w, centre box (CG)
     // TMA-fed column march (k4_*): 116-column band boxes of the vectors, the 112-column
     // w box of the CG iteration, 144-byte mask boxes
     CUtensorMap t4[NVEC];
@@ -588,13 +583,6 @@ int set_smem(K kernel, int bytes) {
 
 // TMA tile path for a broadcast-face stencil (C0/C2/C3 family)
 int setup_tile(gpcg_problem* h) {
-    RC(set_smem(k3_cg_iter<2>, CgStage<2>::kSmem));
-    RC(set_smem(k3_accept<true>, AccStage<true>::kSmem));
-    RC(set_smem(k3_accept<false>, AccStage<false>::kSmem));
-    RC(set_smem(k3_search<true, true>, SrchStage<true, true>::kSmem));
-    RC(set_smem(k3_search<true, false>, SrchStage<true, false>::kSmem));
-    RC(set_smem(k3_search<false, true>, SrchStage<false, true>::kSmem));
-    RC(set_smem(k3_search<false, false>, SrchStage<false, false>::kSmem));
     RC(set_smem(k4_hessvec<true>, m4hv::kSmem));
     RC(set_smem(k4_hessvec<false>, m4hv::kSmem));
     RC(set_smem(k4_cg_iter<false>, m4cg::kSmem));
@@ -629,16 +617,6 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k4_search<true, false>, SrchLayout4<true, false>::kSmem));
     RC(set_smem(k4_search<false, true>, SrchLayout4<false, true>::kSmem));
     RC(set_smem(k4_search<false, false>, SrchLayout4<false, false>::kSmem));
-    auto resident = [&](auto kernel, int smem) {
-        int nb = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kTileThreads, smem);
-        return std::max(1, nb) * h->sms;
-    };
-    const int r_cg = resident(k3_cg_iter<2>, CgStage<2>::kSmem);
-    const int r_acc = h->sb ? resident(k3_accept<true>, AccStage<true>::kSmem)
-                            : resident(k3_accept<false>, AccStage<false>::kSmem);
-    const int r_srch = h->sb ? resident(k3_search<true, true>, SrchStage<true, true>::kSmem)
-                             : resident(k3_search<false, true>, SrchStage<false, true>::kSmem);
     auto res4 = [&](auto kernel, int smem) {
         int nb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, m4::kThreads, smem);
@@ -666,13 +644,6 @@ int setup_tile(gpcg_problem* h) {
         else { if (h->bb) pick(std::false_type(), std::true_type()); else pick(std::false_type(), std::false_type()); }
     }
     for (Slab& S : h->slabs) {
-        for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
-            RC(make_map(h, S, &S.tm[id], S.v[id], false, TBW, TBH));
-        for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.tmm[k], S.m[k], true, MBW, TBH));
-        RC(make_map(h, S, &S.tmWc, S.v[VW], false, TOX, TOY));
-        S.tg = TileGeom{h->nx, S.rows, h->pitch, (h->nx + TOX - 1) / TOX, (S.rows + TOY - 1) / TOY, -S.glo,
-                        S.rows + S.ghi};
-        const int ntiles = S.tg.ntx * S.tg.nty;
         // k4: bands of 112 columns, each split into nsegs row segments: one item per resident CTA
         for (int id : {VY0, VY1, VG0, VG1, VRHO0, VRHO1, VQ0, VQ1, VW, VB, VL, VU, VIN})
             RC(make_map(h, S, &S.t4[id], S.v[id], false, m4::kBW, m4::kBR));
@@ -684,8 +655,8 @@ int setup_tile(gpcg_problem* h) {
         }
         for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t4m[k], S.m[k], true, m4::kMW, m4::kBR));
         for (int id : {VY0, VY1, VW, VB, VL, VU, VIN})
-            RC(make_map(h, S, &S.t5[id], S.v[id], false, m5::kBW, m4::kBR));
-        for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t5m[k], S.m[k], true, m5::kMW, m4::kBR));
+            RC(make_map(h, S, &S.t5[id], S.v[id], false, m5::kBW, m5::kBR5));
+        for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t5m[k], S.m[k], true, m5::kMW, m5::kBR5));
         auto band = [&](int resident, BandGeom& G, int& grid, int out = m4::kOut) {
             G.nbands = (h->nx + out - 1) / out;
             G.nsegs = std::max(1, std::min(resident / G.nbands, (S.rows + 15) / 16));
@@ -712,9 +683,6 @@ int setup_tile(gpcg_problem* h) {
         band(cap_env("GPCG_GP_CTAS_PER_SM", r5acc) / gshare, S.bg5_acc, S.grid5_acc, m5::kOut);
         band(cap_env("GPCG_GP_CTAS_PER_SM", r5srch) / gshare, S.bg5_srch, S.grid5_srch, m5::kOut);
         band(r5init, S.bg5_init, S.grid5_init, m5::kOut);
-        S.grid_t_cg = std::min(ntiles, r_cg);
-        S.grid_t_acc = std::min(ntiles, r_acc);
-        S.grid_t_srch = std::min(ntiles, r_srch);
     }
     h->tile = true;
     h->gfree = (h->tile_mask & 64) != 0;
@@ -930,7 +898,6 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
                   int gp = 0) {
     const bool use_k5 = h->gfree;
     const bool use_k4 = h->tile && (h->tile_mask & 16);
-    const bool use_tile = h->tile && (h->tile_mask & (1 | 16));
     const int mode = dir < 0 ? m5::PROJ : ((dir == VG0 || dir == VG1) ? m5::GP : m5::CG);
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
@@ -973,17 +940,6 @@ int launch_accept(gpcg_problem* h, int y_in, int dir, double sgn, int mask_prev,
                 if (h->bb) bydir(sbt, std::true_type()); else bydir(sbt, std::false_type());
             };
             if (h->sb) bybb(std::true_type()); else bybb(std::false_type());
-        } else if (use_tile) {
-            const CUtensorMap& md = S.tm[dir >= 0 ? dir : y_in];
-            const CUtensorMap& mp = S.tmm[mask_prev >= 0 ? mask_prev : MK0];
-            if (h->sb)
-                k3_accept<true><<<S.grid_t_acc, kTileThreads, AccStage<true>::kSmem, h->st>>>(
-                    S.sop, S.tg, B, S.tm[y_in], md, S.tm[VB], S.tm[VL], S.tm[VU], mp, dir >= 0 ? 1 : 0, sgn,
-                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
-            else
-                k3_accept<false><<<S.grid_t_acc, kTileThreads, AccStage<false>::kSmem, h->st>>>(
-                    S.sop, S.tg, B, S.tm[y_in], md, S.tm[VB], S.tm[VL], S.tm[VU], mp, dir >= 0 ? 1 : 0, sgn,
-                    mask_prev >= 0 ? 1 : 0, S.v[y_out], S.v[g_out], S.m[m_out], h->dS, R, gp);
         } else if (spec2d(h)) {   // accept + regrad + mask + counts + next Cauchy step, one sweep
             const double* dp = dir >= 0 ? S.v[dir] : nullptr;
             const unsigned char* mp = mask_prev >= 0 ? S.m[mask_prev] : nullptr;
@@ -1057,7 +1013,6 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
     const bool dg = (dir == g);
     const bool use_k5 = h->gfree;                                  // K = 2 and the K = 8 retries
     const bool use_k4 = h->tile && (h->tile_mask & 32) && K == 2;  // retries use the column march
-    const bool use_tile = h->tile && (h->tile_mask & 2) && K == 2;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
@@ -1088,14 +1043,6 @@ int launch_search(gpcg_problem* h, int y, int g, int dir, double sgn, int use_al
                 constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
                 k4_search<SB, DG><<<S.grid4_srch, m4::kThreads, SrchLayout4<SB, DG>::kSmem, h->st>>>(
                     S.sop, S.bg_srch, B, S.t4[y], S.t4[dir], S.t4[g], S.t4[VL], S.t4[VU], sgn, use_alpha0, h0, mu, h->dS, R, gp);
-            };
-            if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
-            else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
-        } else if (use_tile) {
-            auto go = [&](auto sbt, auto dgt) {
-                constexpr bool SB = decltype(sbt)::value, DG = decltype(dgt)::value;
-                k3_search<SB, DG><<<S.grid_t_srch, kTileThreads, SrchStage<SB, DG>::kSmem, h->st>>>(
-                    S.sop, S.tg, B, S.tm[y], S.tm[dir], S.tm[g], S.tm[VL], S.tm[VU], sgn, use_alpha0, h0, mu, h->dS, R, gp);
             };
             if (h->sb) { if (dg) go(std::true_type(), std::true_type()); else go(std::true_type(), std::false_type()); }
             else { if (dg) go(std::false_type(), std::true_type()); else go(std::false_type(), std::false_type()); }
@@ -1176,7 +1123,6 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
     const int bb = a ^ 1;
     const bool pc = h->prm.precond == 1;
     const bool use_k4 = h->tile && (h->tile_mask & 8);
-    const bool use_tile = h->tile && (h->tile_mask & 4) && !pc;      // k3 has no PCG variant
     const bool skip = h->cg_skip;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
@@ -1192,10 +1138,6 @@ int enqueue_cg_iter(gpcg_problem* h, int a) {
                     S.sop, S.bg_cg, h->cg_pw ? S.t4c[a] : S.t4[vrho(a)], h->cg_pw ? S.t4c[2 + a] : S.t4[vq(a)],
                     h->cg_pw ? S.t4cw : S.t4wo, S.t4m[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
                     h->dS, R, skip ? S.cgflags : nullptr, h->cg_pw ? 1 : 0);
-        } else if (use_tile) {
-            k3_cg_iter<2><<<S.grid_t_cg, kTileThreads, CgStage<2>::kSmem, h->st>>>(
-                S.sop, S.tg, S.tm[vrho(a)], S.tm[vq(a)], S.tmWc, S.tmm[MKCG], S.v[vrho(bb)], S.v[vq(bb)], S.v[VW],
-                h->dS, R);
         } else if (spec2d(h)) {   // stencil: rho, p ping-pong (p in Q[]), w in place
             auto go = [&](auto bct, auto pct) {
                 constexpr bool BC = decltype(bct)::value, PC = decltype(pct)::value;

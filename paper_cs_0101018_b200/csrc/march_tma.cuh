@@ -25,7 +25,7 @@
 #include "common.cuh"
 #include "fin.cuh"
 #include "march.cuh"
-#include "tile.cuh"
+#include "tma.cuh"
 
 namespace gpcg {
 
@@ -39,8 +39,12 @@ namespace gpcg {
 #ifndef GPCG_CG_MINB
 #define GPCG_CG_MINB (16 / GPCG_M4_WARPS)   // CG sweep CTAs per SM the register budget is sized for
 #endif
+#ifndef GPCG_GP_BR
+#define GPCG_GP_BR 6        // rows per pipeline block of the GP-family (k5 / k6_gp_loop) sweeps (tuning: 6 rows x
+                            // 2 stages 3 % faster than 4 x 3 and 8 x 2 on C3)
+#endif
 #ifndef GPCG_GP_NST
-#define GPCG_GP_NST 3       // pipeline stages of the g-free GP sweeps (k5 / k6_gp_loop; tuning: 3 stages
+#define GPCG_GP_NST 2       // pipeline stages of the g-free GP sweeps (k5 / k6_gp_loop; tuning: 3 stages
                             // and 3 CTAs per SM measured 3 % faster than 4 and 2 on C3)
 #endif
 #ifndef GPCG_GP_MINB
@@ -156,7 +160,8 @@ __device__ __forceinline__ int band_pipeline_ws(const BandGeom& G, int ny, unsig
 // putting warp 0 behind the others at every barrier, and the block to issue next is kept as a
 // cursor in shared memory (item, block, its x0 and first row), advanced without divisions.
 // bars: NST mbarriers (null: after the stages); k0 as in band_pipeline_ws (init at 0 only).
-template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, class Issue, class Begin, class Row>
+template <int NST, int STAGE, int OUT = m4::kOut, int PRE = 2, int POST = 2, int BR = m4::kBR, class Issue,
+          class Begin, class Row>
 __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned char* smem, Issue&& issue_loads,
                                              Begin&& begin, Row&& row, uint64_t* bars = nullptr, int k0 = 0,
                                              int bid = -1, int nb = -1) {
@@ -165,7 +170,7 @@ __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned
     if (bid < 0) { bid = blockIdx.x; nb = gridDim.x; }
     uint64_t* bar = bars ? bars : reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     const int nitems = G.nbands * G.nsegs;
-    const int nblk = (G.seg + PRE + POST + kBR - 1) / kBR;
+    const int nblk = (G.seg + PRE + POST + BR - 1) / BR;
     int nmine = 0;
     for (int t = bid; t < nitems; t += nb) nmine += nblk;
     __shared__ int cur[4];                               // next block to issue: item t, block b, x0, row
@@ -174,7 +179,7 @@ __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned
         if (t >= nitems) return;
         const int stage = (k0 + k) % NST;
         issue_loads(smem + stage * STAGE, x0, yr, &bar[stage]);
-        yr += kBR;
+        yr += BR;
         if (++b == nblk) {
             b = 0;
             t += nb;
@@ -201,9 +206,9 @@ __device__ __forceinline__ int band_pipeline(const BandGeom& G, int ny, unsigned
             const int stage = (k0 + k) % NST;
             unsigned char* st = smem + stage * STAGE;
             mbar_wait(&bar[stage], ((k0 + k) / NST) & 1);
-            const int yr = y0 - PRE + b * kBR;
+            const int yr = y0 - PRE + b * BR;
 #pragma unroll
-            for (int kk = 0; kk < kBR; ++kk) row(st, kk, yr + kk);
+            for (int kk = 0; kk < BR; ++kk) row(st, kk, yr + kk);
             __syncthreads();                              // every warp is done with this stage
             if (threadIdx.x == (k % NW) * 32) {
                 fence_proxy_async();
@@ -854,8 +859,9 @@ namespace m5 {
 constexpr int kOut = 26 * m4::kWarps;        // output columns per band (208 at 8 warps)
 constexpr int kBW = kOut + 8;                // f64 box columns (x0 - 4 .. x0 + kOut + 3): 112 at 4 warps
 constexpr int kMW = (kBW + 15 + 31) / 32 * 32;  // u8 mask box width (start floored to 16 B): 128 at 4 warps
-constexpr int kF = m4::kBR * kBW * 8;
-constexpr int kUt = m4::kBR * kMW;
+constexpr int kBR5 = GPCG_GP_BR;             // rows per pipeline block of the GP-family sweeps
+constexpr int kF = kBR5 * kBW * 8;
+constexpr int kUt = kBR5 * kMW;
 static_assert(kF % 128 == 0 && kUt % 128 == 0, "TMA destinations stay 128-byte aligned");
 enum Mode : int { GP = 0, CG = 1, PROJ = 2 };
 }  // namespace m5
@@ -904,7 +910,7 @@ __device__ __forceinline__ int accept_sweep5(const StencilOp& A, const BandGeom&
     double d_a = 0.0, d_b = 0.0;                  // d(ry-2), d(ry-3)
     double yn_e = 0.0, gn_e = 0.0, l_e = 0.0, u_e = 0.0;   // row ry-2 (emitted)
     const uint32_t tx = L::kMP + (has_mp ? m5::kUt : 0);
-    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG, m5::kBR5>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, tx);
@@ -1047,7 +1053,7 @@ __device__ __forceinline__ int search_sweep5(const StencilOp& A, const BandGeom&
     double s_a[K], s_b[K];                        // s_h at the s row - 1, - 2
 #pragma unroll
     for (int h = 0; h < K; ++h) { s_a[h] = 0.0; s_b[h] = 0.0; }
-    return band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2>(
+    return band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2, m5::kBR5>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, L::kStage);
@@ -1171,7 +1177,7 @@ k5_cg_init(StencilOp A, BandGeom G, const double* __restrict__ brow, const __gri
     unsigned char m_r1 = 0, m_a = 0;
     double u_a = 0.0, u_b = 0.0, rho_a = 0.0;     // u at rows r-2, r-3; rho at r-2
     const uint32_t tx = L::kM + m5::kUt;
-    band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2>(
+    band_pipeline<L::kNST, L::kStage, m5::kOut, 2, 2, m5::kBR5>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, tx);
@@ -1249,7 +1255,7 @@ __device__ __forceinline__ int spec_sweep5(const StencilOp& A, const BandGeom& G
     double g_a = 0.0, g_b = 0.0;                  // g(r-2), g(r-3)
     double as_p = 0.0;                            // (A s)(r-3), from the previous row step
     const uint32_t tx = L::kMP + m5::kUt;
-    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+    return band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG, m5::kBR5>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, tx);
@@ -1356,7 +1362,7 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
     double s_a = 0.0, s_b = 0.0;                                        // s(r-2), s(r-3)
     double d_b = 0.0;                                                   // d(r-3)
     const uint32_t tx = L::kMP + m5::kUt;
-    const int k = band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG>(
+    const int k = band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG, m5::kBR5>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
             mbar_expect_tx(bar, tx);

@@ -161,16 +161,35 @@ def test_nccl_collectives_one_rank(G, oracle, monkeypatch, case, slabs):
     assert np.max(np.abs(x - x_o)) <= 1e-7
 
 
+@pytest.mark.parametrize("precond", [2, 3])
 @pytest.mark.parametrize("case", ["C0", "ragged37x23_full_shift"])
-def test_slab_bjilu_reaches_the_minimiser(G, oracle, case):
+def test_slab_bjilu_reaches_the_minimiser(G, oracle, case, precond):
     """Block-Jacobi ILU with blocks inside each slab (the paper's one block per processor,
     here tiles per slab): a different preconditioner per slab layout, the same x*."""
     make, tol = CASES[case]
     prob = make()
     rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
     with G.Solver.from_problem(prob, slabs=2) as s:
-        s.set_params(precond=2)
+        s.set_params(precond=precond)
         rc, x, st = s.solve(prob.x0, tol)
     assert rc == 0 and rc_o == 0
     assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
     assert np.max(np.abs(x - x_o)) <= 1e-7
+
+
+@pytest.mark.parametrize("slabs", [2, 4])
+def test_multi_slab_persistent_loops_match_single_slab_per_step(G, slabs):
+    """The multi-slab persistent CG / GP loops (one launch over every slab, fused halo writes):
+    one outer iteration with a short GP phase and a fixed-length CG call gives the single-slab
+    iterate to rounding (only the order of the partial sums differs)."""
+    prob = P.c3_family(160, 160)
+    out = {}
+    for ns in (1, slabs):
+        with G.Solver.from_problem(prob, slabs=ns) as s:
+            s.set_params(gp_cap=6, cg_cap=12, eta2=1e-12, refine_cap=1)
+            rc, x, st = s.solve(prob.x0, -1e-14, max_it=1)
+        out[ns] = (x, st)
+    (x1, st1), (xs, sts) = out[1], out[slabs]
+    assert (st1["gp_iters"], st1["cg_iters"]) == (sts["gp_iters"], sts["cg_iters"])
+    assert st1["cg_iters"] == 12 and st1["gp_iters"] >= 2
+    assert np.max(np.abs(x1 - xs)) <= 1e-11 * max(np.max(np.abs(x1)), 1e-300)
