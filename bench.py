@@ -377,22 +377,23 @@ def run_ours(args):
     e2e_val = e2e_hvps / e2e_s
 
     # the GP phase: one GP step = one speculative accept sweep at alpha_0 (k6_gp_loop, 2-D broadcast
-    # faces, one slab) whose bytes per point are those the sweep must move: y and the
-    # previous mask read, y and the mask written (18 B) + l, u unless both are constants (16 B) + b
-    # unless every grid row holds the same b (8 B); g is recomputed, never stored.  A step whose
-    # speculative sweep was rejected (stats gp_spec_rejected) also ran a search sweep (y [+ l, u]
-    # [+ b]) and an accept sweep (the speculative sweep's bytes).
+    # faces, one slab) whose bytes per point are those the sweep must move: y read,
+    # y and the mask written (17 B; the previous mask is recomputed from y, l, u) + l, u unless both
+    # are constants (16 B) + b unless every grid row holds the same b (8 B); g is recomputed, never
+    # stored.  A step whose speculative sweep was rejected (stats gp_spec_rejected) also ran a search
+    # sweep (y [+ l, u] [+ b]) and an accept sweep (y, mask_prev [+ l, u] [+ b] read; y, mask written).
     gp_roof = None
     if agg["gp_iters"] and prob.kind == "stencil2d":
         sb = bool(np.all(prob.l == prob.l[0]) and np.all(prob.u == prob.u[0]))
         bb = bool(np.all(prob.b.reshape(prob.ny, prob.nx) == prob.b[: prob.nx][None, :]))
-        spec_b = 18.0 + (0.0 if sb else 16.0) + (0.0 if bb else 8.0)
+        spec_b = 17.0 + (0.0 if sb else 16.0) + (0.0 if bb else 8.0)
         srch_b = 8.0 + (0.0 if sb else 16.0) + (0.0 if bb else 8.0)
+        acc_b = spec_b + 1.0
         persist = (world * args.slabs == 1 and not prob.wx_ld and not prob.wy_ld and prob.shift is None
                    and os.environ.get("GPCG_GP_PERSIST", "1") != "0")
         rej = agg["gp_spec_rejected"]
         gp_step_s = (agg["t_gp_ms"] / 1e3) / agg["gp_iters"]
-        gp_bytes = (spec_b * agg["gp_iters"] + (srch_b + spec_b) * rej) * prob.n / agg["gp_iters"] / world
+        gp_bytes = (spec_b * agg["gp_iters"] + (srch_b + acc_b) * rej) * prob.n / agg["gp_iters"] / world
         ach = gp_bytes / gp_step_s / 1e9
         gp_roof = {"bound": "hbm",
                    "kernel": ("k6_gp_loop (persistent GP phase; speculative accept sweep per step)" if persist
@@ -402,7 +403,7 @@ def run_ours(args):
                    "bytes_per_launch": gp_bytes, "us_per_launch": gp_step_s * 1e6,
                    "launch": "one GP step (sweep(s) + grid reduction + stop tests), CUDA events around each GP phase",
                    "algorithmic_bytes": f"{spec_b:.0f} B per point per speculative sweep (sb={sb}, bb={bb}); "
-                                        f"+{srch_b + spec_b:.0f} B per point for each of {rej} rejected steps",
+                                        f"+{srch_b + acc_b:.0f} B per point for each of {rej} rejected steps",
                    "survey_8d": {"bytes_per_launch": (74.0 if sb else 122.0) * prob.n / world,
                                  "frac": (74.0 if sb else 122.0) * prob.n / world / gp_step_s / 1e9 / peak,
                                  "what": "SURVEY 8(d): 3 sweeps per GP sub-step (a2, a3, a1)"}}

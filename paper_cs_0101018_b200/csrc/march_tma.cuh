@@ -1361,7 +1361,9 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
     double g_a = 0.0, yn_a = 0.0, l_a = 0.0, u_a = 0.0;                 // row r-2
     double s_a = 0.0, s_b = 0.0;                                        // s(r-2), s(r-3)
     double d_b = 0.0;                                                   // d(r-3)
-    const uint32_t tx = L::kMP + m5::kUt;
+    // mask_prev is not loaded: the previous free mask is !(y == l || y == u) of the row's y itself
+    // (every mask is written from the same comparison of the iterate it belongs to)
+    const uint32_t tx = L::kMP;
     const int k = band_pipeline<L::kNST, L::kStage, m5::kOut, LAG + 1, LAG, m5::kBR5>(
         G, A.ny, smem,
         [&](unsigned char* st, int x0, int yr, uint64_t* bar) {
@@ -1373,7 +1375,6 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
                 tma_load_2d(st + L::kL, m_l, x0 - 4, yt, bar);
                 tma_load_2d(st + L::kU, m_u, x0 - 4, yt, bar);
             }
-            tma_load_2d(st + L::kMP, m_mp, floor16(x0 - 4), yt - LAG, bar);
         },
         [&](int x0, int yb, int ye) {
             gx = x0 - 3 + 26 * wid + lane;
@@ -1422,7 +1423,8 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
                 acc[0] = fma(d2, d2, acc[0]);
                 acc[1] = fma(gn2, gn2, acc[1]);
                 n_act += act ? 1 : 0;
-                n_chg += (st[L::kMP + kk * m5::kMW + c + moff] != m) ? 1 : 0;
+                const bool act_prev = (y_m2 == l_a) || (y_m2 == u_a);     // y(r-2) before the step
+                n_chg += (act_prev != act) ? 1 : 0;
                 const bool binding = (al && gn2 >= 0.0) || (au && gn2 <= 0.0);
                 n_nb += (act && !binding) ? 1 : 0;
                 acc[5] += e;                                                  // <d, A d>
