@@ -3,8 +3,8 @@ with the paper's algorithm settings -- tau = 1e-4 absolute, x0 = l, eta1 = 0.1, 
 0.05 -- at the paper's sizes, with plain CG and with the point-Jacobi
 preconditioner (the "Diagonal" column of Table 4), on one B200.  Prints
 iterations, n_GP, CG iterations, t_CG % and seconds next to the paper's IBM SP numbers
-(context only: FD instead of the FE discretisation, B200 instead of the SP; the paper's
-Tables 1/2 used block-Jacobi ILU(2), which this build does not have).
+(context only: FD instead of the FE discretisation, B200 instead of the SP, 32x32-tile
+blocks instead of one block per processor for the paper's block-Jacobi ILU(2) of Tables 1/2).
 
 usage: python scripts/paper_setting.py [--out profiles/paper_setting.json]
 """
@@ -30,7 +30,7 @@ PAPER = {
 }
 
 
-PRECOND_NAMES = {0: "none", 1: "jacobi", 2: "bj-ilu0 (32x32 tiles)"}
+PRECOND_NAMES = {0: "none", 1: "jacobi", 2: "bj-ilu0 (32x32 tiles)", 3: "bj-ilu2 (32x32 tiles)"}
 
 
 def run(grid, eps, precond):
@@ -57,7 +57,7 @@ def main():
     args = ap.parse_args()
     rows = []
     for grid, eps in [(800, 0.1), (800, 0.9), (1600, 0.1), (1600, 0.9)]:
-        for pc in (0, 1, 2):
+        for pc in (0, 1, 2, 3):
             r = run(grid, eps, pc)
             r["paper"] = PAPER[(grid, eps)]
             rows.append(r)

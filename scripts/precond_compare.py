@@ -1,5 +1,5 @@
 """Preconditioners on the bench workloads (C2 / C1 / C3 1600^2 member, tol of BASELINE.json):
-plain CG (the hot path), point Jacobi, block-Jacobi ILU(0) -- solve time and iteration counts.
+plain CG (the hot path), point Jacobi, block-Jacobi ILU(0) / ILU(2) -- solve time and iteration counts.
 
 usage: python scripts/precond_compare.py [--out profiles/precond_compare_r1.json] [CONFIGS...]
 """
@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 from paper_cs_0101018_b200 import problems as P, gpcg  # noqa: E402
 
-NAMES = {0: "none", 1: "jacobi", 2: "bj-ilu0 (32x32 tiles)"}
+NAMES = {0: "none", 1: "jacobi", 2: "bj-ilu0 (32x32 tiles)", 3: "bj-ilu2 (32x32 tiles)"}
 
 
 def main():
@@ -24,7 +24,7 @@ def main():
     rows = []
     for name in args.configs:
         prob = P.get(name)
-        for pc in (0, 1, 2):
+        for pc in (0, 1, 2, 3):
             s = gpcg.Solver.from_problem(prob, device="cuda")
             s.set_params(precond=pc)
             x0 = torch.from_numpy(prob.x0).cuda()
