@@ -583,6 +583,14 @@ int set_smem(K kernel, int bytes) {
 
 // TMA tile path for a broadcast-face stencil (C0/C2/C3 family)
 int setup_tile(gpcg_problem* h) {
+    {
+        // per-warp CG boxes pay off once the CG vectors (rho x2, p x2, w: 40 B per point) leave
+        // the 126 MB L2 (C3: 64M points); below that the band boxes' 3 TMA operations a block win
+        long long pts = 0;
+        for (const Slab& S : h->slabs) pts += (long long)S.rows * h->nx;
+        h->cg_pw = 40LL * pts > 256LL * 1024 * 1024;
+        if (const char* e = getenv("GPCG_CG_PW")) h->cg_pw = atoi(e) != 0;
+    }
     RC(set_smem(k4_hessvec<true>, m4hv::kSmem));
     RC(set_smem(k4_hessvec<false>, m4hv::kSmem));
     RC(set_smem(k4_cg_iter<false>, m4cg::kSmem));
@@ -657,9 +665,12 @@ int setup_tile(gpcg_problem* h) {
         for (int id : {VY0, VY1, VW, VB, VL, VU, VIN})
             RC(make_map(h, S, &S.t5[id], S.v[id], false, m5::kBW, m5::kBR5));
         for (int k = 0; k < NMSK; ++k) RC(make_map(h, S, &S.t5m[k], S.m[k], true, m5::kMW, m5::kBR5));
-        auto band = [&](int resident, BandGeom& G, int& grid, int out = m4::kOut) {
+        // ipc: items per CTA (> 1 spreads each CTA's work over several shorter segments: the CG
+        // sweep skips the loads of all-active blocks, so equal-area items are not equal work;
+        // several items a CTA even out the grid barrier's wait for the slowest)
+        auto band = [&](int resident, BandGeom& G, int& grid, int out = m4::kOut, int ipc = 1) {
             G.nbands = (h->nx + out - 1) / out;
-            G.nsegs = std::max(1, std::min(resident / G.nbands, (S.rows + 15) / 16));
+            G.nsegs = std::max(1, std::min(resident * ipc / G.nbands, (S.rows + 15) / 16));
             G.seg = (S.rows + G.nsegs - 1) / G.nsegs;
             G.nsegs = (S.rows + G.seg - 1) / G.seg;
             G.rlo = -S.glo;
@@ -671,8 +682,12 @@ int setup_tile(gpcg_problem* h) {
             return (e && atoi(e) > 0) ? std::min(r, atoi(e) * h->sms) : r;
         };
         // several slabs in one persistent CG launch: the resident CTAs are shared among the slabs
-        band(cap_env("GPCG_CG_CTAS_PER_SM", r4cg) / (multi_slab_persistent(h) ? h->nslabs() : 1), S.bg_cg,
-             S.grid4_cg);
+        {
+            int ipc = h->cg_pw ? 16 : 1;                 // C3: 61-row items instead of 1000 (CG 420 -> 372 us)
+            if (const char* e = getenv("GPCG_CG_ITEMS_PER_CTA")) ipc = std::max(1, atoi(e));
+            band(cap_env("GPCG_CG_CTAS_PER_SM", r4cg) / (multi_slab_persistent(h) ? h->nslabs() : 1), S.bg_cg,
+                 S.grid4_cg, m4::kOut, ipc);
+        }
         {
             const long long nf = (long long)S.bg_cg.nbands * S.bg_cg.nsegs * ((S.bg_cg.seg + 4 + m4::kBR - 1) / m4::kBR);
             CK(dalloc(h, &S.cgflags, (size_t)std::max<long long>(nf, 1) * sizeof(unsigned short)));
@@ -680,20 +695,13 @@ int setup_tile(gpcg_problem* h) {
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
         const int gshare = multi_slab_persistent(h) ? h->nslabs() : 1;   // one persistent GP launch, all slabs
-        band(cap_env("GPCG_GP_CTAS_PER_SM", r5acc) / gshare, S.bg5_acc, S.grid5_acc, m5::kOut);
-        band(cap_env("GPCG_GP_CTAS_PER_SM", r5srch) / gshare, S.bg5_srch, S.grid5_srch, m5::kOut);
+        const int gipc = getenv("GPCG_GP_ITEMS_PER_CTA") ? std::max(1, atoi(getenv("GPCG_GP_ITEMS_PER_CTA"))) : 1;
+        band(cap_env("GPCG_GP_CTAS_PER_SM", r5acc) / gshare, S.bg5_acc, S.grid5_acc, m5::kOut, gipc);
+        band(cap_env("GPCG_GP_CTAS_PER_SM", r5srch) / gshare, S.bg5_srch, S.grid5_srch, m5::kOut, gipc);
         band(r5init, S.bg5_init, S.grid5_init, m5::kOut);
     }
     h->tile = true;
     h->gfree = (h->tile_mask & 64) != 0;
-    {
-        // per-warp CG boxes pay off once the CG vectors (rho x2, p x2, w: 40 B per point) leave
-        // the 126 MB L2 (C3: 64M points); below that the band boxes' 3 TMA operations a block win
-        long long pts = 0;
-        for (const Slab& S : h->slabs) pts += (long long)S.rows * h->nx;
-        h->cg_pw = 40LL * pts > 256LL * 1024 * 1024;
-        if (const char* e = getenv("GPCG_CG_PW")) h->cg_pw = atoi(e) != 0;
-    }
     {
         // persistent GP phase: smem of the larger (accept) layout; grid within co-residency
         auto cfg = [&](auto sbt, auto bbt) {
