@@ -444,8 +444,10 @@ int exchange_arrays(gpcg_problem* h, const RowArray* arr, int na) {
 bool has_ghosts(const gpcg_problem* h) { return h->nslabs() > 1 || h->nranks > 1; }
 
 // several slabs of one device, one process: the persistent loops span all slabs (SlabLink)
+// (GPCG_MS_ONE=1, diagnostic: one slab through the multi-slab kernels as well)
 bool multi_slab_persistent(const gpcg_problem* h) {
-    return h->nranks == 1 && !h->use_nccl && h->nslabs() > 1 && h->nslabs() <= kMaxMs;
+    static const bool ms1 = getenv("GPCG_MS_ONE") && atoi(getenv("GPCG_MS_ONE")) != 0;
+    return h->nranks == 1 && !h->use_nccl && (h->nslabs() > 1 || ms1) && h->nslabs() <= kMaxMs;
 }
 
 // 2-D stencil with its specialised sweeps (march / tile kernels); otherwise the generic kernels

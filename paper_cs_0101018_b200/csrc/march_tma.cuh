@@ -1354,8 +1354,11 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
     int gx = 0, moff = 0, y0 = 0, y1 = 0;
     bool col_ok = false;
     Op5<true> op;
-    double bcol = 0.0, fe_bd = 0.0;               // b of the column; east boundary face weight (last column)
-    long long vrow = 0;                           // storage index of (gx, emitted row), advanced per row
+    double bcol = 0.0, fe_bd = 0.0, fen_bd = 0.0; // b of the column; east boundary face weight (last
+                                                  // column), + the north one (last grid row)
+    int r_last = 0;                               // raw row whose emitted row is the last grid row
+    double* yrow = nullptr;                       // y_out / mask_out at (gx, emitted row), advanced per row
+    unsigned char* mrow = nullptr;
     int n_act = 0, n_chg = 0, n_nb = 0;           // the three set counts, as integers (exact)
     double y_m1 = 0.0, y_m2 = 0.0, l_r1 = 0.0, u_r1 = 0.0, b_r1 = 0.0;   // raw rows r-1, r-2
     double g_a = 0.0, yn_a = 0.0, l_a = 0.0, u_a = 0.0;                 // row r-2
@@ -1384,8 +1387,14 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             col_ok = gx >= 0 && gx < A.nx;
             op.init(A, gx);
             fe_bd = gx == A.nx - 1 ? op.fe : 0.0;
+            fen_bd = fe_bd + op.fn;
+            r_last = A.rhi + 1;
             if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
-            vrow = (long long)gx + (long long)A.pitch * (yb - (LAG + 1) - LAG);
+            {
+                const long long v = (long long)gx + (long long)A.pitch * (yb - (LAG + 1) - LAG);
+                yrow = y_out + v;                 // (rows before the item: never dereferenced)
+                mrow = mask_out + v;
+            }
             y_m1 = y_m2 = l_r1 = u_r1 = b_r1 = g_a = yn_a = l_a = u_a = s_a = s_b = d_b = 0.0;
         },
         [&](const unsigned char* st, int kk, int r) {
@@ -1402,21 +1411,26 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             const double s1 = yn1 - y_m1;                                     // s(r-1)
             const double as2 = op.apply(A, r - 2, s_a, s_b, s1);              // (A s)(r-2)
             const double gn2 = g_a + as2;                                     // gn(r-2)
-            const double d2 = pgrad(yn_a, gn2, l_a, u_a);                     // d(r-2)
+            // d(r-2) = pgrad(yn, gn, l, u) (common.cuh) written out, so that its bound tests and
+            // its zero flag serve the mask, the active count and the binding test below as well
+            const bool al = yn_a == l_a, au = yn_a == u_a;
+            const bool zero = (al && !(gn2 < 0.0)) || (au && !(gn2 > 0.0));   // pgrad's zero case
+            const double d2 = zero ? 0.0 : gn2;                               // d(r-2)
             const double dw = __shfl_up_sync(0xffffffffu, d2, 1);             // d(r-2) one column west
             const int re = r - 2;
-            const long long v = vrow;
-            vrow += A.pitch;
+            double* const yp = yrow;
+            unsigned char* const mp = mrow;
+            yrow += A.pitch;
+            mrow += A.pitch;
             if (out_lane && col_ok && re >= y0 && re < y1) {
-                y_out[v] = yn_a;
-                const bool al = yn_a == l_a, au = yn_a == u_a;
+                *yp = yn_a;
                 const bool act = al || au;
                 const unsigned char m = act ? 0 : 1;
-                mask_out[v] = m;
+                *mp = m;
                 // face form of <d, A d>: west and south faces, + the boundary faces of the last
                 // column / row (coefficient fe_bd, and fn on the last grid row)
                 const double ew = d2 - dw, es = d2 - d_b;
-                const double kb = fe_bd + ((r - 1 >= A.rhi) ? op.fn : 0.0);
+                const double kb = r == r_last ? fen_bd : fe_bd;
                 double e = op.fw * ew * ew;
                 e = fma(op.fs * es, es, e);
                 e = fma(kb * d2, d2, e);
@@ -1425,8 +1439,8 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
                 n_act += act ? 1 : 0;
                 const bool act_prev = (y_m2 == l_a) || (y_m2 == u_a);     // y(r-2) before the step
                 n_chg += (act_prev != act) ? 1 : 0;
-                const bool binding = (al && gn2 >= 0.0) || (au && gn2 <= 0.0);
-                n_nb += (act && !binding) ? 1 : 0;
+                // binding: (al && gn >= 0) || (au && gn <= 0) -- pgrad's zero case (finite gn)
+                n_nb += (act && !zero) ? 1 : 0;
                 acc[5] += e;                                                  // <d, A d>
                 acc[6] = fma(g_a, s_a, acc[6]);                               // <g, s>(r-2)
                 acc[7] = fma(s_a, as2, acc[7]);                               // <s, A s>(r-2)
