@@ -857,6 +857,9 @@ int create_vectors(gpcg_problem* h, const double* b, const double* l, const doub
     if (h->hS->r0 != 0.0)
         return set_err(GPCG_EINVAL, "%.0f entries violate l <= u (or NaN/inf in b, l = +inf, u = -inf)", h->hS->r0);
     h->sb = (h->hS->r1 == 0.0);
+#ifdef GPCG_DIAG_FORCE_SB
+    h->sb = true;                   // diagnostic builds only: time the sweeps without the l / u streams
+#endif
     double lu[2];
     CK(cudaMemcpy(lu, h->lu0, sizeof lu, cudaMemcpyDeviceToHost));
     h->lc = lu[0];

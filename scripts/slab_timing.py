@@ -22,8 +22,11 @@ for slabs in [int(a) for a in sys.argv[2:]]:
     torch.cuda.synchronize()
     t1 = time.time()
     cg_us = 1e3 * st["t_cg_timed_ms"] / max(st["cg_iters_timed"], 1)
+    # per free point and iteration: the CG sweep skips all-active blocks, so the per-iteration time
+    # follows the free-set sizes along the path, which differs with the slab count (rounding)
+    cg_ps = 1e9 * st["t_cg_timed_ms"] / max(st["cg_free_iters_timed"], 1)
     gp_us = 1e3 * st["t_gp_ms"] / max(st["gp_iters"], 1)
     print(f"{prob.name} slabs={slabs}: solve {t1 - t0:.3f}s rc={rc} outer={st['outer_iters']} gp={st['gp_iters']} "
-          f"cg={st['cg_iters']} | CG {cg_us:.1f} us/iter | GP {gp_us:.1f} us/step | launches={st['kernel_launches']} "
+          f"cg={st['cg_iters']} | CG {cg_us:.1f} us/iter ({cg_ps:.2f} ps per free point) | GP {gp_us:.1f} us/step | launches={st['kernel_launches']} "
           f"q={st['q']:.15g}", flush=True)
     s.close()
