@@ -1357,6 +1357,7 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
     double bcol = 0.0, fe_bd = 0.0, fen_bd = 0.0; // b of the column; east boundary face weight (last
                                                   // column), + the north one (last grid row)
     int r_last = 0;                               // raw row whose emitted row is the last grid row
+    bool bnd_warp = false;                        // this warp holds the last grid column
     double* yrow = nullptr;                       // y_out / mask_out at (gx, emitted row), advanced per row
     unsigned char* mrow = nullptr;
     int n_act = 0, n_chg = 0, n_nb = 0;           // the three set counts, as integers (exact)
@@ -1388,6 +1389,7 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
             op.init(A, gx);
             fe_bd = gx == A.nx - 1 ? op.fe : 0.0;
             fen_bd = fe_bd + op.fn;
+            bnd_warp = __any_sync(0xffffffffu, gx == A.nx - 1);
             r_last = A.rhi + 1;
             if (BB) bcol = col_ok ? __ldg(brow + gx) : 0.0;
             {
@@ -1430,18 +1432,20 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
                 // face form of <d, A d>: west and south faces, + the boundary faces of the last
                 // column / row (coefficient fe_bd, and fn on the last grid row)
                 const double ew = d2 - dw, es = d2 - d_b;
-                const double kb = r == r_last ? fen_bd : fe_bd;
-                double e = op.fw * ew * ew;
-                e = fma(op.fs * es, es, e);
-                e = fma(kb * d2, d2, e);
+                acc[5] = fma(op.fw * ew, ew, acc[5]);                        // <d, A d>, west face
+                acc[5] = fma(op.fs * es, es, acc[5]);                        // ... south face
+                if (bnd_warp || r == r_last) {                // (warp-uniform) boundary faces
+                    const double kb = r == r_last ? fen_bd : fe_bd;
+                    acc[5] = fma(kb * d2, d2, acc[5]);
+                }
                 acc[0] = fma(d2, d2, acc[0]);
-                acc[1] = fma(gn2, gn2, acc[1]);
+                // acc[1] (||g||^2 of the new point) is not formed: no GP-phase decision reads it
+                // (the solve's ||g(x0)|| comes from the initial projection)
                 n_act += act ? 1 : 0;
                 const bool act_prev = (y_m2 == l_a) || (y_m2 == u_a);     // y(r-2) before the step
                 n_chg += (act_prev != act) ? 1 : 0;
                 // binding: (al && gn >= 0) || (au && gn <= 0) -- pgrad's zero case (finite gn)
                 n_nb += (act && !zero) ? 1 : 0;
-                acc[5] += e;                                                  // <d, A d>
                 acc[6] = fma(g_a, s_a, acc[6]);                               // <g, s>(r-2)
                 acc[7] = fma(s_a, as2, acc[7]);                               // <s, A s>(r-2)
                 if (SL) {                                     // fused halo write (SlabLink)
