@@ -1,10 +1,12 @@
-# r2f: round-2 evidence refresh -- full GPU test suite, the default bench line (C3), the C2 bench
-# line, then the profiling set of gpu_prof_r2.sh (launch list, ncu --set full of both loops, traffic)
+# r2f: compact free-row list (tests, a4 microbenchmark), GP-loop A/B (warps / CTAs per SM)
 mkdir -p gpurun_out
 export GPCG_TRACE_OFF=1
 python -c "import paper_cs_0101018_b200._build as b; b.build()"
-timeout 2400 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/r2f_pytest.log 2>&1; echo "pytest rc=$?"
-grep -E "passed|failed|FAILED|Error" gpurun_out/r2f_pytest.log | tail -3
-timeout 1800 python bench.py > gpurun_out/r2f_bench_C3.json 2> gpurun_out/r2f_bench_C3.err; echo "bench rc=$?"; tail -c 600 gpurun_out/r2f_bench_C3.json
-timeout 900 python bench.py --config C2 > gpurun_out/r2f_bench_C2.json 2> gpurun_out/r2f_bench_C2.err; echo "bench C2 rc=$?"
-TAG=r2f bash scripts/gpu_prof_r2.sh
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "compact or spmv or c4 or golden" > gpurun_out/r2f_pytest.log 2>&1; echo "pytest rc=$?"
+grep -E "passed|failed|FAILED|Error" gpurun_out/r2f_pytest.log | tail -20
+timeout 600 python scripts/a4_compact.py C4 C4s 2>&1 | tail -6
+for V in default w8m2 w4m4 w4m6 old_nst4minb2; do
+  if [ $V = default ]; then L=""; else L=build_variants/$V.so; fi
+  GPCG_LIB=$L timeout 300 python scripts/gp_ab.py C3 300 2>&1 | tail -1
+  GPCG_LIB=$L timeout 300 python scripts/gp_ab.py C2 300 2>&1 | tail -1
+done
