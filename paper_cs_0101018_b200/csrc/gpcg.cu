@@ -2761,4 +2761,10 @@ fail:
     }
 }
 
+#ifdef GPCG_DIAG_TIMES
+// diagnostic builds only: the k6_gp_loop stamps of the last launch (ns, [step][cta][5])
+GPCG_API int gpcg_diag_gp_times(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_diag_t, sizeof(g_diag_t)) == cudaSuccess ? 0 : -1;
+}
+#endif
 }  // extern "C"

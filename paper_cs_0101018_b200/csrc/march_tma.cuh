@@ -1487,13 +1487,39 @@ __device__ __forceinline__ int spec_sweep6(const StencilOp& A, const BandGeom& G
 // an acceptable step (or <d,Ad> <= 0) hands the step back to the host (GP_HOST), as the
 // graph path does.  y, mask ping-pong between buffers 0 / 1 starting from cur0.
 // ============================================================================
+#ifdef GPCG_DIAG_TIMES
+// diagnostic builds only (scripts/gp_step_times.py): per (GP step of the last launch, CTA)
+// globaltimer stamps -- step start, sweep done (after the block reduction), grid barrier
+// passed, sums formed -- and the CTA's SM
+constexpr int kDiagSteps = 64, kDiagCtas = 512;
+__device__ unsigned long long g_diag_t[kDiagSteps][kDiagCtas][5];
+__device__ int g_diag_step[kDiagCtas];            // each CTA's step of the running launch
+__device__ __forceinline__ void diag_stamp(int slot) {
+    if (threadIdx.x != 0 || blockIdx.x >= kDiagCtas) return;
+    const int st = g_diag_step[blockIdx.x];
+    if (st >= kDiagSteps) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_diag_t[st][blockIdx.x][slot] = t;
+    if (slot == 0) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_diag_t[st][blockIdx.x][4] = smid;
+    }
+}
+#else
+__device__ __forceinline__ void diag_stamp(int) {}
+#endif
+
 template <int NS>
 __device__ __forceinline__ void grid_sum(double (&acc)[NS], double* part, unsigned int G_, unsigned int* gbar,
                                          unsigned int& gen, double* red, double* tot) {
     block_reduce<NS>(acc, red);
+    diag_stamp(1);
     if (threadIdx.x == 0)
         for (int q = 0; q < NS; ++q) part[q * G_ + blockIdx.x] = acc[q];
     grid_barrier(gbar, G_, gen);
+    diag_stamp(2);
     double t[NS];
 #pragma unroll
     for (int q = 0; q < NS; ++q) t[q] = 0.0;
@@ -1504,6 +1530,7 @@ __device__ __forceinline__ void grid_sum(double (&acc)[NS], double* part, unsign
     if (threadIdx.x == 0)
         for (int q = 0; q < NS; ++q) tot[q] = t[q];
     __syncthreads();
+    diag_stamp(3);
 }
 
 // The GP phase loop shared by the single- and multi-slab persistent kernels.  spec(cur, alpha_0,
@@ -1535,6 +1562,10 @@ __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __
     while (!done) {
         if (!cauchy_ok) { s_h = -1; done = 1; reason = GP_HOST; break; }
         bool have_accept = false;
+#ifdef GPCG_DIAG_TIMES
+        if (threadIdx.x == 0 && blockIdx.x < kDiagCtas) g_diag_step[blockIdx.x] = (int)(j - S->gp_j);
+        diag_stamp(0);
+#endif
         if (spec) {
             // speculative accept at alpha_0 with the h = 0 search sums (one sweep when accepted)
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};

@@ -1,4 +1,4 @@
-# r2f: round-2 evidence refresh -- full GPU test suite, the default bench line (C3), the C2 bench
+# r2ev (run as r2f, outputs tagged r2f): round-2 evidence refresh -- full GPU test suite, the default bench line (C3), the C2 bench
 # line, then the profiling set of gpu_prof_r2.sh (launch list, ncu --set full of both loops, traffic)
 mkdir -p gpurun_out
 export GPCG_TRACE_OFF=1

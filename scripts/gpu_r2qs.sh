@@ -1,5 +1,5 @@
 # (the quiet-item skipping this script measured was not kept: scripts/patches/gp_quiet_item_skip.patch)
-# r2g: exact skipping of quiet GP items (GPCG_GP_SKIP) x GP items per CTA
+# r2qs (run as r2g): exact skipping of quiet GP items (GPCG_GP_SKIP) x GP items per CTA
 mkdir -p gpurun_out
 export GPCG_TRACE_OFF=1
 python -c "import paper_cs_0101018_b200._build as b; b.build()"
