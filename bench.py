@@ -110,7 +110,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, index):
         self.index = index
@@ -133,7 +133,7 @@ class ClockSampler:
         self.p.wait()
         self.f.flush()
         self.f.seek(0)
-        sm, smax, reasons = [], [], set()
+        sm, smax, reasons, pw, plim, capped = [], [], set(), [], [], 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.f.read().splitlines():
             parts = [x.strip() for x in ln.split(",")]
@@ -147,10 +147,19 @@ class ClockSampler:
             for nm, v in zip(names, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+            capped += parts[8].lower().startswith("active")
+            try:
+                pw.append(float(parts[3]))
+                plim.append(float(parts[9]))
+            except (ValueError, IndexError):
+                pass
         os.unlink(self.f.name)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": float(max(smax)) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "reasons": sorted(reasons),
+                "power_w": float(np.median(pw)) if pw else None,
+                "power_limit_w": float(np.median(plim)) if plim else None,
+                "sw_power_cap_fraction": capped / len(sm) if sm else None}
 
 
 def dist_env():

@@ -697,9 +697,30 @@ int setup_tile(gpcg_problem* h) {
         band(r4acc, S.bg_acc, S.grid4_acc);
         band(r4srch, S.bg_srch, S.grid4_srch);
         const int gshare = multi_slab_persistent(h) ? h->nslabs() : 1;   // one persistent GP launch, all slabs
-        const int gipc = getenv("GPCG_GP_ITEMS_PER_CTA") ? std::max(1, atoi(getenv("GPCG_GP_ITEMS_PER_CTA"))) : 1;
-        band(cap_env("GPCG_GP_CTAS_PER_SM", r5acc) / gshare, S.bg5_acc, S.grid5_acc, m5::kOut, gipc);
-        band(cap_env("GPCG_GP_CTAS_PER_SM", r5srch) / gshare, S.bg5_srch, S.grid5_srch, m5::kOut, gipc);
+        // GP items per CTA: the count (1-4) that minimises the pipeline blocks of the most loaded
+        // CTA -- 1 for one slab of C3 (429 items on 444 CTAs), 2 for each of two slabs (195 items
+        // of 800 rows vs 429 of 364 on 222 CTAs)
+        auto gp_ipc = [&](int resident) {
+            int best = 1;
+            long long best_cost = -1;
+            for (int ipc = 1; ipc <= 4; ++ipc) {
+                BandGeom T;
+                int g = 0;
+                band(resident, T, g, m5::kOut, ipc);
+                const long long items = (long long)T.nbands * T.nsegs;
+                // rows a CTA sweeps: its items' segments + 5 lag rows, in whole pipeline blocks, + one
+                // block per item for the pipeline's restart
+                const long long blk = (T.seg + 5 + m5::kBR5 - 1) / m5::kBR5 + 1;
+                const long long cost = (items + g - 1) / g * blk;
+                if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = ipc; }
+            }
+            return best;
+        };
+        const int r5a = cap_env("GPCG_GP_CTAS_PER_SM", r5acc) / gshare, r5s = cap_env("GPCG_GP_CTAS_PER_SM", r5srch) / gshare;
+        const int gipc = getenv("GPCG_GP_ITEMS_PER_CTA") ? std::max(1, atoi(getenv("GPCG_GP_ITEMS_PER_CTA")))
+                                                         : gp_ipc(std::min(r5a, r5s));
+        band(r5a, S.bg5_acc, S.grid5_acc, m5::kOut, gipc);
+        band(r5s, S.bg5_srch, S.grid5_srch, m5::kOut, gipc);
         band(r5init, S.bg5_init, S.grid5_init, m5::kOut);
     }
     h->tile = true;
