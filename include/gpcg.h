@@ -276,6 +276,27 @@ GPCG_API int gpcg_solve(gpcg_problem *h, const double *x0, double tol, int64_t m
 GPCG_API int gpcg_hessvec(gpcg_problem *h, const double *v, double *y, int reduced);
 
 /*
+ * gpcg_free_count -- |F| of the free set recorded by the last gpcg_project /
+ * gpcg_solve, or -1 if none is recorded or the handle has no
+ * compacted free-row list (2-D stencils, several slabs or ranks).
+ */
+GPCG_API int64_t gpcg_free_count(gpcg_problem *h);
+
+/*
+ * gpcg_hessvec_free -- the reduced Hessian product in the reduced space:
+ * y_free[k] = (A_k Z_k' v)_k = sum_{j in F} A_{f_k j} v_j for k < |F|, where
+ * F = [f_0 < f_1 < ...] is the recorded free set in index order and
+ * A_k = Z_k' A Z_k (Eq. cg2).  Applied in place over the
+ * compacted free-row list (the "alternative technique"; SURVEY
+ * 8(a) a4 (iii)): only the free rows of A are read, no extraction, no n-long
+ * output.  v: n entries (read on F only); y_free: gpcg_free_count(h)
+ * entries; host or device, must not alias.  CSR and 3-D stencil handles on
+ * one slab and rank (GPCG_EINVAL otherwise); GPCG_ESTATE if no free set has
+ * been recorded.  Equals gpcg_hessvec(reduced = 1) at the free rows, bit for bit.
+ */
+GPCG_API int gpcg_hessvec_free(gpcg_problem *h, const double *v, double *y_free);
+
+/*
  * gpcg_project -- px = P[x] = mid(l, u, x) and records its free
  * set F = {i : l_i < px_i < u_i}.  Optional outputs (nullable):
  * ||grad_Omega q(px)||_2^2 (Eq. proj-gradient), |A(px)| and

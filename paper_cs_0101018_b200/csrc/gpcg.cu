@@ -203,6 +203,7 @@ struct Slab {
     unsigned char *xmask = nullptr, *xmaskcg = nullptr;
     // compacted free-row list (compact.cuh; CSR / 3-D operators, one slab): rows of mask fmask
     int* flist = nullptr;
+    unsigned* fbits = nullptr;      // the same set as bits (k_pack_bits: n / 8 bytes, L2-resident)
     long long *fblk = nullptr, *ftot = nullptr;
     long long fcount = -1;
     int fmask = -1;
@@ -512,7 +513,7 @@ void free_all(gpcg_problem* h) {
     for (Slab& S : h->slabs) {
         dfree(h, S.arena);
         for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, S.xarena, (void*)S.bjf, (void*)S.rp,
-                        (void*)S.flist, (void*)S.fblk, (void*)S.ftot,
+                        (void*)S.flist, (void*)S.fbits, (void*)S.fblk, (void*)S.ftot,
                         (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             dfree(h, p);
@@ -1405,12 +1406,15 @@ int build_free_list(gpcg_problem* h, Slab& S, int mk) {
         CK(dalloc(h, &S.flist, (size_t)std::max<long long>(n, 1) * sizeof(int)));
         CK(dalloc(h, &S.fblk, (size_t)(nblk + 1) * sizeof(long long)));
         CK(dalloc(h, &S.ftot, sizeof(long long)));
+        CK(dalloc(h, &S.fbits, (size_t)((n + 31) / 32 + 1) * sizeof(unsigned)));
     }
     k_scan_count<true><<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, S.m[mk], nullptr, S.fblk);
     k_scan_blocks<<<1, 1024, 0, h->st>>>(nblk, S.fblk, S.ftot);
     k_scan_assign<<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, S.m[mk], S.fblk, nullptr, S.flist);
+    if (h->pitch == h->rowlen)      // contiguous owned points (CSR, 3-D): the free bits for the reduced products
+        k_pack_bits<<<(unsigned)((n + kThreads - 1) / kThreads), kThreads, 0, h->st>>>(n, S.m[mk], S.fbits);
     CKLAUNCH();
-    h->launches += 3;
+    h->launches += 4;
     long long m = 0;
     CK(cudaMemcpyAsync(&m, S.ftot, sizeof(long long), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
@@ -2381,6 +2385,28 @@ int create_csr(gpcg_problem** out, const gpcg_dist* dist, void* stream, int64_t 
 // ============================================================================
 // ABI
 // ============================================================================
+// A_F v over the compacted free-row list of the recorded free set (compact_ok handles, S.fmask ==
+// h->free_mask): y_free[k] (|F| entries) and / or y_full at the free rows
+int launch_hessvec_free(gpcg_problem* h, Slab& S, const double* v, double* y_free, double* y_full) {
+    if (S.fcount <= 0) return GPCG_OK;
+    if (h->is_csr) {
+        // 4 rows per warp and kRowUnroll per group: one warp per 16 rows, up to 8 CTAs per SM resident
+        const long long rows_per_cta = (long long)(kThreads / 32) * (32 / kRowLanes) * kRowUnroll;
+        const int g = (int)std::max<long long>(
+            1, std::min<long long>((S.fcount + rows_per_cta - 1) / rows_per_cta, (long long)h->sms * 8));
+        k_hessvec_free_csr<<<g, kThreads, 0, h->st>>>(S.cop, S.fcount, S.flist, S.fbits, v, y_free, y_full);
+    } else {
+        const int g = (int)((S.fcount + kThreads - 1) / kThreads);
+        with_gop(h, S, [&](auto& op) {
+            using Op = std::decay_t<decltype(op)>;
+            k_hessvec_free<Op><<<g, kThreads, 0, h->st>>>(op, S.fcount, S.flist, S.fbits, v, y_free, y_full);
+        });
+    }
+    h->launches++;
+    CKLAUNCH();
+    return GPCG_OK;
+}
+
 extern "C" {
 
 gpcg_params gpcg_params_default(void) {
@@ -2503,6 +2529,38 @@ int gpcg_project(gpcg_problem* h, const double* x, double* px, double* pg_norm2,
     return leave(h);
 }
 
+int64_t gpcg_free_count(gpcg_problem* h) {
+    if (!h || h->free_mask < 0 || !compact_ok(h)) return -1;
+    const Slab& S = h->slabs[0];
+    return S.fmask == h->free_mask ? (int64_t)S.fcount : -1;
+}
+
+int gpcg_hessvec_free(gpcg_problem* h, const double* v, double* y_free) {
+    g_err.clear();
+    if (!h || !v || !y_free) return set_err(GPCG_EINVAL, "NULL argument");
+    if (h->free_mask < 0)
+        return set_err(GPCG_ESTATE, "reduced hessvec needs a free set: call gpcg_project or gpcg_solve first");
+    if (!compact_ok(h))
+        return set_err(GPCG_EINVAL, "gpcg_hessvec_free supports CSR / 3-D operators on one slab and rank");
+    RC(enter(h));
+    Slab& S = h->slabs[0];
+    if (S.fmask != h->free_mask || S.fcount < 0) RC(build_free_list(h, S, h->free_mask));
+    const long long m = S.fcount;
+    const bool vdev = is_device_ptr(v), ydev = is_device_ptr(y_free);
+    const double* vin = v;
+    if (!vdev) {
+        RC(upload_vec(h, VIN, v));
+        vin = S.v[VIN];
+    }
+    double* yout = ydev ? y_free : S.v[VOUT];
+    RC(launch_hessvec_free(h, S, vin, yout, nullptr));
+    if (!ydev && m > 0) {
+        CK(cudaMemcpyAsync(y_free, yout, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    return leave(h);
+}
+
 int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
     g_err.clear();
     if (!h || !v || !y) return set_err(GPCG_EINVAL, "NULL argument");
@@ -2534,14 +2592,7 @@ int gpcg_hessvec(gpcg_problem* h, const double* v, double* y, int reduced) {
                           10 * S.fcount < 3 * nown && h->prm.cg_mode != 0;
         if (rows) {
             CK(cudaMemsetAsync(yout, 0, (size_t)nown * sizeof(double), h->st));
-            if (S.fcount > 0) {
-                const int g = (int)std::max<long long>(
-                    1, std::min<long long>((S.fcount + kThreads - 1) / kThreads, (long long)h->sms * 16));
-                with_gop(h, S, [&](auto& op) {
-                    using Op = std::decay_t<decltype(op)>;
-                    k_hessvec_rows<Op><<<g, kThreads, 0, h->st>>>(op, S.fcount, S.flist, mask, vin, yout);
-                });
-            }
+            RC(launch_hessvec_free(h, S, vin, nullptr, yout));
         } else if (k4) {
             CUtensorMap mv;
             if (vin == S.v[VIN]) mv = S.t4[VIN];

@@ -23,7 +23,8 @@ STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "EINVAL", -2: "ENOMEM", -3: "EC
 # every symbol include/gpcg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["gpcg_params_default", "gpcg_create_stencil2d", "gpcg_create_stencil2d_dist",
            "gpcg_create_stencil3d", "gpcg_create_stencil3d_dist", "gpcg_create_csr",
-           "gpcg_create_csr_dist", "gpcg_set_params", "gpcg_solve", "gpcg_hessvec", "gpcg_project",
+           "gpcg_create_csr_dist", "gpcg_set_params", "gpcg_solve", "gpcg_hessvec", "gpcg_free_count",
+           "gpcg_hessvec_free", "gpcg_project",
            "gpcg_objective", "gpcg_size", "gpcg_destroy", "gpcg_last_error", "gpcg_partition_rows",
            "gpcg_nccl_unique_id"]
 
@@ -102,6 +103,10 @@ def load():
     L.gpcg_solve.argtypes = [P, P, dbl, i64, P, C.POINTER(Stats)]
     L.gpcg_hessvec.restype = i32
     L.gpcg_hessvec.argtypes = [P, P, P, i32]
+    L.gpcg_free_count.restype = i64
+    L.gpcg_free_count.argtypes = [P]
+    L.gpcg_hessvec_free.restype = i32
+    L.gpcg_hessvec_free.argtypes = [P, P, P]
     L.gpcg_project.restype = i32
     L.gpcg_project.argtypes = [P, P, P, C.POINTER(dbl), C.POINTER(i64), C.POINTER(i64)]
     L.gpcg_objective.restype = i32
@@ -361,6 +366,21 @@ class Solver:
         py, ky = _ptr(y, np.float64)
         _check(load().gpcg_hessvec(self._h, pv, py, 1 if reduced else 0))
         return y
+
+    def free_count(self):
+        """|F| of the recorded free set (-1: none, or no compacted free-row list for this handle)"""
+        return int(load().gpcg_free_count(self._h))
+
+    def hessvec_free(self, v, y_free=None):
+        """y_free[k] = (A_F v) at the k-th free index (compact output, gpcg_hessvec_free)"""
+        pv, kv = _ptr(v, np.float64)
+        if y_free is None:
+            y_free = _like(v, max(self.free_count(), 0))
+        py, ky = _ptr(y_free, np.float64)
+        _check(load().gpcg_hessvec_free(self._h, pv, py))
+        if ky is not y_free and not _is_torch(y_free):
+            y_free[...] = ky
+        return y_free
 
     def project(self, x, px=None):
         """-> (px, ||grad_Omega q(px)||^2, |A(px)|, |A(px) minus B(px)|)"""

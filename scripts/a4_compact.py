@@ -1,9 +1,11 @@
 """a4 microbenchmark for the small-free regime: one reduced HVP
 gpcg_hessvec(reduced=1) at the SOLUTION's free set of C4 (CSR) and C4s (3-D stencil), through
 the masked full-length kernel (cg_mode 0) and the compacted free-row list (cg_mode 2 / 3),
-L2 flushed before every rep, CUDA events around each call (the call clears y off F with a
-memset, then runs k_hessvec_rows over F).  Also one solve per mode (CG in place over F vs
-masked full-length).
+L2 flushed before every rep (the call enqueued while the flush runs, so the events time the
+GPU work and not the host's launch latency), CUDA events around each call (the call clears y off F with a
+memset, then runs the free-row kernels over F), and the compact-output product
+gpcg_hessvec_free (|F| outputs in the reduced space, no clear) for the free-row modes.  Also one
+solve per mode (CG in place over F vs masked full-length).
 
 usage: python scripts/a4_compact.py [C4 C4s]
 """
@@ -19,7 +21,7 @@ from paper_cs_0101018_b200 import problems as P, gpcg  # noqa: E402
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 out = []
-flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 1 GB: keeps the GPU busy while the host enqueues the call
 for name in (sys.argv[1:] or ["C4", "C4s"]):
     prob = P.get(name)
     stream = torch.cuda.current_stream()
@@ -41,8 +43,8 @@ for name in (sys.argv[1:] or ["C4", "C4s"]):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tt = []
         for _ in range(30):
-            flush.zero_()
             torch.cuda.synchronize()
+            flush.zero_()              # no sync: the host enqueues the call while the flush runs
             e0.record(stream)
             s.hessvec(v, y, True)
             e1.record(stream)
@@ -57,10 +59,28 @@ for name in (sys.argv[1:] or ["C4", "C4s"]):
             alg = (4.0 + 6 * 8.0 + 8.0 + 8.0) * m            # list + 6 face weights + x + y per free row
             what = "3-D stencil: m (4 free-list + 48 face weights + 8 x + 8 y)"
         zero = 8.0 * prob.n
+        # the compact-output product (gpcg_hessvec_free: |F| outputs, no n-long clear)
+        us_free = None
+        if mode != 0:
+            yc = torch.empty(max(s.free_count(), 1), dtype=torch.float64, device="cuda")
+            for _ in range(5):
+                s.hessvec_free(v, yc)
+            tf = []
+            for _ in range(30):
+                torch.cuda.synchronize()
+                flush.zero_()          # no sync: the host enqueues the call while the flush runs
+                e0.record(stream)
+                s.hessvec_free(v, yc)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tf.append(e0.elapsed_time(e1) * 1e3)
+            us_free = sorted(tf)[len(tf) // 2]
         r = {"config": name, "cg_mode": mode, "n": prob.n, "n_free": m, "solve_s": ts, "rc": rc,
              "cg_iters": st["cg_iters"], "hvp_us": us, "alg_bytes": alg, "alg_what": what,
              "frac_alg": alg / (us * 1e-6) / 1e9 / peak, "zero_fill_bytes": zero,
-             "frac_alg_plus_zero_fill": (alg + zero) / (us * 1e-6) / 1e9 / peak, "peak_gbs": peak}
+             "frac_alg_plus_zero_fill": (alg + zero) / (us * 1e-6) / 1e9 / peak, "peak_gbs": peak,
+             "hvp_free_us": us_free,
+             "frac_alg_free": (alg / (us_free * 1e-6) / 1e9 / peak) if us_free else None}
         print(json.dumps(r), flush=True)
         out.append(r)
         s.close()

@@ -827,6 +827,78 @@ def test_compact_free_rows_same_cg_iterates(G):
     assert np.max(np.abs(x0 - x3)) <= 1e-12 * np.max(np.abs(x0))
 
 
+HVFREE_CASES = {**COMPACT_CASES, "dense40": lambda: dense_problem(40, 3), "c4_family_m7": lambda: P.c4_family(m=7),
+                "c4s_family_9": lambda: P.c4_stencil_family(m=9)}
+
+
+def check_hessvec_free(G, oracle, s, prob, A, x, p):
+    """gpcg_hessvec_free at the free set of P[x] vs ora_spmv_masked on that set (1e-13), and vs
+    the full-length reduced product at the free rows (bitwise where that product also runs over
+    the free-row list: |F| < 0.3 n)."""
+    import torch
+    px, pg2, na, nnb = s.project(x)
+    free = (px > prob.l) & (px < prob.u)
+    m = int(free.sum())
+    assert s.free_count() == m
+    yf = s.hessvec_free(p)
+    assert yf.shape == (m,)
+    yr = s.hessvec(p, reduced=True)
+    if m == 0:
+        assert not np.any(yr)
+        return m
+    yref = oracle.spmv_masked(A, free, p)
+    spmv_close(yf, yref[free], abs_op(A, p * free)[free])
+    if 10 * m < 3 * prob.n:
+        assert np.array_equal(yf, yr[free])
+    else:
+        spmv_close(yf, yr[free], abs_op(A, p * free)[free])
+    yd = s.hessvec_free(torch.from_numpy(p).cuda())       # device in / out: same kernel, same bits
+    assert np.array_equal(yd.cpu().numpy(), yf)
+    return m
+
+
+@pytest.mark.parametrize("case", list(HVFREE_CASES))
+def test_hessvec_free_compact_output(G, oracle, case):
+    """the reduced product written in the reduced space (|F| entries, the
+    CSR-vector row groups for CSR, one thread per free row for the 3-D stencil) at a small, a
+    mid-size, an empty and the full free set; ESTATE before any free set is recorded."""
+    prob = HVFREE_CASES[case]()
+    A = oracle.problem_csr(prob)
+    p = 2.0 * P.uniform(78, 1, prob.n) - 1.0
+    fl, fu = np.isfinite(prob.l), np.isfinite(prob.u)
+    span = np.where(fl & fu, prob.u - prob.l, 1.0)
+    mid = np.where(fl & fu, 0.5 * (prob.l + prob.u),
+                   np.where(fl, prob.l + 0.5, np.where(fu, prob.u - 0.5, 0.0)))
+    with G.Solver.from_problem(prob) as s:
+        assert s.free_count() == -1
+        with pytest.raises(G.GpcgError) as e:
+            s.hessvec_free(p)
+        assert e.value.code == G.ESTATE
+        ms = []
+        for scale in (4.0, 0.9):          # x = mid + scale * (span / 2) * N(0, 1): most / few active
+            x = mid + scale * 0.5 * span * P.gaussian(79, 2, prob.n)
+            ms.append(check_hessvec_free(G, oracle, s, prob, A, x, p))
+        assert ms[0] < ms[1]
+        # every point at a bound -> |F| = 0 (when every point has one); every point free
+        if np.all(fl | fu):
+            out = np.where(fu, prob.u + 1.0, prob.l - 1.0)
+            assert check_hessvec_free(G, oracle, s, prob, A, out, p) == 0
+        assert check_hessvec_free(G, oracle, s, prob, A, mid, p) == prob.n
+
+
+def test_hessvec_free_c4_full_size(G, oracle):
+    """C4 (256^3 CSR, BASELINE.json configs[4]) at full size: the compact reduced product at a
+    ~5 %-free set, every one of its |F| outputs vs ora_spmv_masked."""
+    prob = P.c4()
+    A = oracle.problem_csr(prob)
+    p = 2.0 * P.uniform(80, 1, prob.n) - 1.0
+    x = 0.0125 * P.gaussian(81, 2, prob.n)             # |x| < 0.01 (free) for ~58 %; 1/20 of that
+    x[P.uniform(82, 3, prob.n) > 0.09] = 1.0            # ~5 % free, scattered like C4's solution
+    with G.Solver.from_problem(prob) as s:
+        m = check_hessvec_free(G, oracle, s, prob, A, x, p)
+    assert 0.02 * prob.n < m < 0.08 * prob.n
+
+
 # ------------------------------------------------------------------ CG sweep stage layouts (band / per-warp boxes)
 @pytest.mark.parametrize("pw", ["0", "1"])
 @pytest.mark.parametrize("case", ["C0", "jb80_eps0.9", "c3_family_160"])
