@@ -275,6 +275,14 @@ struct gpcg_problem {
     int grid6_gp = 1;
     size_t smem6_gp = 0;
     unsigned int* gbar = nullptr;   // grid-barrier counter of the persistent kernels
+    // cross-rank protocol of the multi-slab persistent loops (march_tma.cuh XRank):
+    // GPCG_XRANK_EMU=1 runs it on one device with every slab a virtual rank (one launch)
+    bool xr_emu = false;
+    unsigned long long* xr_bar = nullptr;     // [kMaxRanks][local, go, cross][kXrLine] counters (never reset)
+    unsigned long long* xr_base = nullptr;    // [kMaxRanks][kXrLine]: local, cross arrivals, barriers before a launch
+    double* xr_part = nullptr;                // [kMaxRanks][2][kXrSums][xr_stride] mailboxes
+    int* xr_err = nullptr;                    // spin-timeout flag
+    int xr_stride = 0;
     long long launches = 0;
     long long cg_iters_timed = 0, cg_free_iters_timed = 0;
     double t_cg_timed_ms = 0.0;
@@ -518,7 +526,8 @@ void free_all(gpcg_problem* h) {
                         (void*)S.partials, (void*)S.counter})
             dfree(h, p);
     }
-    for (void* p : {(void*)h->red_all, (void*)h->red_tot, (void*)h->lu0, (void*)h->dS, (void*)h->gbar})
+    for (void* p : {(void*)h->red_all, (void*)h->red_tot, (void*)h->lu0, (void*)h->dS, (void*)h->gbar,
+                    (void*)h->xr_bar, (void*)h->xr_base, (void*)h->xr_part, (void*)h->xr_err})
         dfree(h, p);
     if (h->hS) cudaFreeHost(h->hS);
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
@@ -600,8 +609,10 @@ int setup_tile(gpcg_problem* h) {
     RC(set_smem(k4_cg_iter<true>, m4cg::kSmem));
     RC(set_smem(k6_cg_loop<false>, m4cg::kSmem));
     RC(set_smem(k6_cg_loop<true>, m4cg::kSmem));
-    RC(set_smem(k6_cg_loop_ms<false>, m4cg::kSmem));
-    RC(set_smem(k6_cg_loop_ms<true>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop_ms<false, false>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop_ms<true, false>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop_ms<false, true>, m4cg::kSmem));
+    RC(set_smem(k6_cg_loop_ms<true, true>, m4cg::kSmem));
     RC(set_smem(k4_accept<true, true, false>, AccLayout4<true, true, false>::kSmem));
     RC(set_smem(k4_accept<true, false, false>, AccLayout4<true, false, false>::kSmem));
     RC(set_smem(k4_accept<false, true, false>, AccLayout4<false, true, false>::kSmem));
@@ -733,7 +744,8 @@ int setup_tile(gpcg_problem* h) {
             const size_t sm = std::max<size_t>(AccLayout5<SB, BB, m5::GP>::kSmem, SrchLayout5<SB, BB, m5::GP, 2>::kSmem);
             h->smem6_gp = sm;
             cudaFuncSetAttribute(k6_gp_loop<SB, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            cudaFuncSetAttribute(k6_gp_loop_ms<SB, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k6_gp_loop_ms<SB, BB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k6_gp_loop_ms<SB, BB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int nb = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k6_gp_loop<SB, BB>, m4::kThreads, sm);
             return std::max(1, nb) * h->sms;
@@ -804,6 +816,10 @@ int create_streams(gpcg_problem* h, void* stream) {
         h->pool = (e6 && e6[0] == '0') ? nullptr : mem_pool(h->dev);
     }
     CK(dalloc(h, &h->gbar, sizeof(unsigned int)));
+    {
+        const char* e7 = getenv("GPCG_XRANK_EMU");
+        h->xr_emu = e7 && atoi(e7) != 0;
+    }
     CK(cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev_a));
     CK(cudaEventCreate(&h->ev_b));
@@ -1283,6 +1299,54 @@ bool gp_persist(const gpcg_problem* h) {
     return h->gp_persistent && h->gfree && (!h->deferred || multi_slab_persistent(h));
 }
 
+// The XRank of a multi-slab persistent launch: nr = 0 (one device, the plain grid barrier), or
+// under GPCG_XRANK_EMU every slab a virtual rank with its own counter and mailbox (the cross-rank
+// protocol run inside one cooperative launch; same sums in the same order -> same bits).
+int make_xrank(gpcg_problem* h, const int* cta0, int nslabs, int total, XRank* X) {
+    memset(X, 0, sizeof *X);
+    if (!h->xr_emu) return GPCG_OK;
+    if (nslabs > kMaxRanks) return set_err(GPCG_EINVAL, "GPCG_XRANK_EMU: at most %d slabs", kMaxRanks);
+    if (!h->xr_bar) {
+        h->xr_stride = std::max(total, h->sms * 16);
+        const size_t nbar = (size_t)kMaxRanks * 3 * kXrLine, nbase = (size_t)kMaxRanks * kXrLine;
+        CK(dalloc(h, &h->xr_bar, nbar * sizeof(unsigned long long)));
+        CK(dalloc(h, &h->xr_base, nbase * sizeof(unsigned long long)));
+        CK(dalloc(h, &h->xr_part, (size_t)kMaxRanks * 2 * kXrSums * h->xr_stride * sizeof(double)));
+        CK(dalloc(h, &h->xr_err, sizeof(int)));
+        CK(cudaMemsetAsync(h->xr_bar, 0, nbar * sizeof(unsigned long long), h->st));
+        CK(cudaMemsetAsync(h->xr_base, 0, nbase * sizeof(unsigned long long), h->st));
+        CK(cudaMemsetAsync(h->xr_err, 0, sizeof(int), h->st));
+    }
+    if (total > h->xr_stride)
+        return set_err(GPCG_EINVAL, "GPCG_XRANK_EMU: launch of %d CTAs > mailbox %d", total, h->xr_stride);
+    X->nr = nslabs;
+    X->cta_base = 0;
+    X->cta_total = total;
+    X->cta_stride = h->xr_stride;
+    for (int r = 0; r < nslabs; ++r) {
+        X->cta0[r] = cta0[r];
+        X->lbar[r] = h->xr_bar + (size_t)(3 * r) * kXrLine;       // + kXrLine: the rank's go flag
+        X->bar[r] = h->xr_bar + (size_t)(3 * r + 2) * kXrLine;
+        X->base[r] = h->xr_base + (size_t)r * kXrLine;
+        X->part[r] = h->xr_part + (size_t)r * 2 * kXrSums * h->xr_stride;
+    }
+    X->cta0[nslabs] = total;
+    X->err = h->xr_err;
+    X->sys = getenv("GPCG_XRANK_SYS") && atoi(getenv("GPCG_XRANK_SYS")) != 0;   // A/B: system scope on one device
+    return GPCG_OK;
+}
+
+// after a launch with XRank: a spin that timed out (a rank that never arrived) is an error
+int check_xrank(gpcg_problem* h) {
+    if (!h->xr_err) return GPCG_OK;
+    int e = 0;
+    CK(cudaMemcpyAsync(&e, h->xr_err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (e) return set_err(GPCG_ECUDA, "cross-rank barrier: a rank did not arrive within %llu s",
+                          kXrSpinNs / 1000000000ull);
+    return GPCG_OK;
+}
+
 int launch_gp_loop_ms(gpcg_problem* h, int cur) {
     GpMsArgs P;
     memset(&P, 0, sizeof P);
@@ -1316,14 +1380,23 @@ int launch_gp_loop_ms(gpcg_problem* h, int cur) {
         X.cta0 = cta;
         cta += g;
     }
+    int c0[kMaxMs];
+    for (int s = 0; s < h->nslabs(); ++s) c0[s] = P.s[s].cta0;
+    XRank XR;
+    RC(make_xrank(h, c0, h->nslabs(), cta, &XR));
     CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
     double mu = h->prm.mu;
     int spec = h->gp_spec ? 1 : 0;
     void* args[] = {(void*)&P, (void*)&cur, (void*)&mu, (void*)&h->dS, (void*)&h->slabs[0].partials,
-                    (void*)&h->gbar, (void*)&spec};
+                    (void*)&h->gbar, (void*)&spec, (void*)&XR};
     const void* fn;
-    if (h->sb) fn = h->bb ? (const void*)k6_gp_loop_ms<true, true> : (const void*)k6_gp_loop_ms<true, false>;
-    else fn = h->bb ? (const void*)k6_gp_loop_ms<false, true> : (const void*)k6_gp_loop_ms<false, false>;
+    if (h->xr_emu) {
+        if (h->sb) fn = h->bb ? (const void*)k6_gp_loop_ms<true, true, true> : (const void*)k6_gp_loop_ms<true, false, true>;
+        else fn = h->bb ? (const void*)k6_gp_loop_ms<false, true, true> : (const void*)k6_gp_loop_ms<false, false, true>;
+    } else {
+        if (h->sb) fn = h->bb ? (const void*)k6_gp_loop_ms<true, true, false> : (const void*)k6_gp_loop_ms<true, false, false>;
+        else fn = h->bb ? (const void*)k6_gp_loop_ms<false, true, false> : (const void*)k6_gp_loop_ms<false, false, false>;
+    }
     CK(cudaLaunchCooperativeKernel(fn, dim3(cta), dim3(m4::kThreads), args, h->smem6_gp, h->st));
     h->launches++;
     return GPCG_OK;
@@ -1888,14 +1961,22 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
             X.cta0 = cta;
             cta += S.grid4_cg;
         }
+        int c0[kMaxMs];
+        for (int s = 0; s < h->nslabs(); ++s) c0[s] = P.s[s].cta0;
+        XRank XR;
+        RC(make_xrank(h, c0, h->nslabs(), cta, &XR));
         CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
         CK(cudaEventRecord(h->ev_c0, h->st));
-        void* args[] = {(void*)&P, (void*)&h->dS, (void*)&h->slabs[0].partials, (void*)&h->gbar};
-        const void* fn = h->prm.precond == 1 ? (const void*)k6_cg_loop_ms<true> : (const void*)k6_cg_loop_ms<false>;
+        void* args[] = {(void*)&P, (void*)&h->dS, (void*)&h->slabs[0].partials, (void*)&h->gbar, (void*)&XR};
+        const void* fn = h->xr_emu ? (h->prm.precond == 1 ? (const void*)k6_cg_loop_ms<true, true>
+                                                            : (const void*)k6_cg_loop_ms<false, true>)
+                                   : (h->prm.precond == 1 ? (const void*)k6_cg_loop_ms<true, false>
+                                                            : (const void*)k6_cg_loop_ms<false, false>);
         CK(cudaLaunchCooperativeKernel(fn, dim3(cta), dim3(m4::kThreadsWS), args, (size_t)m4cg::kSmem, h->st));
         CK(cudaEventRecord(h->ev_c1, h->st));
         h->launches++;
         RC(sync_scal(h));
+        RC(check_xrank(h));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, h->ev_c0, h->ev_c1));
         h->t_cg_timed_ms += ms;
@@ -2687,6 +2768,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                         h->launches += (long long)h->gp_exec_chunk * launches_per_gp_step(h);
                     }
                     if ((rc = sync_scal(h))) goto fail;
+                    if (persist && (rc = check_xrank(h))) goto fail;
                     const long long jn = S.gp_j;
                     if (persist) st.gp_spec_rejected += S.gp_fb;
                     cur = (int)((cur + (jn - jdone)) & 1);

@@ -511,11 +511,172 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
     __syncthreads();
 }
 
+// ---------------------------------------------------------------- cross-rank groups
+// The persistent loops spanning several ranks (one device each, or -- the one-launch emulation
+// GPCG_XRANK_EMU -- several CTA groups of one launch).  Every rank owns, in its own memory, a
+// local counter (its CTAs' arrivals), a go flag, a cross counter (one arrival per rank and
+// barrier) and a partial-sum mailbox with a row per global CTA id; the other ranks reach the
+// cross counter and the mailbox through peer mappings.  One reduction:
+//   1. every CTA stores its block partials into EVERY rank's mailbox at its global id and
+//      arrives on its rank's local counter (release, gpu scope);
+//   2. the rank's leader (its first CTA) waits for the rank's CTAs (acquire, gpu), fences at
+//      system scope and arrives on EVERY rank's cross counter; it waits for its own cross
+//      counter to count every rank (relaxed polls, then an acquire fence at system scope) and
+//      releases its rank through the go flag (gpu scope);
+//   3. every CTA sums its own rank's mailbox over all global ids in order -- so every rank
+//      forms the same bits and takes the same decision with no second round trip.
+// The PTX memory model's causality order is transitive: a CTA's stores to a peer (ghost rows,
+// partials) precede its local release, which the leader acquires before its system-scope
+// release -- so only the leaders' two operations per reduction need system scope (gpu scope in
+// the one-device emulation, whose ranks share the device).  One NVLink
+// round trip per reduction and nr cross arrivals per rank, whatever the CTA count.
+// Counters are never reset: a rank's base (its counters and barrier count before the running
+// launch) is advanced by the rank's leader at the end of each launch; every rank runs the same
+// barriers (identical decisions), so all bases agree.  The mailbox slot is the parity of the
+// GLOBAL barrier count and the slots' layout does not depend on the launch's CTA count, so a
+// fast rank's first partials of the next launch never land in the slot a slow rank is still
+// summing.  A spin that outlasts kXrSpinNs sets *err and lets the CTA go on (the host turns it
+// into an error instead of a hang).
+constexpr int kMaxRanks = 8;
+constexpr int kXrSums = 8;                    // sums per reduction (GP accept: 8, CG: 2)
+constexpr int kXrLine = 16;                   // u64 per counter: one 128-byte line each
+constexpr unsigned long long kXrSpinNs = 20ull * 1000 * 1000 * 1000;
+struct XRank {
+    int nr;                                   // ranks
+    int cta_base;                             // global id of this launch's CTA 0
+    int cta_total;                            // CTAs over all ranks in this launch
+    int cta_stride;                           // mailbox row length (>= cta_total of every launch)
+    int cta0[kMaxRanks + 1];                  // global CTA range of rank r: [cta0[r], cta0[r + 1])
+    unsigned long long* lbar[kMaxRanks];      // rank r's local counter (own rank only); lbar + kXrLine: its go flag
+    unsigned long long* bar[kMaxRanks];       // rank r's cross counter
+    unsigned long long* base[kMaxRanks];      // rank r's {local, cross, barriers} before the launch (own rank only)
+    double* part[kMaxRanks];                  // rank r's mailbox: [2 slots][kXrSums][cta_stride]
+    int* err;                                 // this rank's spin-timeout flag
+    int sys;                                  // ranks on several devices: the leaders' operations at system
+                                              // scope (the one-device emulation: gpu scope suffices)
+};
+struct XCtx {
+    int me;                                   // this CTA's rank
+    int gid;                                  // global CTA id
+    int tr;                                   // CTAs of this rank
+    bool leader;                              // the rank's first CTA
+    unsigned long long lb0, xb0, n0;          // the rank's base (local, cross arrivals; barriers)
+};
+
+__device__ __forceinline__ XCtx xr_ctx(const XRank& X) {
+    XCtx c;
+    c.gid = X.cta_base + (int)blockIdx.x;
+    c.me = 0;
+    while (c.me + 1 < X.nr && c.gid >= X.cta0[c.me + 1]) ++c.me;
+    c.tr = X.cta0[c.me + 1] - X.cta0[c.me];
+    c.leader = c.gid == X.cta0[c.me];
+    const volatile unsigned long long* b = X.base[c.me];
+    c.lb0 = b[0];
+    c.xb0 = b[1];
+    c.n0 = b[2];
+    return c;
+}
+
+__device__ __forceinline__ unsigned long long xr_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// spin until *ctr >= target: acquire loads at gpu scope, or (cross) relaxed loads and one acquire
+// fence at system scope (gpu scope when sys == 0)
+template <bool CROSS>
+__device__ __forceinline__ void xr_wait(const unsigned long long* ctr, unsigned long long target, int* err,
+                                        int sys = 0) {
+    unsigned long long v;
+    const unsigned long long t0 = xr_now();
+    for (;;) {
+        if (CROSS && sys) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        else if (CROSS) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        if (v >= target) break;
+        if (xr_now() - t0 > kXrSpinNs) { atomicExch(err, 1); break; }
+    }
+    if (CROSS && sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else if (CROSS) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// reduction number gen of this launch (every thread counts)
+__device__ __forceinline__ void xr_barrier(const XRank& X, const XCtx& c, unsigned int& gen) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long xtarget = c.xb0 + (unsigned long long)(gen + 1) * (unsigned long long)X.nr;
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(X.lbar[c.me]) : "memory");
+        if (c.leader) {
+            xr_wait<false>(X.lbar[c.me], c.lb0 + (unsigned long long)(gen + 1) * (unsigned long long)c.tr, X.err);
+            if (X.sys) {
+                asm volatile("fence.acq_rel.sys;" ::: "memory");
+                for (int r = 0; r < X.nr; ++r)
+                    asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(X.bar[r]) : "memory");
+            } else {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                for (int r = 0; r < X.nr; ++r)
+                    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(X.bar[r]) : "memory");
+            }
+            xr_wait<true>(X.bar[c.me], xtarget, X.err, X.sys);
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(X.lbar[c.me] + kXrLine), "l"(xtarget)
+                         : "memory");
+        } else {
+            xr_wait<false>(X.lbar[c.me] + kXrLine, xtarget, X.err);
+        }
+    }
+    ++gen;
+    __syncthreads();
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // peers' ghost-row stores before this CTA's TMA loads
+}
+
+// fixed-order sum of NS block partials over every rank's CTAs (the same bits on every rank)
+template <int NS>
+__device__ __forceinline__ void xr_grid_sum(double (&acc)[NS], const XRank& X, const XCtx& c, unsigned int& gen,
+                                            double* red, double* tot) {
+    block_reduce<NS>(acc, red);
+    const size_t T = (size_t)X.cta_stride;
+    const size_t off = (size_t)((c.n0 + gen) & 1ull) * kXrSums * T;
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) tot[q] = acc[q];
+    __syncthreads();
+    for (int i = threadIdx.x; i < X.nr * NS; i += blockDim.x) {      // this CTA's row, into every mailbox
+        const int r = i / NS, q = i - r * NS;
+        X.part[r][off + q * T + c.gid] = tot[q];
+    }
+    xr_barrier(X, c, gen);
+    const double* pp = X.part[c.me] + off;
+    double t[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) t[q] = 0.0;
+    for (unsigned int b = threadIdx.x; b < (unsigned int)X.cta_total; b += blockDim.x)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) t[q] += __ldcg(pp + q * T + b);
+    block_reduce<NS>(t, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) tot[q] = t[q];
+    __syncthreads();
+}
+
+// end of a launch: the rank's leader advances the rank's base by the launch's barriers
+__device__ __forceinline__ void xr_close(const XRank& X, const XCtx& c, unsigned int gen) {
+    if (threadIdx.x == 0 && c.leader) {
+        unsigned long long* b = X.base[c.me];
+        b[0] = c.lb0 + (unsigned long long)gen * (unsigned long long)c.tr;
+        b[1] = c.xb0 + (unsigned long long)gen * (unsigned long long)X.nr;
+        b[2] = c.n0 + gen;
+    }
+}
+
 // The CG call loop shared by the single- and multi-slab persistent kernels: per iteration
 // sweep(a, alpha, beta, acc, k) -> block partials -> grid barrier -> fixed-order sum of all
 // CTAs' partials (the same in every CTA) -> cg_finalize evaluated in every CTA.
-template <class Sweep>
-__device__ __forceinline__ void cg_loop(Scal* S, double* __restrict__ part, unsigned int* gbar, Sweep&& sweep) {
+template <bool XR = false, class Sweep>
+__device__ __forceinline__ void cg_loop(Scal* S, double* __restrict__ part, unsigned int* gbar, Sweep&& sweep,
+                                        const XRank* X = nullptr) {
     __shared__ double red[2 * 32];
     __shared__ double tot[2];
     // CG state (identical in every CTA)
@@ -527,27 +688,36 @@ __device__ __forceinline__ void cg_loop(Scal* S, double* __restrict__ part, unsi
     unsigned int gen = 0;
     int k = 0;
     const unsigned int G_ = gridDim.x;
+    __shared__ XCtx xc;                           // in shared memory: no registers held across the sweeps
+    if constexpr (XR) {
+        if (threadIdx.x == 0) xc = xr_ctx(*X);
+        __syncthreads();
+    }
     while (!done) {
         const int a = (int)(it & 1);
         double acc[2] = {0.0, 0.0};
         k = sweep(a, alpha, beta, acc, k);
-        // block partials -> part[parity][s][block]
-        block_reduce<2>(acc, red);
-        double* pp = part + (it & 1) * 2 * G_;
-        if (threadIdx.x == 0) {
-            pp[blockIdx.x] = acc[0];
-            pp[G_ + blockIdx.x] = acc[1];
+        if constexpr (XR) {
+            xr_grid_sum<2>(acc, *X, xc, gen, red, tot);
+        } else {
+            // block partials -> part[parity][s][block]
+            block_reduce<2>(acc, red);
+            double* pp = part + (it & 1) * 2 * G_;
+            if (threadIdx.x == 0) {
+                pp[blockIdx.x] = acc[0];
+                pp[G_ + blockIdx.x] = acc[1];
+            }
+            grid_barrier(gbar, G_, gen);
+            // fixed-order sum of the partials, same in every CTA
+            double t[2] = {0.0, 0.0};
+            for (unsigned int b = threadIdx.x; b < G_; b += blockDim.x) {
+                t[0] += __ldcg(pp + b);
+                t[1] += __ldcg(pp + G_ + b);
+            }
+            block_reduce<2>(t, red);
+            if (threadIdx.x == 0) { tot[0] = t[0]; tot[1] = t[1]; }
+            __syncthreads();
         }
-        grid_barrier(gbar, G_, gen);
-        // fixed-order sum of the partials, same in every CTA
-        double t[2] = {0.0, 0.0};
-        for (unsigned int b = threadIdx.x; b < G_; b += blockDim.x) {
-            t[0] += __ldcg(pp + b);
-            t[1] += __ldcg(pp + G_ + b);
-        }
-        block_reduce<2>(t, red);
-        if (threadIdx.x == 0) { tot[0] = t[0]; tot[1] = t[1]; }
-        __syncthreads();
         const double gamma = tot[0], delta = tot[1];
         // cg_finalize (fin.cuh), evaluated in every CTA
         const double dec = 0.5 * alpha * gamma_old;
@@ -577,7 +747,8 @@ __device__ __forceinline__ void cg_loop(Scal* S, double* __restrict__ part, unsi
             S->cg_done = done;
         }
     }
-    // the host zeroes the barrier counter before each launch
+    if constexpr (XR) xr_close(*X, xc, gen);
+    // (one device: the host zeroes the barrier counter before each launch)
 }
 
 template <bool PC>
@@ -597,7 +768,8 @@ k6_cg_loop(StencilOp A, BandGeom G, const __grid_constant__ CUtensorMap m_rho0, 
 
 // k6_cg_loop over several slabs of one device (SlabLink): each slab's CTAs sweep its rows and
 // write the rows its neighbours keep as ghosts into their ghost rows as well; one grid
-// barrier and one fixed-order sum over all CTAs per iteration, as with one slab.
+// barrier and one fixed-order sum over all CTAs per iteration, as with one slab.  XR: the
+// reductions through the cross-rank protocol (XRank) instead of the one-device grid barrier.
 constexpr int kMaxMs = 8;
 struct CgMsSlab {
     CUtensorMap m_rho0, m_rho1, m_p0, m_p1, m_w, m_mask;
@@ -616,22 +788,24 @@ struct CgMsArgs {
     int pw;                                       // per-warp boxes (cg_sweep4)
 };
 
-template <bool PC>
+template <bool PC, bool XR>
 __global__ void __launch_bounds__(m4::kThreadsWS, GPCG_CG_MINB)
-k6_cg_loop_ms(const __grid_constant__ CgMsArgs P, Scal* S, double* __restrict__ part, unsigned int* gbar) {
+k6_cg_loop_ms(const __grid_constant__ CgMsArgs P, Scal* S, double* __restrict__ part, unsigned int* gbar,
+              const __grid_constant__ XRank XRk) {
     extern __shared__ __align__(128) unsigned char smem[];
     int si = 0;
     while (si + 1 < P.nslabs && (int)blockIdx.x >= P.s[si + 1].cta0) ++si;
     const CgMsSlab& X = P.s[si];
     SlabLink L = X.L;
     L.bid = (int)blockIdx.x - X.cta0;
-    cg_loop(S, part, gbar, [&](int a, double alpha, double beta, double (&acc)[2], int k) {
+    auto body = [&](int a, double alpha, double beta, double (&acc)[2], int k) {
         return cg_sweep4<PC>(X.A, X.G, a ? &X.m_rho1 : &X.m_rho0, a ? &X.m_p1 : &X.m_p0, &X.m_w, &X.m_mask,
                              a ? X.rho0 : X.rho1, a ? X.p0 : X.p1, X.w, alpha, beta, smem, acc, k, X.flags,
                              P.pw != 0, &L,
                              a ? X.lo_rho0 : X.lo_rho1, a ? X.lo_p0 : X.lo_p1, a ? X.hi_rho0 : X.hi_rho1,
                              a ? X.hi_p0 : X.hi_p1);
-    });
+    };
+    cg_loop<XR>(S, part, gbar, body, &XRk);
 }
 
 // ============================================================================
@@ -1536,9 +1710,10 @@ __device__ __forceinline__ void grid_sum(double (&acc)[NS], double* part, unsign
 // The GP phase loop shared by the single- and multi-slab persistent kernels.  spec(cur, alpha_0,
 // acc8, k), search(cur, al, acc4, k), accept(cur, alpha, acc6, k) run one sweep of this CTA's
 // items from the y / mask buffers `cur` and return the CTA's running TMA block count.
-template <class Spec, class Search, class Accept>
+template <bool XR = false, class Spec, class Search, class Accept>
 __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __restrict__ part, unsigned int* gbar,
-                                        int spec, Spec&& spec_fn, Search&& search_fn, Accept&& accept_fn) {
+                                        int spec, Spec&& spec_fn, Search&& search_fn, Accept&& accept_fn,
+                                        const XRank* X = nullptr) {
     __shared__ double red[8 * 32];
     __shared__ double tot[8];
     if (S->gp_done) return;
@@ -1559,6 +1734,18 @@ __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __
     unsigned int gen = 0;
     int k = 0, red_i = 0;
     int cur = cur0;
+    __shared__ XCtx xc;                           // in shared memory: no registers held across the sweeps
+    if constexpr (XR) {
+        if (threadIdx.x == 0) xc = xr_ctx(*X);
+        __syncthreads();
+    }
+    // one reduction: the one-device grid sum, or the cross-rank one
+    auto gsum = [&](auto& acc) {
+        constexpr int NS = (int)(sizeof(acc) / sizeof(double));
+        if constexpr (XR) xr_grid_sum<NS>(acc, *X, xc, gen, red, tot);
+        else grid_sum<NS>(acc, part + (red_i & 1) * 8 * G_, G_, gbar, gen, red, tot);
+        ++red_i;
+    };
     while (!done) {
         if (!cauchy_ok) { s_h = -1; done = 1; reason = GP_HOST; break; }
         bool have_accept = false;
@@ -1570,7 +1757,7 @@ __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __
             // speculative accept at alpha_0 with the h = 0 search sums (one sweep when accepted)
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             k = spec_fn(cur, alpha0, acc, k);
-            grid_sum<8>(acc, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
+            gsum(acc);
             const double gs = tot[6], sAs = tot[7];
             const double dq = gs + 0.5 * sAs;
             if (dq <= mu * gs) {                         // Eq. gplsstop at h = 0
@@ -1585,7 +1772,7 @@ __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __
             const double al[2] = {scalbn(alpha0, -h0), scalbn(alpha0, -(h0 + 1))};
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             k = search_fn(cur, al, acc, k);
-            grid_sum<4>(acc, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
+            gsum(acc);
             s_h = -1;
             for (int h = 0; h < 2; ++h) {
                 const double gs = tot[2 * h], sAs = tot[2 * h + 1];
@@ -1602,7 +1789,7 @@ __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __
             // ---- accept y' = P[y - s_alpha g], regrad sums, free mask, next Cauchy form
             double acc6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             k = accept_fn(cur, s_alpha, acc6, k);
-            grid_sum<6>(acc6, part + (red_i++ & 1) * 8 * G_, G_, gbar, gen, red, tot);
+            gsum(acc6);
         }
         pg2 = tot[0]; g2 = tot[1]; n_active = tot[2]; n_changed = tot[3]; n_nb = tot[4];
         dd = tot[0]; dAd = tot[5];
@@ -1627,6 +1814,7 @@ __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __
         S->s_pad = s_spec;                         // GP_HOST after a search: resume the search at h = s_spec
         S->gp_fb = nfb;
     }
+    if constexpr (XR) xr_close(*X, xc, gen);
 }
 
 template <bool SB, bool BB>
@@ -1681,10 +1869,10 @@ struct GpMsArgs {
     int nslabs;
 };
 
-template <bool SB, bool BB>
+template <bool SB, bool BB, bool XR>
 __global__ void __launch_bounds__(m4::kThreads, GPCG_GP_MINB)
 k6_gp_loop_ms(const __grid_constant__ GpMsArgs P, int cur0, double mu, Scal* S, double* __restrict__ part,
-              unsigned int* gbar, int spec) {
+              unsigned int* gbar, int spec, const __grid_constant__ XRank XRk) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[4];
     int si = 0;
@@ -1692,27 +1880,26 @@ k6_gp_loop_ms(const __grid_constant__ GpMsArgs P, int cur0, double mu, Scal* S, 
     const GpMsSlab& X = P.s[si];
     SlabLink Ls = X.Ls, La = X.La;
     Ls.bid = La.bid = (int)blockIdx.x - X.cta0;
-    gp_loop(
-        cur0, mu, S, part, gbar, spec,
-        [&](int cur, double alpha0, double (&acc)[8], int k) {
-            return spec_sweep6<SB, BB>(X.A, X.Ga, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u,
-                                       cur ? &X.m_m1 : &X.m_m0, alpha0, cur ? X.y0p : X.y1p, cur ? X.mk0 : X.mk1,
-                                       smem, acc, bars, k, &La, cur ? X.lo_y0 : X.lo_y1, cur ? X.lo_m0 : X.lo_m1,
-                                       cur ? X.hi_y0 : X.hi_y1, cur ? X.hi_m0 : X.hi_m1);
-        },
-        [&](int cur, const double (&al)[2], double (&acc)[4], int k) {
-            return search_sweep5<SB, BB, m5::GP, 2>(X.A, X.Gs, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0,
-                                                    cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u, al, smem, acc,
-                                                    bars, k, &Ls);
-        },
-        [&](int cur, double alpha, double (&acc)[6], int k) {
-            return accept_sweep5<SB, BB, m5::GP>(X.A, X.Ga, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0,
-                                                 cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u,
-                                                 cur ? &X.m_m1 : &X.m_m0, 1, alpha, cur ? X.y0p : X.y1p,
-                                                 cur ? X.mk0 : X.mk1, smem, acc, bars, k, &La,
-                                                 cur ? X.lo_y0 : X.lo_y1, cur ? X.lo_m0 : X.lo_m1,
-                                                 cur ? X.hi_y0 : X.hi_y1, cur ? X.hi_m0 : X.hi_m1);
-        });
+    auto sp = [&](int cur, double alpha0, double (&acc)[8], int k) {
+        return spec_sweep6<SB, BB>(X.A, X.Ga, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u,
+                                   cur ? &X.m_m1 : &X.m_m0, alpha0, cur ? X.y0p : X.y1p, cur ? X.mk0 : X.mk1,
+                                   smem, acc, bars, k, &La, cur ? X.lo_y0 : X.lo_y1, cur ? X.lo_m0 : X.lo_m1,
+                                   cur ? X.hi_y0 : X.hi_y1, cur ? X.hi_m0 : X.hi_m1);
+    };
+    auto se = [&](int cur, const double (&al)[2], double (&acc)[4], int k) {
+        return search_sweep5<SB, BB, m5::GP, 2>(X.A, X.Gs, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0,
+                                                cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u, al, smem, acc,
+                                                bars, k, &Ls);
+    };
+    auto ac = [&](int cur, double alpha, double (&acc)[6], int k) {
+        return accept_sweep5<SB, BB, m5::GP>(X.A, X.Ga, X.Bd, X.brow, cur ? &X.m_y1 : &X.m_y0,
+                                             cur ? &X.m_y1 : &X.m_y0, &X.m_b, &X.m_l, &X.m_u,
+                                             cur ? &X.m_m1 : &X.m_m0, 1, alpha, cur ? X.y0p : X.y1p,
+                                             cur ? X.mk0 : X.mk1, smem, acc, bars, k, &La,
+                                             cur ? X.lo_y0 : X.lo_y1, cur ? X.lo_m0 : X.lo_m1,
+                                             cur ? X.hi_y0 : X.hi_y1, cur ? X.hi_m0 : X.hi_m1);
+    };
+    gp_loop<XR>(cur0, mu, S, part, gbar, spec, sp, se, ac, &XRk);
 }
 
 }  // namespace gpcg

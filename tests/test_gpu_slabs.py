@@ -193,3 +193,36 @@ def test_multi_slab_persistent_loops_match_single_slab_per_step(G, slabs):
     assert (st1["gp_iters"], st1["cg_iters"]) == (sts["gp_iters"], sts["cg_iters"])
     assert st1["cg_iters"] == 12 and st1["gp_iters"] >= 2
     assert np.max(np.abs(x1 - xs)) <= 1e-11 * max(np.max(np.abs(x1)), 1e-300)
+
+
+@pytest.mark.parametrize("slabs", [2, 3, 5, 8])
+@pytest.mark.parametrize("case", ["C0", "ragged29x17_bcast", "c3_family_160"])
+def test_cross_rank_protocol_emulated(G, oracle, monkeypatch, case, slabs):
+    """The cross-rank protocol of the persistent loops (march_tma.cuh XRank: per-rank arrival
+    counters never reset, partials stored into every rank's mailbox, each rank summing its own
+    copy in global CTA order, the mailbox slot from the global barrier count) run inside one
+    cooperative launch with every slab a virtual rank (GPCG_XRANK_EMU=1): bit for bit the
+    one-device multi-slab loops, over every launch of a solve and of a second solve on the same
+    handle (counters and bases carried across launches), and the oracle's solution."""
+    make, tol = CASES[case]
+    prob = make()
+    if prob.ny < 3 * slabs:
+        pytest.skip("too few rows for this many slabs (3 ghost rows)")
+    res = {}
+    for emu in ("0", "1"):
+        monkeypatch.setenv("GPCG_XRANK_EMU", emu)
+        with G.Solver.from_problem(prob, slabs=slabs) as s:
+            r1 = s.solve(prob.x0, tol)
+            r2 = s.solve(prob.x0, tol)
+        res[emu] = (r1, r2)
+    (a1, a2), (b1, b2) = res["0"], res["1"]
+    for (rc, x, st), (rcb, xb, stb) in ((a1, b1), (a2, b2), (b1, b2)):
+        assert rc == 0 and rcb == 0, (st, stb)
+        assert np.array_equal(x, xb)
+        for k in ("outer_iters", "gp_iters", "cg_iters"):
+            assert st[k] == stb[k], k
+    assert b1[2]["cg_iters"] > 0 and b1[2]["gp_iters"] > 1
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    rc, x, st = b1
+    assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+    assert np.max(np.abs(x - x_o)) <= 1e-7
