@@ -224,8 +224,16 @@ struct Scal {
     long long gp_j, gp_cap;
     int gp_done, gp_reason;
     int gp_fb, gp_pad;               // k6_gp_loop: steps whose speculative sweep was rejected (diagnostic)
+    int spec_ok, spec_pad;           // k_spec accepted this GP step's h = 0 (its search / accept sweeps skip)
 };
 enum GpReason : int { GP_RUNNING = 0, GP_STOP = 1, GP_CONV = 2, GP_HOST = 3 };
+
+// A device-driven GP-phase search / accept sweep with nothing to do: the phase is over, or this
+// step's speculative sweep (k_spec) was accepted.
+__device__ __forceinline__ bool gp_skip(const Scal* S) {
+    return *(const volatile int*)&S->gp_done || *(const volatile int*)&S->spec_ok;
+}
+
 
 // ----------------------------------------------------------------------------
 // deterministic two-stage reduction

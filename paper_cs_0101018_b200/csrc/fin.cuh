@@ -53,6 +53,25 @@ __device__ __forceinline__ void fin_search(const double* t, int K, int h0, doubl
     }
 }
 
+// a1 + a3 speculative (k_spec): t = <g,s>, <s,As> of h = 0, then the accept sums of the point
+// it wrote.  Eq. gplsstop at h = 0 holds -> the step is taken (s_h = 0, the search / accept
+// sweeps of the step skip); else s_h = -1 and they run from h = 1.
+__device__ __forceinline__ void fin_spec(const double* t, double mu, Scal* S) {
+    const double gs = t[0], sAs = t[1];
+    const double dq = gs + 0.5 * sAs;
+    if (dq <= mu * gs) {
+        S->spec_ok = 1;
+        S->s_h = 0;
+        S->s_alpha = S->alpha0;
+        S->s_delta = dq;
+        S->s_gs = gs;
+        fin_accept(t + 2, false, S);
+    } else {
+        S->spec_ok = 0;
+        S->s_h = -1;
+    }
+}
+
 // a5 init: gamma_0 = rho_0'rho_0, delta_0 = rho_0'A_F rho_0.
 __device__ __forceinline__ void cg_init_finalize(double gamma, double delta, double eta2, long long cap, Scal* S) {
     S->cg_it = 0;
@@ -156,6 +175,7 @@ enum FinKind : int {
     FIN_PCG2_INIT = 7,   // block-Jacobi ILU PCG (bjilu.cuh): gamma_0
     FIN_PCG2_ALPHA = 8,  //   p'A p -> alpha
     FIN_PCG2_BETA = 9,   //   r'z -> decrease, stop tests, beta
+    FIN_SPEC = 10,       // k_spec: h = 0 search sums + accept sums
 };
 
 struct FinArgs {
@@ -180,6 +200,8 @@ __global__ void k_combine(const double* __restrict__ per_slab, int nslabs, int n
 __global__ void k_finalize(const double* __restrict__ t, Scal* S, FinArgs a) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (a.gp && S->gp_done) return;               // a sweep of a finished device-driven GP phase
+    if (a.gp && S->spec_ok && (a.kind == FIN_SEARCH || a.kind == FIN_ACCEPT || a.kind == FIN_ACCEPT5))
+        return;                                   // ... or of a step k_spec took
     switch (a.kind) {
         case FIN_ACCEPT:
         case FIN_ACCEPT5:
@@ -213,6 +235,10 @@ __global__ void k_finalize(const double* __restrict__ t, Scal* S, FinArgs a) {
         case FIN_PCG2_BETA:
             pcg2_beta_fin(t[0], S);
             break;
+        case FIN_SPEC:
+            if (!S->cauchy_ok) { S->spec_ok = 0; S->s_h = -1; return; }
+            fin_spec(t, a.mu, S);
+            break;
     }
 }
 
@@ -228,6 +254,7 @@ __global__ void k_gp_begin(Scal* S, double tau, double eta1, long long gp_cap) {
     S->gp_last_dec = 0.0;
     S->gp_done = 0;
     S->gp_reason = GP_RUNNING;
+    S->spec_ok = 0;
     if (sqrt(S->pg2) <= tau) { S->gp_done = 1; S->gp_reason = GP_CONV; }
 }
 
@@ -238,6 +265,7 @@ __global__ void k_gp_begin(Scal* S, double tau, double eta1, long long gp_cap) {
 // Cauchy step with <d,Ad> <= 0) hands the step back to the host (GP_HOST).
 __global__ void k_gp_step(Scal* S) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    S->spec_ok = 0;                                      // the next step's sweeps run
     if (S->gp_done) return;
     if (S->s_h < 0) { S->gp_done = 1; S->gp_reason = GP_HOST; return; }
     const long long j = ++S->gp_j;

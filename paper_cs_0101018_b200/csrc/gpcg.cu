@@ -1055,6 +1055,32 @@ int launch_cauchy(gpcg_problem* h, int y, int g, int gp = 0) {
     return finish_reduce(h, a, 2);
 }
 
+// The GP graph of the generic operators (CSR, 3-D) takes each step speculatively at h = 0
+// (k_spec: search sums + accept in one sweep; GPCG_GP_SPEC=0: off); the 2-D stencils fuse the
+// step into their own sweeps (k6_gp_loop, spec_sweep6).
+bool graph_spec(const gpcg_problem* h) { return h->gp_spec && !spec2d(h); }
+
+int launch_spec(gpcg_problem* h, int cur, int nxt) {
+    const double mu = h->prm.mu;
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const Bounds B = h->bounds(S);
+        with_gop_sb(h, S, [&](auto& op, auto sbt) {
+            using Op = std::decay_t<decltype(op)>;
+            constexpr bool SB = decltype(sbt)::value;
+            k_spec<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[vy(cur)], S.v[vg(cur)], S.v[vy(nxt)],
+                                                          S.v[vg(nxt)], S.m[mk(nxt)], mu, h->dS, h->red(s));
+        });
+        h->launches++;
+        CKLAUNCH();
+    }
+    FinArgs a = fin(FIN_SPEC);
+    a.mu = mu;
+    a.gp = 1;
+    RC(finish_reduce(h, a, 7));
+    return exchange(h, {vy(nxt), vg(nxt)}, {mk(nxt)});
+}
+
 // step sizes per projected-search sweep: the first sweep evaluates search_k
 // (2 or 8 instantiated), later sweeps 8
 int first_k(const gpcg_problem* h) { return h->prm.search_k <= 2 ? 2 : 8; }
@@ -1265,7 +1291,8 @@ int build_gp_graph(gpcg_problem* h, int chunk) {
         for (int i = 0; i < chunk && !rc; ++i) {
             const int cur = (c0 + i) & 1, nxt = cur ^ 1;
             rc = launch_cauchy(h, vy(cur), vg(cur), 1);
-            if (!rc) rc = launch_search(h, vy(cur), vg(cur), vg(cur), -1.0, 1, 0, first_k(h), 1);
+            if (!rc && graph_spec(h)) rc = launch_spec(h, cur, nxt);
+            if (!rc) rc = launch_search(h, vy(cur), vg(cur), vg(cur), -1.0, 1, graph_spec(h) ? 1 : 0, first_k(h), 1);
             if (!rc) rc = launch_accept(h, vy(cur), vg(cur), -1.0, mk(cur), vy(nxt), vg(nxt), mk(nxt), 1);
             if (!rc) {
                 k_gp_step<<<1, 32, 0, h->st>>>(h->dS);
@@ -1290,7 +1317,7 @@ int build_gp_graph(gpcg_problem* h, int chunk) {
 
 int launches_per_gp_step(const gpcg_problem* h) {
     const int fins = h->deferred ? (1 + (h->nslabs() > 1 ? 1 : 0)) : 0;
-    return (fused_cauchy(h) ? 0 : h->nslabs() + fins) + 2 * (h->nslabs() + fins) + 1;
+    return (fused_cauchy(h) ? 0 : h->nslabs() + fins) + (graph_spec(h) ? 3 : 2) * (h->nslabs() + fins) + 1;
 }
 
 // The whole GP phase (until it stops or hands a step back) as one cooperative launch.
@@ -2780,7 +2807,7 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                     // the first search batch found no step: the host finishes this step (the persistent
                     // kernel reports the first step size index it has not tried in s_pad)
                     int hacc = -1;
-                    const int hstart = persist ? std::max(S.s_pad, 0) : first_k(h);
+                    const int hstart = persist ? std::max(S.s_pad, 0) : first_k(h) + (graph_spec(h) ? 1 : 0);
                     if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc, hstart))) goto fail;
                     cur ^= 1;
                     const long long j = jdone + 1;

@@ -32,7 +32,7 @@ k_accept(Op A, Bounds Bd, const double* __restrict__ y_in, const double* __restr
          double sgn, const double* __restrict__ b, const unsigned char* __restrict__ mask_prev,
          double* __restrict__ y_out, double* __restrict__ g_out, unsigned char* __restrict__ mask_out,
          Scal* S, RedScratch R, int gp) {
-    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
+    if (gp && gp_skip(S)) return;                    // device-driven GP phase over / k_spec accepted
     double alpha = 0.0;
     if (dir) {
         if (S->s_h < 0) return;          // uniform across the grid
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kThreads)
 k_search(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g,
          const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu,
          Scal* S, RedScratch R, int gp) {
-    if (gp && *(volatile int*)&S->gp_done) return;   // device-driven GP phase already over
+    if (gp && gp_skip(S)) return;                    // device-driven GP phase over / k_spec accepted
     if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
         if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
         return;
@@ -138,6 +138,59 @@ k_search(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict
         }
     });
     reduce_and_finish<2 * K>(acc, R, [&](double* t) { fin_search(t, K, h0, base, mu, S); });
+}
+
+// ----------------------------------------------------------------------------
+// a1 + a3 speculative (generic operators: CSR, 3-D): the GP step at h = 0 (alpha_0) in ONE
+// sweep -- the search sums of h = 0 and the accepted point together:
+//   s = mid(l, u, y - alpha_0 g) - y at the point and its neighbours (pointwise),
+//   y' = y + s,  g' = g + A s  (one operator application: A y' - b = g + A s),
+//   mask' = [l < y' < u];  sums <g, s>, <s, A s> (Eq. gplsstop at h = 0) and the accept sums.
+// fin_spec keeps the step when q(y') - q(y) = <g,s> + 1/2 <s,As> <= mu <g,s>; otherwise the
+// step's search (from h = 1) and accept sweeps run as before and overwrite y', g', mask' (the
+// next ping-pong buffers).  A GP step is then a Cauchy sweep and this one instead of Cauchy,
+// search and accept.  g' = g + A s rounds differently from A y' - b; every CG-phase accept
+// recomputes g = A y - b, so the difference stays within one GP phase.
+// ----------------------------------------------------------------------------
+template <class Op, bool SB>
+__global__ void __launch_bounds__(kThreads)
+k_spec(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g, double* __restrict__ y_out,
+       double* __restrict__ g_out, unsigned char* __restrict__ mask_out, double mu, Scal* S, RedScratch R) {
+    if (*(volatile int*)&S->gp_done) return;
+    if (!S->cauchy_ok) {                          // <d,Ad> <= 0: no step (uniform; k_finalize mirrors it)
+        if (blockIdx.x == 0 && threadIdx.x == 0) { S->spec_ok = 0; S->s_h = -1; }
+        return;
+    }
+    const double alpha = S->alpha0;
+    double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    A.for_each_point([&](const Pt& p) {
+        double as = 0.0, sv = 0.0, yn = 0.0;
+        A.for_each_nbr(p, [&](int c, double a) {
+            const double yc = __ldg(y + c);
+            const double tc = trial(yc, __ldg(g + c), -1.0, alpha, lo<SB>(Bd, c), hi<SB>(Bd, c));
+            const double sc = tc - yc;
+            if (c == p.v) { sv = sc; yn = tc; }
+            as = fma(a, sc, as);
+        });
+        const double l = lo<SB>(Bd, p.v), u = hi<SB>(Bd, p.v);
+        const double yv = __ldg(y + p.v), gv = __ldg(g + p.v);
+        const double gn = gv + as;
+        y_out[p.v] = yn;
+        g_out[p.v] = gn;
+        const bool act = (yn == l) || (yn == u);
+        mask_out[p.v] = act ? 0 : 1;
+        const bool act_prev = (yv == l) || (yv == u);
+        acc[0] = fma(gv, sv, acc[0]);
+        acc[1] = fma(sv, as, acc[1]);
+        const double pg = pgrad(yn, gn, l, u);
+        acc[2] = fma(pg, pg, acc[2]);
+        acc[3] = fma(gn, gn, acc[3]);
+        acc[4] += act ? 1.0 : 0.0;
+        acc[5] += (act_prev != act) ? 1.0 : 0.0;
+        const bool binding = (yn == l && gn >= 0.0) || (yn == u && gn <= 0.0);
+        acc[6] += (act && !binding) ? 1.0 : 0.0;
+    });
+    reduce_and_finish<7>(acc, R, [&](double* t) { fin_spec(t, mu, S); });
 }
 
 // ----------------------------------------------------------------------------

@@ -159,7 +159,7 @@ k7_accept(Stencil3Op A, Bounds Bd, const double* __restrict__ y_in, const double
           const double* __restrict__ b, const unsigned char* __restrict__ mask_prev, double* __restrict__ y_out,
           double* __restrict__ g_out, unsigned char* __restrict__ mask_out, Scal* S, RedScratch R, int gp) {
     M3_SMEM(1);
-    if (gp && *(volatile int*)&S->gp_done) return;
+    if (gp && gp_skip(S)) return;      // GP phase over / k_spec accepted
     double alpha = 0.0;
     if (dir) {
         if (S->s_h < 0) return;
@@ -265,7 +265,7 @@ k7_search(Stencil3Op A, Bounds Bd, const double* __restrict__ y, const double* _
           const double* __restrict__ dir, double sgn, int use_alpha0, int h0, double mu, Scal* S, RedScratch R,
           int gp) {
     M3_SMEM(K);
-    if (gp && *(volatile int*)&S->gp_done) return;
+    if (gp && gp_skip(S)) return;      // GP phase over / k_spec accepted
     if (use_alpha0 && !S->cauchy_ok) {
         if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
         return;

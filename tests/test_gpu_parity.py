@@ -926,3 +926,38 @@ def test_cg_sweep_box_layouts(G, oracle, monkeypatch, case, pw):
         monkeypatch.setenv("GPCG_CG_PW", pw)
         assert st1["cg_iters"] == st2["cg_iters"]
         assert np.array_equal(x1, x2)
+
+
+# ------------------------------------------------------------------ speculative GP step of the generic operators
+SPEC_CASES = {"c4_family_m16": (lambda: P.c4_family(m=16), -1e-11),
+              "c4s_family_16": (lambda: P.c4_stencil_family(m=16), -1e-11),
+              "dense40": (lambda: dense_problem(40, 3), -1e-12),
+              "c4_family_m24_jacobi": (lambda: P.c4_family(m=24), -1e-11)}
+
+
+@pytest.mark.parametrize("case", list(SPEC_CASES))
+def test_generic_speculative_gp_step(G, oracle, monkeypatch, case):
+    """k_spec (CSR / 3-D GP graph: the h = 0 step's search sums and accepted point in one sweep,
+    g' = g + A s) against the three-sweep step (GPCG_GP_SPEC=0): both reach the oracle's
+    solution, with the same outer / GP iteration counts; and the same with several slabs."""
+    make, tol = SPEC_CASES[case]
+    prob = make()
+    pc = 1 if case.endswith("jacobi") else 0
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    out = {}
+    for spec in ("0", "1"):
+        monkeypatch.setenv("GPCG_GP_SPEC", spec)
+        for slabs in (1, 2):
+            if slabs > 1 and case == "dense40":
+                continue
+            with G.Solver.from_problem(prob, slabs=slabs) as s:
+                s.set_params(precond=pc)
+                rc, x, st = s.solve(prob.x0, tol)
+            assert rc == 0 and rc_o == 0, (spec, slabs, st)
+            assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+            assert np.max(np.abs(x - x_o)) <= 1e-7
+            nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+            assert not nontie
+            out[(spec, slabs)] = st
+    assert out[("1", 1)]["gp_iters"] == out[("0", 1)]["gp_iters"]
+    assert out[("1", 1)]["outer_iters"] == out[("0", 1)]["outer_iters"]
