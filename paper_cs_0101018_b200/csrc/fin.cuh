@@ -53,16 +53,16 @@ __device__ __forceinline__ void fin_search(const double* t, int K, int h0, doubl
     }
 }
 
-// a1 + a3 speculative (k_spec): t = <g,s>, <s,As> of h = 0, then the accept sums of the point
-// it wrote.  Eq. gplsstop at h = 0 holds -> the step is taken (s_h = 0, the search / accept
-// sweeps of the step skip); else s_h = -1 and they run from h = 1.
-__device__ __forceinline__ void fin_spec(const double* t, double mu, Scal* S) {
+// a1 + a3 speculative (k_spec): t = <g,s>, <s,As> of h = 0 (step base), then the accept sums of
+// the point it wrote.  Eq. gplsstop / cglsstop2 at h = 0 holds -> the step is taken (s_h = 0;
+// the GP step's search / accept sweeps skip); else s_h = -1 and the search runs from h = 1.
+__device__ __forceinline__ void fin_spec(const double* t, double base, double mu, Scal* S) {
     const double gs = t[0], sAs = t[1];
     const double dq = gs + 0.5 * sAs;
     if (dq <= mu * gs) {
         S->spec_ok = 1;
         S->s_h = 0;
-        S->s_alpha = S->alpha0;
+        S->s_alpha = base;
         S->s_delta = dq;
         S->s_gs = gs;
         fin_accept(t + 2, false, S);
@@ -236,8 +236,8 @@ __global__ void k_finalize(const double* __restrict__ t, Scal* S, FinArgs a) {
             pcg2_beta_fin(t[0], S);
             break;
         case FIN_SPEC:
-            if (!S->cauchy_ok) { S->spec_ok = 0; S->s_h = -1; return; }
-            fin_spec(t, a.mu, S);
+            if (a.use_alpha0 && !S->cauchy_ok) { S->spec_ok = 0; S->s_h = -1; return; }
+            fin_spec(t, a.use_alpha0 ? S->alpha0 : 1.0, a.mu, S);
             break;
     }
 }

@@ -1055,28 +1055,32 @@ int launch_cauchy(gpcg_problem* h, int y, int g, int gp = 0) {
     return finish_reduce(h, a, 2);
 }
 
-// The GP graph of the generic operators (CSR, 3-D) takes each step speculatively at h = 0
-// (k_spec: search sums + accept in one sweep; GPCG_GP_SPEC=0: off); the 2-D stencils fuse the
-// step into their own sweeps (k6_gp_loop, spec_sweep6).
+// The generic operators (CSR, 3-D) take each GP step and the CG phase's step speculatively at
+// h = 0 (k_spec: search sums + accept in one sweep; GPCG_GP_SPEC=0: off); the 2-D stencils fuse
+// the GP step into their own sweeps (k6_gp_loop, spec_sweep6).
 bool graph_spec(const gpcg_problem* h) { return h->gp_spec && !spec2d(h); }
 
-int launch_spec(gpcg_problem* h, int cur, int nxt) {
+// y(nxt), g(nxt), mask(nxt) = the step at h = 0 from y(cur) along sgn * dir (base alpha_0 or 1)
+int launch_spec(gpcg_problem* h, int cur, int dir, double sgn, int use_alpha0, int gp) {
     const double mu = h->prm.mu;
+    const int nxt = cur ^ 1;
     for (int s = 0; s < h->nslabs(); ++s) {
         Slab& S = h->slabs[s];
         const Bounds B = h->bounds(S);
         with_gop_sb(h, S, [&](auto& op, auto sbt) {
             using Op = std::decay_t<decltype(op)>;
             constexpr bool SB = decltype(sbt)::value;
-            k_spec<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[vy(cur)], S.v[vg(cur)], S.v[vy(nxt)],
-                                                          S.v[vg(nxt)], S.m[mk(nxt)], mu, h->dS, h->red(s));
+            k_spec<Op, SB><<<S.grid, kThreads, 0, h->st>>>(op, B, S.v[vy(cur)], S.v[dir], sgn, use_alpha0, S.v[vg(cur)],
+                                                          S.v[VB], S.v[vy(nxt)], S.v[vg(nxt)], S.m[mk(nxt)], mu, h->dS,
+                                                          h->red(s), gp);
         });
         h->launches++;
         CKLAUNCH();
     }
     FinArgs a = fin(FIN_SPEC);
     a.mu = mu;
-    a.gp = 1;
+    a.gp = gp;
+    a.use_alpha0 = use_alpha0;
     RC(finish_reduce(h, a, 7));
     return exchange(h, {vy(nxt), vg(nxt)}, {mk(nxt)});
 }
@@ -1291,7 +1295,7 @@ int build_gp_graph(gpcg_problem* h, int chunk) {
         for (int i = 0; i < chunk && !rc; ++i) {
             const int cur = (c0 + i) & 1, nxt = cur ^ 1;
             rc = launch_cauchy(h, vy(cur), vg(cur), 1);
-            if (!rc && graph_spec(h)) rc = launch_spec(h, cur, nxt);
+            if (!rc && graph_spec(h)) rc = launch_spec(h, cur, vg(cur), -1.0, 1, 1);
             if (!rc) rc = launch_search(h, vy(cur), vg(cur), vg(cur), -1.0, 1, graph_spec(h) ? 1 : 0, first_k(h), 1);
             if (!rc) rc = launch_accept(h, vy(cur), vg(cur), -1.0, mk(cur), vy(nxt), vg(nxt), mk(nxt), 1);
             if (!rc) {
@@ -2880,7 +2884,13 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 t_cg += ms;
                 // projected search along d_k = Z_k w (Eq. cglsstop2), alpha = 2^-h
                 int hacc = -1;
-                if ((rc = search_and_accept(h, cur, VW, 1.0, 0, &hacc))) goto fail;
+                if (graph_spec(h)) {            // the CG phase's step at alpha = 1 first (k_spec)
+                    if ((rc = launch_spec(h, cur, VW, 1.0, 0, 0)) || (rc = sync_scal(h))) goto fail;
+                    if (S.spec_ok) hacc = 0;
+                    else if ((rc = search_and_accept(h, cur, VW, 1.0, 0, &hacc, 1))) goto fail;
+                } else if ((rc = search_and_accept(h, cur, VW, 1.0, 0, &hacc))) {
+                    goto fail;
+                }
                 st.full_spmvs += 2;
                 cur ^= 1;
                 if (trace_on())

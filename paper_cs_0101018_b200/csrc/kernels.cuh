@@ -141,45 +141,48 @@ k_search(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict
 }
 
 // ----------------------------------------------------------------------------
-// a1 + a3 speculative (generic operators: CSR, 3-D): the GP step at h = 0 (alpha_0) in ONE
-// sweep -- the search sums of h = 0 and the accepted point together:
-//   s = mid(l, u, y - alpha_0 g) - y at the point and its neighbours (pointwise),
-//   y' = y + s,  g' = g + A s  (one operator application: A y' - b = g + A s),
-//   mask' = [l < y' < u];  sums <g, s>, <s, A s> (Eq. gplsstop at h = 0) and the accept sums.
-// fin_spec keeps the step when q(y') - q(y) = <g,s> + 1/2 <s,As> <= mu <g,s>; otherwise the
-// step's search (from h = 1) and accept sweeps run as before and overwrite y', g', mask' (the
-// next ping-pong buffers).  A GP step is then a Cauchy sweep and this one instead of Cauchy,
-// search and accept.  g' = g + A s rounds differently from A y' - b; every CG-phase accept
-// recomputes g = A y - b, so the difference stays within one GP phase.
+// a1 + a3 speculative (generic operators: CSR, 3-D): a projected-search step at h = 0 and its
+// accept in ONE sweep.  GP phase: alpha = alpha_0 along -g (Eq. next-y); CG phase: alpha = 1
+// along w (Eq. cglsstop2).  At the point and its neighbours (pointwise):
+//   y'_c = mid(l, u, y_c + alpha sgn dir_c),  s_c = y'_c - y_c;
+//   g' = A y' - b,  A s,  mask' = [l < y' < u];
+//   sums <g, s>, <s, A s> (the search's h = 0 sums) and the accept sums of y'.
+// Each quantity with the arithmetic (and order of operator terms) of k_search / k_accept, so the
+// result is bit for bit theirs: fin_spec keeps the step when q(y') - q(y) = <g,s> + 1/2 <s,As>
+// <= mu <g,s> (the step's search / accept sweeps then return at once), otherwise they run from
+// h = 1 and overwrite y', g', mask' (the next ping-pong buffers).  One sweep instead of two per
+// accepted step; the next Cauchy step cannot join (d' needs g' at the neighbours' neighbours).
 // ----------------------------------------------------------------------------
 template <class Op, bool SB>
 __global__ void __launch_bounds__(kThreads)
-k_spec(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__ g, double* __restrict__ y_out,
-       double* __restrict__ g_out, unsigned char* __restrict__ mask_out, double mu, Scal* S, RedScratch R) {
-    if (*(volatile int*)&S->gp_done) return;
-    if (!S->cauchy_ok) {                          // <d,Ad> <= 0: no step (uniform; k_finalize mirrors it)
+k_spec(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__ dir, double sgn, int use_alpha0,
+       const double* __restrict__ g, const double* __restrict__ b, double* __restrict__ y_out,
+       double* __restrict__ g_out, unsigned char* __restrict__ mask_out, double mu, Scal* S, RedScratch R, int gp) {
+    if (gp && *(volatile int*)&S->gp_done) return;
+    if (use_alpha0 && !S->cauchy_ok) {            // <d,Ad> <= 0: no step (uniform; k_finalize mirrors it)
         if (blockIdx.x == 0 && threadIdx.x == 0) { S->spec_ok = 0; S->s_h = -1; }
         return;
     }
-    const double alpha = S->alpha0;
+    const double alpha = use_alpha0 ? S->alpha0 : 1.0;
     double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     A.for_each_point([&](const Pt& p) {
-        double as = 0.0, sv = 0.0, yn = 0.0;
+        double ax = 0.0, as = 0.0, sv = 0.0, yn = 0.0;
         A.for_each_nbr(p, [&](int c, double a) {
             const double yc = __ldg(y + c);
-            const double tc = trial(yc, __ldg(g + c), -1.0, alpha, lo<SB>(Bd, c), hi<SB>(Bd, c));
+            const double tc = trial(yc, __ldg(dir + c), sgn, alpha, lo<SB>(Bd, c), hi<SB>(Bd, c));
             const double sc = tc - yc;
             if (c == p.v) { sv = sc; yn = tc; }
+            ax = fma(a, tc, ax);
             as = fma(a, sc, as);
         });
         const double l = lo<SB>(Bd, p.v), u = hi<SB>(Bd, p.v);
         const double yv = __ldg(y + p.v), gv = __ldg(g + p.v);
-        const double gn = gv + as;
+        const double gn = ax - __ldg(b + p.v);
         y_out[p.v] = yn;
         g_out[p.v] = gn;
         const bool act = (yn == l) || (yn == u);
         mask_out[p.v] = act ? 0 : 1;
-        const bool act_prev = (yv == l) || (yv == u);
+        const bool act_prev = (yv == l) || (yv == u);     // = !mask(y): y is feasible
         acc[0] = fma(gv, sv, acc[0]);
         acc[1] = fma(sv, as, acc[1]);
         const double pg = pgrad(yn, gn, l, u);
@@ -190,7 +193,8 @@ k_spec(Op A, Bounds Bd, const double* __restrict__ y, const double* __restrict__
         const bool binding = (yn == l && gn >= 0.0) || (yn == u && gn <= 0.0);
         acc[6] += (act && !binding) ? 1.0 : 0.0;
     });
-    reduce_and_finish<7>(acc, R, [&](double* t) { fin_spec(t, mu, S); });
+    const double base = alpha;
+    reduce_and_finish<7>(acc, R, [&](double* t) { fin_spec(t, base, mu, S); });
 }
 
 // ----------------------------------------------------------------------------

@@ -937,9 +937,10 @@ SPEC_CASES = {"c4_family_m16": (lambda: P.c4_family(m=16), -1e-11),
 
 @pytest.mark.parametrize("case", list(SPEC_CASES))
 def test_generic_speculative_gp_step(G, oracle, monkeypatch, case):
-    """k_spec (CSR / 3-D GP graph: the h = 0 step's search sums and accepted point in one sweep,
-    g' = g + A s) against the three-sweep step (GPCG_GP_SPEC=0): both reach the oracle's
-    solution, with the same outer / GP iteration counts; and the same with several slabs."""
+    """k_spec (CSR / 3-D: the h = 0 step of each GP step and of the CG phase -- search sums and
+    accepted point in one sweep, each with the arithmetic of k_search / k_accept) against the
+    search + accept sweeps (GPCG_GP_SPEC=0): the oracle's solution, and bit for bit the same
+    iterate and iteration counts, with one and with two slabs."""
     make, tol = SPEC_CASES[case]
     prob = make()
     pc = 1 if case.endswith("jacobi") else 0
@@ -958,6 +959,11 @@ def test_generic_speculative_gp_step(G, oracle, monkeypatch, case):
             assert np.max(np.abs(x - x_o)) <= 1e-7
             nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
             assert not nontie
-            out[(spec, slabs)] = st
-    assert out[("1", 1)]["gp_iters"] == out[("0", 1)]["gp_iters"]
-    assert out[("1", 1)]["outer_iters"] == out[("0", 1)]["outer_iters"]
+            out[(spec, slabs)] = (x, st)
+    for slabs in (1, 2):
+        if ("1", slabs) not in out:
+            continue
+        (x1, st1), (x0, st0) = out[("1", slabs)], out[("0", slabs)]
+        assert np.array_equal(x1, x0)
+        for k in ("outer_iters", "gp_iters", "cg_iters", "q"):
+            assert st1[k] == st0[k], k
