@@ -3,91 +3,18 @@
 // restricted to the free index set) for the small-free regime (C4: ~5 % free).
 //
 // F = [v_0 < v_1 < ... < v_{m-1}], the free points of the current mask in owned-point order,
-// is built by the deterministic prefix sums of extract.cuh (k_scan_*).  The kernels iterate
-// k < m with v = F[k] instead of every point: A's rows are read in place (no copy of its
-// values, unlike the extraction ablation), the CG vectors stay full-length and zero off F
-// (neighbour values are read only where the mask says free), so a CG iteration touches the
-// free rows and their neighbours only -- O(m) instead of O(n) work and bytes.  Same arithmetic
-// (and order of the operator terms) as k_cg_init / k_cg_iter / k_hessvec of kernels.cuh.
+// is built by the deterministic prefix sums of extract.cuh (k_scan_*), with pos[v] = k for v in F
+// and the same set as bits.  The kernels iterate k < m with v = F[k] instead of every point: A's
+// rows are read in place (no copy of its values, unlike the extraction ablation), the CG vectors
+// live in the reduced space (m entries, coalesced), and neighbours are visited only where the
+// free bits say so -- O(m) instead of O(n) work and bytes.  Same arithmetic (and order of the
+// operator terms) as k_cg_init / k_cg_iter / k_hessvec of kernels.cuh.
 #pragma once
 
 #include "common.cuh"
 #include "fin.cuh"
 
 namespace gpcg {
-
-// grid-stride over the free list
-template <class Body>
-__device__ __forceinline__ void for_each_free_row(long long m, const int* __restrict__ rows, Body&& body) {
-    for (long long k = blockIdx.x * (long long)kThreads + threadIdx.x; k < m; k += (long long)gridDim.x * kThreads)
-        body(__ldg(rows + k));
-}
-
-template <class Op, bool PC>
-__global__ void __launch_bounds__(kThreads)
-k_cg_init_rows(Op A, long long m, const int* __restrict__ rows, const double* __restrict__ g,
-               const unsigned char* __restrict__ mask, double* __restrict__ rho, double* __restrict__ q,
-               double* __restrict__ s, double* __restrict__ p, double* __restrict__ w,
-               const double* __restrict__ dinv, double eta2, long long cap, Scal* S, RedScratch R) {
-    double acc[2] = {0.0, 0.0};
-    for_each_free_row(m, rows, [&](int v) {
-        const Pt pt = A.point(v);
-        p[v] = 0.0; w[v] = 0.0; s[v] = 0.0;
-        double qv = 0.0, uv = 0.0;
-        A.for_each_nbr(pt, [&](int c, double a) {
-            const double rc = mask[c] ? -__ldg(g + c) : 0.0;
-            const double uc = PC ? rc * __ldg(dinv + c) : rc;
-            if (c == v) uv = uc;
-            qv = fma(a, uc, qv);
-        });
-        const double rv = -__ldg(g + v);
-        rho[v] = rv;
-        q[v] = qv;
-        acc[0] = fma(rv, uv, acc[0]);
-        acc[1] = fma(uv, qv, acc[1]);
-    });
-    reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
-}
-
-template <class Op, bool PC>
-__global__ void __launch_bounds__(kThreads)
-k_cg_iter_rows(Op A, long long m, const int* __restrict__ rows, const unsigned char* __restrict__ mask,
-               const double* __restrict__ rho, const double* __restrict__ q, const double* __restrict__ s,
-               double* __restrict__ rho_n, double* __restrict__ q_n, double* __restrict__ s_n,
-               double* __restrict__ p, double* __restrict__ w, const double* __restrict__ dinv, Scal* S,
-               RedScratch R) {
-    if (*(volatile int*)&S->cg_done) return;
-    const double alpha = S->cg_alpha, beta = S->cg_beta;
-    double acc[2] = {0.0, 0.0};
-    for_each_free_row(m, rows, [&](int v) {
-        const Pt pt = A.point(v);
-        const double rv = rho[v], qv = q[v], sv = s[v];
-        const double pn = fma(beta, p[v], PC ? rv * __ldg(dinv + v) : rv);
-        const double sn = fma(beta, sv, qv);
-        w[v] = fma(alpha, pn, w[v]);
-        p[v] = pn;
-        s_n[v] = sn;
-        double rnv = 0.0, unv = 0.0, qn = 0.0;
-        A.for_each_nbr(pt, [&](int c, double a) {
-            double uc;
-            if (c == v) {
-                rnv = fma(-alpha, sn, rv);
-                unv = PC ? rnv * __ldg(dinv + v) : rnv;
-                uc = unv;
-            } else {
-                if (!mask[c]) return;
-                const double rc = fma(-alpha, fma(beta, s[c], q[c]), rho[c]);
-                uc = PC ? rc * __ldg(dinv + c) : rc;
-            }
-            qn = fma(a, uc, qn);
-        });
-        rho_n[v] = rnv;
-        q_n[v] = qn;
-        acc[0] = fma(rnv, unv, acc[0]);
-        acc[1] = fma(unv, qn, acc[1]);
-    });
-    reduce_and_finish<2>(acc, R, [&](double* t) { cg_finalize(t[0], t[1], S); });
-}
 
 // ---------------------------------------------------------------- free bits + reduced product
 // The free set as bits: word w holds the mask bytes 32 w .. 32 w + 31 (n / 8 bytes -- 2 MB at
@@ -102,6 +29,86 @@ k_pack_bits(long long n, const unsigned char* __restrict__ mask, unsigned* __res
 
 __device__ __forceinline__ bool free_bit(const unsigned* __restrict__ bits, int c) {
     return (__ldg(bits + (c >> 5)) >> (c & 31)) & 1u;
+}
+
+// The CG vectors live in the REDUCED space (index k of F, the w of Eq. cg2 itself): rho, q, s,
+// p, w of m entries each, read and written coalesced; only the operator's rows of A (in place),
+// the free bits and -- for free neighbours -- pos[c] (the k of point c) and their compact values
+// are gathered.  Same recurrences, arithmetic and order of operator terms as k_cg_init /
+// k_cg_iter (kernels.cuh), so the same iterates as the masked full-length kernels.
+template <class Op, bool PC>
+__global__ void __launch_bounds__(kThreads)
+k_cg_init_c(Op A, long long m, const int* __restrict__ rows, const unsigned* __restrict__ bits,
+            const double* __restrict__ g, double* __restrict__ rho, double* __restrict__ q, double* __restrict__ s,
+            double* __restrict__ p, double* __restrict__ w, const double* __restrict__ dinv, double eta2,
+            long long cap, Scal* S, RedScratch R) {
+    double acc[2] = {0.0, 0.0};
+    for (long long k = blockIdx.x * (long long)kThreads + threadIdx.x; k < m; k += (long long)gridDim.x * kThreads) {
+        const int v = __ldg(rows + k);
+        p[k] = 0.0; w[k] = 0.0; s[k] = 0.0;
+        double qv = 0.0, uv = 0.0;
+        A.for_each_nbr(A.point(v), [&](int c, double a) {
+            const double rc = free_bit(bits, c) ? -__ldg(g + c) : 0.0;
+            const double uc = PC ? rc * __ldg(dinv + c) : rc;
+            if (c == v) uv = uc;
+            qv = fma(a, uc, qv);
+        });
+        const double rv = -__ldg(g + v);
+        rho[k] = rv;
+        q[k] = qv;
+        acc[0] = fma(rv, uv, acc[0]);
+        acc[1] = fma(uv, qv, acc[1]);
+    }
+    reduce_and_finish<2>(acc, R, [&](double* t) { cg_init_finalize(t[0], t[1], eta2, cap, S); });
+}
+
+template <class Op, bool PC>
+__global__ void __launch_bounds__(kThreads)
+k_cg_iter_c(Op A, long long m, const int* __restrict__ rows, const unsigned* __restrict__ bits,
+            const int* __restrict__ pos, const double* __restrict__ rho, const double* __restrict__ q,
+            const double* __restrict__ s, double* __restrict__ rho_n, double* __restrict__ q_n,
+            double* __restrict__ s_n, double* __restrict__ p, double* __restrict__ w,
+            const double* __restrict__ dinv, Scal* S, RedScratch R) {
+    if (*(volatile int*)&S->cg_done) return;
+    const double alpha = S->cg_alpha, beta = S->cg_beta;
+    double acc[2] = {0.0, 0.0};
+    for (long long k = blockIdx.x * (long long)kThreads + threadIdx.x; k < m; k += (long long)gridDim.x * kThreads) {
+        const int v = __ldg(rows + k);
+        const double rv = rho[k], qv = q[k], sv = s[k];
+        const double dv = PC ? __ldg(dinv + v) : 1.0;
+        const double pn = fma(beta, p[k], PC ? rv * dv : rv);
+        const double sn = fma(beta, sv, qv);
+        w[k] = fma(alpha, pn, w[k]);
+        p[k] = pn;
+        s_n[k] = sn;
+        double rnv = 0.0, unv = 0.0, qn = 0.0;
+        A.for_each_nbr(A.point(v), [&](int c, double a) {
+            double uc;
+            if (c == v) {
+                rnv = fma(-alpha, sn, rv);
+                unv = PC ? rnv * dv : rnv;
+                uc = unv;
+            } else {
+                if (!free_bit(bits, c)) return;
+                const int kc = __ldg(pos + c);
+                const double rc = fma(-alpha, fma(beta, s[kc], q[kc]), rho[kc]);
+                uc = PC ? rc * __ldg(dinv + c) : rc;
+            }
+            qn = fma(a, uc, qn);
+        });
+        rho_n[k] = rnv;
+        q_n[k] = qn;
+        acc[0] = fma(rnv, unv, acc[0]);
+        acc[1] = fma(unv, qn, acc[1]);
+    }
+    reduce_and_finish<2>(acc, R, [&](double* t) { cg_finalize(t[0], t[1], S); });
+}
+
+// w (full length, cleared by the caller) at the free points from the reduced-space w
+__global__ void __launch_bounds__(kThreads)
+k_scatter_free(long long m, const int* __restrict__ rows, const double* __restrict__ wc, double* __restrict__ w) {
+    const long long k = blockIdx.x * (long long)kThreads + threadIdx.x;
+    if (k < m) w[__ldg(rows + k)] = wc[k];
 }
 
 // y = (A_F x) on the free rows: y_free[k] = sum_{c in F} a_{F[k] c} x_c (compact output, the

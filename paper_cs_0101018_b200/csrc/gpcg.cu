@@ -204,6 +204,9 @@ struct Slab {
     // compacted free-row list (compact.cuh; CSR / 3-D operators, one slab): rows of mask fmask
     int* flist = nullptr;
     unsigned* fbits = nullptr;      // the same set as bits (k_pack_bits: n / 8 bytes, L2-resident)
+    int* fpos = nullptr;            // pos[v] = k for v = F[k] (stale elsewhere: read under a free bit)
+    double* cv = nullptr;           // reduced-space CG vectors: rho0/1, q0/1, s0/1, p, w (cv_cap each)
+    long long cv_cap = 0;
     long long *fblk = nullptr, *ftot = nullptr;
     long long fcount = -1;
     int fmask = -1;
@@ -263,6 +266,8 @@ struct gpcg_problem {
     cudaGraphExec_t cg_exec = nullptr;
     int cg_exec_chunk = 0;
     cudaGraphExec_t gp_exec[2] = {nullptr, nullptr};   // GP chunk graphs starting from buffers 0 / 1
+    cudaGraphExec_t gp_exec_s[2] = {nullptr, nullptr}; // ... of gp_exec_s_chunk (< gp_exec_chunk) steps: a phase's first launch
+    int gp_exec_s_chunk = 0;
     cudaGraphExec_t bj_exec = nullptr;  // block-Jacobi ILU PCG chunk graph (precond = 2 / 3)
     int bj_exec_chunk = 0, bj_exec_pc = 0;
     int gp_exec_chunk = 0;
@@ -521,7 +526,7 @@ void free_all(gpcg_problem* h) {
     for (Slab& S : h->slabs) {
         dfree(h, S.arena);
         for (void* p : {(void*)S.wxb, (void*)S.wyb, (void*)S.shb, (void*)S.brow, (void*)S.cgflags, S.xarena, (void*)S.bjf, (void*)S.rp,
-                        (void*)S.flist, (void*)S.fbits, (void*)S.fblk, (void*)S.ftot,
+                        (void*)S.flist, (void*)S.fbits, (void*)S.fpos, (void*)S.cv, (void*)S.fblk, (void*)S.ftot,
                         (void*)S.ci, (void*)S.val,
                         (void*)S.partials, (void*)S.counter})
             dfree(h, p);
@@ -533,6 +538,8 @@ void free_all(gpcg_problem* h) {
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
     if (h->bj_exec) cudaGraphExecDestroy(h->bj_exec);
     for (cudaGraphExec_t g : h->gp_exec)
+        if (g) cudaGraphExecDestroy(g);
+    for (cudaGraphExec_t g : h->gp_exec_s)
         if (g) cudaGraphExecDestroy(g);
     if (h->comm && nccl_api()) nccl_api()->CommDestroy(h->comm);
     for (cudaEvent_t e : {h->ev_sync, h->ev_a, h->ev_b, h->ev_c0, h->ev_c1})
@@ -1283,10 +1290,7 @@ int build_cg_graph(gpcg_problem* h, int chunk) {
 
 // GP chunk: `chunk` steps of [Cauchy (generic kernels), first search batch, accept, k_gp_step]
 // starting from buffers c0, the buffers alternating per step (a finished phase makes the rest no-ops)
-int build_gp_graph(gpcg_problem* h, int chunk) {
-    if (h->gp_exec[0] && h->gp_exec_chunk == chunk) return GPCG_OK;
-    for (cudaGraphExec_t& g : h->gp_exec)
-        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+int build_gp_graph_into(gpcg_problem* h, int chunk, cudaGraphExec_t (&out)[2]) {
     for (int c0 = 0; c0 < 2; ++c0) {
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
@@ -1311,11 +1315,28 @@ int build_gp_graph(gpcg_problem* h, int chunk) {
             return rc;
         }
         if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-        e = cudaGraphInstantiate(&h->gp_exec[c0], graph, 0);
+        e = cudaGraphInstantiate(&out[c0], graph, 0);
         cudaGraphDestroy(graph);
         if (e != cudaSuccess) return set_err(GPCG_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
     }
+    return GPCG_OK;
+}
+
+// the chunk graphs, and a 2-step pair for the first launch of each phase (short phases -- C4's
+// are 2-3 steps -- then launch no no-op steps)
+int build_gp_graph(gpcg_problem* h, int chunk) {
+    if (h->gp_exec[0] && h->gp_exec_chunk == chunk) return GPCG_OK;
+    for (cudaGraphExec_t& g : h->gp_exec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (cudaGraphExec_t& g : h->gp_exec_s)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    RC(build_gp_graph_into(h, chunk, h->gp_exec));
     h->gp_exec_chunk = chunk;
+    h->gp_exec_s_chunk = 0;
+    if (chunk > 2) {
+        RC(build_gp_graph_into(h, 2, h->gp_exec_s));
+        h->gp_exec_s_chunk = 2;
+    }
     return GPCG_OK;
 }
 
@@ -1511,10 +1532,11 @@ int build_free_list(gpcg_problem* h, Slab& S, int mk) {
         CK(dalloc(h, &S.fblk, (size_t)(nblk + 1) * sizeof(long long)));
         CK(dalloc(h, &S.ftot, sizeof(long long)));
         CK(dalloc(h, &S.fbits, (size_t)((n + 31) / 32 + 1) * sizeof(unsigned)));
+        if (h->pitch == h->rowlen) CK(dalloc(h, &S.fpos, (size_t)std::max<long long>(n, 1) * sizeof(int)));
     }
     k_scan_count<true><<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, S.m[mk], nullptr, S.fblk);
     k_scan_blocks<<<1, 1024, 0, h->st>>>(nblk, S.fblk, S.ftot);
-    k_scan_assign<<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, S.m[mk], S.fblk, nullptr, S.flist);
+    k_scan_assign<<<(unsigned)nblk, 256, 0, h->st>>>(n, h->rowlen, h->pitch, S.m[mk], S.fblk, S.fpos, S.flist);
     if (h->pitch == h->rowlen)      // contiguous owned points (CSR, 3-D): the free bits for the reduced products
         k_pack_bits<<<(unsigned)((n + kThreads - 1) / kThreads), kThreads, 0, h->st>>>(n, S.m[mk], S.fbits);
     CKLAUNCH();
@@ -1541,8 +1563,17 @@ int run_cg_compact(gpcg_problem* h, int cur, double eta2, long long cap, long lo
     RC(build_free_list(h, S, cur));
     const long long n = S.rows * (long long)h->rowlen;
     const long long mm = S.fcount;
+    if (mm > S.cv_cap) {                           // reduced-space vectors, grown on demand
+        dfree(h, S.cv);
+        S.cv = nullptr;
+        S.cv_cap = std::min<long long>(n, mm + mm / 4 + 1024);
+        CK(dalloc(h, &S.cv, (size_t)8 * S.cv_cap * sizeof(double)));
+    }
+    double* cvv[8];
+    for (int k = 0; k < 8; ++k) cvv[k] = S.cv + (size_t)k * S.cv_cap;
+    double *rho2[2] = {cvv[0], cvv[1]}, *q2[2] = {cvv[2], cvv[3]}, *s2[2] = {cvv[4], cvv[5]};
+    double *pc_ = cvv[6], *wc = cvv[7];
     CK(cudaMemsetAsync(S.v[VW], 0, (size_t)n * sizeof(double), h->st));       // w = 0 off F
-    CK(cudaMemcpyAsync(S.m[MKCG], S.m[cur], (size_t)n, cudaMemcpyDeviceToDevice, h->st));
     CK(cudaEventRecord(h->ev_c1, h->st));
     CK(cudaEventSynchronize(h->ev_c1));
     float ms_x = 0.f;
@@ -1555,33 +1586,32 @@ int run_cg_compact(gpcg_problem* h, int cur, double eta2, long long cap, long lo
     with_gop(h, S, [&](auto& op) {
         using Op = std::decay_t<decltype(op)>;
         if (pc)
-            k_cg_init_rows<Op, true><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.v[vg(cur)], S.m[MKCG], S.v[VRHO0],
-                                                                S.v[VQ0], S.v[VS0], S.v[VP], S.v[VW], S.v[VD], eta2,
-                                                                cap, h->dS, R);
+            k_cg_init_c<Op, true><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.fbits, S.v[vg(cur)], rho2[0], q2[0],
+                                                             s2[0], pc_, wc, S.v[VD], eta2, cap, h->dS, R);
         else
-            k_cg_init_rows<Op, false><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.v[vg(cur)], S.m[MKCG], S.v[VRHO0],
-                                                                 S.v[VQ0], S.v[VS0], S.v[VP], S.v[VW], S.v[VD], eta2,
-                                                                 cap, h->dS, R);
+            k_cg_init_c<Op, false><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.fbits, S.v[vg(cur)], rho2[0], q2[0],
+                                                              s2[0], pc_, wc, S.v[VD], eta2, cap, h->dS, R);
     });
     CKLAUNCH();
     h->launches++;
-    const int chunk = std::max(2, (h->prm.cg_chunk + 1) & ~1);
-    for (;;) {
+    // chunks of 4, 8, 16, ... iterations up to cg_chunk: short CG calls (C4: 3-4 iterations) launch
+    // few no-op iterations, long ones poll as rarely as before
+    const int chunk_max = std::max(2, (h->prm.cg_chunk + 1) & ~1);
+    int chunk = std::min(4, chunk_max);
+    for (;; chunk = std::min(2 * chunk, chunk_max)) {
         CK(cudaEventRecord(h->ev_c0, h->st));
         for (int i = 0; i < chunk; ++i) {
             const int a = i & 1, bb = a ^ 1;
             with_gop(h, S, [&](auto& op) {
                 using Op = std::decay_t<decltype(op)>;
                 if (pc)
-                    k_cg_iter_rows<Op, true><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.m[MKCG], S.v[vrho(a)],
-                                                                        S.v[vq(a)], S.v[vs(a)], S.v[vrho(bb)],
-                                                                        S.v[vq(bb)], S.v[vs(bb)], S.v[VP], S.v[VW],
-                                                                        S.v[VD], h->dS, R);
+                    k_cg_iter_c<Op, true><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.fbits, S.fpos, rho2[a], q2[a],
+                                                                     s2[a], rho2[bb], q2[bb], s2[bb], pc_, wc,
+                                                                     S.v[VD], h->dS, R);
                 else
-                    k_cg_iter_rows<Op, false><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.m[MKCG], S.v[vrho(a)],
-                                                                         S.v[vq(a)], S.v[vs(a)], S.v[vrho(bb)],
-                                                                         S.v[vq(bb)], S.v[vs(bb)], S.v[VP], S.v[VW],
-                                                                         S.v[VD], h->dS, R);
+                    k_cg_iter_c<Op, false><<<g, kThreads, 0, h->st>>>(op, mm, S.flist, S.fbits, S.fpos, rho2[a],
+                                                                      q2[a], s2[a], rho2[bb], q2[bb], s2[bb], pc_, wc,
+                                                                      S.v[VD], h->dS, R);
             });
         }
         CKLAUNCH();
@@ -1595,6 +1625,9 @@ int run_cg_compact(gpcg_problem* h, int cur, double eta2, long long cap, long lo
         h->cg_iters_timed += chunk;
         h->cg_free_iters_timed += chunk * mm;
     }
+    k_scatter_free<<<(unsigned)((mm + kThreads - 1) / kThreads), kThreads, 0, h->st>>>(mm, S.flist, wc, S.v[VW]);
+    CKLAUNCH();
+    h->launches++;
     *iters = h->hS->cg_it;
     if (h->hS->cg_reason == CG_NOTSPD)
         return set_err(GPCG_ENOTSPD, "CG breakdown: <p, A_k p> <= 0 at iteration %lld (A not SPD)",
@@ -2618,6 +2651,8 @@ int gpcg_set_params(gpcg_problem* h, const gpcg_params* p) {
     // the GP graphs bake in search_k / mu (and the chunk): rebuilt at the next solve
     for (cudaGraphExec_t& g : h->gp_exec)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (cudaGraphExec_t& g : h->gp_exec_s)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     return GPCG_OK;
 }
 
@@ -2791,13 +2826,17 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                 CKLAUNCH();
                 long long jdone = 0;
                 const bool persist = gp_persist(h);
+                bool first = true;
                 for (;;) {
                     if (persist) {
                         if ((rc = launch_gp_loop(h, cur))) goto fail;
                     } else {
-                        CK(cudaGraphLaunch(h->gp_exec[cur], h->st));
-                        h->launches += (long long)h->gp_exec_chunk * launches_per_gp_step(h);
+                        const bool small = first && h->gp_exec_s[0];
+                        CK(cudaGraphLaunch(small ? h->gp_exec_s[cur] : h->gp_exec[cur], h->st));
+                        h->launches += (long long)(small ? h->gp_exec_s_chunk : h->gp_exec_chunk) *
+                                       launches_per_gp_step(h);
                     }
+                    first = false;
                     if ((rc = sync_scal(h))) goto fail;
                     if (persist && (rc = check_xrank(h))) goto fail;
                     const long long jn = S.gp_j;
