@@ -522,7 +522,15 @@ def main():
         return run_reference(args)
     from paper_cs_0101018_b200 import _build
     _build.build()
-    return run_ours(args)
+    try:
+        return run_ours(args)
+    except Exception as e:          # one JSON line that says what failed, instead of none
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "reduced HVP/s", "n_gpus": args.gpus,
+                              "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                              "config": {"workload": args.config}, "error": f"{type(e).__name__}: {e}"[:400]}),
+                  flush=True)
+        raise
 
 
 if __name__ == "__main__":
