@@ -29,7 +29,8 @@ Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl
 N > 1 runs under torchrun (one process per GPU): the SAME problem split into N row
 slabs (gpcg_create_*_dist: NCCL halo exchange + one allreduce per CG iteration),
 i.e. strong scaling; see DESIGN.md "Multi-GPU".  --slabs S (N = 1) splits the
-problem into S slabs on the one GPU (device-copy halos: the multi-rank code path).
+problem into S slabs on the one GPU (the multi-slab persistent loops with fused halo
+writes; device-copy halos between the other sweeps).
 """
 import argparse
 import json

@@ -1553,8 +1553,8 @@ int build_free_list(gpcg_problem* h, Slab& S, int mk) {
 bool compact_ok(const gpcg_problem* h) { return !spec2d(h) && h->nslabs() == 1 && h->nranks == 1 && !h->deferred; }
 
 // CG on A_F applied in place over the free-row list (cg_mode 3, and cg_mode 2 for small free
-// sets): the C-G recurrences of k_cg_init / k_cg_iter on the free rows only; vectors full-length
-// (zero off F), no copy of A's values.  On return W holds w (zero off F).
+// sets): the C-G recurrences of k_cg_init / k_cg_iter on the free rows only, the vectors in the
+// reduced space (m entries), no copy of A's values.  On return W holds w (zero off F).
 int run_cg_compact(gpcg_problem* h, int cur, double eta2, long long cap, long long* iters) {
     if (!compact_ok(h))
         return set_err(GPCG_EINVAL, "cg_mode = 3 (free-row list) supports CSR / 3-D operators on one slab and rank");
