@@ -69,10 +69,12 @@ def load_peaks():
 def cg_kernel_name(prob, slabs_total=1):
     """The CG-iteration kernel libgpcg.so selects for this problem (gpcg.cu run_cg /
     enqueue_cg_iter); slabs_total > 1 (ranks x local slabs) uses the graph-chunk path."""
+    compact = prob.kind in ("csr", "stencil3d") and slabs_total == 1   # cg_mode 2 -> 3 for small free sets
     if prob.kind == "csr":
-        return "k_cg_iter<CsrOp>"
+        return "k_cg_iter_c<CsrOp> (free-row list, reduced-space vectors) / k_cg_iter<CsrOp>" if compact \
+            else "k_cg_iter<CsrOp>"
     if prob.kind == "stencil3d":
-        return "k_cg_iter<Stencil3Op>"
+        return "k_cg_iter_c<Stencil3Op> / k7_cg_iter" if compact else "k7_cg_iter"
     bc = not prob.wx_ld and not prob.wy_ld and prob.shift is None
     tile = int(os.environ.get("GPCG_TILE", "127") or 127)
     if os.environ.get("GPCG_GENERIC") == "1":
@@ -322,9 +324,15 @@ def run_ours(args):
     bpp = cg_bytes_per_free_point(prob)
     it_t = max(agg["cg_iters_timed"], 1)
     # per launch of this rank's kernel: the global free count split evenly over ranks
-    bytes_per_launch = (bpp * agg["cg_free_iters_timed"] + 1.0 * prob.n * agg["cg_iters_timed"]) / it_t / world
-    min_bytes_per_launch = (cg_min_bytes_per_free_point(prob) * agg["cg_free_iters_timed"]
-                            + 1.0 * prob.n * agg["cg_iters_timed"]) / it_t / world
+    # the mask is read at every point (1 B), except by the free-row-list CG of CSR / 3-D operators
+    # with a small free set (cg_mode 2 -> 3), which reads a 4-B list entry per free row instead
+    compact = (prob.kind in ("csr", "stencil3d") and world * args.slabs == 1
+               and agg["cg_free_iters_timed"] < 0.3 * prob.n * max(agg["cg_iters_timed"], 1))
+    per_pt, per_free = (0.0, 4.0) if compact else (1.0, 0.0)
+    bytes_per_launch = ((bpp + per_free) * agg["cg_free_iters_timed"]
+                        + per_pt * prob.n * agg["cg_iters_timed"]) / it_t / world
+    min_bytes_per_launch = ((cg_min_bytes_per_free_point(prob) + per_free) * agg["cg_free_iters_timed"]
+                            + per_pt * prob.n * agg["cg_iters_timed"]) / it_t / world
     launch_s = (agg["t_cg_timed_ms"] / 1e3) / it_t
     achieved = bytes_per_launch / launch_s / 1e9 if agg["cg_iters_timed"] else None
     achieved_min = min_bytes_per_launch / launch_s / 1e9 if agg["cg_iters_timed"] else None
@@ -419,6 +427,25 @@ def run_ours(args):
                                  "what": "SURVEY 8(d): 3 sweeps per GP sub-step (a2, a3, a1)"}}
         if traffic.get("gp"):
             gp_roof["dram_over_algorithmic"] = traffic["gp"] / gp_bytes
+    elif agg["gp_iters"] and prob.kind in ("csr", "stencil3d") and os.environ.get("GPCG_GP_SPEC", "1") != "0":
+        # CSR / 3-D GP graph: one GP step = a Cauchy sweep (y, g read) + k_spec (y, g, b read; y', g',
+        # mask' written), each reading the operator (CSR: 8 B row_ptr + 12 B per stored entry; 3-D:
+        # the face / shift arrays, 48 B per point) and l, u unless both are constants (16 B)
+        sb = bool(np.all(prob.l == prob.l[0]) and np.all(prob.u == prob.u[0]))
+        op_b = (8.0 + 12.0 * prob.val.size / prob.n) if prob.kind == "csr" else 48.0
+        bnd = 0.0 if sb else 16.0
+        step_b = (16.0 + op_b + bnd) + (24.0 + op_b + bnd + 17.0)
+        gp_step_s = (agg["t_gp_ms"] / 1e3) / agg["gp_iters"]
+        gp_bytes = step_b * prob.n / world
+        ach = gp_bytes / gp_step_s / 1e9
+        gp_roof = {"bound": "hbm", "kernel": "k_cauchy + k_spec (GP graph: Cauchy sweep + speculative h = 0 step)",
+                   "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                   "frac_of_8TBs": ach / 8000.0, "traffic": traffic.get("gp"), "peak_source": peak_src,
+                   "bytes_per_launch": gp_bytes, "us_per_launch": gp_step_s * 1e6,
+                   "launch": "one GP step (Cauchy + k_spec sweeps, reductions, k_gp_step; the phase's no-op "
+                             "launches included), CUDA events around each GP phase",
+                   "algorithmic_bytes": f"{step_b:.0f} B per point per GP step (operator {op_b:.0f} B, sb={sb}), "
+                                        f"every step's speculative sweep kept"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -471,8 +498,11 @@ def run_ours(args):
                          "bytes_per_launch": min_bytes_per_launch, "us_per_launch": launch_s * 1e6,
                          "dram_over_algorithmic": (traffic["cg"] / min_bytes_per_launch) if traffic.get("cg") else None,
                          "launch": "one CG iteration (reduced HVP + vector updates + reduction)",
-                         "algorithmic_bytes": f"{cg_min_bytes_per_free_point(prob):.0f} B per free point + 1 B mask "
-                                              f"per point (DESIGN.md 6: the kernel's three-vector recurrence)",
+                         "algorithmic_bytes": (f"{cg_min_bytes_per_free_point(prob) + per_free:.0f} B per free point "
+                                               f"(reduced-space vectors, the free rows of A, the list entry)"
+                                               if compact else
+                                               f"{cg_min_bytes_per_free_point(prob):.0f} B per free point + 1 B mask "
+                                               f"per point (DESIGN.md 6: the kernel's three-vector recurrence)"),
                          "survey_8d": {"bytes_per_launch": bytes_per_launch, "achieved": achieved,
                                        "frac": (achieved / peak) if achieved else None,
                                        "what": f"{bpp:.0f} B per free point + 1 B mask per point (SURVEY.md 8(d) "

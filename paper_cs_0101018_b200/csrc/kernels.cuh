@@ -369,6 +369,17 @@ k_check_inputs(int cols, int rows, int pitch, const double* __restrict__ b, cons
     reduce_and_finish<2>(acc, R, [&](double* t) { S->r0 = t[0]; S->r1 = t[1]; });
 }
 
+// create-time validation of a one-slab CSR operator uploaded as given: r0 = #rows with
+// row_ptr[i + 1] < row_ptr[i], r1 = #column indices outside [0, n)
+__global__ void k_check_csr(long long n, const long long* __restrict__ rp, const int* __restrict__ ci, long long nnz,
+                            Scal* S, RedScratch R) {
+    double acc[2] = {0.0, 0.0};
+    const long long t0 = blockIdx.x * (long long)kThreads + threadIdx.x, st = (long long)gridDim.x * kThreads;
+    for (long long i = t0; i < n; i += st) acc[0] += (rp[i + 1] < rp[i]) ? 1.0 : 0.0;
+    for (long long k = t0; k < nnz; k += st) acc[1] += (ci[k] < 0 || ci[k] >= n) ? 1.0 : 0.0;
+    reduce_and_finish<2>(acc, R, [&](double* t) { S->r0 = t[0]; S->r1 = t[1]; });
+}
+
 __global__ void k_count_nonfinite(long long n, const double* __restrict__ a, Scal* S, RedScratch R) {
     double acc[2] = {0.0, 0.0};
     for (long long v = blockIdx.x * (long long)kThreads + threadIdx.x; v < n; v += (long long)gridDim.x * kThreads)

@@ -967,3 +967,35 @@ def test_generic_speculative_gp_step(G, oracle, monkeypatch, case):
         assert np.array_equal(x1, x0)
         for k in ("outer_iters", "gp_iters", "cg_iters", "q"):
             assert st1[k] == st0[k], k
+
+
+@pytest.mark.parametrize("device", [False, True])
+@pytest.mark.parametrize("slabs", [1, 2])
+def test_csr_create_validation(G, device, slabs):
+    """gpcg_create_csr rejects a non-monotone row_ptr, a column outside [0, n) and a non-finite
+    value (EINVAL) -- on the one-slab path (arrays uploaded as given, checked by k_check_csr /
+    k_count_nonfinite) and the slab path (host checks) -- from host and from device arrays; the
+    valid matrix creates and solves."""
+    import torch
+    prob = dense_problem(12, 5)
+    bad = {"rp": lambda: (np.concatenate([prob.row_ptr[:3], [prob.row_ptr[2] - 1], prob.row_ptr[4:]]),
+                          prob.col, prob.val),
+           "col": lambda: (prob.row_ptr, np.where(np.arange(prob.col.size) == 7, 12, prob.col).astype(np.int32),
+                           prob.val),
+           "val": lambda: (prob.row_ptr, prob.col, np.where(np.arange(prob.val.size) == 9, np.nan, prob.val))}
+
+    def make(rp, ci, va):
+        if device:
+            rp, ci, va = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (rp, ci, va))
+        if slabs == 1:
+            return G.Solver.csr(prob.n, rp, ci, va, prob.b, prob.l, prob.u)
+        p2 = P.Problem(**{**prob.__dict__})
+        p2.row_ptr, p2.col, p2.val = (np.asarray(a.cpu() if hasattr(a, "cpu") else a) for a in (rp, ci, va))
+        return G.Solver.from_problem(p2, slabs=slabs)
+    for what, f in bad.items():
+        with pytest.raises(G.GpcgError) as e:
+            make(*f())
+        assert e.value.code == G.EINVAL, what
+    with make(prob.row_ptr, prob.col, prob.val) as s:
+        rc, x, st = s.solve(prob.x0, -1e-10)
+    assert rc == 0
