@@ -111,6 +111,7 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
@@ -129,7 +130,7 @@ const NcclApi* nccl_api() {
         if (lib) {
 #define NSYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(lib, "nccl" #f))
             NSYM(GetUniqueId); NSYM(CommInitRank); NSYM(CommDestroy); NSYM(AllReduce); NSYM(Broadcast);
-            NSYM(Send); NSYM(Recv); NSYM(GroupStart); NSYM(GroupEnd); NSYM(GetErrorString);
+            NSYM(Send); NSYM(Recv); NSYM(GroupStart); NSYM(GroupEnd); NSYM(GetErrorString); NSYM(AllGather);
 #undef NSYM
             ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Broadcast &&
                  api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
@@ -223,6 +224,17 @@ struct Slab {
 
 }  // namespace
 
+// A slab as the neighbour whose fused halo stores write into its ghost rows sees it: the origins
+// of rho0/1, p0/1 (the CG loop's ping-pong; VQ* hold p) and y0/1, mask0/1 (the GP loop's), its rows
+// and ghost depths.  From a slab of this process, or (GPCG_XRANK) the facing slab of the
+// neighbouring rank through its IPC-mapped arena.
+struct XrSide {
+    double* v[6];                   // VRHO0, VRHO1, VQ0, VQ1, VY0, VY1
+    unsigned char* m[2];            // MK0, MK1
+    int rows, glo, ghi;
+};
+constexpr int kXrVec[6] = {VRHO0, VRHO1, VQ0, VQ1, VY0, VY1};
+
 struct gpcg_problem {
     int dev = 0, sms = 148;
     cudaMemPool_t pool = nullptr;   // device allocations (mem_pool); null: cudaMalloc / cudaFree
@@ -288,6 +300,13 @@ struct gpcg_problem {
     double* xr_part = nullptr;                // [kMaxRanks][2][kXrSums][xr_stride] mailboxes
     int* xr_err = nullptr;                    // spin-timeout flag
     int xr_stride = 0;
+    // GPCG_XRANK=1 with several ranks: the loops span the ranks (setup_xrank_real)
+    bool xr_real = false;
+    void* xr_region = nullptr;                // this rank's counters / base / err / mailbox (cudaMalloc)
+    void* xr_peer[kMaxRanks] = {};            // the other ranks' regions, IPC-mapped
+    std::vector<void*> xr_mapped;             // every opened mapping (closed at destroy)
+    XrSide xr_lo{}, xr_hi{};                  // the lower / upper rank's facing slab
+    int xr_cta_cg[kMaxRanks] = {}, xr_cta_gp[kMaxRanks] = {};
     long long launches = 0;
     long long cg_iters_timed = 0, cg_free_iters_timed = 0;
     double t_cg_timed_ms = 0.0;
@@ -461,6 +480,7 @@ bool has_ghosts(const gpcg_problem* h) { return h->nslabs() > 1 || h->nranks > 1
 // (GPCG_MS_ONE=1, diagnostic: one slab through the multi-slab kernels as well)
 bool multi_slab_persistent(const gpcg_problem* h) {
     static const bool ms1 = getenv("GPCG_MS_ONE") && atoi(getenv("GPCG_MS_ONE")) != 0;
+    if (h->xr_real) return h->nslabs() <= kMaxMs;
     return h->nranks == 1 && !h->use_nccl && (h->nslabs() > 1 || ms1) && h->nslabs() <= kMaxMs;
 }
 
@@ -534,6 +554,16 @@ void free_all(gpcg_problem* h) {
     for (void* p : {(void*)h->red_all, (void*)h->red_tot, (void*)h->lu0, (void*)h->dS, (void*)h->gbar,
                     (void*)h->xr_bar, (void*)h->xr_base, (void*)h->xr_part, (void*)h->xr_err})
         dfree(h, p);
+    if (h->xr_real && h->comm && nccl_api()) {      // no rank frees what a peer still maps
+        int* one = nullptr;
+        if (cudaMalloc(&one, sizeof(int)) == cudaSuccess) {
+            nccl_api()->AllReduce(one, one, 1, ncclInt32, ncclSum, h->comm, h->st);
+            cudaStreamSynchronize(h->st);
+            cudaFree(one);
+        }
+    }
+    for (void* p : h->xr_mapped) cudaIpcCloseMemHandle(p);
+    if (h->xr_region) cudaFree(h->xr_region);
     if (h->hS) cudaFreeHost(h->hS);
     if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
     if (h->bj_exec) cudaGraphExecDestroy(h->bj_exec);
@@ -820,7 +850,8 @@ int create_streams(gpcg_problem* h, void* stream) {
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     {
         const char* e6 = getenv("GPCG_POOL");
-        h->pool = (e6 && e6[0] == '0') ? nullptr : mem_pool(h->dev);
+        const char* e8 = getenv("GPCG_XRANK");              // IPC-exported arenas need cudaMalloc memory
+        h->pool = ((e6 && e6[0] == '0') || (e8 && atoi(e8) != 0)) ? nullptr : mem_pool(h->dev);
     }
     CK(dalloc(h, &h->gbar, sizeof(unsigned int)));
     {
@@ -1351,11 +1382,149 @@ bool gp_persist(const gpcg_problem* h) {
     return h->gp_persistent && h->gfree && (!h->deferred || multi_slab_persistent(h));
 }
 
+XrSide side_of(const Slab& N) {
+    XrSide x;
+    for (int k = 0; k < 6; ++k) x.v[k] = N.v[kXrVec[k]];
+    x.m[0] = N.m[MK0];
+    x.m[1] = N.m[MK1];
+    x.rows = N.rows;
+    x.glo = N.glo;
+    x.ghi = N.ghi;
+    return x;
+}
+
+// the slab whose ghost rows slab S's fused halo stores write into, below (lo) or above it
+bool neighbour_side(const gpcg_problem* h, const Slab& S, bool lo, XrSide* out) {
+    const int nb = lo ? S.nb_lo : S.nb_hi;
+    if (nb >= 0) { *out = side_of(h->slabs[nb]); return true; }
+    if (nb == NB_REMOTE && h->xr_real) { *out = lo ? h->xr_lo : h->xr_hi; return true; }
+    return false;
+}
+
+// GPCG_XRANK=1, several ranks, 2-D broadcast-face stencil on the persistent loops: export this
+// rank's counter / mailbox region and the arenas of its two boundary slabs (CUDA IPC), all-gather
+// them with the CTA counts of its launches over the handle's NCCL communicator, open the other
+// ranks' regions and the neighbours' facing arenas.  Not run here: one GPU per
+// machine (the one-launch emulation runs the same kernels and neighbour tables).
+struct XrRecord {
+    cudaIpcMemHandle_t region, arena_lo, arena_hi;
+    long long off_lo[8], off_hi[8];           // kXrVec origins, then MK0, MK1: bytes from the arena base
+    int rows_lo, glo_lo, ghi_lo, rows_hi, glo_hi, ghi_hi;
+    int ctas_cg, ctas_gp;
+};
+
+int setup_xrank_real(gpcg_problem* h) {
+    const NcclApi* N = nccl_api();
+    if (!N || !N->AllGather) return set_err(GPCG_ENCCL, "GPCG_XRANK: ncclAllGather not available");
+    if (h->nranks > kMaxRanks) return set_err(GPCG_EINVAL, "GPCG_XRANK: at most %d ranks", kMaxRanks);
+    if (h->pool) return set_err(GPCG_EINVAL, "GPCG_XRANK: the arenas must come from cudaMalloc");
+    constexpr size_t L = kXrLine * sizeof(unsigned long long);
+    h->xr_stride = h->nranks * h->sms * 8;
+    const size_t bytes = 5 * L + (size_t)2 * kXrSums * h->xr_stride * sizeof(double);
+    CK(cudaMalloc(&h->xr_region, bytes));
+    CK(cudaMemset(h->xr_region, 0, bytes));
+    XrRecord me;
+    memset(&me, 0, sizeof me);
+    CK(cudaIpcGetMemHandle(&me.region, h->xr_region));
+    const Slab& F = h->slabs.front();
+    const Slab& B = h->slabs.back();
+    CK(cudaIpcGetMemHandle(&me.arena_lo, F.arena));
+    CK(cudaIpcGetMemHandle(&me.arena_hi, B.arena));
+    auto offs = [](const Slab& S, long long* o) {
+        const XrSide x = side_of(S);
+        const char* a = static_cast<const char*>(S.arena);
+        for (int k = 0; k < 6; ++k) o[k] = reinterpret_cast<const char*>(x.v[k]) - a;
+        o[6] = reinterpret_cast<const char*>(x.m[0]) - a;
+        o[7] = reinterpret_cast<const char*>(x.m[1]) - a;
+    };
+    offs(F, me.off_lo);
+    offs(B, me.off_hi);
+    me.rows_lo = F.rows; me.glo_lo = F.glo; me.ghi_lo = F.ghi;
+    me.rows_hi = B.rows; me.glo_hi = B.glo; me.ghi_hi = B.ghi;
+    for (const Slab& S : h->slabs) {
+        me.ctas_cg += S.grid4_cg;
+        me.ctas_gp += std::max(1, std::min(S.grid5_srch, S.grid5_acc));
+    }
+    std::vector<XrRecord> all(h->nranks);
+    char* dbuf = nullptr;
+    CK(cudaMalloc(&dbuf, (size_t)(h->nranks + 1) * sizeof(XrRecord)));
+    CK(cudaMemcpy(dbuf, &me, sizeof me, cudaMemcpyHostToDevice));
+    const ncclResult_t nr = N->AllGather(dbuf, dbuf + sizeof(XrRecord), sizeof(XrRecord), ncclChar, h->comm, h->st);
+    cudaError_t ce = cudaStreamSynchronize(h->st);
+    if (ce == cudaSuccess)
+        ce = cudaMemcpy(all.data(), dbuf + sizeof(XrRecord), (size_t)h->nranks * sizeof(XrRecord), cudaMemcpyDeviceToHost);
+    cudaFree(dbuf);
+    if (nr != ncclSuccess) return set_err(GPCG_ENCCL, "GPCG_XRANK: record all-gather failed");
+    CK(ce);
+    auto open = [&](const cudaIpcMemHandle_t& hd, void** p) {
+        const cudaError_t e = cudaIpcOpenMemHandle(p, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e == cudaSuccess) h->xr_mapped.push_back(*p);
+        return e;
+    };
+    for (int r = 0; r < h->nranks; ++r) {
+        h->xr_cta_cg[r] = all[r].ctas_cg;
+        h->xr_cta_gp[r] = all[r].ctas_gp;
+        if (r != h->rank) CK(open(all[r].region, &h->xr_peer[r]));
+    }
+    auto side = [](char* base, const long long* o, int rows, int glo, int ghi) {
+        XrSide x;
+        for (int k = 0; k < 6; ++k) x.v[k] = reinterpret_cast<double*>(base + o[k]);
+        x.m[0] = reinterpret_cast<unsigned char*>(base + o[6]);
+        x.m[1] = reinterpret_cast<unsigned char*>(base + o[7]);
+        x.rows = rows; x.glo = glo; x.ghi = ghi;
+        return x;
+    };
+    if (h->rank > 0) {                        // the lower rank's top slab
+        const XrRecord& R = all[h->rank - 1];
+        void* p = nullptr;
+        CK(open(R.arena_hi, &p));
+        h->xr_lo = side(static_cast<char*>(p), R.off_hi, R.rows_hi, R.glo_hi, R.ghi_hi);
+    }
+    if (h->rank < h->nranks - 1) {            // the upper rank's bottom slab
+        const XrRecord& R = all[h->rank + 1];
+        void* p = nullptr;
+        CK(open(R.arena_lo, &p));
+        h->xr_hi = side(static_cast<char*>(p), R.off_lo, R.rows_lo, R.glo_lo, R.ghi_lo);
+    }
+    h->xr_err = reinterpret_cast<int*>(static_cast<char*>(h->xr_region) + 4 * L);
+    h->xr_real = true;
+    return GPCG_OK;
+}
+
 // The XRank of a multi-slab persistent launch: nr = 0 (one device, the plain grid barrier), or
 // under GPCG_XRANK_EMU every slab a virtual rank with its own counter and mailbox (the cross-rank
 // protocol run inside one cooperative launch; same sums in the same order -> same bits).
-int make_xrank(gpcg_problem* h, const int* cta0, int nslabs, int total, XRank* X) {
+int make_xrank(gpcg_problem* h, const int* cta0, int nslabs, int total, XRank* X, bool cg) {
     memset(X, 0, sizeof *X);
+    if (h->xr_real) {
+        const int* ctas = cg ? h->xr_cta_cg : h->xr_cta_gp;
+        X->nr = h->nranks;
+        int acc = 0;
+        for (int r = 0; r < h->nranks; ++r) {
+            X->cta0[r] = acc;
+            acc += ctas[r];
+        }
+        X->cta0[h->nranks] = acc;
+        X->cta_total = acc;
+        X->cta_base = X->cta0[h->rank];
+        X->cta_stride = h->xr_stride;
+        if (total != ctas[h->rank] || acc > h->xr_stride)
+            return set_err(GPCG_EINVAL, "cross-rank launch of %d CTAs (exported %d, all ranks %d, mailbox %d)", total,
+                           ctas[h->rank], acc, h->xr_stride);
+        char* R = static_cast<char*>(h->xr_region);
+        constexpr size_t L = kXrLine * sizeof(unsigned long long);
+        X->lbar[h->rank] = reinterpret_cast<unsigned long long*>(R);               // line 0; line 1: go flag
+        X->base[h->rank] = reinterpret_cast<unsigned long long*>(R + 3 * L);
+        X->err = reinterpret_cast<int*>(R + 4 * L);
+        for (int r = 0; r < h->nranks; ++r) {
+            char* Q = r == h->rank ? R : static_cast<char*>(h->xr_peer[r]);
+            X->bar[r] = reinterpret_cast<unsigned long long*>(Q + 2 * L);
+            X->part[r] = reinterpret_cast<double*>(Q + 5 * L);
+        }
+        X->sys = 1;
+        return GPCG_OK;
+    }
+    (void)cg;
     if (!h->xr_emu) return GPCG_OK;
     if (nslabs > kMaxRanks) return set_err(GPCG_EINVAL, "GPCG_XRANK_EMU: at most %d slabs", kMaxRanks);
     if (!h->xr_bar) {
@@ -1417,15 +1586,14 @@ int launch_gp_loop_ms(gpcg_problem* h, int cur) {
         X.y0p = S.v[VY0]; X.y1p = S.v[VY1]; X.mk0 = S.m[MK0]; X.mk1 = S.m[MK1];
         const int g = std::max(1, std::min(S.grid5_srch, S.grid5_acc));
         X.Ls = SlabLink{0, g, 0, 0, 0};
-        if (S.nb_lo >= 0) {
-            Slab& N = h->slabs[S.nb_lo];
-            X.lo_y0 = N.v[VY0]; X.lo_y1 = N.v[VY1]; X.lo_m0 = N.m[MK0]; X.lo_m1 = N.m[MK1];
+        XrSide N;
+        if (neighbour_side(h, S, true, &N)) {
+            X.lo_y0 = N.v[4]; X.lo_y1 = N.v[5]; X.lo_m0 = N.m[0]; X.lo_m1 = N.m[1];
             X.Ls.lo_rows = N.rows;
             X.Ls.lo_ghost = N.ghi;
         }
-        if (S.nb_hi >= 0) {
-            Slab& N = h->slabs[S.nb_hi];
-            X.hi_y0 = N.v[VY0]; X.hi_y1 = N.v[VY1]; X.hi_m0 = N.m[MK0]; X.hi_m1 = N.m[MK1];
+        if (neighbour_side(h, S, false, &N)) {
+            X.hi_y0 = N.v[4]; X.hi_y1 = N.v[5]; X.hi_m0 = N.m[0]; X.hi_m1 = N.m[1];
             X.Ls.hi_ghost = N.glo;
         }
         X.La = X.Ls;
@@ -1435,14 +1603,14 @@ int launch_gp_loop_ms(gpcg_problem* h, int cur) {
     int c0[kMaxMs];
     for (int s = 0; s < h->nslabs(); ++s) c0[s] = P.s[s].cta0;
     XRank XR;
-    RC(make_xrank(h, c0, h->nslabs(), cta, &XR));
+    RC(make_xrank(h, c0, h->nslabs(), cta, &XR, false));
     CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
     double mu = h->prm.mu;
     int spec = h->gp_spec ? 1 : 0;
     void* args[] = {(void*)&P, (void*)&cur, (void*)&mu, (void*)&h->dS, (void*)&h->slabs[0].partials,
                     (void*)&h->gbar, (void*)&spec, (void*)&XR};
     const void* fn;
-    if (h->xr_emu) {
+    if (h->xr_emu || h->xr_real) {
         if (h->sb) fn = h->bb ? (const void*)k6_gp_loop_ms<true, true, true> : (const void*)k6_gp_loop_ms<true, false, true>;
         else fn = h->bb ? (const void*)k6_gp_loop_ms<false, true, true> : (const void*)k6_gp_loop_ms<false, false, true>;
     } else {
@@ -1455,7 +1623,7 @@ int launch_gp_loop_ms(gpcg_problem* h, int cur) {
 }
 
 int launch_gp_loop(gpcg_problem* h, int cur) {
-    if (h->nslabs() > 1) return launch_gp_loop_ms(h, cur);
+    if (h->nslabs() > 1 || h->xr_real) return launch_gp_loop_ms(h, cur);
     Slab& S = h->slabs[0];
     CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
     Bounds B = h->bounds(S);
@@ -2018,15 +2186,14 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
             X.rho0 = S.v[VRHO0]; X.rho1 = S.v[VRHO1]; X.p0 = S.v[VQ0]; X.p1 = S.v[VQ1]; X.w = S.v[VW];
             X.flags = h->cg_skip ? S.cgflags : nullptr;
             X.L = SlabLink{0, S.grid4_cg, 0, 0, 0};
-            if (S.nb_lo >= 0) {
-                Slab& N = h->slabs[S.nb_lo];
-                X.lo_rho0 = N.v[VRHO0]; X.lo_rho1 = N.v[VRHO1]; X.lo_p0 = N.v[VQ0]; X.lo_p1 = N.v[VQ1];
+            XrSide N;
+            if (neighbour_side(h, S, true, &N)) {
+                X.lo_rho0 = N.v[0]; X.lo_rho1 = N.v[1]; X.lo_p0 = N.v[2]; X.lo_p1 = N.v[3];
                 X.L.lo_rows = N.rows;
                 X.L.lo_ghost = N.ghi;
             }
-            if (S.nb_hi >= 0) {
-                Slab& N = h->slabs[S.nb_hi];
-                X.hi_rho0 = N.v[VRHO0]; X.hi_rho1 = N.v[VRHO1]; X.hi_p0 = N.v[VQ0]; X.hi_p1 = N.v[VQ1];
+            if (neighbour_side(h, S, false, &N)) {
+                X.hi_rho0 = N.v[0]; X.hi_rho1 = N.v[1]; X.hi_p0 = N.v[2]; X.hi_p1 = N.v[3];
                 X.L.hi_ghost = N.glo;
             }
             X.cta0 = cta;
@@ -2035,11 +2202,11 @@ int run_cg(gpcg_problem* h, int cur, long long m, double eta2, long long cap, lo
         int c0[kMaxMs];
         for (int s = 0; s < h->nslabs(); ++s) c0[s] = P.s[s].cta0;
         XRank XR;
-        RC(make_xrank(h, c0, h->nslabs(), cta, &XR));
+        RC(make_xrank(h, c0, h->nslabs(), cta, &XR, true));
         CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned int), h->st));
         CK(cudaEventRecord(h->ev_c0, h->st));
         void* args[] = {(void*)&P, (void*)&h->dS, (void*)&h->slabs[0].partials, (void*)&h->gbar, (void*)&XR};
-        const void* fn = h->xr_emu ? (h->prm.precond == 1 ? (const void*)k6_cg_loop_ms<true, true>
+        const void* fn = (h->xr_emu || h->xr_real) ? (h->prm.precond == 1 ? (const void*)k6_cg_loop_ms<true, true>
                                                             : (const void*)k6_cg_loop_ms<false, true>)
                                    : (h->prm.precond == 1 ? (const void*)k6_cg_loop_ms<true, false>
                                                             : (const void*)k6_cg_loop_ms<false, false>);
@@ -2263,6 +2430,9 @@ int create_stencil(gpcg_problem** out, const gpcg_dist* dist, void* stream, int6
         if (e && *e) h->tile_mask = atoi(e) & 127;
         if (h->bc && !h->generic && h->tile_mask != 0 && (rc = setup_tile(h))) return fail(rc);
     }
+    if (h->nranks > 1 && getenv("GPCG_XRANK") && atoi(getenv("GPCG_XRANK")) != 0 && h->tile && h->gfree &&
+        (rc = setup_xrank_real(h)))
+        return fail(rc);
     h->nnz = 5 * h->n_global - 2 * nx - 2 * ny;
     if ((rc = leave(h))) return fail(rc);
     *out = h;

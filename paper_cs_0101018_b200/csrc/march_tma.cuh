@@ -692,6 +692,7 @@ __device__ __forceinline__ void cg_loop(Scal* S, double* __restrict__ part, unsi
     if constexpr (XR) {
         if (threadIdx.x == 0) xc = xr_ctx(*X);
         __syncthreads();
+        if (X->sys) xr_barrier(*X, xc, gen);      // ranks: no fused store before every peer left its last kernel
     }
     while (!done) {
         const int a = (int)(it & 1);
@@ -1738,6 +1739,7 @@ __device__ __forceinline__ void gp_loop(int cur0, double mu, Scal* S, double* __
     if constexpr (XR) {
         if (threadIdx.x == 0) xc = xr_ctx(*X);
         __syncthreads();
+        if (X->sys) xr_barrier(*X, xc, gen);      // ranks: no fused store before every peer left its last kernel
     }
     // one reduction: the one-device grid sum, or the cross-rank one
     auto gsum = [&](auto& acc) {

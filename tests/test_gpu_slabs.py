@@ -195,15 +195,21 @@ def test_multi_slab_persistent_loops_match_single_slab_per_step(G, slabs):
     assert np.max(np.abs(x1 - xs)) <= 1e-11 * max(np.max(np.abs(x1)), 1e-300)
 
 
+@pytest.mark.parametrize("sys_scope", ["0", "1"])
 @pytest.mark.parametrize("slabs", [2, 3, 5, 8])
 @pytest.mark.parametrize("case", ["C0", "ragged29x17_bcast", "c3_family_160"])
-def test_cross_rank_protocol_emulated(G, oracle, monkeypatch, case, slabs):
+def test_cross_rank_protocol_emulated(G, oracle, monkeypatch, case, slabs, sys_scope):
     """The cross-rank protocol of the persistent loops (march_tma.cuh XRank: per-rank arrival
     counters never reset, partials stored into every rank's mailbox, each rank summing its own
     copy in global CTA order, the mailbox slot from the global barrier count) run inside one
     cooperative launch with every slab a virtual rank (GPCG_XRANK_EMU=1): bit for bit the
     one-device multi-slab loops, over every launch of a solve and of a second solve on the same
-    handle (counters and bases carried across launches), and the oracle's solution."""
+    handle (counters and bases carried across launches), and the oracle's solution.  sys_scope = 1
+    (GPCG_XRANK_SYS): the leaders' operations at system scope and the entry barrier of every
+    launch, as ranks on several devices run them."""
+    if sys_scope == "1" and slabs in (3, 5):
+        pytest.skip("system scope: 2 and 8 virtual ranks")
+    monkeypatch.setenv("GPCG_XRANK_SYS", sys_scope)
     make, tol = CASES[case]
     prob = make()
     if prob.ny < 3 * slabs:
@@ -226,3 +232,16 @@ def test_cross_rank_protocol_emulated(G, oracle, monkeypatch, case, slabs):
     rc, x, st = b1
     assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
     assert np.max(np.abs(x - x_o)) <= 1e-7
+
+
+def test_xrank_switch_single_rank(G, oracle, monkeypatch):
+    """GPCG_XRANK=1 on one rank: nothing spans ranks, but the handle's arenas come from cudaMalloc
+    (IPC-exportable) instead of the memory pool -- the same solution, bit for bit."""
+    prob = P.c0()
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("GPCG_XRANK", v)
+        with G.Solver.from_problem(prob, slabs=2) as s:
+            out.append(s.solve(prob.x0, -1e-12))
+    (rc0, x0, st0), (rc1, x1, st1) = out
+    assert rc0 == rc1 == 0 and np.array_equal(x0, x1) and st0["cg_iters"] == st1["cg_iters"]
