@@ -25,7 +25,7 @@ sweeps are measured in the HBM regime).  --config C2 runs the paper-size grid.
             masked operator Z Z' A Z Z') for a fixed number of iterations -- the
             same unit of work as `value`, independent of the solve's phase.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference] [--slabs S]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference] [--slabs S] [--xrank]
 N > 1 runs under torchrun (one process per GPU): the SAME problem split into N row
 slabs (gpcg_create_*_dist: NCCL halo exchange + one allreduce per CG iteration),
 i.e. strong scaling; see DESIGN.md "Multi-GPU".  --slabs S (N = 1) splits the
@@ -66,9 +66,10 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def cg_kernel_name(prob, slabs_total=1):
+def cg_kernel_name(prob, slabs_total=1, ms=False):
     """The CG-iteration kernel libgpcg.so selects for this problem (gpcg.cu run_cg /
-    enqueue_cg_iter); slabs_total > 1 (ranks x local slabs) uses the graph-chunk path."""
+    enqueue_cg_iter); slabs_total > 1: the multi-slab persistent loop (ms: slabs of one device, or ranks
+    with --xrank), else graph chunks."""
     compact = prob.kind in ("csr", "stencil3d") and slabs_total == 1   # cg_mode 2 -> 3 for small free sets
     if prob.kind == "csr":
         return "k_cg_iter_c<CsrOp> (free-row list, reduced-space vectors) / k_cg_iter<CsrOp>" if compact \
@@ -82,6 +83,8 @@ def cg_kernel_name(prob, slabs_total=1):
     if bc and tile & 8:
         if os.environ.get("GPCG_CG_PERSIST", "1") != "0" and slabs_total == 1:
             return "k6_cg_loop (persistent cooperative CG, TMA-fed column march; per-iteration time)"
+        if os.environ.get("GPCG_CG_PERSIST", "1") != "0" and ms:
+            return "k6_cg_loop_ms (persistent CG over every slab / rank, fused halo writes; per-iteration time)"
         return "k4_cg_iter (TMA-fed column march)"
     if bc and tile & 4:
         return "k3_cg_iter<2> (TMA tile)"
@@ -407,15 +410,18 @@ def run_ours(args):
         spec_b = 17.0 + (0.0 if sb else 16.0) + (0.0 if bb else 8.0)
         srch_b = 8.0 + (0.0 if sb else 16.0) + (0.0 if bb else 8.0)
         acc_b = spec_b + 1.0
-        persist = (world * args.slabs == 1 and not prob.wx_ld and not prob.wy_ld and prob.shift is None
-                   and os.environ.get("GPCG_GP_PERSIST", "1") != "0")
+        bc_gp = (not prob.wx_ld and not prob.wy_ld and prob.shift is None
+                 and os.environ.get("GPCG_GP_PERSIST", "1") != "0")
+        persist = bc_gp and world * args.slabs == 1
+        persist_ms = bc_gp and ((world == 1 and args.slabs > 1) or (world > 1 and args.xrank))
         rej = agg["gp_spec_rejected"]
         gp_step_s = (agg["t_gp_ms"] / 1e3) / agg["gp_iters"]
         gp_bytes = (spec_b * agg["gp_iters"] + (srch_b + acc_b) * rej) * prob.n / agg["gp_iters"] / world
         ach = gp_bytes / gp_step_s / 1e9
         gp_roof = {"bound": "hbm",
                    "kernel": ("k6_gp_loop (persistent GP phase; speculative accept sweep per step)" if persist
-                              else "k5_search / k5_accept GP graph chunks"),
+                              else "k6_gp_loop_ms (persistent GP phase over every slab / rank, fused halo writes)"
+                              if persist_ms else "k5_search / k5_accept GP graph chunks"),
                    "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                    "frac_of_8TBs": ach / 8000.0, "traffic": traffic.get("gp"), "peak_source": peak_src,
                    "bytes_per_launch": gp_bytes, "us_per_launch": gp_step_s * 1e6,
@@ -480,7 +486,9 @@ def run_ours(args):
                              "the 126 MB L2 anyway",
                        "parallelism": ("1 GPU, 1 slab" if world == 1 and args.slabs == 1 else
                                        f"{world} GPU(s) x {args.slabs} row slab(s) of one problem "
-                                       f"(halo exchange + one allreduce per CG iteration)")},
+                                       + ("(persistent loops across ranks over IPC-mapped peer memory)"
+                                          if args.xrank and world > 1 else
+                                          "(halo exchange + one allreduce per CG iteration)"))},
             "solve": {"s_per_solve": tot_ms / args.steps / 1e3, "outer_iters": last["outer_iters"],
                       "gp_iters": last["gp_iters"], "cg_iters": last["cg_iters"],
                       "n_free": last["n_free"], "q": last["q"], "pg_norm": last["pg_norm"],
@@ -490,7 +498,9 @@ def run_ours(args):
             # the five-vector C-G form for CSR = SURVEY 8(d)'s figure); SURVEY 8(d)'s 80 B figure
             # (which also streams A p and A rho) beside it -- against that count the kernel exceeds
             # the copy peak, because it recomputes A p and A rho from neighbours instead of streaming them.
-            "roofline": {"bound": "hbm", "kernel": cg_kernel_name(prob, world * args.slabs),
+            "roofline": {"bound": "hbm", "kernel": cg_kernel_name(prob, world * args.slabs,
+                                                                  (world == 1 and args.slabs > 1) or
+                                                                  (world > 1 and args.xrank)),
                          "achieved": achieved_min, "peak": peak, "unit": "GB/s",
                          "frac": (achieved_min / peak) if achieved_min else None,
                          "frac_of_8TBs": (achieved_min / 8000.0) if achieved_min else None,
@@ -548,7 +558,12 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slabs", type=int, default=1)
+    ap.add_argument("--xrank", action="store_true",
+                    help="N > 1: the persistent loops span the ranks over IPC-mapped peer memory (GPCG_XRANK=1; "
+                         "DESIGN.md 8) instead of NCCL graph chunks")
     args = ap.parse_args()
+    if args.xrank:
+        os.environ["GPCG_XRANK"] = "1"      # read at create
     if args.impl == "reference":
         return run_reference(args)
     from paper_cs_0101018_b200 import _build
