@@ -488,6 +488,8 @@ def run_ours(args):
                                        f"{world} GPU(s) x {args.slabs} row slab(s) of one problem "
                                        + ("(persistent loops across ranks over IPC-mapped peer memory)"
                                           if args.xrank and world > 1 else
+                                          "(persistent loops over every slab, fused halo writes)"
+                                          if world == 1 else
                                           "(halo exchange + one allreduce per CG iteration)"))},
             "solve": {"s_per_solve": tot_ms / args.steps / 1e3, "outer_iters": last["outer_iters"],
                       "gp_iters": last["gp_iters"], "cg_iters": last["cg_iters"],
