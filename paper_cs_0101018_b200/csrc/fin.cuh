@@ -72,6 +72,25 @@ __device__ __forceinline__ void fin_spec(const double* t, double base, double mu
     }
 }
 
+// k5_spec (2-D GP graph): t = ||d||^2, ||g||^2 (not formed), |A|, #changed, |A\B|, <d,Ad> of the
+// speculative point, then <g,s>, <s,As> of h = 0.  Accepted -> the step is taken at the old
+// alpha_0 and the accept sums (with the next Cauchy form) are applied; else s_h = -1.
+__device__ __forceinline__ void fin_spec6(const double* t, double mu, Scal* S) {
+    const double gs = t[6], sAs = t[7];
+    const double dq = gs + 0.5 * sAs;
+    if (dq <= mu * gs) {
+        S->spec_ok = 1;
+        S->s_h = 0;
+        S->s_alpha = S->alpha0;
+        S->s_delta = dq;
+        S->s_gs = gs;
+        fin_accept(t, true, S);
+    } else {
+        S->spec_ok = 0;
+        S->s_h = -1;
+    }
+}
+
 // a5 init: gamma_0 = rho_0'rho_0, delta_0 = rho_0'A_F rho_0.
 __device__ __forceinline__ void cg_init_finalize(double gamma, double delta, double eta2, long long cap, Scal* S) {
     S->cg_it = 0;
@@ -176,6 +195,7 @@ enum FinKind : int {
     FIN_PCG2_ALPHA = 8,  //   p'A p -> alpha
     FIN_PCG2_BETA = 9,   //   r'z -> decrease, stop tests, beta
     FIN_SPEC = 10,       // k_spec: h = 0 search sums + accept sums
+    FIN_SPEC6 = 11,      // k5_spec: accept sums + Cauchy form + h = 0 search sums
 };
 
 struct FinArgs {
@@ -238,6 +258,10 @@ __global__ void k_finalize(const double* __restrict__ t, Scal* S, FinArgs a) {
         case FIN_SPEC:
             if (a.use_alpha0 && !S->cauchy_ok) { S->spec_ok = 0; S->s_h = -1; return; }
             fin_spec(t, a.use_alpha0 ? S->alpha0 : 1.0, a.mu, S);
+            break;
+        case FIN_SPEC6:
+            if (!S->cauchy_ok) { S->spec_ok = 0; S->s_h = -1; return; }
+            fin_spec6(t, a.mu, S);
             break;
     }
 }

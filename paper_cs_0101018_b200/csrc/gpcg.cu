@@ -661,6 +661,8 @@ int setup_tile(gpcg_problem* h) {
 #define K5ACC(SB, BB, M) RC(set_smem(k5_accept<SB, BB, M>, AccLayout5<SB, BB, M>::kSmem));
 #define K5ACC2(SB, BB) K5ACC(SB, BB, m5::GP) K5ACC(SB, BB, m5::CG) K5ACC(SB, BB, m5::PROJ)
     K5ACC2(true, true) K5ACC2(true, false) K5ACC2(false, true) K5ACC2(false, false)
+#define K5SP(SB, BB) RC(set_smem(k5_spec<SB, BB>, AccLayout5<SB, BB, m5::GP>::kSmem));
+    K5SP(true, true) K5SP(true, false) K5SP(false, true) K5SP(false, false)
 #define K5S(SB, BB, M, K) RC(set_smem(k5_search<SB, BB, M, K>, SrchLayout5<SB, BB, M, K>::kSmem));
 #define K5S2(SB, BB) K5S(SB, BB, m5::GP, 2) K5S(SB, BB, m5::GP, 8) K5S(SB, BB, m5::CG, 2) K5S(SB, BB, m5::CG, 8)
     K5S2(true, true) K5S2(true, false) K5S2(false, true) K5S2(false, false)
@@ -1097,6 +1099,34 @@ int launch_cauchy(gpcg_problem* h, int y, int g, int gp = 0) {
 // h = 0 (k_spec: search sums + accept in one sweep; GPCG_GP_SPEC=0: off); the 2-D stencils fuse
 // the GP step into their own sweeps (k6_gp_loop, spec_sweep6).
 bool graph_spec(const gpcg_problem* h) { return h->gp_spec && !spec2d(h); }
+// the 2-D GP graph (slabs / ranks off the persistent loop) takes its steps with k5_spec
+bool graph_spec5(const gpcg_problem* h) { return h->gp_spec && spec2d(h) && h->gfree; }
+
+int launch_spec5(gpcg_problem* h, int cur) {
+    const int nxt = cur ^ 1;
+    const double mu = h->prm.mu;
+    for (int s = 0; s < h->nslabs(); ++s) {
+        Slab& S = h->slabs[s];
+        const Bounds B = h->bounds(S);
+        auto go = [&](auto sbt, auto bbt) {
+            constexpr bool SB = decltype(sbt)::value, BB = decltype(bbt)::value;
+            k5_spec<SB, BB><<<S.grid5_acc, m4::kThreads, AccLayout5<SB, BB, m5::GP>::kSmem, h->st>>>(
+                S.sop, S.bg5_acc, B, S.brow, S.t5[vy(cur)], S.t5[VB], S.t5[VL], S.t5[VU], S.t5m[mk(cur)],
+                S.v[vy(nxt)], S.m[mk(nxt)], mu, h->dS, h->red(s));
+        };
+        auto bybb = [&](auto sbt) {
+            if (h->bb) go(sbt, std::true_type()); else go(sbt, std::false_type());
+        };
+        if (h->sb) bybb(std::true_type()); else bybb(std::false_type());
+        h->launches++;
+        CKLAUNCH();
+    }
+    FinArgs a = fin(FIN_SPEC6);
+    a.mu = mu;
+    a.gp = 1;
+    RC(finish_reduce(h, a, 8));
+    return exchange(h, {vy(nxt)}, {mk(nxt)});    // g is not stored
+}
 
 // y(nxt), g(nxt), mask(nxt) = the step at h = 0 from y(cur) along sgn * dir (base alpha_0 or 1)
 int launch_spec(gpcg_problem* h, int cur, int dir, double sgn, int use_alpha0, int gp) {
@@ -1331,7 +1361,9 @@ int build_gp_graph_into(gpcg_problem* h, int chunk, cudaGraphExec_t (&out)[2]) {
             const int cur = (c0 + i) & 1, nxt = cur ^ 1;
             rc = launch_cauchy(h, vy(cur), vg(cur), 1);
             if (!rc && graph_spec(h)) rc = launch_spec(h, cur, vg(cur), -1.0, 1, 1);
-            if (!rc) rc = launch_search(h, vy(cur), vg(cur), vg(cur), -1.0, 1, graph_spec(h) ? 1 : 0, first_k(h), 1);
+            if (!rc && graph_spec5(h)) rc = launch_spec5(h, cur);
+            const int h0 = (graph_spec(h) || graph_spec5(h)) ? 1 : 0;
+            if (!rc) rc = launch_search(h, vy(cur), vg(cur), vg(cur), -1.0, 1, h0, first_k(h), 1);
             if (!rc) rc = launch_accept(h, vy(cur), vg(cur), -1.0, mk(cur), vy(nxt), vg(nxt), mk(nxt), 1);
             if (!rc) {
                 k_gp_step<<<1, 32, 0, h->st>>>(h->dS);
@@ -1373,7 +1405,8 @@ int build_gp_graph(gpcg_problem* h, int chunk) {
 
 int launches_per_gp_step(const gpcg_problem* h) {
     const int fins = h->deferred ? (1 + (h->nslabs() > 1 ? 1 : 0)) : 0;
-    return (fused_cauchy(h) ? 0 : h->nslabs() + fins) + (graph_spec(h) ? 3 : 2) * (h->nslabs() + fins) + 1;
+    return (fused_cauchy(h) ? 0 : h->nslabs() + fins) +
+           ((graph_spec(h) || graph_spec5(h)) ? 3 : 2) * (h->nslabs() + fins) + 1;
 }
 
 // The whole GP phase (until it stops or hands a step back) as one cooperative launch.
@@ -3095,7 +3128,8 @@ int gpcg_solve(gpcg_problem* h, const double* x0, double tol, int64_t max_it, do
                     // the first search batch found no step: the host finishes this step (the persistent
                     // kernel reports the first step size index it has not tried in s_pad)
                     int hacc = -1;
-                    const int hstart = persist ? std::max(S.s_pad, 0) : first_k(h) + (graph_spec(h) ? 1 : 0);
+                    const int hstart = persist ? std::max(S.s_pad, 0)
+                                               : first_k(h) + ((graph_spec(h) || graph_spec5(h)) ? 1 : 0);
                     if ((rc = search_and_accept(h, cur, vg(cur), -1.0, 1, &hacc, hstart))) goto fail;
                     cur ^= 1;
                     const long long j = jdone + 1;

@@ -1180,7 +1180,7 @@ k5_accept(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, c
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u,
           const __grid_constant__ CUtensorMap m_mp, int has_mp, double* __restrict__ y_out,
           unsigned char* __restrict__ mask_out, Scal* S, RedScratch R, int gp) {
-    if (gp && *(volatile int*)&S->gp_done) return;
+    if (gp && gp_skip(S)) return;      // GP phase over / k5_spec accepted
     double alpha = 0.0;
     if (MODE != m5::PROJ) {
         if (S->s_h < 0) return;                   // uniform: no accepted step in this batch
@@ -1301,7 +1301,7 @@ k5_search(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, c
           const __grid_constant__ CUtensorMap m_l, const __grid_constant__ CUtensorMap m_u, int h0, double mu,
           Scal* S, RedScratch R, int gp) {
     constexpr bool use_alpha0 = MODE == m5::GP;
-    if (gp && *(volatile int*)&S->gp_done) return;
+    if (gp && gp_skip(S)) return;      // GP phase over / k5_spec accepted
     if (use_alpha0 && !S->cauchy_ok) {           // <d,Ad> <= 0: no step (host reports ENOTSPD)
         if (blockIdx.x == 0 && threadIdx.x == 0) S->s_h = -1;
         return;
@@ -1849,6 +1849,29 @@ k6_gp_loop(StencilOp A, BandGeom Gs, BandGeom Ga, Bounds Bd, const double* __res
                                                  &m_l, &m_u, cur ? &m_m1 : &m_m0, 1, alpha, cur ? y0p : y1p,
                                                  cur ? mk0 : mk1, smem, acc, bars, k);
         });
+}
+
+// The speculative GP step as ONE graph node (the GP graph chunks of slabs / ranks, which cannot
+// run the persistent loop): spec_sweep6 at alpha_0 from y(cur) into y(nxt), mask(nxt) -- the
+// accepted point, its set counts and next Cauchy form, and the h = 0 search sums, the same sweep
+// and sums as k6_gp_loop's -- then fin_spec6: Eq. gplsstop at h = 0 keeps the step (the step's
+// search / accept nodes return at once) or lets them run from h = 1.
+template <bool SB, bool BB>
+__global__ void __launch_bounds__(m4::kThreads, GPCG_GP_MINB)
+k5_spec(StencilOp A, BandGeom G, Bounds Bd, const double* __restrict__ brow, const __grid_constant__ CUtensorMap m_y,
+        const __grid_constant__ CUtensorMap m_b, const __grid_constant__ CUtensorMap m_l,
+        const __grid_constant__ CUtensorMap m_u, const __grid_constant__ CUtensorMap m_m,
+        double* __restrict__ y_out, unsigned char* __restrict__ mask_out, double mu, Scal* S, RedScratch R) {
+    if (*(volatile int*)&S->gp_done) return;
+    if (!S->cauchy_ok) {                          // <d,Ad> <= 0: no step (uniform; k_finalize mirrors it)
+        if (blockIdx.x == 0 && threadIdx.x == 0) { S->spec_ok = 0; S->s_h = -1; }
+        return;
+    }
+    const double alpha0 = S->alpha0;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    spec_sweep6<SB, BB>(A, G, Bd, brow, &m_y, &m_b, &m_l, &m_u, &m_m, alpha0, y_out, mask_out, smem, acc, nullptr, 0);
+    reduce_and_finish<8>(acc, R, [&](double* t) { fin_spec6(t, mu, S); });
 }
 
 // k6_gp_loop over several slabs of one device (SlabLink): the accepted y and the new mask of

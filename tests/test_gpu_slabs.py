@@ -245,3 +245,28 @@ def test_xrank_switch_single_rank(G, oracle, monkeypatch):
             out.append(s.solve(prob.x0, -1e-12))
     (rc0, x0, st0), (rc1, x1, st1) = out
     assert rc0 == rc1 == 0 and np.array_equal(x0, x1) and st0["cg_iters"] == st1["cg_iters"]
+
+
+@pytest.mark.parametrize("mode", ["1slab", "2slabs", "2slabs_nccl"])
+@pytest.mark.parametrize("case", ["C0", "ragged29x17_bcast", "c3_family_160"])
+def test_gp_graph_speculative_step(G, oracle, monkeypatch, case, mode):
+    """The 2-D GP graph chunks (the ranks' path: GPCG_GP_PERSIST=0 here) take each step with
+    k5_spec (the persistent loop's speculative sweep as one node; search / accept only when it is
+    rejected): the oracle's solution with and without it (GPCG_GP_SPEC=0), one slab, two slabs
+    with deferred reductions, and two slabs with every sum through a 1-rank NCCL communicator."""
+    make, tol = CASES[case]
+    prob = make()
+    monkeypatch.setenv("GPCG_GP_PERSIST", "0")
+    if mode == "2slabs_nccl":
+        monkeypatch.setenv("GPCG_FORCE_NCCL", "1")
+    slabs = 1 if mode == "1slab" else 2
+    rc_o, x_o, st_o = oracle.solve_problem(prob, tol=tol)
+    for spec in ("1", "0"):
+        monkeypatch.setenv("GPCG_GP_SPEC", spec)
+        with G.Solver.from_problem(prob, slabs=slabs) as s:
+            rc, x, st = s.solve(prob.x0, tol)
+        assert rc == 0 and rc_o == 0, (spec, st)
+        assert abs(st["q"] - st_o["q"]) <= 1e-10 * abs(st_o["q"])
+        assert np.max(np.abs(x - x_o)) <= 1e-7
+        nm, nontie = _tie_mismatches(x, x_o, prob.l, prob.u)
+        assert not nontie
