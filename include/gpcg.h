@@ -150,9 +150,20 @@ GPCG_API gpcg_params gpcg_params_default(void);
  *                 slabs on the same device, exchanging ghost rows by device
  *                 copies and summing slab totals in slab order -- the same
  *                 arithmetic as nranks * local_slabs ranks (used to test the
- *                 slab path on one GPU).
+ *                 slab path on one GPU).  stencil2d with broadcast faces: the
+ *                 slabs of one device run the CG call / GP phase as ONE
+ *                 persistent launch whose sweeps write their neighbours' ghost
+ *                 rows directly (no exchange step).
+ * Environment GPCG_XRANK=1 (read at create; stencil2d with broadcast faces, up
+ * to 8 ranks): those persistent launches span the ranks -- each rank maps its
+ * neighbours' ghost rows and every rank's counters / partial-sum mailbox over
+ * CUDA IPC (exported and all-gathered over the NCCL communicator at create),
+ * one NVLink round trip per global sum; the memory pool is off.  Built, not yet
+ * run on several GPUs.
  * Errors: GPCG_EINVAL for a bad range or a slab of < 3 stencil2d rows (< 1 plane
- * / CSR row) or a CSR band beyond the neighbouring slab; GPCG_ENCCL if NCCL fails.
+ * / CSR row) or a CSR band beyond the neighbouring slab; GPCG_ENCCL if NCCL fails
+ * (GPCG_XRANK: also if ncclAllGather is missing); GPCG_ECUDA if a CUDA IPC call
+ * fails or a cross-rank wait exceeds 20 s.
  */
 typedef struct {
     int32_t rank, nranks;
